@@ -1,0 +1,167 @@
+/*
+ * attn_softmax.h -- C ABI of libattnsm.so, the B200 (sm_100a) attention-softmax
+ * stage of arXiv 1909.00562 (the data-parallel half of the hybrid scheme,
+ * Fig. 3), forward and backward.
+ *
+ * The operation (section 3.2, Eqs. 1-6; readings R1-R11 in DESIGN.md):
+ *   per sentence b and target row i (all rows computed, only valid rows count)
+ *     e_ij   = H_dec[b,i] . H_enc[b,j]                    Eq. 2,
+ *                                                          dot form, W_alpha = I (R1)
+ *     alpha  = softmax_j(e_i) over j < src_len[b]; 0 else  Eq. 1
+ *     C_i    = sum_j alpha_ij H_enc[b,j]                   Eq. 3
+ *     Hc_i   = tanh(W_c[:, :d] H_i + W_c[:, d:] C_i)       Eq. 4
+ *     l_iv   = W_out[v] . Hc_i                             Eq. 5
+ *     loss   = loss_scale * sum_{valid (b,i)} (logsumexp_v l_iv - l_{i,y_i})
+ *                                                          Eq. 6
+ *   and the gradients of loss w.r.t. H_dec, H_enc, W_c, W_out.  With a
+ *   communicator, dW_c, dW_out and loss are summed over ranks (the rootless
+ *   equivalent of "GPU 0 as the root for accumulating and synchronizing",
+ *   PAPER.md:121).
+ *
+ * Layouts: all matrices are dense row-major with no padding between rows.
+ *   H_dec [B,N,d]  decoder top-layer states (the paper's H, transposed)
+ *   H_enc [B,M,d]  encoder top-layer states (the paper's S, transposed)
+ *   W_c   [d,2d]   columns [0,d) multiply H, [d,2d) multiply C (paper order
+ *                  [H;C], R5; north_star's "W_c[c;h]" is the same matrix with
+ *                  its column halves swapped)
+ *   W_out [V,d]    F_c of Eq. 5, no bias (R6)
+ *   tgt_ids [B,N] int32, read only where i < tgt_len[b]
+ * dtype ATTN_BF16: H_dec, H_enc, W_c, W_out, dH_dec, dH_enc are bf16; all
+ *   accumulation, softmax statistics, loss and dW_c / dW_out are fp32.
+ * dtype ATTN_F32: everything fp32 (CUDA-core path, for the parity config).
+ *
+ * Ownership: the caller allocates and frees every buffer, including the
+ *   workspace (size from attn_softmax_workspace_size).  The library never
+ *   allocates device memory inside attn_softmax_fwd_bwd.  attn_comm_t is owned
+ *   by the library between attn_comm_init and attn_comm_destroy.
+ * Semantics: calls are asynchronous on `stream` (a cudaStream_t); every output
+ *   is final when the stream reaches the end of the enqueued work (including
+ *   the allreduce).  Gradients are OVERWRITTEN.  Inputs are read-only.  Padded
+ *   slots (j >= src_len, i >= tgt_len) may hold any finite values and do not
+ *   affect any output; padded rows of dH_dec / dH_enc are written as exact 0.
+ * Errors: every entry point returns attn_status_t; attn_last_error() gives a
+ *   thread-local message naming the offending argument (and both shapes for a
+ *   shape mismatch).  No partial work is enqueued on a validation
+ *   error.
+ */
+#ifndef ATTN_SOFTMAX_H
+#define ATTN_SOFTMAX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ATTN_OK = 0,
+  ATTN_ERR_INVALID_ARG = 1,  /* null pointer, bad enum, negative size        */
+  ATTN_ERR_SHAPE = 2,        /* src_len > M, tgt_len > N, or d, V, B <= 0    */
+  ATTN_ERR_EMPTY_SOURCE = 3, /* some src_len[b] < 1       */
+  ATTN_ERR_NO_TARGETS = 4,   /* sum_b tgt_len[b] == 0          */
+  ATTN_ERR_TOKEN_RANGE = 5,  /* a valid target id outside [0, V);
+                                checked only by attn_softmax_check_ids      */
+  ATTN_ERR_WORKSPACE = 6,    /* workspace_bytes < attn_softmax_workspace_size */
+  ATTN_ERR_UNSUPPORTED = 7,  /* dtype/shape/alignment the kernels do not take:
+                                bf16 needs d % 64 == 0 and 16-byte aligned
+                                pointers                                     */
+  ATTN_ERR_CUDA = 8,         /* a CUDA runtime/driver call failed            */
+  ATTN_ERR_NCCL = 9          /* NCCL missing or a NCCL call failed           */
+} attn_status_t;
+
+typedef enum { ATTN_F32 = 0, ATTN_BF16 = 1 } attn_dtype_t;
+
+/* Local (per-GPU) shard shape: B sentences, N padded target steps, M padded
+ * source positions, d hidden size, V vocabulary size. */
+typedef struct {
+  int32_t batch;    /* B */
+  int32_t tgt_len;  /* N */
+  int32_t src_len;  /* M */
+  int32_t hidden;   /* d */
+  int32_t vocab;    /* V */
+  attn_dtype_t dtype;
+} attn_shape_t;
+
+typedef struct attn_comm attn_comm_t; /* opaque: NCCL communicator + comm stream */
+
+/* Bytes of device workspace attn_softmax_fwd_bwd needs for shape *s (0 on an
+ * invalid shape; see attn_last_error). */
+size_t attn_softmax_workspace_size(const attn_shape_t* s);
+
+/* The whole stage, forward + backward, on `stream`.
+ *   src_lens_host, tgt_lens_host: [B] HOST arrays, validated and copied.
+ *   tgt_ids: [B,N] device int32.
+ *   W_alpha / dW_alpha: must be NULL (dot score, R1); the Eq. 2 "general"
+ *     score is not implemented in this build (ATTN_ERR_UNSUPPORTED).
+ *   loss_scale: multiplies the summed token NLL (the harness passes
+ *     1 / global valid target tokens, R9).
+ *   loss: [1] device fp32 = loss_scale * sum of this shard's token NLL
+ *     (summed over ranks when comm != NULL).
+ *   dH_dec [B,N,d], dH_enc [B,M,d]: dtype s->dtype, overwritten.
+ *   dW_c [d,2d], dW_out [V,d]: fp32, overwritten (allreduced when comm).
+ *   comm: NULL for local gradients. */
+attn_status_t attn_softmax_fwd_bwd(
+    const attn_shape_t* s,
+    const void* H_dec, const void* H_enc,
+    const int32_t* src_lens_host, const int32_t* tgt_lens_host,
+    const int32_t* tgt_ids,
+    const void* W_c, const void* W_out, const void* W_alpha,
+    float loss_scale,
+    float* loss,
+    void* dH_dec, void* dH_enc,
+    float* dW_c, float* dW_out, float* dW_alpha,
+    void* workspace, size_t workspace_bytes,
+    attn_comm_t* comm,
+    void* stream);
+
+/* End-to-end variant for callers whose per-step activations live in HOST
+ * memory (pinned for overlap): H_dec_host, H_enc_host and tgt_ids_host are
+ * copied host->device into `staging` (size attn_softmax_host_staging_size),
+ * the stage runs as attn_softmax_fwd_bwd, and the loss is copied back into
+ * loss_host.  Weights and gradients stay on the device.  loss_host is valid
+ * once `stream` has reached the end of the enqueued work. */
+size_t attn_softmax_host_staging_size(const attn_shape_t* s);
+attn_status_t attn_softmax_fwd_bwd_host(
+    const attn_shape_t* s,
+    const void* H_dec_host, const void* H_enc_host,
+    const int32_t* src_lens_host, const int32_t* tgt_lens_host,
+    const int32_t* tgt_ids_host,
+    const void* W_c, const void* W_out,
+    float loss_scale,
+    float* loss_host,
+    void* dH_dec, void* dH_enc,
+    float* dW_c, float* dW_out,
+    void* staging, size_t staging_bytes,
+    void* workspace, size_t workspace_bytes,
+    attn_comm_t* comm,
+    void* stream);
+
+/* Debug-build style check of the valid target ids: synchronous, returns
+ * ATTN_ERR_TOKEN_RANGE if any tgt_ids[b,i] (i < tgt_len[b]) is outside [0,V). */
+attn_status_t attn_softmax_check_ids(const attn_shape_t* s,
+                                     const int32_t* tgt_lens_host,
+                                     const int32_t* tgt_ids, void* stream);
+
+/* In-place sum allreduce of `count` fp32 values over the communicator's ranks,
+ * enqueued on `stream`. */
+attn_status_t attn_grad_allreduce(attn_comm_t* c, float* buf, size_t count,
+                                  void* stream);
+
+/* Communicator bootstrap: rank 0 creates a 128-byte id, the harness
+ * broadcasts it, every rank calls attn_comm_init on its own device. */
+attn_status_t attn_comm_get_unique_id(uint8_t id[128]);
+attn_status_t attn_comm_init(const uint8_t id[128], int nranks, int rank,
+                             int device, attn_comm_t** out);
+attn_status_t attn_comm_destroy(attn_comm_t* c);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* attn_last_error(void);
+
+/* Library version string, e.g. "attnsm 0.1 sm_100a". */
+const char* attn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ATTN_SOFTMAX_H */

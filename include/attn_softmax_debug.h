@@ -1,0 +1,54 @@
+/*
+ * attn_softmax_debug.h -- test / tuning surface of libattnsm.so.
+ *
+ * Not needed by users of the stage.  The parity tests use it to compare the
+ * stashed intermediates of a finished attn_softmax_fwd_bwd call (which live in
+ * the caller's workspace) with the oracle stage by stage, to exercise the
+ * tcgen05 GEMM core on its own, and to set tuning knobs.
+ */
+#ifndef ATTN_SOFTMAX_DEBUG_H
+#define ATTN_SOFTMAX_DEBUG_H
+
+#include "attn_softmax.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Byte offsets, inside the workspace, of the intermediates that stay valid
+ * after attn_softmax_fwd_bwd returns and its stream work completes.  T = B*N.
+ *   alpha  fp32 [B,N,M]  attention weights (Eq. 1), exact 0 where masked
+ *   ctx    dtype [T,d]   context vectors C (Eq. 3)
+ *   hc     dtype [T,d]   attentional states H_c (Eq. 4)
+ *   lse    fp32 [T]      log-sum-exp of the Eq. 5 logits per row
+ *   nll    fp32 [T]      per-row token NLL (0 on padded rows)
+ *   vocab_chunk          V-chunk width the backward uses (columns)          */
+typedef struct {
+  size_t alpha, ctx, hc, lse, nll;
+  int64_t vocab_chunk;
+} attn_ws_views_t;
+
+attn_status_t attn_softmax_workspace_views(const attn_shape_t* s,
+                                           attn_ws_views_t* out);
+
+/* C[M,N] (fp32, row-major, ldc = N) = A * B^T on the tcgen05 GEMM core.
+ *   A: a_mn == 0 -> K-major bf16 [M,K] (row stride K)
+ *      a_mn == 1 -> MN-major bf16 [K,M] (row stride M)
+ *   B: b_mn == 0 -> K-major bf16 [N,K];  b_mn == 1 -> MN-major bf16 [K,N]
+ * K % 8 == 0 and M % 8 == 0 / N % 8 == 0 for the MN-major operands (16-byte
+ * TMA row strides). */
+attn_status_t attn_debug_gemm_bf16(int M, int N, int K,
+                                   const void* A, int a_mn,
+                                   const void* B, int b_mn,
+                                   float* C, void* stream);
+
+/* Tuning knobs (process-wide).  Keys:
+ *   "vocab_chunk"   V-chunk width of the vocab backward (multiple of 256,
+ *                   0 = automatic from the L2 size)
+ *   "gemm_ctas"     persistent GEMM grid size (0 = number of SMs)          */
+attn_status_t attn_softmax_set_option(const char* key, int64_t value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ATTN_SOFTMAX_DEBUG_H */

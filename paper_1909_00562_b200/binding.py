@@ -1,0 +1,221 @@
+"""ctypes binding of libattnsm.so (include/attn_softmax.h).
+
+Argument marshalling only: every step of the stage runs in the library's
+CUDA kernels.  PyTorch supplies device memory and streams.  There is no CPU
+fallback -- if the library is missing, lib() raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libattnsm.so")
+
+ATTN_F32, ATTN_BF16 = 0, 1
+STATUS = {0: "ATTN_OK", 1: "ATTN_ERR_INVALID_ARG", 2: "ATTN_ERR_SHAPE",
+          3: "ATTN_ERR_EMPTY_SOURCE", 4: "ATTN_ERR_NO_TARGETS",
+          5: "ATTN_ERR_TOKEN_RANGE", 6: "ATTN_ERR_WORKSPACE",
+          7: "ATTN_ERR_UNSUPPORTED", 8: "ATTN_ERR_CUDA", 9: "ATTN_ERR_NCCL"}
+
+# every symbol include/attn_softmax.h and attn_softmax_debug.h declare
+EXPORTS = [
+    "attn_softmax_workspace_size", "attn_softmax_fwd_bwd",
+    "attn_softmax_host_staging_size", "attn_softmax_fwd_bwd_host",
+    "attn_softmax_check_ids", "attn_grad_allreduce", "attn_comm_get_unique_id",
+    "attn_comm_init", "attn_comm_destroy", "attn_last_error", "attn_version",
+    "attn_softmax_workspace_views", "attn_debug_gemm_bf16",
+    "attn_softmax_set_option",
+]
+
+
+class AttnError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+class AttnShape(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("tgt_len", ctypes.c_int32),
+                ("src_len", ctypes.c_int32), ("hidden", ctypes.c_int32),
+                ("vocab", ctypes.c_int32), ("dtype", ctypes.c_int32)]
+
+
+class AttnWsViews(ctypes.Structure):
+    _fields_ = [("alpha", ctypes.c_size_t), ("ctx", ctypes.c_size_t),
+                ("hc", ctypes.c_size_t), ("lse", ctypes.c_size_t),
+                ("nll", ctypes.c_size_t), ("vocab_chunk", ctypes.c_int64)]
+
+
+_lib = None
+_P = ctypes.c_void_p
+
+
+def lib() -> ctypes.CDLL:
+    """Load libattnsm.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"libattnsm.so not built: {LIB_PATH} is missing "
+                           "(run __graft_entry__.build()); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    S = ctypes.POINTER(AttnShape)
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    L.attn_softmax_workspace_size.argtypes = [S]
+    L.attn_softmax_workspace_size.restype = ctypes.c_size_t
+    L.attn_softmax_fwd_bwd.argtypes = [S, _P, _P, i32p, i32p, _P, _P, _P, _P,
+                                       ctypes.c_float, _P, _P, _P, _P, _P, _P,
+                                       _P, ctypes.c_size_t, _P, _P]
+    L.attn_softmax_fwd_bwd.restype = ctypes.c_int
+    L.attn_softmax_host_staging_size.argtypes = [S]
+    L.attn_softmax_host_staging_size.restype = ctypes.c_size_t
+    L.attn_softmax_fwd_bwd_host.argtypes = [S, _P, _P, i32p, i32p, _P, _P, _P,
+                                            ctypes.c_float, _P, _P, _P, _P, _P,
+                                            _P, ctypes.c_size_t, _P, ctypes.c_size_t,
+                                            _P, _P]
+    L.attn_softmax_fwd_bwd_host.restype = ctypes.c_int
+    L.attn_softmax_check_ids.argtypes = [S, i32p, _P, _P]
+    L.attn_softmax_check_ids.restype = ctypes.c_int
+    L.attn_grad_allreduce.argtypes = [_P, _P, ctypes.c_size_t, _P]
+    L.attn_grad_allreduce.restype = ctypes.c_int
+    L.attn_comm_get_unique_id.argtypes = [ctypes.c_char_p]
+    L.attn_comm_get_unique_id.restype = ctypes.c_int
+    L.attn_comm_init.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
+                                 ctypes.c_int, ctypes.POINTER(_P)]
+    L.attn_comm_init.restype = ctypes.c_int
+    L.attn_comm_destroy.argtypes = [_P]
+    L.attn_comm_destroy.restype = ctypes.c_int
+    L.attn_last_error.argtypes = []
+    L.attn_last_error.restype = ctypes.c_char_p
+    L.attn_version.argtypes = []
+    L.attn_version.restype = ctypes.c_char_p
+    L.attn_softmax_workspace_views.argtypes = [S, ctypes.POINTER(AttnWsViews)]
+    L.attn_softmax_workspace_views.restype = ctypes.c_int
+    L.attn_debug_gemm_bf16.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       _P, ctypes.c_int, _P, ctypes.c_int, _P, _P]
+    L.attn_debug_gemm_bf16.restype = ctypes.c_int
+    L.attn_softmax_set_option.argtypes = [ctypes.c_char_p, ctypes.c_int64]
+    L.attn_softmax_set_option.restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(code: int):
+    if code != 0:
+        raise AttnError(code, lib().attn_last_error().decode())
+
+
+def shape(B, N, M, d, V, dtype) -> AttnShape:
+    dt = {"f32": ATTN_F32, "bf16": ATTN_BF16, ATTN_F32: ATTN_F32,
+          ATTN_BF16: ATTN_BF16}[dtype]
+    return AttnShape(B, N, M, d, V, dt)
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _i32(a):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def attn_softmax_workspace_size(s: AttnShape) -> int:
+    n = lib().attn_softmax_workspace_size(ctypes.byref(s))
+    if n == 0:
+        raise AttnError(2, lib().attn_last_error().decode())
+    return n
+
+
+def attn_softmax_host_staging_size(s: AttnShape) -> int:
+    return lib().attn_softmax_host_staging_size(ctypes.byref(s))
+
+
+def attn_softmax_workspace_views(s: AttnShape) -> AttnWsViews:
+    v = AttnWsViews()
+    _check(lib().attn_softmax_workspace_views(ctypes.byref(s), ctypes.byref(v)))
+    return v
+
+
+def attn_softmax_fwd_bwd(s, H_dec, H_enc, src_lens, tgt_lens, tgt_ids, W_c,
+                         W_out, loss_scale, loss, dH_dec, dH_enc, dW_c, dW_out,
+                         workspace, comm=None, stream=None, W_alpha=None,
+                         dW_alpha=None):
+    src, src_p = _i32(src_lens)
+    tgt, tgt_p = _i32(tgt_lens)
+    _check(lib().attn_softmax_fwd_bwd(
+        ctypes.byref(s), _ptr(H_dec), _ptr(H_enc), src_p, tgt_p, _ptr(tgt_ids),
+        _ptr(W_c), _ptr(W_out), _ptr(W_alpha), float(loss_scale), _ptr(loss),
+        _ptr(dH_dec), _ptr(dH_enc), _ptr(dW_c), _ptr(dW_out), _ptr(dW_alpha),
+        _ptr(workspace), workspace.numel() * workspace.element_size(),
+        comm, _stream(stream)))
+
+
+def attn_softmax_fwd_bwd_host(s, H_dec_host, H_enc_host, src_lens, tgt_lens,
+                              tgt_ids_host, W_c, W_out, loss_scale, loss_host,
+                              dH_dec, dH_enc, dW_c, dW_out, staging, workspace,
+                              comm=None, stream=None):
+    src, src_p = _i32(src_lens)
+    tgt, tgt_p = _i32(tgt_lens)
+    _check(lib().attn_softmax_fwd_bwd_host(
+        ctypes.byref(s), _ptr(H_dec_host), _ptr(H_enc_host), src_p, tgt_p,
+        _ptr(tgt_ids_host), _ptr(W_c), _ptr(W_out), float(loss_scale),
+        _ptr(loss_host), _ptr(dH_dec), _ptr(dH_enc), _ptr(dW_c), _ptr(dW_out),
+        _ptr(staging), staging.numel() * staging.element_size(),
+        _ptr(workspace), workspace.numel() * workspace.element_size(),
+        comm, _stream(stream)))
+
+
+def attn_softmax_check_ids(s, tgt_lens, tgt_ids, stream=None):
+    tgt, tgt_p = _i32(tgt_lens)
+    _check(lib().attn_softmax_check_ids(ctypes.byref(s), tgt_p, _ptr(tgt_ids),
+                                        _stream(stream)))
+
+
+def attn_grad_allreduce(comm, buf, stream=None):
+    _check(lib().attn_grad_allreduce(comm, _ptr(buf), buf.numel(), _stream(stream)))
+
+
+def attn_comm_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().attn_comm_get_unique_id(buf))
+    return buf.raw
+
+
+def attn_comm_init(uid: bytes, nranks: int, rank: int, device: int):
+    out = _P()
+    _check(lib().attn_comm_init(uid, nranks, rank, device, ctypes.byref(out)))
+    return out
+
+
+def attn_comm_destroy(comm):
+    _check(lib().attn_comm_destroy(comm))
+
+
+def attn_debug_gemm_bf16(M, N, K, A, a_mn, B, b_mn, C, stream=None):
+    _check(lib().attn_debug_gemm_bf16(M, N, K, _ptr(A), int(a_mn), _ptr(B),
+                                      int(b_mn), _ptr(C), _stream(stream)))
+
+
+def attn_softmax_set_option(key: str, value: int):
+    _check(lib().attn_softmax_set_option(key.encode(), int(value)))
+
+
+def attn_last_error() -> str:
+    return lib().attn_last_error().decode()
+
+
+def attn_version() -> str:
+    return lib().attn_version().decode()

@@ -1,0 +1,760 @@
+// attn_softmax.cu -- libattnsm.so: the C ABI of include/attn_softmax.h, the
+// host planner (validation, workspace carving, TMA descriptors, V-chunk
+// schedule, streams / events) and the kernel launches of the stage.
+//
+// Stage order:
+//   F1-F2  attention scores, masked softmax, context       Eqs. 1-3
+//   F3     proj_tanh  H_c = tanh([H|C] W_c^T)              Eq. 4
+//   F4     vocab_fwd  per-tile (max, sumexp) + target logit, then lse_reduce
+//                                                           Eqs. 5-6
+//   B1     for each V-chunk c: dlogits_c (recomputed logits), dW_out[c],
+//          dHc += dL_c W_out[c] (last chunk: dz = dHc (1 - H_c^2))
+//   B2     dW_c = dz^T [H|C];  [dH_part | dC] = dz W_c
+//   B3     attention backward -> dH_dec, dH_enc
+//   X      dW_out chunks, dW_c, loss allreduced (comm != NULL)
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/attn_softmax.h"
+#include "../../include/attn_softmax_debug.h"
+#include "comm.h"
+#include "gemm_simt.cuh"
+#include "gemm_tc.cuh"
+#include "small_kernels.cuh"
+
+using namespace attnsm;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+static attn_status_t fail(attn_status_t code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(ATTN_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                  \
+  } while (0)
+
+extern "C" const char* attn_last_error(void) { return g_err.c_str(); }
+attn_status_t attn_set_error(attn_status_t code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+extern "C" const char* attn_version(void) { return "attnsm 0.1 sm_100a"; }
+
+// ------------------------------------------------------------------ options
+static int64_t g_opt_vocab_chunk = 0;
+static int64_t g_opt_gemm_ctas = 0;
+
+extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value) {
+  if (!key) return fail(ATTN_ERR_INVALID_ARG, "set_option: key is NULL");
+  if (!strcmp(key, "vocab_chunk")) {
+    if (value < 0 || value % 256 != 0)
+      return fail(ATTN_ERR_INVALID_ARG, "vocab_chunk must be a non-negative multiple of 256 (got %lld)",
+                  (long long)value);
+    g_opt_vocab_chunk = value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "gemm_ctas")) {
+    if (value < 0) return fail(ATTN_ERR_INVALID_ARG, "gemm_ctas must be >= 0");
+    g_opt_gemm_ctas = value;
+    return ATTN_OK;
+  }
+  return fail(ATTN_ERR_INVALID_ARG, "unknown option '%s'", key);
+}
+
+// ------------------------------------------------------------------ device info
+struct DevInfo {
+  int sms = 148;
+  size_t l2 = 126u << 20;
+};
+static DevInfo dev_info() {
+  DevInfo d;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+      d.sms = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) == cudaSuccess && v > 0) d.l2 = v;
+  }
+  return d;
+}
+
+// ------------------------------------------------------------------ TMA maps
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+
+// 2D bf16 tensor [outer, inner] with row stride ld (elements); box {64, box_outer}.
+static attn_status_t make_map(CUtensorMap* m, const void* ptr, long long inner, long long outer,
+                              long long ld, int box_outer) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (inner < 1) inner = 1;
+  if (outer < 1) outer = 1;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): ptr=%p inner=%lld outer=%lld ld=%lld",
+                (int)r, ptr, inner, outer, ld);
+  return ATTN_OK;
+}
+
+// ------------------------------------------------------------------ GEMM descriptions
+// C[M,N] = A[M,K] B[N,K]^T.  A: a_mn=0 -> [M,K] (ld lda), a_mn=1 -> [K,M].
+// K-major A may be split along K at a_ksplit between a0 / a1 (same ld).
+// B: b_mn=0 -> [N,K] (ld ldb), b_mn=1 -> [K,N]; MN-major B may be split along
+// N at b_nsplit between b0 / b1; b_koff shifts B's K coordinate; b_kext is the
+// K extent of the B tensor (defaults to K + b_koff).
+struct GemmDesc {
+  int M = 0, N = 0, K = 0;
+  const void* a0 = nullptr; const void* a1 = nullptr; int a_ksplit = 0; int a_mn = 0; long long lda = 0;
+  const void* b0 = nullptr; const void* b1 = nullptr; int b_nsplit = 0; int b_mn = 0; long long ldb = 0;
+  int b_koff = 0; long long b_kext = 0;
+  int k_splits = 1;
+  EpiParams epi{};
+};
+
+static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr, int tile_begin) {
+  memset(&pr, 0, sizeof(pr));
+  pr.M = g.M; pr.N = g.N; pr.K = g.K;
+  pr.tiles_m = (g.M + TC_BM - 1) / TC_BM;
+  pr.tiles_n = (g.N + TC_BN - 1) / TC_BN;
+  pr.kb_total = (g.K + TC_BK - 1) / TC_BK;
+  pr.k_splits = std::max(1, std::min(g.k_splits, pr.kb_total));
+  pr.kb_per_split = (pr.kb_total + pr.k_splits - 1) / pr.k_splits;
+  pr.k_splits = (pr.kb_total + pr.kb_per_split - 1) / pr.kb_per_split;
+  pr.tile_begin = tile_begin;
+  pr.a_mn = g.a_mn; pr.b_mn = g.b_mn;
+  pr.a_ksplit = g.a1 ? g.a_ksplit : 0;
+  pr.b_nsplit = g.b1 ? g.b_nsplit : 0;
+  pr.b_koff = g.b_koff;
+  pr.epi = g.epi;
+  attn_status_t st;
+  const long long bk = g.b_kext ? g.b_kext : (long long)g.K + g.b_koff;
+  if (!g.a_mn) {
+    const long long k0 = pr.a_ksplit ? pr.a_ksplit : g.K;
+    if ((st = make_map(&maps[0], g.a0, k0, g.M, g.lda, TC_BM)) != ATTN_OK) return st;
+    if ((st = make_map(&maps[1], pr.a_ksplit ? g.a1 : g.a0, pr.a_ksplit ? g.K - pr.a_ksplit : k0,
+                       g.M, g.lda, TC_BM)) != ATTN_OK) return st;
+  } else {
+    if ((st = make_map(&maps[0], g.a0, g.M, g.K, g.lda, 64)) != ATTN_OK) return st;
+    maps[1] = maps[0];
+  }
+  if (!g.b_mn) {
+    if ((st = make_map(&maps[2], g.b0, bk, g.N, g.ldb, TC_BN)) != ATTN_OK) return st;
+    maps[3] = maps[2];
+  } else {
+    const long long n0 = pr.b_nsplit ? pr.b_nsplit : g.N;
+    if ((st = make_map(&maps[2], g.b0, n0, bk, g.ldb, 64)) != ATTN_OK) return st;
+    if ((st = make_map(&maps[3], pr.b_nsplit ? g.b1 : g.b0, pr.b_nsplit ? g.N - pr.b_nsplit : n0,
+                       bk, g.ldb, 64)) != ATTN_OK) return st;
+  }
+  return ATTN_OK;
+}
+
+static void fill_simt(const GemmDesc& g, SimtProblem& pr, int tile_begin) {
+  memset(&pr, 0, sizeof(pr));
+  pr.M = g.M; pr.N = g.N; pr.K = g.K;
+  pr.tiles_m = (g.M + SG_BM - 1) / SG_BM;
+  pr.tiles_n = (g.N + SG_BN - 1) / SG_BN;
+  const int kchunks = (g.K + SG_BK - 1) / SG_BK;
+  int ks = std::max(1, std::min(g.k_splits, kchunks));
+  const int per = (kchunks + ks - 1) / ks;
+  pr.k_per_split = per * SG_BK;
+  pr.k_splits = (g.K + pr.k_per_split - 1) / pr.k_per_split;
+  pr.tile_begin = tile_begin;
+  pr.a0 = (const float*)g.a0; pr.a1 = (const float*)g.a1; pr.a_ksplit = g.a_ksplit;
+  if (!g.a_mn) { pr.sam = g.lda; pr.sak = 1; } else { pr.sam = 1; pr.sak = g.lda; }
+  pr.b0 = (const float*)g.b0; pr.b1 = (const float*)g.b1; pr.b_nsplit = g.b_nsplit; pr.b_koff = g.b_koff;
+  if (!g.b_mn) { pr.sbn = g.ldb; pr.sbk = 1; } else { pr.sbn = 1; pr.sbk = g.ldb; }
+  pr.epi = g.epi;
+}
+
+static int tc_smem_bytes() { return TC_SMEM_BYTES; }
+
+template <typename OutT>
+static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cudaStream_t stream) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<OutT, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes()));
+    attr_set = true;
+  }
+  TcParams P;
+  memset(&P, 0, sizeof(P));
+  int tiles = 0;
+  for (int i = 0; i < n; ++i) {
+    attn_status_t st = fill_tc(gs[i], P.maps[i], P.prob[i], tiles);
+    if (st != ATTN_OK) return st;
+    tiles += P.prob[i].tiles_m * P.prob[i].tiles_n * P.prob[i].k_splits;
+  }
+  P.nprob = n;
+  P.total_tiles = tiles;
+  P.tile_counter = counter;
+  if (tiles == 0) return ATTN_OK;
+  const DevInfo di = dev_info();
+  int grid = g_opt_gemm_ctas > 0 ? (int)g_opt_gemm_ctas : di.sms;
+  grid = std::min(grid, tiles);
+  gemm_tc_kernel<OutT, true><<<grid, TC_THREADS, tc_smem_bytes(), stream>>>(P);
+  CUDA_TRY(cudaGetLastError());
+  return ATTN_OK;
+}
+
+static attn_status_t launch_simt_group(const GemmDesc* gs, int n, cudaStream_t stream) {
+  SimtParams P;
+  memset(&P, 0, sizeof(P));
+  int tiles = 0;
+  for (int i = 0; i < n; ++i) {
+    fill_simt(gs[i], P.prob[i], tiles);
+    tiles += P.prob[i].tiles_m * P.prob[i].tiles_n * P.prob[i].k_splits;
+  }
+  P.nprob = n;
+  if (tiles == 0) return ATTN_OK;
+  gemm_simt_kernel<float><<<tiles, 256, 0, stream>>>(P);
+  CUDA_TRY(cudaGetLastError());
+  return ATTN_OK;
+}
+
+// ------------------------------------------------------------------ shapes / workspace
+static size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+static attn_status_t check_shape(const attn_shape_t* s) {
+  if (!s) return fail(ATTN_ERR_INVALID_ARG, "shape is NULL");
+  if (s->dtype != ATTN_F32 && s->dtype != ATTN_BF16)
+    return fail(ATTN_ERR_UNSUPPORTED, "dtype %d is not ATTN_F32 (0) or ATTN_BF16 (1)", (int)s->dtype);
+  if (s->batch <= 0 || s->tgt_len <= 0 || s->src_len <= 0 || s->hidden <= 0 || s->vocab <= 0)
+    return fail(ATTN_ERR_SHAPE,
+                "shape [B=%d, N=%d, M=%d, d=%d, V=%d]: every extent must be >= 1", s->batch,
+                s->tgt_len, s->src_len, s->hidden, s->vocab);
+  const long long T = (long long)s->batch * s->tgt_len;
+  if (T > (1ll << 30) || (long long)s->vocab > (1ll << 30) || s->hidden > (1 << 16))
+    return fail(ATTN_ERR_UNSUPPORTED, "shape [B=%d, N=%d, d=%d, V=%d] exceeds the supported range",
+                s->batch, s->tgt_len, s->hidden, s->vocab);
+  if (s->dtype == ATTN_BF16 && s->hidden % 64 != 0)
+    return fail(ATTN_ERR_UNSUPPORTED,
+                "bf16 path needs hidden %% 64 == 0 (TMA / UMMA K blocks); got d=%d", s->hidden);
+  return ATTN_OK;
+}
+
+struct Plan {
+  int B, N, M, d, V;
+  long long T;
+  bool bf16;
+  size_t elt;
+  int tileN;          // column tile of the vocab GEMM engine
+  int ntn;            // column tiles over V
+  int Vc;             // V-chunk width (multiple of 256)
+  int nchunks;
+  size_t off_lens, off_counters, off_blockpart, off_alpha, off_dalpha, off_ctx, off_hc, off_part,
+      off_tgtlogit, off_lse, off_nll, off_rowscale, off_dl, off_dhc, off_dz, off_dhc2;
+  size_t total;
+};
+constexpr int kNumCounters = 1024;
+
+static Plan make_plan(const attn_shape_t* s) {
+  Plan p;
+  p.B = s->batch; p.N = s->tgt_len; p.M = s->src_len; p.d = s->hidden; p.V = s->vocab;
+  p.T = (long long)p.B * p.N;
+  p.bf16 = s->dtype == ATTN_BF16;
+  p.elt = p.bf16 ? 2 : 4;
+  p.tileN = p.bf16 ? TC_BN : SG_BN;
+  p.ntn = (p.V + p.tileN - 1) / p.tileN;
+  const long long vpad = (p.V + 255) / 256 * 256;
+  long long vc = g_opt_vocab_chunk;
+  if (vc <= 0) {
+    // dlogits chunk (T x Vc) sized to stay L2-resident next to H_c, dHc and
+    // the W_out chunk
+    const long long budget = 28ll << 20;
+    vc = budget / (p.T * (long long)p.elt) / 256 * 256;
+    vc = std::max(vc, 256ll);
+  }
+  vc = std::min(vc, vpad);
+  p.Vc = (int)vc;
+  p.nchunks = (int)((p.V + p.Vc - 1) / p.Vc);
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes); return r; };
+  p.off_lens = take(2 * sizeof(int) * p.B);
+  p.off_counters = take(sizeof(int) * kNumCounters);
+  p.off_blockpart = take(sizeof(double) * ((p.T + 7) / 8 + 1));
+  p.off_alpha = take(sizeof(float) * p.T * p.M);
+  p.off_dalpha = take(sizeof(float) * p.T * p.M);
+  p.off_ctx = take(p.elt * p.T * p.d);
+  p.off_hc = take(p.elt * p.T * p.d);
+  p.off_part = take(sizeof(float2) * p.T * p.ntn);
+  p.off_tgtlogit = take(sizeof(float) * p.T);
+  p.off_lse = take(sizeof(float) * p.T);
+  p.off_nll = take(sizeof(float) * p.T);
+  p.off_rowscale = take(sizeof(float) * p.T);
+  p.off_dl = take(2 * p.elt * p.T * (size_t)p.Vc);
+  p.off_dhc = take(sizeof(float) * p.T * p.d);
+  p.off_dz = take(p.elt * p.T * p.d);
+  p.off_dhc2 = take(sizeof(float) * p.T * 2 * p.d);
+  p.total = o;
+  return p;
+}
+
+extern "C" size_t attn_softmax_workspace_size(const attn_shape_t* s) {
+  if (check_shape(s) != ATTN_OK) return 0;
+  return make_plan(s).total;
+}
+
+extern "C" attn_status_t attn_softmax_workspace_views(const attn_shape_t* s, attn_ws_views_t* out) {
+  attn_status_t st = check_shape(s);
+  if (st != ATTN_OK) return st;
+  if (!out) return fail(ATTN_ERR_INVALID_ARG, "out is NULL");
+  Plan p = make_plan(s);
+  out->alpha = p.off_alpha;
+  out->ctx = p.off_ctx;
+  out->hc = p.off_hc;
+  out->lse = p.off_lse;
+  out->nll = p.off_nll;
+  out->vocab_chunk = p.Vc;
+  return ATTN_OK;
+}
+
+// ------------------------------------------------------------------ attention (bgemm) launches
+template <typename TA0, typename TB0, typename TA1, typename TB1, typename OutT>
+static attn_status_t launch_bgemm(const BGemm<TA0, TB0, TA1, TB1, OutT>& g, cudaStream_t stream) {
+  if (g.batch == 0 || g.M == 0 || g.N == 0) return ATTN_OK;
+  dim3 grid((g.N + SG_BN - 1) / SG_BN, (g.M + SG_BM - 1) / SG_BM, g.batch);
+  bgemm_kernel<TA0, TB0, TA1, TB1, OutT><<<grid, 256, 0, stream>>>(g);
+  CUDA_TRY(cudaGetLastError());
+  return ATTN_OK;
+}
+
+template <typename T>
+static attn_status_t attention_forward(const Plan& p, const T* H, const T* S, const int* src_len,
+                                       float* alpha, T* ctx, cudaStream_t stream) {
+  // F1: scores e_b = H_b S_b^T (Eq. 2, dot form)
+  {
+    BGemm<T, T, T, T, float> g{};
+    g.batch = p.B; g.M = p.N; g.N = p.M; g.K0 = p.d; g.K1 = 0;
+    g.s0 = {H, (long long)p.N * p.d, p.d, 1, S, (long long)p.M * p.d, p.d, 1};
+    g.s1 = {H, 0, 0, 0, S, 0, 0, 0};
+    g.out = alpha; g.sob = (long long)p.N * p.M; g.som = p.M; g.son = 1;
+    attn_status_t st = launch_bgemm(g, stream);
+    if (st != ATTN_OK) return st;
+  }
+  // Eq. 1: masked row softmax (in place)
+  {
+    const int rows = (int)p.T;
+    softmax_fwd_kernel<<<(rows + 7) / 8, 256, 0, stream>>>(alpha, src_len, rows, p.N, p.M);
+    CUDA_TRY(cudaGetLastError());
+  }
+  // F2: C_b = alpha_b S_b (Eq. 3)
+  {
+    BGemm<float, T, float, T, T> g{};
+    g.batch = p.B; g.M = p.N; g.N = p.d; g.K0 = p.M; g.K1 = 0;
+    g.s0 = {alpha, (long long)p.N * p.M, p.M, 1, S, (long long)p.M * p.d, 1, p.d};
+    g.s1 = {alpha, 0, 0, 0, S, 0, 0, 0};
+    g.out = ctx; g.sob = (long long)p.N * p.d; g.som = p.d; g.son = 1;
+    return launch_bgemm(g, stream);
+  }
+}
+
+template <typename T>
+static attn_status_t attention_backward(const Plan& p, const T* H, const T* S, const float* alpha,
+                                        float* dalpha, const float* dhc2, T* dH, T* dS,
+                                        cudaStream_t stream) {
+  const long long ld2 = 2ll * p.d;
+  const float* dC = dhc2 + p.d;   // columns [d, 2d) of [dH_part | dC]
+  // dalpha_b = dC_b S_b^T
+  {
+    BGemm<float, T, float, T, float> g{};
+    g.batch = p.B; g.M = p.N; g.N = p.M; g.K0 = p.d; g.K1 = 0;
+    g.s0 = {dC, (long long)p.N * ld2, ld2, 1, S, (long long)p.M * p.d, p.d, 1};
+    g.s1 = {dC, 0, 0, 0, S, 0, 0, 0};
+    g.out = dalpha; g.sob = (long long)p.N * p.M; g.som = p.M; g.son = 1;
+    attn_status_t st = launch_bgemm(g, stream);
+    if (st != ATTN_OK) return st;
+  }
+  {
+    const int rows = (int)p.T;
+    softmax_bwd_kernel<<<(rows + 7) / 8, 256, 0, stream>>>(alpha, dalpha, rows, p.M);
+    CUDA_TRY(cudaGetLastError());
+  }
+  // dH_dec_b = dH_part_b + de_b S_b
+  {
+    BGemm<float, T, float, T, T> g{};
+    g.batch = p.B; g.M = p.N; g.N = p.d; g.K0 = p.M; g.K1 = 0;
+    g.s0 = {dalpha, (long long)p.N * p.M, p.M, 1, S, (long long)p.M * p.d, 1, p.d};
+    g.s1 = {dalpha, 0, 0, 0, S, 0, 0, 0};
+    g.out = dH; g.sob = (long long)p.N * p.d; g.som = p.d; g.son = 1;
+    g.add = dhc2; g.sadd_b = (long long)p.N * ld2; g.sadd_m = ld2; g.sadd_n = 1;
+    attn_status_t st = launch_bgemm(g, stream);
+    if (st != ATTN_OK) return st;
+  }
+  // dH_enc_b = alpha_b^T dC_b + de_b^T H_b  (two K segments over the decoder rows)
+  {
+    BGemm<float, float, float, T, T> g{};
+    g.batch = p.B; g.M = p.M; g.N = p.d; g.K0 = p.N; g.K1 = p.N;
+    g.s0 = {alpha, (long long)p.N * p.M, 1, p.M, dC, (long long)p.N * ld2, 1, ld2};
+    g.s1 = {dalpha, (long long)p.N * p.M, 1, p.M, H, (long long)p.N * p.d, 1, p.d};
+    g.out = dS; g.sob = (long long)p.M * p.d; g.som = p.d; g.son = 1;
+    return launch_bgemm(g, stream);
+  }
+}
+
+// ------------------------------------------------------------------ the stage
+struct Bufs {
+  int* src_len; int* tgt_len; unsigned int* counters; double* blockpart;
+  float* alpha; float* dalpha; void* ctx; void* hc; float2* part; float* tgt_logit;
+  float* lse; float* nll; float* rowscale; void* dl[2]; float* dhc; void* dz; float* dhc2;
+};
+
+static Bufs carve(const Plan& p, void* ws) {
+  char* w = (char*)ws;
+  Bufs b;
+  b.src_len = (int*)(w + p.off_lens);
+  b.tgt_len = b.src_len + p.B;
+  b.counters = (unsigned int*)(w + p.off_counters);
+  b.blockpart = (double*)(w + p.off_blockpart);
+  b.alpha = (float*)(w + p.off_alpha);
+  b.dalpha = (float*)(w + p.off_dalpha);
+  b.ctx = w + p.off_ctx;
+  b.hc = w + p.off_hc;
+  b.part = (float2*)(w + p.off_part);
+  b.tgt_logit = (float*)(w + p.off_tgtlogit);
+  b.lse = (float*)(w + p.off_lse);
+  b.nll = (float*)(w + p.off_nll);
+  b.rowscale = (float*)(w + p.off_rowscale);
+  b.dl[0] = w + p.off_dl;
+  b.dl[1] = w + p.off_dl + p.elt * p.T * (size_t)p.Vc;
+  b.dhc = (float*)(w + p.off_dhc);
+  b.dz = w + p.off_dz;
+  b.dhc2 = (float*)(w + p.off_dhc2);
+  return b;
+}
+
+static bool misaligned(const void* ptr) { return ptr && (reinterpret_cast<uintptr_t>(ptr) & 15); }
+
+static attn_status_t validate(const attn_shape_t* s, const void* H_dec, const void* H_enc,
+                              const int32_t* src_lens, const int32_t* tgt_lens,
+                              const int32_t* tgt_ids, const void* W_c, const void* W_out,
+                              const void* W_alpha, const float* loss, const void* dH_dec,
+                              const void* dH_enc, const float* dW_c, const float* dW_out,
+                              const float* dW_alpha, size_t ws_bytes, const void* ws) {
+  attn_status_t st = check_shape(s);
+  if (st != ATTN_OK) return st;
+  struct { const void* p; const char* n; } req[] = {
+      {H_dec, "H_dec"}, {H_enc, "H_enc"}, {src_lens, "src_lens_host"}, {tgt_lens, "tgt_lens_host"},
+      {tgt_ids, "tgt_ids"}, {W_c, "W_c"}, {W_out, "W_out"}, {loss, "loss"}, {dH_dec, "dH_dec"},
+      {dH_enc, "dH_enc"}, {dW_c, "dW_c"}, {dW_out, "dW_out"}, {ws, "workspace"}};
+  for (auto& r : req)
+    if (!r.p) return fail(ATTN_ERR_INVALID_ARG, "%s is NULL", r.n);
+  if (W_alpha || dW_alpha)
+    return fail(ATTN_ERR_UNSUPPORTED,
+                "W_alpha / dW_alpha must be NULL: the Eq. 2 'general' score (W_alpha) is not in "
+                "this build; the hot path uses the dot score (DESIGN.md R1)");
+  long long total_tgt = 0;
+  for (int b = 0; b < s->batch; ++b) {
+    if (src_lens[b] < 1)
+      return fail(ATTN_ERR_EMPTY_SOURCE, "src_lens_host[%d] = %d: every sentence needs >= 1 source position",
+                  b, src_lens[b]);
+    if (src_lens[b] > s->src_len)
+      return fail(ATTN_ERR_SHAPE, "src_lens_host[%d] = %d exceeds the padded source length M = %d of "
+                  "H_enc [%d, %d, %d]", b, src_lens[b], s->src_len, s->batch, s->src_len, s->hidden);
+    if (tgt_lens[b] < 0 || tgt_lens[b] > s->tgt_len)
+      return fail(ATTN_ERR_SHAPE, "tgt_lens_host[%d] = %d is outside [0, N = %d] of H_dec [%d, %d, %d]",
+                  b, tgt_lens[b], s->tgt_len, s->batch, s->tgt_len, s->hidden);
+    total_tgt += tgt_lens[b];
+  }
+  if (total_tgt == 0) return fail(ATTN_ERR_NO_TARGETS, "no valid target tokens (sum of tgt_lens_host is 0)");
+  Plan p = make_plan(s);
+  if (ws_bytes < p.total)
+    return fail(ATTN_ERR_WORKSPACE, "workspace_bytes = %zu < required %zu", ws_bytes, p.total);
+  if (s->dtype == ATTN_BF16) {
+    const void* al[] = {H_dec, H_enc, W_c, W_out, dH_dec, dH_enc, dW_c, dW_out, ws};
+    for (const void* a : al)
+      if (misaligned(a)) return fail(ATTN_ERR_UNSUPPORTED, "bf16 path needs 16-byte aligned pointers");
+  }
+  return ATTN_OK;
+}
+
+template <typename T>
+static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int32_t* tgt_ids,
+                               const T* W_c, const T* W_out, float loss_scale, float* loss, T* dH,
+                               T* dS, float* dW_c, float* dW_out, const Bufs& b, attn_comm_t* comm,
+                               cudaStream_t stream) {
+  attn_status_t st;
+  const bool tc = p.bf16;
+  int counter_idx = 0;
+  auto next_counter = [&]() { return (int*)(b.counters + 1 + (counter_idx++)); };
+  auto gemm = [&](const GemmDesc* gs, int n) -> attn_status_t {
+    if (tc) return launch_tc_group<__nv_bfloat16>(gs, n, next_counter(), stream);
+    return launch_simt_group(gs, n, stream);
+  };
+  const int d = p.d, V = p.V;
+  const long long TT = p.T;
+  CUDA_TRY(cudaMemsetAsync(b.counters, 0, sizeof(unsigned int) * kNumCounters, stream));
+
+  // ---- F1, F2 (Eqs. 1-3)
+  if ((st = attention_forward<T>(p, H, S, b.src_len, b.alpha, (T*)b.ctx, stream)) != ATTN_OK) return st;
+
+  // ---- F3 (Eq. 4): H_c = tanh([H | C] W_c^T)
+  {
+    GemmDesc g;
+    g.M = (int)TT; g.N = d; g.K = 2 * d;
+    g.a0 = H; g.a1 = b.ctx; g.a_ksplit = d; g.a_mn = 0; g.lda = d;
+    g.b0 = W_c; g.b_mn = 0; g.ldb = 2ll * d;
+    g.epi.kind = EPI_TANH; g.epi.out = b.hc; g.epi.ldo = d; g.epi.ncols_valid = d; g.epi.ncols_store = d;
+    if ((st = gemm(&g, 1)) != ATTN_OK) return st;
+  }
+  // ---- F4 (Eq. 5): per-tile (max, sumexp) and target logit, logits discarded
+  {
+    GemmDesc g;
+    g.M = (int)TT; g.N = V; g.K = d;
+    g.a0 = b.hc; g.a_mn = 0; g.lda = d;
+    g.b0 = W_out; g.b_mn = 0; g.ldb = d;
+    g.epi.kind = EPI_LSE; g.epi.ncols_valid = V; g.epi.ncols_store = V; g.epi.col_base = 0;
+    g.epi.part = b.part; g.epi.part_ld = p.ntn; g.epi.tgt_logit = b.tgt_logit; g.epi.tgt = tgt_ids;
+    if ((st = gemm(&g, 1)) != ATTN_OK) return st;
+  }
+  // ---- Eq. 6: lse, token NLL, row scale, loss
+  {
+    const int blocks = (int)((TT + 7) / 8);
+    lse_reduce_kernel<<<blocks, 256, 0, stream>>>(b.part, p.ntn, b.tgt_logit, b.tgt_len, (int)TT, p.N,
+                                                  loss_scale, b.lse, b.nll, b.rowscale, b.blockpart,
+                                                  b.counters, loss);
+    CUDA_TRY(cudaGetLastError());
+  }
+  CommRun cr;
+  if (comm) {
+    if ((st = comm_begin(comm, stream, &cr)) != ATTN_OK) return st;
+  }
+
+  // ---- B1: V-chunked vocab backward
+  auto dl_desc = [&](int c) {
+    GemmDesc g;
+    const int c0 = c * p.Vc;
+    const int vcc = std::min(p.Vc, V - c0);
+    g.M = (int)TT; g.N = vcc; g.K = d;
+    g.a0 = b.hc; g.a_mn = 0; g.lda = d;
+    g.b0 = (const char*)W_out + (size_t)c0 * d * sizeof(T); g.b_mn = 0; g.ldb = d;
+    g.epi.kind = EPI_DLOGITS; g.epi.out = b.dl[c & 1]; g.epi.ldo = p.Vc;
+    g.epi.ncols_valid = vcc; g.epi.ncols_store = p.Vc; g.epi.col_base = c0;
+    g.epi.lse = b.lse; g.epi.rowscale = b.rowscale; g.epi.tgt = tgt_ids;
+    return g;
+  };
+  auto dwo_desc = [&](int c) {
+    GemmDesc g;
+    const int c0 = c * p.Vc;
+    const int vcc = std::min(p.Vc, V - c0);
+    g.M = vcc; g.N = d; g.K = (int)TT;
+    g.a0 = b.dl[c & 1]; g.a_mn = 1; g.lda = p.Vc;
+    g.b0 = b.hc; g.b_mn = 1; g.ldb = d;
+    g.epi.kind = EPI_STORE_F32; g.epi.out = dW_out + (size_t)c0 * d; g.epi.ldo = d;
+    g.epi.ncols_valid = d; g.epi.ncols_store = d;
+    return g;
+  };
+  auto dhc_desc = [&](int c) {
+    GemmDesc g;
+    const int c0 = c * p.Vc;
+    const int vcc = std::min(p.Vc, V - c0);
+    g.M = (int)TT; g.N = d; g.K = vcc;
+    g.a0 = b.dl[c & 1]; g.a_mn = 0; g.lda = p.Vc;
+    g.b0 = W_out; g.b_mn = 1; g.ldb = d; g.b_koff = c0; g.b_kext = V;
+    g.epi.kind = EPI_DHC; g.epi.acc_f32 = b.dhc; g.epi.ldo = d; g.epi.hc = b.hc; g.epi.out = b.dz;
+    g.epi.ncols_valid = d; g.epi.ncols_store = d;
+    g.epi.first = (c == 0); g.epi.last = (c == p.nchunks - 1);
+    return g;
+  };
+  {
+    GemmDesc g0 = dl_desc(0);
+    if ((st = gemm(&g0, 1)) != ATTN_OK) return st;
+    for (int c = 0; c < p.nchunks; ++c) {
+      GemmDesc gs[3];
+      int n = 0;
+      gs[n++] = dwo_desc(c);   // K = T: the long tiles first
+      gs[n++] = dhc_desc(c);
+      if (c + 1 < p.nchunks) gs[n++] = dl_desc(c + 1);
+      if ((st = gemm(gs, n)) != ATTN_OK) return st;
+      if (comm) {
+        const int c0 = c * p.Vc;
+        const int vcc = std::min(p.Vc, V - c0);
+        if ((st = comm_enqueue_allreduce(comm, &cr, stream, dW_out + (size_t)c0 * d,
+                                         (size_t)vcc * d)) != ATTN_OK)
+          return st;
+      }
+    }
+  }
+  // ---- B2: dW_c = dz^T [H | C];  [dH_part | dC] = dz W_c
+  {
+    GemmDesc gs[2];
+    GemmDesc& g = gs[0];
+    g.M = d; g.N = 2 * d; g.K = (int)TT;
+    g.a0 = b.dz; g.a_mn = 1; g.lda = d;
+    g.b0 = H; g.b1 = b.ctx; g.b_nsplit = d; g.b_mn = 1; g.ldb = d;
+    g.epi.kind = EPI_STORE_F32; g.epi.out = dW_c; g.epi.ldo = 2ll * d;
+    g.epi.ncols_valid = 2 * d; g.epi.ncols_store = 2 * d;
+    GemmDesc& h = gs[1];
+    h.M = (int)TT; h.N = 2 * d; h.K = d;
+    h.a0 = b.dz; h.a_mn = 0; h.lda = d;
+    h.b0 = W_c; h.b_mn = 1; h.ldb = 2ll * d;
+    h.epi.kind = EPI_STORE_F32; h.epi.out = b.dhc2; h.epi.ldo = 2ll * d;
+    h.epi.ncols_valid = 2 * d; h.epi.ncols_store = 2 * d;
+    if ((st = gemm(gs, 2)) != ATTN_OK) return st;
+    if (comm) {
+      if ((st = comm_enqueue_allreduce(comm, &cr, stream, dW_c, (size_t)d * 2 * d)) != ATTN_OK) return st;
+    }
+  }
+  // ---- B3: attention backward
+  if ((st = attention_backward<T>(p, H, S, b.alpha, b.dalpha, b.dhc2, dH, dS, stream)) != ATTN_OK)
+    return st;
+  if (comm) {
+    if ((st = comm_enqueue_allreduce(comm, &cr, stream, loss, 1)) != ATTN_OK) return st;
+    if ((st = comm_end(comm, &cr, stream)) != ATTN_OK) return st;
+  }
+  return ATTN_OK;
+}
+
+extern "C" attn_status_t attn_softmax_fwd_bwd(
+    const attn_shape_t* s, const void* H_dec, const void* H_enc, const int32_t* src_lens_host,
+    const int32_t* tgt_lens_host, const int32_t* tgt_ids, const void* W_c, const void* W_out,
+    const void* W_alpha, float loss_scale, float* loss, void* dH_dec, void* dH_enc, float* dW_c,
+    float* dW_out, float* dW_alpha, void* workspace, size_t workspace_bytes, attn_comm_t* comm,
+    void* stream_) {
+  attn_status_t st = validate(s, H_dec, H_enc, src_lens_host, tgt_lens_host, tgt_ids, W_c, W_out,
+                              W_alpha, loss, dH_dec, dH_enc, dW_c, dW_out, dW_alpha,
+                              workspace_bytes, workspace);
+  if (st != ATTN_OK) return st;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const Plan p = make_plan(s);
+  const Bufs b = carve(p, workspace);
+  // lengths: host -> workspace (the harness's arrays are small and pageable)
+  std::vector<int32_t> lens(2 * p.B);
+  memcpy(lens.data(), src_lens_host, sizeof(int32_t) * p.B);
+  memcpy(lens.data() + p.B, tgt_lens_host, sizeof(int32_t) * p.B);
+  CUDA_TRY(cudaMemcpyAsync(b.src_len, lens.data(), sizeof(int32_t) * 2 * p.B,
+                           cudaMemcpyHostToDevice, stream));
+  if (p.bf16)
+    return run_stage<__nv_bfloat16>(p, (const __nv_bfloat16*)H_dec, (const __nv_bfloat16*)H_enc,
+                                    tgt_ids, (const __nv_bfloat16*)W_c,
+                                    (const __nv_bfloat16*)W_out, loss_scale, loss,
+                                    (__nv_bfloat16*)dH_dec, (__nv_bfloat16*)dH_enc, dW_c, dW_out,
+                                    b, comm, stream);
+  return run_stage<float>(p, (const float*)H_dec, (const float*)H_enc, tgt_ids, (const float*)W_c,
+                          (const float*)W_out, loss_scale, loss, (float*)dH_dec, (float*)dH_enc,
+                          dW_c, dW_out, b, comm, stream);
+}
+
+// ------------------------------------------------------------------ host-buffer variant
+extern "C" size_t attn_softmax_host_staging_size(const attn_shape_t* s) {
+  if (check_shape(s) != ATTN_OK) return 0;
+  const size_t elt = s->dtype == ATTN_BF16 ? 2 : 4;
+  const size_t T = (size_t)s->batch * s->tgt_len;
+  return align_up(elt * T * s->hidden) + align_up(elt * (size_t)s->batch * s->src_len * s->hidden) +
+         align_up(sizeof(int32_t) * T) + align_up(sizeof(float));
+}
+
+extern "C" attn_status_t attn_softmax_fwd_bwd_host(
+    const attn_shape_t* s, const void* H_dec_host, const void* H_enc_host,
+    const int32_t* src_lens_host, const int32_t* tgt_lens_host, const int32_t* tgt_ids_host,
+    const void* W_c, const void* W_out, float loss_scale, float* loss_host, void* dH_dec,
+    void* dH_enc, float* dW_c, float* dW_out, void* staging, size_t staging_bytes,
+    void* workspace, size_t workspace_bytes, attn_comm_t* comm, void* stream_) {
+  attn_status_t st = check_shape(s);
+  if (st != ATTN_OK) return st;
+  if (!H_dec_host || !H_enc_host || !tgt_ids_host || !loss_host || !staging)
+    return fail(ATTN_ERR_INVALID_ARG, "host-variant buffer is NULL");
+  const size_t need = attn_softmax_host_staging_size(s);
+  if (staging_bytes < need)
+    return fail(ATTN_ERR_WORKSPACE, "staging_bytes = %zu < required %zu", staging_bytes, need);
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const size_t elt = s->dtype == ATTN_BF16 ? 2 : 4;
+  const size_t T = (size_t)s->batch * s->tgt_len;
+  const size_t bh = elt * T * s->hidden, be = elt * (size_t)s->batch * s->src_len * s->hidden;
+  char* st0 = (char*)staging;
+  void* dHd = st0;
+  void* dHe = st0 + align_up(bh);
+  int32_t* dIds = (int32_t*)(st0 + align_up(bh) + align_up(be));
+  float* dLoss = (float*)((char*)dIds + align_up(sizeof(int32_t) * T));
+  CUDA_TRY(cudaMemcpyAsync(dHd, H_dec_host, bh, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemcpyAsync(dHe, H_enc_host, be, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemcpyAsync(dIds, tgt_ids_host, sizeof(int32_t) * T, cudaMemcpyHostToDevice, stream));
+  st = attn_softmax_fwd_bwd(s, dHd, dHe, src_lens_host, tgt_lens_host, dIds, W_c, W_out, nullptr,
+                            loss_scale, dLoss, dH_dec, dH_enc, dW_c, dW_out, nullptr, workspace,
+                            workspace_bytes, comm, stream_);
+  if (st != ATTN_OK) return st;
+  CUDA_TRY(cudaMemcpyAsync(loss_host, dLoss, sizeof(float), cudaMemcpyDeviceToHost, stream));
+  return ATTN_OK;
+}
+
+// ------------------------------------------------------------------ id check
+extern "C" attn_status_t attn_softmax_check_ids(const attn_shape_t* s, const int32_t* tgt_lens_host,
+                                                const int32_t* tgt_ids, void* stream_) {
+  attn_status_t st = check_shape(s);
+  if (st != ATTN_OK) return st;
+  if (!tgt_lens_host || !tgt_ids) return fail(ATTN_ERR_INVALID_ARG, "NULL argument");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const int T = s->batch * s->tgt_len;
+  int* dev = nullptr;
+  CUDA_TRY(cudaMallocAsync(&dev, sizeof(int) * (1 + s->batch), stream));
+  CUDA_TRY(cudaMemsetAsync(dev, 0, sizeof(int), stream));
+  CUDA_TRY(cudaMemcpyAsync(dev + 1, tgt_lens_host, sizeof(int) * s->batch, cudaMemcpyHostToDevice, stream));
+  check_ids_kernel<<<(T + 255) / 256, 256, 0, stream>>>(tgt_ids, dev + 1, T, s->tgt_len, s->vocab, dev);
+  int bad = 0;
+  CUDA_TRY(cudaMemcpyAsync(&bad, dev, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaFreeAsync(dev, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  if (bad) return fail(ATTN_ERR_TOKEN_RANGE, "a valid target id is outside [0, V = %d)", s->vocab);
+  return ATTN_OK;
+}
+
+// ------------------------------------------------------------------ debug GEMM
+extern "C" attn_status_t attn_debug_gemm_bf16(int M, int N, int K, const void* A, int a_mn,
+                                              const void* B, int b_mn, float* C, void* stream_) {
+  if (M <= 0 || N <= 0 || K <= 0 || !A || !B || !C)
+    return fail(ATTN_ERR_INVALID_ARG, "debug_gemm: bad arguments");
+  GemmDesc g;
+  g.M = M; g.N = N; g.K = K;
+  g.a0 = A; g.a_mn = a_mn; g.lda = a_mn ? M : K;
+  g.b0 = B; g.b_mn = b_mn; g.ldb = b_mn ? N : K;
+  g.epi.kind = EPI_STORE_F32; g.epi.out = C; g.epi.ldo = N; g.epi.ncols_valid = N; g.epi.ncols_store = N;
+  int* counter = nullptr;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  CUDA_TRY(cudaMallocAsync(&counter, sizeof(int), stream));
+  CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int), stream));
+  attn_status_t st = launch_tc_group<__nv_bfloat16>(&g, 1, counter, stream);
+  CUDA_TRY(cudaFreeAsync(counter, stream));
+  return st;
+}

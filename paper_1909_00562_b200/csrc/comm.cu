@@ -1,0 +1,168 @@
+// comm.cu -- NCCL communicator of libattnsm.so (see comm.h).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "comm.h"
+
+// Minimal NCCL ABI (nccl.h 2.x): opaque comm, 128-byte unique id, enums.
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+enum { ncclSuccess_ = 0, ncclInProgress_ = 7 };
+enum { ncclFloat32_ = 7 };
+enum { ncclSum_ = 0 };
+
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+  std::string why;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    void* h = nullptr;
+    for (const char* n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+      if (!h) h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) {
+      api.why = std::string("dlopen(libnccl.so.2) failed: ") + (dlerror() ? dlerror() : "?");
+      return;
+    }
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+    api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy;
+    if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
+  });
+  return api;
+}
+
+struct attn_comm {
+  ncclComm_t comm = nullptr;
+  cudaStream_t stream = nullptr;
+  std::vector<cudaEvent_t> events;  // fork events, reused round-robin
+  cudaEvent_t join = nullptr;
+  int device = 0;
+};
+
+// errors are reported through attn_last_error(); defined in attn_softmax.cu
+attn_status_t attn_set_error(attn_status_t code, const char* msg);
+
+static attn_status_t err(attn_status_t code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  return attn_set_error(code, buf);
+}
+
+#define CUDA_OK(expr)                                                                            \
+  do {                                                                                           \
+    cudaError_t e_ = (expr);                                                                     \
+    if (e_ != cudaSuccess) return err(ATTN_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+#define NCCL_OK(expr)                                                                        \
+  do {                                                                                       \
+    ncclResult_t r_ = (expr);                                                                \
+    if (r_ != ncclSuccess_)                                                                  \
+      return err(ATTN_ERR_NCCL, "%s: %s", #expr,                                             \
+                 nccl().GetErrorString ? nccl().GetErrorString(r_) : "nccl error");          \
+  } while (0)
+
+extern "C" attn_status_t attn_comm_get_unique_id(uint8_t id[128]) {
+  if (!id) return err(ATTN_ERR_INVALID_ARG, "id is NULL");
+  NcclApi& api = nccl();
+  if (!api.ok) return err(ATTN_ERR_NCCL, "%s", api.why.c_str());
+  ncclUniqueId u;
+  NCCL_OK(api.GetUniqueId(&u));
+  memcpy(id, u.internal, 128);
+  return ATTN_OK;
+}
+
+extern "C" attn_status_t attn_comm_init(const uint8_t id[128], int nranks, int rank, int device,
+                                        attn_comm_t** out) {
+  if (!id || !out) return err(ATTN_ERR_INVALID_ARG, "id / out is NULL");
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return err(ATTN_ERR_INVALID_ARG, "rank %d of %d is invalid", rank, nranks);
+  NcclApi& api = nccl();
+  if (!api.ok) return err(ATTN_ERR_NCCL, "%s", api.why.c_str());
+  CUDA_OK(cudaSetDevice(device));
+  attn_comm* c = new attn_comm();
+  c->device = device;
+  ncclUniqueId u;
+  memcpy(u.internal, id, 128);
+  ncclResult_t r = api.CommInitRank(&c->comm, nranks, u, rank);
+  if (r != ncclSuccess_) {
+    delete c;
+    return err(ATTN_ERR_NCCL, "ncclCommInitRank: %s", api.GetErrorString ? api.GetErrorString(r) : "?");
+  }
+  // high-priority comm stream so the allreduce kernels get SMs as GEMM CTAs retire
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  CUDA_OK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi));
+  c->events.resize(64);
+  for (auto& e : c->events) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CUDA_OK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
+  *out = c;
+  return ATTN_OK;
+}
+
+extern "C" attn_status_t attn_comm_destroy(attn_comm_t* c) {
+  if (!c) return ATTN_OK;
+  cudaStreamSynchronize(c->stream);
+  if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+  for (auto& e : c->events) cudaEventDestroy(e);
+  cudaEventDestroy(c->join);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return ATTN_OK;
+}
+
+extern "C" attn_status_t attn_grad_allreduce(attn_comm_t* c, float* buf, size_t count, void* stream) {
+  if (!c || (!buf && count)) return err(ATTN_ERR_INVALID_ARG, "comm / buf is NULL");
+  if (count == 0) return ATTN_OK;
+  NCCL_OK(nccl().AllReduce(buf, buf, count, ncclFloat32_, ncclSum_, c->comm, (cudaStream_t)stream));
+  return ATTN_OK;
+}
+
+attn_status_t comm_begin(attn_comm_t* c, cudaStream_t compute, CommRun* run) {
+  (void)compute;
+  run->n_enqueued = 0;
+  return c ? ATTN_OK : err(ATTN_ERR_INVALID_ARG, "comm is NULL");
+}
+
+attn_status_t comm_enqueue_allreduce(attn_comm_t* c, CommRun* run, cudaStream_t compute, float* buf,
+                                     size_t count) {
+  cudaEvent_t e = c->events[run->n_enqueued % c->events.size()];
+  CUDA_OK(cudaEventRecord(e, compute));
+  CUDA_OK(cudaStreamWaitEvent(c->stream, e, 0));
+  NCCL_OK(nccl().AllReduce(buf, buf, count, ncclFloat32_, ncclSum_, c->comm, c->stream));
+  run->n_enqueued++;
+  return ATTN_OK;
+}
+
+attn_status_t comm_end(attn_comm_t* c, CommRun* run, cudaStream_t compute) {
+  (void)run;
+  CUDA_OK(cudaEventRecord(c->join, c->stream));
+  CUDA_OK(cudaStreamWaitEvent(compute, c->join, 0));
+  return ATTN_OK;
+}

@@ -1,0 +1,26 @@
+// comm.h -- NCCL plumbing of libattnsm.so (internal).
+//
+// The gradient exchange of the data-parallel stage ("GPU 0 as
+// the root for accumulating and synchronizing") is a rootless NCCL sum
+// allreduce over NVLink / NVSwitch.  NCCL is resolved at run time with
+// dlopen("libnccl.so.2") (the copy torch already loaded), so the library has
+// no link-time NCCL dependency and single-GPU use never touches it.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "../../include/attn_softmax.h"
+
+// One in-flight fwd_bwd call's use of the communicator: the compute stream
+// forks to the comm stream after each finished gradient block and joins back
+// at the end.
+struct CommRun {
+  int n_enqueued = 0;
+};
+
+attn_status_t comm_begin(attn_comm_t* c, cudaStream_t compute, CommRun* run);
+// Enqueue an in-place fp32 sum allreduce of buf[0..count) that starts once
+// `compute` reaches this point, on the communicator's own stream.
+attn_status_t comm_enqueue_allreduce(attn_comm_t* c, CommRun* run, cudaStream_t compute,
+                                     float* buf, size_t count);
+// Make `compute` wait for every allreduce enqueued in this run.
+attn_status_t comm_end(attn_comm_t* c, CommRun* run, cudaStream_t compute);

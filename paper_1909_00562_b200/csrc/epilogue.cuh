@@ -1,0 +1,219 @@
+// epilogue.cuh -- row-oriented GEMM epilogues shared by the tcgen05 engine
+// (gemm_tc.cuh) and the fp32 CUDA-core engine (gemm_simt.cuh).
+//
+// Both engines hand an epilogue one output row at a time, in chunks of 32
+// consecutive fp32 accumulator columns (the tcgen05.ld 32x32b.x32 shape: one
+// row per thread, so row reductions need no cross-thread traffic).
+//
+//   EPI_STORE_F32  out[r,c] = acc                    (dW_out chunk, dW_c, [dH|dC])
+//   EPI_TANH       out[r,c] = tanh(acc)              (Eq. 4)
+//   EPI_LSE        per (row, column tile): running max m and sum_c exp(acc-m)
+//                  over columns c < ncols_valid, and the target logit when the
+//                  row's target id falls in the tile (Eqs. 5-6 forward)
+//   EPI_DLOGITS    out[r,c] = rowscale[r] * (exp(acc - lse[r]) - [c+col_base == y_r])
+//                  (softmax - onehot; backward of Eqs. 5-6)
+//   EPI_DHC        dHc += acc over V-chunks; on the last chunk
+//                  dz = dHc * (1 - Hc^2)  (tanh backward of Eq. 4)
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+
+namespace attnsm {
+
+enum EpiKind : int { EPI_STORE_F32 = 0, EPI_TANH = 1, EPI_LSE = 2, EPI_DLOGITS = 3, EPI_DHC = 4 };
+
+struct EpiParams {
+  int kind;
+  int ncols_valid;       // columns < ncols_valid are real (V tail, chunk tail)
+  int ncols_store;       // columns < ncols_store may be written (row capacity)
+  int col_base;          // global column of problem column 0 (V-chunk start)
+  void* out;             // STORE_F32: float; TANH/DLOGITS: OutT; DHC: OutT (dz)
+  long long ldo;         // row stride of out (elements)
+  long long split_stride;// element offset between split-K partial outputs
+  float2* part;          // LSE: [rows, part_ld] (max, sumexp)
+  int part_ld;
+  float* tgt_logit;      // LSE: [rows]
+  const int* tgt;        // LSE/DLOGITS: [rows] target ids
+  const float* lse;      // DLOGITS: [rows]
+  const float* rowscale; // DLOGITS: [rows] loss_scale on valid rows, 0 on padded
+  float* acc_f32;        // DHC: running dHc [rows, ldo] fp32
+  const void* hc;        // DHC: H_c [rows, ldo] OutT
+  int first, last;       // DHC: first / last V-chunk
+};
+
+template <typename T> __device__ __forceinline__ T to_out(float x);
+template <> __device__ __forceinline__ float to_out<float>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+__device__ __forceinline__ float to_f32(float x) { return x; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+template <bool kFast>
+__device__ __forceinline__ float tanh_f(float x) {
+  if constexpr (kFast) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+  } else {
+    return tanhf(x);
+  }
+}
+template <bool kFast>
+__device__ __forceinline__ float exp_f(float x) {
+  if constexpr (kFast) return __expf(x);
+  else return expf(x);
+}
+
+// Store 32 consecutive values (vectorised when the whole chunk fits and the
+// row is 16-byte aligned).
+template <typename OutT>
+__device__ __forceinline__ void store_row32(OutT* rowp, int col0, int ncols_store,
+                                            const float (&v)[32], bool vec_ok) {
+  if (vec_ok && col0 + 32 <= ncols_store) {
+    if constexpr (sizeof(OutT) == 2) {
+      uint4* dst = reinterpret_cast<uint4*>(rowp + col0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
+          w[e] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+        dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    } else {
+      float4* dst = reinterpret_cast<float4*>(rowp + col0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col0 + j < ncols_store) rowp[col0 + j] = to_out<OutT>(v[j]);
+  }
+}
+
+struct LseState {
+  float m, s, t;
+  int has_t;
+};
+
+// One output row of one tile.  `row` is the problem row (< M checked by the
+// caller), `tile_n` the column-tile index inside the problem, `col0` the
+// problem column of v[0].
+template <typename OutT, bool kFast>
+struct RowEpilogue {
+  const EpiParams& p;
+  int row;
+  int split;
+  LseState st;
+  int y;
+  float lse, rs;
+  __device__ __forceinline__ RowEpilogue(const EpiParams& p_, int row_, int split_)
+      : p(p_), row(row_), split(split_) {
+    st.m = -INFINITY;
+    st.s = 0.f;
+    st.t = 0.f;
+    st.has_t = 0;
+    y = -1;
+    lse = 0.f;
+    rs = 0.f;
+    if (p.kind == EPI_LSE || p.kind == EPI_DLOGITS) y = p.tgt[row] - p.col_base;
+    if (p.kind == EPI_DLOGITS) {
+      lse = p.lse[row];
+      rs = p.rowscale[row];
+    }
+  }
+
+  __device__ __forceinline__ void chunk(int col0, float (&v)[32]) {
+    const int kind = p.kind;
+    if (kind == EPI_LSE) {
+      const int nv = p.ncols_valid - col0;
+      if (nv <= 0) return;
+      float cm = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nv) cm = fmaxf(cm, v[j]);
+      const float nm = fmaxf(st.m, cm);
+      float s = st.s * exp_f<kFast>(st.m - nm);
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nv) s += exp_f<kFast>(v[j] - nm);
+      st.s = s;
+      st.m = nm;
+      const int yl = y - col0;
+      if (yl >= 0 && yl < 32 && yl < nv) {
+        float t = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) t = (j == yl) ? v[j] : t;
+        st.t = t;
+        st.has_t = 1;
+      }
+    } else if (kind == EPI_DLOGITS) {
+      if (col0 >= p.ncols_store) return;
+      const int yl = y - col0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        float g = rs * (exp_f<kFast>(v[j] - lse) - (j == yl ? 1.f : 0.f));
+        v[j] = (col0 + j < p.ncols_valid) ? g : 0.f;
+      }
+      OutT* rowp = reinterpret_cast<OutT*>(p.out) + (long long)row * p.ldo;
+      store_row32<OutT>(rowp, col0, p.ncols_store, v, (p.ldo * sizeof(OutT)) % 16 == 0);
+    } else if (kind == EPI_TANH) {
+      if (col0 >= p.ncols_store) return;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = tanh_f<kFast>(v[j]);
+      OutT* rowp = reinterpret_cast<OutT*>(p.out) + (long long)row * p.ldo;
+      store_row32<OutT>(rowp, col0, p.ncols_store, v, (p.ldo * sizeof(OutT)) % 16 == 0);
+    } else if (kind == EPI_STORE_F32) {
+      if (col0 >= p.ncols_store) return;
+      float* rowp = reinterpret_cast<float*>(p.out) + (long long)split * p.split_stride +
+                    (long long)row * p.ldo;
+      store_row32<float>(rowp, col0, p.ncols_store, v, (p.ldo * 4) % 16 == 0);
+    } else if (kind == EPI_DHC) {
+      if (col0 >= p.ncols_store) return;
+      float* accp = p.acc_f32 + (long long)row * p.ldo;
+      const bool vec = (p.ldo * 4) % 16 == 0 && col0 + 32 <= p.ncols_store;
+      if (!p.first) {
+        if (vec) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4 a = reinterpret_cast<const float4*>(accp + col0)[q];
+            v[4 * q] += a.x;
+            v[4 * q + 1] += a.y;
+            v[4 * q + 2] += a.z;
+            v[4 * q + 3] += a.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < p.ncols_store) v[j] += accp[col0 + j];
+        }
+      }
+      if (!p.last) {
+        store_row32<float>(accp, col0, p.ncols_store, v, (p.ldo * 4) % 16 == 0);
+      } else {
+        const OutT* hcp = reinterpret_cast<const OutT*>(p.hc) + (long long)row * p.ldo;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float h = (col0 + j < p.ncols_store) ? to_f32(hcp[col0 + j]) : 0.f;
+          v[j] = v[j] * (1.f - h * h);
+        }
+        OutT* dzp = reinterpret_cast<OutT*>(p.out) + (long long)row * p.ldo;
+        store_row32<OutT>(dzp, col0, p.ncols_store, v, (p.ldo * sizeof(OutT)) % 16 == 0);
+      }
+    }
+  }
+
+  __device__ __forceinline__ void finish(int tile_n) {
+    if (p.kind == EPI_LSE) {
+      p.part[(long long)row * p.part_ld + tile_n] = make_float2(st.m, st.s);
+      if (st.has_t) p.tgt_logit[row] = st.t;
+    }
+  }
+};
+
+}  // namespace attnsm

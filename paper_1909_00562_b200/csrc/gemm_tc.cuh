@@ -1,0 +1,267 @@
+// gemm_tc.cuh -- persistent, warp-specialised tcgen05 GEMM engine (sm_100a).
+//
+//   D[M,N] (fp32, in TMEM) = A[M,K] * B[N,K]^T,  bf16 operands staged by TMA
+//   (128-byte swizzle) into a 4-stage shared-memory ring; the epilogue reads
+//   the accumulator with tcgen05.ld and runs one of the row epilogues of
+//   epilogue.cuh.  One launch runs a GROUP of up to kMaxProblems independent
+//   problems (e.g. the V-chunk c dW_out and dHc GEMMs together with the
+//   chunk c+1 dlogits GEMM); CTAs pull tiles from a global atomic counter so
+//   long-K and short-K tiles balance across the 148 SMs.
+//
+// Roles (256 threads, one CTA per SM):
+//   warp 0      tile scheduler + TMA producer (one elected lane)
+//   warp 1      MMA issuer (one lane issues tcgen05.mma for the whole CTA)
+//   warp 2      TMEM allocator (512 columns = two 128x256 fp32 accumulators)
+//   warps 4..7  epilogue: warp w reads TMEM lanes 32*(w%4)..+31 = tile rows
+//
+// Operands may be K-major (row-major [rows, K]) or MN-major (row-major
+// [K, rows]); see DESIGN.md "tcgen05 encodings" for the descriptor fields.
+#pragma once
+#include "epilogue.cuh"
+#include "ptx.cuh"
+
+namespace attnsm {
+
+constexpr int TC_BM = 128;
+constexpr int TC_BN = 256;
+constexpr int TC_BK = 64;
+constexpr int TC_STAGES = 4;
+constexpr int TC_THREADS = 256;
+constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;             // 16 KB
+constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;             // 32 KB
+constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;   // 48 KB
+constexpr int TC_SCHED = 4;
+constexpr int TC_SMEM_BYTES = TC_STAGES * TC_STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+constexpr int kMaxProblems = 4;
+
+struct TcProblem {
+  int M, N, K;
+  int tiles_m, tiles_n, k_splits, kb_per_split, kb_total;
+  int tile_begin;
+  int a_mn, b_mn;
+  int a_ksplit;   // K-major A: k < a_ksplit -> map a0 else a1 (at k - a_ksplit); 0 = none
+  int b_nsplit;   // MN-major B: n < b_nsplit -> map b0 else b1 (at n - b_nsplit); 0 = none
+  int b_koff;     // added to B's K coordinate
+  EpiParams epi;
+};
+
+struct alignas(64) TcParams {
+  CUtensorMap maps[kMaxProblems][4];  // a0, a1, b0, b1
+  TcProblem prob[kMaxProblems];
+  int nprob;
+  int total_tiles;
+  int* tile_counter;
+};
+
+__device__ __forceinline__ int tc_find_problem(const TcParams& P, int t) {
+  int p = 0;
+#pragma unroll
+  for (int i = 1; i < kMaxProblems; ++i)
+    if (i < P.nprob && t >= P.prob[i].tile_begin) p = i;
+  return p;
+}
+
+struct TcTile {
+  int p, m0, n0, tn, split, kb0, kb1;
+};
+
+__device__ __forceinline__ TcTile tc_decode(const TcParams& P, int t) {
+  TcTile r;
+  r.p = tc_find_problem(P, t);
+  const TcProblem& pr = P.prob[r.p];
+  int local = t - pr.tile_begin;
+  const int per_split = pr.tiles_m * pr.tiles_n;
+  r.split = local / per_split;
+  local -= r.split * per_split;
+  const int tm = local % pr.tiles_m;
+  r.tn = local / pr.tiles_m;
+  r.m0 = tm * TC_BM;
+  r.n0 = r.tn * TC_BN;
+  r.kb0 = r.split * pr.kb_per_split;
+  r.kb1 = min(pr.kb_total, r.kb0 + pr.kb_per_split);
+  return r;
+}
+
+template <typename OutT, bool kFast>
+__global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_constant__ TcParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE_BYTES);
+  uint64_t* full = bars;                       // [STAGES]
+  uint64_t* empty = full + TC_STAGES;          // [STAGES]
+  uint64_t* tfull = empty + TC_STAGES;         // [2]
+  uint64_t* tempty = tfull + 2;                // [2]
+  uint64_t* sfull = tempty + 2;                // [SCHED]
+  uint64_t* sempty = sfull + TC_SCHED;         // [SCHED]
+  int* sched_tile = reinterpret_cast<int*>(sempty + TC_SCHED);   // [SCHED]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_tile + TC_SCHED);
+
+  const uint32_t warp = warp_id_uniform();
+  const uint32_t lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < TC_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    for (int i = 0; i < TC_SCHED; ++i) {
+      mbar_init(&sfull[i], 1);
+      mbar_init(&sempty[i], 1 + 4);
+    }
+    fence_barrier_init();
+    for (int p = 0; p < P.nprob; ++p)
+      for (int j = 0; j < 4; ++j) tma_prefetch_desc(&P.maps[p][j]);
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- tile scheduler + TMA producer
+      int s = 0;
+      uint32_t ph = 0;
+      int r = 0;
+      uint32_t rph = 0;
+      for (;;) {
+        int t = atomicAdd(P.tile_counter, 1);
+        if (t >= P.total_tiles) t = -1;
+        mbar_wait(&sempty[r], rph ^ 1);
+        sched_tile[r] = t;
+        mbar_arrive(&sfull[r]);
+        if (++r == TC_SCHED) { r = 0; rph ^= 1; }
+        if (t < 0) break;
+        const TcTile tl = tc_decode(P, t);
+        const TcProblem& pr = P.prob[tl.p];
+        const CUtensorMap* ma0 = &P.maps[tl.p][0];
+        const CUtensorMap* ma1 = &P.maps[tl.p][1];
+        const CUtensorMap* mb0 = &P.maps[tl.p][2];
+        const CUtensorMap* mb1 = &P.maps[tl.p][3];
+        for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* sA = smem + s * TC_STAGE_BYTES;
+          uint8_t* sB = sA + TC_A_BYTES;
+          mbar_arrive_expect_tx(&full[s], TC_STAGE_BYTES);
+          const int k0 = kb * TC_BK;
+          if (!pr.a_mn) {
+            if (pr.a_ksplit > 0 && k0 >= pr.a_ksplit)
+              tma_load_2d(sA, ma1, &full[s], k0 - pr.a_ksplit, tl.m0);
+            else
+              tma_load_2d(sA, ma0, &full[s], k0, tl.m0);
+          } else {
+#pragma unroll
+            for (int i = 0; i < TC_BM / 64; ++i)
+              tma_load_2d(sA + i * 8192, ma0, &full[s], tl.m0 + 64 * i, k0);
+          }
+          const int kb_ = k0 + pr.b_koff;
+          if (!pr.b_mn) {
+            tma_load_2d(sB, mb0, &full[s], kb_, tl.n0);
+          } else {
+#pragma unroll
+            for (int i = 0; i < TC_BN / 64; ++i) {
+              const int n = tl.n0 + 64 * i;
+              if (pr.b_nsplit > 0 && n >= pr.b_nsplit)
+                tma_load_2d(sB + i * 8192, mb1, &full[s], n - pr.b_nsplit, kb_);
+              else
+                tma_load_2d(sB + i * 8192, mb0, &full[s], n, kb_);
+            }
+          }
+          if (++s == TC_STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      int s = 0;
+      uint32_t ph = 0;
+      int r = 0;
+      uint32_t rph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (;;) {
+        mbar_wait(&sfull[r], rph);
+        const int t = sched_tile[r];
+        mbar_arrive(&sempty[r]);
+        if (++r == TC_SCHED) { r = 0; rph ^= 1; }
+        if (t < 0) break;
+        const TcTile tl = tc_decode(P, t);
+        const TcProblem& pr = P.prob[tl.p];
+        const uint32_t idesc = umma_idesc_bf16(TC_BM, TC_BN, pr.a_mn, pr.b_mn);
+        const uint32_t a_lbo = pr.a_mn ? 8192u : 16u;
+        const uint32_t b_lbo = pr.b_mn ? 8192u : 16u;
+        const uint32_t a_kstep = pr.a_mn ? 2048u : 32u;
+        const uint32_t b_kstep = pr.b_mn ? 2048u : 32u;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t dcol = tmem_base + acc * TC_BN;
+        for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t sA = smem_u32(smem + s * TC_STAGE_BYTES);
+          const uint32_t sB = sA + TC_A_BYTES;
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k) {
+            const uint64_t ad = umma_sdesc(sA + k * a_kstep, a_lbo, 1024);
+            const uint64_t bd = umma_sdesc(sB + k * b_kstep, b_lbo, 1024);
+            umma_bf16(dcol, ad, bd, idesc, (kb > tl.kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
+          if (++s == TC_STAGES) { s = 0; ph ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue
+    const uint32_t q = warp & 3;
+    int r = 0;
+    uint32_t rph = 0;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (;;) {
+      mbar_wait(&sfull[r], rph);
+      const int t = sched_tile[r];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty[r]);
+      if (++r == TC_SCHED) { r = 0; rph ^= 1; }
+      if (t < 0) break;
+      const TcTile tl = tc_decode(P, t);
+      const TcProblem& pr = P.prob[tl.p];
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const int row = tl.m0 + q * 32 + lane;
+      const bool row_ok = row < pr.M;
+      const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * TC_BN;
+      RowEpilogue<OutT, kFast> epi(pr.epi, row_ok ? row : 0, tl.split);
+      const int ncol_chunks = min(TC_BN, pr.N - tl.n0 + 31) / 32;
+#pragma unroll 1
+      for (int c = 0; c < TC_BN / 32; ++c) {
+        float v[32];
+        if (c < ncol_chunks) {   // warp-uniform
+          tmem_ld32(taddr + c * 32, v);
+          if (row_ok) epi.chunk(tl.n0 + c * 32, v);
+        }
+      }
+      if (row_ok) epi.finish(tl.tn);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem_base, 512);
+}
+
+}  // namespace attnsm

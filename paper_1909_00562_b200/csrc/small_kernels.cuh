@@ -1,0 +1,139 @@
+// small_kernels.cuh -- memory-bound kernels of the stage (both dtype paths).
+//
+//   softmax_fwd_kernel   Eq. 1: masked row softmax of the
+//                        attention scores over j < src_len[b]; masked
+//                        positions become exactly 0 (reading R8).  One warp
+//                        per decoder row, warp-shuffle max / sum.
+//   softmax_bwd_kernel   backward of Eq. 1: de_ij = a_ij (da_ij - sum_k a_ik da_ik)
+//   lse_reduce_kernel    Eqs. 5-6: combine the per-tile (max, sumexp)
+//                        partials of the vocab GEMM epilogue into lse_t, the
+//                        token NLL lse_t - l_{t,y_t} on valid rows, the row
+//                        scale of the backward, and the deterministic loss sum.
+//   check_ids_kernel     target-id range check (ATTN_ERR_TOKEN_RANGE)
+#pragma once
+#include <cstdint>
+
+namespace attnsm {
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// buf [B*N, M] fp32: scores in, alpha out (in place).
+__global__ void __launch_bounds__(256) softmax_fwd_kernel(float* __restrict__ buf,
+                                                          const int* __restrict__ src_len,
+                                                          int rows, int N, int M) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int L = src_len[row / N];
+  float* e = buf + (long long)row * M;
+  float mx = -INFINITY;
+  for (int j = lane; j < L; j += 32) mx = fmaxf(mx, e[j]);
+  mx = warp_max(mx);
+  float s = 0.f;
+  for (int j = lane; j < L; j += 32) s += expf(e[j] - mx);
+  s = warp_sum(s);
+  const float inv = 1.f / s;
+  for (int j = lane; j < M; j += 32) e[j] = (j < L) ? expf(e[j] - mx) * inv : 0.f;
+}
+
+// alpha [B*N, M], da [B*N, M] (dalpha in, de out in place).
+__global__ void __launch_bounds__(256) softmax_bwd_kernel(const float* __restrict__ alpha,
+                                                          float* __restrict__ da, int rows,
+                                                          int M) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* a = alpha + (long long)row * M;
+  float* g = da + (long long)row * M;
+  float D = 0.f;
+  for (int j = lane; j < M; j += 32) D += a[j] * g[j];
+  D = warp_sum(D);
+  for (int j = lane; j < M; j += 32) g[j] = a[j] * (g[j] - D);
+}
+
+// One warp per row t = b*N + i.  part [T, part_ld] (max, sumexp).
+// Block partial sums (double) go to blockpart[]; the last block to finish
+// sums them in index order (deterministic) and writes *loss.
+__global__ void __launch_bounds__(256) lse_reduce_kernel(
+    const float2* __restrict__ part, int part_ld, const float* __restrict__ tgt_logit,
+    const int* __restrict__ tgt_len, int T, int N, float loss_scale, float* __restrict__ lse_out,
+    float* __restrict__ nll_out, float* __restrict__ rowscale, double* __restrict__ blockpart,
+    unsigned int* __restrict__ done_counter, float* __restrict__ loss) {
+  __shared__ double wsum[8];
+  __shared__ bool is_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + warp;
+  double contrib = 0.0;
+  if (row < T) {
+    const float2* pr = part + (long long)row * part_ld;
+    float mx = -INFINITY;
+    for (int j = lane; j < part_ld; j += 32) mx = fmaxf(mx, pr[j].x);
+    mx = warp_max(mx);
+    float s = 0.f;
+    for (int j = lane; j < part_ld; j += 32) {
+      const float2 q = pr[j];
+      s += q.y * expf(q.x - mx);
+    }
+    s = warp_sum(s);
+    const float lse = mx + logf(s);
+    const bool valid = (row % N) < tgt_len[row / N];
+    const float nll = valid ? lse - tgt_logit[row] : 0.f;
+    if (lane == 0) {
+      lse_out[row] = lse;
+      nll_out[row] = nll;
+      rowscale[row] = valid ? loss_scale : 0.f;
+    }
+    contrib = (double)nll;
+  }
+  if (lane == 0) wsum[warp] = contrib;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < 8; ++w) b += wsum[w];
+    blockpart[blockIdx.x] = b;
+    __threadfence();
+    const unsigned int prev = atomicAdd(done_counter, 1u);
+    is_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (is_last) {
+    __threadfence();
+    if (threadIdx.x < 32) {
+      double acc = 0.0;
+      // fixed assignment of blocks to lanes, fixed shuffle tree: deterministic
+      for (int i = threadIdx.x; i < (int)gridDim.x; i += 32)
+        acc += ((volatile double*)blockpart)[i];
+      acc = warp_sum_d(acc);
+      if (threadIdx.x == 0) {
+        *loss = (float)(acc * (double)loss_scale);
+        *done_counter = 0u;
+      }
+    }
+  }
+}
+
+__global__ void check_ids_kernel(const int* __restrict__ ids, const int* __restrict__ tgt_len,
+                                 int T, int N, int V, int* __restrict__ bad) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  if ((t % N) < tgt_len[t / N]) {
+    const int y = ids[t];
+    if (y < 0 || y >= V) atomicExch(bad, 1);
+  }
+}
+
+}  // namespace attnsm

@@ -1,0 +1,74 @@
+"""Convenience wrapper over the C ABI: allocates the workspace and outputs
+with PyTorch and calls attn_softmax_fwd_bwd.  No arithmetic happens here."""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+
+from . import binding
+
+_TORCH_DTYPE = {"f32": torch.float32, "bf16": torch.bfloat16}
+
+
+class AttnSoftmaxStage:
+    """One GPU's shard of the data-parallel attention-softmax stage."""
+
+    def __init__(self, B: int, N: int, M: int, d: int, V: int, dtype: str,
+                 device: Optional[torch.device] = None):
+        self.B, self.N, self.M, self.d, self.V, self.dtype = B, N, M, d, V, dtype
+        self.tdtype = _TORCH_DTYPE[dtype]
+        self.device = torch.device(device or "cuda")
+        self.shape = binding.shape(B, N, M, d, V, dtype)
+        nbytes = binding.attn_softmax_workspace_size(self.shape)
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.views_meta = binding.attn_softmax_workspace_views(self.shape)
+
+    def alloc_outputs(self):
+        dev, B, N, M, d, V = self.device, self.B, self.N, self.M, self.d, self.V
+        return dict(
+            loss=torch.empty(1, dtype=torch.float32, device=dev),
+            dH_dec=torch.empty(B, N, d, dtype=self.tdtype, device=dev),
+            dH_enc=torch.empty(B, M, d, dtype=self.tdtype, device=dev),
+            dW_c=torch.empty(d, 2 * d, dtype=torch.float32, device=dev),
+            dW_out=torch.empty(V, d, dtype=torch.float32, device=dev))
+
+    def __call__(self, H_dec, H_enc, src_len, tgt_len, tgt_ids, W_c, W_out,
+                 loss_scale: float, out=None, comm=None, stream=None):
+        if out is None:
+            out = self.alloc_outputs()
+        binding.attn_softmax_fwd_bwd(
+            self.shape, H_dec, H_enc, src_len, tgt_len, tgt_ids, W_c, W_out,
+            loss_scale, out["loss"], out["dH_dec"], out["dH_enc"], out["dW_c"],
+            out["dW_out"], self.workspace, comm=comm, stream=stream)
+        return out
+
+    def views(self):
+        """Intermediates of the last call, as views into the workspace."""
+        v, ws = self.views_meta, self.workspace
+        T = self.B * self.N
+
+        def view(off, n, dt):
+            esz = torch.empty((), dtype=dt).element_size()
+            return ws[off: off + n * esz].view(dt)
+
+        return dict(
+            alpha=view(v.alpha, T * self.M, torch.float32).view(self.B, self.N, self.M),
+            C=view(v.ctx, T * self.d, self.tdtype).view(self.B, self.N, self.d),
+            Hc=view(v.hc, T * self.d, self.tdtype).view(self.B, self.N, self.d),
+            lse=view(v.lse, T, torch.float32),
+            nll=view(v.nll, T, torch.float32),
+            vocab_chunk=int(v.vocab_chunk))
+
+
+def to_device(inp: dict, dtype: str, device="cuda"):
+    """numpy inputs from synthetic.make_inputs -> torch device tensors."""
+    td = _TORCH_DTYPE[dtype]
+    out = {}
+    for k in ("H_dec", "H_enc", "W_c", "W_out", "W_alpha"):
+        if k in inp:
+            out[k] = torch.from_numpy(inp[k]).to(device=device, dtype=td).contiguous()
+    out["tgt_ids"] = torch.from_numpy(inp["tgt_ids"]).to(device=device, dtype=torch.int32).contiguous()
+    out["src_len"] = inp["src_len"]
+    out["tgt_len"] = inp["tgt_len"]
+    return out

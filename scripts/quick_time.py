@@ -1,0 +1,34 @@
+"""Quick C1 timing of the stage (development aid, not the bench contract)."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from paper_1909_00562_b200 import binding
+from paper_1909_00562_b200.stage import AttnSoftmaxStage, to_device
+from synthetic import CONFIGS, make_inputs, global_valid_tokens
+
+name = sys.argv[1] if len(sys.argv) > 1 else "paper"
+cfg = CONFIGS[name]
+t0 = time.time()
+inp = make_inputs(cfg)
+print(f"inputs {time.time()-t0:.1f}s", flush=True)
+st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
+dv = to_device(inp, cfg.dtype)
+scale = 1.0 / global_valid_tokens(cfg, cfg.B)
+out = st.alloc_outputs()
+args = (dv["H_dec"], dv["H_enc"], dv["src_len"], dv["tgt_len"], dv["tgt_ids"], dv["W_c"], dv["W_out"], scale)
+for _ in range(3):
+    st(*args, out=out)
+torch.cuda.synchronize()
+print("loss", out["loss"].item(), "vc", st.views()["vocab_chunk"], flush=True)
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+ev[0].record()
+n = 10
+for _ in range(n):
+    st(*args, out=out)
+ev[1].record()
+torch.cuda.synchronize()
+ms = ev[0].elapsed_time(ev[1]) / n
+tok = int(inp["tgt_len"].sum())
+flops = tok * (6 * cfg.d * cfg.V + 12 * cfg.d * cfg.d + 12 * cfg.M * cfg.d)
+print(f"{name}: {ms:.3f} ms/step, {tok/ms*1e3:.0f} tok/s, useful {flops/ms/1e9:.1f} TFLOP/s")

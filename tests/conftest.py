@@ -20,5 +20,15 @@ def cuda_lib():
     import torch
     if not torch.cuda.is_available():
         pytest.fail("gpu test selected but torch.cuda.is_available() is False")
-    from paper_1909_00562_b200 import binding
+    from paper_1909_00562_b200 import binding, build
+    build.build()
+    return binding.lib()
+
+
+@pytest.fixture(scope="session")
+def built_lib():
+    """Build libattnsm.so in-tree if needed (nvcc cross-compiles without a
+    GPU) and load it."""
+    from paper_1909_00562_b200 import binding, build
+    build.build()
     return binding.lib()

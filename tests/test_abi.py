@@ -1,0 +1,138 @@
+"""C-ABI surface checks that need no GPU: the library loads, exports every
+symbol the headers declare, and rejects bad arguments with the documented
+status codes before touching the device (include/attn_softmax.h "Errors")."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_1909_00562_b200 import binding
+from paper_1909_00562_b200.binding import AttnError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_functions():
+    names = set()
+    for h in ("attn_softmax.h", "attn_softmax_debug.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names |= set(re.findall(r"\b(attn_[a-z_0-9]+)\s*\(", src))
+    return names
+
+
+def test_exports_every_declared_symbol(built_lib):
+    declared = _declared_functions()
+    assert len(declared) >= 14
+    assert declared == set(binding.EXPORTS)
+    for name in declared:
+        assert hasattr(built_lib, name), name
+    assert "sm_100a" in binding.attn_version()
+
+
+def test_sass_is_tcgen05(built_lib):
+    """The GEMM core is tcgen05 + TMA (UTCHMMA / UTMALDG / LDTM in SASS)."""
+    import shutil, subprocess
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cuobjdump):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([cuobjdump, "-sass", binding.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    for mnem in ("UTCHMMA", "UTMALDG", "LDTM"):
+        assert mnem in sass, mnem
+    assert "HMMA.16816" not in sass  # no legacy mma.sync path
+
+
+def test_workspace_size(built_lib):
+    s = binding.shape(128, 50, 50, 1024, 50000, "bf16")
+    n = binding.attn_softmax_workspace_size(s)
+    assert 100 << 20 < n < 1 << 31
+    v = binding.attn_softmax_workspace_views(s)
+    offs = [v.alpha, v.ctx, v.hc, v.lse, v.nll]
+    assert all(0 < o < n for o in offs)
+    assert v.vocab_chunk % 256 == 0 and v.vocab_chunk > 0
+    for bad in [binding.shape(0, 50, 50, 1024, 50000, "bf16"),
+                binding.shape(1, 50, 50, 1000, 50000, "bf16"),   # d % 64 != 0
+                binding.AttnShape(1, 1, 1, 8, 8, 5)]:
+        assert built_lib.attn_softmax_workspace_size(ctypes.byref(bad)) == 0
+        assert binding.attn_last_error()
+
+
+class _Fake:
+    """Stands in for a device tensor; validation fails before any use."""
+    def __init__(self, n=1 << 40):
+        self._n = n
+
+    def data_ptr(self):
+        return 0x10000000
+
+    def numel(self):
+        return self._n
+
+    def element_size(self):
+        return 1
+
+
+def _call(s, src, tgt, ws=None, **over):
+    f = _Fake()
+    args = dict(H_dec=f, H_enc=f, tgt_ids=f, W_c=f, W_out=f, loss=f, dH_dec=f,
+                dH_enc=f, dW_c=f, dW_out=f, workspace=ws or f)
+    args.update(over)
+    binding.attn_softmax_fwd_bwd(s, args["H_dec"], args["H_enc"], src, tgt,
+                                 args["tgt_ids"], args["W_c"], args["W_out"], 1.0,
+                                 args["loss"], args["dH_dec"], args["dH_enc"],
+                                 args["dW_c"], args["dW_out"], args["workspace"],
+                                 stream=0, W_alpha=over.get("W_alpha"))
+
+
+@pytest.mark.parametrize("src,tgt,status", [
+    ([0, 3], [2, 2], "ATTN_ERR_EMPTY_SOURCE"),
+    ([6, 3], [2, 2], "ATTN_ERR_SHAPE"),
+    ([5, 3], [6, 2], "ATTN_ERR_SHAPE"),
+    ([5, 3], [-1, 2], "ATTN_ERR_SHAPE"),
+    ([5, 3], [0, 0], "ATTN_ERR_NO_TARGETS"),
+])
+def test_length_errors(built_lib, src, tgt, status):
+    s = binding.shape(2, 5, 5, 64, 300, "bf16")
+    with pytest.raises(AttnError) as e:
+        _call(s, src, tgt)
+    assert e.value.status == status
+    if status == "ATTN_ERR_SHAPE":
+        # the message names the offending argument and the tensor shape
+        assert "lens_host" in str(e.value) and "[2, 5, 64]" in str(e.value)
+
+
+def test_null_and_workspace_errors(built_lib):
+    s = binding.shape(2, 5, 5, 64, 300, "bf16")
+
+    class Null(_Fake):
+        def data_ptr(self):
+            return 0
+    with pytest.raises(AttnError) as e:
+        _call(s, [5, 3], [5, 4], H_enc=Null())
+    assert e.value.status == "ATTN_ERR_INVALID_ARG" and "H_enc" in str(e.value)
+    with pytest.raises(AttnError) as e:
+        _call(s, [5, 3], [5, 4], ws=_Fake(1000))
+    assert e.value.status == "ATTN_ERR_WORKSPACE"
+    with pytest.raises(AttnError) as e:
+        _call(s, [5, 3], [5, 4], W_alpha=_Fake())
+    assert e.value.status == "ATTN_ERR_UNSUPPORTED"
+
+    class Odd(_Fake):
+        def data_ptr(self):
+            return 0x10000008
+    with pytest.raises(AttnError) as e:
+        _call(s, [5, 3], [5, 4], W_out=Odd())
+    assert e.value.status == "ATTN_ERR_UNSUPPORTED"
+
+
+def test_options_and_comm_args(built_lib):
+    with pytest.raises(AttnError):
+        binding.attn_softmax_set_option("vocab_chunk", 100)
+    with pytest.raises(AttnError):
+        binding.attn_softmax_set_option("nope", 1)
+    binding.attn_softmax_set_option("vocab_chunk", 0)
+    with pytest.raises(AttnError) as e:
+        binding.attn_comm_init(b"\0" * 128, 2, 5, 0)
+    assert e.value.status == "ATTN_ERR_INVALID_ARG"

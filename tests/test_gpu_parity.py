@@ -1,0 +1,140 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on
+the same seeded inputs.  Bars (BASELINE.json north_star): bf16 -- loss rel
+<= 2e-3, every gradient rel-L2 <= 2e-2; fp32 -- 1e-5 and 1e-4."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import attn_softmax_oracle as O
+from synthetic import CONFIGS, make_inputs, global_valid_tokens
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f32": dict(loss=1e-5, grad=1e-4, inter=1e-5),
+       "bf16": dict(loss=2e-3, grad=2e-2, inter=1e-2)}
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def run_gpu(cfg, inp, scale, vocab_chunk=0):
+    from paper_1909_00562_b200 import binding
+    from paper_1909_00562_b200.stage import AttnSoftmaxStage, to_device
+    binding.attn_softmax_set_option("vocab_chunk", vocab_chunk)
+    try:
+        st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
+        dv = to_device(inp, cfg.dtype)
+        out = st(dv["H_dec"], dv["H_enc"], dv["src_len"], dv["tgt_len"], dv["tgt_ids"],
+                 dv["W_c"], dv["W_out"], scale)
+        torch.cuda.synchronize()
+    finally:
+        binding.attn_softmax_set_option("vocab_chunk", 0)
+    res = {k: v.float().cpu().numpy() for k, v in out.items()}
+    res["loss"] = float(res["loss"][0])
+    views = st.views()
+    for k in ("alpha", "C", "Hc", "lse", "nll"):
+        res[k] = views[k].float().cpu().numpy()
+    res["vocab_chunk"] = views["vocab_chunk"]
+    return res
+
+
+def oracle(inp, scale):
+    return O.fwd_bwd(inp["H_dec"], inp["H_enc"], inp["src_len"], inp["tgt_len"],
+                     inp["tgt_ids"], inp["W_c"], inp["W_out"], scale)
+
+
+# ------------------------------------------------------------ GEMM core ----
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 520, 200), (1000, 264, 1536)])
+def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K):
+    """The tcgen05 engine alone, all operand majors, with M/N/K tails."""
+    from paper_1909_00562_b200 import binding
+    g = torch.Generator(device="cpu").manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, generator=g).bfloat16()
+    B = torch.randn(N, K, generator=g).bfloat16()
+    ref = A.double() @ B.double().T
+    Ad = (A.T.contiguous() if a_mn else A).cuda()
+    Bd = (B.T.contiguous() if b_mn else B).cuda()
+    C = torch.full((M, N), float("nan"), device="cuda")
+    binding.attn_debug_gemm_bf16(M, N, K, Ad, a_mn, Bd, b_mn, C)
+    torch.cuda.synchronize()
+    err = (C.double().cpu() - ref).abs().max().item()
+    assert err < 1e-3 * max(1.0, ref.abs().max().item()), err
+
+
+# ------------------------------------------------------ end-to-end parity --
+@pytest.mark.parametrize("name,vc", [("tiny", 0), ("tiny_ragged", 0), ("small_f32", 0),
+                                     ("small_f32", 256), ("small", 0), ("small", 1024),
+                                     ("medium", 0), ("medium", 2048)])
+def test_parity_vs_oracle(cuda_lib, name, vc):
+    cfg = CONFIGS[name]
+    inp = make_inputs(cfg)
+    scale = 1.0 / global_valid_tokens(cfg, cfg.B)
+    g = run_gpu(cfg, inp, scale, vocab_chunk=vc)
+    f, b = oracle(inp, scale)
+    tol = TOL[cfg.dtype]
+    assert abs(g["loss"] - f["loss"]) <= tol["loss"] * abs(f["loss"]), (g["loss"], f["loss"])
+    for k in ("dH_dec", "dH_enc", "dW_c", "dW_out"):
+        e = rel_l2(g[k], b[k])
+        assert e <= tol["grad"], (k, e)
+    # stage by stage (intermediates stashed in the workspace)
+    assert rel_l2(g["alpha"], f["alpha"]) <= tol["inter"]
+    assert rel_l2(g["C"], f["C"]) <= tol["inter"]
+    assert rel_l2(g["Hc"], f["Hc"]) <= tol["inter"]
+    lse_tol = 1e-4 if cfg.dtype == "f32" else 2e-2
+    assert np.max(np.abs(g["lse"] - f["lse"])) <= lse_tol
+    # exactness properties (I2, I3, I4)
+    for bb in range(cfg.B):
+        L, Tb = int(inp["src_len"][bb]), int(inp["tgt_len"][bb])
+        assert np.all(g["alpha"][bb, :, L:] == 0.0)
+        assert np.all(g["dH_enc"][bb, L:] == 0.0)
+        assert np.all(g["dH_dec"][bb, Tb:] == 0.0)
+        assert np.all(g["nll"][bb * cfg.N + Tb:(bb + 1) * cfg.N] == 0.0)
+    # I1 rows sum to 1
+    assert np.abs(g["alpha"].sum(-1) - 1).max() < 1e-5
+
+
+@pytest.mark.parametrize("name", ["tiny_ragged", "small"])
+def test_padding_garbage_is_bitwise_inert(cuda_lib, name):
+    """I5: finite garbage in padded slots changes no GPU output bit."""
+    cfg = CONFIGS[name]
+    inp = make_inputs(cfg)
+    alt = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in inp.items()}
+    rng = np.random.default_rng(5)
+    for b in range(cfg.B):
+        L, Tb = int(inp["src_len"][b]), int(inp["tgt_len"][b])
+        alt["H_enc"][b, L:] = np.float32(rng.uniform(-3, 3))
+        alt["H_dec"][b, Tb:] = np.float32(rng.uniform(-3, 3))
+        alt["tgt_ids"][b, Tb:] = rng.integers(-5000, 5000)
+    scale = 1.0 / global_valid_tokens(cfg, cfg.B)
+    g0 = run_gpu(cfg, inp, scale)
+    g1 = run_gpu(cfg, alt, scale)
+    assert g0["loss"] == g1["loss"]
+    for k in ("dW_c", "dW_out"):
+        np.testing.assert_array_equal(g0[k], g1[k])
+    for b in range(cfg.B):
+        np.testing.assert_array_equal(g0["dH_dec"][b], g1["dH_dec"][b])
+        np.testing.assert_array_equal(g0["dH_enc"][b], g1["dH_enc"][b])
+
+
+def test_dw_out_column_sums_vanish(cuda_lib):
+    """I6 on the GPU result: sum_v dW_out[v,:] = 0 (each dlogits row sums to 0)."""
+    cfg = CONFIGS["medium"]
+    inp = make_inputs(cfg)
+    g = run_gpu(cfg, inp, 1.0 / global_valid_tokens(cfg, cfg.B))
+    col = g["dW_out"].astype(np.float64).sum(0)
+    scale = np.abs(g["dW_out"]).sum(0).max()
+    assert np.abs(col).max() < 2e-2 * scale
+
+
+def test_deterministic(cuda_lib):
+    cfg = CONFIGS["small"]
+    inp = make_inputs(cfg)
+    s = 1.0 / global_valid_tokens(cfg, cfg.B)
+    a, b = run_gpu(cfg, inp, s), run_gpu(cfg, inp, s)
+    assert a["loss"] == b["loss"]
+    for k in ("dH_dec", "dH_enc", "dW_c", "dW_out"):
+        np.testing.assert_array_equal(a[k], b[k])
