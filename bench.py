@@ -1,0 +1,371 @@
+"""Benchmark of the B200 attention-softmax stage (fwd + bwd), bench contract.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config paper]
+                  [--impl ours|reference] [--no-cpu-baseline]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL): each rank holds
+its own B = 128 sentences (weak scaling, BASELINE.json configs[2]) and the
+library allreduces dW_c / dW_out / loss over NVLink inside the call.
+
+Printed (rank 0, one JSON line): target tokens/s of the whole job (`value`,
+device-timed, inputs resident), `e2e` (the same metric through the C-ABI
+host-buffer entry point with the per-step H2D copies of the activations and
+the D2H read of the loss inside the timed region), `roofline` of the dominant
+kernel (the V-chunked vocab-backward tcgen05 GEMM launches) from CUDA events
+recorded by the library on the launching stream, `cpu_baseline` (the fp64
+oracle on a bounded sample of the same workload, host cores), clocks sampled
+during the timed region, and the launch count.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "attention-softmax fwd+bwd target tokens/sec at 1/2/4/8 B200; tensor-pipe % of peak"
+UNIT = "target tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="paper")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-sentences", type=int, default=0)
+    return ap.parse_args()
+
+
+def workload_desc(cfg, world):
+    return {"workload": f"{cfg.name}: per-GPU B={cfg.B} sentences, N={cfg.N} target / "
+                        f"M={cfg.M} source steps, d={cfg.d}, V={cfg.V}, {cfg.dtype}, "
+                        f"lengths={cfg.lengths}",
+            "B_per_gpu": cfg.B, "N": cfg.N, "M": cfg.M, "d": cfg.d, "V": cfg.V,
+            "global_batch": cfg.B * world, "parallelism": f"dp{world}",
+            "l2": "flushed between timed steps (256 MiB write outside the timed events)"}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm=d.get("hbm_gbs", 6443.5), bf16=d.get("bf16_tflops", 1678.0),
+                    bf16_sus=d.get("bf16_tflops_sustained", d.get("bf16_tflops", 1678.0)),
+                    src="measured (MEASURED_PEAKS.json)")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0,
+                src="fallback (B200_PROFILING.md)")
+
+
+# ------------------------------------------------------------ clocks ------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons, pw = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+                pw.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(pw) if pw else None}
+
+
+# ------------------------------------------------------------ reference ---
+_W_CACHE = {}
+
+
+def cpu_oracle_run(cfg, n_sent: int, seed_offset: int = 0):
+    """Time the fp64 oracle (as it stands) on n_sent sentences of the
+    workload with the full d and V.  Returns (valid tokens, seconds)."""
+    import numpy as np
+    from oracle import attn_softmax_oracle as O
+    from synthetic import make_inputs, make_weights
+    if cfg.name not in _W_CACHE:
+        _W_CACHE[cfg.name] = make_weights(cfg)
+    inp = make_inputs(cfg, sentences=range(seed_offset, seed_offset + n_sent),
+                      with_weights=False)
+    inp.update(_W_CACHE[cfg.name])
+    scale = 1.0 / max(1, int(inp["tgt_len"].sum()))
+    t0 = time.perf_counter()
+    O.fwd_bwd(inp["H_dec"], inp["H_enc"], inp["src_len"], inp["tgt_len"], inp["tgt_ids"],
+              inp["W_c"], inp["W_out"], scale)
+    dt = time.perf_counter() - t0
+    return int(np.sum(inp["tgt_len"])), dt
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"]
+        if n:
+            return int(max(n))
+    except Exception:
+        pass
+    return os.cpu_count()
+
+
+def cpu_baseline(cfg, target_s=12.0, fixed=0):
+    """Bounded sample: grow the sentence count until one run takes ~target_s."""
+    n = fixed or 2
+    tok, dt = cpu_oracle_run(cfg, n)
+    if not fixed:
+        while dt < target_s / 3 and n < cfg.B:
+            n = min(cfg.B, max(n + 1, int(n * target_s / max(dt, 1e-3) * 0.6)))
+            tok, dt = cpu_oracle_run(cfg, n)
+    return {"value": tok / dt, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+            "sample": f"{n} of {cfg.B} sentences of {cfg.name} (full d={cfg.d}, V={cfg.V}), "
+                      f"{tok} target tokens, one fwd+bwd in {dt:.2f} s, numpy fp64"}
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    # sized so the whole --steps K --warmup W run ends within minutes
+    per_step_target = max(1.0, 150.0 / max(1, args.steps + args.warmup))
+    n = 1
+    tok, dt = cpu_oracle_run(cfg, n)
+    n = max(1, min(cfg.B, int(per_step_target / max(dt, 1e-3))))
+    for i in range(args.warmup):
+        cpu_oracle_run(cfg, n, seed_offset=i)
+    total_tok, total_t = 0, 0.0
+    for i in range(args.steps):
+        tok, dt = cpu_oracle_run(cfg, n, seed_offset=i)
+        total_tok += tok
+        total_t += dt
+    v = total_tok / total_t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total_t / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_desc(cfg, world),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+                             "sample": f"{n} sentences per step of {cfg.name} (full d, V)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ ours --------
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    from synthetic import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1909_00562_b200 import binding, build
+    from paper_1909_00562_b200.stage import AttnSoftmaxStage, to_device
+    from synthetic import global_valid_tokens, make_inputs, shard_range
+
+    if rank == 0:
+        build.build()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
+        build.build()   # no-op unless stale; every rank loads the same .so
+    lib = binding.lib()
+
+    comm = None
+    if world > 1:
+        uid = [binding.attn_comm_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = binding.attn_comm_init(uid[0], world, rank, local)
+
+    # ---- inputs: this rank's sentences of the global batch (weak scaling)
+    B_global = cfg.B * world
+    lo, hi = shard_range(B_global, world, rank)
+    inp = make_inputs(cfg, sentences=range(lo, hi))
+    scale = 1.0 / global_valid_tokens(cfg, B_global)
+    tok_local = int(inp["tgt_len"].sum())
+    st = AttnSoftmaxStage(hi - lo, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype, device=dev)
+    dv = to_device(inp, cfg.dtype, device=dev)
+    out = st.alloc_outputs()
+    stream = torch.cuda.current_stream(dev)
+    call_args = (dv["H_dec"], dv["H_enc"], dv["src_len"], dv["tgt_len"], dv["tgt_ids"],
+                 dv["W_c"], dv["W_out"], scale)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        st(*call_args, out=out, comm=comm, stream=stream)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    launches_per_step = binding.attn_softmax_last_launches()
+
+    # ---- device-timed region: K steps, L2 flushed between steps
+    binding.attn_softmax_set_option("stage_events", 1)
+    clk = ClockSampler(local)
+    clk.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    stage_ms = {}
+    barrier()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+        for k, v in binding.attn_softmax_stage_times().items():
+            stage_ms[k] = stage_ms.get(k, 0.0) + v
+    barrier()
+    clocks = clk.stop()
+    binding.attn_softmax_set_option("stage_events", 0)
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    ntok = torch.tensor([tok_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ntok, op=dist.ReduceOp.SUM)
+    total_ms = float(t.item())
+    tok_job = float(ntok.item())
+    value = tok_job * args.steps / (total_ms / 1e3)
+    loss = float(out["loss"].item())
+
+    # ---- e2e: host-buffer entry point, H2D of activations + D2H of loss per step
+    pin = {k: dv[k].cpu().pin_memory() for k in ("H_dec", "H_enc", "tgt_ids")}
+    staging = torch.empty(binding.attn_softmax_host_staging_size(st.shape), dtype=torch.uint8,
+                          device=dev)
+    loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
+    h2d = sum(v.numel() * v.element_size() for v in pin.values())
+
+    def step_host():
+        binding.attn_softmax_fwd_bwd_host(
+            st.shape, pin["H_dec"], pin["H_enc"], dv["src_len"], dv["tgt_len"], pin["tgt_ids"],
+            dv["W_c"], dv["W_out"], scale, loss_host, out["dH_dec"], out["dH_enc"], out["dW_c"],
+            out["dW_out"], staging, st.workspace, comm=comm, stream=stream)
+        stream.synchronize()   # the loss is read on the host every step
+    for _ in range(2):
+        step_host()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step_host()
+    e1.record(stream)
+    barrier()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = tok_job * args.steps / (float(e2e_ms.item()) / 1e3)
+    assert abs(float(loss_host.item()) - loss) <= 1e-6 * max(1.0, abs(loss)), "e2e loss mismatch"
+
+    # ---- roofline of the dominant kernel: the vocab-backward tcgen05 GEMM
+    # launches (one per V-chunk + 1).  Algorithmic FLOPs per valid token:
+    # 4 d V (dW_out and dHc); the logit recompute (2 d V) is excluded.
+    pk = peaks()
+    T_valid = tok_local
+    vb_ms = stage_ms.get("vocab_bwd", 0.0) / args.steps
+    vb_flops = 4.0 * cfg.d * cfg.V * T_valid
+    vf_ms = stage_ms.get("vocab_fwd", 0.0) / args.steps
+    vf_flops = 2.0 * cfg.d * cfg.V * T_valid
+    achieved = vb_flops / (vb_ms / 1e3) / 1e12 if vb_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(cfg.name, {}).get("vocab_bwd_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_sus"],
+                "unit": "TFLOP/s", "frac": (achieved / pk["bf16_sus"]) if achieved else None,
+                "traffic": traffic,
+                "kernel": "gemm_tc_kernel vocab-backward launches (dlogits recompute + dW_out + dHc "
+                          "per V-chunk); achieved counts 4 d V useful FLOP per valid token",
+                "peak_source": pk["src"] + ", sustained bf16",
+                "vocab_fwd": {"achieved": vf_flops / (vf_ms / 1e3) / 1e12 if vf_ms > 0 else None,
+                              "peak": pk["bf16"], "unit": "TFLOP/s"},
+                "stage_ms": {k: v / args.steps for k, v in stage_ms.items()}}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
+            "data": "synthetic (seeded, DESIGN.md input recipe)",
+            "config": workload_desc(cfg, world),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": 4},
+            "roofline": roofline,
+            "gpu_launches": int(launches_per_step) * args.steps,
+            "clocks": clocks,
+            "loss": loss,
+            "useful_tflops": tok_job * (6 * cfg.d * cfg.V + 12 * cfg.d ** 2 + 12 * cfg.M * cfg.d)
+                             * args.steps / (total_ms / 1e3) / 1e12 / world}
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg, fixed=args.cpu_sample_sentences)
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        binding.attn_comm_destroy(comm)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -42,10 +42,22 @@ attn_status_t attn_debug_gemm_bf16(int M, int N, int K,
                                    const void* B, int b_mn,
                                    float* C, void* stream);
 
+/* Per-step timing of the last attn_softmax_fwd_bwd call on this process,
+ * recorded with CUDA events on the caller's stream when the "stage_events"
+ * option is 1.  Steps, in order: attn_fwd, proj_tanh, vocab_fwd, lse_reduce,
+ * vocab_bwd, proj_bwd, attn_bwd.  attn_softmax_stage_time synchronizes on the
+ * step's closing event. */
+int attn_softmax_stage_count(void);
+attn_status_t attn_softmax_stage_time(int i, const char** name, float* ms);
+
+/* Number of kernels the last attn_softmax_fwd_bwd call launched. */
+long long attn_softmax_last_launches(void);
+
 /* Tuning knobs (process-wide).  Keys:
  *   "vocab_chunk"   V-chunk width of the vocab backward (multiple of 256,
  *                   0 = automatic from the L2 size)
- *   "gemm_ctas"     persistent GEMM grid size (0 = number of SMs)          */
+ *   "gemm_ctas"     persistent GEMM grid size (0 = number of SMs)
+ *   "stage_events"  1 = record per-step CUDA events (see above)            */
 attn_status_t attn_softmax_set_option(const char* key, int64_t value);
 
 #ifdef __cplusplus

@@ -28,7 +28,8 @@ EXPORTS = [
     "attn_softmax_check_ids", "attn_grad_allreduce", "attn_comm_get_unique_id",
     "attn_comm_init", "attn_comm_destroy", "attn_last_error", "attn_version",
     "attn_softmax_workspace_views", "attn_debug_gemm_bf16",
-    "attn_softmax_set_option",
+    "attn_softmax_set_option", "attn_softmax_stage_count",
+    "attn_softmax_stage_time", "attn_softmax_last_launches",
 ]
 
 
@@ -101,6 +102,13 @@ def lib() -> ctypes.CDLL:
     L.attn_debug_gemm_bf16.restype = ctypes.c_int
     L.attn_softmax_set_option.argtypes = [ctypes.c_char_p, ctypes.c_int64]
     L.attn_softmax_set_option.restype = ctypes.c_int
+    L.attn_softmax_stage_count.argtypes = []
+    L.attn_softmax_stage_count.restype = ctypes.c_int
+    L.attn_softmax_stage_time.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_char_p),
+                                          ctypes.POINTER(ctypes.c_float)]
+    L.attn_softmax_stage_time.restype = ctypes.c_int
+    L.attn_softmax_last_launches.argtypes = []
+    L.attn_softmax_last_launches.restype = ctypes.c_longlong
     _lib = L
     return L
 
@@ -211,6 +219,21 @@ def attn_debug_gemm_bf16(M, N, K, A, a_mn, B, b_mn, C, stream=None):
 
 def attn_softmax_set_option(key: str, value: int):
     _check(lib().attn_softmax_set_option(key.encode(), int(value)))
+
+
+def attn_softmax_stage_times() -> dict:
+    """{step name: ms} of the last call (needs option stage_events = 1)."""
+    out = {}
+    for i in range(lib().attn_softmax_stage_count()):
+        name = ctypes.c_char_p()
+        ms = ctypes.c_float()
+        _check(lib().attn_softmax_stage_time(i, ctypes.byref(name), ctypes.byref(ms)))
+        out[name.value.decode()] = ms.value
+    return out
+
+
+def attn_softmax_last_launches() -> int:
+    return int(lib().attn_softmax_last_launches())
 
 
 def attn_last_error() -> str:

@@ -61,6 +61,45 @@ attn_status_t attn_set_error(attn_status_t code, const char* msg) {
 }
 extern "C" const char* attn_version(void) { return "attnsm 0.1 sm_100a"; }
 
+// ------------------------------------------------------------------ stage events / launch count
+// Debug surface (attn_softmax_debug.h): when "stage_events" is on, the stage
+// records a CUDA event on the caller's stream after each step so a harness
+// can time every step of the path on the launching stream.
+struct Prof {
+  bool on = false;
+  bool created = false;
+  int n = 0;
+  cudaEvent_t ev[32];
+  const char* name[32];
+};
+static Prof g_prof;
+static long long g_launches = 0;
+
+static void prof_mark(const char* name, cudaStream_t s) {
+  if (!g_prof.on) return;
+  if (!g_prof.created) {
+    for (int i = 0; i < 32; ++i) cudaEventCreate(&g_prof.ev[i]);
+    g_prof.created = true;
+  }
+  if (g_prof.n >= 32) return;
+  cudaEventRecord(g_prof.ev[g_prof.n], s);
+  g_prof.name[g_prof.n++] = name;
+}
+
+extern "C" int attn_softmax_stage_count(void) { return g_prof.n > 0 ? g_prof.n - 1 : 0; }
+
+extern "C" attn_status_t attn_softmax_stage_time(int i, const char** name, float* ms) {
+  if (i < 0 || i + 1 >= g_prof.n) return fail(ATTN_ERR_INVALID_ARG, "stage index %d out of range", i);
+  CUDA_TRY(cudaEventSynchronize(g_prof.ev[i + 1]));
+  float t = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&t, g_prof.ev[i], g_prof.ev[i + 1]));
+  if (name) *name = g_prof.name[i + 1];
+  if (ms) *ms = t;
+  return ATTN_OK;
+}
+
+extern "C" long long attn_softmax_last_launches(void) { return g_launches; }
+
 // ------------------------------------------------------------------ options
 static int64_t g_opt_vocab_chunk = 0;
 static int64_t g_opt_gemm_ctas = 0;
@@ -72,6 +111,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
       return fail(ATTN_ERR_INVALID_ARG, "vocab_chunk must be a non-negative multiple of 256 (got %lld)",
                   (long long)value);
     g_opt_vocab_chunk = value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "stage_events")) {
+    g_prof.on = value != 0;
     return ATTN_OK;
   }
   if (!strcmp(key, "gemm_ctas")) {
@@ -236,6 +279,7 @@ static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cu
   grid = std::min(grid, tiles);
   gemm_tc_kernel<OutT, true><<<grid, TC_THREADS, tc_smem_bytes(), stream>>>(P);
   CUDA_TRY(cudaGetLastError());
+  ++g_launches;
   return ATTN_OK;
 }
 
@@ -251,6 +295,7 @@ static attn_status_t launch_simt_group(const GemmDesc* gs, int n, cudaStream_t s
   if (tiles == 0) return ATTN_OK;
   gemm_simt_kernel<float><<<tiles, 256, 0, stream>>>(P);
   CUDA_TRY(cudaGetLastError());
+  ++g_launches;
   return ATTN_OK;
 }
 
@@ -358,6 +403,7 @@ static attn_status_t launch_bgemm(const BGemm<TA0, TB0, TA1, TB1, OutT>& g, cuda
   dim3 grid((g.N + SG_BN - 1) / SG_BN, (g.M + SG_BM - 1) / SG_BM, g.batch);
   bgemm_kernel<TA0, TB0, TA1, TB1, OutT><<<grid, 256, 0, stream>>>(g);
   CUDA_TRY(cudaGetLastError());
+  ++g_launches;
   return ATTN_OK;
 }
 
@@ -379,6 +425,7 @@ static attn_status_t attention_forward(const Plan& p, const T* H, const T* S, co
     const int rows = (int)p.T;
     softmax_fwd_kernel<<<(rows + 7) / 8, 256, 0, stream>>>(alpha, src_len, rows, p.N, p.M);
     CUDA_TRY(cudaGetLastError());
+    ++g_launches;
   }
   // F2: C_b = alpha_b S_b (Eq. 3)
   {
@@ -411,6 +458,7 @@ static attn_status_t attention_backward(const Plan& p, const T* H, const T* S, c
     const int rows = (int)p.T;
     softmax_bwd_kernel<<<(rows + 7) / 8, 256, 0, stream>>>(alpha, dalpha, rows, p.M);
     CUDA_TRY(cudaGetLastError());
+    ++g_launches;
   }
   // dH_dec_b = dH_part_b + de_b S_b
   {
@@ -526,9 +574,13 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   const int d = p.d, V = p.V;
   const long long TT = p.T;
   CUDA_TRY(cudaMemsetAsync(b.counters, 0, sizeof(unsigned int) * kNumCounters, stream));
+  g_prof.n = 0;
+  g_launches = 0;
+  prof_mark("start", stream);
 
   // ---- F1, F2 (Eqs. 1-3)
   if ((st = attention_forward<T>(p, H, S, b.src_len, b.alpha, (T*)b.ctx, stream)) != ATTN_OK) return st;
+  prof_mark("attn_fwd", stream);
 
   // ---- F3 (Eq. 4): H_c = tanh([H | C] W_c^T)
   {
@@ -539,6 +591,7 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
     g.epi.kind = EPI_TANH; g.epi.out = b.hc; g.epi.ldo = d; g.epi.ncols_valid = d; g.epi.ncols_store = d;
     if ((st = gemm(&g, 1)) != ATTN_OK) return st;
   }
+  prof_mark("proj_tanh", stream);
   // ---- F4 (Eq. 5): per-tile (max, sumexp) and target logit, logits discarded
   {
     GemmDesc g;
@@ -549,6 +602,7 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
     g.epi.part = b.part; g.epi.part_ld = p.ntn; g.epi.tgt_logit = b.tgt_logit; g.epi.tgt = tgt_ids;
     if ((st = gemm(&g, 1)) != ATTN_OK) return st;
   }
+  prof_mark("vocab_fwd", stream);
   // ---- Eq. 6: lse, token NLL, row scale, loss
   {
     const int blocks = (int)((TT + 7) / 8);
@@ -556,7 +610,9 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
                                                   loss_scale, b.lse, b.nll, b.rowscale, b.blockpart,
                                                   b.counters, loss);
     CUDA_TRY(cudaGetLastError());
+    ++g_launches;
   }
+  prof_mark("lse_reduce", stream);
   CommRun cr;
   if (comm) {
     if ((st = comm_begin(comm, stream, &cr)) != ATTN_OK) return st;
@@ -617,6 +673,7 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
       }
     }
   }
+  prof_mark("vocab_bwd", stream);
   // ---- B2: dW_c = dz^T [H | C];  [dH_part | dC] = dz W_c
   {
     GemmDesc gs[2];
@@ -637,9 +694,11 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
       if ((st = comm_enqueue_allreduce(comm, &cr, stream, dW_c, (size_t)d * 2 * d)) != ATTN_OK) return st;
     }
   }
+  prof_mark("proj_bwd", stream);
   // ---- B3: attention backward
   if ((st = attention_backward<T>(p, H, S, b.alpha, b.dalpha, b.dhc2, dH, dS, stream)) != ATTN_OK)
     return st;
+  prof_mark("attn_bwd", stream);
   if (comm) {
     if ((st = comm_enqueue_allreduce(comm, &cr, stream, loss, 1)) != ATTN_OK) return st;
     if ((st = comm_end(comm, &cr, stream)) != ATTN_OK) return st;
