@@ -161,24 +161,32 @@ static PFN_encodeTiled get_encode() {
   return fn;
 }
 
-// 2D bf16 tensor [outer, inner] with row stride ld (elements); box {64, box_outer}.
-static attn_status_t make_map(CUtensorMap* m, const void* ptr, long long inner, long long outer,
-                              long long ld, int box_outer) {
+// 2D tensor [outer, inner] with row stride ld (elements), 128-byte swizzle.
+static attn_status_t make_map_t(CUtensorMap* m, const void* ptr, bool f32, long long inner,
+                                long long outer, long long ld, int box_inner, int box_outer) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   if (inner < 1) inner = 1;
   if (outer < 1) outer = 1;
+  const int esz = f32 ? 4 : 2;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
-  cuuint32_t box[2] = {64, (cuuint32_t)box_outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * esz)};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
-                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
-    return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): ptr=%p inner=%lld outer=%lld ld=%lld",
-                (int)r, ptr, inner, outer, ld);
+    return fail(ATTN_ERR_CUDA,
+                "cuTensorMapEncodeTiled failed (%d): ptr=%p inner=%lld outer=%lld ld=%lld box=%dx%d",
+                (int)r, ptr, inner, outer, ld, box_inner, box_outer);
   return ATTN_OK;
+}
+// bf16 operand map, box {64, box_outer}
+static attn_status_t make_map(CUtensorMap* m, const void* ptr, long long inner, long long outer,
+                              long long ld, int box_outer) {
+  return make_map_t(m, ptr, false, inner, outer, ld, 64, box_outer);
 }
 
 // ------------------------------------------------------------------ GEMM descriptions
@@ -230,6 +238,16 @@ static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr
     if ((st = make_map(&maps[2], g.b0, n0, bk, g.ldb, 64)) != ATTN_OK) return st;
     if ((st = make_map(&maps[3], pr.b_nsplit ? g.b1 : g.b0, pr.b_nsplit ? g.N - pr.b_nsplit : n0,
                        bk, g.ldb, 64)) != ATTN_OK) return st;
+  }
+  // epilogue output: TMA store / reduce-add boxes of 32 rows x 128 bytes
+  if (g.epi.kind != EPI_LSE) {
+    const bool f32 = epi_out_is_f32(g.epi.kind);
+    if (pr.k_splits != 1) return fail(ATTN_ERR_UNSUPPORTED, "split-K is not used on the tcgen05 path");
+    if ((st = make_map_t(&maps[4], g.epi.out, f32, g.epi.ncols_store, g.M, g.epi.ldo, f32 ? 32 : 64,
+                         32)) != ATTN_OK)
+      return st;
+  } else {
+    maps[4] = maps[0];
   }
   return ATTN_OK;
 }
@@ -327,6 +345,7 @@ struct Plan {
   size_t elt;
   int tileN;          // column tile of the vocab GEMM engine
   int ntn;            // column tiles over V
+  int part_ld;        // LSE partial slots per row (tcgen05: 2 column halves per tile)
   int Vc;             // V-chunk width (multiple of 256)
   int nchunks;
   size_t off_lens, off_counters, off_blockpart, off_alpha, off_dalpha, off_ctx, off_hc, off_part,
@@ -343,6 +362,7 @@ static Plan make_plan(const attn_shape_t* s) {
   p.elt = p.bf16 ? 2 : 4;
   p.tileN = p.bf16 ? TC_BN : SG_BN;
   p.ntn = (p.V + p.tileN - 1) / p.tileN;
+  p.part_ld = p.bf16 ? 2 * p.ntn : p.ntn;
   const long long vpad = (p.V + 255) / 256 * 256;
   long long vc = g_opt_vocab_chunk;
   if (vc <= 0) {
@@ -364,7 +384,7 @@ static Plan make_plan(const attn_shape_t* s) {
   p.off_dalpha = take(sizeof(float) * p.T * p.M);
   p.off_ctx = take(p.elt * p.T * p.d);
   p.off_hc = take(p.elt * p.T * p.d);
-  p.off_part = take(sizeof(float2) * p.T * p.ntn);
+  p.off_part = take(sizeof(float2) * p.T * p.part_ld);
   p.off_tgtlogit = take(sizeof(float) * p.T);
   p.off_lse = take(sizeof(float) * p.T);
   p.off_nll = take(sizeof(float) * p.T);
@@ -599,14 +619,14 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
     g.a0 = b.hc; g.a_mn = 0; g.lda = d;
     g.b0 = W_out; g.b_mn = 0; g.ldb = d;
     g.epi.kind = EPI_LSE; g.epi.ncols_valid = V; g.epi.ncols_store = V; g.epi.col_base = 0;
-    g.epi.part = b.part; g.epi.part_ld = p.ntn; g.epi.tgt_logit = b.tgt_logit; g.epi.tgt = tgt_ids;
+    g.epi.part = b.part; g.epi.part_ld = p.part_ld; g.epi.tgt_logit = b.tgt_logit; g.epi.tgt = tgt_ids;
     if ((st = gemm(&g, 1)) != ATTN_OK) return st;
   }
   prof_mark("vocab_fwd", stream);
   // ---- Eq. 6: lse, token NLL, row scale, loss
   {
     const int blocks = (int)((TT + 7) / 8);
-    lse_reduce_kernel<<<blocks, 256, 0, stream>>>(b.part, p.ntn, b.tgt_logit, b.tgt_len, (int)TT, p.N,
+    lse_reduce_kernel<<<blocks, 256, 0, stream>>>(b.part, p.part_ld, b.tgt_logit, b.tgt_len, (int)TT, p.N,
                                                   loss_scale, b.lse, b.nll, b.rowscale, b.blockpart,
                                                   b.counters, loss);
     CUDA_TRY(cudaGetLastError());
@@ -649,9 +669,10 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
     g.M = (int)TT; g.N = d; g.K = vcc;
     g.a0 = b.dl[c & 1]; g.a_mn = 0; g.lda = p.Vc;
     g.b0 = W_out; g.b_mn = 1; g.ldb = d; g.b_koff = c0; g.b_kext = V;
-    g.epi.kind = EPI_DHC; g.epi.acc_f32 = b.dhc; g.epi.ldo = d; g.epi.hc = b.hc; g.epi.out = b.dz;
+    // dHc accumulates over the V-chunks: the first chunk stores, later ones
+    // add (TMA reduce-add on the tcgen05 path)
+    g.epi.kind = (c == 0) ? EPI_STORE_F32 : EPI_ACCUM_F32; g.epi.out = b.dhc; g.epi.ldo = d;
     g.epi.ncols_valid = d; g.epi.ncols_store = d;
-    g.epi.first = (c == 0); g.epi.last = (c == p.nchunks - 1);
     return g;
   };
   {
@@ -672,6 +693,14 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
           return st;
       }
     }
+  }
+  // tanh backward of Eq. 4: dz = dHc (1 - H_c^2)
+  {
+    const long long n = TT * d;
+    dz_kernel<T><<<(int)std::min<long long>((n + 255) / 256, 148ll * 16), 256, 0, stream>>>(
+        b.dhc, (const T*)b.hc, (T*)b.dz, n);
+    CUDA_TRY(cudaGetLastError());
+    ++g_launches;
   }
   prof_mark("vocab_bwd", stream);
   // ---- B2: dW_c = dz^T [H | C];  [dH_part | dC] = dz W_c

@@ -12,22 +12,27 @@
 //                  row's target id falls in the tile (Eqs. 5-6 forward)
 //   EPI_DLOGITS    out[r,c] = rowscale[r] * (exp(acc - lse[r]) - [c+col_base == y_r])
 //                  (softmax - onehot; backward of Eqs. 5-6)
-//   EPI_DHC        dHc += acc over V-chunks; on the last chunk
-//                  dz = dHc * (1 - Hc^2)  (tanh backward of Eq. 4)
+//   EPI_ACCUM_F32  out[r,c] += acc                   (dHc over V-chunks; the tcgen05
+//                  engine does it with a TMA reduce-add, no loads)
 #pragma once
 #include <cstdint>
 #include <cuda_bf16.h>
 
 namespace attnsm {
 
-enum EpiKind : int { EPI_STORE_F32 = 0, EPI_TANH = 1, EPI_LSE = 2, EPI_DLOGITS = 3, EPI_DHC = 4 };
+enum EpiKind : int { EPI_STORE_F32 = 0, EPI_TANH = 1, EPI_LSE = 2, EPI_DLOGITS = 3, EPI_ACCUM_F32 = 4 };
+
+// Output element type of each kind (tcgen05 path: bf16 activations).
+__host__ __device__ constexpr bool epi_out_is_f32(int kind) {
+  return kind == EPI_STORE_F32 || kind == EPI_ACCUM_F32;
+}
 
 struct EpiParams {
   int kind;
   int ncols_valid;       // columns < ncols_valid are real (V tail, chunk tail)
   int ncols_store;       // columns < ncols_store may be written (row capacity)
   int col_base;          // global column of problem column 0 (V-chunk start)
-  void* out;             // STORE_F32: float; TANH/DLOGITS: OutT; DHC: OutT (dz)
+  void* out;             // STORE_F32 / ACCUM_F32: float; TANH / DLOGITS: OutT
   long long ldo;         // row stride of out (elements)
   long long split_stride;// element offset between split-K partial outputs
   float2* part;          // LSE: [rows, part_ld] (max, sumexp)
@@ -36,9 +41,6 @@ struct EpiParams {
   const int* tgt;        // LSE/DLOGITS: [rows] target ids
   const float* lse;      // DLOGITS: [rows]
   const float* rowscale; // DLOGITS: [rows] loss_scale on valid rows, 0 on padded
-  float* acc_f32;        // DHC: running dHc [rows, ldo] fp32
-  const void* hc;        // DHC: H_c [rows, ldo] OutT
-  int first, last;       // DHC: first / last V-chunk
 };
 
 template <typename T> __device__ __forceinline__ T to_out(float x);
@@ -173,44 +175,35 @@ struct RowEpilogue {
       float* rowp = reinterpret_cast<float*>(p.out) + (long long)split * p.split_stride +
                     (long long)row * p.ldo;
       store_row32<float>(rowp, col0, p.ncols_store, v, (p.ldo * 4) % 16 == 0);
-    } else if (kind == EPI_DHC) {
+    } else if (kind == EPI_ACCUM_F32) {
       if (col0 >= p.ncols_store) return;
-      float* accp = p.acc_f32 + (long long)row * p.ldo;
-      const bool vec = (p.ldo * 4) % 16 == 0 && col0 + 32 <= p.ncols_store;
-      if (!p.first) {
-        if (vec) {
+      float* rowp = reinterpret_cast<float*>(p.out) + (long long)row * p.ldo;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            float4 a = reinterpret_cast<const float4*>(accp + col0)[q];
-            v[4 * q] += a.x;
-            v[4 * q + 1] += a.y;
-            v[4 * q + 2] += a.z;
-            v[4 * q + 3] += a.w;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (col0 + j < p.ncols_store) v[j] += accp[col0 + j];
-        }
-      }
-      if (!p.last) {
-        store_row32<float>(accp, col0, p.ncols_store, v, (p.ldo * 4) % 16 == 0);
-      } else {
-        const OutT* hcp = reinterpret_cast<const OutT*>(p.hc) + (long long)row * p.ldo;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float h = (col0 + j < p.ncols_store) ? to_f32(hcp[col0 + j]) : 0.f;
-          v[j] = v[j] * (1.f - h * h);
-        }
-        OutT* dzp = reinterpret_cast<OutT*>(p.out) + (long long)row * p.ldo;
-        store_row32<OutT>(dzp, col0, p.ncols_store, v, (p.ldo * sizeof(OutT)) % 16 == 0);
-      }
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < p.ncols_store) rowp[col0 + j] += v[j];
     }
   }
 
-  __device__ __forceinline__ void finish(int tile_n) {
+  // tcgen05 path: transform v in place (TANH, DLOGITS) or update the LSE
+  // state; the engine stages and stores the result with TMA.
+  __device__ __forceinline__ void transform(int col0, float (&v)[32]) {
+    const int kind = p.kind;
+    if (kind == EPI_LSE) {
+      chunk(col0, v);
+    } else if (kind == EPI_DLOGITS) {
+      const int yl = y - col0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        v[j] = rs * (exp_f<kFast>(v[j] - lse) - (j == yl ? 1.f : 0.f));
+    } else if (kind == EPI_TANH) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = tanh_f<kFast>(v[j]);
+    }
+  }
+
+  __device__ __forceinline__ void finish(int slot) {
     if (p.kind == EPI_LSE) {
-      p.part[(long long)row * p.part_ld + tile_n] = make_float2(st.m, st.s);
+      p.part[(long long)row * p.part_ld + slot] = make_float2(st.m, st.s);
       if (st.has_t) p.tgt_logit[row] = st.t;
     }
   }

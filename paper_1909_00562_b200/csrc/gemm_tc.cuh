@@ -8,11 +8,14 @@
 //   chunk c+1 dlogits GEMM); CTAs pull tiles from a global atomic counter so
 //   long-K and short-K tiles balance across the 148 SMs.
 //
-// Roles (256 threads, one CTA per SM):
-//   warp 0      tile scheduler + TMA producer (one elected lane)
-//   warp 1      MMA issuer (one lane issues tcgen05.mma for the whole CTA)
-//   warp 2      TMEM allocator (512 columns = two 128x256 fp32 accumulators)
-//   warps 4..7  epilogue: warp w reads TMEM lanes 32*(w%4)..+31 = tile rows
+// Roles (384 threads, one CTA per SM):
+//   warp 0       tile scheduler + TMA producer (one elected lane)
+//   warp 1       MMA issuer (one lane issues tcgen05.mma for the whole CTA)
+//   warp 2       TMEM allocator (512 columns = two 128x256 fp32 accumulators)
+//   warps 4..11  epilogue: warp w reads TMEM lanes 32*(w%4)..+31 (tile rows)
+//                and column half (w-4)/4; results are staged in shared
+//                memory (128-byte swizzle, conflict-free) and written with
+//                TMA bulk stores, or TMA reduce-adds for accumulation.
 //
 // Operands may be K-major (row-major [rows, K]) or MN-major (row-major
 // [K, rows]); see DESIGN.md "tcgen05 encodings" for the descriptor fields.
@@ -26,12 +29,15 @@ constexpr int TC_BM = 128;
 constexpr int TC_BN = 256;
 constexpr int TC_BK = 64;
 constexpr int TC_STAGES = 4;
-constexpr int TC_THREADS = 256;
+constexpr int TC_THREADS = 384;
+constexpr int TC_EPI_WARPS = 8;
+constexpr int TC_STG_BYTES = 4096;                        // per epilogue warp
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;             // 16 KB
 constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;             // 32 KB
 constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;   // 48 KB
 constexpr int TC_SCHED = 4;
-constexpr int TC_SMEM_BYTES = TC_STAGES * TC_STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+constexpr int TC_SMEM_BYTES =
+    TC_STAGES * TC_STAGE_BYTES + TC_EPI_WARPS * TC_STG_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 constexpr int kMaxProblems = 4;
 
 struct TcProblem {
@@ -46,7 +52,7 @@ struct TcProblem {
 };
 
 struct alignas(64) TcParams {
-  CUtensorMap maps[kMaxProblems][4];  // a0, a1, b0, b1
+  CUtensorMap maps[kMaxProblems][5];  // a0, a1, b0, b1, out
   TcProblem prob[kMaxProblems];
   int nprob;
   int total_tiles;
@@ -87,7 +93,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE_BYTES);
+  uint8_t* staging = smem + TC_STAGES * TC_STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + TC_EPI_WARPS * TC_STG_BYTES);
   uint64_t* full = bars;                       // [STAGES]
   uint64_t* empty = full + TC_STAGES;          // [STAGES]
   uint64_t* tfull = empty + TC_STAGES;         // [2]
@@ -107,15 +114,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], TC_EPI_WARPS);
     }
     for (int i = 0; i < TC_SCHED; ++i) {
       mbar_init(&sfull[i], 1);
-      mbar_init(&sempty[i], 1 + 4);
+      mbar_init(&sempty[i], 1 + TC_EPI_WARPS);
     }
     fence_barrier_init();
     for (int p = 0; p < P.nprob; ++p)
-      for (int j = 0; j < 4; ++j) tma_prefetch_desc(&P.maps[p][j]);
+      for (int j = 0; j < 5; ++j) tma_prefetch_desc(&P.maps[p][j]);
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
@@ -221,8 +228,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue
-    const uint32_t q = warp & 3;
+    // ---------------- epilogue (8 warps)
+    const uint32_t ew = warp - 4;
+    const uint32_t q = warp & 3;        // TMEM lane quarter = tile rows 32q..32q+31
+    const uint32_t h = ew >> 2;         // column half of the 256-wide tile
+    const uint32_t stg = smem_u32(staging + ew * TC_STG_BYTES);
+    const uint32_t swz = lane & 7;
     int r = 0;
     uint32_t rph = 0;
     int acc = 0;
@@ -236,27 +247,77 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       if (t < 0) break;
       const TcTile tl = tc_decode(P, t);
       const TcProblem& pr = P.prob[tl.p];
+      const int kind = pr.epi.kind;
+      const CUtensorMap* omap = &P.maps[tl.p][4];
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int row = tl.m0 + q * 32 + lane;
+      const int row0 = tl.m0 + q * 32;
+      const int row = row0 + lane;
       const bool row_ok = row < pr.M;
-      const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * TC_BN;
+      const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * TC_BN + h * 128;
       RowEpilogue<OutT, kFast> epi(pr.epi, row_ok ? row : 0, tl.split);
-      const int ncol_chunks = min(TC_BN, pr.N - tl.n0 + 31) / 32;
+      const int col_h = tl.n0 + h * 128;
+      const int lim = (kind == EPI_LSE) ? pr.epi.ncols_valid : pr.epi.ncols_store;
+      const int n_act = max(0, min(4, (lim - col_h + 31) / 32));   // warp-uniform
+      const bool f32out = epi_out_is_f32(kind);
 #pragma unroll 1
-      for (int c = 0; c < TC_BN / 32; ++c) {
+      for (int c = 0; c < n_act; ++c) {
         float v[32];
-        if (c < ncol_chunks) {   // warp-uniform
-          tmem_ld32(taddr + c * 32, v);
-          if (row_ok) epi.chunk(tl.n0 + c * 32, v);
+        tmem_ld32(taddr + c * 32, v);
+        const int col = col_h + c * 32;
+        if (kind == EPI_LSE) {
+          if (row_ok) epi.chunk(col, v);
+          continue;
+        }
+        epi.transform(col, v);
+        if (f32out) {
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            st_shared_v4(stg + lane * 128 + ((g ^ swz) << 4), __float_as_uint(v[4 * g]),
+                         __float_as_uint(v[4 * g + 1]), __float_as_uint(v[4 * g + 2]),
+                         __float_as_uint(v[4 * g + 3]));
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (kind == EPI_ACCUM_F32) tma_reduce_add_2d(omap, staging + ew * TC_STG_BYTES, col, row0);
+            else tma_store_2d(omap, staging + ew * TC_STG_BYTES, col, row0);
+            bulk_commit();
+          }
+        } else {
+          if ((c & 1) == 0) {
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * g + 2 * e], v[8 * g + 2 * e + 1]);
+              w[e] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            const uint32_t gi = (c & 1) * 4 + g;
+            st_shared_v4(stg + lane * 128 + ((gi ^ swz) << 4), w[0], w[1], w[2], w[3]);
+          }
+          if ((c & 1) == 1 || c == n_act - 1) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(omap, staging + ew * TC_STG_BYTES, col_h + (c & ~1) * 32, row0);
+              bulk_commit();
+            }
+          }
         }
       }
-      if (row_ok) epi.finish(tl.tn);
+      if (kind == EPI_LSE && row_ok) epi.finish(tl.tn * 2 + h);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
+    if (lane == 0) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();

@@ -13,6 +13,8 @@
 #pragma once
 #include <cstdint>
 
+#include "epilogue.cuh"
+
 namespace attnsm {
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -123,6 +125,20 @@ __global__ void __launch_bounds__(256) lse_reduce_kernel(
         *done_counter = 0u;
       }
     }
+  }
+}
+
+// Backward of Eq. 4's tanh: dz = dHc * (1 - H_c^2), written in the
+// activation dtype (the operand of the W_c backward GEMMs).
+template <typename T>
+__global__ void __launch_bounds__(256) dz_kernel(const float* __restrict__ dhc,
+                                                 const T* __restrict__ hc, T* __restrict__ dz,
+                                                 long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = i; k < n; k += stride) {
+    const float h = to_f32(hc[k]);
+    dz[k] = to_out<T>(dhc[k] * (1.f - h * h));
   }
 }
 
