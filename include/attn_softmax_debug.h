@@ -57,7 +57,9 @@ long long attn_softmax_last_launches(void);
  *   "vocab_chunk"   V-chunk width of the vocab backward (multiple of 256,
  *                   0 = automatic from the L2 size)
  *   "gemm_ctas"     persistent GEMM grid size (0 = number of SMs)
- *   "stage_events"  1 = record per-step CUDA events (see above)            */
+ *   "stage_events"  1 = record per-step CUDA events (see above)
+ *   "debug_epilogue" attn_debug_gemm_bf16 epilogue: 0 = fp32 TMA store,
+ *                   1 = read the accumulator only (mainloop timing)         */
 attn_status_t attn_softmax_set_option(const char* key, int64_t value);
 
 #ifdef __cplusplus

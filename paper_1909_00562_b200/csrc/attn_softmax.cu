@@ -101,6 +101,8 @@ extern "C" attn_status_t attn_softmax_stage_time(int i, const char** name, float
 extern "C" long long attn_softmax_last_launches(void) { return g_launches; }
 
 // ------------------------------------------------------------------ options
+// debug_epilogue option: 0 = fp32 TMA store, 1 = accumulator read only (no store)
+static int g_debug_epi = 0;
 static int64_t g_opt_vocab_chunk = 0;
 static int64_t g_opt_gemm_ctas = 0;
 
@@ -111,6 +113,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
       return fail(ATTN_ERR_INVALID_ARG, "vocab_chunk must be a non-negative multiple of 256 (got %lld)",
                   (long long)value);
     g_opt_vocab_chunk = value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "debug_epilogue")) {
+    g_debug_epi = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "stage_events")) {
@@ -240,7 +246,7 @@ static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr
                        bk, g.ldb, 64)) != ATTN_OK) return st;
   }
   // epilogue output: TMA store / reduce-add boxes of 32 rows x 128 bytes
-  if (g.epi.kind != EPI_LSE) {
+  if (g.epi.kind != EPI_LSE && g.epi.kind != EPI_NONE) {
     const bool f32 = epi_out_is_f32(g.epi.kind);
     if (pr.k_splits != 1) return fail(ATTN_ERR_UNSUPPORTED, "split-K is not used on the tcgen05 path");
     if ((st = make_map_t(&maps[4], g.epi.out, f32, g.epi.ncols_store, g.M, g.epi.ldo, f32 ? 32 : 64,
@@ -838,6 +844,7 @@ extern "C" attn_status_t attn_debug_gemm_bf16(int M, int N, int K, const void* A
   g.a0 = A; g.a_mn = a_mn; g.lda = a_mn ? M : K;
   g.b0 = B; g.b_mn = b_mn; g.ldb = b_mn ? N : K;
   g.epi.kind = EPI_STORE_F32; g.epi.out = C; g.epi.ldo = N; g.epi.ncols_valid = N; g.epi.ncols_store = N;
+  if (g_debug_epi == 1) g.epi.kind = EPI_NONE;
   int* counter = nullptr;
   cudaStream_t stream = (cudaStream_t)stream_;
   CUDA_TRY(cudaMallocAsync(&counter, sizeof(int), stream));

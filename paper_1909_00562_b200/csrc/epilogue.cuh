@@ -20,7 +20,10 @@
 
 namespace attnsm {
 
-enum EpiKind : int { EPI_STORE_F32 = 0, EPI_TANH = 1, EPI_LSE = 2, EPI_DLOGITS = 3, EPI_ACCUM_F32 = 4 };
+enum EpiKind : int {
+  EPI_STORE_F32 = 0, EPI_TANH = 1, EPI_LSE = 2, EPI_DLOGITS = 3, EPI_ACCUM_F32 = 4,
+  EPI_NONE = 5   // debug: read the accumulator, store nothing
+};
 
 // Output element type of each kind (tcgen05 path: bf16 activations).
 __host__ __device__ constexpr bool epi_out_is_f32(int kind) {

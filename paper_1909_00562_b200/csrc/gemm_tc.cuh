@@ -137,9 +137,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       uint32_t ph = 0;
       int r = 0;
       uint32_t rph = 0;
+      // the next tile index is fetched one tile ahead so the global atomic's
+      // latency overlaps the current tile's loads
+      int t_next = atomicAdd(P.tile_counter, 1);
       for (;;) {
-        int t = atomicAdd(P.tile_counter, 1);
+        int t = t_next;
         if (t >= P.total_tiles) t = -1;
+        else t_next = atomicAdd(P.tile_counter, 1);
         mbar_wait(&sempty[r], rph ^ 1);
         sched_tile[r] = t;
         mbar_arrive(&sfull[r]);
@@ -269,6 +273,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           if (row_ok) epi.chunk(col, v);
           continue;
         }
+        if (kind == EPI_NONE) continue;
         epi.transform(col, v);
         if (f32out) {
           if (lane == 0) bulk_wait_read0();

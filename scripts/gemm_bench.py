@@ -15,7 +15,10 @@ shapes = [  # name, M, N, K, a_mn, b_mn
     ("square 8192", 8192, 8192, 8192, 0, 0),
     ("square 8192 MN/MN", 8192, 8192, 8192, 1, 1),
 ]
-for name, M, N, K, amn, bmn in shapes:
+import itertools
+for (name, M, N, K, amn, bmn), epi in itertools.product(shapes, (0, 1)):
+    binding.attn_softmax_set_option("debug_epilogue", epi)
+    name = name + (" [no store]" if epi else "")
     A = torch.randn(K, M, device="cuda").bfloat16() if amn else torch.randn(M, K, device="cuda").bfloat16()
     B = torch.randn(K, N, device="cuda").bfloat16() if bmn else torch.randn(N, K, device="cuda").bfloat16()
     C = torch.empty(M, N, device="cuda")
