@@ -845,11 +845,12 @@ extern "C" attn_status_t attn_debug_gemm_bf16(int M, int N, int K, const void* A
   g.b0 = B; g.b_mn = b_mn; g.ldb = b_mn ? N : K;
   g.epi.kind = EPI_STORE_F32; g.epi.out = C; g.epi.ldo = N; g.epi.ncols_valid = N; g.epi.ncols_store = N;
   if (g_debug_epi == 1) g.epi.kind = EPI_NONE;
-  int* counter = nullptr;
+  // one persistent device counter per process (debug entry only); the memset
+  // is stream-ordered so the call can be captured in a CUDA graph
+  static int* counter = nullptr;
+  if (!counter) CUDA_TRY(cudaMalloc(&counter, sizeof(int)));
   cudaStream_t stream = (cudaStream_t)stream_;
-  CUDA_TRY(cudaMallocAsync(&counter, sizeof(int), stream));
   CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int), stream));
   attn_status_t st = launch_tc_group<__nv_bfloat16>(&g, 1, counter, stream);
-  CUDA_TRY(cudaFreeAsync(counter, stream));
   return st;
 }
