@@ -58,6 +58,8 @@ long long attn_softmax_last_launches(void);
  *                   0 = automatic from the L2 size)
  *   "gemm_ctas"     persistent GEMM grid size (0 = number of SMs)
  *   "stage_events"  1 = record per-step CUDA events (see above)
+ *   "mn_3d_tma"     1 (default) = load MN-major operand tiles with one 3D TMA
+ *                   box per stage; 0 = one 2D box per 64-wide atom
  *   "debug_epilogue" attn_debug_gemm_bf16 epilogue: 0 = fp32 TMA store,
  *                   1 = read the accumulator only (mainloop timing)         */
 attn_status_t attn_softmax_set_option(const char* key, int64_t value);

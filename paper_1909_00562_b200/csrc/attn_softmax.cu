@@ -103,6 +103,7 @@ extern "C" long long attn_softmax_last_launches(void) { return g_launches; }
 // ------------------------------------------------------------------ options
 // debug_epilogue option: 0 = fp32 TMA store, 1 = accumulator read only (no store)
 static int g_debug_epi = 0;
+static int g_opt_mn3d = 1;  // MN-major operands via one 3D TMA box
 static int64_t g_opt_vocab_chunk = 0;
 static int64_t g_opt_gemm_ctas = 0;
 
@@ -113,6 +114,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
       return fail(ATTN_ERR_INVALID_ARG, "vocab_chunk must be a non-negative multiple of 256 (got %lld)",
                   (long long)value);
     g_opt_vocab_chunk = value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "mn_3d_tma")) {
+    g_opt_mn3d = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "debug_epilogue")) {
@@ -189,6 +194,27 @@ static attn_status_t make_map_t(CUtensorMap* m, const void* ptr, bool f32, long 
                 (int)r, ptr, inner, outer, ld, box_inner, box_outer);
   return ATTN_OK;
 }
+// MN-major bf16 operand [K rows, MN cols] (row stride ld) as a 3D tensor
+// {64 (MN within an atom), K, MN/64 (atom)} with strides {ld*2, 128 B}; one
+// box {64, 64, atoms} lands in shared memory as `atoms` consecutive 8 KB
+// K x 64 blocks -- the canonical MN-major SW128 layout with LBO = 8 KB.
+static attn_status_t make_map_mn3d(CUtensorMap* m, const void* ptr, long long mn, long long k,
+                                   long long ld, int atoms) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {64, (cuuint64_t)std::max(1ll, k), (cuuint64_t)std::max(1ll, mn / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), 128};
+  cuuint32_t box[3] = {64, 64, (cuuint32_t)atoms};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled (3D MN-major) failed (%d): mn=%lld k=%lld ld=%lld",
+                (int)r, mn, k, ld);
+  return ATTN_OK;
+}
+
 // bf16 operand map, box {64, box_outer}
 static attn_status_t make_map(CUtensorMap* m, const void* ptr, long long inner, long long outer,
                               long long ld, int box_outer) {
@@ -232,6 +258,10 @@ static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr
     if ((st = make_map(&maps[0], g.a0, k0, g.M, g.lda, TC_BM)) != ATTN_OK) return st;
     if ((st = make_map(&maps[1], pr.a_ksplit ? g.a1 : g.a0, pr.a_ksplit ? g.K - pr.a_ksplit : k0,
                        g.M, g.lda, TC_BM)) != ATTN_OK) return st;
+  } else if (g_opt_mn3d && g.M % 64 == 0) {
+    pr.a_3d = 1;
+    if ((st = make_map_mn3d(&maps[0], g.a0, g.M, g.K, g.lda, TC_BM / 64)) != ATTN_OK) return st;
+    maps[1] = maps[0];
   } else {
     if ((st = make_map(&maps[0], g.a0, g.M, g.K, g.lda, 64)) != ATTN_OK) return st;
     maps[1] = maps[0];
@@ -241,9 +271,19 @@ static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr
     maps[3] = maps[2];
   } else {
     const long long n0 = pr.b_nsplit ? pr.b_nsplit : g.N;
-    if ((st = make_map(&maps[2], g.b0, n0, bk, g.ldb, 64)) != ATTN_OK) return st;
-    if ((st = make_map(&maps[3], pr.b_nsplit ? g.b1 : g.b0, pr.b_nsplit ? g.N - pr.b_nsplit : n0,
-                       bk, g.ldb, 64)) != ATTN_OK) return st;
+    const long long n1 = pr.b_nsplit ? g.N - pr.b_nsplit : n0;
+    // a split point must not fall inside a tile; atoms past the extent are
+    // zero-filled by TMA, so only whole 64-column atoms are required
+    const bool ok3d = pr.b_nsplit ? (n0 % TC_BN == 0 && n1 % 64 == 0) : (n0 % 64 == 0);
+    if (g_opt_mn3d && ok3d) {
+      pr.b_3d = 1;
+      if ((st = make_map_mn3d(&maps[2], g.b0, n0, bk, g.ldb, TC_BN / 64)) != ATTN_OK) return st;
+      if ((st = make_map_mn3d(&maps[3], pr.b_nsplit ? g.b1 : g.b0, n1, bk, g.ldb, TC_BN / 64)) != ATTN_OK)
+        return st;
+    } else {
+      if ((st = make_map(&maps[2], g.b0, n0, bk, g.ldb, 64)) != ATTN_OK) return st;
+      if ((st = make_map(&maps[3], pr.b_nsplit ? g.b1 : g.b0, n1, bk, g.ldb, 64)) != ATTN_OK) return st;
+    }
   }
   // epilogue output: TMA store / reduce-add boxes of 32 rows x 128 bytes
   if (g.epi.kind != EPI_LSE && g.epi.kind != EPI_NONE) {

@@ -45,6 +45,7 @@ struct TcProblem {
   int tiles_m, tiles_n, k_splits, kb_per_split, kb_total;
   int tile_begin;
   int a_mn, b_mn;
+  int a_3d, b_3d;   // MN-major operand loaded as ONE 3D box {64, 64, rows/64} (atoms as dim 2)
   int a_ksplit;   // K-major A: k < a_ksplit -> map a0 else a1 (at k - a_ksplit); 0 = none
   int b_nsplit;   // MN-major B: n < b_nsplit -> map b0 else b1 (at n - b_nsplit); 0 = none
   int b_koff;     // added to B's K coordinate
@@ -166,6 +167,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
               tma_load_2d(sA, ma1, &full[s], k0 - pr.a_ksplit, tl.m0);
             else
               tma_load_2d(sA, ma0, &full[s], k0, tl.m0);
+          } else if (pr.a_3d) {
+            tma_load_3d(sA, ma0, &full[s], 0, k0, tl.m0 / 64);
           } else {
 #pragma unroll
             for (int i = 0; i < TC_BM / 64; ++i)
@@ -174,6 +177,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           const int kb_ = k0 + pr.b_koff;
           if (!pr.b_mn) {
             tma_load_2d(sB, mb0, &full[s], kb_, tl.n0);
+          } else if (pr.b_3d) {
+            if (pr.b_nsplit > 0 && tl.n0 >= pr.b_nsplit)
+              tma_load_3d(sB, mb1, &full[s], 0, kb_, (tl.n0 - pr.b_nsplit) / 64);
+            else
+              tma_load_3d(sB, mb0, &full[s], 0, kb_, tl.n0 / 64);
           } else {
 #pragma unroll
             for (int i = 0; i < TC_BN / 64; ++i) {

@@ -47,11 +47,15 @@ def oracle(inp, scale):
 
 
 # ------------------------------------------------------------ GEMM core ----
+@pytest.mark.parametrize("mn3d", [0, 1])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 0), (0, 1), (1, 1)])
-@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (296, 520, 200), (1000, 264, 1536)])
-def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K):
-    """The tcgen05 engine alone, all operand majors, with M/N/K tails."""
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (296, 520, 200), (1000, 264, 1536),
+                                   (320, 640, 192)])
+def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d):
+    """The tcgen05 engine alone, all operand majors (MN-major via 2D atom
+    boxes or one 3D box), with M/N/K tails."""
     from paper_1909_00562_b200 import binding
+    binding.attn_softmax_set_option("mn_3d_tma", mn3d)
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N + K)
     A = torch.randn(M, K, generator=g).bfloat16()
     B = torch.randn(N, K, generator=g).bfloat16()
@@ -61,6 +65,7 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K):
     C = torch.full((M, N), float("nan"), device="cuda")
     binding.attn_debug_gemm_bf16(M, N, K, Ad, a_mn, Bd, b_mn, C)
     torch.cuda.synchronize()
+    binding.attn_softmax_set_option("mn_3d_tma", 1)
     err = (C.double().cpu() - ref).abs().max().item()
     assert err < 1e-3 * max(1.0, ref.abs().max().item()), err
 
