@@ -172,147 +172,160 @@ static PFN_encodeTiled get_encode() {
   return fn;
 }
 
-// 2D tensor [outer, inner] with row stride ld (elements), 128-byte swizzle.
-static attn_status_t make_map_t(CUtensorMap* m, const void* ptr, bool f32, long long inner,
-                                long long outer, long long ld, int box_inner, int box_outer) {
+// rank-r tensor map, 128-byte swizzle, zero fill out of bounds.
+static attn_status_t encode(CUtensorMap* m, const void* ptr, bool f32, int rank,
+                            const cuuint64_t* dims, const cuuint64_t* strides_bytes,
+                            const cuuint32_t* box) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  if (inner < 1) inner = 1;
-  if (outer < 1) outer = 1;
-  const int esz = f32 ? 4 : 2;
-  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * esz)};
-  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                   const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS)
-    return fail(ATTN_ERR_CUDA,
-                "cuTensorMapEncodeTiled failed (%d): ptr=%p inner=%lld outer=%lld ld=%lld box=%dx%d",
-                (int)r, ptr, inner, outer, ld, box_inner, box_outer);
-  return ATTN_OK;
-}
-// MN-major bf16 operand [K rows, MN cols] (row stride ld) as a 3D tensor
-// {64 (MN within an atom), K, MN/64 (atom)} with strides {ld*2, 128 B}; one
-// box {64, 64, atoms} lands in shared memory as `atoms` consecutive 8 KB
-// K x 64 blocks -- the canonical MN-major SW128 layout with LBO = 8 KB.
-static attn_status_t make_map_mn3d(CUtensorMap* m, const void* ptr, long long mn, long long k,
-                                   long long ld, int atoms) {
-  PFN_encodeTiled enc = get_encode();
-  if (!enc) return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {64, (cuuint64_t)std::max(1ll, k), (cuuint64_t)std::max(1ll, mn / 64)};
-  cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), 128};
-  cuuint32_t box[3] = {64, 64, (cuuint32_t)atoms};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
-                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
+                   const_cast<void*>(ptr), dims, strides_bytes, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
-    return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled (3D MN-major) failed (%d): mn=%lld k=%lld ld=%lld",
-                (int)r, mn, k, ld);
+    return fail(ATTN_ERR_CUDA,
+                "cuTensorMapEncodeTiled failed (%d): rank %d ptr=%p dims=[%llu,%llu,%llu,%llu]",
+                (int)r, rank, ptr, (unsigned long long)dims[0],
+                (unsigned long long)(rank > 1 ? dims[1] : 0), (unsigned long long)(rank > 2 ? dims[2] : 0),
+                (unsigned long long)(rank > 3 ? dims[3] : 0));
   return ATTN_OK;
-}
-
-// bf16 operand map, box {64, box_outer}
-static attn_status_t make_map(CUtensorMap* m, const void* ptr, long long inner, long long outer,
-                              long long ld, int box_outer) {
-  return make_map_t(m, ptr, false, inner, outer, ld, 64, box_outer);
 }
 
 // ------------------------------------------------------------------ GEMM descriptions
-// C[M,N] = A[M,K] B[N,K]^T.  A: a_mn=0 -> [M,K] (ld lda), a_mn=1 -> [K,M].
-// K-major A may be split along K at a_ksplit between a0 / a1 (same ld).
-// B: b_mn=0 -> [N,K] (ld ldb), b_mn=1 -> [K,N]; MN-major B may be split along
-// N at b_nsplit between b0 / b1; b_koff shifts B's K coordinate; b_kext is the
-// K extent of the B tensor (defaults to K + b_koff).
+// C[M,N] = A[M,K] B[N,K]^T per batch item.  A K-major operand is [rows, K]
+// (row stride ld), an MN-major one [K, cols]; batch items are bstride
+// elements apart.  k_ext is the operand's K extent (TMA zero-fills beyond
+// it); mn_ext its M / N extent (rows for K-major, columns for MN-major).
+struct Operand {
+  const void* p = nullptr;
+  long long ld = 0, bstride = 0, k_ext = 0, mn_ext = 0;
+};
 struct GemmDesc {
-  int M = 0, N = 0, K = 0;
-  const void* a0 = nullptr; const void* a1 = nullptr; int a_ksplit = 0; int a_mn = 0; long long lda = 0;
-  const void* b0 = nullptr; const void* b1 = nullptr; int b_nsplit = 0; int b_mn = 0; long long ldb = 0;
-  int b_koff = 0; long long b_kext = 0;
-  int k_splits = 1;
+  int M = 0, N = 0, K = 0, batch = 1;
+  int a_mn = 0, b_mn = 0;
+  Operand a0, a1, b0, b1;
+  int kseg = 0;      // two K segments: k-blocks [0,kseg) read a0/b0, the rest a1/(b1 if b_seg)
+  int b_seg = 0;
+  int b_nsplit = 0;  // MN-major B: columns >= b_nsplit come from b1
+  int b_koff = 0;
+  long long out_bstride = 0;   // batch stride of the epilogue output (elements)
   EpiParams epi{};
 };
 
+static attn_status_t operand_map(CUtensorMap* m, const Operand& o, bool mn, int box_rows, int batch,
+                                 int* mode) {
+  const long long bs = batch > 1 ? o.bstride : (o.mn_ext + 1) * o.ld;
+  if (!mn) {
+    cuuint64_t dims[3] = {(cuuint64_t)std::max(1ll, o.k_ext), (cuuint64_t)std::max(1ll, o.mn_ext),
+                          (cuuint64_t)batch};
+    cuuint64_t st[2] = {(cuuint64_t)(o.ld * 2), (cuuint64_t)(bs * 2)};
+    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+    *mode = 0;
+    return encode(m, o.p, false, 3, dims, st, box);
+  }
+  if (g_opt_mn3d && o.mn_ext % 64 == 0) {
+    cuuint64_t dims[4] = {64, (cuuint64_t)std::max(1ll, o.k_ext), (cuuint64_t)(o.mn_ext / 64),
+                          (cuuint64_t)batch};
+    cuuint64_t st[3] = {(cuuint64_t)(o.ld * 2), 128, (cuuint64_t)(bs * 2)};
+    cuuint32_t box[4] = {64, 64, (cuuint32_t)(box_rows / 64), 1};
+    *mode = 1;
+    return encode(m, o.p, false, 4, dims, st, box);
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)std::max(1ll, o.mn_ext), (cuuint64_t)std::max(1ll, o.k_ext),
+                        (cuuint64_t)batch};
+  cuuint64_t st[2] = {(cuuint64_t)(o.ld * 2), (cuuint64_t)(bs * 2)};
+  cuuint32_t box[3] = {64, 64, 1};
+  *mode = 2;
+  return encode(m, o.p, false, 3, dims, st, box);
+}
+
 static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr, int tile_begin) {
   memset(&pr, 0, sizeof(pr));
-  pr.M = g.M; pr.N = g.N; pr.K = g.K;
+  pr.M = g.M; pr.N = g.N; pr.K = g.K; pr.batch = g.batch;
   pr.tiles_m = (g.M + TC_BM - 1) / TC_BM;
   pr.tiles_n = (g.N + TC_BN - 1) / TC_BN;
-  pr.kb_total = (g.K + TC_BK - 1) / TC_BK;
-  pr.k_splits = std::max(1, std::min(g.k_splits, pr.kb_total));
-  pr.kb_per_split = (pr.kb_total + pr.k_splits - 1) / pr.k_splits;
-  pr.k_splits = (pr.kb_total + pr.kb_per_split - 1) / pr.kb_per_split;
+  pr.kseg = g.kseg;
+  pr.kb_total = g.kseg > 0 ? g.kseg + (int)((g.a1.k_ext + TC_BK - 1) / TC_BK)
+                           : (g.K + TC_BK - 1) / TC_BK;
   pr.tile_begin = tile_begin;
   pr.a_mn = g.a_mn; pr.b_mn = g.b_mn;
-  pr.a_ksplit = g.a1 ? g.a_ksplit : 0;
-  pr.b_nsplit = g.b1 ? g.b_nsplit : 0;
+  pr.b_seg = g.b_seg;
+  pr.b_nsplit = g.b_nsplit;
   pr.b_koff = g.b_koff;
   pr.epi = g.epi;
   attn_status_t st;
-  const long long bk = g.b_kext ? g.b_kext : (long long)g.K + g.b_koff;
-  if (!g.a_mn) {
-    const long long k0 = pr.a_ksplit ? pr.a_ksplit : g.K;
-    if ((st = make_map(&maps[0], g.a0, k0, g.M, g.lda, TC_BM)) != ATTN_OK) return st;
-    if ((st = make_map(&maps[1], pr.a_ksplit ? g.a1 : g.a0, pr.a_ksplit ? g.K - pr.a_ksplit : k0,
-                       g.M, g.lda, TC_BM)) != ATTN_OK) return st;
-  } else if (g_opt_mn3d && g.M % 64 == 0) {
-    pr.a_3d = 1;
-    if ((st = make_map_mn3d(&maps[0], g.a0, g.M, g.K, g.lda, TC_BM / 64)) != ATTN_OK) return st;
-    maps[1] = maps[0];
+  int mode0 = 0, mode1 = 0;
+  if ((st = operand_map(&maps[0], g.a0, g.a_mn, TC_BM, g.batch, &mode0)) != ATTN_OK) return st;
+  if (g.kseg > 0) {
+    if ((st = operand_map(&maps[1], g.a1, g.a_mn, TC_BM, g.batch, &mode1)) != ATTN_OK) return st;
+    if (mode1 != mode0) return fail(ATTN_ERR_UNSUPPORTED, "A segments need the same tile mode");
   } else {
-    if ((st = make_map(&maps[0], g.a0, g.M, g.K, g.lda, 64)) != ATTN_OK) return st;
     maps[1] = maps[0];
   }
-  if (!g.b_mn) {
-    if ((st = make_map(&maps[2], g.b0, bk, g.N, g.ldb, TC_BN)) != ATTN_OK) return st;
-    maps[3] = maps[2];
-  } else {
-    const long long n0 = pr.b_nsplit ? pr.b_nsplit : g.N;
-    const long long n1 = pr.b_nsplit ? g.N - pr.b_nsplit : n0;
-    // a split point must not fall inside a tile; atoms past the extent are
-    // zero-filled by TMA, so only whole 64-column atoms are required
-    const bool ok3d = pr.b_nsplit ? (n0 % TC_BN == 0 && n1 % 64 == 0) : (n0 % 64 == 0);
-    if (g_opt_mn3d && ok3d) {
-      pr.b_3d = 1;
-      if ((st = make_map_mn3d(&maps[2], g.b0, n0, bk, g.ldb, TC_BN / 64)) != ATTN_OK) return st;
-      if ((st = make_map_mn3d(&maps[3], pr.b_nsplit ? g.b1 : g.b0, n1, bk, g.ldb, TC_BN / 64)) != ATTN_OK)
-        return st;
-    } else {
-      if ((st = make_map(&maps[2], g.b0, n0, bk, g.ldb, 64)) != ATTN_OK) return st;
-      if ((st = make_map(&maps[3], pr.b_nsplit ? g.b1 : g.b0, n1, bk, g.ldb, 64)) != ATTN_OK) return st;
+  pr.a_mode = mode0;
+  if ((st = operand_map(&maps[2], g.b0, g.b_mn, TC_BN, g.batch, &mode0)) != ATTN_OK) return st;
+  if (g.b_seg || g.b_nsplit) {
+    if ((st = operand_map(&maps[3], g.b1, g.b_mn, TC_BN, g.batch, &mode1)) != ATTN_OK) return st;
+    if (mode1 != mode0) {
+      // keep both halves on the per-atom path
+      int m2;
+      const int save = g_opt_mn3d;
+      g_opt_mn3d = 0;
+      st = operand_map(&maps[2], g.b0, g.b_mn, TC_BN, g.batch, &m2);
+      if (st == ATTN_OK) st = operand_map(&maps[3], g.b1, g.b_mn, TC_BN, g.batch, &m2);
+      g_opt_mn3d = save;
+      if (st != ATTN_OK) return st;
+      mode0 = m2;
     }
+    if (g.b_nsplit && mode0 == 1 && g.b_nsplit % TC_BN != 0) {
+      int m2;
+      const int save = g_opt_mn3d;
+      g_opt_mn3d = 0;
+      st = operand_map(&maps[2], g.b0, g.b_mn, TC_BN, g.batch, &m2);
+      if (st == ATTN_OK) st = operand_map(&maps[3], g.b1, g.b_mn, TC_BN, g.batch, &m2);
+      g_opt_mn3d = save;
+      if (st != ATTN_OK) return st;
+      mode0 = m2;
+    }
+  } else {
+    maps[3] = maps[2];
   }
+  pr.b_mode = mode0;
   // epilogue output: TMA store / reduce-add boxes of 32 rows x 128 bytes
-  if (g.epi.kind != EPI_LSE && g.epi.kind != EPI_NONE) {
-    const bool f32 = epi_out_is_f32(g.epi.kind);
-    if (pr.k_splits != 1) return fail(ATTN_ERR_UNSUPPORTED, "split-K is not used on the tcgen05 path");
-    if ((st = make_map_t(&maps[4], g.epi.out, f32, g.epi.ncols_store, g.M, g.epi.ldo, f32 ? 32 : 64,
-                         32)) != ATTN_OK)
-      return st;
+  const int k = g.epi.kind;
+  if (k != EPI_LSE && k != EPI_NONE && k != EPI_ATTN_SOFTMAX && k != EPI_ATTN_SOFTMAX_BWD) {
+    const bool f32 = epi_out_is_f32(k);
+    const int esz = f32 ? 4 : 2;
+    const long long bs = g.batch > 1 ? g.out_bstride : (long long)(g.M + 1) * g.epi.ldo;
+    cuuint64_t dims[3] = {(cuuint64_t)g.epi.ncols_store, (cuuint64_t)g.M, (cuuint64_t)g.batch};
+    cuuint64_t strides[2] = {(cuuint64_t)(g.epi.ldo * esz), (cuuint64_t)(bs * esz)};
+    cuuint32_t box[3] = {(cuuint32_t)(f32 ? 32 : 64), 32, 1};
+    if ((st = encode(&maps[4], g.epi.out, f32, 3, dims, strides, box)) != ATTN_OK) return st;
   } else {
     maps[4] = maps[0];
   }
   return ATTN_OK;
 }
 
+// fp32 CUDA-core engine: same description, pointer + strides.
 static void fill_simt(const GemmDesc& g, SimtProblem& pr, int tile_begin) {
   memset(&pr, 0, sizeof(pr));
   pr.M = g.M; pr.N = g.N; pr.K = g.K;
   pr.tiles_m = (g.M + SG_BM - 1) / SG_BM;
   pr.tiles_n = (g.N + SG_BN - 1) / SG_BN;
-  const int kchunks = (g.K + SG_BK - 1) / SG_BK;
-  int ks = std::max(1, std::min(g.k_splits, kchunks));
-  const int per = (kchunks + ks - 1) / ks;
-  pr.k_per_split = per * SG_BK;
-  pr.k_splits = (g.K + pr.k_per_split - 1) / pr.k_per_split;
+  pr.k_per_split = ((g.K + SG_BK - 1) / SG_BK) * SG_BK;
+  pr.k_splits = 1;
   pr.tile_begin = tile_begin;
-  pr.a0 = (const float*)g.a0; pr.a1 = (const float*)g.a1; pr.a_ksplit = g.a_ksplit;
-  if (!g.a_mn) { pr.sam = g.lda; pr.sak = 1; } else { pr.sam = 1; pr.sak = g.lda; }
-  pr.b0 = (const float*)g.b0; pr.b1 = (const float*)g.b1; pr.b_nsplit = g.b_nsplit; pr.b_koff = g.b_koff;
-  if (!g.b_mn) { pr.sbn = g.ldb; pr.sbk = 1; } else { pr.sbn = 1; pr.sbk = g.ldb; }
+  pr.a0 = (const float*)g.a0.p;
+  pr.a1 = g.kseg > 0 ? (const float*)g.a1.p : nullptr;
+  pr.a_ksplit = (int)g.a0.k_ext;
+  if (!g.a_mn) { pr.sam = g.a0.ld; pr.sak = 1; } else { pr.sam = 1; pr.sak = g.a0.ld; }
+  pr.b0 = (const float*)g.b0.p;
+  pr.b1 = g.b_nsplit ? (const float*)g.b1.p : nullptr;
+  pr.b_nsplit = g.b_nsplit;
+  pr.b_koff = g.b_koff;
+  if (!g.b_mn) { pr.sbn = g.b0.ld; pr.sbk = 1; } else { pr.sbn = 1; pr.sbk = g.b0.ld; }
   pr.epi = g.epi;
 }
 
@@ -332,7 +345,7 @@ static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cu
   for (int i = 0; i < n; ++i) {
     attn_status_t st = fill_tc(gs[i], P.maps[i], P.prob[i], tiles);
     if (st != ATTN_OK) return st;
-    tiles += P.prob[i].tiles_m * P.prob[i].tiles_n * P.prob[i].k_splits;
+    tiles += P.prob[i].tiles_m * P.prob[i].tiles_n * P.prob[i].batch;
   }
   P.nprob = n;
   P.total_tiles = tiles;
@@ -363,6 +376,19 @@ static attn_status_t launch_simt_group(const GemmDesc* gs, int n, cudaStream_t s
   return ATTN_OK;
 }
 
+// operand helpers: dense row-major [rows, cols] tensors
+static Operand kmaj(const void* p, long long rows, long long k, long long ld, long long bstride = 0) {
+  Operand o;
+  o.p = p; o.ld = ld; o.bstride = bstride; o.k_ext = k; o.mn_ext = rows;
+  return o;
+}
+static Operand mnmaj(const void* p, long long k_rows, long long mn_cols, long long ld,
+                     long long bstride = 0) {
+  Operand o;
+  o.p = p; o.ld = ld; o.bstride = bstride; o.k_ext = k_rows; o.mn_ext = mn_cols;
+  return o;
+}
+
 // ------------------------------------------------------------------ shapes / workspace
 static size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
@@ -381,6 +407,10 @@ static attn_status_t check_shape(const attn_shape_t* s) {
   if (s->dtype == ATTN_BF16 && s->hidden % 64 != 0)
     return fail(ATTN_ERR_UNSUPPORTED,
                 "bf16 path needs hidden %% 64 == 0 (TMA / UMMA K blocks); got d=%d", s->hidden);
+  if (s->dtype == ATTN_BF16 && s->src_len > 128)
+    return fail(ATTN_ERR_UNSUPPORTED,
+                "bf16 path needs M <= 128 source positions (one attention tile per sentence); "
+                "got M=%d", s->src_len);
   return ATTN_OK;
 }
 
@@ -395,7 +425,9 @@ struct Plan {
   int Vc;             // V-chunk width (multiple of 256)
   int nchunks;
   size_t off_lens, off_counters, off_blockpart, off_alpha, off_dalpha, off_ctx, off_hc, off_part,
-      off_tgtlogit, off_lse, off_nll, off_rowscale, off_dl, off_dhc, off_dz, off_dhc2;
+      off_tgtlogit, off_lse, off_nll, off_rowscale, off_dl, off_dhc, off_dz, off_dhc2, off_abf,
+      off_debf;
+  int Mp;             // bf16 path: row stride of the bf16 alpha / de operands (64-multiple)
   size_t total;
 };
 constexpr int kNumCounters = 1024;
@@ -439,6 +471,9 @@ static Plan make_plan(const attn_shape_t* s) {
   p.off_dhc = take(sizeof(float) * p.T * p.d);
   p.off_dz = take(p.elt * p.T * p.d);
   p.off_dhc2 = take(sizeof(float) * p.T * 2 * p.d);
+  p.Mp = (p.M + 63) / 64 * 64;
+  p.off_abf = take(p.bf16 ? 2 * p.T * p.Mp : 0);
+  p.off_debf = take(p.bf16 ? 2 * p.T * p.Mp : 0);
   p.total = o;
   return p;
 }
@@ -553,6 +588,7 @@ struct Bufs {
   int* src_len; int* tgt_len; unsigned int* counters; double* blockpart;
   float* alpha; float* dalpha; void* ctx; void* hc; float2* part; float* tgt_logit;
   float* lse; float* nll; float* rowscale; void* dl[2]; float* dhc; void* dz; float* dhc2;
+  void* abf; void* debf; float* dhpart; void* dcbf;   // bf16 path
 };
 
 static Bufs carve(const Plan& p, void* ws) {
@@ -576,6 +612,10 @@ static Bufs carve(const Plan& p, void* ws) {
   b.dhc = (float*)(w + p.off_dhc);
   b.dz = w + p.off_dz;
   b.dhc2 = (float*)(w + p.off_dhc2);
+  b.abf = w + p.off_abf;
+  b.debf = w + p.off_debf;
+  b.dhpart = b.dhc2;                          // bf16 path: dH_part fp32 [T, d]
+  b.dcbf = (char*)(b.dhc2 + p.T * p.d);       //            dC bf16 [T, d]
   return b;
 }
 
@@ -624,6 +664,169 @@ static attn_status_t validate(const attn_shape_t* s, const void* H_dec, const vo
   return ATTN_OK;
 }
 
+// ---------------------------------------------------------------- GEMM plans
+// Every GEMM of the stage, described once for both engines.  T = B*N rows.
+
+// F3 (Eq. 4): H_c = tanh([H | C] W_c^T): two K segments (H, then C).
+static GemmDesc g_proj(const Plan& p, const void* H, const void* ctx, const void* W_c, void* hc) {
+  GemmDesc g;
+  const int d = p.d;
+  g.M = (int)p.T; g.N = d; g.K = 2 * d;
+  g.a0 = kmaj(H, p.T, d, d);
+  g.a1 = kmaj(ctx, p.T, d, d);
+  g.kseg = (d + TC_BK - 1) / TC_BK;
+  g.b0 = kmaj(W_c, d, 2 * d, 2 * d);
+  g.epi.kind = EPI_TANH; g.epi.out = hc; g.epi.ldo = d; g.epi.ncols_valid = d; g.epi.ncols_store = d;
+  return g;
+}
+// F4 (Eq. 5): logits tile -> (max, sumexp) partials + target logit
+static GemmDesc g_vocab_fwd(const Plan& p, const Bufs& b, const void* W_out, const int* tgt) {
+  GemmDesc g;
+  g.M = (int)p.T; g.N = p.V; g.K = p.d;
+  g.a0 = kmaj(b.hc, p.T, p.d, p.d);
+  g.b0 = kmaj(W_out, p.V, p.d, p.d);
+  g.epi.kind = EPI_LSE; g.epi.ncols_valid = p.V; g.epi.ncols_store = p.V; g.epi.col_base = 0;
+  g.epi.part = b.part; g.epi.part_ld = p.part_ld; g.epi.tgt_logit = b.tgt_logit; g.epi.tgt = tgt;
+  return g;
+}
+// B1, chunk c: dlogits_c = rowscale (softmax - onehot) of the recomputed logits
+static GemmDesc g_dlogits(const Plan& p, const Bufs& b, const void* W_out, const int* tgt, int c) {
+  GemmDesc g;
+  const int c0 = c * p.Vc, vcc = std::min(p.Vc, p.V - c0);
+  g.M = (int)p.T; g.N = vcc; g.K = p.d;
+  g.a0 = kmaj(b.hc, p.T, p.d, p.d);
+  g.b0 = kmaj((const char*)W_out + (size_t)c0 * p.d * p.elt, vcc, p.d, p.d);
+  g.epi.kind = EPI_DLOGITS; g.epi.out = b.dl[c & 1]; g.epi.ldo = p.Vc;
+  g.epi.ncols_valid = vcc; g.epi.ncols_store = p.bf16 ? vcc : p.Vc; g.epi.col_base = c0;
+  g.epi.lse = b.lse; g.epi.rowscale = b.rowscale; g.epi.tgt = tgt;
+  return g;
+}
+// B1, chunk c: dW_out[c] = dlogits_c^T H_c   (both operands MN-major)
+static GemmDesc g_dwout(const Plan& p, const Bufs& b, float* dW_out, int c) {
+  GemmDesc g;
+  const int c0 = c * p.Vc, vcc = std::min(p.Vc, p.V - c0);
+  g.M = vcc; g.N = p.d; g.K = (int)p.T;
+  g.a_mn = 1; g.a0 = mnmaj(b.dl[c & 1], p.T, vcc, p.Vc);
+  g.b_mn = 1; g.b0 = mnmaj(b.hc, p.T, p.d, p.d);
+  g.epi.kind = EPI_STORE_F32; g.epi.out = dW_out + (size_t)c0 * p.d; g.epi.ldo = p.d;
+  g.epi.ncols_valid = p.d; g.epi.ncols_store = p.d;
+  return g;
+}
+// B1, chunk c: dHc (+)= dlogits_c W_out[c]   (B MN-major, K offset c0)
+static GemmDesc g_dhc(const Plan& p, const Bufs& b, const void* W_out, int c) {
+  GemmDesc g;
+  const int c0 = c * p.Vc, vcc = std::min(p.Vc, p.V - c0);
+  g.M = (int)p.T; g.N = p.d; g.K = vcc;
+  g.a0 = kmaj(b.dl[c & 1], p.T, vcc, p.Vc);
+  g.b_mn = 1; g.b0 = mnmaj(W_out, p.V, p.d, p.d); g.b_koff = c0;
+  g.epi.kind = (c == 0) ? EPI_STORE_F32 : EPI_ACCUM_F32; g.epi.out = b.dhc; g.epi.ldo = p.d;
+  g.epi.ncols_valid = p.d; g.epi.ncols_store = p.d;
+  return g;
+}
+// B2: dW_c = dz^T [H | C]   (A MN-major, B MN-major split at column d)
+static GemmDesc g_dwc(const Plan& p, const Bufs& b, const void* H, float* dW_c) {
+  GemmDesc g;
+  const int d = p.d;
+  g.M = d; g.N = 2 * d; g.K = (int)p.T;
+  g.a_mn = 1; g.a0 = mnmaj(b.dz, p.T, d, d);
+  g.b_mn = 1; g.b0 = mnmaj(H, p.T, d, d); g.b1 = mnmaj(b.ctx, p.T, d, d); g.b_nsplit = d;
+  g.epi.kind = EPI_STORE_F32; g.epi.out = dW_c; g.epi.ldo = 2ll * d;
+  g.epi.ncols_valid = 2 * d; g.epi.ncols_store = 2 * d;
+  return g;
+}
+// B2: dz W_c restricted to output columns [col0, col0 + ncol) (W_c MN-major)
+static GemmDesc g_dzwc(const Plan& p, const Bufs& b, const void* W_c, int col0, int ncol,
+                       int kind, void* out, long long ldo) {
+  GemmDesc g;
+  const int d = p.d;
+  g.M = (int)p.T; g.N = ncol; g.K = d;
+  g.a0 = kmaj(b.dz, p.T, d, d);
+  g.b_mn = 1; g.b0 = mnmaj((const char*)W_c + (size_t)col0 * p.elt, d, ncol, 2ll * d);
+  g.epi.kind = kind; g.epi.out = out; g.epi.ldo = ldo;
+  g.epi.ncols_valid = ncol; g.epi.ncols_store = ncol;
+  return g;
+}
+
+// ---------------------------------------------------------------- attention on tcgen05 (bf16)
+// One small GEMM per sentence (batched problems; M <= 128 source positions).
+static attn_status_t attention_forward_tc(const Plan& p, const void* H, const void* S, const Bufs& b,
+                                          cudaStream_t stream, int* (*next)(void*), void* ctx_) {
+  const int d = p.d, N = p.N, M = p.M, Mp = p.Mp, B = p.B;
+  // F1 + Eq. 1: scores E_b = H_b S_b^T with the masked row softmax fused
+  {
+    GemmDesc g;
+    g.batch = B; g.M = N; g.N = M; g.K = d;
+    g.a0 = kmaj(H, N, d, d, (long long)N * d);
+    g.b0 = kmaj(S, M, d, d, (long long)M * d);
+    g.epi.kind = EPI_ATTN_SOFTMAX; g.epi.stash_f32 = b.alpha; g.epi.ncols_valid = M;
+    g.epi.out = b.abf; g.epi.ldo = Mp; g.epi.ncols_store = Mp; g.epi.src_len = b.src_len;
+    attn_status_t st = launch_tc_group<__nv_bfloat16>(&g, 1, next(ctx_), stream);
+    if (st != ATTN_OK) return st;
+  }
+  // F2 (Eq. 3): C_b = alpha_b S_b   (S as MN-major B, K = source positions)
+  GemmDesc g;
+  g.batch = B; g.M = N; g.N = d; g.K = M;
+  g.a0 = kmaj(b.abf, N, M, Mp, (long long)N * Mp);
+  g.b_mn = 1; g.b0 = mnmaj(S, M, d, d, (long long)M * d);
+  g.epi.kind = EPI_STORE_BF16; g.epi.out = b.ctx; g.epi.ldo = d; g.epi.ncols_valid = d;
+  g.epi.ncols_store = d;
+  g.out_bstride = (long long)N * d;
+  return launch_tc_group<__nv_bfloat16>(&g, 1, next(ctx_), stream);
+}
+
+static attn_status_t attention_backward_tc(const Plan& p, const void* H, const void* S,
+                                           void* dH, void* dS, const Bufs& b, cudaStream_t stream,
+                                           int* (*next)(void*), void* ctx_) {
+  const int d = p.d, N = p.N, M = p.M, Mp = p.Mp, B = p.B;
+  // dalpha_b = dC_b S_b^T with the softmax backward fused: de (bf16)
+  {
+    GemmDesc g;
+    g.batch = B; g.M = N; g.N = M; g.K = d;
+    g.a0 = kmaj(b.dcbf, N, d, d, (long long)N * d);
+    g.b0 = kmaj(S, M, d, d, (long long)M * d);
+    g.epi.kind = EPI_ATTN_SOFTMAX_BWD; g.epi.stash_f32 = b.alpha; g.epi.ncols_valid = M;
+    g.epi.out = b.debf; g.epi.ldo = Mp; g.epi.ncols_store = Mp;
+    attn_status_t st = launch_tc_group<__nv_bfloat16>(&g, 1, next(ctx_), stream);
+    if (st != ATTN_OK) return st;
+  }
+  GemmDesc gs[2];
+  // dH_dec_b = dH_part_b + de_b S_b
+  {
+    GemmDesc& g = gs[0];
+    g.batch = B; g.M = N; g.N = d; g.K = M;
+    g.a0 = kmaj(b.debf, N, M, Mp, (long long)N * Mp);
+    g.b_mn = 1; g.b0 = mnmaj(S, M, d, d, (long long)M * d);
+    g.epi.kind = EPI_ADD_BF16; g.epi.out = dH; g.epi.ldo = d; g.epi.ncols_valid = d;
+    g.epi.ncols_store = d; g.epi.addend = b.dhpart; g.epi.add_ld = d;
+    g.out_bstride = (long long)N * d;
+  }
+  // dH_enc_b = alpha_b^T dC_b + de_b^T H_b: two K segments over the decoder rows
+  {
+    GemmDesc& g = gs[1];
+    g.batch = B; g.M = M; g.N = d; g.K = 2 * N;
+    g.a_mn = 1;
+    g.a0 = mnmaj(b.abf, N, Mp, Mp, (long long)N * Mp);
+    g.a1 = mnmaj(b.debf, N, Mp, Mp, (long long)N * Mp);
+    g.kseg = (N + TC_BK - 1) / TC_BK;
+    g.b_mn = 1; g.b_seg = 1;
+    g.b0 = mnmaj(b.dcbf, N, d, d, (long long)N * d);
+    g.b1 = mnmaj(H, N, d, d, (long long)N * d);
+    g.epi.kind = EPI_STORE_BF16; g.epi.out = dS; g.epi.ldo = d; g.epi.ncols_valid = d;
+    g.epi.ncols_store = d;
+    g.out_bstride = (long long)M * d;
+  }
+  return launch_tc_group<__nv_bfloat16>(gs, 2, next(ctx_), stream);
+}
+
+struct CounterCtx {
+  const Bufs* b;
+  int idx;
+};
+static int* next_counter_fn(void* c) {
+  CounterCtx* cc = (CounterCtx*)c;
+  return (int*)(cc->b->counters + 1 + (cc->idx++));
+}
+
 template <typename T>
 static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int32_t* tgt_ids,
                                const T* W_c, const T* W_out, float loss_scale, float* loss, T* dH,
@@ -631,13 +834,12 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
                                cudaStream_t stream) {
   attn_status_t st;
   const bool tc = p.bf16;
-  int counter_idx = 0;
-  auto next_counter = [&]() { return (int*)(b.counters + 1 + (counter_idx++)); };
+  CounterCtx cctx{&b, 0};
   auto gemm = [&](const GemmDesc* gs, int n) -> attn_status_t {
-    if (tc) return launch_tc_group<__nv_bfloat16>(gs, n, next_counter(), stream);
+    if (tc) return launch_tc_group<__nv_bfloat16>(gs, n, next_counter_fn(&cctx), stream);
     return launch_simt_group(gs, n, stream);
   };
-  const int d = p.d, V = p.V;
+  const int d = p.d;
   const long long TT = p.T;
   CUDA_TRY(cudaMemsetAsync(b.counters, 0, sizeof(unsigned int) * kNumCounters, stream));
   g_prof.n = 0;
@@ -645,36 +847,31 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   prof_mark("start", stream);
 
   // ---- F1, F2 (Eqs. 1-3)
-  if ((st = attention_forward<T>(p, H, S, b.src_len, b.alpha, (T*)b.ctx, stream)) != ATTN_OK) return st;
+  if (tc)
+    st = attention_forward_tc(p, H, S, b, stream, next_counter_fn, &cctx);
+  else
+    st = attention_forward<T>(p, H, S, b.src_len, b.alpha, (T*)b.ctx, stream);
+  if (st != ATTN_OK) return st;
   prof_mark("attn_fwd", stream);
 
-  // ---- F3 (Eq. 4): H_c = tanh([H | C] W_c^T)
+  // ---- F3 (Eq. 4)
   {
-    GemmDesc g;
-    g.M = (int)TT; g.N = d; g.K = 2 * d;
-    g.a0 = H; g.a1 = b.ctx; g.a_ksplit = d; g.a_mn = 0; g.lda = d;
-    g.b0 = W_c; g.b_mn = 0; g.ldb = 2ll * d;
-    g.epi.kind = EPI_TANH; g.epi.out = b.hc; g.epi.ldo = d; g.epi.ncols_valid = d; g.epi.ncols_store = d;
+    GemmDesc g = g_proj(p, H, b.ctx, W_c, b.hc);
     if ((st = gemm(&g, 1)) != ATTN_OK) return st;
   }
   prof_mark("proj_tanh", stream);
-  // ---- F4 (Eq. 5): per-tile (max, sumexp) and target logit, logits discarded
+  // ---- F4 (Eq. 5): logits discarded, per-tile (max, sumexp) kept
   {
-    GemmDesc g;
-    g.M = (int)TT; g.N = V; g.K = d;
-    g.a0 = b.hc; g.a_mn = 0; g.lda = d;
-    g.b0 = W_out; g.b_mn = 0; g.ldb = d;
-    g.epi.kind = EPI_LSE; g.epi.ncols_valid = V; g.epi.ncols_store = V; g.epi.col_base = 0;
-    g.epi.part = b.part; g.epi.part_ld = p.part_ld; g.epi.tgt_logit = b.tgt_logit; g.epi.tgt = tgt_ids;
+    GemmDesc g = g_vocab_fwd(p, b, W_out, tgt_ids);
     if ((st = gemm(&g, 1)) != ATTN_OK) return st;
   }
   prof_mark("vocab_fwd", stream);
   // ---- Eq. 6: lse, token NLL, row scale, loss
   {
     const int blocks = (int)((TT + 7) / 8);
-    lse_reduce_kernel<<<blocks, 256, 0, stream>>>(b.part, p.part_ld, b.tgt_logit, b.tgt_len, (int)TT, p.N,
-                                                  loss_scale, b.lse, b.nll, b.rowscale, b.blockpart,
-                                                  b.counters, loss);
+    lse_reduce_kernel<<<blocks, 256, 0, stream>>>(b.part, p.part_ld, b.tgt_logit, b.tgt_len, (int)TT,
+                                                  p.N, loss_scale, b.lse, b.nll, b.rowscale,
+                                                  b.blockpart, b.counters, loss);
     CUDA_TRY(cudaGetLastError());
     ++g_launches;
   }
@@ -684,56 +881,21 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
     if ((st = comm_begin(comm, stream, &cr)) != ATTN_OK) return st;
   }
 
-  // ---- B1: V-chunked vocab backward
-  auto dl_desc = [&](int c) {
-    GemmDesc g;
-    const int c0 = c * p.Vc;
-    const int vcc = std::min(p.Vc, V - c0);
-    g.M = (int)TT; g.N = vcc; g.K = d;
-    g.a0 = b.hc; g.a_mn = 0; g.lda = d;
-    g.b0 = (const char*)W_out + (size_t)c0 * d * sizeof(T); g.b_mn = 0; g.ldb = d;
-    g.epi.kind = EPI_DLOGITS; g.epi.out = b.dl[c & 1]; g.epi.ldo = p.Vc;
-    g.epi.ncols_valid = vcc; g.epi.ncols_store = p.Vc; g.epi.col_base = c0;
-    g.epi.lse = b.lse; g.epi.rowscale = b.rowscale; g.epi.tgt = tgt_ids;
-    return g;
-  };
-  auto dwo_desc = [&](int c) {
-    GemmDesc g;
-    const int c0 = c * p.Vc;
-    const int vcc = std::min(p.Vc, V - c0);
-    g.M = vcc; g.N = d; g.K = (int)TT;
-    g.a0 = b.dl[c & 1]; g.a_mn = 1; g.lda = p.Vc;
-    g.b0 = b.hc; g.b_mn = 1; g.ldb = d;
-    g.epi.kind = EPI_STORE_F32; g.epi.out = dW_out + (size_t)c0 * d; g.epi.ldo = d;
-    g.epi.ncols_valid = d; g.epi.ncols_store = d;
-    return g;
-  };
-  auto dhc_desc = [&](int c) {
-    GemmDesc g;
-    const int c0 = c * p.Vc;
-    const int vcc = std::min(p.Vc, V - c0);
-    g.M = (int)TT; g.N = d; g.K = vcc;
-    g.a0 = b.dl[c & 1]; g.a_mn = 0; g.lda = p.Vc;
-    g.b0 = W_out; g.b_mn = 1; g.ldb = d; g.b_koff = c0; g.b_kext = V;
-    // dHc accumulates over the V-chunks: the first chunk stores, later ones
-    // add (TMA reduce-add on the tcgen05 path)
-    g.epi.kind = (c == 0) ? EPI_STORE_F32 : EPI_ACCUM_F32; g.epi.out = b.dhc; g.epi.ldo = d;
-    g.epi.ncols_valid = d; g.epi.ncols_store = d;
-    return g;
-  };
+  // ---- B1: V-chunked vocab backward.  Launch c runs dW_out[c] and dHc += ...
+  // for chunk c together with the dlogits of chunk c+1 (double-buffered).
   {
-    GemmDesc g0 = dl_desc(0);
+    GemmDesc g0 = g_dlogits(p, b, W_out, tgt_ids, 0);
     if ((st = gemm(&g0, 1)) != ATTN_OK) return st;
     for (int c = 0; c < p.nchunks; ++c) {
       GemmDesc gs[3];
       int n = 0;
-      gs[n++] = dwo_desc(c);   // K = T: the long tiles first
-      gs[n++] = dhc_desc(c);
-      if (c + 1 < p.nchunks) gs[n++] = dl_desc(c + 1);
+      gs[n++] = g_dwout(p, b, dW_out, c);   // K = T: the long tiles first
+      gs[n++] = g_dhc(p, b, W_out, c);
+      if (c + 1 < p.nchunks) gs[n++] = g_dlogits(p, b, W_out, tgt_ids, c + 1);
       if ((st = gemm(gs, n)) != ATTN_OK) return st;
       if (comm) {
         const int c0 = c * p.Vc;
-        const int vcc = std::min(p.Vc, V - c0);
+        const int vcc = std::min(p.Vc, p.V - c0);
         if ((st = comm_enqueue_allreduce(comm, &cr, stream, dW_out + (size_t)c0 * d,
                                          (size_t)vcc * d)) != ATTN_OK)
           return st;
@@ -749,30 +911,29 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
     ++g_launches;
   }
   prof_mark("vocab_bwd", stream);
-  // ---- B2: dW_c = dz^T [H | C];  [dH_part | dC] = dz W_c
+  // ---- B2: dW_c = dz^T [H | C];  dH_part = dz W_c[:, :d];  dC = dz W_c[:, d:]
   {
-    GemmDesc gs[2];
-    GemmDesc& g = gs[0];
-    g.M = d; g.N = 2 * d; g.K = (int)TT;
-    g.a0 = b.dz; g.a_mn = 1; g.lda = d;
-    g.b0 = H; g.b1 = b.ctx; g.b_nsplit = d; g.b_mn = 1; g.ldb = d;
-    g.epi.kind = EPI_STORE_F32; g.epi.out = dW_c; g.epi.ldo = 2ll * d;
-    g.epi.ncols_valid = 2 * d; g.epi.ncols_store = 2 * d;
-    GemmDesc& h = gs[1];
-    h.M = (int)TT; h.N = 2 * d; h.K = d;
-    h.a0 = b.dz; h.a_mn = 0; h.lda = d;
-    h.b0 = W_c; h.b_mn = 1; h.ldb = 2ll * d;
-    h.epi.kind = EPI_STORE_F32; h.epi.out = b.dhc2; h.epi.ldo = 2ll * d;
-    h.epi.ncols_valid = 2 * d; h.epi.ncols_store = 2 * d;
-    if ((st = gemm(gs, 2)) != ATTN_OK) return st;
+    GemmDesc gs[3];
+    int n = 0;
+    gs[n++] = g_dwc(p, b, H, dW_c);
+    if (tc) {
+      gs[n++] = g_dzwc(p, b, W_c, 0, d, EPI_STORE_F32, b.dhpart, d);
+      gs[n++] = g_dzwc(p, b, W_c, d, d, EPI_STORE_BF16, b.dcbf, d);
+    } else {
+      gs[n++] = g_dzwc(p, b, W_c, 0, 2 * d, EPI_STORE_F32, b.dhc2, 2ll * d);
+    }
+    if ((st = gemm(gs, n)) != ATTN_OK) return st;
     if (comm) {
       if ((st = comm_enqueue_allreduce(comm, &cr, stream, dW_c, (size_t)d * 2 * d)) != ATTN_OK) return st;
     }
   }
   prof_mark("proj_bwd", stream);
   // ---- B3: attention backward
-  if ((st = attention_backward<T>(p, H, S, b.alpha, b.dalpha, b.dhc2, dH, dS, stream)) != ATTN_OK)
-    return st;
+  if (tc)
+    st = attention_backward_tc(p, H, S, dH, dS, b, stream, next_counter_fn, &cctx);
+  else
+    st = attention_backward<T>(p, H, S, b.alpha, b.dalpha, b.dhc2, dH, dS, stream);
+  if (st != ATTN_OK) return st;
   prof_mark("attn_bwd", stream);
   if (comm) {
     if ((st = comm_enqueue_allreduce(comm, &cr, stream, loss, 1)) != ATTN_OK) return st;
@@ -881,8 +1042,8 @@ extern "C" attn_status_t attn_debug_gemm_bf16(int M, int N, int K, const void* A
     return fail(ATTN_ERR_INVALID_ARG, "debug_gemm: bad arguments");
   GemmDesc g;
   g.M = M; g.N = N; g.K = K;
-  g.a0 = A; g.a_mn = a_mn; g.lda = a_mn ? M : K;
-  g.b0 = B; g.b_mn = b_mn; g.ldb = b_mn ? N : K;
+  g.a_mn = a_mn; g.a0 = a_mn ? mnmaj(A, K, M, M) : kmaj(A, M, K, K);
+  g.b_mn = b_mn; g.b0 = b_mn ? mnmaj(B, K, N, N) : kmaj(B, N, K, K);
   g.epi.kind = EPI_STORE_F32; g.epi.out = C; g.epi.ldo = N; g.epi.ncols_valid = N; g.epi.ncols_store = N;
   if (g_debug_epi == 1) g.epi.kind = EPI_NONE;
   // one persistent device counter per process (debug entry only); the memset

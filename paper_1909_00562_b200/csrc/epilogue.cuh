@@ -22,7 +22,11 @@ namespace attnsm {
 
 enum EpiKind : int {
   EPI_STORE_F32 = 0, EPI_TANH = 1, EPI_LSE = 2, EPI_DLOGITS = 3, EPI_ACCUM_F32 = 4,
-  EPI_NONE = 5   // debug: read the accumulator, store nothing
+  EPI_NONE = 5,               // debug: read the accumulator, store nothing
+  EPI_STORE_BF16 = 6,         // out = acc (bf16): C, dC, dH_enc
+  EPI_ADD_BF16 = 7,           // out = acc + addend (fp32) -> bf16: dH_dec = dH_part + de S
+  EPI_ATTN_SOFTMAX = 8,       // masked row softmax of the scores (Eq. 1), tcgen05 path
+  EPI_ATTN_SOFTMAX_BWD = 9    // its backward, tcgen05 path
 };
 
 // Output element type of each kind (tcgen05 path: bf16 activations).
@@ -44,6 +48,10 @@ struct EpiParams {
   const int* tgt;        // LSE/DLOGITS: [rows] target ids
   const float* lse;      // DLOGITS: [rows]
   const float* rowscale; // DLOGITS: [rows] loss_scale on valid rows, 0 on padded
+  float* stash_f32;      // ATTN_SOFTMAX(_BWD): alpha fp32 [rows, ncols_valid]
+  const int* src_len;    // ATTN_SOFTMAX: [batch]
+  const float* addend;   // ADD_BF16: [rows, add_ld] fp32
+  long long add_ld;
 };
 
 template <typename T> __device__ __forceinline__ T to_out(float x);

@@ -2,11 +2,14 @@
 //
 //   D[M,N] (fp32, in TMEM) = A[M,K] * B[N,K]^T,  bf16 operands staged by TMA
 //   (128-byte swizzle) into a 4-stage shared-memory ring; the epilogue reads
-//   the accumulator with tcgen05.ld and runs one of the row epilogues of
-//   epilogue.cuh.  One launch runs a GROUP of up to kMaxProblems independent
-//   problems (e.g. the V-chunk c dW_out and dHc GEMMs together with the
-//   chunk c+1 dlogits GEMM); CTAs pull tiles from a global atomic counter so
-//   long-K and short-K tiles balance across the 148 SMs.
+//   the accumulator with tcgen05.ld and runs one of the epilogues below.
+//   One launch runs a GROUP of up to kMaxProblems independent problems (e.g.
+//   the V-chunk c dW_out and dHc GEMMs together with the chunk c+1 dlogits
+//   GEMM); CTAs pull tiles from a global atomic counter so long-K and
+//   short-K tiles balance across the 148 SMs.  A problem may be BATCHED (one
+//   small GEMM per sentence: the attention steps), in which case every
+//   tensor map carries the sentence as its outermost coordinate and rows past
+//   a sentence's extent are zero-filled (loads) or clipped (stores) by TMA.
 //
 // Roles (384 threads, one CTA per SM):
 //   warp 0       tile scheduler + TMA producer (one elected lane)
@@ -17,8 +20,13 @@
 //                memory (128-byte swizzle, conflict-free) and written with
 //                TMA bulk stores, or TMA reduce-adds for accumulation.
 //
-// Operands may be K-major (row-major [rows, K]) or MN-major (row-major
-// [K, rows]); see DESIGN.md "tcgen05 encodings" for the descriptor fields.
+// Operand tiles:
+//   mode 0  K-major  [rows, K]: one 3D box {64 (K), rows, 1 (batch)}
+//   mode 1  MN-major [K, MN]:   one 4D box {64, 64 (K), rows/64 (atoms), 1}
+//   mode 2  MN-major [K, MN]:   one 3D box {64, 64, 1} per 64-wide atom
+// A K range may be split into two SEGMENTS (k-blocks < kseg read maps 0, the
+// rest read maps 1 from K = 0 again): [H | C] of Eq. 4, and the two terms of
+// the attention backward dH_enc = alpha^T dC + de^T H.
 #pragma once
 #include "epilogue.cuh"
 #include "ptx.cuh"
@@ -41,14 +49,16 @@ constexpr int TC_SMEM_BYTES =
 constexpr int kMaxProblems = 4;
 
 struct TcProblem {
-  int M, N, K;
-  int tiles_m, tiles_n, k_splits, kb_per_split, kb_total;
+  int M, N, K;      // per batch item
+  int batch;
+  int tiles_m, tiles_n, kb_total;
   int tile_begin;
-  int a_mn, b_mn;
-  int a_3d, b_3d;   // MN-major operand loaded as ONE 3D box {64, 64, rows/64} (atoms as dim 2)
-  int a_ksplit;   // K-major A: k < a_ksplit -> map a0 else a1 (at k - a_ksplit); 0 = none
-  int b_nsplit;   // MN-major B: n < b_nsplit -> map b0 else b1 (at n - b_nsplit); 0 = none
-  int b_koff;     // added to B's K coordinate
+  int a_mn, b_mn;   // UMMA majorness
+  int a_mode, b_mode;
+  int kseg;         // k-blocks in segment 0 (0 = one segment)
+  int b_seg;        // B switches to map b1 in segment 1 (else continues in b0)
+  int b_nsplit;     // B column split between maps b0 / b1 (MN-major B, 0 = none)
+  int b_koff;       // added to B's K coordinate (elements)
   EpiParams epi;
 };
 
@@ -69,7 +79,7 @@ __device__ __forceinline__ int tc_find_problem(const TcParams& P, int t) {
 }
 
 struct TcTile {
-  int p, m0, n0, tn, split, kb0, kb1;
+  int p, b, m0, n0, tn;
 };
 
 __device__ __forceinline__ TcTile tc_decode(const TcParams& P, int t) {
@@ -77,16 +87,93 @@ __device__ __forceinline__ TcTile tc_decode(const TcParams& P, int t) {
   r.p = tc_find_problem(P, t);
   const TcProblem& pr = P.prob[r.p];
   int local = t - pr.tile_begin;
-  const int per_split = pr.tiles_m * pr.tiles_n;
-  r.split = local / per_split;
-  local -= r.split * per_split;
+  const int per_b = pr.tiles_m * pr.tiles_n;
+  r.b = local / per_b;
+  local -= r.b * per_b;
   const int tm = local % pr.tiles_m;
   r.tn = local / pr.tiles_m;
   r.m0 = tm * TC_BM;
   r.n0 = r.tn * TC_BN;
-  r.kb0 = r.split * pr.kb_per_split;
-  r.kb1 = min(pr.kb_total, r.kb0 + pr.kb_per_split);
   return r;
+}
+
+// Load one operand tile (rows x 64 K) of k-block kb into smem.
+__device__ __forceinline__ void tc_load_operand(uint8_t* dst, const CUtensorMap* m, uint64_t* bar,
+                                                int mode, int rows, int r0, int k0, int b) {
+  if (mode == 0) {
+    tma_load_3d(dst, m, bar, k0, r0, b);
+  } else if (mode == 1) {
+    tma_load_4d(dst, m, bar, 0, k0, r0 / 64, b);
+  } else {
+    for (int i = 0; i < rows / 64; ++i) tma_load_3d(dst + i * 8192, m, bar, r0 + 64 * i, k0, b);
+  }
+}
+
+// ---------------------------------------------------------------- attention epilogues
+// Masked row softmax of the scores tile (Eq. 1): one thread per decoder row,
+// M_src <= 128 columns (column half 0 only).  Writes alpha (fp32 stash, row
+// stride ncols_valid = M) and its bf16 copy (row stride ldo = Mp, the operand
+// of Eq. 3 and of the backward), both exactly 0 for j >= src_len.
+__device__ __forceinline__ void epi_attn_softmax(const EpiParams& e, uint32_t taddr, int n_act,
+                                                 int rowg, bool row_ok, int L) {
+  float v[32];
+  float mx = -INFINITY;
+  for (int c = 0; c < n_act; ++c) {
+    tmem_ld32(taddr + c * 32, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (c * 32 + j < L) mx = fmaxf(mx, v[j]);
+  }
+  float s = 0.f;
+  for (int c = 0; c < n_act; ++c) {
+    tmem_ld32(taddr + c * 32, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (c * 32 + j < L) s += expf(v[j] - mx);
+  }
+  const float inv = 1.f / s;
+  float* af = e.stash_f32 + (long long)rowg * e.ncols_valid;
+  __nv_bfloat16* ab = reinterpret_cast<__nv_bfloat16*>(e.out) + (long long)rowg * e.ldo;
+  for (int c = 0; c < n_act; ++c) {
+    tmem_ld32(taddr + c * 32, v);
+    if (!row_ok) continue;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int col = c * 32 + j;
+      const float a = (col < L) ? expf(v[j] - mx) * inv : 0.f;
+      if (col < e.ncols_valid) af[col] = a;
+      if (col < e.ldo) ab[col] = __float2bfloat16_rn(a);
+    }
+  }
+}
+
+// Backward of Eq. 1 on the dalpha tile: de = alpha (dalpha - sum_j alpha dalpha),
+// written as bf16 (row stride ldo = Mp), exactly 0 where alpha is.
+__device__ __forceinline__ void epi_attn_softmax_bwd(const EpiParams& e, uint32_t taddr, int n_act,
+                                                     int rowg, bool row_ok) {
+  float v[32];
+  const float* af = e.stash_f32 + (long long)rowg * e.ncols_valid;
+  float D = 0.f;
+  for (int c = 0; c < n_act; ++c) {
+    tmem_ld32(taddr + c * 32, v);
+    if (!row_ok) continue;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int col = c * 32 + j;
+      if (col < e.ncols_valid) D += af[col] * v[j];
+    }
+  }
+  __nv_bfloat16* db = reinterpret_cast<__nv_bfloat16*>(e.out) + (long long)rowg * e.ldo;
+  for (int c = 0; c < n_act; ++c) {
+    tmem_ld32(taddr + c * 32, v);
+    if (!row_ok) continue;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int col = c * 32 + j;
+      const float a = (col < e.ncols_valid) ? af[col] : 0.f;
+      if (col < e.ldo) db[col] = __float2bfloat16_rn(a * (v[j] - D));
+    }
+  }
 }
 
 template <typename OutT, bool kFast>
@@ -156,41 +243,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         const CUtensorMap* ma1 = &P.maps[tl.p][1];
         const CUtensorMap* mb0 = &P.maps[tl.p][2];
         const CUtensorMap* mb1 = &P.maps[tl.p][3];
-        for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
+        for (int kb = 0; kb < pr.kb_total; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* sA = smem + s * TC_STAGE_BYTES;
           uint8_t* sB = sA + TC_A_BYTES;
           mbar_arrive_expect_tx(&full[s], TC_STAGE_BYTES);
-          const int k0 = kb * TC_BK;
-          if (!pr.a_mn) {
-            if (pr.a_ksplit > 0 && k0 >= pr.a_ksplit)
-              tma_load_2d(sA, ma1, &full[s], k0 - pr.a_ksplit, tl.m0);
+          const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
+          const int ka = (seg1 ? kb - pr.kseg : kb) * TC_BK;
+          tc_load_operand(sA, seg1 ? ma1 : ma0, &full[s], pr.a_mode, TC_BM, tl.m0, ka, tl.b);
+          const bool bseg1 = seg1 && pr.b_seg;
+          const int kbk = (bseg1 ? kb - pr.kseg : kb) * TC_BK + pr.b_koff;
+          const CUtensorMap* mb = bseg1 ? mb1 : mb0;
+          if (pr.b_nsplit > 0 && pr.b_mode == 1) {
+            if (tl.n0 >= pr.b_nsplit)
+              tma_load_4d(sB, mb1, &full[s], 0, kbk, (tl.n0 - pr.b_nsplit) / 64, tl.b);
             else
-              tma_load_2d(sA, ma0, &full[s], k0, tl.m0);
-          } else if (pr.a_3d) {
-            tma_load_3d(sA, ma0, &full[s], 0, k0, tl.m0 / 64);
-          } else {
-#pragma unroll
-            for (int i = 0; i < TC_BM / 64; ++i)
-              tma_load_2d(sA + i * 8192, ma0, &full[s], tl.m0 + 64 * i, k0);
-          }
-          const int kb_ = k0 + pr.b_koff;
-          if (!pr.b_mn) {
-            tma_load_2d(sB, mb0, &full[s], kb_, tl.n0);
-          } else if (pr.b_3d) {
-            if (pr.b_nsplit > 0 && tl.n0 >= pr.b_nsplit)
-              tma_load_3d(sB, mb1, &full[s], 0, kb_, (tl.n0 - pr.b_nsplit) / 64);
-            else
-              tma_load_3d(sB, mb0, &full[s], 0, kb_, tl.n0 / 64);
-          } else {
-#pragma unroll
+              tma_load_4d(sB, mb0, &full[s], 0, kbk, tl.n0 / 64, tl.b);
+          } else if (pr.b_nsplit > 0) {
             for (int i = 0; i < TC_BN / 64; ++i) {
               const int n = tl.n0 + 64 * i;
-              if (pr.b_nsplit > 0 && n >= pr.b_nsplit)
-                tma_load_2d(sB + i * 8192, mb1, &full[s], n - pr.b_nsplit, kb_);
+              if (n >= pr.b_nsplit)
+                tma_load_3d(sB + i * 8192, mb1, &full[s], n - pr.b_nsplit, kbk, tl.b);
               else
-                tma_load_2d(sB + i * 8192, mb0, &full[s], n, kb_);
+                tma_load_3d(sB + i * 8192, mb0, &full[s], n, kbk, tl.b);
             }
+          } else {
+            tc_load_operand(sB, mb, &full[s], pr.b_mode, TC_BN, tl.n0, kbk, tl.b);
           }
           if (++s == TC_STAGES) { s = 0; ph ^= 1; }
         }
@@ -221,7 +299,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t dcol = tmem_base + acc * TC_BN;
-        for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
+        for (int kb = 0; kb < pr.kb_total; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t sA = smem_u32(smem + s * TC_STAGE_BYTES);
@@ -230,7 +308,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           for (int k = 0; k < TC_BK / 16; ++k) {
             const uint64_t ad = umma_sdesc(sA + k * a_kstep, a_lbo, 1024);
             const uint64_t bd = umma_sdesc(sB + k * b_kstep, b_lbo, 1024);
-            umma_bf16(dcol, ad, bd, idesc, (kb > tl.kb0 || k > 0) ? 1u : 0u);
+            umma_bf16(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
           }
           umma_commit(&empty[s]);
           if (++s == TC_STAGES) { s = 0; ph ^= 1; }
@@ -263,68 +341,90 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       const CUtensorMap* omap = &P.maps[tl.p][4];
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int row0 = tl.m0 + q * 32;
+      const int row0 = tl.m0 + q * 32;           // row inside the batch item
       const int row = row0 + lane;
       const bool row_ok = row < pr.M;
+      const int rowg = tl.b * pr.M + (row_ok ? row : 0);   // row of the flattened [batch*M] arrays
       const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * TC_BN + h * 128;
-      RowEpilogue<OutT, kFast> epi(pr.epi, row_ok ? row : 0, tl.split);
       const int col_h = tl.n0 + h * 128;
-      const int lim = (kind == EPI_LSE) ? pr.epi.ncols_valid : pr.epi.ncols_store;
+      const int lim = (kind == EPI_LSE || kind == EPI_ATTN_SOFTMAX || kind == EPI_ATTN_SOFTMAX_BWD)
+                          ? pr.epi.ncols_valid : pr.epi.ncols_store;
       const int n_act = max(0, min(4, (lim - col_h + 31) / 32));   // warp-uniform
-      const bool f32out = epi_out_is_f32(kind);
+      if (kind == EPI_ATTN_SOFTMAX) {
+        if (n_act > 0) epi_attn_softmax(pr.epi, taddr, n_act, rowg, row_ok, pr.epi.src_len[tl.b]);
+      } else if (kind == EPI_ATTN_SOFTMAX_BWD) {
+        if (n_act > 0) epi_attn_softmax_bwd(pr.epi, taddr, n_act, rowg, row_ok);
+      } else {
+        RowEpilogue<OutT, kFast> epi(pr.epi, rowg, 0);
+        const bool f32out = epi_out_is_f32(kind);
 #pragma unroll 1
-      for (int c = 0; c < n_act; ++c) {
-        float v[32];
-        tmem_ld32(taddr + c * 32, v);
-        const int col = col_h + c * 32;
-        if (kind == EPI_LSE) {
-          if (row_ok) epi.chunk(col, v);
-          continue;
-        }
-        if (kind == EPI_NONE) continue;
-        epi.transform(col, v);
-        if (f32out) {
-          if (lane == 0) bulk_wait_read0();
-          __syncwarp();
-#pragma unroll
-          for (int g = 0; g < 8; ++g)
-            st_shared_v4(stg + lane * 128 + ((g ^ swz) << 4), __float_as_uint(v[4 * g]),
-                         __float_as_uint(v[4 * g + 1]), __float_as_uint(v[4 * g + 2]),
-                         __float_as_uint(v[4 * g + 3]));
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            if (kind == EPI_ACCUM_F32) tma_reduce_add_2d(omap, staging + ew * TC_STG_BYTES, col, row0);
-            else tma_store_2d(omap, staging + ew * TC_STG_BYTES, col, row0);
-            bulk_commit();
+        for (int c = 0; c < n_act; ++c) {
+          float v[32];
+          tmem_ld32(taddr + c * 32, v);
+          const int col = col_h + c * 32;
+          if (kind == EPI_LSE) {
+            if (row_ok) epi.chunk(col, v);
+            continue;
           }
-        } else {
-          if ((c & 1) == 0) {
+          if (kind == EPI_NONE) continue;
+          epi.transform(col, v);
+          if (kind == EPI_ADD_BF16 && row_ok) {
+            const float4* ad = reinterpret_cast<const float4*>(pr.epi.addend +
+                                                               (long long)rowg * pr.epi.add_ld + col);
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              const float4 a4 = ad[g];
+              v[4 * g] += a4.x;
+              v[4 * g + 1] += a4.y;
+              v[4 * g + 2] += a4.z;
+              v[4 * g + 3] += a4.w;
+            }
+          }
+          if (f32out) {
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
-          }
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            uint32_t w[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * g + 2 * e], v[8 * g + 2 * e + 1]);
-              w[e] = *reinterpret_cast<uint32_t*>(&h2);
-            }
-            const uint32_t gi = (c & 1) * 4 + g;
-            st_shared_v4(stg + lane * 128 + ((gi ^ swz) << 4), w[0], w[1], w[2], w[3]);
-          }
-          if ((c & 1) == 1 || c == n_act - 1) {
+            for (int g = 0; g < 8; ++g)
+              st_shared_v4(stg + lane * 128 + ((g ^ swz) << 4), __float_as_uint(v[4 * g]),
+                           __float_as_uint(v[4 * g + 1]), __float_as_uint(v[4 * g + 2]),
+                           __float_as_uint(v[4 * g + 3]));
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(omap, staging + ew * TC_STG_BYTES, col_h + (c & ~1) * 32, row0);
+              if (kind == EPI_ACCUM_F32)
+                tma_reduce_add_3d(omap, staging + ew * TC_STG_BYTES, col, row0, tl.b);
+              else
+                tma_store_3d(omap, staging + ew * TC_STG_BYTES, col, row0, tl.b);
               bulk_commit();
+            }
+          } else {
+            if ((c & 1) == 0) {
+              if (lane == 0) bulk_wait_read0();
+              __syncwarp();
+            }
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              uint32_t w[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * g + 2 * e], v[8 * g + 2 * e + 1]);
+                w[e] = *reinterpret_cast<uint32_t*>(&h2);
+              }
+              const uint32_t gi = (c & 1) * 4 + g;
+              st_shared_v4(stg + lane * 128 + ((gi ^ swz) << 4), w[0], w[1], w[2], w[3]);
+            }
+            if ((c & 1) == 1 || c == n_act - 1) {
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_3d(omap, staging + ew * TC_STG_BYTES, col_h + (c & ~1) * 32, row0, tl.b);
+                bulk_commit();
+              }
             }
           }
         }
+        if (kind == EPI_LSE && row_ok) epi.finish(tl.tn * 2 + h);
       }
-      if (kind == EPI_LSE && row_ok) epi.finish(tl.tn * 2 + h);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
