@@ -12,6 +12,11 @@ cfg = CONFIGS[name]
 t0 = time.time()
 inp = make_inputs(cfg)
 print(f"inputs {time.time()-t0:.1f}s", flush=True)
+if os.environ.get("ATTN_VC"):
+    binding.attn_softmax_set_option("vocab_chunk", int(os.environ["ATTN_VC"]))
+if os.environ.get("ATTN_CTAS"):
+    binding.attn_softmax_set_option("gemm_ctas", int(os.environ["ATTN_CTAS"]))
+binding.attn_softmax_set_option("stage_events", 1)
 st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
 dv = to_device(inp, cfg.dtype)
 scale = 1.0 / global_valid_tokens(cfg, cfg.B)
@@ -31,4 +36,6 @@ torch.cuda.synchronize()
 ms = ev[0].elapsed_time(ev[1]) / n
 tok = int(inp["tgt_len"].sum())
 flops = tok * (6 * cfg.d * cfg.V + 12 * cfg.d * cfg.d + 12 * cfg.M * cfg.d)
+st(*args, out=out)
+print({k: round(v, 4) for k, v in binding.attn_softmax_stage_times().items()})
 print(f"{name}: {ms:.3f} ms/step, {tok/ms*1e3:.0f} tok/s, useful {flops/ms/1e9:.1f} TFLOP/s")
