@@ -104,6 +104,7 @@ extern "C" long long attn_softmax_last_launches(void) { return g_launches; }
 // debug_epilogue option: 0 = fp32 TMA store, 1 = accumulator read only (no store)
 static int g_debug_epi = 0;
 static int g_opt_mn3d = 1;  // MN-major operands via one 3D TMA box
+static int g_opt_pair = 1;
 static int64_t g_opt_vocab_chunk = 0;
 static int64_t g_opt_gemm_ctas = 0;
 
@@ -114,6 +115,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
       return fail(ATTN_ERR_INVALID_ARG, "vocab_chunk must be a non-negative multiple of 256 (got %lld)",
                   (long long)value);
     g_opt_vocab_chunk = value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "cta_pair")) {
+    g_opt_pair = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "mn_3d_tma")) {
@@ -240,10 +245,12 @@ static attn_status_t operand_map(CUtensorMap* m, const Operand& o, bool mn, int 
   return encode(m, o.p, false, 3, dims, st, box);
 }
 
-static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr, int tile_begin) {
+static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr, int tile_begin,
+                             int pair) {
   memset(&pr, 0, sizeof(pr));
+  const int tile_m = TC_BM * pair, b_rows = TC_BN / pair;
   pr.M = g.M; pr.N = g.N; pr.K = g.K; pr.batch = g.batch;
-  pr.tiles_m = (g.M + TC_BM - 1) / TC_BM;
+  pr.tiles_m = (g.M + tile_m - 1) / tile_m;
   pr.tiles_n = (g.N + TC_BN - 1) / TC_BN;
   pr.kseg = g.kseg;
   pr.kb_total = g.kseg > 0 ? g.kseg + (int)((g.a1.k_ext + TC_BK - 1) / TC_BK)
@@ -264,26 +271,26 @@ static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr
     maps[1] = maps[0];
   }
   pr.a_mode = mode0;
-  if ((st = operand_map(&maps[2], g.b0, g.b_mn, TC_BN, g.batch, &mode0)) != ATTN_OK) return st;
+  if ((st = operand_map(&maps[2], g.b0, g.b_mn, b_rows, g.batch, &mode0)) != ATTN_OK) return st;
   if (g.b_seg || g.b_nsplit) {
-    if ((st = operand_map(&maps[3], g.b1, g.b_mn, TC_BN, g.batch, &mode1)) != ATTN_OK) return st;
+    if ((st = operand_map(&maps[3], g.b1, g.b_mn, b_rows, g.batch, &mode1)) != ATTN_OK) return st;
     if (mode1 != mode0) {
       // keep both halves on the per-atom path
       int m2;
       const int save = g_opt_mn3d;
       g_opt_mn3d = 0;
-      st = operand_map(&maps[2], g.b0, g.b_mn, TC_BN, g.batch, &m2);
-      if (st == ATTN_OK) st = operand_map(&maps[3], g.b1, g.b_mn, TC_BN, g.batch, &m2);
+      st = operand_map(&maps[2], g.b0, g.b_mn, b_rows, g.batch, &m2);
+      if (st == ATTN_OK) st = operand_map(&maps[3], g.b1, g.b_mn, b_rows, g.batch, &m2);
       g_opt_mn3d = save;
       if (st != ATTN_OK) return st;
       mode0 = m2;
     }
-    if (g.b_nsplit && mode0 == 1 && g.b_nsplit % TC_BN != 0) {
+    if (g.b_nsplit && mode0 == 1 && g.b_nsplit % b_rows != 0) {
       int m2;
       const int save = g_opt_mn3d;
       g_opt_mn3d = 0;
-      st = operand_map(&maps[2], g.b0, g.b_mn, TC_BN, g.batch, &m2);
-      if (st == ATTN_OK) st = operand_map(&maps[3], g.b1, g.b_mn, TC_BN, g.batch, &m2);
+      st = operand_map(&maps[2], g.b0, g.b_mn, b_rows, g.batch, &m2);
+      if (st == ATTN_OK) st = operand_map(&maps[3], g.b1, g.b_mn, b_rows, g.batch, &m2);
       g_opt_mn3d = save;
       if (st != ATTN_OK) return st;
       mode0 = m2;
@@ -331,11 +338,13 @@ static void fill_simt(const GemmDesc& g, SimtProblem& pr, int tile_begin) {
 
 static int tc_smem_bytes() { return TC_SMEM_BYTES; }
 
-template <typename OutT>
-static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cudaStream_t stream) {
+// g_opt_pair: vocab / projection GEMMs on CTA pairs (cta_group::2)
+
+template <typename OutT, int kPair>
+static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
-    CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<OutT, true>,
+    CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<OutT, true, kPair>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes()));
     attr_set = true;
   }
@@ -343,7 +352,7 @@ static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cu
   memset(&P, 0, sizeof(P));
   int tiles = 0;
   for (int i = 0; i < n; ++i) {
-    attn_status_t st = fill_tc(gs[i], P.maps[i], P.prob[i], tiles);
+    attn_status_t st = fill_tc(gs[i], P.maps[i], P.prob[i], tiles, kPair);
     if (st != ATTN_OK) return st;
     tiles += P.prob[i].tiles_m * P.prob[i].tiles_n * P.prob[i].batch;
   }
@@ -352,12 +361,32 @@ static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cu
   P.tile_counter = counter;
   if (tiles == 0) return ATTN_OK;
   const DevInfo di = dev_info();
-  int grid = g_opt_gemm_ctas > 0 ? (int)g_opt_gemm_ctas : di.sms;
-  grid = std::min(grid, tiles);
-  gemm_tc_kernel<OutT, true><<<grid, TC_THREADS, tc_smem_bytes(), stream>>>(P);
-  CUDA_TRY(cudaGetLastError());
+  int units = (g_opt_gemm_ctas > 0 ? (int)g_opt_gemm_ctas : di.sms) / kPair;
+  units = std::max(1, std::min(units, tiles));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(units * kPair);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = tc_smem_bytes();
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kPair;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = kPair == 2 ? 1 : 0;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<OutT, true, kPair>, P));
   ++g_launches;
   return ATTN_OK;
+}
+
+// pair = 2 puts the group on CTA pairs; batched (attention) groups stay on
+// single CTAs (a sentence has <= 128 decoder rows).
+template <typename OutT>
+static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cudaStream_t stream,
+                                     int pair = 1) {
+  if (pair == 2 && g_opt_pair) return launch_tc_group_k<OutT, 2>(gs, n, counter, stream);
+  return launch_tc_group_k<OutT, 1>(gs, n, counter, stream);
 }
 
 static attn_status_t launch_simt_group(const GemmDesc* gs, int n, cudaStream_t stream) {
@@ -836,7 +865,7 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   const bool tc = p.bf16;
   CounterCtx cctx{&b, 0};
   auto gemm = [&](const GemmDesc* gs, int n) -> attn_status_t {
-    if (tc) return launch_tc_group<__nv_bfloat16>(gs, n, next_counter_fn(&cctx), stream);
+    if (tc) return launch_tc_group<__nv_bfloat16>(gs, n, next_counter_fn(&cctx), stream, 2);
     return launch_simt_group(gs, n, stream);
   };
   const int d = p.d;
@@ -1052,6 +1081,6 @@ extern "C" attn_status_t attn_debug_gemm_bf16(int M, int N, int K, const void* A
   if (!counter) CUDA_TRY(cudaMalloc(&counter, sizeof(int)));
   cudaStream_t stream = (cudaStream_t)stream_;
   CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int), stream));
-  attn_status_t st = launch_tc_group<__nv_bfloat16>(&g, 1, counter, stream);
+  attn_status_t st = launch_tc_group<__nv_bfloat16>(&g, 1, counter, stream, 2);
   return st;
 }

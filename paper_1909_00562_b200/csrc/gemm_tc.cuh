@@ -33,20 +33,32 @@
 
 namespace attnsm {
 
-constexpr int TC_BM = 128;
-constexpr int TC_BN = 256;
+constexpr int TC_BM = 128;    // accumulator rows per CTA (TMEM lanes)
+constexpr int TC_BN = 256;    // tile columns
 constexpr int TC_BK = 64;
-constexpr int TC_STAGES = 4;
 constexpr int TC_THREADS = 384;
 constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_STG_BYTES = 4096;                        // per epilogue warp
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;             // 16 KB
-constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;             // 32 KB
-constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;   // 48 KB
+constexpr int TC_RING_BYTES = 192 * 1024;                 // operand ring
 constexpr int TC_SCHED = 4;
 constexpr int TC_SMEM_BYTES =
-    TC_STAGES * TC_STAGE_BYTES + TC_EPI_WARPS * TC_STG_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+    TC_RING_BYTES + TC_EPI_WARPS * TC_STG_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 constexpr int kMaxProblems = 4;
+
+// kPair = 1: one CTA computes a 128 x 256 tile (tcgen05 cta_group::1).
+// kPair = 2: a CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile
+// with cta_group::2: each CTA stages its 128 rows of A and 128 rows of B, so
+// a stage is 32 KB instead of 48 KB (6 stages instead of 4) and the operand
+// traffic per FLOP through shared memory and L2 drops by a third.
+template <int kPair>
+struct TcCfg {
+  static constexpr int TILE_M = TC_BM * kPair;
+  static constexpr int B_ROWS = TC_BN / kPair;                 // B rows staged per CTA
+  static constexpr int B_BYTES = B_ROWS * TC_BK * 2;
+  static constexpr int STAGE = TC_A_BYTES + B_BYTES;           // 48 KB | 32 KB
+  static constexpr int STAGES = TC_RING_BYTES / STAGE;         // 4 | 6
+};
 
 struct TcProblem {
   int M, N, K;      // per batch item
@@ -82,6 +94,7 @@ struct TcTile {
   int p, b, m0, n0, tn;
 };
 
+template <int kPair>
 __device__ __forceinline__ TcTile tc_decode(const TcParams& P, int t) {
   TcTile r;
   r.p = tc_find_problem(P, t);
@@ -92,20 +105,35 @@ __device__ __forceinline__ TcTile tc_decode(const TcParams& P, int t) {
   local -= r.b * per_b;
   const int tm = local % pr.tiles_m;
   r.tn = local / pr.tiles_m;
-  r.m0 = tm * TC_BM;
+  r.m0 = tm * TcCfg<kPair>::TILE_M;
   r.n0 = r.tn * TC_BN;
   return r;
 }
 
+// TMA load issue: single CTA (local barrier) or pair (leader's barrier).
+template <int kPair>
+__device__ __forceinline__ void tl3(void* dst, const CUtensorMap* m, uint64_t* bar, uint32_t barc,
+                                    int c0, int c1, int c2) {
+  if constexpr (kPair == 2) tma_load_3d_pair(dst, m, barc, c0, c1, c2);
+  else tma_load_3d(dst, m, bar, c0, c1, c2);
+}
+template <int kPair>
+__device__ __forceinline__ void tl4(void* dst, const CUtensorMap* m, uint64_t* bar, uint32_t barc,
+                                    int c0, int c1, int c2, int c3) {
+  if constexpr (kPair == 2) tma_load_4d_pair(dst, m, barc, c0, c1, c2, c3);
+  else tma_load_4d(dst, m, bar, c0, c1, c2, c3);
+}
 // Load one operand tile (rows x 64 K) of k-block kb into smem.
+template <int kPair>
 __device__ __forceinline__ void tc_load_operand(uint8_t* dst, const CUtensorMap* m, uint64_t* bar,
-                                                int mode, int rows, int r0, int k0, int b) {
+                                                uint32_t barc, int mode, int rows, int r0, int k0,
+                                                int b) {
   if (mode == 0) {
-    tma_load_3d(dst, m, bar, k0, r0, b);
+    tl3<kPair>(dst, m, bar, barc, k0, r0, b);
   } else if (mode == 1) {
-    tma_load_4d(dst, m, bar, 0, k0, r0 / 64, b);
+    tl4<kPair>(dst, m, bar, barc, 0, k0, r0 / 64, b);
   } else {
-    for (int i = 0; i < rows / 64; ++i) tma_load_3d(dst + i * 8192, m, bar, r0 + 64 * i, k0, b);
+    for (int i = 0; i < rows / 64; ++i) tl3<kPair>(dst + i * 8192, m, bar, barc, r0 + 64 * i, k0, b);
   }
 }
 
@@ -176,16 +204,17 @@ __device__ __forceinline__ void epi_attn_softmax_bwd(const EpiParams& e, uint32_
   }
 }
 
-template <typename OutT, bool kFast>
+template <typename OutT, bool kFast, int kPair>
 __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_constant__ TcParams P) {
+  using Cfg = TcCfg<kPair>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* staging = smem + TC_STAGES * TC_STAGE_BYTES;
+  uint8_t* staging = smem + TC_RING_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(staging + TC_EPI_WARPS * TC_STG_BYTES);
   uint64_t* full = bars;                       // [STAGES]
-  uint64_t* empty = full + TC_STAGES;          // [STAGES]
-  uint64_t* tfull = empty + TC_STAGES;         // [2]
+  uint64_t* empty = full + Cfg::STAGES;        // [STAGES]
+  uint64_t* tfull = empty + Cfg::STAGES;       // [2]
   uint64_t* tempty = tfull + 2;                // [2]
   uint64_t* sfull = tempty + 2;                // [SCHED]
   uint64_t* sempty = sfull + TC_SCHED;         // [SCHED]
@@ -194,89 +223,115 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
 
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();
+  const uint32_t rank = (kPair == 2) ? cluster_ctarank() : 0;   // 0 = pair leader
+  const bool leader = rank == 0;
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < TC_STAGES; ++i) {
+    for (int i = 0; i < Cfg::STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], TC_EPI_WARPS);
+      mbar_init(&tempty[i], TC_EPI_WARPS * kPair);
     }
     for (int i = 0; i < TC_SCHED; ++i) {
       mbar_init(&sfull[i], 1);
-      mbar_init(&sempty[i], 1 + TC_EPI_WARPS);
+      // leader: its MMA + epilogue warps (+ the peer's producer and epilogue warps)
+      mbar_init(&sempty[i], 1 + TC_EPI_WARPS + (kPair == 2 ? 1 + TC_EPI_WARPS : 0));
     }
     fence_barrier_init();
     for (int p = 0; p < P.nprob; ++p)
       for (int j = 0; j < 5; ++j) tma_prefetch_desc(&P.maps[p][j]);
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (warp == 2) {
+    if constexpr (kPair == 2) tmem_alloc_pair(tmem_slot, 512);
+    else tmem_alloc(tmem_slot, 512);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // shared::cluster addresses of the leader's barriers (pair mode)
+  auto leader_addr = [&](void* p) -> uint32_t { return mapa_shared(smem_u32(p), 0); };
+
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- tile scheduler + TMA producer
+      // ---------------- tile scheduler (leader) + TMA producer (both CTAs)
       int s = 0;
       uint32_t ph = 0;
       int r = 0;
       uint32_t rph = 0;
       // the next tile index is fetched one tile ahead so the global atomic's
       // latency overlaps the current tile's loads
-      int t_next = atomicAdd(P.tile_counter, 1);
+      int t_next = leader ? atomicAdd(P.tile_counter, 1) : 0;
       for (;;) {
-        int t = t_next;
-        if (t >= P.total_tiles) t = -1;
-        else t_next = atomicAdd(P.tile_counter, 1);
-        mbar_wait(&sempty[r], rph ^ 1);
-        sched_tile[r] = t;
-        mbar_arrive(&sfull[r]);
+        int t;
+        if (leader) {
+          t = t_next;
+          if (t >= P.total_tiles) t = -1;
+          else t_next = atomicAdd(P.tile_counter, 1);
+          mbar_wait(&sempty[r], rph ^ 1);
+          sched_tile[r] = t;
+          if constexpr (kPair == 2) {
+            st_shared_cluster_u32(mapa_shared(smem_u32(&sched_tile[r]), 1), (uint32_t)t);
+            mbar_arrive_cluster(mapa_shared(smem_u32(&sfull[r]), 1));
+          }
+          mbar_arrive(&sfull[r]);
+        } else {
+          mbar_wait_cluster(&sfull[r], rph);
+          t = sched_tile[r];
+          mbar_arrive_cluster(leader_addr(&sempty[r]));
+        }
         if (++r == TC_SCHED) { r = 0; rph ^= 1; }
         if (t < 0) break;
-        const TcTile tl = tc_decode(P, t);
+        const TcTile tl = tc_decode<kPair>(P, t);
         const TcProblem& pr = P.prob[tl.p];
         const CUtensorMap* ma0 = &P.maps[tl.p][0];
         const CUtensorMap* ma1 = &P.maps[tl.p][1];
         const CUtensorMap* mb0 = &P.maps[tl.p][2];
         const CUtensorMap* mb1 = &P.maps[tl.p][3];
+        const int am0 = tl.m0 + TC_BM * rank;               // this CTA's A rows
+        const int bn0 = tl.n0 + Cfg::B_ROWS * rank;         // this CTA's B rows
         for (int kb = 0; kb < pr.kb_total; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* sA = smem + s * TC_STAGE_BYTES;
+          uint8_t* sA = smem + s * Cfg::STAGE;
           uint8_t* sB = sA + TC_A_BYTES;
-          mbar_arrive_expect_tx(&full[s], TC_STAGE_BYTES);
+          uint32_t barc = 0;
+          if constexpr (kPair == 2) barc = leader_addr(&full[s]);
+          if (leader) mbar_arrive_expect_tx(&full[s], Cfg::STAGE * kPair);
           const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
           const int ka = (seg1 ? kb - pr.kseg : kb) * TC_BK;
-          tc_load_operand(sA, seg1 ? ma1 : ma0, &full[s], pr.a_mode, TC_BM, tl.m0, ka, tl.b);
+          tc_load_operand<kPair>(sA, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode, TC_BM, am0, ka,
+                                 tl.b);
           const bool bseg1 = seg1 && pr.b_seg;
           const int kbk = (bseg1 ? kb - pr.kseg : kb) * TC_BK + pr.b_koff;
           const CUtensorMap* mb = bseg1 ? mb1 : mb0;
           if (pr.b_nsplit > 0 && pr.b_mode == 1) {
-            if (tl.n0 >= pr.b_nsplit)
-              tma_load_4d(sB, mb1, &full[s], 0, kbk, (tl.n0 - pr.b_nsplit) / 64, tl.b);
+            if (bn0 >= pr.b_nsplit)
+              tl4<kPair>(sB, mb1, &full[s], barc, 0, kbk, (bn0 - pr.b_nsplit) / 64, tl.b);
             else
-              tma_load_4d(sB, mb0, &full[s], 0, kbk, tl.n0 / 64, tl.b);
+              tl4<kPair>(sB, mb0, &full[s], barc, 0, kbk, bn0 / 64, tl.b);
           } else if (pr.b_nsplit > 0) {
-            for (int i = 0; i < TC_BN / 64; ++i) {
-              const int n = tl.n0 + 64 * i;
+            for (int i = 0; i < Cfg::B_ROWS / 64; ++i) {
+              const int n = bn0 + 64 * i;
               if (n >= pr.b_nsplit)
-                tma_load_3d(sB + i * 8192, mb1, &full[s], n - pr.b_nsplit, kbk, tl.b);
+                tl3<kPair>(sB + i * 8192, mb1, &full[s], barc, n - pr.b_nsplit, kbk, tl.b);
               else
-                tma_load_3d(sB + i * 8192, mb0, &full[s], n, kbk, tl.b);
+                tl3<kPair>(sB + i * 8192, mb0, &full[s], barc, n, kbk, tl.b);
             }
           } else {
-            tc_load_operand(sB, mb, &full[s], pr.b_mode, TC_BN, tl.n0, kbk, tl.b);
+            tc_load_operand<kPair>(sB, mb, &full[s], barc, pr.b_mode, Cfg::B_ROWS, bn0, kbk, tl.b);
           }
-          if (++s == TC_STAGES) { s = 0; ph ^= 1; }
+          if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (pair leader only)
       int s = 0;
       uint32_t ph = 0;
       int r = 0;
@@ -289,9 +344,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         mbar_arrive(&sempty[r]);
         if (++r == TC_SCHED) { r = 0; rph ^= 1; }
         if (t < 0) break;
-        const TcTile tl = tc_decode(P, t);
+        const TcTile tl = tc_decode<kPair>(P, t);
         const TcProblem& pr = P.prob[tl.p];
-        const uint32_t idesc = umma_idesc_bf16(TC_BM, TC_BN, pr.a_mn, pr.b_mn);
+        const uint32_t idesc = umma_idesc_bf16(Cfg::TILE_M, TC_BN, pr.a_mn, pr.b_mn);
         const uint32_t a_lbo = pr.a_mn ? 8192u : 16u;
         const uint32_t b_lbo = pr.b_mn ? 8192u : 16u;
         const uint32_t a_kstep = pr.a_mn ? 2048u : 32u;
@@ -302,18 +357,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         for (int kb = 0; kb < pr.kb_total; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint32_t sA = smem_u32(smem + s * TC_STAGE_BYTES);
+          const uint32_t sA = smem_u32(smem + s * Cfg::STAGE);
           const uint32_t sB = sA + TC_A_BYTES;
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k) {
             const uint64_t ad = umma_sdesc(sA + k * a_kstep, a_lbo, 1024);
             const uint64_t bd = umma_sdesc(sB + k * b_kstep, b_lbo, 1024);
-            umma_bf16(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            if constexpr (kPair == 2) umma_bf16_pair(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            else umma_bf16(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
           }
-          umma_commit(&empty[s]);
-          if (++s == TC_STAGES) { s = 0; ph ^= 1; }
+          if constexpr (kPair == 2) umma_commit_pair(&empty[s]);
+          else umma_commit(&empty[s]);
+          if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
-        umma_commit(&tfull[acc]);
+        if constexpr (kPair == 2) umma_commit_pair(&tfull[acc]);
+        else umma_commit(&tfull[acc]);
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
     }
@@ -329,19 +387,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     int acc = 0;
     uint32_t aph = 0;
     for (;;) {
-      mbar_wait(&sfull[r], rph);
+      if (kPair == 2 && !leader) mbar_wait_cluster(&sfull[r], rph);
+      else mbar_wait(&sfull[r], rph);
       const int t = sched_tile[r];
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sempty[r]);
+      if (lane == 0) {
+        if (kPair == 2 && !leader) mbar_arrive_cluster(leader_addr(&sempty[r]));
+        else mbar_arrive(&sempty[r]);
+      }
       if (++r == TC_SCHED) { r = 0; rph ^= 1; }
       if (t < 0) break;
-      const TcTile tl = tc_decode(P, t);
+      const TcTile tl = tc_decode<kPair>(P, t);
       const TcProblem& pr = P.prob[tl.p];
       const int kind = pr.epi.kind;
       const CUtensorMap* omap = &P.maps[tl.p][4];
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int row0 = tl.m0 + q * 32;           // row inside the batch item
+      const int row0 = tl.m0 + TC_BM * rank + q * 32;   // row inside the batch item
       const int row = row0 + lane;
       const bool row_ok = row < pr.M;
       const int rowg = tl.b * pr.M + (row_ok ? row : 0);   // row of the flattened [batch*M] arrays
@@ -427,15 +489,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (kPair == 2 && !leader) mbar_arrive_cluster(leader_addr(&tempty[acc]));
+        else mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
     if (lane == 0) bulk_wait0();
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem_base, 512);
+  if (warp == 2) {
+    if constexpr (kPair == 2) tmem_dealloc_pair(tmem_base, 512);
+    else tmem_dealloc(tmem_base, 512);
+  }
 }
 
 }  // namespace attnsm

@@ -47,15 +47,18 @@ def oracle(inp, scale):
 
 
 # ------------------------------------------------------------ GEMM core ----
+@pytest.mark.parametrize("pair", [1, 2])
 @pytest.mark.parametrize("mn3d", [0, 1])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 0), (0, 1), (1, 1)])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (296, 520, 200), (1000, 264, 1536),
                                    (320, 640, 192)])
-def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d):
-    """The tcgen05 engine alone, all operand majors (MN-major via 2D atom
-    boxes or one 3D box), with M/N/K tails."""
+def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, pair):
+    """The tcgen05 engine alone: single CTA (cta_group::1, 128x256 tiles) and
+    CTA pair (cta_group::2, 256x256), all operand majors (MN-major via per-atom
+    boxes or one box per stage), with M/N/K tails."""
     from paper_1909_00562_b200 import binding
     binding.attn_softmax_set_option("mn_3d_tma", mn3d)
+    binding.attn_softmax_set_option("cta_pair", 1 if pair == 2 else 0)
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N + K)
     A = torch.randn(M, K, generator=g).bfloat16()
     B = torch.randn(N, K, generator=g).bfloat16()
@@ -66,6 +69,7 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d):
     binding.attn_debug_gemm_bf16(M, N, K, Ad, a_mn, Bd, b_mn, C)
     torch.cuda.synchronize()
     binding.attn_softmax_set_option("mn_3d_tma", 1)
+    binding.attn_softmax_set_option("cta_pair", 1)
     err = (C.double().cpu() - ref).abs().max().item()
     assert err < 1e-3 * max(1.0, ref.abs().max().item()), err
 
