@@ -101,10 +101,12 @@ extern "C" attn_status_t attn_softmax_stage_time(int i, const char** name, float
 extern "C" long long attn_softmax_last_launches(void) { return g_launches; }
 
 // ------------------------------------------------------------------ options
+// cta_pair option: bitmask of GEMM groups run on CTA pairs (see PAIR_*)
+#define PAIR_DEFAULT (2 | 4 | 8)
 // debug_epilogue option: 0 = fp32 TMA store, 1 = accumulator read only (no store)
 static int g_debug_epi = 0;
 static int g_opt_mn3d = 1;  // MN-major operands via one 3D TMA box
-static int g_opt_pair = 1;
+static int g_opt_pair = PAIR_DEFAULT;
 static int64_t g_opt_vocab_chunk = 0;
 static int64_t g_opt_gemm_ctas = 0;
 
@@ -382,10 +384,13 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
 
 // pair = 2 puts the group on CTA pairs; batched (attention) groups stay on
 // single CTAs (a sentence has <= 128 decoder rows).
+// `group_bit` selects the bit of the "cta_pair" option that enables pairs for
+// this GEMM group (0 = never paired).
+enum : int { PAIR_FWD = 1, PAIR_VBWD = 2, PAIR_PBWD = 4, PAIR_DEBUG = 8 };
 template <typename OutT>
 static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cudaStream_t stream,
-                                     int pair = 1) {
-  if (pair == 2 && g_opt_pair) return launch_tc_group_k<OutT, 2>(gs, n, counter, stream);
+                                     int group_bit = 0) {
+  if (group_bit && (g_opt_pair & group_bit)) return launch_tc_group_k<OutT, 2>(gs, n, counter, stream);
   return launch_tc_group_k<OutT, 1>(gs, n, counter, stream);
 }
 
@@ -864,8 +869,8 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   attn_status_t st;
   const bool tc = p.bf16;
   CounterCtx cctx{&b, 0};
-  auto gemm = [&](const GemmDesc* gs, int n) -> attn_status_t {
-    if (tc) return launch_tc_group<__nv_bfloat16>(gs, n, next_counter_fn(&cctx), stream, 2);
+  auto gemm = [&](const GemmDesc* gs, int n, int pair_bit) -> attn_status_t {
+    if (tc) return launch_tc_group<__nv_bfloat16>(gs, n, next_counter_fn(&cctx), stream, pair_bit);
     return launch_simt_group(gs, n, stream);
   };
   const int d = p.d;
@@ -886,13 +891,13 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   // ---- F3 (Eq. 4)
   {
     GemmDesc g = g_proj(p, H, b.ctx, W_c, b.hc);
-    if ((st = gemm(&g, 1)) != ATTN_OK) return st;
+    if ((st = gemm(&g, 1, PAIR_FWD)) != ATTN_OK) return st;
   }
   prof_mark("proj_tanh", stream);
   // ---- F4 (Eq. 5): logits discarded, per-tile (max, sumexp) kept
   {
     GemmDesc g = g_vocab_fwd(p, b, W_out, tgt_ids);
-    if ((st = gemm(&g, 1)) != ATTN_OK) return st;
+    if ((st = gemm(&g, 1, PAIR_FWD)) != ATTN_OK) return st;
   }
   prof_mark("vocab_fwd", stream);
   // ---- Eq. 6: lse, token NLL, row scale, loss
@@ -914,14 +919,14 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   // for chunk c together with the dlogits of chunk c+1 (double-buffered).
   {
     GemmDesc g0 = g_dlogits(p, b, W_out, tgt_ids, 0);
-    if ((st = gemm(&g0, 1)) != ATTN_OK) return st;
+    if ((st = gemm(&g0, 1, PAIR_VBWD)) != ATTN_OK) return st;
     for (int c = 0; c < p.nchunks; ++c) {
       GemmDesc gs[3];
       int n = 0;
       gs[n++] = g_dwout(p, b, dW_out, c);   // K = T: the long tiles first
       gs[n++] = g_dhc(p, b, W_out, c);
       if (c + 1 < p.nchunks) gs[n++] = g_dlogits(p, b, W_out, tgt_ids, c + 1);
-      if ((st = gemm(gs, n)) != ATTN_OK) return st;
+      if ((st = gemm(gs, n, PAIR_VBWD)) != ATTN_OK) return st;
       if (comm) {
         const int c0 = c * p.Vc;
         const int vcc = std::min(p.Vc, p.V - c0);
@@ -951,7 +956,7 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
     } else {
       gs[n++] = g_dzwc(p, b, W_c, 0, 2 * d, EPI_STORE_F32, b.dhc2, 2ll * d);
     }
-    if ((st = gemm(gs, n)) != ATTN_OK) return st;
+    if ((st = gemm(gs, n, PAIR_PBWD)) != ATTN_OK) return st;
     if (comm) {
       if ((st = comm_enqueue_allreduce(comm, &cr, stream, dW_c, (size_t)d * 2 * d)) != ATTN_OK) return st;
     }
@@ -1081,6 +1086,6 @@ extern "C" attn_status_t attn_debug_gemm_bf16(int M, int N, int K, const void* A
   if (!counter) CUDA_TRY(cudaMalloc(&counter, sizeof(int)));
   cudaStream_t stream = (cudaStream_t)stream_;
   CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int), stream));
-  attn_status_t st = launch_tc_group<__nv_bfloat16>(&g, 1, counter, stream, 2);
+  attn_status_t st = launch_tc_group<__nv_bfloat16>(&g, 1, counter, stream, PAIR_DEBUG);
   return st;
 }

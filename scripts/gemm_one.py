@@ -7,7 +7,7 @@ from paper_1909_00562_b200 import binding
 M, N, K, amn, bmn = (int(x) for x in sys.argv[1:6])
 pair = int(sys.argv[6]) if len(sys.argv) > 6 else 2
 epi = int(sys.argv[7]) if len(sys.argv) > 7 else 0
-binding.attn_softmax_set_option("cta_pair", 1 if pair == 2 else 0)
+binding.attn_softmax_set_option("cta_pair", 8 if pair == 2 else 0)
 binding.attn_softmax_set_option("debug_epilogue", epi)
 A = torch.randn(K, M, device="cuda").bfloat16() if amn else torch.randn(M, K, device="cuda").bfloat16()
 B = torch.randn(K, N, device="cuda").bfloat16() if bmn else torch.randn(N, K, device="cuda").bfloat16()

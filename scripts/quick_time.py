@@ -14,6 +14,8 @@ inp = make_inputs(cfg)
 print(f"inputs {time.time()-t0:.1f}s", flush=True)
 if os.environ.get("ATTN_VC"):
     binding.attn_softmax_set_option("vocab_chunk", int(os.environ["ATTN_VC"]))
+if os.environ.get("ATTN_PAIR"):
+    binding.attn_softmax_set_option("cta_pair", int(os.environ["ATTN_PAIR"]))
 if os.environ.get("ATTN_CTAS"):
     binding.attn_softmax_set_option("gemm_ctas", int(os.environ["ATTN_CTAS"]))
 binding.attn_softmax_set_option("stage_events", 1)

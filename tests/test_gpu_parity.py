@@ -58,7 +58,7 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, pair):
     boxes or one box per stage), with M/N/K tails."""
     from paper_1909_00562_b200 import binding
     binding.attn_softmax_set_option("mn_3d_tma", mn3d)
-    binding.attn_softmax_set_option("cta_pair", 1 if pair == 2 else 0)
+    binding.attn_softmax_set_option("cta_pair", 8 if pair == 2 else 0)
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N + K)
     A = torch.randn(M, K, generator=g).bfloat16()
     B = torch.randn(N, K, generator=g).bfloat16()
@@ -69,7 +69,7 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, pair):
     binding.attn_debug_gemm_bf16(M, N, K, Ad, a_mn, Bd, b_mn, C)
     torch.cuda.synchronize()
     binding.attn_softmax_set_option("mn_3d_tma", 1)
-    binding.attn_softmax_set_option("cta_pair", 1)
+    binding.attn_softmax_set_option("cta_pair", 14)
     err = (C.double().cpu() - ref).abs().max().item()
     assert err < 1e-3 * max(1.0, ref.abs().max().item()), err
 
