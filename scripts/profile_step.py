@@ -7,6 +7,9 @@ from paper_1909_00562_b200.stage import AttnSoftmaxStage, to_device
 from synthetic import CONFIGS, make_inputs, global_valid_tokens
 
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "paper"]
+for k, opt in (("ATTN_VC", "vocab_chunk"), ("ATTN_PAIR", "cta_pair"), ("ATTN_CTAS", "gemm_ctas")):
+    if os.environ.get(k):
+        binding.attn_softmax_set_option(opt, int(os.environ[k]))
 inp = make_inputs(cfg)
 st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
 dv = to_device(inp, cfg.dtype)
