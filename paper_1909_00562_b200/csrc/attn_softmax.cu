@@ -102,7 +102,7 @@ extern "C" long long attn_softmax_last_launches(void) { return g_launches; }
 
 // ------------------------------------------------------------------ options
 // cta_pair option: bitmask of GEMM groups run on CTA pairs (see PAIR_*)
-#define PAIR_DEFAULT (2 | 4 | 8)
+#define PAIR_DEFAULT 8   /* stage GEMMs on single CTAs (measured faster), debug entry paired */
 // debug_epilogue option: 0 = fp32 TMA store, 1 = accumulator read only (no store)
 static int g_debug_epi = 0;
 static int g_opt_mn3d = 1;  // MN-major operands via one 3D TMA box
@@ -480,7 +480,7 @@ static Plan make_plan(const attn_shape_t* s) {
   if (vc <= 0) {
     // dlogits chunk (T x Vc) sized to stay L2-resident next to H_c, dHc and
     // the W_out chunk
-    const long long budget = 28ll << 20;
+    const long long budget = 56ll << 20;
     vc = budget / (p.T * (long long)p.elt) / 256 * 256;
     vc = std::max(vc, 256ll);
   }
