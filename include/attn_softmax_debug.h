@@ -63,6 +63,7 @@ long long attn_softmax_last_launches(void);
  *                   (128 x 256): 1 = forward vocab / projection, 2 = vocab
  *                   backward chunks, 4 = projection backward, 8 = the debug
  *                   GEMM entry.  Default 8.
+ *   "gemm_variant"  debug experiment bits of the GEMM producer (0 = default)
  *   "mn_3d_tma"     1 (default) = load MN-major operand tiles with one 3D TMA
  *                   box per stage; 0 = one 2D box per 64-wide atom
  *   "debug_epilogue" attn_debug_gemm_bf16 epilogue: 0 = fp32 TMA store,

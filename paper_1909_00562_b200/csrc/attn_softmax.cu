@@ -107,6 +107,7 @@ extern "C" long long attn_softmax_last_launches(void) { return g_launches; }
 static int g_debug_epi = 0;
 static int g_opt_mn3d = 1;  // MN-major operands via one 3D TMA box
 static int g_opt_pair = PAIR_DEFAULT;
+static int g_opt_variant = 0;   // "gemm_variant": debug experiment bits
 static int64_t g_opt_vocab_chunk = 0;
 static int64_t g_opt_gemm_ctas = 0;
 
@@ -117,6 +118,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
       return fail(ATTN_ERR_INVALID_ARG, "vocab_chunk must be a non-negative multiple of 256 (got %lld)",
                   (long long)value);
     g_opt_vocab_chunk = value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "gemm_variant")) {
+    g_opt_variant = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "cta_pair")) {
@@ -221,13 +226,13 @@ struct GemmDesc {
 };
 
 static attn_status_t operand_map(CUtensorMap* m, const Operand& o, bool mn, int box_rows, int batch,
-                                 int* mode) {
+                                 int* mode, bool is_b = false) {
   const long long bs = batch > 1 ? o.bstride : (o.mn_ext + 1) * o.ld;
   if (!mn) {
     cuuint64_t dims[3] = {(cuuint64_t)std::max(1ll, o.k_ext), (cuuint64_t)std::max(1ll, o.mn_ext),
                           (cuuint64_t)batch};
     cuuint64_t st[2] = {(cuuint64_t)(o.ld * 2), (cuuint64_t)(bs * 2)};
-    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+    cuuint32_t box[3] = {64, (cuuint32_t)((is_b && (g_opt_variant & 1)) ? 64 : box_rows), 1};
     *mode = 0;
     return encode(m, o.p, false, 3, dims, st, box);
   }
@@ -273,9 +278,9 @@ static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr
     maps[1] = maps[0];
   }
   pr.a_mode = mode0;
-  if ((st = operand_map(&maps[2], g.b0, g.b_mn, b_rows, g.batch, &mode0)) != ATTN_OK) return st;
+  if ((st = operand_map(&maps[2], g.b0, g.b_mn, b_rows, g.batch, &mode0, true)) != ATTN_OK) return st;
   if (g.b_seg || g.b_nsplit) {
-    if ((st = operand_map(&maps[3], g.b1, g.b_mn, b_rows, g.batch, &mode1)) != ATTN_OK) return st;
+    if ((st = operand_map(&maps[3], g.b1, g.b_mn, b_rows, g.batch, &mode1, true)) != ATTN_OK) return st;
     if (mode1 != mode0) {
       // keep both halves on the per-atom path
       int m2;
@@ -361,6 +366,7 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   P.nprob = n;
   P.total_tiles = tiles;
   P.tile_counter = counter;
+  P.variant = g_opt_variant;
   if (tiles == 0) return ATTN_OK;
   const DevInfo di = dev_info();
   int units = (g_opt_gemm_ctas > 0 ? (int)g_opt_gemm_ctas : di.sms) / kPair;

@@ -80,6 +80,7 @@ struct alignas(64) TcParams {
   int nprob;
   int total_tiles;
   int* tile_counter;
+  int variant;   // debug experiment bits (0 = production path)
 };
 
 __device__ __forceinline__ int tc_find_problem(const TcParams& P, int t) {
@@ -304,8 +305,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           if (leader) mbar_arrive_expect_tx(&full[s], Cfg::STAGE * kPair);
           const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
           const int ka = (seg1 ? kb - pr.kseg : kb) * TC_BK;
-          tc_load_operand<kPair>(sA, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode, TC_BM, am0, ka,
-                                 tl.b);
+          if (!(P.variant & 2))
+            tc_load_operand<kPair>(sA, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode, TC_BM, am0, ka,
+                                   tl.b);
           const bool bseg1 = seg1 && pr.b_seg;
           const int kbk = (bseg1 ? kb - pr.kseg : kb) * TC_BK + pr.b_koff;
           const CUtensorMap* mb = bseg1 ? mb1 : mb0;
@@ -322,9 +324,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
               else
                 tl3<kPair>(sB + i * 8192, mb0, &full[s], barc, n, kbk, tl.b);
             }
+          } else if ((P.variant & 1) && pr.b_mode == 0) {
+            // experiment: K-major B as 64-row boxes (map box rows = 64)
+            for (int i = 0; i < Cfg::B_ROWS / 64; ++i)
+              tl3<kPair>(sB + i * 8192, mb, &full[s], barc, kbk, bn0 + 64 * i, tl.b);
           } else {
             tc_load_operand<kPair>(sB, mb, &full[s], barc, pr.b_mode, Cfg::B_ROWS, bn0, kbk, tl.b);
           }
+          if (P.variant & 2)
+            tc_load_operand<kPair>(sA, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode, TC_BM, am0, ka,
+                                   tl.b);
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
       }
