@@ -259,45 +259,54 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
   auto leader_addr = [&](void* p) -> uint32_t { return mapa_shared(smem_u32(p), 0); };
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- tile scheduler (leader) + TMA producer (both CTAs)
-      int s = 0;
-      uint32_t ph = 0;
-      int r = 0;
-      uint32_t rph = 0;
-      // the next tile index is fetched one tile ahead so the global atomic's
-      // latency overlaps the current tile's loads
-      int t_next = leader ? atomicAdd(P.tile_counter, 1) : 0;
-      for (;;) {
-        int t;
-        if (leader) {
-          t = t_next;
-          if (t >= P.total_tiles) t = -1;
-          else t_next = atomicAdd(P.tile_counter, 1);
-          mbar_wait(&sempty[r], rph ^ 1);
+    // ---------------- tile scheduler (leader) + TMA producer (both CTAs).
+    // The whole warp runs the loop (waits are per lane, values warp-uniform);
+    // one elected lane issues, so TMA operands live in uniform registers.
+    int s = 0;
+    uint32_t ph = 0;
+    int r = 0;
+    uint32_t rph = 0;
+    // the next tile index is fetched one tile ahead so the global atomic's
+    // latency overlaps the current tile's loads
+    int t_next = 0;
+    if (leader && lane == 0) t_next = atomicAdd(P.tile_counter, 1);
+    for (;;) {
+      int t;
+      if (leader) {
+        t = __shfl_sync(0xffffffffu, t_next, 0);
+        if (t >= P.total_tiles) t = -1;
+        else if (lane == 0) t_next = atomicAdd(P.tile_counter, 1);
+        mbar_wait(&sempty[r], rph ^ 1);
+        if (elect_one()) {
           sched_tile[r] = t;
           if constexpr (kPair == 2) {
             st_shared_cluster_u32(mapa_shared(smem_u32(&sched_tile[r]), 1), (uint32_t)t);
             mbar_arrive_cluster(mapa_shared(smem_u32(&sfull[r]), 1));
           }
           mbar_arrive(&sfull[r]);
-        } else {
-          mbar_wait_cluster(&sfull[r], rph);
-          t = sched_tile[r];
-          mbar_arrive_cluster(leader_addr(&sempty[r]));
         }
-        if (++r == TC_SCHED) { r = 0; rph ^= 1; }
-        if (t < 0) break;
-        const TcTile tl = tc_decode<kPair>(P, t);
-        const TcProblem& pr = P.prob[tl.p];
-        const CUtensorMap* ma0 = &P.maps[tl.p][0];
-        const CUtensorMap* ma1 = &P.maps[tl.p][1];
-        const CUtensorMap* mb0 = &P.maps[tl.p][2];
-        const CUtensorMap* mb1 = &P.maps[tl.p][3];
-        const int am0 = tl.m0 + TC_BM * rank;               // this CTA's A rows
-        const int bn0 = tl.n0 + Cfg::B_ROWS * rank;         // this CTA's B rows
-        for (int kb = 0; kb < pr.kb_total; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
+        __syncwarp();
+      } else {
+        mbar_wait_cluster(&sfull[r], rph);
+        t = sched_tile[r];
+        __syncwarp();
+        if (elect_one()) mbar_arrive_cluster(leader_addr(&sempty[r]));
+        __syncwarp();
+      }
+      if (++r == TC_SCHED) { r = 0; rph ^= 1; }
+      if (t < 0) break;
+      const TcTile tl = tc_decode<kPair>(P, t);
+      const TcProblem& pr = P.prob[tl.p];
+      const CUtensorMap* ma0 = &P.maps[tl.p][0];
+      const CUtensorMap* ma1 = &P.maps[tl.p][1];
+      const CUtensorMap* mb0 = &P.maps[tl.p][2];
+      const CUtensorMap* mb1 = &P.maps[tl.p][3];
+      const int am0 = tl.m0 + TC_BM * rank;               // this CTA's A rows
+      const int bn0 = tl.n0 + Cfg::B_ROWS * rank;         // this CTA's B rows
+      const int kb_total = pr.kb_total;
+      for (int kb = 0; kb < kb_total; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        if (elect_one()) {
           uint8_t* sA = smem + s * Cfg::STAGE;
           uint8_t* sB = sA + TC_A_BYTES;
           uint32_t barc = 0;
@@ -305,9 +314,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           if (leader) mbar_arrive_expect_tx(&full[s], Cfg::STAGE * kPair);
           const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
           const int ka = (seg1 ? kb - pr.kseg : kb) * TC_BK;
-          if (!(P.variant & 2))
-            tc_load_operand<kPair>(sA, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode, TC_BM, am0, ka,
-                                   tl.b);
+          tc_load_operand<kPair>(sA, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode, TC_BM, am0, ka,
+                                 tl.b);
           const bool bseg1 = seg1 && pr.b_seg;
           const int kbk = (bseg1 ? kb - pr.kseg : kb) * TC_BK + pr.b_koff;
           const CUtensorMap* mb = bseg1 ? mb1 : mb0;
@@ -324,23 +332,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
               else
                 tl3<kPair>(sB + i * 8192, mb0, &full[s], barc, n, kbk, tl.b);
             }
-          } else if ((P.variant & 1) && pr.b_mode == 0) {
-            // experiment: K-major B as 64-row boxes (map box rows = 64)
-            for (int i = 0; i < Cfg::B_ROWS / 64; ++i)
-              tl3<kPair>(sB + i * 8192, mb, &full[s], barc, kbk, bn0 + 64 * i, tl.b);
           } else {
             tc_load_operand<kPair>(sB, mb, &full[s], barc, pr.b_mode, Cfg::B_ROWS, bn0, kbk, tl.b);
           }
-          if (P.variant & 2)
-            tc_load_operand<kPair>(sA, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode, TC_BM, am0, ka,
-                                   tl.b);
-          if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
+        __syncwarp();
+        if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
-      // ---------------- MMA issuer (pair leader only)
+    if (leader) {
+      // ---------------- MMA issuer (pair leader only): the whole warp waits,
+      // one elected lane issues tcgen05.mma and the commits.
       int s = 0;
       uint32_t ph = 0;
       int r = 0;
@@ -350,7 +353,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       for (;;) {
         mbar_wait(&sfull[r], rph);
         const int t = sched_tile[r];
-        mbar_arrive(&sempty[r]);
+        __syncwarp();
+        if (elect_one()) mbar_arrive(&sempty[r]);
+        __syncwarp();
         if (++r == TC_SCHED) { r = 0; rph ^= 1; }
         if (t < 0) break;
         const TcTile tl = tc_decode<kPair>(P, t);
@@ -360,27 +365,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         const uint32_t b_lbo = pr.b_mn ? 8192u : 16u;
         const uint32_t a_kstep = pr.a_mn ? 2048u : 32u;
         const uint32_t b_kstep = pr.b_mn ? 2048u : 32u;
+        const int kb_total = pr.kb_total;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t dcol = tmem_base + acc * TC_BN;
-        for (int kb = 0; kb < pr.kb_total; ++kb) {
+        for (int kb = 0; kb < kb_total; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint32_t sA = smem_u32(smem + s * Cfg::STAGE);
-          const uint32_t sB = sA + TC_A_BYTES;
+          if (elect_one()) {
+            const uint32_t sA = smem_u32(smem + s * Cfg::STAGE);
+            const uint32_t sB = sA + TC_A_BYTES;
 #pragma unroll
-          for (int k = 0; k < TC_BK / 16; ++k) {
-            const uint64_t ad = umma_sdesc(sA + k * a_kstep, a_lbo, 1024);
-            const uint64_t bd = umma_sdesc(sB + k * b_kstep, b_lbo, 1024);
-            if constexpr (kPair == 2) umma_bf16_pair(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
-            else umma_bf16(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < TC_BK / 16; ++k) {
+              const uint64_t ad = umma_sdesc(sA + k * a_kstep, a_lbo, 1024);
+              const uint64_t bd = umma_sdesc(sB + k * b_kstep, b_lbo, 1024);
+              if constexpr (kPair == 2) umma_bf16_pair(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              else umma_bf16(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            }
+            if constexpr (kPair == 2) umma_commit_pair(&empty[s]);
+            else umma_commit(&empty[s]);
           }
-          if constexpr (kPair == 2) umma_commit_pair(&empty[s]);
-          else umma_commit(&empty[s]);
+          __syncwarp();
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
-        if constexpr (kPair == 2) umma_commit_pair(&tfull[acc]);
-        else umma_commit(&tfull[acc]);
+        if (elect_one()) {
+          if constexpr (kPair == 2) umma_commit_pair(&tfull[acc]);
+          else umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
     }
