@@ -62,7 +62,7 @@ long long attn_softmax_last_launches(void);
  *                   cta_group::2, 256 x 256 tiles) instead of single CTAs
  *                   (128 x 256): 1 = forward vocab / projection, 2 = vocab
  *                   backward chunks, 4 = projection backward, 8 = the debug
- *                   GEMM entry.  Default 8.
+ *                   GEMM entry.  Default 14.
  *   "gemm_variant"  debug experiment bits of the GEMM producer (0 = default)
  *   "mn_3d_tma"     1 (default) = load MN-major operand tiles with one 3D TMA
  *                   box per stage; 0 = one 2D box per 64-wide atom

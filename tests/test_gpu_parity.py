@@ -69,7 +69,7 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, pair):
     binding.attn_debug_gemm_bf16(M, N, K, Ad, a_mn, Bd, b_mn, C)
     torch.cuda.synchronize()
     binding.attn_softmax_set_option("mn_3d_tma", 1)
-    binding.attn_softmax_set_option("cta_pair", 8)
+    binding.attn_softmax_set_option("cta_pair", 14)
     err = (C.double().cpu() - ref).abs().max().item()
     assert err < 1e-3 * max(1.0, ref.abs().max().item()), err
 
@@ -90,7 +90,7 @@ def test_parity_vs_oracle(cuda_lib, name, vc, pair):
     try:
         g = run_gpu(cfg, inp, scale, vocab_chunk=vc)
     finally:
-        binding.attn_softmax_set_option("cta_pair", 8)
+        binding.attn_softmax_set_option("cta_pair", 14)
     f, b = oracle(inp, scale)
     tol = TOL[cfg.dtype]
     assert abs(g["loss"] - f["loss"]) <= tol["loss"] * abs(f["loss"]), (g["loss"], f["loss"])
