@@ -284,29 +284,44 @@ def main():
     value = tok_job * args.steps / (total_ms / 1e3)
     loss = float(out["loss"].item())
 
-    # ---- e2e: host-buffer entry point, H2D of activations + D2H of loss per step
+    # ---- e2e through the C ABI with HOST buffers: every step copies its own
+    # activations (H_dec, H_enc, tgt_ids) host->device from pinned memory and
+    # reads its loss back; step i+1's copy is prefetched on the library's copy
+    # stream while step i computes (attn_softmax_prefetch_host +
+    # attn_softmax_fwd_bwd_staged, double-buffered staging).
     pin = {k: dv[k].cpu().pin_memory() for k in ("H_dec", "H_enc", "tgt_ids")}
-    staging = torch.empty(binding.attn_softmax_host_staging_size(st.shape), dtype=torch.uint8,
-                          device=dev)
+    stg_bytes = binding.attn_softmax_host_staging_size(st.shape)
+    staging = [torch.empty(stg_bytes, dtype=torch.uint8, device=dev) for _ in range(2)]
     loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
     h2d = sum(v.numel() * v.element_size() for v in pin.values())
 
-    def step_host():
-        binding.attn_softmax_fwd_bwd_host(
-            st.shape, pin["H_dec"], pin["H_enc"], dv["src_len"], dv["tgt_len"], pin["tgt_ids"],
-            dv["W_c"], dv["W_out"], scale, loss_host, out["dH_dec"], out["dH_enc"], out["dW_c"],
-            out["dW_out"], staging, st.workspace, comm=comm, stream=stream)
-        stream.synchronize()   # the loss is read on the host every step
-    for _ in range(2):
-        step_host()
+    def e2e_run(nsteps):
+        binding.attn_softmax_prefetch_host(st.shape, pin["H_dec"], pin["H_enc"], pin["tgt_ids"],
+                                           staging[0], stream=stream)
+        for i in range(nsteps):
+            if i + 1 < nsteps:
+                binding.attn_softmax_prefetch_host(st.shape, pin["H_dec"], pin["H_enc"],
+                                                   pin["tgt_ids"], staging[(i + 1) % 2],
+                                                   stream=stream)
+            binding.attn_softmax_fwd_bwd_staged(
+                st.shape, staging[i % 2], dv["src_len"], dv["tgt_len"], dv["W_c"], dv["W_out"],
+                scale, loss_host, out["dH_dec"], out["dH_enc"], out["dW_c"], out["dW_out"],
+                st.workspace, comm=comm, stream=stream)
+            stream.synchronize()   # the step's loss is read on the host
+            _ = float(loss_host.item())
+    e2e_run(3)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_wall = time.perf_counter()
     e0.record(stream)
-    for _ in range(args.steps):
-        step_host()
+    e2e_run(args.steps)
     e1.record(stream)
     barrier()
-    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    t_wall = time.perf_counter() - t_wall
+    # the copies run on the library's copy stream, so time on the host clock
+    # around the whole loop (it brackets every copy and every compute)
+    e2e_ms = torch.tensor([max(e0.elapsed_time(e1), 1e3 * t_wall)], dtype=torch.float64,
+                          device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_value = tok_job * args.steps / (float(e2e_ms.item()) / 1e3)

@@ -137,6 +137,34 @@ attn_status_t attn_softmax_fwd_bwd_host(
     attn_comm_t* comm,
     void* stream);
 
+/* Pipelined host-buffer variant (double-buffered staging).
+ * attn_softmax_prefetch_host enqueues the host->device copy of one step's
+ * activations (H_dec, H_enc, tgt_ids from HOST, pinned for overlap) into
+ * `staging` on the library's own copy stream, ordered after all work already
+ * enqueued on `stream` (so a staging buffer the previous step still reads is
+ * not overwritten).  attn_softmax_fwd_bwd_staged then runs the stage on a
+ * prefetched staging buffer (waiting only for that buffer's copy) and copies
+ * the loss into loss_host.  A training loop prefetches step i+1 into the
+ * other buffer before running step i, so the copies overlap the compute.
+ * staging_bytes >= attn_softmax_host_staging_size(s). */
+attn_status_t attn_softmax_prefetch_host(
+    const attn_shape_t* s,
+    const void* H_dec_host, const void* H_enc_host, const int32_t* tgt_ids_host,
+    void* staging, size_t staging_bytes,
+    void* stream);
+attn_status_t attn_softmax_fwd_bwd_staged(
+    const attn_shape_t* s,
+    const void* staging, size_t staging_bytes,
+    const int32_t* src_lens_host, const int32_t* tgt_lens_host,
+    const void* W_c, const void* W_out,
+    float loss_scale,
+    float* loss_host,
+    void* dH_dec, void* dH_enc,
+    float* dW_c, float* dW_out,
+    void* workspace, size_t workspace_bytes,
+    attn_comm_t* comm,
+    void* stream);
+
 /* Debug-build style check of the valid target ids: synchronous, returns
  * ATTN_ERR_TOKEN_RANGE if any tgt_ids[b,i] (i < tgt_len[b]) is outside [0,V). */
 attn_status_t attn_softmax_check_ids(const attn_shape_t* s,

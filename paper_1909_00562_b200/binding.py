@@ -25,6 +25,7 @@ STATUS = {0: "ATTN_OK", 1: "ATTN_ERR_INVALID_ARG", 2: "ATTN_ERR_SHAPE",
 EXPORTS = [
     "attn_softmax_workspace_size", "attn_softmax_fwd_bwd",
     "attn_softmax_host_staging_size", "attn_softmax_fwd_bwd_host",
+    "attn_softmax_prefetch_host", "attn_softmax_fwd_bwd_staged",
     "attn_softmax_check_ids", "attn_grad_allreduce", "attn_comm_get_unique_id",
     "attn_comm_init", "attn_comm_destroy", "attn_last_error", "attn_version",
     "attn_softmax_workspace_views", "attn_debug_gemm_bf16",
@@ -80,6 +81,12 @@ def lib() -> ctypes.CDLL:
                                             _P, ctypes.c_size_t, _P, ctypes.c_size_t,
                                             _P, _P]
     L.attn_softmax_fwd_bwd_host.restype = ctypes.c_int
+    L.attn_softmax_prefetch_host.argtypes = [S, _P, _P, _P, _P, ctypes.c_size_t, _P]
+    L.attn_softmax_prefetch_host.restype = ctypes.c_int
+    L.attn_softmax_fwd_bwd_staged.argtypes = [S, _P, ctypes.c_size_t, i32p, i32p, _P, _P,
+                                              ctypes.c_float, _P, _P, _P, _P, _P, _P,
+                                              ctypes.c_size_t, _P, _P]
+    L.attn_softmax_fwd_bwd_staged.restype = ctypes.c_int
     L.attn_softmax_check_ids.argtypes = [S, i32p, _P, _P]
     L.attn_softmax_check_ids.restype = ctypes.c_int
     L.attn_grad_allreduce.argtypes = [_P, _P, ctypes.c_size_t, _P]
@@ -183,6 +190,24 @@ def attn_softmax_fwd_bwd_host(s, H_dec_host, H_enc_host, src_lens, tgt_lens,
         _ptr(loss_host), _ptr(dH_dec), _ptr(dH_enc), _ptr(dW_c), _ptr(dW_out),
         _ptr(staging), staging.numel() * staging.element_size(),
         _ptr(workspace), workspace.numel() * workspace.element_size(),
+        comm, _stream(stream)))
+
+
+def attn_softmax_prefetch_host(s, H_dec_host, H_enc_host, tgt_ids_host, staging, stream=None):
+    _check(lib().attn_softmax_prefetch_host(
+        ctypes.byref(s), _ptr(H_dec_host), _ptr(H_enc_host), _ptr(tgt_ids_host), _ptr(staging),
+        staging.numel() * staging.element_size(), _stream(stream)))
+
+
+def attn_softmax_fwd_bwd_staged(s, staging, src_lens, tgt_lens, W_c, W_out, loss_scale,
+                                loss_host, dH_dec, dH_enc, dW_c, dW_out, workspace,
+                                comm=None, stream=None):
+    src, src_p = _i32(src_lens)
+    tgt, tgt_p = _i32(tgt_lens)
+    _check(lib().attn_softmax_fwd_bwd_staged(
+        ctypes.byref(s), _ptr(staging), staging.numel() * staging.element_size(), src_p, tgt_p,
+        _ptr(W_c), _ptr(W_out), float(loss_scale), _ptr(loss_host), _ptr(dH_dec), _ptr(dH_enc),
+        _ptr(dW_c), _ptr(dW_out), _ptr(workspace), workspace.numel() * workspace.element_size(),
         comm, _stream(stream)))
 
 

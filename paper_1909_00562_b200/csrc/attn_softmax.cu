@@ -1054,6 +1054,105 @@ extern "C" attn_status_t attn_softmax_fwd_bwd_host(
   return ATTN_OK;
 }
 
+// ------------------------------------------------------------------ pipelined host variant
+// Library-owned copy stream and per-staging-buffer "ready" events.
+struct StagingSlot {
+  const void* ptr = nullptr;
+  cudaEvent_t ready = nullptr;
+};
+static std::mutex g_stage_mu;
+static StagingSlot g_slots[8];
+static int g_slot_next = 0;
+static cudaStream_t g_copy_stream = nullptr;
+static cudaEvent_t g_free_ev = nullptr;
+
+static attn_status_t staging_slot(const void* ptr, cudaEvent_t* ev) {
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  for (auto& sl : g_slots)
+    if (sl.ptr == ptr) { *ev = sl.ready; return ATTN_OK; }
+  StagingSlot& sl = g_slots[g_slot_next++ % 8];
+  if (!sl.ready) CUDA_TRY(cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
+  sl.ptr = ptr;
+  *ev = sl.ready;
+  return ATTN_OK;
+}
+
+struct StagingViews {
+  void* H_dec; void* H_enc; int32_t* ids; float* loss;
+};
+static StagingViews staging_views(const attn_shape_t* s, const void* staging) {
+  const size_t elt = s->dtype == ATTN_BF16 ? 2 : 4;
+  const size_t T = (size_t)s->batch * s->tgt_len;
+  const size_t bh = elt * T * s->hidden, be = elt * (size_t)s->batch * s->src_len * s->hidden;
+  char* p = (char*)staging;
+  StagingViews v;
+  v.H_dec = p;
+  v.H_enc = p + align_up(bh);
+  v.ids = (int32_t*)(p + align_up(bh) + align_up(be));
+  v.loss = (float*)((char*)v.ids + align_up(sizeof(int32_t) * T));
+  return v;
+}
+
+extern "C" attn_status_t attn_softmax_prefetch_host(const attn_shape_t* s, const void* H_dec_host,
+                                                    const void* H_enc_host,
+                                                    const int32_t* tgt_ids_host, void* staging,
+                                                    size_t staging_bytes, void* stream_) {
+  attn_status_t st = check_shape(s);
+  if (st != ATTN_OK) return st;
+  if (!H_dec_host || !H_enc_host || !tgt_ids_host || !staging)
+    return fail(ATTN_ERR_INVALID_ARG, "prefetch: NULL argument");
+  if (staging_bytes < attn_softmax_host_staging_size(s))
+    return fail(ATTN_ERR_WORKSPACE, "staging_bytes = %zu < required %zu", staging_bytes,
+                attn_softmax_host_staging_size(s));
+  {
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    if (!g_copy_stream) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&g_copy_stream, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&g_free_ev, cudaEventDisableTiming));
+    }
+  }
+  cudaEvent_t ready;
+  if ((st = staging_slot(staging, &ready)) != ATTN_OK) return st;
+  // the staging buffer is free once everything enqueued on `stream` so far is done
+  CUDA_TRY(cudaEventRecord(g_free_ev, (cudaStream_t)stream_));
+  CUDA_TRY(cudaStreamWaitEvent(g_copy_stream, g_free_ev, 0));
+  const size_t elt = s->dtype == ATTN_BF16 ? 2 : 4;
+  const size_t T = (size_t)s->batch * s->tgt_len;
+  StagingViews v = staging_views(s, staging);
+  CUDA_TRY(cudaMemcpyAsync(v.H_dec, H_dec_host, elt * T * s->hidden, cudaMemcpyHostToDevice,
+                           g_copy_stream));
+  CUDA_TRY(cudaMemcpyAsync(v.H_enc, H_enc_host, elt * (size_t)s->batch * s->src_len * s->hidden,
+                           cudaMemcpyHostToDevice, g_copy_stream));
+  CUDA_TRY(cudaMemcpyAsync(v.ids, tgt_ids_host, sizeof(int32_t) * T, cudaMemcpyHostToDevice,
+                           g_copy_stream));
+  CUDA_TRY(cudaEventRecord(ready, g_copy_stream));
+  return ATTN_OK;
+}
+
+extern "C" attn_status_t attn_softmax_fwd_bwd_staged(
+    const attn_shape_t* s, const void* staging, size_t staging_bytes, const int32_t* src_lens_host,
+    const int32_t* tgt_lens_host, const void* W_c, const void* W_out, float loss_scale,
+    float* loss_host, void* dH_dec, void* dH_enc, float* dW_c, float* dW_out, void* workspace,
+    size_t workspace_bytes, attn_comm_t* comm, void* stream_) {
+  attn_status_t st = check_shape(s);
+  if (st != ATTN_OK) return st;
+  if (!staging || !loss_host) return fail(ATTN_ERR_INVALID_ARG, "staged: NULL argument");
+  if (staging_bytes < attn_softmax_host_staging_size(s))
+    return fail(ATTN_ERR_WORKSPACE, "staging_bytes = %zu < required %zu", staging_bytes,
+                attn_softmax_host_staging_size(s));
+  cudaEvent_t ready;
+  if ((st = staging_slot(staging, &ready)) != ATTN_OK) return st;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  CUDA_TRY(cudaStreamWaitEvent(stream, ready, 0));
+  StagingViews v = staging_views(s, staging);
+  st = attn_softmax_fwd_bwd(s, v.H_dec, v.H_enc, src_lens_host, tgt_lens_host, v.ids, W_c, W_out,
+                            nullptr, loss_scale, v.loss, dH_dec, dH_enc, dW_c, dW_out, nullptr,
+                            workspace, workspace_bytes, comm, stream_);
+  if (st != ATTN_OK) return st;
+  CUDA_TRY(cudaMemcpyAsync(loss_host, v.loss, sizeof(float), cudaMemcpyDeviceToHost, stream));
+  return ATTN_OK;
+}
+
 // ------------------------------------------------------------------ id check
 extern "C" attn_status_t attn_softmax_check_ids(const attn_shape_t* s, const int32_t* tgt_lens_host,
                                                 const int32_t* tgt_ids, void* stream_) {

@@ -155,3 +155,46 @@ def test_deterministic(cuda_lib):
     assert a["loss"] == b["loss"]
     for k in ("dH_dec", "dH_enc", "dW_c", "dW_out"):
         np.testing.assert_array_equal(a[k], b[k])
+
+
+def test_host_buffer_paths_match_device_path(cuda_lib):
+    """attn_softmax_fwd_bwd_host and the pipelined prefetch + staged entry
+    points give bit-identical results to the device-pointer call."""
+    from paper_1909_00562_b200 import binding
+    from paper_1909_00562_b200.stage import AttnSoftmaxStage, to_device
+    cfg = CONFIGS["small"]
+    inp = make_inputs(cfg)
+    scale = 1.0 / global_valid_tokens(cfg, cfg.B)
+    st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
+    dv = to_device(inp, cfg.dtype)
+    ref = st(dv["H_dec"], dv["H_enc"], dv["src_len"], dv["tgt_len"], dv["tgt_ids"],
+             dv["W_c"], dv["W_out"], scale)
+    ref = {k: v.clone() for k, v in ref.items()}
+    pin = {k: dv[k].cpu().pin_memory() for k in ("H_dec", "H_enc", "tgt_ids")}
+    nbytes = binding.attn_softmax_host_staging_size(st.shape)
+    staging = [torch.empty(nbytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    loss_host = torch.empty(1).pin_memory()
+    out = st.alloc_outputs()
+    binding.attn_softmax_fwd_bwd_host(st.shape, pin["H_dec"], pin["H_enc"], dv["src_len"],
+                                      dv["tgt_len"], pin["tgt_ids"], dv["W_c"], dv["W_out"], scale,
+                                      loss_host, out["dH_dec"], out["dH_enc"], out["dW_c"],
+                                      out["dW_out"], staging[0], st.workspace)
+    torch.cuda.synchronize()
+    assert loss_host.item() == ref["loss"].item()
+    for k in ("dH_dec", "dH_enc", "dW_c", "dW_out"):
+        assert torch.equal(out[k], ref[k]), k
+    for i in range(3):   # pipelined: prefetch step i+1 while step i runs
+        if i == 0:
+            binding.attn_softmax_prefetch_host(st.shape, pin["H_dec"], pin["H_enc"],
+                                               pin["tgt_ids"], staging[0])
+        binding.attn_softmax_prefetch_host(st.shape, pin["H_dec"], pin["H_enc"], pin["tgt_ids"],
+                                           staging[(i + 1) % 2])
+        out = st.alloc_outputs()
+        binding.attn_softmax_fwd_bwd_staged(st.shape, staging[i % 2], dv["src_len"],
+                                            dv["tgt_len"], dv["W_c"], dv["W_out"], scale,
+                                            loss_host, out["dH_dec"], out["dH_enc"],
+                                            out["dW_c"], out["dW_out"], st.workspace)
+        torch.cuda.synchronize()
+        assert loss_host.item() == ref["loss"].item()
+        for k in ("dH_dec", "dH_enc", "dW_c", "dW_out"):
+            assert torch.equal(out[k], ref[k]), k
