@@ -81,7 +81,23 @@ struct alignas(64) TcParams {
   int total_tiles;
   int* tile_counter;
   int variant;   // debug experiment bits (0 = production path)
+  long long* trace;   // debug: per-tile timestamps (null = off); 8 x int64 per tile
 };
+
+// trace record layout per tile t (clock64 of the SM that ran it):
+//   [0] smid  [1] producer: first load issued  [2] producer: last load issued
+//   [3] MMA: tile id seen  [4] MMA: first MMA issued  [5] MMA: last commit
+//   [6] epilogue warp 4: accumulator ready (tfull)  [7] epilogue warp 4: done
+__device__ __forceinline__ long long clk64() {
+  long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 
 __device__ __forceinline__ int tc_find_problem(const TcParams& P, int t) {
   int p = 0;
@@ -307,6 +323,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       for (int kb = 0; kb < kb_total; ++kb) {
         mbar_wait(&empty[s], ph ^ 1);
         if (elect_one()) {
+          if (P.trace && leader && (kb == 0 || kb == kb_total - 1))
+            P.trace[(long long)t * 8 + (kb == 0 ? 1 : 2)] = clk64();
+          if (P.trace && leader && kb == 0) P.trace[(long long)t * 8] = smid();
           uint8_t* sA = smem + s * Cfg::STAGE;
           uint8_t* sB = sA + TC_A_BYTES;
           uint32_t barc = 0;
@@ -354,7 +373,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         mbar_wait(&sfull[r], rph);
         const int t = sched_tile[r];
         __syncwarp();
-        if (elect_one()) mbar_arrive(&sempty[r]);
+        if (elect_one()) {
+          mbar_arrive(&sempty[r]);
+          if (P.trace && t >= 0) P.trace[(long long)t * 8 + 3] = clk64();
+        }
         __syncwarp();
         if (++r == TC_SCHED) { r = 0; rph ^= 1; }
         if (t < 0) break;
@@ -373,6 +395,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           mbar_wait(&full[s], ph);
           tc_fence_after();
           if (elect_one()) {
+            if (P.trace && kb == 0) P.trace[(long long)t * 8 + 4] = clk64();
             const uint32_t sA = smem_u32(smem + s * Cfg::STAGE);
             const uint32_t sB = sA + TC_A_BYTES;
 #pragma unroll
@@ -391,6 +414,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         if (elect_one()) {
           if constexpr (kPair == 2) umma_commit_pair(&tfull[acc]);
           else umma_commit(&tfull[acc]);
+          if (P.trace) P.trace[(long long)t * 8 + 5] = clk64();
         }
         __syncwarp();
         if (++acc == 2) { acc = 0; aph ^= 1; }
@@ -424,6 +448,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       const CUtensorMap* omap = &P.maps[tl.p][4];
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
+      if (P.trace && warp == 4 && lane == 0 && leader) P.trace[(long long)t * 8 + 6] = clk64();
       const int row0 = tl.m0 + TC_BM * rank + q * 32;   // row inside the batch item
       const int row = row0 + lane;
       const bool row_ok = row < pr.M;
@@ -510,6 +535,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       }
       tc_fence_before();
       __syncwarp();
+      if (P.trace && warp == 4 && lane == 0 && leader) P.trace[(long long)t * 8 + 7] = clk64();
       if (lane == 0) {
         if (kPair == 2 && !leader) mbar_arrive_cluster(leader_addr(&tempty[acc]));
         else mbar_arrive(&tempty[acc]);

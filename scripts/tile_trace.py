@@ -1,0 +1,42 @@
+"""Per-tile timeline of one tcgen05 GEMM launch (debug trace option)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from paper_1909_00562_b200 import binding, build
+build.build()
+M, N, K, amn, bmn, pair, epi = (int(x) for x in sys.argv[1:8])
+binding.attn_softmax_set_option("cta_pair", 8 if pair == 2 else 0)
+binding.attn_softmax_set_option("debug_epilogue", epi)
+A = torch.randn(K, M, device="cuda").bfloat16() if amn else torch.randn(M, K, device="cuda").bfloat16()
+B = torch.randn(K, N, device="cuda").bfloat16() if bmn else torch.randn(N, K, device="cuda").bfloat16()
+C = torch.empty(M, N, device="cuda")
+tm = 128 * pair
+tiles = ((M + tm - 1) // tm) * ((N + 255) // 256)
+tr = torch.zeros(tiles * 8, dtype=torch.int64, device="cuda")
+for _ in range(3):
+    binding.attn_debug_gemm_bf16(M, N, K, A, amn, B, bmn, C)
+binding.attn_softmax_set_option("gemm_trace", tr.data_ptr())
+binding.attn_debug_gemm_bf16(M, N, K, A, amn, B, bmn, C)
+torch.cuda.synchronize()
+binding.attn_softmax_set_option("gemm_trace", 0)
+t = tr.view(tiles, 8).cpu().numpy().astype(np.int64)
+kb = (K + 63) // 64
+mma = t[:, 5] - t[:, 4]
+print(f"tiles {tiles}, k-blocks/tile {kb}, ideal MMA cycles/tile {kb*512//pair*pair}")
+print("MMA span (first issue -> last commit issue) cycles: median %d p10 %d p90 %d" % tuple(np.percentile(mma, [50, 10, 90])))
+# per SM: gap between consecutive tiles' first MMA issues
+gaps, stalls, epis, loadlead = [], [], [], []
+for sm in np.unique(t[:, 0]):
+    rows = t[t[:, 0] == sm]
+    rows = rows[np.argsort(rows[:, 4])]
+    for a, b in zip(rows[:-1], rows[1:]):
+        gaps.append(b[4] - a[4])
+        stalls.append(b[4] - a[5])          # last commit of prev -> first MMA of next
+    epis.extend(rows[:, 7] - rows[:, 6])
+    loadlead.extend(rows[:, 4] - rows[:, 1])
+print("tile-to-tile period cycles: median %d p10 %d p90 %d" % tuple(np.percentile(gaps, [50, 10, 90])))
+print("boundary gap (prev last commit -> next first MMA): median %d p90 %d" % tuple(np.percentile(stalls, [50, 90])))
+print("epilogue time (tfull -> tempty arrive): median %d p90 %d" % tuple(np.percentile(epis, [50, 90])))
+print("first load issue -> first MMA: median %d p90 %d" % tuple(np.percentile(loadlead, [50, 90])))
+print("MMA-id-seen -> first MMA: median %d" % np.percentile(t[:, 4] - t[:, 3], 50))
