@@ -331,13 +331,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           uint8_t* sB = sA + TC_A_BYTES;
           uint32_t barc = 0;
           if constexpr (kPair == 2) barc = leader_addr(&full[s]);
-          if ((P.variant & 4) && loads_issued >= Cfg::STAGES) {
+          const bool noload = (P.variant & 4) && loads_issued >= Cfg::STAGES;
+          ++loads_issued;
+          if (noload) {
             // experiment: no more TMA traffic, MMAs rerun the resident stages
             if (leader) mbar_arrive(&full[s]);
-            ++loads_issued;
-            goto next_stage;
-          }
-          ++loads_issued;
+          } else {
           if (leader) mbar_arrive_expect_tx(&full[s], Cfg::STAGE * kPair);
           const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
           const int ka = (seg1 ? kb - pr.kseg : kb) * TC_BK;
@@ -362,7 +361,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           } else {
             tc_load_operand<kPair>(sB, mb, &full[s], barc, pr.b_mode, Cfg::B_ROWS, bn0, kbk, tl.b);
           }
-        next_stage:;
+          }
         }
         __syncwarp();
         if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
