@@ -64,7 +64,7 @@ long long attn_softmax_last_launches(void);
  *                   backward chunks, 4 = projection backward, 8 = the debug
  *                   GEMM entry.  Default 14.
  *   "gemm_variant"  debug experiment bits of the GEMM producer (0 = default)
- *   "gemm_trace"    device address of an int64 buffer (8 per tile) that the
+ *   "gemm_trace"    device address of an int64 buffer (16 per tile) that the
  *                   next tcgen05 launches fill with per-tile clock64 stamps
  *                   (0 = off; debug only)
  *   "mn_3d_tma"     1 (default) = load MN-major operand tiles with one 3D TMA

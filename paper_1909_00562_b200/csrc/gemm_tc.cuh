@@ -325,8 +325,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         mbar_wait(&empty[s], ph ^ 1);
         if (elect_one()) {
           if (P.trace && leader && (kb == 0 || kb == kb_total - 1))
-            P.trace[(long long)t * 8 + (kb == 0 ? 1 : 2)] = clk64();
-          if (P.trace && leader && kb == 0) P.trace[(long long)t * 8] = smid();
+            P.trace[(long long)t * 16 + (kb == 0 ? 1 : 2)] = clk64();
+          if (P.trace && leader && kb == 0) P.trace[(long long)t * 16] = smid();
+          if (P.trace && leader && kb == 0) P.trace[(long long)t * 16 + 11] = clk64();
           uint8_t* sA = smem + s * Cfg::STAGE;
           uint8_t* sB = sA + TC_A_BYTES;
           uint32_t barc = 0;
@@ -383,13 +384,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         __syncwarp();
         if (elect_one()) {
           mbar_arrive(&sempty[r]);
-          if (P.trace && t >= 0) P.trace[(long long)t * 8 + 3] = clk64();
+          if (P.trace && t >= 0) P.trace[(long long)t * 16 + 3] = clk64();
         }
         __syncwarp();
         if (++r == TC_SCHED) { r = 0; rph ^= 1; }
         if (t < 0) break;
         const TcTile tl = tc_decode<kPair>(P, t);
         const TcProblem& pr = P.prob[tl.p];
+        if (P.trace && lane == 0) P.trace[(long long)t * 16 + 8] = clk64();   // decoded
         const uint32_t idesc = umma_idesc_bf16(Cfg::TILE_M, TC_BN, pr.a_mn, pr.b_mn);
         const uint32_t a_lbo = pr.a_mn ? 8192u : 16u;
         const uint32_t b_lbo = pr.b_mn ? 8192u : 16u;
@@ -398,12 +400,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         const int kb_total = pr.kb_total;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
+        if (P.trace && lane == 0) P.trace[(long long)t * 16 + 9] = clk64();   // accumulator free
         const uint32_t dcol = tmem_base + acc * TC_BN;
         for (int kb = 0; kb < kb_total; ++kb) {
+          if (P.trace && lane == 0 && kb == 0) P.trace[(long long)t * 16 + 10] = clk64();
           mbar_wait(&full[s], ph);
           tc_fence_after();
           if (elect_one()) {
-            if (P.trace && kb == 0) P.trace[(long long)t * 8 + 4] = clk64();
+            if (P.trace && kb == 0) P.trace[(long long)t * 16 + 4] = clk64();
             const uint32_t sA = smem_u32(smem + s * Cfg::STAGE);
             const uint32_t sB = sA + TC_A_BYTES;
 #pragma unroll
@@ -422,7 +426,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         if (elect_one()) {
           if constexpr (kPair == 2) umma_commit_pair(&tfull[acc]);
           else umma_commit(&tfull[acc]);
-          if (P.trace) P.trace[(long long)t * 8 + 5] = clk64();
+          if (P.trace) P.trace[(long long)t * 16 + 5] = clk64();
         }
         __syncwarp();
         if (++acc == 2) { acc = 0; aph ^= 1; }
@@ -456,7 +460,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       const CUtensorMap* omap = &P.maps[tl.p][4];
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      if (P.trace && warp == 4 && lane == 0 && leader) P.trace[(long long)t * 8 + 6] = clk64();
+      if (P.trace && warp == 4 && lane == 0 && leader) P.trace[(long long)t * 16 + 6] = clk64();
       const int row0 = tl.m0 + TC_BM * rank + q * 32;   // row inside the batch item
       const int row = row0 + lane;
       const bool row_ok = row < pr.M;
@@ -543,7 +547,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       }
       tc_fence_before();
       __syncwarp();
-      if (P.trace && warp == 4 && lane == 0 && leader) P.trace[(long long)t * 8 + 7] = clk64();
+      if (P.trace && warp == 4 && lane == 0 && leader) P.trace[(long long)t * 16 + 7] = clk64();
       if (lane == 0) {
         if (kPair == 2 && !leader) mbar_arrive_cluster(leader_addr(&tempty[acc]));
         else mbar_arrive(&tempty[acc]);

@@ -15,14 +15,14 @@ B = torch.randn(K, N, device="cuda").bfloat16() if bmn else torch.randn(N, K, de
 C = torch.empty(M, N, device="cuda")
 tm = 128 * pair
 tiles = ((M + tm - 1) // tm) * ((N + 255) // 256)
-tr = torch.zeros(tiles * 8, dtype=torch.int64, device="cuda")
+tr = torch.zeros(tiles * 16, dtype=torch.int64, device="cuda")
 for _ in range(3):
     binding.attn_debug_gemm_bf16(M, N, K, A, amn, B, bmn, C)
 binding.attn_softmax_set_option("gemm_trace", tr.data_ptr())
 binding.attn_debug_gemm_bf16(M, N, K, A, amn, B, bmn, C)
 torch.cuda.synchronize()
 binding.attn_softmax_set_option("gemm_trace", 0)
-t = tr.view(tiles, 8).cpu().numpy().astype(np.int64)
+t = tr.view(tiles, 16).cpu().numpy().astype(np.int64)
 kb = (K + 63) // 64
 mma = t[:, 5] - t[:, 4]
 print(f"tiles {tiles}, k-blocks/tile {kb}, ideal MMA cycles/tile {kb*512//pair*pair}")
@@ -41,4 +41,15 @@ print("tile-to-tile period cycles: median %d p10 %d p90 %d" % tuple(np.percentil
 print("boundary gap (prev last commit -> next first MMA): median %d p90 %d" % tuple(np.percentile(stalls, [50, 90])))
 print("epilogue time (tfull -> tempty arrive): median %d p90 %d" % tuple(np.percentile(epis, [50, 90])))
 print("first load issue -> first MMA: median %d p90 %d" % tuple(np.percentile(loadlead, [50, 90])))
-print("MMA-id-seen -> first MMA: median %d" % np.percentile(t[:, 4] - t[:, 3], 50))
+print("MMA-id-seen -> decoded: %d | decoded -> acc free: %d | acc free -> full wait start: %d | full wait -> first MMA: %d" % (
+    np.percentile(t[:, 8] - t[:, 3], 50), np.percentile(t[:, 9] - t[:, 8], 50),
+    np.percentile(t[:, 10] - t[:, 9], 50), np.percentile(t[:, 4] - t[:, 10], 50)))
+prev_commit = []
+for sm in np.unique(t[:, 0]):
+    rows = t[t[:, 0] == sm]
+    rows = rows[np.argsort(rows[:, 4])]
+    for a, b in zip(rows[:-1], rows[1:]):
+        prev_commit.append((b[3] - a[5], b[11] - a[5]))
+pc = np.array(prev_commit)
+print("prev last commit -> next id seen (MMA): %d | prev last commit -> next first load issue (producer): %d" % (
+    np.percentile(pc[:, 0], 50), np.percentile(pc[:, 1], 50)))
