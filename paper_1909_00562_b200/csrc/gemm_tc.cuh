@@ -292,7 +292,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       if (leader) {
         t = __shfl_sync(0xffffffffu, t_next, 0);
         if (t >= P.total_tiles) t = -1;
-        else if (lane == 0) t_next = atomicAdd(P.tile_counter, 1);
         mbar_wait(&sempty[r], rph ^ 1);
         if (elect_one()) {
           sched_tile[r] = t;
@@ -303,6 +302,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           mbar_arrive(&sfull[r]);
         }
         __syncwarp();
+        // prefetch the following tile index only AFTER publishing this one:
+        // the arrive has release semantics and would otherwise wait for the
+        // atomic's round trip before the next tile's loads are issued
+        if (t >= 0 && lane == 0) t_next = atomicAdd(P.tile_counter, 1);
       } else {
         mbar_wait_cluster(&sfull[r], rph);
         t = sched_tile[r];
