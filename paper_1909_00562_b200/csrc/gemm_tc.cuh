@@ -284,13 +284,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     uint32_t rph = 0;
     // the next tile index is fetched one tile ahead so the global atomic's
     // latency overlaps the current tile's loads
+    // The tile counter atomic is issued by lane 1: lane 0 issues every
+    // mbarrier arrive (release semantics), which would otherwise wait for the
+    // atomic's global round trip.
     int t_next = 0;
     int loads_issued = 0;
-    if (leader && lane == 0) t_next = atomicAdd(P.tile_counter, 1);
+    if (leader && lane == 1) t_next = atomicAdd(P.tile_counter, 1);
     for (;;) {
       int t;
       if (leader) {
-        t = __shfl_sync(0xffffffffu, t_next, 0);
+        t = __shfl_sync(0xffffffffu, t_next, 1);
         if (t >= P.total_tiles) t = -1;
         mbar_wait(&sempty[r], rph ^ 1);
         if (elect_one()) {
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         // prefetch the following tile index only AFTER publishing this one:
         // the arrive has release semantics and would otherwise wait for the
         // atomic's round trip before the next tile's loads are issued
-        if (t >= 0 && lane == 0) t_next = atomicAdd(P.tile_counter, 1);
+        if (t >= 0 && lane == 1) t_next = atomicAdd(P.tile_counter, 1);
       } else {
         mbar_wait_cluster(&sfull[r], rph);
         t = sched_tile[r];
