@@ -318,8 +318,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       }
       if (++r == TC_SCHED) { r = 0; rph ^= 1; }
       if (t < 0) break;
+      if (P.trace && leader && lane == 0) P.trace[(long long)t * 16 + 12] = clk64();   // published
       const TcTile tl = tc_decode<kPair>(P, t);
       const TcProblem& pr = P.prob[tl.p];
+      if (P.trace && leader && lane == 0) P.trace[(long long)t * 16 + 13] = clk64();   // decoded
       const CUtensorMap* ma0 = &P.maps[tl.p][0];
       const CUtensorMap* ma1 = &P.maps[tl.p][1];
       const CUtensorMap* mb0 = &P.maps[tl.p][2];
@@ -328,6 +330,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       const int bn0 = tl.n0 + Cfg::B_ROWS * rank;         // this CTA's B rows
       const int kb_total = pr.kb_total;
       for (int kb = 0; kb < kb_total; ++kb) {
+        if (P.trace && leader && lane == 0 && kb == kb_total - 1) P.trace[(long long)t * 16 + 14] = clk64();
         mbar_wait(&empty[s], ph ^ 1);
         if (elect_one()) {
           if (P.trace && leader && (kb == 0 || kb == kb_total - 1))

@@ -51,5 +51,13 @@ for sm in np.unique(t[:, 0]):
     for a, b in zip(rows[:-1], rows[1:]):
         prev_commit.append((b[3] - a[5], b[11] - a[5]))
 pc = np.array(prev_commit)
+pp = []
+for sm in np.unique(t[:, 0]):
+    rows = t[t[:, 0] == sm]
+    rows = rows[np.argsort(rows[:, 4])]
+    for a, b in zip(rows[:-1], rows[1:]):
+        pp.append((b[12] - a[2], b[13] - b[12], b[11] - b[13], a[2] - a[14], b[11] - a[2]))
+pp = np.array(pp)
+print("producer: prev last-load -> next published %d | publish -> decoded %d | decoded -> first load %d | last empty wait %d | prev last load -> next first load %d" % tuple(np.percentile(pp[:, i], 50) for i in range(5)))
 print("prev last commit -> next id seen (MMA): %d | prev last commit -> next first load issue (producer): %d" % (
     np.percentile(pc[:, 0], 50), np.percentile(pc[:, 1], 50)))
