@@ -289,7 +289,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     // atomic's global round trip.
     int t_next = 0;
     int loads_issued = 0;
-    if (leader && lane == 1) t_next = atomicAdd(P.tile_counter, 1);
+    const bool static_sched = (P.variant & 8) != 0;   // experiment: round-robin, no atomic
+    const int unit = blockIdx.x / kPair, nunits = gridDim.x / kPair;
+    if (leader && lane == 1) t_next = static_sched ? unit : atomicAdd(P.tile_counter, 1);
     for (;;) {
       int t;
       if (leader) {
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         // prefetch the following tile index only AFTER publishing this one:
         // the arrive has release semantics and would otherwise wait for the
         // atomic's round trip before the next tile's loads are issued
-        if (t >= 0 && lane == 1) t_next = atomicAdd(P.tile_counter, 1);
+        if (t >= 0 && lane == 1) t_next = static_sched ? t + nunits : atomicAdd(P.tile_counter, 1);
       } else {
         mbar_wait_cluster(&sfull[r], rph);
         t = sched_tile[r];
