@@ -95,6 +95,15 @@ __device__ __forceinline__ long long clk64() {
   asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
   return c;
 }
+// stamp taken by every lane of a converged warp, stored by lane 2 (never lane
+// 0, whose mbarrier arrives have release semantics and would wait for it)
+#define TC_TRACE(t, i)                                                  \
+  do {                                                                  \
+    if (P.trace) {                                                      \
+      const long long c_ = clk64();                                     \
+      if (lane == 2) P.trace[(long long)(t) * 16 + (i)] = c_;           \
+    }                                                                   \
+  } while (0)
 __device__ __forceinline__ uint32_t smid() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -323,10 +332,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       }
       if (++r == TC_SCHED) { r = 0; rph ^= 1; }
       if (t < 0) break;
-      if (P.trace && leader && lane == 0) P.trace[(long long)t * 16 + 12] = clk64();   // published
+      if (leader) TC_TRACE(t, 12);   // published
+      if (leader && P.trace && lane == 2) P.trace[(long long)t * 16] = smid();
       const TcTile tl = tc_decode<kPair>(P, t);
       const TcProblem& pr = P.prob[tl.p];
-      if (P.trace && leader && lane == 0) P.trace[(long long)t * 16 + 13] = clk64();   // decoded
+      if (leader) TC_TRACE(t, 13);   // decoded
       const CUtensorMap* ma0 = &P.maps[tl.p][0];
       const CUtensorMap* ma1 = &P.maps[tl.p][1];
       const CUtensorMap* mb0 = &P.maps[tl.p][2];
@@ -335,13 +345,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       const int bn0 = tl.n0 + Cfg::B_ROWS * rank;         // this CTA's B rows
       const int kb_total = pr.kb_total;
       for (int kb = 0; kb < kb_total; ++kb) {
-        if (P.trace && leader && lane == 0 && kb == kb_total - 1) P.trace[(long long)t * 16 + 14] = clk64();
         mbar_wait(&empty[s], ph ^ 1);
         if (elect_one()) {
           if (P.trace && leader && (kb == 0 || kb == kb_total - 1))
-            P.trace[(long long)t * 16 + (kb == 0 ? 1 : 2)] = clk64();
-          if (P.trace && leader && kb == 0) P.trace[(long long)t * 16] = smid();
-          if (P.trace && leader && kb == 0) P.trace[(long long)t * 16 + 11] = clk64();
           uint8_t* sA = smem + s * Cfg::STAGE;
           uint8_t* sB = sA + TC_A_BYTES;
           uint32_t barc = 0;
@@ -379,6 +385,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           }
         }
         __syncwarp();
+        if (leader && kb == 0) TC_TRACE(t, 11);             // first load issued
+        if (leader && kb == kb_total - 1) TC_TRACE(t, 2);   // last load issued
         if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
       }
     }
@@ -396,16 +404,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         mbar_wait(&sfull[r], rph);
         const int t = sched_tile[r];
         __syncwarp();
-        if (elect_one()) {
-          mbar_arrive(&sempty[r]);
-          if (P.trace && t >= 0) P.trace[(long long)t * 16 + 3] = clk64();
-        }
+        if (elect_one()) mbar_arrive(&sempty[r]);
         __syncwarp();
+        if (t >= 0) TC_TRACE(t, 3);   // MMA saw the tile
         if (++r == TC_SCHED) { r = 0; rph ^= 1; }
         if (t < 0) break;
         const TcTile tl = tc_decode<kPair>(P, t);
         const TcProblem& pr = P.prob[tl.p];
-        if (P.trace && lane == 0) P.trace[(long long)t * 16 + 8] = clk64();   // decoded
+        TC_TRACE(t, 8);   // decoded
         const uint32_t idesc = umma_idesc_bf16(Cfg::TILE_M, TC_BN, pr.a_mn, pr.b_mn);
         const uint32_t a_lbo = pr.a_mn ? 8192u : 16u;
         const uint32_t b_lbo = pr.b_mn ? 8192u : 16u;
@@ -414,14 +420,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         const int kb_total = pr.kb_total;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
-        if (P.trace && lane == 0) P.trace[(long long)t * 16 + 9] = clk64();   // accumulator free
+        TC_TRACE(t, 9);   // accumulator free
         const uint32_t dcol = tmem_base + acc * TC_BN;
         for (int kb = 0; kb < kb_total; ++kb) {
-          if (P.trace && lane == 0 && kb == 0) P.trace[(long long)t * 16 + 10] = clk64();
+          if (kb == 0) TC_TRACE(t, 10);
           mbar_wait(&full[s], ph);
           tc_fence_after();
           if (elect_one()) {
-            if (P.trace && kb == 0) P.trace[(long long)t * 16 + 4] = clk64();
             const uint32_t sA = smem_u32(smem + s * Cfg::STAGE);
             const uint32_t sB = sA + TC_A_BYTES;
 #pragma unroll
@@ -435,14 +440,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
             else umma_commit(&empty[s]);
           }
           __syncwarp();
+          if (kb == 0) TC_TRACE(t, 4);   // first MMAs issued
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
         if (elect_one()) {
           if constexpr (kPair == 2) umma_commit_pair(&tfull[acc]);
           else umma_commit(&tfull[acc]);
-          if (P.trace) P.trace[(long long)t * 16 + 5] = clk64();
         }
         __syncwarp();
+        TC_TRACE(t, 5);   // last commit issued
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
     }
@@ -474,7 +480,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       const CUtensorMap* omap = &P.maps[tl.p][4];
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      if (P.trace && warp == 0 && lane == 0 && leader) P.trace[(long long)t * 16 + 6] = clk64();
+      if (warp == 0 && leader) TC_TRACE(t, 6);
       const int row0 = tl.m0 + TC_BM * rank + q * 32;   // row inside the batch item
       const int row = row0 + lane;
       const bool row_ok = row < pr.M;
@@ -561,7 +567,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       }
       tc_fence_before();
       __syncwarp();
-      if (P.trace && warp == 0 && lane == 0 && leader) P.trace[(long long)t * 16 + 7] = clk64();
+      if (warp == 0 && leader) TC_TRACE(t, 7);
       if (lane == 0) {
         if (kPair == 2 && !leader) mbar_arrive_cluster(leader_addr(&tempty[acc]));
         else mbar_arrive(&tempty[acc]);

@@ -36,7 +36,7 @@ for sm in np.unique(t[:, 0]):
         gaps.append(b[4] - a[4])
         stalls.append(b[4] - a[5])          # last commit of prev -> first MMA of next
     epis.extend(rows[:, 7] - rows[:, 6])
-    loadlead.extend(rows[:, 4] - rows[:, 1])
+    loadlead.extend(rows[:, 4] - rows[:, 11])
 print("tile-to-tile period cycles: median %d p10 %d p90 %d" % tuple(np.percentile(gaps, [50, 10, 90])))
 print("boundary gap (prev last commit -> next first MMA): median %d p90 %d" % tuple(np.percentile(stalls, [50, 90])))
 print("epilogue time (tfull -> tempty arrive): median %d p90 %d" % tuple(np.percentile(epis, [50, 90])))
@@ -56,7 +56,7 @@ for sm in np.unique(t[:, 0]):
     rows = t[t[:, 0] == sm]
     rows = rows[np.argsort(rows[:, 4])]
     for a, b in zip(rows[:-1], rows[1:]):
-        pp.append((b[12] - a[2], b[13] - b[12], b[11] - b[13], a[2] - a[14], b[11] - a[2]))
+        pp.append((b[12] - a[2], b[13] - b[12], b[11] - b[13], 0, b[11] - a[2]))
 pp = np.array(pp)
 print("producer: prev last-load -> next published %d | publish -> decoded %d | decoded -> first load %d | last empty wait %d | prev last load -> next first load %d" % tuple(np.percentile(pp[:, i], 50) for i in range(5)))
 print("prev last commit -> next id seen (MMA): %d | prev last commit -> next first load issue (producer): %d" % (
