@@ -347,7 +347,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       for (int kb = 0; kb < kb_total; ++kb) {
         mbar_wait(&empty[s], ph ^ 1);
         if (elect_one()) {
-          if (P.trace && leader && (kb == 0 || kb == kb_total - 1))
           uint8_t* sA = smem + s * Cfg::STAGE;
           uint8_t* sB = sA + TC_A_BYTES;
           uint32_t barc = 0;
