@@ -290,24 +290,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     // ---------------- tile scheduler (leader) + TMA producer (both CTAs).
     // The whole warp runs the loop (waits are per lane, values warp-uniform);
     // one elected lane issues, so TMA operands live in uniform registers.
+    // The schedule is software-pipelined: tile i+1 is fetched, published to
+    // the ring and decoded right after tile i's first load is issued, so the
+    // tile boundary costs nothing but the empty-slot wait.  The tile counter
+    // atomic is issued by lane 1: lane 0 issues every mbarrier arrive
+    // (release semantics), which would otherwise wait for its round trip.
     int s = 0;
     uint32_t ph = 0;
     int r = 0;
     uint32_t rph = 0;
-    // the next tile index is fetched one tile ahead so the global atomic's
-    // latency overlaps the current tile's loads
-    // The tile counter atomic is issued by lane 1: lane 0 issues every
-    // mbarrier arrive (release semantics), which would otherwise wait for the
-    // atomic's global round trip.
-    int t_next = 0;
     int loads_issued = 0;
     const bool static_sched = (P.variant & 8) != 0;   // experiment: round-robin, no atomic
     const int unit = blockIdx.x / kPair, nunits = gridDim.x / kPair;
-    if (leader && lane == 1) t_next = static_sched ? unit : atomicAdd(P.tile_counter, 1);
-    for (;;) {
+    int t_raw = 0;   // lane 1: result of the latest tile-counter fetch
+    auto fetch = [&](int prev) {
+      if (lane == 1) t_raw = static_sched ? (prev < 0 ? unit : prev + nunits) : atomicAdd(P.tile_counter, 1);
+    };
+    // next tile id: the leader takes it from the counter and publishes it to
+    // its ring (and the peer's); the peer reads its ring
+    auto next_tile = [&](int prev) -> int {
       int t;
       if (leader) {
-        t = __shfl_sync(0xffffffffu, t_next, 1);
+        t = __shfl_sync(0xffffffffu, t_raw, 1);
         if (t >= P.total_tiles) t = -1;
         mbar_wait(&sempty[r], rph ^ 1);
         if (elect_one()) {
@@ -319,10 +323,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           mbar_arrive(&sfull[r]);
         }
         __syncwarp();
-        // prefetch the following tile index only AFTER publishing this one:
-        // the arrive has release semantics and would otherwise wait for the
-        // atomic's round trip before the next tile's loads are issued
-        if (t >= 0 && lane == 1) t_next = static_sched ? t + nunits : atomicAdd(P.tile_counter, 1);
+        if (t >= 0) fetch(t);
       } else {
         mbar_wait_cluster(&sfull[r], rph);
         t = sched_tile[r];
@@ -331,12 +332,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         __syncwarp();
       }
       if (++r == TC_SCHED) { r = 0; rph ^= 1; }
-      if (t < 0) break;
-      if (leader) TC_TRACE(t, 12);   // published
-      if (leader && P.trace && lane == 2) P.trace[(long long)t * 16] = smid();
-      const TcTile tl = tc_decode<kPair>(P, t);
+      return t;
+    };
+    if (leader) fetch(-1);
+    int t = next_tile(-1);
+    TcTile tl{};
+    if (t >= 0) tl = tc_decode<kPair>(P, t);
+    while (t >= 0) {
       const TcProblem& pr = P.prob[tl.p];
-      if (leader) TC_TRACE(t, 13);   // decoded
+      if (leader && P.trace && lane == 2) P.trace[(long long)t * 16] = smid();
       const CUtensorMap* ma0 = &P.maps[tl.p][0];
       const CUtensorMap* ma1 = &P.maps[tl.p][1];
       const CUtensorMap* mb0 = &P.maps[tl.p][2];
@@ -344,6 +348,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       const int am0 = tl.m0 + TC_BM * rank;               // this CTA's A rows
       const int bn0 = tl.n0 + Cfg::B_ROWS * rank;         // this CTA's B rows
       const int kb_total = pr.kb_total;
+      int t_nxt = -1;
+      TcTile tl_nxt{};
       for (int kb = 0; kb < kb_total; ++kb) {
         mbar_wait(&empty[s], ph ^ 1);
         if (elect_one()) {
@@ -357,58 +363,73 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
             // experiment: no more TMA traffic, MMAs rerun the resident stages
             if (leader) mbar_arrive(&full[s]);
           } else {
-          if (leader) mbar_arrive_expect_tx(&full[s], Cfg::STAGE * kPair);
-          const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
-          const int ka = (seg1 ? kb - pr.kseg : kb) * TC_BK;
-          tc_load_operand<kPair>(sA, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode, TC_BM, am0, ka,
-                                 tl.b);
-          const bool bseg1 = seg1 && pr.b_seg;
-          const int kbk = (bseg1 ? kb - pr.kseg : kb) * TC_BK + pr.b_koff;
-          const CUtensorMap* mb = bseg1 ? mb1 : mb0;
-          if (pr.b_nsplit > 0 && pr.b_mode == 1) {
-            if (bn0 >= pr.b_nsplit)
-              tl4<kPair>(sB, mb1, &full[s], barc, 0, kbk, (bn0 - pr.b_nsplit) / 64, tl.b);
-            else
-              tl4<kPair>(sB, mb0, &full[s], barc, 0, kbk, bn0 / 64, tl.b);
-          } else if (pr.b_nsplit > 0) {
-            for (int i = 0; i < Cfg::B_ROWS / 64; ++i) {
-              const int n = bn0 + 64 * i;
-              if (n >= pr.b_nsplit)
-                tl3<kPair>(sB + i * 8192, mb1, &full[s], barc, n - pr.b_nsplit, kbk, tl.b);
+            if (leader) mbar_arrive_expect_tx(&full[s], Cfg::STAGE * kPair);
+            const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
+            const int ka = (seg1 ? kb - pr.kseg : kb) * TC_BK;
+            tc_load_operand<kPair>(sA, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode, TC_BM, am0,
+                                   ka, tl.b);
+            const bool bseg1 = seg1 && pr.b_seg;
+            const int kbk = (bseg1 ? kb - pr.kseg : kb) * TC_BK + pr.b_koff;
+            const CUtensorMap* mb = bseg1 ? mb1 : mb0;
+            if (pr.b_nsplit > 0 && pr.b_mode == 1) {
+              if (bn0 >= pr.b_nsplit)
+                tl4<kPair>(sB, mb1, &full[s], barc, 0, kbk, (bn0 - pr.b_nsplit) / 64, tl.b);
               else
-                tl3<kPair>(sB + i * 8192, mb0, &full[s], barc, n, kbk, tl.b);
+                tl4<kPair>(sB, mb0, &full[s], barc, 0, kbk, bn0 / 64, tl.b);
+            } else if (pr.b_nsplit > 0) {
+              for (int i = 0; i < Cfg::B_ROWS / 64; ++i) {
+                const int n = bn0 + 64 * i;
+                if (n >= pr.b_nsplit)
+                  tl3<kPair>(sB + i * 8192, mb1, &full[s], barc, n - pr.b_nsplit, kbk, tl.b);
+                else
+                  tl3<kPair>(sB + i * 8192, mb0, &full[s], barc, n, kbk, tl.b);
+              }
+            } else {
+              tc_load_operand<kPair>(sB, mb, &full[s], barc, pr.b_mode, Cfg::B_ROWS, bn0, kbk,
+                                     tl.b);
             }
-          } else {
-            tc_load_operand<kPair>(sB, mb, &full[s], barc, pr.b_mode, Cfg::B_ROWS, bn0, kbk, tl.b);
-          }
           }
         }
         __syncwarp();
         if (leader && kb == 0) TC_TRACE(t, 11);             // first load issued
         if (leader && kb == kb_total - 1) TC_TRACE(t, 2);   // last load issued
         if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
+        if (kb == 0) {
+          // the next tile: fetch, publish and decode in the shadow of this one
+          t_nxt = next_tile(t);
+          if (t_nxt >= 0) tl_nxt = tc_decode<kPair>(P, t_nxt);
+          if (leader && t_nxt >= 0) TC_TRACE(t_nxt, 12);
+        }
       }
+      t = t_nxt;
+      tl = tl_nxt;
     }
   } else if (warp == kWarpMma) {
     if (leader) {
       // ---------------- MMA issuer (pair leader only): the whole warp waits,
-      // one elected lane issues tcgen05.mma and the commits.
+      // one elected lane issues tcgen05.mma and the commits.  The next tile
+      // is read from the ring and decoded during the current tile's second
+      // k-block (the producer published it after this tile's first load).
       int s = 0;
       uint32_t ph = 0;
       int r = 0;
       uint32_t rph = 0;
       int acc = 0;
       uint32_t aph = 0;
-      for (;;) {
+      auto read_tile = [&]() -> int {
         mbar_wait(&sfull[r], rph);
         const int t = sched_tile[r];
         __syncwarp();
         if (elect_one()) mbar_arrive(&sempty[r]);
         __syncwarp();
-        if (t >= 0) TC_TRACE(t, 3);   // MMA saw the tile
         if (++r == TC_SCHED) { r = 0; rph ^= 1; }
-        if (t < 0) break;
-        const TcTile tl = tc_decode<kPair>(P, t);
+        return t;
+      };
+      int t = read_tile();
+      TcTile tl{};
+      if (t >= 0) tl = tc_decode<kPair>(P, t);
+      while (t >= 0) {
+        TC_TRACE(t, 3);
         const TcProblem& pr = P.prob[tl.p];
         TC_TRACE(t, 8);   // decoded
         const uint32_t idesc = umma_idesc_bf16(Cfg::TILE_M, TC_BN, pr.a_mn, pr.b_mn);
@@ -417,6 +438,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         const uint32_t a_kstep = pr.a_mn ? 2048u : 32u;
         const uint32_t b_kstep = pr.b_mn ? 2048u : 32u;
         const int kb_total = pr.kb_total;
+        const int kb_read = kb_total > 1 ? 1 : 0;
+        int t_nxt = -1;
+        TcTile tl_nxt{};
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         TC_TRACE(t, 9);   // accumulator free
@@ -441,6 +465,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           __syncwarp();
           if (kb == 0) TC_TRACE(t, 4);   // first MMAs issued
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
+          if (kb == kb_read) {
+            t_nxt = read_tile();
+            if (t_nxt >= 0) tl_nxt = tc_decode<kPair>(P, t_nxt);
+          }
         }
         if (elect_one()) {
           if constexpr (kPair == 2) umma_commit_pair(&tfull[acc]);
@@ -449,6 +477,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         __syncwarp();
         TC_TRACE(t, 5);   // last commit issued
         if (++acc == 2) { acc = 0; aph ^= 1; }
+        t = t_nxt;
+        tl = tl_nxt;
       }
     }
   } else if (warp < TC_EPI_WARPS) {
