@@ -67,6 +67,8 @@ long long attn_softmax_last_launches(void);
  *   "gemm_trace"    device address of an int64 buffer (16 per tile) that the
  *                   next tcgen05 launches fill with per-tile clock64 stamps
  *                   (0 = off; debug only)
+ *   "gemm_trace_launch" trace only the launch with this index inside an
+ *                   attn_softmax_fwd_bwd call (-1 = every launch)
  *   "mn_3d_tma"     1 (default) = load MN-major operand tiles with one 3D TMA
  *                   box per stage; 0 = one 2D box per 64-wide atom
  *   "debug_epilogue" attn_debug_gemm_bf16 epilogue: 0 = fp32 TMA store,

@@ -109,6 +109,7 @@ static int g_opt_mn3d = 1;  // MN-major operands via one 3D TMA box
 static int g_opt_pair = PAIR_DEFAULT;
 static int g_opt_variant = 0;   // "gemm_variant": debug experiment bits
 static long long* g_trace = nullptr;   // "gemm_trace": device pointer of a per-tile trace buffer
+static long long g_trace_launch = -1;  // "gemm_trace_launch": trace only this launch index of a call (-1 = all)
 static int64_t g_opt_vocab_chunk = 0;
 static int64_t g_opt_gemm_ctas = 0;
 
@@ -119,6 +120,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
       return fail(ATTN_ERR_INVALID_ARG, "vocab_chunk must be a non-negative multiple of 256 (got %lld)",
                   (long long)value);
     g_opt_vocab_chunk = value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "gemm_trace_launch")) {
+    g_trace_launch = value;
     return ATTN_OK;
   }
   if (!strcmp(key, "gemm_trace")) {
@@ -372,7 +377,7 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   P.total_tiles = tiles;
   P.tile_counter = counter;
   P.variant = g_opt_variant;
-  P.trace = g_trace;
+  P.trace = (g_trace_launch < 0 || g_trace_launch == g_launches) ? g_trace : nullptr;
   if (tiles == 0) return ATTN_OK;
   const DevInfo di = dev_info();
   int units = (g_opt_gemm_ctas > 0 ? (int)g_opt_gemm_ctas : di.sms) / kPair;
