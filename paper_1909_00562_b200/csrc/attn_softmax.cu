@@ -1196,6 +1196,10 @@ extern "C" attn_status_t attn_debug_gemm_bf16(int M, int N, int K, const void* A
   g.b_mn = b_mn; g.b0 = b_mn ? mnmaj(B, K, N, N) : kmaj(B, N, K, K);
   g.epi.kind = EPI_STORE_F32; g.epi.out = C; g.epi.ldo = N; g.epi.ncols_valid = N; g.epi.ncols_store = N;
   if (g_debug_epi == 1) g.epi.kind = EPI_NONE;
+  if (g_debug_epi == 2 || g_debug_epi == 3) {
+    // bf16 output written into the (larger) fp32 buffer C as [M, N] bf16
+    g.epi.kind = g_debug_epi == 2 ? EPI_STORE_BF16 : EPI_TANH;
+  }
   // one persistent device counter per process (debug entry only); the memset
   // is stream-ordered so the call can be captured in a CUDA graph
   static int* counter = nullptr;

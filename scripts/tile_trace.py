@@ -12,7 +12,7 @@ binding.attn_softmax_set_option("cta_pair", 8 if pair == 2 else 0)
 binding.attn_softmax_set_option("debug_epilogue", epi)
 A = torch.randn(K, M, device="cuda").bfloat16() if amn else torch.randn(M, K, device="cuda").bfloat16()
 B = torch.randn(K, N, device="cuda").bfloat16() if bmn else torch.randn(N, K, device="cuda").bfloat16()
-C = torch.empty(M, N, device="cuda")
+C = torch.empty(M, N, device="cuda")  # fp32 (bf16 epilogues use its first half)
 tm = 128 * pair
 tiles = ((M + tm - 1) // tm) * ((N + 255) // 256)
 tr = torch.zeros(tiles * 16, dtype=torch.int64, device="cuda")
