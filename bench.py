@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-sentences", type=int, default=0)
+    ap.add_argument("--force-comm", action="store_true",
+                    help="use the NCCL communicator even with one rank (exercises the path)")
     return ap.parse_args()
 
 
@@ -222,9 +224,10 @@ def main():
     lib = binding.lib()
 
     comm = None
-    if world > 1:
+    if world > 1 or args.force_comm:
         uid = [binding.attn_comm_get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0)
         comm = binding.attn_comm_init(uid[0], world, rank, local)
 
     # ---- inputs: this rank's sentences of the global batch (weak scaling)

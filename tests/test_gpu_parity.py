@@ -198,3 +198,33 @@ def test_host_buffer_paths_match_device_path(cuda_lib):
         assert loss_host.item() == ref["loss"].item()
         for k in ("dH_dec", "dH_enc", "dW_c", "dW_out"):
             assert torch.equal(out[k], ref[k]), k
+
+
+def test_single_rank_nccl_communicator(cuda_lib):
+    """The NCCL path of attn_softmax_fwd_bwd (dlopen'ed libnccl, comm stream,
+    per-chunk dW_out allreduce, dW_c and loss allreduce, join) on a 1-rank
+    communicator: the sum over one rank is the identity, so results must be
+    bitwise equal to the local call.  attn_grad_allreduce is checked too."""
+    from paper_1909_00562_b200 import binding
+    from paper_1909_00562_b200.stage import AttnSoftmaxStage, to_device
+    cfg = CONFIGS["small"]
+    inp = make_inputs(cfg)
+    scale = 1.0 / global_valid_tokens(cfg, cfg.B)
+    st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
+    dv = to_device(inp, cfg.dtype)
+    args = (dv["H_dec"], dv["H_enc"], dv["src_len"], dv["tgt_len"], dv["tgt_ids"],
+            dv["W_c"], dv["W_out"], scale)
+    ref = {k: v.clone() for k, v in st(*args).items()}
+    uid = binding.attn_comm_get_unique_id()
+    comm = binding.attn_comm_init(uid, 1, 0, torch.cuda.current_device())
+    try:
+        out = st(*args, comm=comm)
+        torch.cuda.synchronize()
+        for k in ("loss", "dH_dec", "dH_enc", "dW_c", "dW_out"):
+            assert torch.equal(out[k], ref[k]), k
+        buf = torch.arange(1000, dtype=torch.float32, device="cuda")
+        binding.attn_grad_allreduce(comm, buf)
+        torch.cuda.synchronize()
+        assert torch.equal(buf, torch.arange(1000, dtype=torch.float32, device="cuda"))
+    finally:
+        binding.attn_comm_destroy(comm)
