@@ -369,12 +369,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     // waits, one elected lane issues, so TMA operands live in uniform registers.
     int s = 0;
     uint32_t ph = 0;
-    TcSlot sl = take();
-    while (sl.t >= 0) {
+    for (;;) {
+      const TcSlot sl = take();
       const int t = sl.t;
+      if (t < 0) break;
       const TcTile tl = sl.tl;
-      TcSlot nxt;
-      nxt.t = -1;
       const TcProblem& pr = P.prob[tl.p];
       if (leader && P.trace && lane == 2) P.trace[(long long)t * 16] = smid();
       const CUtensorMap* ma0 = &P.maps[tl.p][0];
@@ -420,9 +419,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         if (leader && kb == 0) TC_TRACE(t, 11);             // first load issued
         if (leader && kb == kb_total - 1) TC_TRACE(t, 2);   // last load issued
         if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
-        if (kb == 0) nxt = take();   // next tile, off the boundary
       }
-      sl = nxt;
     }
   } else if (warp == kWarpMma) {
     if (leader) {
