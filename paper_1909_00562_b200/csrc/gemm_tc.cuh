@@ -122,12 +122,6 @@ struct TcTile {
   int p, b, m0, n0, tn;
 };
 
-// one entry of the in-CTA tile ring written by the scheduler warp
-struct TcSlot {
-  int t;     // global tile index, -1 = end of work
-  TcTile tl; // decoded tile
-};
-
 template <int kPair>
 __device__ __forceinline__ TcTile tc_decode(const TcParams& P, int t) {
   TcTile r;
@@ -272,15 +266,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
   uint64_t* tempty = tfull + 2;                // [2]
   uint64_t* sfull = tempty + 2;                // [SCHED]
   uint64_t* sempty = sfull + TC_SCHED;         // [SCHED]
-  TcSlot* ring = reinterpret_cast<TcSlot*>(sempty + TC_SCHED);   // [SCHED]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + TC_SCHED);
+  int* sched_tile = reinterpret_cast<int*>(sempty + TC_SCHED);   // [SCHED]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_tile + TC_SCHED);
 
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();
   const uint32_t rank = (kPair == 2) ? cluster_ctarank() : 0;   // 0 = pair leader
   const bool leader = rank == 0;
 
-  constexpr uint32_t kWarpAlloc = 8, kWarpSched = 9, kWarpProducer = 10, kWarpMma = 11;
+  constexpr uint32_t kWarpAlloc = 8, kWarpProducer = 10, kWarpMma = 11;
   if (warp == kWarpProducer && lane == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
       mbar_init(&full[i], 1);
@@ -292,9 +286,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     }
     for (int i = 0; i < TC_SCHED; ++i) {
       mbar_init(&sfull[i], 1);
-      // leader: its producer, MMA and epilogue warps (+ the peer's producer and
-      // epilogue warps, whose ring the leader's scheduler also fills)
-      mbar_init(&sempty[i], 2 + TC_EPI_WARPS + (kPair == 2 ? 1 + TC_EPI_WARPS : 0));
+      // leader: its MMA + epilogue warps (+ the peer's producer and epilogue warps)
+      mbar_init(&sempty[i], 1 + TC_EPI_WARPS + (kPair == 2 ? 1 + TC_EPI_WARPS : 0));
     }
     fence_barrier_init();
     for (int p = 0; p < P.nprob; ++p)
@@ -313,67 +306,59 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
   // shared::cluster addresses of the leader's barriers (pair mode)
   auto leader_addr = [&](void* p) -> uint32_t { return mapa_shared(smem_u32(p), 0); };
 
-  // ring consumer: wait for the next slot, read it, release it
-  int r = 0;
-  uint32_t rph = 0;
-  auto take = [&]() -> TcSlot {
-    if (kPair == 2 && !leader) mbar_wait_cluster(&sfull[r], rph);
-    else mbar_wait(&sfull[r], rph);
-    const TcSlot sl = ring[r];
-    __syncwarp();
-    if (elect_one()) {
-      if (kPair == 2 && !leader) mbar_arrive_cluster(leader_addr(&sempty[r]));
-      else mbar_arrive(&sempty[r]);
-    }
-    __syncwarp();
-    if (++r == TC_SCHED) { r = 0; rph ^= 1; }
-    return sl;
-  };
-
-  if (warp == kWarpSched) {
-    // ---------------- tile scheduler (one per CTA, the pair leader's for a
-    // pair): pulls tile indices from the global counter, decodes them and
-    // fills the ring up to TC_SCHED tiles ahead of the slowest consumer, so
-    // no scheduling work sits on the producer's or the MMA issuer's path.
-    // The atomic is issued by lane 1 (lane 0 issues the release arrives).
-    if (leader) {
-      int t_raw = 0;
-      if (lane == 1) t_raw = atomicAdd(P.tile_counter, 1);
-      for (;;) {
-        int t = __shfl_sync(0xffffffffu, t_raw, 1);
+  if (warp == kWarpProducer) {
+    // ---------------- tile scheduler (leader) + TMA producer (both CTAs).
+    // The whole warp runs the loop (waits are per lane, values warp-uniform);
+    // one elected lane issues, so TMA operands live in uniform registers.
+    // The schedule is software-pipelined: tile i+1 is fetched, published to
+    // the ring and decoded right after tile i's first load is issued, so the
+    // tile boundary costs nothing but the empty-slot wait.  The tile counter
+    // atomic is issued by lane 1: lane 0 issues every mbarrier arrive
+    // (release semantics), which would otherwise wait for its round trip.
+    int s = 0;
+    uint32_t ph = 0;
+    int r = 0;
+    uint32_t rph = 0;
+    int loads_issued = 0;
+    const bool static_sched = (P.variant & 8) != 0;   // experiment: round-robin, no atomic
+    const int unit = blockIdx.x / kPair, nunits = gridDim.x / kPair;
+    int t_raw = 0;   // lane 1: result of the latest tile-counter fetch
+    auto fetch = [&](int prev) {
+      if (lane == 1) t_raw = static_sched ? (prev < 0 ? unit : prev + nunits) : atomicAdd(P.tile_counter, 1);
+    };
+    // next tile id: the leader takes it from the counter and publishes it to
+    // its ring (and the peer's); the peer reads its ring
+    auto next_tile = [&](int prev) -> int {
+      int t;
+      if (leader) {
+        t = __shfl_sync(0xffffffffu, t_raw, 1);
         if (t >= P.total_tiles) t = -1;
-        if (t >= 0 && lane == 1) t_raw = atomicAdd(P.tile_counter, 1);
-        TcSlot sl;
-        sl.t = t;
-        sl.tl = TcTile{};
-        if (t >= 0) sl.tl = tc_decode<kPair>(P, t);
         mbar_wait(&sempty[r], rph ^ 1);
         if (elect_one()) {
-          ring[r] = sl;
+          sched_tile[r] = t;
           if constexpr (kPair == 2) {
-            const uint32_t rs = mapa_shared(smem_u32(&ring[r]), 1);
-            const int* w = reinterpret_cast<const int*>(&sl);
-#pragma unroll
-            for (int i = 0; i < (int)(sizeof(TcSlot) / 4); ++i) st_shared_cluster_u32(rs + 4 * i, (uint32_t)w[i]);
+            st_shared_cluster_u32(mapa_shared(smem_u32(&sched_tile[r]), 1), (uint32_t)t);
             mbar_arrive_cluster(mapa_shared(smem_u32(&sfull[r]), 1));
           }
           mbar_arrive(&sfull[r]);
         }
         __syncwarp();
-        if (++r == TC_SCHED) { r = 0; rph ^= 1; }
-        if (t < 0) break;
+        if (t >= 0) fetch(t);
+      } else {
+        mbar_wait_cluster(&sfull[r], rph);
+        t = sched_tile[r];
+        __syncwarp();
+        if (elect_one()) mbar_arrive_cluster(leader_addr(&sempty[r]));
+        __syncwarp();
       }
-    }
-  } else if (warp == kWarpProducer) {
-    // ---------------- TMA producer (both CTAs of a pair): the whole warp
-    // waits, one elected lane issues, so TMA operands live in uniform registers.
-    int s = 0;
-    uint32_t ph = 0;
-    for (;;) {
-      const TcSlot sl = take();
-      const int t = sl.t;
-      if (t < 0) break;
-      const TcTile tl = sl.tl;
+      if (++r == TC_SCHED) { r = 0; rph ^= 1; }
+      return t;
+    };
+    if (leader) fetch(-1);
+    int t = next_tile(-1);
+    TcTile tl{};
+    if (t >= 0) tl = tc_decode<kPair>(P, t);
+    while (t >= 0) {
       const TcProblem& pr = P.prob[tl.p];
       if (leader && P.trace && lane == 2) P.trace[(long long)t * 16] = smid();
       const CUtensorMap* ma0 = &P.maps[tl.p][0];
@@ -383,6 +368,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       const int am0 = tl.m0 + TC_BM * rank;               // this CTA's A rows
       const int bn0 = tl.n0 + Cfg::B_ROWS * rank;         // this CTA's B rows
       const int kb_total = pr.kb_total;
+      int t_nxt = -1;
+      TcTile tl_nxt{};
       for (int kb = 0; kb < kb_total; ++kb) {
         mbar_wait(&empty[s], ph ^ 1);
         if (elect_one()) {
@@ -390,52 +377,81 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           uint8_t* sB = sA + TC_A_BYTES;
           uint32_t barc = 0;
           if constexpr (kPair == 2) barc = leader_addr(&full[s]);
-          if (leader) mbar_arrive_expect_tx(&full[s], Cfg::STAGE * kPair);
-          const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
-          const int ka = (seg1 ? kb - pr.kseg : kb) * TC_BK;
-          tc_load_operand<kPair>(sA, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode, TC_BM, am0, ka,
-                                 tl.b);
-          const bool bseg1 = seg1 && pr.b_seg;
-          const int kbk = (bseg1 ? kb - pr.kseg : kb) * TC_BK + pr.b_koff;
-          const CUtensorMap* mb = bseg1 ? mb1 : mb0;
-          if (pr.b_nsplit > 0 && pr.b_mode == 1) {
-            if (bn0 >= pr.b_nsplit)
-              tl4<kPair>(sB, mb1, &full[s], barc, 0, kbk, (bn0 - pr.b_nsplit) / 64, tl.b);
-            else
-              tl4<kPair>(sB, mb0, &full[s], barc, 0, kbk, bn0 / 64, tl.b);
-          } else if (pr.b_nsplit > 0) {
-            for (int i = 0; i < Cfg::B_ROWS / 64; ++i) {
-              const int n = bn0 + 64 * i;
-              if (n >= pr.b_nsplit)
-                tl3<kPair>(sB + i * 8192, mb1, &full[s], barc, n - pr.b_nsplit, kbk, tl.b);
-              else
-                tl3<kPair>(sB + i * 8192, mb0, &full[s], barc, n, kbk, tl.b);
-            }
+          const bool noload = (P.variant & 4) && loads_issued >= Cfg::STAGES;
+          ++loads_issued;
+          if (noload) {
+            // experiment: no more TMA traffic, MMAs rerun the resident stages
+            if (leader) mbar_arrive(&full[s]);
           } else {
-            tc_load_operand<kPair>(sB, mb, &full[s], barc, pr.b_mode, Cfg::B_ROWS, bn0, kbk, tl.b);
+            if (leader) mbar_arrive_expect_tx(&full[s], Cfg::STAGE * kPair);
+            const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
+            const int ka = (seg1 ? kb - pr.kseg : kb) * TC_BK;
+            tc_load_operand<kPair>(sA, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode, TC_BM, am0,
+                                   ka, tl.b);
+            const bool bseg1 = seg1 && pr.b_seg;
+            const int kbk = (bseg1 ? kb - pr.kseg : kb) * TC_BK + pr.b_koff;
+            const CUtensorMap* mb = bseg1 ? mb1 : mb0;
+            if (pr.b_nsplit > 0 && pr.b_mode == 1) {
+              if (bn0 >= pr.b_nsplit)
+                tl4<kPair>(sB, mb1, &full[s], barc, 0, kbk, (bn0 - pr.b_nsplit) / 64, tl.b);
+              else
+                tl4<kPair>(sB, mb0, &full[s], barc, 0, kbk, bn0 / 64, tl.b);
+            } else if (pr.b_nsplit > 0) {
+              for (int i = 0; i < Cfg::B_ROWS / 64; ++i) {
+                const int n = bn0 + 64 * i;
+                if (n >= pr.b_nsplit)
+                  tl3<kPair>(sB + i * 8192, mb1, &full[s], barc, n - pr.b_nsplit, kbk, tl.b);
+                else
+                  tl3<kPair>(sB + i * 8192, mb0, &full[s], barc, n, kbk, tl.b);
+              }
+            } else {
+              tc_load_operand<kPair>(sB, mb, &full[s], barc, pr.b_mode, Cfg::B_ROWS, bn0, kbk,
+                                     tl.b);
+            }
           }
         }
         __syncwarp();
         if (leader && kb == 0) TC_TRACE(t, 11);             // first load issued
         if (leader && kb == kb_total - 1) TC_TRACE(t, 2);   // last load issued
         if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
+        if (kb == 0) {
+          // the next tile: fetch, publish and decode in the shadow of this one
+          t_nxt = next_tile(t);
+          if (t_nxt >= 0) tl_nxt = tc_decode<kPair>(P, t_nxt);
+          if (leader && t_nxt >= 0) TC_TRACE(t_nxt, 12);
+        }
       }
+      t = t_nxt;
+      tl = tl_nxt;
     }
   } else if (warp == kWarpMma) {
     if (leader) {
       // ---------------- MMA issuer (pair leader only): the whole warp waits,
-      // one elected lane issues tcgen05.mma and the commits.  The next tile is
-      // taken from the ring during the current tile's second k-block.
+      // one elected lane issues tcgen05.mma and the commits.  The next tile
+      // is read from the ring and decoded during the current tile's second
+      // k-block (the producer published it after this tile's first load).
       int s = 0;
       uint32_t ph = 0;
+      int r = 0;
+      uint32_t rph = 0;
       int acc = 0;
       uint32_t aph = 0;
-      TcSlot sl = take();
-      while (sl.t >= 0) {
-        const int t = sl.t;
-        const TcTile tl = sl.tl;
+      auto read_tile = [&]() -> int {
+        mbar_wait(&sfull[r], rph);
+        const int t = sched_tile[r];
+        __syncwarp();
+        if (elect_one()) mbar_arrive(&sempty[r]);
+        __syncwarp();
+        if (++r == TC_SCHED) { r = 0; rph ^= 1; }
+        return t;
+      };
+      int t = read_tile();
+      TcTile tl{};
+      if (t >= 0) tl = tc_decode<kPair>(P, t);
+      while (t >= 0) {
         TC_TRACE(t, 3);
         const TcProblem& pr = P.prob[tl.p];
+        TC_TRACE(t, 8);   // decoded
         const uint32_t idesc = umma_idesc_bf16(Cfg::TILE_M, TC_BN, pr.a_mn, pr.b_mn);
         const uint32_t a_lbo = pr.a_mn ? 8192u : 16u;
         const uint32_t b_lbo = pr.b_mn ? 8192u : 16u;
@@ -443,8 +459,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         const uint32_t b_kstep = pr.b_mn ? 2048u : 32u;
         const int kb_total = pr.kb_total;
         const int kb_read = kb_total > 1 ? 1 : 0;
-        TcSlot nxt;
-        nxt.t = -1;
+        int t_nxt = -1;
+        TcTile tl_nxt{};
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         TC_TRACE(t, 9);   // accumulator free
@@ -469,7 +485,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           __syncwarp();
           if (kb == 0) TC_TRACE(t, 4);   // first MMAs issued
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
-          if (kb == kb_read) nxt = take();
+          if (kb == kb_read) {
+            t_nxt = read_tile();
+            if (t_nxt >= 0) tl_nxt = tc_decode<kPair>(P, t_nxt);
+          }
         }
         if (elect_one()) {
           if constexpr (kPair == 2) umma_commit_pair(&tfull[acc]);
@@ -478,7 +497,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         __syncwarp();
         TC_TRACE(t, 5);   // last commit issued
         if (++acc == 2) { acc = 0; aph ^= 1; }
-        sl = nxt;
+        t = t_nxt;
+        tl = tl_nxt;
       }
     }
   } else if (warp < TC_EPI_WARPS) {
@@ -488,13 +508,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     const uint32_t h = ew >> 2;         // column half of the 256-wide tile
     const uint32_t stg = smem_u32(staging + ew * TC_STG_BYTES);
     const uint32_t swz = lane & 7;
+    int r = 0;
+    uint32_t rph = 0;
     int acc = 0;
     uint32_t aph = 0;
     for (;;) {
-      const TcSlot sl = take();
-      const int t = sl.t;
+      if (kPair == 2 && !leader) mbar_wait_cluster(&sfull[r], rph);
+      else mbar_wait(&sfull[r], rph);
+      const int t = sched_tile[r];
+      __syncwarp();
+      if (lane == 0) {
+        if (kPair == 2 && !leader) mbar_arrive_cluster(leader_addr(&sempty[r]));
+        else mbar_arrive(&sempty[r]);
+      }
+      if (++r == TC_SCHED) { r = 0; rph ^= 1; }
       if (t < 0) break;
-      const TcTile tl = sl.tl;
+      const TcTile tl = tc_decode<kPair>(P, t);
       const TcProblem& pr = P.prob[tl.p];
       const int kind = pr.epi.kind;
       const CUtensorMap* omap = &P.maps[tl.p][4];
