@@ -549,6 +549,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
 #pragma unroll 1
         for (int c = 0; c < n_act; ++c) {
           float v[32];
+          if ((P.variant & 32) && c > 0) __nanosleep(400);   // experiment: pace the stores
           tmem_ld32(taddr + c * 32, v);
           const int col = col_h + c * 32;
           if (kind == EPI_LSE) {
