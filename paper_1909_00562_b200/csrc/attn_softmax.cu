@@ -107,6 +107,7 @@ extern "C" long long attn_softmax_last_launches(void) { return g_launches; }
 static int g_debug_epi = 0;
 static int g_opt_mn3d = 1;  // MN-major operands via one 3D TMA box
 static int g_opt_pair = PAIR_DEFAULT;
+static int g_opt_mcast = 0;   // "b_multicast": bitmask of GEMM groups on 2-CTA clusters sharing B
 static int g_opt_variant = 0;   // "gemm_variant": debug experiment bits
 static long long* g_trace = nullptr;   // "gemm_trace": device pointer of a per-tile trace buffer
 static long long g_trace_launch = -1;  // "gemm_trace_launch": trace only this launch index of a call (-1 = all)
@@ -132,6 +133,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "gemm_variant")) {
     g_opt_variant = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "b_multicast")) {
+    g_opt_mcast = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "cta_pair")) {
@@ -369,7 +374,7 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   memset(&P, 0, sizeof(P));
   int tiles = 0;
   for (int i = 0; i < n; ++i) {
-    attn_status_t st = fill_tc(gs[i], P.maps[i], P.prob[i], tiles, kPair);
+    attn_status_t st = fill_tc(gs[i], P.maps[i], P.prob[i], tiles, kPair >= 2 ? 2 : 1);
     if (st != ATTN_OK) return st;
     tiles += P.prob[i].tiles_m * P.prob[i].tiles_n * P.prob[i].batch;
   }
@@ -380,20 +385,21 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   P.trace = (g_trace_launch < 0 || g_trace_launch == g_launches) ? g_trace : nullptr;
   if (tiles == 0) return ATTN_OK;
   const DevInfo di = dev_info();
-  int units = (g_opt_gemm_ctas > 0 ? (int)g_opt_gemm_ctas : di.sms) / kPair;
+  const int csize = kPair >= 2 ? 2 : 1;
+  int units = (g_opt_gemm_ctas > 0 ? (int)g_opt_gemm_ctas : di.sms) / csize;
   units = std::max(1, std::min(units, tiles));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(units * kPair);
+  cfg.gridDim = dim3(units * csize);
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = tc_smem_bytes();
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kPair;
+  attr[0].val.clusterDim.x = kPair >= 2 ? 2 : 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = kPair == 2 ? 1 : 0;
+  cfg.numAttrs = kPair >= 2 ? 1 : 0;
   CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<OutT, true, kPair>, P));
   ++g_launches;
   return ATTN_OK;
@@ -407,6 +413,7 @@ enum : int { PAIR_FWD = 1, PAIR_VBWD = 2, PAIR_PBWD = 4, PAIR_DEBUG = 8 };
 template <typename OutT>
 static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cudaStream_t stream,
                                      int group_bit = 0) {
+  if (group_bit && (g_opt_mcast & group_bit)) return launch_tc_group_k<OutT, 3>(gs, n, counter, stream);
   if (group_bit && (g_opt_pair & group_bit)) return launch_tc_group_k<OutT, 2>(gs, n, counter, stream);
   return launch_tc_group_k<OutT, 1>(gs, n, counter, stream);
 }

@@ -50,16 +50,22 @@ constexpr int kMaxProblems = 4;
 
 // kPair = 1: one CTA computes a 128 x 256 tile (tcgen05 cta_group::1).
 // kPair = 2: a CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile
-// with cta_group::2: each CTA stages its 128 rows of A and 128 rows of B, so
-// a stage is 32 KB instead of 48 KB (6 stages instead of 4) and the operand
-// traffic per FLOP through shared memory and L2 drops by a third.
+//            with cta_group::2: each CTA stages its 128 rows of A and 128 rows
+//            of B (32 KB stages, 6 of them); the MMA reads the peer's B half.
+// kPair = 3: a cluster of 2 CTAs computes two vertically adjacent 128 x 256
+//            tiles that share the B tile: each CTA loads half of B and TMA-
+//            multicasts it to both, so both MMAs (cta_group::1) read local
+//            shared memory while the L2 -> SM operand traffic per FLOP drops
+//            by a third (48 KB stages, 4 of them).
 template <int kPair>
 struct TcCfg {
-  static constexpr int TILE_M = TC_BM * kPair;
-  static constexpr int B_ROWS = TC_BN / kPair;                 // B rows staged per CTA
-  static constexpr int B_BYTES = B_ROWS * TC_BK * 2;
-  static constexpr int STAGE = TC_A_BYTES + B_BYTES;           // 48 KB | 32 KB
-  static constexpr int STAGES = TC_RING_BYTES / STAGE;         // 4 | 6
+  static constexpr int TILE_M = kPair == 1 ? TC_BM : 2 * TC_BM;   // rows per scheduled tile
+  static constexpr int MMA_M = kPair == 2 ? 2 * TC_BM : TC_BM;     // UMMA M
+  static constexpr int B_ROWS = kPair == 1 ? TC_BN : TC_BN / 2;    // B rows loaded per CTA
+  static constexpr int B_SMEM = (kPair == 2 ? TC_BN / 2 : TC_BN) * TC_BK * 2;
+  static constexpr int STAGE = TC_A_BYTES + B_SMEM;                // 48 KB | 32 KB | 48 KB
+  static constexpr int STAGES = TC_RING_BYTES / STAGE;             // 4 | 6 | 4
+  static constexpr int CLUSTER = kPair == 1 ? 1 : 2;
 };
 
 struct TcProblem {
@@ -150,6 +156,17 @@ __device__ __forceinline__ void tl4(void* dst, const CUtensorMap* m, uint64_t* b
                                     int c0, int c1, int c2, int c3) {
   if constexpr (kPair == 2) tma_load_4d_pair(dst, m, barc, c0, c1, c2, c3);
   else tma_load_4d(dst, m, bar, c0, c1, c2, c3);
+}
+// multicast-to-both variants (kPair == 3, B operand)
+__device__ __forceinline__ void tc_load_operand_mc(uint8_t* dst, const CUtensorMap* m, uint64_t* bar,
+                                                   int mode, int rows, int r0, int k0, int b) {
+  if (mode == 0) {
+    tma_load_3d_mc(dst, m, bar, k0, r0, b, 3);
+  } else if (mode == 1) {
+    tma_load_4d_mc(dst, m, bar, 0, k0, r0 / 64, b, 3);
+  } else {
+    for (int i = 0; i < rows / 64; ++i) tma_load_3d_mc(dst + i * 8192, m, bar, r0 + 64 * i, k0, b, 3);
+  }
 }
 // Load one operand tile (rows x 64 K) of k-block kb into smem.
 template <int kPair>
@@ -271,23 +288,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
 
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();
-  const uint32_t rank = (kPair == 2) ? cluster_ctarank() : 0;   // 0 = pair leader
+  constexpr bool kClu = kPair >= 2;     // cluster of 2 CTAs
+  constexpr bool kMc = kPair == 3;      // B multicast, per-CTA MMAs
+  const uint32_t rank = kClu ? cluster_ctarank() : 0;   // 0 = cluster leader
   const bool leader = rank == 0;
 
   constexpr uint32_t kWarpAlloc = 8, kWarpProducer = 10, kWarpMma = 11;
   if (warp == kWarpProducer && lane == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], kMc ? 2 : 1);   // kMc: both CTAs' MMAs free a stage
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], TC_EPI_WARPS * kPair);
+      mbar_init(&tempty[i], TC_EPI_WARPS * (kPair == 2 ? 2 : 1));
     }
     for (int i = 0; i < TC_SCHED; ++i) {
       mbar_init(&sfull[i], 1);
       // leader: its MMA + epilogue warps (+ the peer's producer and epilogue warps)
-      mbar_init(&sempty[i], 1 + TC_EPI_WARPS + (kPair == 2 ? 1 + TC_EPI_WARPS : 0));
+      mbar_init(&sempty[i], 1 + TC_EPI_WARPS + (kClu ? 1 + TC_EPI_WARPS : 0) + (kMc ? 1 : 0));
     }
     fence_barrier_init();
     for (int p = 0; p < P.nprob; ++p)
@@ -298,7 +317,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     else tmem_alloc(tmem_slot, 512);
   }
   tc_fence_before();
-  if constexpr (kPair == 2) cluster_sync();
+  if constexpr (kClu) cluster_sync();
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
@@ -336,7 +355,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         mbar_wait(&sempty[r], rph ^ 1);
         if (elect_one()) {
           sched_tile[r] = t;
-          if constexpr (kPair == 2) {
+          if constexpr (kClu) {
             st_shared_cluster_u32(mapa_shared(smem_u32(&sched_tile[r]), 1), (uint32_t)t);
             mbar_arrive_cluster(mapa_shared(smem_u32(&sfull[r]), 1));
           }
@@ -381,7 +400,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           ++loads_issued;
           if (noload) {
             // experiment: no more TMA traffic, MMAs rerun the resident stages
-            if (leader) mbar_arrive(&full[s]);
+            if (leader || kMc) mbar_arrive(&full[s]);
+          } else if constexpr (kMc) {
+            // own A rows; own half of B, multicast into both CTAs' B tile
+            mbar_arrive_expect_tx(&full[s], Cfg::STAGE);
+            const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
+            const int ka = (seg1 ? kb - pr.kseg : kb) * TC_BK;
+            tc_load_operand<1>(sA, seg1 ? ma1 : ma0, &full[s], 0, pr.a_mode, TC_BM, am0, ka, tl.b);
+            const bool bseg1 = seg1 && pr.b_seg;
+            const int kbk = (bseg1 ? kb - pr.kseg : kb) * TC_BK + pr.b_koff;
+            const CUtensorMap* mb = bseg1 ? mb1 : mb0;
+            uint8_t* sBh = sB + rank * (Cfg::B_SMEM / 2);
+            if (pr.b_nsplit > 0 && pr.b_mode == 1) {
+              if (bn0 >= pr.b_nsplit)
+                tma_load_4d_mc(sBh, mb1, &full[s], 0, kbk, (bn0 - pr.b_nsplit) / 64, tl.b, 3);
+              else
+                tma_load_4d_mc(sBh, mb0, &full[s], 0, kbk, bn0 / 64, tl.b, 3);
+            } else if (pr.b_nsplit > 0) {
+              for (int i = 0; i < Cfg::B_ROWS / 64; ++i) {
+                const int n = bn0 + 64 * i;
+                if (n >= pr.b_nsplit)
+                  tma_load_3d_mc(sBh + i * 8192, mb1, &full[s], n - pr.b_nsplit, kbk, tl.b, 3);
+                else
+                  tma_load_3d_mc(sBh + i * 8192, mb0, &full[s], n, kbk, tl.b, 3);
+              }
+            } else {
+              tc_load_operand_mc(sBh, mb, &full[s], pr.b_mode, Cfg::B_ROWS, bn0, kbk, tl.b);
+            }
           } else {
             if (leader) mbar_arrive_expect_tx(&full[s], Cfg::STAGE * kPair);
             const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
@@ -425,7 +470,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       tl = tl_nxt;
     }
   } else if (warp == kWarpMma) {
-    if (leader) {
+    if (leader || kMc) {
       // ---------------- MMA issuer (pair leader only): the whole warp waits,
       // one elected lane issues tcgen05.mma and the commits.  The next tile
       // is read from the ring and decoded during the current tile's second
@@ -437,10 +482,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       int acc = 0;
       uint32_t aph = 0;
       auto read_tile = [&]() -> int {
-        mbar_wait(&sfull[r], rph);
+        if (kClu && !leader) mbar_wait_cluster(&sfull[r], rph);
+        else mbar_wait(&sfull[r], rph);
         const int t = sched_tile[r];
         __syncwarp();
-        if (elect_one()) mbar_arrive(&sempty[r]);
+        if (elect_one()) {
+          if (kClu && !leader) mbar_arrive_cluster(leader_addr(&sempty[r]));
+          else mbar_arrive(&sempty[r]);
+        }
         __syncwarp();
         if (++r == TC_SCHED) { r = 0; rph ^= 1; }
         return t;
@@ -452,7 +501,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         TC_TRACE(t, 3);
         const TcProblem& pr = P.prob[tl.p];
         TC_TRACE(t, 8);   // decoded
-        const uint32_t idesc = umma_idesc_bf16(Cfg::TILE_M, TC_BN, pr.a_mn, pr.b_mn);
+        const uint32_t idesc = umma_idesc_bf16(Cfg::MMA_M, TC_BN, pr.a_mn, pr.b_mn);
         const uint32_t a_lbo = pr.a_mn ? 8192u : 16u;
         const uint32_t b_lbo = pr.b_mn ? 8192u : 16u;
         const uint32_t a_kstep = pr.a_mn ? 2048u : 32u;
@@ -480,6 +529,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
               else umma_bf16(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
             }
             if constexpr (kPair == 2) umma_commit_pair(&empty[s]);
+            else if constexpr (kMc) umma_commit_mc(&empty[s], 3);
             else umma_commit(&empty[s]);
           }
           __syncwarp();
@@ -513,12 +563,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     int acc = 0;
     uint32_t aph = 0;
     for (;;) {
-      if (kPair == 2 && !leader) mbar_wait_cluster(&sfull[r], rph);
+      if (kClu && !leader) mbar_wait_cluster(&sfull[r], rph);
       else mbar_wait(&sfull[r], rph);
       const int t = sched_tile[r];
       __syncwarp();
       if (lane == 0) {
-        if (kPair == 2 && !leader) mbar_arrive_cluster(leader_addr(&sempty[r]));
+        if (kClu && !leader) mbar_arrive_cluster(leader_addr(&sempty[r]));
         else mbar_arrive(&sempty[r]);
       }
       if (++r == TC_SCHED) { r = 0; rph ^= 1; }
@@ -646,7 +696,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     if (lane == 0) bulk_wait0();
   }
   tc_fence_before();
-  if constexpr (kPair == 2) cluster_sync();
+  if constexpr (kClu) cluster_sync();
   else __syncthreads();
   tc_fence_after();
   if (warp == kWarpAlloc) {

@@ -16,6 +16,8 @@ if os.environ.get("ATTN_VC"):
     binding.attn_softmax_set_option("vocab_chunk", int(os.environ["ATTN_VC"]))
 if os.environ.get("ATTN_PAIR"):
     binding.attn_softmax_set_option("cta_pair", int(os.environ["ATTN_PAIR"]))
+if os.environ.get("ATTN_MCAST"):
+    binding.attn_softmax_set_option("b_multicast", int(os.environ["ATTN_MCAST"]))
 if os.environ.get("ATTN_CTAS"):
     binding.attn_softmax_set_option("gemm_ctas", int(os.environ["ATTN_CTAS"]))
 binding.attn_softmax_set_option("stage_events", 1)

@@ -10,11 +10,12 @@ binding.attn_softmax_set_option("gemm_variant", int(sys.argv[8]) if len(sys.argv
 if len(sys.argv) > 8 and False:
     binding.attn_softmax_set_option("gemm_variant", int(sys.argv[8]))
 binding.attn_softmax_set_option("cta_pair", 8 if pair == 2 else 0)
+binding.attn_softmax_set_option("b_multicast", 8 if pair == 3 else 0)
 binding.attn_softmax_set_option("debug_epilogue", epi)
 A = torch.randn(K, M, device="cuda").bfloat16() if amn else torch.randn(M, K, device="cuda").bfloat16()
 B = torch.randn(K, N, device="cuda").bfloat16() if bmn else torch.randn(N, K, device="cuda").bfloat16()
 C = torch.empty(M, N, device="cuda")  # fp32 (bf16 epilogues use its first half)
-tm = 128 * pair
+tm = 128 * (2 if pair >= 2 else 1)
 tiles = ((M + tm - 1) // tm) * ((N + 255) // 256)
 tr = torch.zeros(tiles * 16, dtype=torch.int64, device="cuda")
 for _ in range(3):

@@ -47,7 +47,7 @@ def oracle(inp, scale):
 
 
 # ------------------------------------------------------------ GEMM core ----
-@pytest.mark.parametrize("pair", [1, 2])
+@pytest.mark.parametrize("pair", [1, 2, 3])
 @pytest.mark.parametrize("mn3d", [0, 1])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 0), (0, 1), (1, 1)])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (296, 520, 200), (1000, 264, 1536),
@@ -59,6 +59,7 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, pair):
     from paper_1909_00562_b200 import binding
     binding.attn_softmax_set_option("mn_3d_tma", mn3d)
     binding.attn_softmax_set_option("cta_pair", 8 if pair == 2 else 0)
+    binding.attn_softmax_set_option("b_multicast", 8 if pair == 3 else 0)
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N + K)
     A = torch.randn(M, K, generator=g).bfloat16()
     B = torch.randn(N, K, generator=g).bfloat16()
@@ -70,6 +71,7 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, pair):
     torch.cuda.synchronize()
     binding.attn_softmax_set_option("mn_3d_tma", 1)
     binding.attn_softmax_set_option("cta_pair", 14)
+    binding.attn_softmax_set_option("b_multicast", 0)
     err = (C.double().cpu() - ref).abs().max().item()
     assert err < 1e-3 * max(1.0, ref.abs().max().item()), err
 
@@ -79,18 +81,22 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, pair):
                                           ("small_f32", 0, 8), ("small_f32", 256, 8),
                                           ("small", 0, 8), ("small", 1024, 8), ("small", 0, 15),
                                           ("medium", 0, 8), ("medium", 2048, 8),
-                                          ("medium", 2048, 15)])
+                                          ("medium", 2048, 15), ("small", 0, -15),
+                                          ("medium", 1024, -15)])
 def test_parity_vs_oracle(cuda_lib, name, vc, pair):
-    """pair = cta_pair bitmask (15: every non-batched GEMM group on CTA pairs)."""
+    """pair = cta_pair bitmask (15: every non-batched GEMM group on CTA pairs);
+    negative = the same bitmask for B-multicast clusters."""
     from paper_1909_00562_b200 import binding
     cfg = CONFIGS[name]
     inp = make_inputs(cfg)
     scale = 1.0 / global_valid_tokens(cfg, cfg.B)
-    binding.attn_softmax_set_option("cta_pair", pair)
+    binding.attn_softmax_set_option("cta_pair", max(pair, 0))
+    binding.attn_softmax_set_option("b_multicast", max(-pair, 0))
     try:
         g = run_gpu(cfg, inp, scale, vocab_chunk=vc)
     finally:
         binding.attn_softmax_set_option("cta_pair", 14)
+        binding.attn_softmax_set_option("b_multicast", 0)
     f, b = oracle(inp, scale)
     tol = TOL[cfg.dtype]
     assert abs(g["loss"] - f["loss"]) <= tol["loss"] * abs(f["loss"]), (g["loss"], f["loss"])
