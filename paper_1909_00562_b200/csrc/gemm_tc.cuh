@@ -110,6 +110,11 @@ __device__ __forceinline__ long long clk64() {
       if (lane == 2) P.trace[(long long)(t) * 16 + (i)] = c_;           \
     }                                                                   \
   } while (0)
+__device__ __forceinline__ long long gtime() {
+  long long c;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(c));
+  return c;
+}
 __device__ __forceinline__ uint32_t smid() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -534,6 +539,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           }
           __syncwarp();
           if (kb == 0) TC_TRACE(t, 4);   // first MMAs issued
+          if (kb == 0 && P.trace) {
+            const long long gt = gtime();
+            if (lane == 2) P.trace[(long long)t * 16 + 14] = gt;
+          }
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
           if (kb == kb_read) {
             t_nxt = read_tile();
@@ -546,6 +555,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         }
         __syncwarp();
         TC_TRACE(t, 5);   // last commit issued
+        if (P.trace) {
+          const long long gt = gtime();
+          if (lane == 2) P.trace[(long long)t * 16 + 15] = gt;
+        }
         if (++acc == 2) { acc = 0; aph ^= 1; }
         t = t_nxt;
         tl = tl_nxt;
