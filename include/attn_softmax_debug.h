@@ -66,7 +66,6 @@ long long attn_softmax_last_launches(void);
  *   "b_multicast"   bitmask (same bits as cta_pair) of GEMM groups run on
  *                   2-CTA clusters that share the B tile by TMA multicast
  *                   (two 128 x 256 tiles, per-CTA MMAs); wins over cta_pair
- *   "gemm_variant"  debug experiment bits of the GEMM producer (0 = default)
  *   "gemm_trace"    device address of an int64 buffer (16 per tile) that the
  *                   next tcgen05 launches fill with per-tile clock64 stamps
  *                   (0 = off; debug only)

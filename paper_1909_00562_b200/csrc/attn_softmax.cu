@@ -108,7 +108,6 @@ static int g_debug_epi = 0;
 static int g_opt_mn3d = 1;  // MN-major operands via one 3D TMA box
 static int g_opt_pair = PAIR_DEFAULT;
 static int g_opt_mcast = 0;   // "b_multicast": bitmask of GEMM groups on 2-CTA clusters sharing B
-static int g_opt_variant = 0;   // "gemm_variant": debug experiment bits
 static long long* g_trace = nullptr;   // "gemm_trace": device pointer of a per-tile trace buffer
 static long long g_trace_launch = -1;  // "gemm_trace_launch": trace only this launch index of a call (-1 = all)
 static int64_t g_opt_vocab_chunk = 0;
@@ -129,10 +128,6 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "gemm_trace")) {
     g_trace = reinterpret_cast<long long*>(value);
-    return ATTN_OK;
-  }
-  if (!strcmp(key, "gemm_variant")) {
-    g_opt_variant = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "b_multicast")) {
@@ -247,7 +242,7 @@ static attn_status_t operand_map(CUtensorMap* m, const Operand& o, bool mn, int 
     cuuint64_t dims[3] = {(cuuint64_t)std::max(1ll, o.k_ext), (cuuint64_t)std::max(1ll, o.mn_ext),
                           (cuuint64_t)batch};
     cuuint64_t st[2] = {(cuuint64_t)(o.ld * 2), (cuuint64_t)(bs * 2)};
-    cuuint32_t box[3] = {64, (cuuint32_t)((is_b && (g_opt_variant & 1)) ? 64 : box_rows), 1};
+    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
     *mode = 0;
     return encode(m, o.p, false, 3, dims, st, box);
   }
@@ -381,7 +376,6 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   P.nprob = n;
   P.total_tiles = tiles;
   P.tile_counter = counter;
-  P.variant = g_opt_variant;
   P.trace = (g_trace_launch < 0 || g_trace_launch == g_launches) ? g_trace : nullptr;
   if (tiles == 0) return ATTN_OK;
   const DevInfo di = dev_info();

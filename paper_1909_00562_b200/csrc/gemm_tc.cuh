@@ -88,7 +88,6 @@ struct alignas(64) TcParams {
   int nprob;
   int total_tiles;
   int* tile_counter;
-  int variant;   // debug experiment bits (0 = production path)
   long long* trace;   // debug: per-tile timestamps (null = off); 8 x int64 per tile
 };
 
@@ -254,26 +253,6 @@ __device__ __forceinline__ void epi_attn_softmax_bwd(const EpiParams& e, uint32_
   }
 }
 
-// Write one staged 32-row x 128-byte block (128-byte swizzled rows, as the
-// TMA store expects) with coalesced 16-byte global stores: lane l moves
-// granule l%8 of rows l/8, l/8+4, ...  Rows >= row_lim and bytes past
-// col_bytes_lim are skipped.  accumulate = fp32 reduce-add.
-__device__ __forceinline__ void stg_block(uint32_t stg, uint8_t* gbase, long long ld_bytes,
-                                          int row_lim, int col_bytes_lim, uint32_t lane,
-                                          bool accumulate) {
-  const uint32_t gi = lane & 7;
-  if ((int)(gi * 16) >= col_bytes_lim) return;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int row = (int)(lane >> 3) + 4 * i;
-    if (row >= row_lim) break;
-    const uint4 v = ld_shared_v4(stg + row * 128 + ((gi ^ (row & 7)) << 4));
-    uint8_t* p = gbase + (long long)row * ld_bytes + gi * 16;
-    if (accumulate) red_add_v4_f32(reinterpret_cast<float*>(p), v);
-    else *reinterpret_cast<uint4*>(p) = v;
-  }
-}
-
 template <typename OutT, bool kFast, int kPair>
 __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_constant__ TcParams P) {
   using Cfg = TcCfg<kPair>;
@@ -343,12 +322,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     uint32_t ph = 0;
     int r = 0;
     uint32_t rph = 0;
-    int loads_issued = 0;
-    const bool static_sched = (P.variant & 8) != 0;   // experiment: round-robin, no atomic
-    const int unit = blockIdx.x / kPair, nunits = gridDim.x / kPair;
     int t_raw = 0;   // lane 1: result of the latest tile-counter fetch
-    auto fetch = [&](int prev) {
-      if (lane == 1) t_raw = static_sched ? (prev < 0 ? unit : prev + nunits) : atomicAdd(P.tile_counter, 1);
+    auto fetch = [&](int) {
+      if (lane == 1) t_raw = atomicAdd(P.tile_counter, 1);
     };
     // next tile id: the leader takes it from the counter and publishes it to
     // its ring (and the peer's); the peer reads its ring
@@ -401,12 +377,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           uint8_t* sB = sA + TC_A_BYTES;
           uint32_t barc = 0;
           if constexpr (kPair == 2) barc = leader_addr(&full[s]);
-          const bool noload = (P.variant & 4) && loads_issued >= Cfg::STAGES;
-          ++loads_issued;
-          if (noload) {
-            // experiment: no more TMA traffic, MMAs rerun the resident stages
-            if (leader || kMc) mbar_arrive(&full[s]);
-          } else if constexpr (kMc) {
+          if constexpr (kMc) {
             // own A rows; own half of B, multicast into both CTAs' B tile
             mbar_arrive_expect_tx(&full[s], Cfg::STAGE);
             const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
@@ -612,7 +583,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
 #pragma unroll 1
         for (int c = 0; c < n_act; ++c) {
           float v[32];
-          if ((P.variant & 32) && c > 0) __nanosleep(400);   // experiment: pace the stores
           tmem_ld32(taddr + c * 32, v);
           const int col = col_h + c * 32;
           if (kind == EPI_LSE) {
@@ -641,14 +611,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
               st_shared_v4(stg + lane * 128 + ((g ^ swz) << 4), __float_as_uint(v[4 * g]),
                            __float_as_uint(v[4 * g + 1]), __float_as_uint(v[4 * g + 2]),
                            __float_as_uint(v[4 * g + 3]));
-            if (P.variant & 16) {
-              __syncwarp();
-              uint8_t* gb = reinterpret_cast<uint8_t*>(pr.epi.out) +
-                            ((long long)tl.b * pr.M * pr.epi.ldo + (long long)row0 * pr.epi.ldo + col) * 4;
-              stg_block(stg, gb, pr.epi.ldo * 4, pr.M - row0, (pr.epi.ncols_store - col) * 4, lane,
-                        kind == EPI_ACCUM_F32);
-              __syncwarp();
-            } else {
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
@@ -657,7 +619,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
               else
                 tma_store_3d(omap, staging + ew * TC_STG_BYTES, col, row0, tl.b);
               bulk_commit();
-            }
             }
           } else {
             if ((c & 1) == 0) {
@@ -676,21 +637,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
               st_shared_v4(stg + lane * 128 + ((gi ^ swz) << 4), w[0], w[1], w[2], w[3]);
             }
             if ((c & 1) == 1 || c == n_act - 1) {
-              if (P.variant & 16) {
-                __syncwarp();
-                const int c0 = col_h + (c & ~1) * 32;
-                uint8_t* gb = reinterpret_cast<uint8_t*>(pr.epi.out) +
-                              ((long long)tl.b * pr.M * pr.epi.ldo + (long long)row0 * pr.epi.ldo + c0) * 2;
-                stg_block(stg, gb, pr.epi.ldo * 2, pr.M - row0, (pr.epi.ncols_store - c0) * 2, lane,
-                          false);
-                __syncwarp();
-              } else {
               fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0) {
                 tma_store_3d(omap, staging + ew * TC_STG_BYTES, col_h + (c & ~1) * 32, row0, tl.b);
                 bulk_commit();
-              }
               }
             }
           }

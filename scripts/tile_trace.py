@@ -6,9 +6,6 @@ import torch
 from paper_1909_00562_b200 import binding, build
 build.build()
 M, N, K, amn, bmn, pair, epi = (int(x) for x in sys.argv[1:8])
-binding.attn_softmax_set_option("gemm_variant", int(sys.argv[8]) if len(sys.argv) > 8 else 0)
-if len(sys.argv) > 8 and False:
-    binding.attn_softmax_set_option("gemm_variant", int(sys.argv[8]))
 binding.attn_softmax_set_option("cta_pair", 8 if pair == 2 else 0)
 binding.attn_softmax_set_option("b_multicast", 8 if pair == 3 else 0)
 binding.attn_softmax_set_option("debug_epilogue", epi)
