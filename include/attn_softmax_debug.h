@@ -62,7 +62,7 @@ long long attn_softmax_last_launches(void);
  *                   cta_group::2, 256 x 256 tiles) instead of single CTAs
  *                   (128 x 256): 1 = forward vocab / projection, 2 = vocab
  *                   backward chunks, 4 = projection backward, 8 = the debug
- *                   GEMM entry.  Default 14.
+ *                   GEMM entry.  Default 8.
  *   "b_multicast"   bitmask (same bits as cta_pair) of GEMM groups run on
  *                   2-CTA clusters that share the B tile by TMA multicast
  *                   (two 128 x 256 tiles, per-CTA MMAs); wins over cta_pair

@@ -102,7 +102,7 @@ extern "C" long long attn_softmax_last_launches(void) { return g_launches; }
 
 // ------------------------------------------------------------------ options
 // cta_pair option: bitmask of GEMM groups run on CTA pairs (see PAIR_*)
-#define PAIR_DEFAULT (2 | 4 | 8)   /* backward groups + debug entry on CTA pairs; forward vocab single (measured) */
+#define PAIR_DEFAULT 8   /* stage GEMMs on single CTAs (same-box A/B: fastest); debug entry paired */
 // debug_epilogue option: 0 = fp32 TMA store, 1 = accumulator read only (no store)
 static int g_debug_epi = 0;
 static int g_opt_mn3d = 1;  // MN-major operands via one 3D TMA box

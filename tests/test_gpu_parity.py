@@ -70,7 +70,7 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, pair):
     binding.attn_debug_gemm_bf16(M, N, K, Ad, a_mn, Bd, b_mn, C)
     torch.cuda.synchronize()
     binding.attn_softmax_set_option("mn_3d_tma", 1)
-    binding.attn_softmax_set_option("cta_pair", 14)
+    binding.attn_softmax_set_option("cta_pair", 8)
     binding.attn_softmax_set_option("b_multicast", 0)
     err = (C.double().cpu() - ref).abs().max().item()
     assert err < 1e-3 * max(1.0, ref.abs().max().item()), err
@@ -95,7 +95,7 @@ def test_parity_vs_oracle(cuda_lib, name, vc, pair):
     try:
         g = run_gpu(cfg, inp, scale, vocab_chunk=vc)
     finally:
-        binding.attn_softmax_set_option("cta_pair", 14)
+        binding.attn_softmax_set_option("cta_pair", 8)
         binding.attn_softmax_set_option("b_multicast", 0)
     f, b = oracle(inp, scale)
     tol = TOL[cfg.dtype]
