@@ -63,6 +63,9 @@ long long attn_softmax_last_launches(void);
  *                   (128 x 256): 1 = forward vocab / projection, 2 = vocab
  *                   backward chunks, 4 = projection backward, 8 = the debug
  *                   GEMM entry.  Default 8.
+ *   "interleave"    bitmask (same bits as cta_pair) of GEMM groups whose tile
+ *                   dispatch alternates the last problem's tiles with the
+ *                   others' (spreads the dlogits stores of a chunk launch)
  *   "b_multicast"   bitmask (same bits as cta_pair) of GEMM groups run on
  *                   2-CTA clusters that share the B tile by TMA multicast
  *                   (two 128 x 256 tiles, per-CTA MMAs); wins over cta_pair

@@ -108,6 +108,7 @@ static int g_debug_epi = 0;
 static int g_opt_mn3d = 1;  // MN-major operands via one 3D TMA box
 static int g_opt_pair = PAIR_DEFAULT;
 static int g_opt_mcast = 0;   // "b_multicast": bitmask of GEMM groups on 2-CTA clusters sharing B
+static int g_opt_interleave = 0;   // "interleave": bitmask of GEMM groups with interleaved dispatch
 static long long* g_trace = nullptr;   // "gemm_trace": device pointer of a per-tile trace buffer
 static long long g_trace_launch = -1;  // "gemm_trace_launch": trace only this launch index of a call (-1 = all)
 static int64_t g_opt_vocab_chunk = 0;
@@ -128,6 +129,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "gemm_trace")) {
     g_trace = reinterpret_cast<long long*>(value);
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "interleave")) {
+    g_opt_interleave = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "b_multicast")) {
@@ -358,7 +363,8 @@ static int tc_smem_bytes() { return TC_SMEM_BYTES; }
 // g_opt_pair: vocab / projection GEMMs on CTA pairs (cta_group::2)
 
 template <typename OutT, int kPair>
-static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, cudaStream_t stream) {
+static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, cudaStream_t stream,
+                                       int group_bit) {
   static bool attr_set = false;
   if (!attr_set) {
     CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<OutT, true, kPair>,
@@ -375,6 +381,7 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   }
   P.nprob = n;
   P.total_tiles = tiles;
+  P.interleave = (group_bit & g_opt_interleave) ? 1 : 0;
   P.tile_counter = counter;
   P.trace = (g_trace_launch < 0 || g_trace_launch == g_launches) ? g_trace : nullptr;
   if (tiles == 0) return ATTN_OK;
@@ -407,9 +414,11 @@ enum : int { PAIR_FWD = 1, PAIR_VBWD = 2, PAIR_PBWD = 4, PAIR_DEBUG = 8 };
 template <typename OutT>
 static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cudaStream_t stream,
                                      int group_bit = 0) {
-  if (group_bit && (g_opt_mcast & group_bit)) return launch_tc_group_k<OutT, 3>(gs, n, counter, stream);
-  if (group_bit && (g_opt_pair & group_bit)) return launch_tc_group_k<OutT, 2>(gs, n, counter, stream);
-  return launch_tc_group_k<OutT, 1>(gs, n, counter, stream);
+  if (group_bit && (g_opt_mcast & group_bit))
+    return launch_tc_group_k<OutT, 3>(gs, n, counter, stream, group_bit);
+  if (group_bit && (g_opt_pair & group_bit))
+    return launch_tc_group_k<OutT, 2>(gs, n, counter, stream, group_bit);
+  return launch_tc_group_k<OutT, 1>(gs, n, counter, stream, group_bit);
 }
 
 static attn_status_t launch_simt_group(const GemmDesc* gs, int n, cudaStream_t stream) {
