@@ -475,6 +475,7 @@ static attn_status_t check_shape(const attn_shape_t* s) {
   return ATTN_OK;
 }
 
+constexpr int kNumCounters = 1024;
 struct Plan {
   int B, N, M, d, V;
   long long T;
@@ -491,7 +492,6 @@ struct Plan {
   int Mp;             // bf16 path: row stride of the bf16 alpha / de operands (64-multiple)
   size_t total;
 };
-constexpr int kNumCounters = 1024;
 
 static Plan make_plan(const attn_shape_t* s) {
   Plan p;
@@ -513,6 +513,8 @@ static Plan make_plan(const attn_shape_t* s) {
     vc = std::max(vc, 1024ll);
   }
   vc = std::min(vc, vpad);
+  // one tile counter per tcgen05 launch: keep the chunk count well inside
+  while ((p.V + vc - 1) / vc > kNumCounters - 64) vc += 256;
   p.Vc = (int)vc;
   p.nchunks = (int)((p.V + p.Vc - 1) / p.Vc);
   size_t o = 0;

@@ -67,6 +67,10 @@ CONFIGS = {
     "small_f32": Config("small_f32", 5, 13, 11, 40, 300, "f32", 5, "ragged"),
     "small": Config("small", 7, 37, 41, 256, 3001, "bf16", 6, "ragged"),
     "medium": Config("medium", 16, 50, 50, 512, 9000, "bf16", 7, "ragged"),
+    # awkward shapes: d not a multiple of 256, N > 128 (two attention row
+    # tiles per sentence), M not a multiple of 64, V tiny and odd
+    "odd": Config("odd", 3, 130, 100, 320, 777, "bf16", 8, "ragged"),
+    "odd_f32": Config("odd_f32", 3, 17, 9, 24, 77, "f32", 9, "ragged"),
 }
 
 

@@ -82,7 +82,8 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, pair):
                                           ("small", 0, 8), ("small", 1024, 8), ("small", 0, 15),
                                           ("medium", 0, 8), ("medium", 2048, 8),
                                           ("medium", 2048, 15), ("small", 0, -15),
-                                          ("medium", 1024, -15)])
+                                          ("medium", 1024, -15), ("odd", 0, 8), ("odd", 256, 15),
+                                          ("odd_f32", 0, 8)])
 def test_parity_vs_oracle(cuda_lib, name, vc, pair):
     """pair = cta_pair bitmask (15: every non-batched GEMM group on CTA pairs);
     negative = the same bitmask for B-multicast clusters."""
