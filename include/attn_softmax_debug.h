@@ -66,6 +66,11 @@ long long attn_softmax_last_launches(void);
  *   "interleave"    bitmask (same bits as cta_pair) of GEMM groups whose tile
  *                   dispatch alternates the last problem's tiles with the
  *                   others' (spreads the dlogits stores of a chunk launch)
+ *   "wide_tiles"    bitmask (same bits as cta_pair) of GEMM groups run on
+ *                   wide single-CTA 256 x 256 tiles (two M = 128 MMAs share
+ *                   each B tile; one tile in TMEM at a time).  Default 2 (the
+ *                   vocab backward; the automatic V-chunk then holds at least
+ *                   two long tiles per SM).  Takes precedence over cta_pair.
  *   "b_multicast"   bitmask (same bits as cta_pair) of GEMM groups run on
  *                   2-CTA clusters that share the B tile by TMA multicast
  *                   (two 128 x 256 tiles, per-CTA MMAs); wins over cta_pair

@@ -13,7 +13,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libattnsm.so")
+# ATTNSM_LIB: load another build of the same library (same-box A/B timing)
+LIB_PATH = os.environ.get("ATTNSM_LIB") or os.path.join(_HERE, "lib", "libattnsm.so")
 
 ATTN_F32, ATTN_BF16 = 0, 1
 STATUS = {0: "ATTN_OK", 1: "ATTN_ERR_INVALID_ARG", 2: "ATTN_ERR_SHAPE",

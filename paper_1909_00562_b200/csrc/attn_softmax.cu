@@ -101,6 +101,10 @@ extern "C" attn_status_t attn_softmax_stage_time(int i, const char** name, float
 extern "C" long long attn_softmax_last_launches(void) { return g_launches; }
 
 // ------------------------------------------------------------------ options
+// GEMM groups, the bits of the cta_pair / b_multicast / wide_tiles / interleave
+// options: forward vocab + projection, vocab backward chunks, projection
+// backward, the debug GEMM entry
+enum : int { PAIR_FWD = 1, PAIR_VBWD = 2, PAIR_PBWD = 4, PAIR_DEBUG = 8 };
 // cta_pair option: bitmask of GEMM groups run on CTA pairs (see PAIR_*)
 #define PAIR_DEFAULT 8   /* stage GEMMs on single CTAs (same-box A/B: fastest); debug entry paired */
 // debug_epilogue option: 0 = fp32 TMA store, 1 = accumulator read only (no store)
@@ -108,6 +112,9 @@ static int g_debug_epi = 0;
 static int g_opt_mn3d = 1;  // MN-major operands via one 3D TMA box
 static int g_opt_pair = PAIR_DEFAULT;
 static int g_opt_mcast = 0;   // "b_multicast": bitmask of GEMM groups on 2-CTA clusters sharing B
+// "wide_tiles": bitmask of GEMM groups on 256 x 256 single-CTA tiles; default
+// the vocab backward (same-box A/B at C1 / C3 / C4: -6 to -8% per step)
+static int g_opt_wide = PAIR_VBWD;
 static int g_opt_interleave = 0;   // "interleave": bitmask of GEMM groups with interleaved dispatch
 static long long* g_trace = nullptr;   // "gemm_trace": device pointer of a per-tile trace buffer
 static long long g_trace_launch = -1;  // "gemm_trace_launch": trace only this launch index of a call (-1 = all)
@@ -133,6 +140,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "interleave")) {
     g_opt_interleave = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "wide_tiles")) {
+    g_opt_wide = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "b_multicast")) {
@@ -267,10 +278,12 @@ static attn_status_t operand_map(CUtensorMap* m, const Operand& o, bool mn, int 
   return encode(m, o.p, false, 3, dims, st, box);
 }
 
+// pair: 1 = 128 x 256 tiles, 2 = CTA pair (256 rows, B split), 4 = wide
+// single CTA (256 rows, whole B tile)
 static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr, int tile_begin,
                              int pair) {
   memset(&pr, 0, sizeof(pr));
-  const int tile_m = TC_BM * pair, b_rows = TC_BN / pair;
+  const int tile_m = pair == 1 ? TC_BM : 2 * TC_BM, b_rows = pair == 2 ? TC_BN / 2 : TC_BN;
   pr.M = g.M; pr.N = g.N; pr.K = g.K; pr.batch = g.batch;
   pr.tiles_m = (g.M + tile_m - 1) / tile_m;
   pr.tiles_n = (g.N + TC_BN - 1) / TC_BN;
@@ -375,7 +388,8 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   memset(&P, 0, sizeof(P));
   int tiles = 0;
   for (int i = 0; i < n; ++i) {
-    attn_status_t st = fill_tc(gs[i], P.maps[i], P.prob[i], tiles, kPair >= 2 ? 2 : 1);
+    attn_status_t st = fill_tc(gs[i], P.maps[i], P.prob[i], tiles,
+                               kPair == 4 ? 4 : (kPair >= 2 ? 2 : 1));
     if (st != ATTN_OK) return st;
     tiles += P.prob[i].tiles_m * P.prob[i].tiles_n * P.prob[i].batch;
   }
@@ -386,7 +400,7 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   P.trace = (g_trace_launch < 0 || g_trace_launch == g_launches) ? g_trace : nullptr;
   if (tiles == 0) return ATTN_OK;
   const DevInfo di = dev_info();
-  const int csize = kPair >= 2 ? 2 : 1;
+  const int csize = TcCfg<kPair>::CLUSTER;
   int units = (g_opt_gemm_ctas > 0 ? (int)g_opt_gemm_ctas : di.sms) / csize;
   units = std::max(1, std::min(units, tiles));
   cudaLaunchConfig_t cfg = {};
@@ -396,11 +410,11 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kPair >= 2 ? 2 : 1;
+  attr[0].val.clusterDim.x = csize;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = kPair >= 2 ? 1 : 0;
+  cfg.numAttrs = csize > 1 ? 1 : 0;
   CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<OutT, true, kPair>, P));
   ++g_launches;
   return ATTN_OK;
@@ -410,10 +424,11 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
 // single CTAs (a sentence has <= 128 decoder rows).
 // `group_bit` selects the bit of the "cta_pair" option that enables pairs for
 // this GEMM group (0 = never paired).
-enum : int { PAIR_FWD = 1, PAIR_VBWD = 2, PAIR_PBWD = 4, PAIR_DEBUG = 8 };
 template <typename OutT>
 static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cudaStream_t stream,
                                      int group_bit = 0) {
+  if (group_bit && (g_opt_wide & group_bit))
+    return launch_tc_group_k<OutT, 4>(gs, n, counter, stream, group_bit);
   if (group_bit && (g_opt_mcast & group_bit))
     return launch_tc_group_k<OutT, 3>(gs, n, counter, stream, group_bit);
   if (group_bit && (g_opt_pair & group_bit))
@@ -511,6 +526,14 @@ static Plan make_plan(const attn_shape_t* s) {
     // C1 / C3 / C4)
     vc = ((p.V + 11) / 12 + 255) / 256 * 256;
     vc = std::max(vc, 1024ll);
+    if (p.bf16 && (g_opt_wide & PAIR_VBWD)) {
+      // wide 256 x 256 tiles: widen the chunk until one launch holds at least
+      // two long (dW_out + dHc) tiles per SM of a B200 (148 SMs; a fixed
+      // constant so the workspace size does not depend on the device)
+      const long long ntd = (p.d + 255) / 256, ntt = (p.T + 255) / 256;
+      const long long need = 2 * 148 / ntd - ntt;   // dW_out row tiles per chunk
+      if (need > 0) vc = std::max(vc, need * 256);
+    }
   }
   vc = std::min(vc, vpad);
   // one tile counter per tcgen05 launch: keep the chunk count well inside

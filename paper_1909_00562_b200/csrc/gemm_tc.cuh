@@ -57,15 +57,24 @@ constexpr int kMaxProblems = 4;
 //            multicasts it to both, so both MMAs (cta_group::1) read local
 //            shared memory while the L2 -> SM operand traffic per FLOP drops
 //            by a third (48 KB stages, 4 of them).
+// kPair = 4 ("wide"): one CTA computes a 256 x 256 tile as two M = 128 MMAs
+//            per K step that share the B tile (accumulators in TMEM columns
+//            0-255 and 256-511): twice the MMA work per staged byte of the
+//            128 x 256 tile, at the price of one tile in TMEM at a time (the
+//            epilogue is not overlapped with the next tile's MMAs).  64 KB
+//            stages, 3 of them.
 template <int kPair>
 struct TcCfg {
+  static constexpr bool WIDE = kPair == 4;
   static constexpr int TILE_M = kPair == 1 ? TC_BM : 2 * TC_BM;   // rows per scheduled tile
   static constexpr int MMA_M = kPair == 2 ? 2 * TC_BM : TC_BM;     // UMMA M
-  static constexpr int B_ROWS = kPair == 1 ? TC_BN : TC_BN / 2;    // B rows loaded per CTA
+  static constexpr int B_ROWS = (kPair == 2 || kPair == 3) ? TC_BN / 2 : TC_BN;   // B rows loaded per CTA
+  static constexpr int A_SMEM = (WIDE ? 2 : 1) * TC_A_BYTES;
   static constexpr int B_SMEM = (kPair == 2 ? TC_BN / 2 : TC_BN) * TC_BK * 2;
-  static constexpr int STAGE = TC_A_BYTES + B_SMEM;                // 48 KB | 32 KB | 48 KB
-  static constexpr int STAGES = TC_RING_BYTES / STAGE;             // 4 | 6 | 4
-  static constexpr int CLUSTER = kPair == 1 ? 1 : 2;
+  static constexpr int STAGE = A_SMEM + B_SMEM;                    // 48 | 32 | 48 | 64 KB
+  static constexpr int STAGES = TC_RING_BYTES / STAGE;             // 4 | 6 | 4 | 3
+  static constexpr int CLUSTER = (kPair == 2 || kPair == 3) ? 2 : 1;
+  static constexpr int ACCS = WIDE ? 1 : 2;                        // tiles resident in TMEM
 };
 
 struct TcProblem {
@@ -281,7 +290,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
 
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();
-  constexpr bool kClu = kPair >= 2;     // cluster of 2 CTAs
+  constexpr bool kClu = kPair == 2 || kPair == 3;   // cluster of 2 CTAs
+  constexpr bool kWide = Cfg::WIDE;
   constexpr bool kMc = kPair == 3;      // B multicast, per-CTA MMAs
   const uint32_t rank = kClu ? cluster_ctarank() : 0;   // 0 = cluster leader
   const bool leader = rank == 0;
@@ -383,7 +393,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         mbar_wait(&empty[s], ph ^ 1);
         if (elect_one()) {
           uint8_t* sA = smem + s * Cfg::STAGE;
-          uint8_t* sB = sA + TC_A_BYTES;
+          uint8_t* sB = sA + Cfg::A_SMEM;
           uint32_t barc = 0;
           if constexpr (kPair == 2) barc = leader_addr(&full[s]);
           if constexpr (kMc) {
@@ -413,11 +423,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
               tc_load_operand_mc(sBh, mb, &full[s], pr.b_mode, Cfg::B_ROWS, bn0, kbk, tl.b);
             }
           } else {
-            if (leader) mbar_arrive_expect_tx(&full[s], Cfg::STAGE * kPair);
+            if (leader) mbar_arrive_expect_tx(&full[s], Cfg::STAGE * Cfg::CLUSTER);
             const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
             const int ka = (seg1 ? kb - pr.kseg : kb) * TC_BK;
             tc_load_operand<kPair>(sA, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode, TC_BM, am0,
                                    ka, tl.b);
+            if constexpr (kWide)   // the second 128-row half of A
+              tc_load_operand<kPair>(sA + TC_A_BYTES, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode,
+                                     TC_BM, am0 + TC_BM, ka, tl.b);
             const bool bseg1 = seg1 && pr.b_seg;
             const int kbk = (bseg1 ? kb - pr.kseg : kb) * TC_BK + pr.b_koff;
             const CUtensorMap* mb = bseg1 ? mb1 : mb0;
@@ -505,13 +518,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           tc_fence_after();
           if (elect_one()) {
             const uint32_t sA = smem_u32(smem + s * Cfg::STAGE);
-            const uint32_t sB = sA + TC_A_BYTES;
+            const uint32_t sB = sA + Cfg::A_SMEM;
 #pragma unroll
             for (int k = 0; k < TC_BK / 16; ++k) {
               const uint64_t ad = umma_sdesc(sA + k * a_kstep, a_lbo, 1024);
               const uint64_t bd = umma_sdesc(sB + k * b_kstep, b_lbo, 1024);
               if constexpr (kPair == 2) umma_bf16_pair(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
               else umma_bf16(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              if constexpr (kWide) {   // rows 128..255 into TMEM columns 256..511
+                const uint64_t ad2 = umma_sdesc(sA + TC_A_BYTES + k * a_kstep, a_lbo, 1024);
+                umma_bf16(dcol + TC_BN, ad2, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              }
             }
             if constexpr (kPair == 2) umma_commit_pair(&empty[s]);
             else if constexpr (kMc) umma_commit_mc(&empty[s], 3);
@@ -539,7 +556,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           const long long gt = gtime();
           if (lane == 2) P.trace[(long long)t * 16 + 15] = gt;
         }
-        if (++acc == 2) { acc = 0; aph ^= 1; }
+        if (++acc == Cfg::ACCS) { acc = 0; aph ^= 1; }
         t = t_nxt;
         tl = tl_nxt;
       }
@@ -573,11 +590,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       if (warp == 0 && leader) TC_TRACE(t, 6);
-      const int row0 = tl.m0 + TC_BM * rank + q * 32;   // row inside the batch item
+      // wide tiles: two 128-row halves, the second in TMEM columns 256..511
+#pragma unroll 1
+      for (int sub = 0; sub < (kWide ? 2 : 1); ++sub) {
+      const int row0 = tl.m0 + TC_BM * rank + sub * TC_BM + q * 32;   // row inside the batch item
       const int row = row0 + lane;
       const bool row_ok = row < pr.M;
       const int rowg = tl.b * pr.M + (row_ok ? row : 0);   // row of the flattened [batch*M] arrays
-      const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * TC_BN + h * 128;
+      const uint32_t taddr = tmem_base + ((q * 32u) << 16) + (acc + sub) * TC_BN + h * 128;
       const int col_h = tl.n0 + h * 128;
       const int lim = (kind == EPI_LSE || kind == EPI_ATTN_SOFTMAX || kind == EPI_ATTN_SOFTMAX_BWD)
                           ? pr.epi.ncols_valid : pr.epi.ncols_store;
@@ -657,6 +677,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         }
         if (kind == EPI_LSE && row_ok) epi.finish(tl.tn * 2 + h);
       }
+      }
       tc_fence_before();
       __syncwarp();
       if (warp == 0 && leader) TC_TRACE(t, 7);
@@ -664,7 +685,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         if (kPair == 2 && !leader) mbar_arrive_cluster(leader_addr(&tempty[acc]));
         else mbar_arrive(&tempty[acc]);
       }
-      if (++acc == 2) { acc = 0; aph ^= 1; }
+      if (++acc == Cfg::ACCS) { acc = 0; aph ^= 1; }
     }
     if (lane == 0) bulk_wait0();
   }

@@ -11,6 +11,8 @@ build.build()
 idx = int(sys.argv[1])
 if len(sys.argv) > 2:
     binding.attn_softmax_set_option("cta_pair", int(sys.argv[2]))
+wide = int(os.environ.get("ATTN_WIDE", "0"))
+binding.attn_softmax_set_option("wide_tiles", wide)
 cfg = CONFIGS["paper"]
 inp = make_inputs(cfg)
 st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
@@ -33,7 +35,9 @@ kinds = sys.argv[3].split(",") if len(sys.argv) > 3 else None
 span = t[:, 5] - t[:, 4]
 print(f"launch {idx}: {n} tiles; kernel span {(t[:,5].max()-t[:,4].min())} cycles (per-SM clocks, rough)")
 # group by span size (problem types have distinct k-block counts)
-for lo, hi, name in ((0, 13000, "short"), (13000, 40000, "mid"), (40000, 10**9, "long")):
+buckets = (((0, 30000, "short"), (30000, 90000, "mid"), (90000, 10**9, "long")) if wide else
+           ((0, 13000, "short"), (13000, 40000, "mid"), (40000, 10**9, "long")))
+for lo, hi, name in buckets:
     sel = (span >= lo) & (span < hi)
     if sel.sum():
         print(f"  {name:6s} tiles {sel.sum():5d}: MMA span median {np.median(span[sel]):.0f} p90 {np.percentile(span[sel],90):.0f}; epilogue {np.median((t[:,7]-t[:,6])[sel]):.0f}")

@@ -8,11 +8,13 @@ build.build()
 M, N, K, amn, bmn, pair, epi = (int(x) for x in sys.argv[1:8])
 binding.attn_softmax_set_option("cta_pair", 8 if pair == 2 else 0)
 binding.attn_softmax_set_option("b_multicast", 8 if pair == 3 else 0)
+binding.attn_softmax_set_option("wide_tiles", 8 if pair == 4 else 0)
 binding.attn_softmax_set_option("debug_epilogue", epi)
 A = torch.randn(K, M, device="cuda").bfloat16() if amn else torch.randn(M, K, device="cuda").bfloat16()
 B = torch.randn(K, N, device="cuda").bfloat16() if bmn else torch.randn(N, K, device="cuda").bfloat16()
 C = torch.empty(M, N, device="cuda")  # fp32 (bf16 epilogues use its first half)
 tm = 128 * (2 if pair >= 2 else 1)
+kb_units = 2 if pair == 4 else 1   # MMA work per k-block in 128x256x64 units
 tiles = ((M + tm - 1) // tm) * ((N + 255) // 256)
 tr = torch.zeros(tiles * 16, dtype=torch.int64, device="cuda")
 for _ in range(3):
@@ -24,7 +26,7 @@ binding.attn_softmax_set_option("gemm_trace", 0)
 t = tr.view(tiles, 16).cpu().numpy().astype(np.int64)
 kb = (K + 63) // 64
 mma = t[:, 5] - t[:, 4]
-print(f"tiles {tiles}, k-blocks/tile {kb}, ideal MMA cycles/tile {kb*512//pair*pair}")
+print(f"tiles {tiles}, k-blocks/tile {kb}, ideal MMA cycles/tile {kb*512*kb_units}")
 print("MMA span (first issue -> last commit issue) cycles: median %d p10 %d p90 %d" % tuple(np.percentile(mma, [50, 10, 90])))
 # per SM: gap between consecutive tiles' first MMA issues
 gaps, stalls, epis, loadlead = [], [], [], []

@@ -47,19 +47,21 @@ def oracle(inp, scale):
 
 
 # ------------------------------------------------------------ GEMM core ----
-@pytest.mark.parametrize("pair", [1, 2, 3])
+@pytest.mark.parametrize("pair", [1, 2, 3, 4])
 @pytest.mark.parametrize("mn3d", [0, 1])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 0), (0, 1), (1, 1)])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (296, 520, 200), (1000, 264, 1536),
                                    (320, 640, 192)])
 def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, pair):
-    """The tcgen05 engine alone: single CTA (cta_group::1, 128x256 tiles) and
-    CTA pair (cta_group::2, 256x256), all operand majors (MN-major via per-atom
-    boxes or one box per stage), with M/N/K tails."""
+    """The tcgen05 engine alone: single CTA (cta_group::1, 128x256 tiles), CTA
+    pair (cta_group::2, 256x256), B-multicast cluster, and wide single-CTA
+    256x256 tiles; all operand majors (MN-major via per-atom boxes or one box
+    per stage), with M/N/K tails."""
     from paper_1909_00562_b200 import binding
     binding.attn_softmax_set_option("mn_3d_tma", mn3d)
     binding.attn_softmax_set_option("cta_pair", 8 if pair == 2 else 0)
     binding.attn_softmax_set_option("b_multicast", 8 if pair == 3 else 0)
+    binding.attn_softmax_set_option("wide_tiles", 8 if pair == 4 else 0)
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N + K)
     A = torch.randn(M, K, generator=g).bfloat16()
     B = torch.randn(N, K, generator=g).bfloat16()
@@ -69,35 +71,51 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, pair):
     C = torch.full((M, N), float("nan"), device="cuda")
     binding.attn_debug_gemm_bf16(M, N, K, Ad, a_mn, Bd, b_mn, C)
     torch.cuda.synchronize()
+    set_modes(binding, "default")
     binding.attn_softmax_set_option("mn_3d_tma", 1)
-    binding.attn_softmax_set_option("cta_pair", 8)
-    binding.attn_softmax_set_option("b_multicast", 0)
     err = (C.double().cpu() - ref).abs().max().item()
     assert err < 1e-3 * max(1.0, ref.abs().max().item()), err
 
 
 # ------------------------------------------------------ end-to-end parity --
-@pytest.mark.parametrize("name,vc,pair", [("tiny", 0, 8), ("tiny_ragged", 0, 8),
-                                          ("small_f32", 0, 8), ("small_f32", 256, 8),
-                                          ("small", 0, 8), ("small", 1024, 8), ("small", 0, 15),
-                                          ("medium", 0, 8), ("medium", 2048, 8),
-                                          ("medium", 2048, 15), ("small", 0, -15),
-                                          ("medium", 1024, -15), ("odd", 0, 8), ("odd", 256, 15),
-                                          ("odd_f32", 0, 8)])
-def test_parity_vs_oracle(cuda_lib, name, vc, pair):
-    """pair = cta_pair bitmask (15: every non-batched GEMM group on CTA pairs);
-    negative = the same bitmask for B-multicast clusters."""
+def set_modes(binding, mode):
+    """GEMM tile modes per group (bits: 1 forward, 2 vocab backward, 4
+    projection backward, 8 debug entry): "pN" CTA pairs, "mN" B-multicast
+    clusters, "wN" wide single-CTA tiles (the other groups on 128x256
+    single-CTA tiles), "default" the library default (wide vocab backward)."""
+    pair, mcast, wide = 8, 0, 2
+    if mode != "default":
+        mask = int(mode[1:])
+        pair = mask if mode[0] == "p" else 0
+        mcast = mask if mode[0] == "m" else 0
+        wide = mask if mode[0] == "w" else 0
+    binding.attn_softmax_set_option("cta_pair", pair)
+    binding.attn_softmax_set_option("b_multicast", mcast)
+    binding.attn_softmax_set_option("wide_tiles", wide)
+
+
+@pytest.mark.parametrize("name,vc,mode", [("tiny", 0, "p8"), ("tiny_ragged", 0, "p8"),
+                                          ("small_f32", 0, "p8"), ("small_f32", 256, "p8"),
+                                          ("small", 0, "p8"), ("small", 1024, "p8"),
+                                          ("small", 0, "p15"), ("medium", 0, "p8"),
+                                          ("medium", 2048, "p8"), ("medium", 2048, "p15"),
+                                          ("small", 0, "m15"), ("medium", 1024, "m15"),
+                                          ("small", 0, "w15"), ("medium", 2048, "w15"),
+                                          ("small", 0, "w0"), ("medium", 0, "w0"),
+                                          ("medium", 0, "default"), ("small", 0, "default"),
+                                          ("odd", 0, "p8"), ("odd", 256, "p15"), ("odd", 256, "w15"),
+                                          ("odd_f32", 0, "p8")])
+def test_parity_vs_oracle(cuda_lib, name, vc, mode):
+    """mode = GEMM tile modes per group (see set_modes)."""
     from paper_1909_00562_b200 import binding
     cfg = CONFIGS[name]
     inp = make_inputs(cfg)
     scale = 1.0 / global_valid_tokens(cfg, cfg.B)
-    binding.attn_softmax_set_option("cta_pair", max(pair, 0))
-    binding.attn_softmax_set_option("b_multicast", max(-pair, 0))
+    set_modes(binding, mode)
     try:
         g = run_gpu(cfg, inp, scale, vocab_chunk=vc)
     finally:
-        binding.attn_softmax_set_option("cta_pair", 8)
-        binding.attn_softmax_set_option("b_multicast", 0)
+        set_modes(binding, "default")
     f, b = oracle(inp, scale)
     tol = TOL[cfg.dtype]
     assert abs(g["loss"] - f["loss"]) <= tol["loss"] * abs(f["loss"]), (g["loss"], f["loss"])
