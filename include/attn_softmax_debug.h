@@ -63,9 +63,6 @@ long long attn_softmax_last_launches(void);
  *                   (128 x 256): 1 = forward vocab / projection, 2 = vocab
  *                   backward chunks, 4 = projection backward, 8 = the debug
  *                   GEMM entry.  Default 8.
- *   "interleave"    bitmask (same bits as cta_pair) of GEMM groups whose tile
- *                   dispatch alternates the last problem's tiles with the
- *                   others' (spreads the dlogits stores of a chunk launch)
  *   "wide_tiles"    bitmask (same bits as cta_pair) of GEMM groups run on
  *                   wide single-CTA 256 x 256 tiles (two M = 128 MMAs share
  *                   each B tile; one tile in TMEM at a time).  Default 2 (the

@@ -101,7 +101,7 @@ extern "C" attn_status_t attn_softmax_stage_time(int i, const char** name, float
 extern "C" long long attn_softmax_last_launches(void) { return g_launches; }
 
 // ------------------------------------------------------------------ options
-// GEMM groups, the bits of the cta_pair / b_multicast / wide_tiles / interleave
+// GEMM groups, the bits of the cta_pair / b_multicast / wide_tiles
 // options: forward vocab + projection, vocab backward chunks, projection
 // backward, the debug GEMM entry
 enum : int { PAIR_FWD = 1, PAIR_VBWD = 2, PAIR_PBWD = 4, PAIR_DEBUG = 8 };
@@ -115,7 +115,6 @@ static int g_opt_mcast = 0;   // "b_multicast": bitmask of GEMM groups on 2-CTA 
 // "wide_tiles": bitmask of GEMM groups on 256 x 256 single-CTA tiles; default
 // the vocab backward (same-box A/B at C1 / C3 / C4: -6 to -8% per step)
 static int g_opt_wide = PAIR_VBWD;
-static int g_opt_interleave = 0;   // "interleave": bitmask of GEMM groups with interleaved dispatch
 static long long* g_trace = nullptr;   // "gemm_trace": device pointer of a per-tile trace buffer
 static long long g_trace_launch = -1;  // "gemm_trace_launch": trace only this launch index of a call (-1 = all)
 static int64_t g_opt_vocab_chunk = 0;
@@ -136,10 +135,6 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "gemm_trace")) {
     g_trace = reinterpret_cast<long long*>(value);
-    return ATTN_OK;
-  }
-  if (!strcmp(key, "interleave")) {
-    g_opt_interleave = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "wide_tiles")) {
@@ -395,7 +390,6 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   }
   P.nprob = n;
   P.total_tiles = tiles;
-  P.interleave = (group_bit & g_opt_interleave) ? 1 : 0;
   P.tile_counter = counter;
   P.trace = (g_trace_launch < 0 || g_trace_launch == g_launches) ? g_trace : nullptr;
   if (tiles == 0) return ATTN_OK;

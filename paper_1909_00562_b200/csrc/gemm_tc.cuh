@@ -96,7 +96,6 @@ struct alignas(64) TcParams {
   TcProblem prob[kMaxProblems];
   int nprob;
   int total_tiles;
-  int interleave;   // 1: alternate the last problem's tiles with the others'
   int* tile_counter;
   long long* trace;   // debug: per-tile timestamps (null = off); 8 x int64 per tile
 };
@@ -144,14 +143,6 @@ struct TcTile {
 
 template <int kPair>
 __device__ __forceinline__ TcTile tc_decode(const TcParams& P, int t) {
-  if (P.interleave && P.nprob > 1) {
-    // dispatch order: long tiles (problems 0..n-2) alternate with the last
-    // problem's short tiles, spreading its store traffic over the launch
-    const int L = P.prob[P.nprob - 1].tile_begin, S = P.total_tiles - L;
-    const int m2 = 2 * min(L, S);
-    if (t < m2) t = (t & 1) ? L + (t >> 1) : (t >> 1);
-    else t = (L > S) ? t - S : t;   // the rest are all long (L > S) or all short
-  }
   TcTile r;
   r.p = tc_find_problem(P, t);
   const TcProblem& pr = P.prob[r.p];

@@ -18,8 +18,6 @@ if os.environ.get("ATTN_PAIR"):
     binding.attn_softmax_set_option("cta_pair", int(os.environ["ATTN_PAIR"]))
 if os.environ.get("ATTN_MCAST"):
     binding.attn_softmax_set_option("b_multicast", int(os.environ["ATTN_MCAST"]))
-if os.environ.get("ATTN_IL"):
-    binding.attn_softmax_set_option("interleave", int(os.environ["ATTN_IL"]))
 if os.environ.get("ATTN_WIDE"):
     binding.attn_softmax_set_option("wide_tiles", int(os.environ["ATTN_WIDE"]))
 if os.environ.get("ATTN_CTAS"):
