@@ -780,6 +780,7 @@ static GemmDesc g_dlogits(const Plan& p, const Bufs& b, const void* W_out, const
   g.epi.kind = EPI_DLOGITS; g.epi.out = b.dl[c & 1]; g.epi.ldo = p.Vc;
   g.epi.ncols_valid = vcc; g.epi.ncols_store = p.bf16 ? vcc : p.Vc; g.epi.col_base = c0;
   g.epi.lse = b.lse; g.epi.rowscale = b.rowscale; g.epi.tgt = tgt;
+  g.epi.tgt_logit = b.tgt_logit;
   return g;
 }
 // B1, chunk c: dW_out[c] = dlogits_c^T H_c   (both operands MN-major)
@@ -965,8 +966,10 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   // ---- B1: V-chunked vocab backward.  Launch c runs dW_out[c] and dHc += ...
   // for chunk c together with the dlogits of chunk c+1 (double-buffered).
   {
+    // chunk 0's dlogits alone: 128 x 256 tiles (short K; two accumulators in
+    // TMEM so each tile's exp epilogue overlaps the next tile's MMAs)
     GemmDesc g0 = g_dlogits(p, b, W_out, tgt_ids, 0);
-    if ((st = gemm(&g0, 1, PAIR_VBWD)) != ATTN_OK) return st;
+    if ((st = gemm(&g0, 1, 0)) != ATTN_OK) return st;
     for (int c = 0; c < p.nchunks; ++c) {
       GemmDesc gs[3];
       int n = 0;

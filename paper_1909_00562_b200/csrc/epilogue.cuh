@@ -48,6 +48,8 @@ struct EpiParams {
   const int* tgt;        // LSE/DLOGITS: [rows] target ids
   const float* lse;      // DLOGITS: [rows]
   const float* rowscale; // DLOGITS: [rows] loss_scale on valid rows, 0 on padded
+                         // (tcgen05 DLOGITS also reads tgt_logit: the forward's
+                         // target logit, for the -onehot term)
   float* stash_f32;      // ATTN_SOFTMAX(_BWD): alpha fp32 [rows, ncols_valid]
   const int* src_len;    // ATTN_SOFTMAX: [batch]
   const float* addend;   // ADD_BF16: [rows, add_ld] fp32
@@ -72,6 +74,13 @@ __device__ __forceinline__ float tanh_f(float x) {
     return tanhf(x);
   }
 }
+__device__ __forceinline__ float ex2_mufu(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float kLog2e = 1.4426950408889634f;
+
 template <bool kFast>
 __device__ __forceinline__ float exp_f(float x) {
   if constexpr (kFast) return __expf(x);
@@ -125,6 +134,8 @@ struct RowEpilogue {
   LseState st;
   int y;
   float lse, rs;
+  float c2;    // tcgen05 DLOGITS: log2(rs) - lse log2(e) (very negative on padded rows)
+  float fix;   // tcgen05 DLOGITS: the target column's value rs (p_y - 1)
   __device__ __forceinline__ RowEpilogue(const EpiParams& p_, int row_, int split_)
       : p(p_), row(row_), split(split_) {
     st.m = -INFINITY;
@@ -135,9 +146,15 @@ struct RowEpilogue {
     lse = 0.f;
     rs = 0.f;
     if (p.kind == EPI_LSE || p.kind == EPI_DLOGITS) y = p.tgt[row] - p.col_base;
+    c2 = 0.f;
+    fix = 0.f;
     if (p.kind == EPI_DLOGITS) {
       lse = p.lse[row];
       rs = p.rowscale[row];
+      if (kFast) {
+        c2 = rs > 0.f ? __log2f(rs) - lse * kLog2e : -1000.f;
+        if (p.tgt_logit) fix = rs * (__expf(p.tgt_logit[row] - lse) - 1.f);
+      }
     }
   }
 
@@ -202,10 +219,12 @@ struct RowEpilogue {
     if (kind == EPI_LSE) {
       chunk(col0, v);
     } else if (kind == EPI_DLOGITS) {
-      const int yl = y - col0;
+      // rs * softmax = 2^(l log2 e + log2 rs - lse log2 e): one FFMA and one
+      // MUFU ex2 per element; the -rs onehot term is written separately (the
+      // engine overwrites the target column with `fix`).  (Moving part of the
+      // exponentials to an FMA-pipe polynomial measured slower.)
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        v[j] = rs * (exp_f<kFast>(v[j] - lse) - (j == yl ? 1.f : 0.f));
+      for (int j = 0; j < 32; ++j) v[j] = ex2_mufu(fmaf(v[j], kLog2e, c2));
     } else if (kind == EPI_TANH) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = tanh_f<kFast>(v[j]);

@@ -656,6 +656,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
               const uint32_t gi = (c & 1) * 4 + g;
               st_shared_v4(stg + lane * 128 + ((gi ^ swz) << 4), w[0], w[1], w[2], w[3]);
             }
+            if (kind == EPI_DLOGITS) {   // the -onehot term: the target column gets rs (p_y - 1)
+              const int yl = epi.y - col;
+              if ((unsigned)yl < 32u && row_ok && epi.rs > 0.f) {
+                const uint32_t gi = (c & 1) * 4 + (yl >> 3);
+                st_shared_u16(stg + lane * 128 + ((gi ^ swz) << 4) + (yl & 7) * 2,
+                              __bfloat16_as_ushort(__float2bfloat16_rn(epi.fix)));
+              }
+            }
             if ((c & 1) == 1 || c == n_act - 1) {
               fence_proxy_async_smem();
               __syncwarp();
