@@ -57,3 +57,16 @@ for sm in np.unique(t[:, 0]):
     starts.append((rows[:, 4].min(), rows[:, 5].max()))
 st_ = np.array(starts)
 print("  per-SM first MMA spread %d cycles, last commit spread %d cycles" % (st_[:,0].max()-st_[:,0].min(), st_[:,1].max()-st_[:,1].min()))
+# MMA-warp breakdown of the tile boundary (medians, cycles)
+prev = []
+for sm in np.unique(t[:, 0]):
+    rows = t[t[:, 0] == sm]
+    rows = rows[np.argsort(rows[:, 4])]
+    for a, b in zip(rows[:-1], rows[1:]):
+        prev.append((b[3] - a[5], b[8] - b[3], b[9] - b[8], b[10] - b[9], b[4] - b[10],
+                     b[11] - a[2], b[4] - b[11]))
+pv = np.array(prev)
+print("  prev commit->id seen %d | ->decoded %d | ->acc free %d | ->full wait %d | ->first MMA %d" %
+      tuple(np.median(pv[:, i]) for i in range(5)))
+print("  producer: prev last load -> next first load %d | next first load -> its first MMA %d" %
+      tuple(np.median(pv[:, i]) for i in (5, 6)))
