@@ -6,7 +6,8 @@
  * The operation (section 3.2, Eqs. 1-6; readings R1-R11 in DESIGN.md):
  *   per sentence b and target row i (all rows computed, only valid rows count)
  *     e_ij   = H_dec[b,i] . H_enc[b,j]                    Eq. 2,
- *                                                          dot form, W_alpha = I (R1)
+ *                                                          dot form, W_alpha = I (R1);
+ *                                                          with W_alpha: (H_dec W_alpha) . H_enc
  *     alpha  = softmax_j(e_i) over j < src_len[b]; 0 else  Eq. 1
  *     C_i    = sum_j alpha_ij H_enc[b,j]                   Eq. 3
  *     Hc_i   = tanh(W_c[:, :d] H_i + W_c[:, d:] C_i)       Eq. 4
@@ -92,8 +93,14 @@ size_t attn_softmax_workspace_size(const attn_shape_t* s);
 /* The whole stage, forward + backward, on `stream`.
  *   src_lens_host, tgt_lens_host: [B] HOST arrays, validated and copied.
  *   tgt_ids: [B,N] device int32.
- *   W_alpha / dW_alpha: must be NULL (dot score, R1); the Eq. 2 "general"
- *     score is not implemented in this build (ATTN_ERR_UNSUPPORTED).
+ *   W_alpha / dW_alpha: both NULL = the dot score of the hot path (R1:
+ *     e_ij = H_dec[b,i] . H_enc[b,j]); both set = the Eq. 2 "general" score
+ *     alpha_hat = H^T W_alpha S, row form
+ *     e_ij = (H_dec[b,i] W_alpha) . H_enc[b,j].  W_alpha [d,d] row-major in
+ *     s->dtype (read-only); dW_alpha [d,d] fp32, overwritten (allreduced with
+ *     the other weight gradients when comm != NULL).  Exactly one of the two
+ *     NULL is ATTN_ERR_INVALID_ARG.  The host-buffer variants below use the
+ *     dot score.
  *   loss_scale: multiplies the summed token NLL (the harness passes
  *     1 / global valid target tokens, R9).
  *   loss: [1] device fp32 = loss_scale * sum of this shard's token NLL

@@ -497,7 +497,7 @@ struct Plan {
   int nchunks;
   size_t off_lens, off_counters, off_blockpart, off_alpha, off_dalpha, off_ctx, off_hc, off_part,
       off_tgtlogit, off_lse, off_nll, off_rowscale, off_dl, off_dhc, off_dz, off_dhc2, off_abf,
-      off_debf;
+      off_debf, off_q;
   int Mp;             // bf16 path: row stride of the bf16 alpha / de operands (64-multiple)
   size_t total;
 };
@@ -555,6 +555,7 @@ static Plan make_plan(const attn_shape_t* s) {
   p.Mp = (p.M + 63) / 64 * 64;
   p.off_abf = take(p.bf16 ? 2 * p.T * p.Mp : 0);
   p.off_debf = take(p.bf16 ? 2 * p.T * p.Mp : 0);
+  p.off_q = take(p.elt * p.T * p.d);   // Eq. 2 general score: Q = H W_alpha
   p.total = o;
   return p;
 }
@@ -621,8 +622,8 @@ static attn_status_t attention_forward(const Plan& p, const T* H, const T* S, co
 }
 
 template <typename T>
-static attn_status_t attention_backward(const Plan& p, const T* H, const T* S, const float* alpha,
-                                        float* dalpha, const float* dhc2, T* dH, T* dS,
+static attn_status_t attention_backward(const Plan& p, const T* Q, const T* S, const float* alpha,
+                                        float* dalpha, const float* dhc2, T* dH, T* dS, T* dq,
                                         cudaStream_t stream) {
   const long long ld2 = 2ll * p.d;
   const float* dC = dhc2 + p.d;   // columns [d, 2d) of [dH_part | dC]
@@ -642,14 +643,15 @@ static attn_status_t attention_backward(const Plan& p, const T* H, const T* S, c
     CUDA_TRY(cudaGetLastError());
     ++g_launches;
   }
-  // dH_dec_b = dH_part_b + de_b S_b
+  // dot score: dH_dec_b = dH_part_b + de_b S_b;  general score (dq != NULL):
+  // dQ_b = de_b S_b (the caller adds dQ W_alpha^T to dH_part)
   {
     BGemm<float, T, float, T, T> g{};
     g.batch = p.B; g.M = p.N; g.N = p.d; g.K0 = p.M; g.K1 = 0;
     g.s0 = {dalpha, (long long)p.N * p.M, p.M, 1, S, (long long)p.M * p.d, 1, p.d};
     g.s1 = {dalpha, 0, 0, 0, S, 0, 0, 0};
-    g.out = dH; g.sob = (long long)p.N * p.d; g.som = p.d; g.son = 1;
-    g.add = dhc2; g.sadd_b = (long long)p.N * ld2; g.sadd_m = ld2; g.sadd_n = 1;
+    g.out = dq ? dq : dH; g.sob = (long long)p.N * p.d; g.som = p.d; g.son = 1;
+    if (!dq) { g.add = dhc2; g.sadd_b = (long long)p.N * ld2; g.sadd_m = ld2; g.sadd_n = 1; }
     attn_status_t st = launch_bgemm(g, stream);
     if (st != ATTN_OK) return st;
   }
@@ -658,7 +660,7 @@ static attn_status_t attention_backward(const Plan& p, const T* H, const T* S, c
     BGemm<float, float, float, T, T> g{};
     g.batch = p.B; g.M = p.M; g.N = p.d; g.K0 = p.N; g.K1 = p.N;
     g.s0 = {alpha, (long long)p.N * p.M, 1, p.M, dC, (long long)p.N * ld2, 1, ld2};
-    g.s1 = {dalpha, (long long)p.N * p.M, 1, p.M, H, (long long)p.N * p.d, 1, p.d};
+    g.s1 = {dalpha, (long long)p.N * p.M, 1, p.M, Q, (long long)p.N * p.d, 1, p.d};
     g.out = dS; g.sob = (long long)p.M * p.d; g.som = p.d; g.son = 1;
     return launch_bgemm(g, stream);
   }
@@ -670,6 +672,8 @@ struct Bufs {
   float* alpha; float* dalpha; void* ctx; void* hc; float2* part; float* tgt_logit;
   float* lse; float* nll; float* rowscale; void* dl[2]; float* dhc; void* dz; float* dhc2;
   void* abf; void* debf; float* dhpart; void* dcbf;   // bf16 path
+  void* q;    // Eq. 2 general score: Q = H W_alpha [T, d] (dtype)
+  void* dq;   // its gradient [T, d] (dtype); aliases dz, which is dead by then
 };
 
 static Bufs carve(const Plan& p, void* ws) {
@@ -697,6 +701,8 @@ static Bufs carve(const Plan& p, void* ws) {
   b.debf = w + p.off_debf;
   b.dhpart = b.dhc2;                          // bf16 path: dH_part fp32 [T, d]
   b.dcbf = (char*)(b.dhc2 + p.T * p.d);       //            dC bf16 [T, d]
+  b.q = w + p.off_q;
+  b.dq = b.dz;
   return b;
 }
 
@@ -716,10 +722,10 @@ static attn_status_t validate(const attn_shape_t* s, const void* H_dec, const vo
       {dH_enc, "dH_enc"}, {dW_c, "dW_c"}, {dW_out, "dW_out"}, {ws, "workspace"}};
   for (auto& r : req)
     if (!r.p) return fail(ATTN_ERR_INVALID_ARG, "%s is NULL", r.n);
-  if (W_alpha || dW_alpha)
-    return fail(ATTN_ERR_UNSUPPORTED,
-                "W_alpha / dW_alpha must be NULL: the Eq. 2 'general' score (W_alpha) is not in "
-                "this build; the hot path uses the dot score (DESIGN.md R1)");
+  if ((W_alpha == nullptr) != (dW_alpha == nullptr))
+    return fail(ATTN_ERR_INVALID_ARG,
+                "W_alpha and dW_alpha go together: both NULL (dot score, DESIGN.md R1) or both "
+                "set (Eq. 2 general score); got W_alpha=%p dW_alpha=%p", W_alpha, (const void*)dW_alpha);
   long long total_tgt = 0;
   for (int b = 0; b < s->batch; ++b) {
     if (src_lens[b] < 1)
@@ -738,7 +744,8 @@ static attn_status_t validate(const attn_shape_t* s, const void* H_dec, const vo
   if (ws_bytes < p.total)
     return fail(ATTN_ERR_WORKSPACE, "workspace_bytes = %zu < required %zu", ws_bytes, p.total);
   if (s->dtype == ATTN_BF16) {
-    const void* al[] = {H_dec, H_enc, W_c, W_out, dH_dec, dH_enc, dW_c, dW_out, ws};
+    const void* al[] = {H_dec, H_enc, W_c, W_out, dH_dec, dH_enc, dW_c, dW_out, ws, W_alpha,
+                        dW_alpha};
     for (const void* a : al)
       if (misaligned(a)) return fail(ATTN_ERR_UNSUPPORTED, "bf16 path needs 16-byte aligned pointers");
   }
@@ -829,16 +836,59 @@ static GemmDesc g_dzwc(const Plan& p, const Bufs& b, const void* W_c, int col0, 
   return g;
 }
 
+// Eq. 2 general score: Q = H W_alpha  (W_alpha [d,d] as MN-major B)
+static GemmDesc g_query(const Plan& p, const Bufs& b, const void* H, const void* Wa) {
+  GemmDesc g;
+  const int d = p.d;
+  g.M = (int)p.T; g.N = d; g.K = d;
+  g.a0 = kmaj(H, p.T, d, d);
+  g.b_mn = 1; g.b0 = mnmaj(Wa, d, d, d);
+  g.epi.kind = p.bf16 ? EPI_STORE_BF16 : EPI_STORE_F32; g.epi.out = b.q; g.epi.ldo = d;
+  g.epi.ncols_valid = d; g.epi.ncols_store = d;
+  return g;
+}
+// its backward: dH_dec (+)= dQ W_alpha^T  (W_alpha K-major as stored)
+static GemmDesc g_query_bwd_dh(const Plan& p, const Bufs& b, const void* Wa, void* dH, int kind) {
+  GemmDesc g;
+  const int d = p.d;
+  g.M = (int)p.T; g.N = d; g.K = d;
+  g.a0 = kmaj(b.dq, p.T, d, d);
+  g.b0 = kmaj(Wa, d, d, d);
+  g.epi.kind = kind; g.epi.out = dH; g.epi.ldo = d; g.epi.ncols_valid = d; g.epi.ncols_store = d;
+  g.epi.addend = b.dhpart; g.epi.add_ld = d;
+  return g;
+}
+// dW_alpha = H^T dQ  (both operands MN-major)
+static GemmDesc g_query_bwd_dw(const Plan& p, const Bufs& b, const void* H, float* dWa) {
+  GemmDesc g;
+  const int d = p.d;
+  g.M = d; g.N = d; g.K = (int)p.T;
+  g.a_mn = 1; g.a0 = mnmaj(H, p.T, d, d);
+  g.b_mn = 1; g.b0 = mnmaj(b.dq, p.T, d, d);
+  g.epi.kind = EPI_STORE_F32; g.epi.out = dWa; g.epi.ldo = d; g.epi.ncols_valid = d;
+  g.epi.ncols_store = d;
+  return g;
+}
+
 // ---------------------------------------------------------------- attention on tcgen05 (bf16)
 // One small GEMM per sentence (batched problems; M <= 128 source positions).
 static attn_status_t attention_forward_tc(const Plan& p, const void* H, const void* S, const Bufs& b,
-                                          cudaStream_t stream, int* (*next)(void*), void* ctx_) {
+                                          cudaStream_t stream, int* (*next)(void*), void* ctx_,
+                                          const void* Wa) {
   const int d = p.d, N = p.N, M = p.M, Mp = p.Mp, B = p.B;
+  // Eq. 2 general score: Q = H W_alpha (row form of H^T W_alpha), else Q = H
+  const void* Q = H;
+  if (Wa) {
+    GemmDesc g = g_query(p, b, H, Wa);
+    attn_status_t st = launch_tc_group<__nv_bfloat16>(&g, 1, next(ctx_), stream, PAIR_FWD);
+    if (st != ATTN_OK) return st;
+    Q = b.q;
+  }
   // F1 + Eq. 1: scores E_b = H_b S_b^T with the masked row softmax fused
   {
     GemmDesc g;
     g.batch = B; g.M = N; g.N = M; g.K = d;
-    g.a0 = kmaj(H, N, d, d, (long long)N * d);
+    g.a0 = kmaj(Q, N, d, d, (long long)N * d);
     g.b0 = kmaj(S, M, d, d, (long long)M * d);
     g.epi.kind = EPI_ATTN_SOFTMAX; g.epi.stash_f32 = b.alpha; g.epi.ncols_valid = M;
     g.epi.out = b.abf; g.epi.ldo = Mp; g.epi.ncols_store = Mp; g.epi.src_len = b.src_len;
@@ -858,8 +908,10 @@ static attn_status_t attention_forward_tc(const Plan& p, const void* H, const vo
 
 static attn_status_t attention_backward_tc(const Plan& p, const void* H, const void* S,
                                            void* dH, void* dS, const Bufs& b, cudaStream_t stream,
-                                           int* (*next)(void*), void* ctx_) {
+                                           int* (*next)(void*), void* ctx_, const void* Wa,
+                                           float* dWa) {
   const int d = p.d, N = p.N, M = p.M, Mp = p.Mp, B = p.B;
+  const void* Q = Wa ? b.q : H;
   // dalpha_b = dC_b S_b^T with the softmax backward fused: de (bf16)
   {
     GemmDesc g;
@@ -872,14 +924,19 @@ static attn_status_t attention_backward_tc(const Plan& p, const void* H, const v
     if (st != ATTN_OK) return st;
   }
   GemmDesc gs[2];
-  // dH_dec_b = dH_part_b + de_b S_b
+  // dQ_b = de_b S_b; dot score: dH_dec_b = dH_part_b + dQ_b (fused add),
+  // general score: dQ stored, dH_dec = dH_part + dQ W_alpha^T below
   {
     GemmDesc& g = gs[0];
     g.batch = B; g.M = N; g.N = d; g.K = M;
     g.a0 = kmaj(b.debf, N, M, Mp, (long long)N * Mp);
     g.b_mn = 1; g.b0 = mnmaj(S, M, d, d, (long long)M * d);
-    g.epi.kind = EPI_ADD_BF16; g.epi.out = dH; g.epi.ldo = d; g.epi.ncols_valid = d;
-    g.epi.ncols_store = d; g.epi.addend = b.dhpart; g.epi.add_ld = d;
+    g.epi.ldo = d; g.epi.ncols_valid = d; g.epi.ncols_store = d;
+    if (Wa) {
+      g.epi.kind = EPI_STORE_BF16; g.epi.out = b.dq;
+    } else {
+      g.epi.kind = EPI_ADD_BF16; g.epi.out = dH; g.epi.addend = b.dhpart; g.epi.add_ld = d;
+    }
     g.out_bstride = (long long)N * d;
   }
   // dH_enc_b = alpha_b^T dC_b + de_b^T H_b: two K segments over the decoder rows
@@ -892,12 +949,16 @@ static attn_status_t attention_backward_tc(const Plan& p, const void* H, const v
     g.kseg = (N + TC_BK - 1) / TC_BK;
     g.b_mn = 1; g.b_seg = 1;
     g.b0 = mnmaj(b.dcbf, N, d, d, (long long)N * d);
-    g.b1 = mnmaj(H, N, d, d, (long long)N * d);
+    g.b1 = mnmaj(Q, N, d, d, (long long)N * d);
     g.epi.kind = EPI_STORE_BF16; g.epi.out = dS; g.epi.ldo = d; g.epi.ncols_valid = d;
     g.epi.ncols_store = d;
     g.out_bstride = (long long)M * d;
   }
-  return launch_tc_group<__nv_bfloat16>(gs, 2, next(ctx_), stream);
+  attn_status_t st = launch_tc_group<__nv_bfloat16>(gs, 2, next(ctx_), stream);
+  if (st != ATTN_OK || !Wa) return st;
+  // general score: dH_dec = dH_part + dQ W_alpha^T;  dW_alpha = H^T dQ
+  GemmDesc ga[2] = {g_query_bwd_dh(p, b, Wa, dH, EPI_ADD_BF16), g_query_bwd_dw(p, b, H, dWa)};
+  return launch_tc_group<__nv_bfloat16>(ga, 2, next(ctx_), stream, PAIR_PBWD);
 }
 
 struct CounterCtx {
@@ -911,9 +972,9 @@ static int* next_counter_fn(void* c) {
 
 template <typename T>
 static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int32_t* tgt_ids,
-                               const T* W_c, const T* W_out, float loss_scale, float* loss, T* dH,
-                               T* dS, float* dW_c, float* dW_out, const Bufs& b, attn_comm_t* comm,
-                               cudaStream_t stream) {
+                               const T* W_c, const T* W_out, const T* Wa, float loss_scale,
+                               float* loss, T* dH, T* dS, float* dW_c, float* dW_out, float* dWa,
+                               const Bufs& b, attn_comm_t* comm, cudaStream_t stream) {
   attn_status_t st;
   const bool tc = p.bf16;
   CounterCtx cctx{&b, 0};
@@ -928,11 +989,16 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   g_launches = 0;
   prof_mark("start", stream);
 
-  // ---- F1, F2 (Eqs. 1-3)
-  if (tc)
-    st = attention_forward_tc(p, H, S, b, stream, next_counter_fn, &cctx);
-  else
-    st = attention_forward<T>(p, H, S, b.src_len, b.alpha, (T*)b.ctx, stream);
+  // ---- F1, F2 (Eqs. 1-3); Eq. 2 general score: Q = H W_alpha first
+  if (tc) {
+    st = attention_forward_tc(p, H, S, b, stream, next_counter_fn, &cctx, Wa);
+  } else {
+    if (Wa) {
+      GemmDesc g = g_query(p, b, H, Wa);
+      if ((st = gemm(&g, 1, 0)) != ATTN_OK) return st;
+    }
+    st = attention_forward<T>(p, Wa ? (const T*)b.q : H, S, b.src_len, b.alpha, (T*)b.ctx, stream);
+  }
   if (st != ATTN_OK) return st;
   prof_mark("attn_fwd", stream);
 
@@ -1013,12 +1079,25 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   }
   prof_mark("proj_bwd", stream);
   // ---- B3: attention backward
-  if (tc)
-    st = attention_backward_tc(p, H, S, dH, dS, b, stream, next_counter_fn, &cctx);
-  else
-    st = attention_backward<T>(p, H, S, b.alpha, b.dalpha, b.dhc2, dH, dS, stream);
+  if (tc) {
+    st = attention_backward_tc(p, H, S, dH, dS, b, stream, next_counter_fn, &cctx, Wa, dWa);
+  } else {
+    st = attention_backward<T>(p, Wa ? (const T*)b.q : H, S, b.alpha, b.dalpha, b.dhc2, dH, dS,
+                               Wa ? (T*)b.dq : nullptr, stream);
+    if (st == ATTN_OK && Wa) {
+      // dH_dec = dH_part + dQ W_alpha^T (accumulated onto a copy of dH_part);
+      // dW_alpha = H^T dQ
+      CUDA_TRY(cudaMemcpy2DAsync(dH, sizeof(T) * d, b.dhc2, sizeof(float) * 2 * d, sizeof(T) * d,
+                                 (size_t)TT, cudaMemcpyDeviceToDevice, stream));
+      GemmDesc ga[2] = {g_query_bwd_dh(p, b, Wa, dH, EPI_ACCUM_F32), g_query_bwd_dw(p, b, H, dWa)};
+      st = gemm(ga, 2, 0);
+    }
+  }
   if (st != ATTN_OK) return st;
   prof_mark("attn_bwd", stream);
+  if (comm && dWa) {
+    if ((st = comm_enqueue_allreduce(comm, &cr, stream, dWa, (size_t)d * d)) != ATTN_OK) return st;
+  }
   if (comm) {
     if ((st = comm_enqueue_allreduce(comm, &cr, stream, loss, 1)) != ATTN_OK) return st;
     if ((st = comm_end(comm, &cr, stream)) != ATTN_OK) return st;
@@ -1048,12 +1127,13 @@ extern "C" attn_status_t attn_softmax_fwd_bwd(
   if (p.bf16)
     return run_stage<__nv_bfloat16>(p, (const __nv_bfloat16*)H_dec, (const __nv_bfloat16*)H_enc,
                                     tgt_ids, (const __nv_bfloat16*)W_c,
-                                    (const __nv_bfloat16*)W_out, loss_scale, loss,
-                                    (__nv_bfloat16*)dH_dec, (__nv_bfloat16*)dH_enc, dW_c, dW_out,
-                                    b, comm, stream);
+                                    (const __nv_bfloat16*)W_out, (const __nv_bfloat16*)W_alpha,
+                                    loss_scale, loss, (__nv_bfloat16*)dH_dec,
+                                    (__nv_bfloat16*)dH_enc, dW_c, dW_out, dW_alpha, b, comm,
+                                    stream);
   return run_stage<float>(p, (const float*)H_dec, (const float*)H_enc, tgt_ids, (const float*)W_c,
-                          (const float*)W_out, loss_scale, loss, (float*)dH_dec, (float*)dH_enc,
-                          dW_c, dW_out, b, comm, stream);
+                          (const float*)W_out, (const float*)W_alpha, loss_scale, loss,
+                          (float*)dH_dec, (float*)dH_enc, dW_c, dW_out, dW_alpha, b, comm, stream);
 }
 
 // ------------------------------------------------------------------ host-buffer variant

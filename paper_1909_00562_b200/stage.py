@@ -24,23 +24,29 @@ class AttnSoftmaxStage:
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.views_meta = binding.attn_softmax_workspace_views(self.shape)
 
-    def alloc_outputs(self):
+    def alloc_outputs(self, general_score: bool = False):
         dev, B, N, M, d, V = self.device, self.B, self.N, self.M, self.d, self.V
-        return dict(
+        out = dict(
             loss=torch.empty(1, dtype=torch.float32, device=dev),
             dH_dec=torch.empty(B, N, d, dtype=self.tdtype, device=dev),
             dH_enc=torch.empty(B, M, d, dtype=self.tdtype, device=dev),
             dW_c=torch.empty(d, 2 * d, dtype=torch.float32, device=dev),
             dW_out=torch.empty(V, d, dtype=torch.float32, device=dev))
+        if general_score:
+            out["dW_alpha"] = torch.empty(d, d, dtype=torch.float32, device=dev)
+        return out
 
     def __call__(self, H_dec, H_enc, src_len, tgt_len, tgt_ids, W_c, W_out,
-                 loss_scale: float, out=None, comm=None, stream=None):
+                 loss_scale: float, out=None, comm=None, stream=None, W_alpha=None):
+        """W_alpha [d,d] (dtype of the stage) selects the Eq. 2 "general"
+        score; None is the dot score of the hot path."""
         if out is None:
-            out = self.alloc_outputs()
+            out = self.alloc_outputs(W_alpha is not None)
         binding.attn_softmax_fwd_bwd(
             self.shape, H_dec, H_enc, src_len, tgt_len, tgt_ids, W_c, W_out,
             loss_scale, out["loss"], out["dH_dec"], out["dH_enc"], out["dW_c"],
-            out["dW_out"], self.workspace, comm=comm, stream=stream)
+            out["dW_out"], self.workspace, comm=comm, stream=stream,
+            W_alpha=W_alpha, dW_alpha=out.get("dW_alpha") if W_alpha is not None else None)
         return out
 
     def views(self):

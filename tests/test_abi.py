@@ -115,9 +115,9 @@ def test_null_and_workspace_errors(built_lib):
     with pytest.raises(AttnError) as e:
         _call(s, [5, 3], [5, 4], ws=_Fake(1000))
     assert e.value.status == "ATTN_ERR_WORKSPACE"
-    with pytest.raises(AttnError) as e:
+    with pytest.raises(AttnError) as e:   # W_alpha without dW_alpha
         _call(s, [5, 3], [5, 4], W_alpha=_Fake())
-    assert e.value.status == "ATTN_ERR_UNSUPPORTED"
+    assert e.value.status == "ATTN_ERR_INVALID_ARG" and "dW_alpha" in str(e.value)
 
     class Odd(_Fake):
         def data_ptr(self):

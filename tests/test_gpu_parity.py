@@ -20,7 +20,7 @@ def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-def run_gpu(cfg, inp, scale, vocab_chunk=0):
+def run_gpu(cfg, inp, scale, vocab_chunk=0, comm=None):
     from paper_1909_00562_b200 import binding
     from paper_1909_00562_b200.stage import AttnSoftmaxStage, to_device
     binding.attn_softmax_set_option("vocab_chunk", vocab_chunk)
@@ -28,7 +28,7 @@ def run_gpu(cfg, inp, scale, vocab_chunk=0):
         st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
         dv = to_device(inp, cfg.dtype)
         out = st(dv["H_dec"], dv["H_enc"], dv["src_len"], dv["tgt_len"], dv["tgt_ids"],
-                 dv["W_c"], dv["W_out"], scale)
+                 dv["W_c"], dv["W_out"], scale, W_alpha=dv.get("W_alpha"), comm=comm)
         torch.cuda.synchronize()
     finally:
         binding.attn_softmax_set_option("vocab_chunk", 0)
@@ -43,7 +43,8 @@ def run_gpu(cfg, inp, scale, vocab_chunk=0):
 
 def oracle(inp, scale):
     return O.fwd_bwd(inp["H_dec"], inp["H_enc"], inp["src_len"], inp["tgt_len"],
-                     inp["tgt_ids"], inp["W_c"], inp["W_out"], scale)
+                     inp["tgt_ids"], inp["W_c"], inp["W_out"], scale,
+                     W_alpha=inp.get("W_alpha"))
 
 
 # ------------------------------------------------------------ GEMM core ----
@@ -137,6 +138,37 @@ def test_parity_vs_oracle(cuda_lib, name, vc, mode):
         assert np.all(g["nll"][bb * cfg.N + Tb:(bb + 1) * cfg.N] == 0.0)
     # I1 rows sum to 1
     assert np.abs(g["alpha"].sum(-1) - 1).max() < 1e-5
+
+
+@pytest.mark.parametrize("name,vc,mode", [("tiny_ragged", 0, "p8"), ("small_f32", 0, "p8"),
+                                          ("odd_f32", 0, "p8"), ("small", 0, "default"),
+                                          ("small", 1024, "p15"), ("medium", 0, "default"),
+                                          ("medium", 2048, "w0"), ("odd", 256, "w15")])
+def test_parity_general_score(cuda_lib, name, vc, mode):
+    """NEXT-1: the Eq. 2 "general" score alpha_hat = H^T W_alpha S
+     -- Q = H W_alpha on the tensor cores, dW_alpha = H^T dQ,
+    dH_dec = dH_part + dQ W_alpha^T -- against the oracle's W_alpha branch."""
+    from paper_1909_00562_b200 import binding
+    cfg = CONFIGS[name]
+    inp = make_inputs(cfg, with_alpha=True)
+    scale = 1.0 / global_valid_tokens(cfg, cfg.B)
+    set_modes(binding, mode)
+    try:
+        g = run_gpu(cfg, inp, scale, vocab_chunk=vc)
+    finally:
+        set_modes(binding, "default")
+    f, b = oracle(inp, scale)
+    tol = TOL[cfg.dtype]
+    assert abs(g["loss"] - f["loss"]) <= tol["loss"] * abs(f["loss"]), (g["loss"], f["loss"])
+    for k in ("dH_dec", "dH_enc", "dW_c", "dW_out", "dW_alpha"):
+        e = rel_l2(g[k], b[k])
+        assert e <= tol["grad"], (k, e)
+    assert rel_l2(g["alpha"], f["alpha"]) <= tol["inter"]
+    for bb in range(cfg.B):
+        L, Tb = int(inp["src_len"][bb]), int(inp["tgt_len"][bb])
+        assert np.all(g["alpha"][bb, :, L:] == 0.0)
+        assert np.all(g["dH_enc"][bb, L:] == 0.0)
+        assert np.all(g["dH_dec"][bb, Tb:] == 0.0)
 
 
 @pytest.mark.parametrize("name", ["tiny_ragged", "small"])
@@ -247,6 +279,14 @@ def test_single_rank_nccl_communicator(cuda_lib):
         torch.cuda.synchronize()
         for k in ("loss", "dH_dec", "dH_enc", "dW_c", "dW_out"):
             assert torch.equal(out[k], ref[k]), k
+        # general score (NEXT-1): dW_alpha joins the allreduce
+        inp_a = make_inputs(cfg, with_alpha=True)
+        Wa = to_device(inp_a, cfg.dtype)["W_alpha"]
+        ref_a = {k: v.clone() for k, v in st(*args, W_alpha=Wa).items()}
+        out_a = st(*args, W_alpha=Wa, comm=comm)
+        torch.cuda.synchronize()
+        for k in ("loss", "dH_dec", "dH_enc", "dW_c", "dW_out", "dW_alpha"):
+            assert torch.equal(out_a[k], ref_a[k]), k
         buf = torch.arange(1000, dtype=torch.float32, device="cuda")
         binding.attn_grad_allreduce(comm, buf)
         torch.cuda.synchronize()
