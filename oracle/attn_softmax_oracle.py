@@ -17,7 +17,10 @@ and no fusion, chunking or online-LSE reformulation:
                                                                     DESIGN.md R1)
   Eq. 3  (PAPER.md:136-139)  C = alpha . S
   Eq. 4  (PAPER.md:140-145)  H_c = tanh(W_c [H; C])
-  Eq. 5  P = Softmax{F_c(H_c)},  F_c(x) = W_out x (no bias, R6)
+  Eq. 5  P = Softmax{F_c(H_c)},  F_c(x) = W_out x (no bias on
+                                                     the hot path, R6; optional
+                                                     b_out: F_c(x) = W_out x + b_out,
+                                                     SPEC.md:171, NEXT-1)
   Eq. 6  P_i = P(y_i | y_<i, x); loss = scale * sum -log P_i(y_i)
 
 The backward pass is the closed-form reverse-mode derivative of the above
@@ -113,12 +116,17 @@ def context_decoded(H_dec, C, W_c):
     return z, np.tanh(z)
 
 
-def vocab_logits(Hc_rows, W_out):
-    """Eq. 5: F_c(H_c) = W_out h_c for each row (no bias, R6).
+def vocab_logits(Hc_rows, W_out, b_out=None):
+    """Eq. 5: F_c(H_c) = W_out h_c for each row (no bias on
+    the hot path, R6); with b_out [V] the "liner function" F_c carries SPEC's
+    bias: W_out h_c + b_out.
 
     Hc_rows [R,d] -> logits [R,V].
     """
-    return _f64(Hc_rows) @ _f64(W_out).T
+    logits = _f64(Hc_rows) @ _f64(W_out).T
+    if b_out is not None:
+        logits = logits + _f64(b_out)[None, :]
+    return logits
 
 
 def log_sum_exp(logits):
@@ -144,7 +152,7 @@ def _valid_rows(tgt_len, B, N):
 
 
 def forward(H_dec, H_enc, src_len, tgt_len, tgt_ids, W_c, W_out, loss_scale,
-            W_alpha=None):
+            W_alpha=None, b_out=None):
     """Eqs. 1-6 in order.  Returns a dict of every intermediate (fp64)."""
     H = _f64(H_dec)
     S = _f64(H_enc)
@@ -154,7 +162,7 @@ def forward(H_dec, H_enc, src_len, tgt_len, tgt_ids, W_c, W_out, loss_scale,
     C = context_vectors(alpha, S)                              # Eq. 3
     z, Hc = context_decoded(H, C, W_c)                         # Eq. 4
     Hc_rows = Hc.reshape(B * N, d)
-    logits = vocab_logits(Hc_rows, W_out)                      # Eq. 5
+    logits = vocab_logits(Hc_rows, W_out, b_out)               # Eq. 5
     lse = log_sum_exp(logits)
     y = np.asarray(tgt_ids).reshape(-1)
     valid = _valid_rows(tgt_len, B, N)
@@ -171,11 +179,13 @@ def forward(H_dec, H_enc, src_len, tgt_len, tgt_ids, W_c, W_out, loss_scale,
 # (DP gradient sum semantics PAPER.md:121)
 # --------------------------------------------------------------------------
 
-def backward(H_dec, H_enc, src_len, W_c, W_out, loss_scale, fwd, W_alpha=None):
-    """Gradients of loss w.r.t. H_dec, H_enc, W_c, W_out (and W_alpha).
+def backward(H_dec, H_enc, src_len, W_c, W_out, loss_scale, fwd, W_alpha=None,
+             b_out=None):
+    """Gradients of loss w.r.t. H_dec, H_enc, W_c, W_out (and W_alpha, b_out).
 
     Step 8  dl_iv = scale (softmax(l_i)_v - [v = y_i]) on valid rows, else 0
     Step 9  dW_out = sum_rows dl_i^T hc_i ; dhc_i = sum_v dl_iv W_out[v]
+            (b_out: db_out = sum_rows dl_i)
     Step 10 dz = dhc * (1 - hc^2) ; dW_c = sum_i dz_i [h_i ; c_i]^T
     Step 11 dh_i = W_c[:, :d]^T dz_i ; dc_i = W_c[:, d:]^T dz_i
     Step 12 dalpha_ij = dc_i . S_j ; D_i = sum_j alpha_ij dalpha_ij ;
@@ -201,6 +211,7 @@ def backward(H_dec, H_enc, src_len, W_c, W_out, loss_scale, fwd, W_alpha=None):
     # step 9
     Hc_rows = Hc.reshape(B * N, d)
     dW_out = dl.T @ Hc_rows
+    db_out = dl.sum(axis=0) if b_out is not None else None
     dHc = (dl @ W_out).reshape(B, N, d)
     # step 10
     dz = dHc * (1.0 - Hc * Hc)
@@ -227,14 +238,15 @@ def backward(H_dec, H_enc, src_len, W_c, W_out, loss_scale, fwd, W_alpha=None):
     dS = np.swapaxes(alpha, 1, 2) @ dC + np.swapaxes(de, 1, 2) @ q
     return dict(dlogits=dl, dHc=dHc, dz=dz, dC=dC, dalpha=dalpha, de=de,
                 dH_dec=dH, dH_enc=dS, dW_c=dW_c, dW_out=dW_out,
-                dW_alpha=dW_alpha)
+                dW_alpha=dW_alpha, db_out=db_out)
 
 
 def fwd_bwd(H_dec, H_enc, src_len, tgt_len, tgt_ids, W_c, W_out, loss_scale,
-            W_alpha=None):
+            W_alpha=None, b_out=None):
     """The whole stage: forward (Eqs. 1-6) then backward.  Returns
     (fwd dict, bwd dict)."""
     fwd = forward(H_dec, H_enc, src_len, tgt_len, tgt_ids, W_c, W_out,
-                  loss_scale, W_alpha)
-    bwd = backward(H_dec, H_enc, src_len, W_c, W_out, loss_scale, fwd, W_alpha)
+                  loss_scale, W_alpha, b_out)
+    bwd = backward(H_dec, H_enc, src_len, W_c, W_out, loss_scale, fwd, W_alpha,
+                   b_out)
     return fwd, bwd

@@ -118,8 +118,9 @@ def global_valid_tokens(cfg: Config, B_global: int) -> int:
     return sum(lengths(cfg, b)[1] for b in range(B_global))
 
 
-def make_weights(cfg: Config, with_alpha: bool = False):
-    """W_c [d,2d], W_out [V,d] (and W_alpha [d,d]) ~ U(-0.1, 0.1)."""
+def make_weights(cfg: Config, with_alpha: bool = False, with_bias: bool = False):
+    """W_c [d,2d], W_out [V,d] (and W_alpha [d,d], b_out [V]) ~ U(-0.1, 0.1)
+    (b_out ~ U(-1, 1): wide enough that the bias visibly shapes the softmax)."""
     d, V = cfg.d, cfg.V
     W_c = np.random.default_rng([cfg.seed, 1001]).uniform(
         -0.1, 0.1, size=(d, 2 * d)).astype(np.float32)
@@ -129,13 +130,17 @@ def make_weights(cfg: Config, with_alpha: bool = False):
     if with_alpha:
         out["W_alpha"] = np.random.default_rng([cfg.seed, 1003]).uniform(
             -0.1, 0.1, size=(d, d)).astype(np.float32)
+    if with_bias:
+        out["b_out"] = np.random.default_rng([cfg.seed, 1004]).uniform(
+            -1.0, 1.0, size=(V,)).astype(np.float32)
     if cfg.dtype == "bf16":
         out = {k: round_bf16(v) for k, v in out.items()}
     return out
 
 
 def make_inputs(cfg: Config, sentences: Optional[Sequence[int]] = None,
-                with_weights: bool = True, with_alpha: bool = False):
+                with_weights: bool = True, with_alpha: bool = False,
+                with_bias: bool = False):
     """Activations of the given global sentence ids (default: 0..B-1).
 
     Returns a dict of fp32 numpy arrays (bf16-representable for bf16
@@ -165,7 +170,7 @@ def make_inputs(cfg: Config, sentences: Optional[Sequence[int]] = None,
     out = dict(H_dec=H_dec, H_enc=H_enc, src_len=src, tgt_len=tgt,
                tgt_ids=ids)
     if with_weights:
-        out.update(make_weights(cfg, with_alpha))
+        out.update(make_weights(cfg, with_alpha, with_bias))
     return out
 
 

@@ -279,12 +279,14 @@ def _rel_l2(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-@pytest.mark.parametrize("with_alpha", [False, True])
-def test_finite_differences(with_alpha):
+@pytest.mark.parametrize("with_alpha,with_bias", [(False, False), (True, False), (False, True),
+                                                  (True, True)])
+def test_finite_differences(with_alpha, with_bias):
     """Central differences in fp64 (SPEC.md:131-142 grad_check): every
-    gradient, including W_alpha for the Eq. 2 'general' score (NEXT-1)."""
+    gradient, including W_alpha for the Eq. 2 'general' score and the F_c
+    bias b_out (NEXT-1)."""
     cfg = CONFIGS["tiny_ragged"]
-    inp = make_inputs(cfg, with_alpha=with_alpha)
+    inp = make_inputs(cfg, with_alpha=with_alpha, with_bias=with_bias)
     inp = {k: (v.astype(np.float64) if v.dtype == np.float32 else v)
            for k, v in inp.items()}
     Wa = inp.get("W_alpha")
@@ -296,17 +298,20 @@ def test_finite_differences(with_alpha):
         x = dict(inp, **over)
         f = O.forward(x["H_dec"], x["H_enc"], x["src_len"], x["tgt_len"],
                       x["tgt_ids"], x["W_c"], x["W_out"], scale,
-                      W_alpha=over.get("W_alpha", Wa))
+                      W_alpha=over.get("W_alpha", Wa), b_out=x.get("b_out"))
         return f["loss"]
 
     f, g = O.fwd_bwd(inp["H_dec"], inp["H_enc"], inp["src_len"], inp["tgt_len"],
-                     inp["tgt_ids"], inp["W_c"], inp["W_out"], scale, W_alpha=Wa)
+                     inp["tgt_ids"], inp["W_c"], inp["W_out"], scale, W_alpha=Wa,
+                     b_out=inp.get("b_out"))
     names = [("H_dec", "dH_dec"), ("H_enc", "dH_enc"), ("W_c", "dW_c"),
              ("W_out", "dW_out")]
     base = dict(inp)
     if Wa is not None:
         base["W_alpha"] = Wa
         names.append(("W_alpha", "dW_alpha"))
+    if with_bias:
+        names.append(("b_out", "db_out"))
     eps = 1e-6
     for x_name, g_name in names:
         x = base[x_name]
@@ -322,11 +327,12 @@ def test_finite_differences(with_alpha):
 
 
 # ----------------------------------------- independent torch float64 ----
-def _torch_stage(inp, scale, W_alpha=None):
+def _torch_stage(inp, scale, W_alpha=None, b_out=None):
     """Direct composition of Eqs. 1-6 with torch ops (float64, CPU)."""
     t = lambda a: torch.tensor(np.asarray(a, np.float64), requires_grad=True)
     Hd, He, Wc, Wo = t(inp["H_dec"]), t(inp["H_enc"]), t(inp["W_c"]), t(inp["W_out"])
     Wa = t(W_alpha) if W_alpha is not None else None
+    bo = t(b_out) if b_out is not None else None
     B, N, d = Hd.shape
     M = He.shape[1]
     src = torch.tensor(inp["src_len"]).long()
@@ -337,7 +343,7 @@ def _torch_stage(inp, scale, W_alpha=None):
     a = torch.softmax(e, dim=-1)
     C = torch.einsum("bij,bjd->bid", a, He)
     Hc = torch.tanh(torch.cat([Hd, C], dim=-1) @ Wc.T)
-    logits = Hc.reshape(B * N, d) @ Wo.T
+    logits = F.linear(Hc.reshape(B * N, d), Wo, bo)
     valid = (torch.arange(N)[None, :] < tgt[:, None]).reshape(-1)
     y = torch.tensor(inp["tgt_ids"]).long().reshape(-1).clamp(0, Wo.shape[0] - 1)
     nll = F.cross_entropy(logits, y, reduction="none")
@@ -348,23 +354,30 @@ def _torch_stage(inp, scale, W_alpha=None):
                dH_enc=He.grad.numpy(), dW_c=Wc.grad.numpy(), dW_out=Wo.grad.numpy())
     if Wa is not None:
         out["dW_alpha"] = Wa.grad.numpy()
+    if bo is not None:
+        out["db_out"] = bo.grad.numpy()
     return out
 
 
-@pytest.mark.parametrize("name,with_alpha", [("tiny_ragged", False),
-                                             ("small_f32", False),
-                                             ("small_f32", True)])
-def test_torch_float64_autograd(name, with_alpha):
+@pytest.mark.parametrize("name,with_alpha,with_bias", [("tiny_ragged", False, False),
+                                                       ("small_f32", False, False),
+                                                       ("small_f32", True, False),
+                                                       ("small_f32", False, True),
+                                                       ("tiny_ragged", True, True)])
+def test_torch_float64_autograd(name, with_alpha, with_bias):
     cfg = CONFIGS[name]
-    inp = make_inputs(cfg, with_alpha=with_alpha)
+    inp = make_inputs(cfg, with_alpha=with_alpha, with_bias=with_bias)
     Wa = inp.get("W_alpha")
+    bo = inp.get("b_out")
     scale = 1.0 / int(inp["tgt_len"].sum())
-    ref = _torch_stage(inp, scale, Wa)
-    f, g = _run(inp, scale=scale, W_alpha=Wa)
+    ref = _torch_stage(inp, scale, Wa, bo)
+    f, g = O.fwd_bwd(inp["H_dec"], inp["H_enc"], inp["src_len"], inp["tgt_len"],
+                     inp["tgt_ids"], inp["W_c"], inp["W_out"], scale, W_alpha=Wa, b_out=bo)
     assert abs(f["loss"] - ref["loss"]) < 1e-12 * abs(ref["loss"])
     for k in ("alpha", "C", "Hc"):
         np.testing.assert_allclose(f[k], ref[k], rtol=1e-11, atol=1e-14)
-    keys = ["dH_dec", "dH_enc", "dW_c", "dW_out"] + (["dW_alpha"] if with_alpha else [])
+    keys = (["dH_dec", "dH_enc", "dW_c", "dW_out"] + (["dW_alpha"] if with_alpha else [])
+            + (["db_out"] if with_bias else []))
     for k in keys:
         assert _rel_l2(g[k], ref[k]) < 1e-11, k
 
@@ -395,3 +408,46 @@ def test_cross_entropy_special_case():
     assert abs(nll.sum() - ref.item()) < 1e-12 * abs(ref.item())
     # lse of a constant row is c + ln V exactly (closed form)
     assert abs(O.log_sum_exp(np.full((1, 50), 2.5))[0] - (2.5 + math.log(50))) < 1e-14
+
+
+# ------------------------------------------------------ F_c bias (NEXT-1) --
+def test_e6_bias_only_closed_form():
+    """E6: W_out = 0 with a bias b: every valid row's logits are b, so
+    loss = scale * sum_valid (logsumexp(b) - b_y) and
+    db_out = scale * (T_valid softmax(b) - count_valid(y)); dHc = dl W_out = 0,
+    so dW_c, dH_dec and dH_enc vanish exactly."""
+    cfg = CONFIGS["tiny_ragged"]
+    inp = make_inputs(cfg, with_bias=True)
+    b = inp["b_out"].astype(np.float64)
+    V = cfg.V
+    W0 = np.zeros((V, cfg.d))
+    scale = 0.37
+    f, g = O.fwd_bwd(inp["H_dec"], inp["H_enc"], inp["src_len"], inp["tgt_len"],
+                     inp["tgt_ids"], inp["W_c"], W0, scale, b_out=b)
+    lse_b = math.log(sum(math.exp(x) for x in b))
+    ys = [int(inp["tgt_ids"][i, j]) for i in range(cfg.B) for j in range(int(inp["tgt_len"][i]))]
+    loss = scale * sum(lse_b - b[y] for y in ys)
+    assert abs(f["loss"] - loss) < 1e-12 * abs(loss)
+    p = np.array([math.exp(x - lse_b) for x in b])
+    counts = np.bincount(ys, minlength=V)
+    np.testing.assert_allclose(g["db_out"], scale * (len(ys) * p - counts), rtol=1e-11, atol=1e-14)
+    assert np.all(g["dW_c"] == 0) and np.all(g["dH_dec"] == 0) and np.all(g["dH_enc"] == 0)
+
+
+def test_bias_shift_invariance_and_zero_sum():
+    """Softmax is invariant to a constant shift of the bias: b_out + c gives
+    the same loss and gradients; and db_out sums to zero (each dl row does)."""
+    cfg = CONFIGS["small_f32"]
+    inp = make_inputs(cfg, with_bias=True)
+    scale = 1.0 / int(inp["tgt_len"].sum())
+    args = (inp["H_dec"], inp["H_enc"], inp["src_len"], inp["tgt_len"], inp["tgt_ids"],
+            inp["W_c"], inp["W_out"], scale)
+    f0, g0 = O.fwd_bwd(*args, b_out=inp["b_out"])
+    f1, g1 = O.fwd_bwd(*args, b_out=inp["b_out"].astype(np.float64) + 3.25)
+    assert abs(f0["loss"] - f1["loss"]) < 1e-11 * abs(f0["loss"])
+    for k in ("dW_out", "dW_c", "dH_dec", "dH_enc", "db_out"):
+        np.testing.assert_allclose(g1[k], g0[k], rtol=1e-8, atol=1e-15)
+    assert abs(g0["db_out"].sum()) < 1e-12
+    # and a nonzero bias really changes the result (the term is not dropped)
+    f2, _ = O.fwd_bwd(*args)
+    assert abs(f2["loss"] - f0["loss"]) > 1e-3
