@@ -122,6 +122,28 @@ attn_status_t attn_softmax_fwd_bwd(
     attn_comm_t* comm,
     void* stream);
 
+/* attn_softmax_fwd_bwd plus the optional F_c bias of Eq. 5 (NEXT-1):
+ *   b_out [V] (s->dtype, read-only) makes the logits l_iv = W_out[v] . Hc_i +
+ *   b_out[v] (SPEC.md:171's "Hdim x V plus bias" reading of the paper's
+ *   linear F_c); db_out [V] fp32 receives
+ *   sum_{valid rows} loss_scale (softmax(l_i) - onehot(y_i)), overwritten
+ *   (allreduced when comm != NULL).  b_out and db_out are both NULL (no bias:
+ *   identical to attn_softmax_fwd_bwd) or both set, else
+ *   ATTN_ERR_INVALID_ARG.  Everything else as attn_softmax_fwd_bwd. */
+attn_status_t attn_softmax_fwd_bwd_ex(
+    const attn_shape_t* s,
+    const void* H_dec, const void* H_enc,
+    const int32_t* src_lens_host, const int32_t* tgt_lens_host,
+    const int32_t* tgt_ids,
+    const void* W_c, const void* W_out, const void* W_alpha, const void* b_out,
+    float loss_scale,
+    float* loss,
+    void* dH_dec, void* dH_enc,
+    float* dW_c, float* dW_out, float* dW_alpha, float* db_out,
+    void* workspace, size_t workspace_bytes,
+    attn_comm_t* comm,
+    void* stream);
+
 /* End-to-end variant for callers whose per-step activations live in HOST
  * memory (pinned for overlap): H_dec_host, H_enc_host and tgt_ids_host are
  * copied host->device into `staging` (size attn_softmax_host_staging_size),

@@ -24,7 +24,7 @@ STATUS = {0: "ATTN_OK", 1: "ATTN_ERR_INVALID_ARG", 2: "ATTN_ERR_SHAPE",
 
 # every symbol include/attn_softmax.h and attn_softmax_debug.h declare
 EXPORTS = [
-    "attn_softmax_workspace_size", "attn_softmax_fwd_bwd",
+    "attn_softmax_workspace_size", "attn_softmax_fwd_bwd", "attn_softmax_fwd_bwd_ex",
     "attn_softmax_host_staging_size", "attn_softmax_fwd_bwd_host",
     "attn_softmax_prefetch_host", "attn_softmax_fwd_bwd_staged",
     "attn_softmax_check_ids", "attn_grad_allreduce", "attn_comm_get_unique_id",
@@ -75,6 +75,10 @@ def lib() -> ctypes.CDLL:
                                        ctypes.c_float, _P, _P, _P, _P, _P, _P,
                                        _P, ctypes.c_size_t, _P, _P]
     L.attn_softmax_fwd_bwd.restype = ctypes.c_int
+    L.attn_softmax_fwd_bwd_ex.argtypes = [S, _P, _P, i32p, i32p, _P, _P, _P, _P, _P,
+                                          ctypes.c_float, _P, _P, _P, _P, _P, _P, _P,
+                                          _P, ctypes.c_size_t, _P, _P]
+    L.attn_softmax_fwd_bwd_ex.restype = ctypes.c_int
     L.attn_softmax_host_staging_size.argtypes = [S]
     L.attn_softmax_host_staging_size.restype = ctypes.c_size_t
     L.attn_softmax_fwd_bwd_host.argtypes = [S, _P, _P, i32p, i32p, _P, _P, _P,
@@ -175,6 +179,20 @@ def attn_softmax_fwd_bwd(s, H_dec, H_enc, src_lens, tgt_lens, tgt_ids, W_c,
         ctypes.byref(s), _ptr(H_dec), _ptr(H_enc), src_p, tgt_p, _ptr(tgt_ids),
         _ptr(W_c), _ptr(W_out), _ptr(W_alpha), float(loss_scale), _ptr(loss),
         _ptr(dH_dec), _ptr(dH_enc), _ptr(dW_c), _ptr(dW_out), _ptr(dW_alpha),
+        _ptr(workspace), workspace.numel() * workspace.element_size(),
+        comm, _stream(stream)))
+
+
+def attn_softmax_fwd_bwd_ex(s, H_dec, H_enc, src_lens, tgt_lens, tgt_ids, W_c, W_out,
+                            loss_scale, loss, dH_dec, dH_enc, dW_c, dW_out, workspace,
+                            comm=None, stream=None, W_alpha=None, dW_alpha=None, b_out=None,
+                            db_out=None):
+    src, src_p = _i32(src_lens)
+    tgt, tgt_p = _i32(tgt_lens)
+    _check(lib().attn_softmax_fwd_bwd_ex(
+        ctypes.byref(s), _ptr(H_dec), _ptr(H_enc), src_p, tgt_p, _ptr(tgt_ids),
+        _ptr(W_c), _ptr(W_out), _ptr(W_alpha), _ptr(b_out), float(loss_scale), _ptr(loss),
+        _ptr(dH_dec), _ptr(dH_enc), _ptr(dW_c), _ptr(dW_out), _ptr(dW_alpha), _ptr(db_out),
         _ptr(workspace), workspace.numel() * workspace.element_size(),
         comm, _stream(stream)))
 

@@ -768,17 +768,20 @@ static GemmDesc g_proj(const Plan& p, const void* H, const void* ctx, const void
   return g;
 }
 // F4 (Eq. 5): logits tile -> (max, sumexp) partials + target logit
-static GemmDesc g_vocab_fwd(const Plan& p, const Bufs& b, const void* W_out, const int* tgt) {
+static GemmDesc g_vocab_fwd(const Plan& p, const Bufs& b, const void* W_out, const int* tgt,
+                            const void* b_out) {
   GemmDesc g;
   g.M = (int)p.T; g.N = p.V; g.K = p.d;
   g.a0 = kmaj(b.hc, p.T, p.d, p.d);
   g.b0 = kmaj(W_out, p.V, p.d, p.d);
   g.epi.kind = EPI_LSE; g.epi.ncols_valid = p.V; g.epi.ncols_store = p.V; g.epi.col_base = 0;
   g.epi.part = b.part; g.epi.part_ld = p.part_ld; g.epi.tgt_logit = b.tgt_logit; g.epi.tgt = tgt;
+  g.epi.bias = b_out;
   return g;
 }
 // B1, chunk c: dlogits_c = rowscale (softmax - onehot) of the recomputed logits
-static GemmDesc g_dlogits(const Plan& p, const Bufs& b, const void* W_out, const int* tgt, int c) {
+static GemmDesc g_dlogits(const Plan& p, const Bufs& b, const void* W_out, const int* tgt, int c,
+                          const void* b_out) {
   GemmDesc g;
   const int c0 = c * p.Vc, vcc = std::min(p.Vc, p.V - c0);
   g.M = (int)p.T; g.N = vcc; g.K = p.d;
@@ -788,6 +791,7 @@ static GemmDesc g_dlogits(const Plan& p, const Bufs& b, const void* W_out, const
   g.epi.ncols_valid = vcc; g.epi.ncols_store = p.bf16 ? vcc : p.Vc; g.epi.col_base = c0;
   g.epi.lse = b.lse; g.epi.rowscale = b.rowscale; g.epi.tgt = tgt;
   g.epi.tgt_logit = b.tgt_logit;
+  g.epi.bias = b_out;
   return g;
 }
 // B1, chunk c: dW_out[c] = dlogits_c^T H_c   (both operands MN-major)
@@ -972,9 +976,10 @@ static int* next_counter_fn(void* c) {
 
 template <typename T>
 static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int32_t* tgt_ids,
-                               const T* W_c, const T* W_out, const T* Wa, float loss_scale,
-                               float* loss, T* dH, T* dS, float* dW_c, float* dW_out, float* dWa,
-                               const Bufs& b, attn_comm_t* comm, cudaStream_t stream) {
+                               const T* W_c, const T* W_out, const T* Wa, const T* b_out,
+                               float loss_scale, float* loss, T* dH, T* dS, float* dW_c,
+                               float* dW_out, float* dWa, float* db_out, const Bufs& b,
+                               attn_comm_t* comm, cudaStream_t stream) {
   attn_status_t st;
   const bool tc = p.bf16;
   CounterCtx cctx{&b, 0};
@@ -1010,7 +1015,7 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   prof_mark("proj_tanh", stream);
   // ---- F4 (Eq. 5): logits discarded, per-tile (max, sumexp) kept
   {
-    GemmDesc g = g_vocab_fwd(p, b, W_out, tgt_ids);
+    GemmDesc g = g_vocab_fwd(p, b, W_out, tgt_ids, b_out);
     if ((st = gemm(&g, 1, PAIR_FWD)) != ATTN_OK) return st;
   }
   prof_mark("vocab_fwd", stream);
@@ -1034,15 +1039,24 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   {
     // chunk 0's dlogits alone: 128 x 256 tiles (short K; two accumulators in
     // TMEM so each tile's exp epilogue overlaps the next tile's MMAs)
-    GemmDesc g0 = g_dlogits(p, b, W_out, tgt_ids, 0);
+    GemmDesc g0 = g_dlogits(p, b, W_out, tgt_ids, 0, b_out);
     if ((st = gemm(&g0, 1, 0)) != ATTN_OK) return st;
     for (int c = 0; c < p.nchunks; ++c) {
       GemmDesc gs[3];
       int n = 0;
       gs[n++] = g_dwout(p, b, dW_out, c);   // K = T: the long tiles first
       gs[n++] = g_dhc(p, b, W_out, c);
-      if (c + 1 < p.nchunks) gs[n++] = g_dlogits(p, b, W_out, tgt_ids, c + 1);
+      if (c + 1 < p.nchunks) gs[n++] = g_dlogits(p, b, W_out, tgt_ids, c + 1, b_out);
       if ((st = gemm(gs, n, PAIR_VBWD)) != ATTN_OK) return st;
+      if (db_out) {
+        // F_c bias: db_out[chunk c] = column sums of dlogits_c (still intact:
+        // the next launch is the one that overwrites its buffer)
+        const int c0 = c * p.Vc, vcc = std::min(p.Vc, p.V - c0);
+        colsum_kernel<T><<<(vcc + 63) / 64, dim3(32, 8), 0, stream>>>(
+            (const T*)b.dl[c & 1], p.Vc, (int)TT, vcc, db_out + c0);
+        CUDA_TRY(cudaGetLastError());
+        ++g_launches;
+      }
       if (comm) {
         const int c0 = c * p.Vc;
         const int vcc = std::min(p.Vc, p.V - c0);
@@ -1098,6 +1112,9 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   if (comm && dWa) {
     if ((st = comm_enqueue_allreduce(comm, &cr, stream, dWa, (size_t)d * d)) != ATTN_OK) return st;
   }
+  if (comm && db_out) {
+    if ((st = comm_enqueue_allreduce(comm, &cr, stream, db_out, (size_t)p.V)) != ATTN_OK) return st;
+  }
   if (comm) {
     if ((st = comm_enqueue_allreduce(comm, &cr, stream, loss, 1)) != ATTN_OK) return st;
     if ((st = comm_end(comm, &cr, stream)) != ATTN_OK) return st;
@@ -1105,16 +1122,20 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   return ATTN_OK;
 }
 
-extern "C" attn_status_t attn_softmax_fwd_bwd(
+extern "C" attn_status_t attn_softmax_fwd_bwd_ex(
     const attn_shape_t* s, const void* H_dec, const void* H_enc, const int32_t* src_lens_host,
     const int32_t* tgt_lens_host, const int32_t* tgt_ids, const void* W_c, const void* W_out,
-    const void* W_alpha, float loss_scale, float* loss, void* dH_dec, void* dH_enc, float* dW_c,
-    float* dW_out, float* dW_alpha, void* workspace, size_t workspace_bytes, attn_comm_t* comm,
-    void* stream_) {
+    const void* W_alpha, const void* b_out, float loss_scale, float* loss, void* dH_dec,
+    void* dH_enc, float* dW_c, float* dW_out, float* dW_alpha, float* db_out, void* workspace,
+    size_t workspace_bytes, attn_comm_t* comm, void* stream_) {
   attn_status_t st = validate(s, H_dec, H_enc, src_lens_host, tgt_lens_host, tgt_ids, W_c, W_out,
                               W_alpha, loss, dH_dec, dH_enc, dW_c, dW_out, dW_alpha,
                               workspace_bytes, workspace);
   if (st != ATTN_OK) return st;
+  if ((b_out == nullptr) != (db_out == nullptr))
+    return fail(ATTN_ERR_INVALID_ARG,
+                "b_out and db_out go together: both NULL (no F_c bias, DESIGN.md R6) or both set; "
+                "got b_out=%p db_out=%p", b_out, (const void*)db_out);
   cudaStream_t stream = (cudaStream_t)stream_;
   const Plan p = make_plan(s);
   const Bufs b = carve(p, workspace);
@@ -1128,12 +1149,25 @@ extern "C" attn_status_t attn_softmax_fwd_bwd(
     return run_stage<__nv_bfloat16>(p, (const __nv_bfloat16*)H_dec, (const __nv_bfloat16*)H_enc,
                                     tgt_ids, (const __nv_bfloat16*)W_c,
                                     (const __nv_bfloat16*)W_out, (const __nv_bfloat16*)W_alpha,
-                                    loss_scale, loss, (__nv_bfloat16*)dH_dec,
-                                    (__nv_bfloat16*)dH_enc, dW_c, dW_out, dW_alpha, b, comm,
-                                    stream);
+                                    (const __nv_bfloat16*)b_out, loss_scale, loss,
+                                    (__nv_bfloat16*)dH_dec, (__nv_bfloat16*)dH_enc, dW_c, dW_out,
+                                    dW_alpha, db_out, b, comm, stream);
   return run_stage<float>(p, (const float*)H_dec, (const float*)H_enc, tgt_ids, (const float*)W_c,
-                          (const float*)W_out, (const float*)W_alpha, loss_scale, loss,
-                          (float*)dH_dec, (float*)dH_enc, dW_c, dW_out, dW_alpha, b, comm, stream);
+                          (const float*)W_out, (const float*)W_alpha, (const float*)b_out,
+                          loss_scale, loss, (float*)dH_dec, (float*)dH_enc, dW_c, dW_out,
+                          dW_alpha, db_out, b, comm, stream);
+}
+
+extern "C" attn_status_t attn_softmax_fwd_bwd(
+    const attn_shape_t* s, const void* H_dec, const void* H_enc, const int32_t* src_lens_host,
+    const int32_t* tgt_lens_host, const int32_t* tgt_ids, const void* W_c, const void* W_out,
+    const void* W_alpha, float loss_scale, float* loss, void* dH_dec, void* dH_enc, float* dW_c,
+    float* dW_out, float* dW_alpha, void* workspace, size_t workspace_bytes, attn_comm_t* comm,
+    void* stream_) {
+  return attn_softmax_fwd_bwd_ex(s, H_dec, H_enc, src_lens_host, tgt_lens_host, tgt_ids, W_c,
+                                 W_out, W_alpha, nullptr, loss_scale, loss, dH_dec, dH_enc, dW_c,
+                                 dW_out, dW_alpha, nullptr, workspace, workspace_bytes, comm,
+                                 stream_);
 }
 
 // ------------------------------------------------------------------ host-buffer variant

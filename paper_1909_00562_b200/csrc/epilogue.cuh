@@ -54,6 +54,8 @@ struct EpiParams {
   const int* src_len;    // ATTN_SOFTMAX: [batch]
   const float* addend;   // ADD_BF16: [rows, add_ld] fp32
   long long add_ld;
+  const void* bias;      // LSE / DLOGITS: optional F_c bias b_out [V] (OutT), indexed by
+                         // col_base + column (NEXT-1); NULL on the hot path
 };
 
 template <typename T> __device__ __forceinline__ T to_out(float x);
@@ -118,6 +120,22 @@ __device__ __forceinline__ void store_row32(OutT* rowp, int col0, int ncols_stor
   }
 }
 
+// v[j] += b[col + j] for the 32 columns of a chunk that are < nvalid (all
+// threads read the same addresses: broadcast loads).
+template <typename OutT>
+__device__ __forceinline__ void add_bias32(const void* bias, int gcol, int nvalid_rel,
+                                           float (&v)[32]) {
+  const OutT* b = reinterpret_cast<const OutT*>(bias) + gcol;
+  if (nvalid_rel >= 32) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] += to_f32(b[j]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nvalid_rel) v[j] += to_f32(b[j]);
+  }
+}
+
 struct LseState {
   float m, s, t;
   int has_t;
@@ -163,6 +181,7 @@ struct RowEpilogue {
     if (kind == EPI_LSE) {
       const int nv = p.ncols_valid - col0;
       if (nv <= 0) return;
+      if (p.bias) add_bias32<OutT>(p.bias, p.col_base + col0, nv, v);
       float cm = -INFINITY;
 #pragma unroll
       for (int j = 0; j < 32; ++j)
@@ -185,6 +204,7 @@ struct RowEpilogue {
     } else if (kind == EPI_DLOGITS) {
       if (col0 >= p.ncols_store) return;
       const int yl = y - col0;
+      if (p.bias) add_bias32<OutT>(p.bias, p.col_base + col0, p.ncols_valid - col0, v);
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         float g = rs * (exp_f<kFast>(v[j] - lse) - (j == yl ? 1.f : 0.f));
@@ -223,6 +243,7 @@ struct RowEpilogue {
       // MUFU ex2 per element; the -rs onehot term is written separately (the
       // engine overwrites the target column with `fix`).  (Moving part of the
       // exponentials to an FMA-pipe polynomial measured slower.)
+      if (p.bias) add_bias32<OutT>(p.bias, p.col_base + col0, p.ncols_valid - col0, v);
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = ex2_mufu(fmaf(v[j], kLog2e, c2));
     } else if (kind == EPI_TANH) {

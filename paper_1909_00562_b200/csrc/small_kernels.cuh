@@ -10,6 +10,8 @@
 //                        token NLL lse_t - l_{t,y_t} on valid rows, the row
 //                        scale of the backward, and the deterministic loss sum.
 //   check_ids_kernel     target-id range check (ATTN_ERR_TOKEN_RANGE)
+//   colsum_kernel        db_out of the F_c bias (NEXT-1): column sums of one
+//                        dlogits V-chunk, fixed summation order
 #pragma once
 #include <cstdint>
 
@@ -139,6 +141,39 @@ __global__ void __launch_bounds__(256) dz_kernel(const float* __restrict__ dhc,
   for (long long k = i; k < n; k += stride) {
     const float h = to_f32(hc[k]);
     dz[k] = to_out<T>(dhc[k] * (1.f - h * h));
+  }
+}
+
+// db[c] = sum_t dl[t, c] for c < ncols (dl row stride ld).  Block (32, 8):
+// 64 columns per block, thread (x, y) sums columns 2x, 2x+1 over rows
+// y, y+8, ...; the 8 row partials are then added in a fixed order.
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ dl, long long ld, int rows,
+                                                     int ncols, float* __restrict__ db) {
+  __shared__ float part[8][64];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int c = blockIdx.x * 64 + 2 * tx;
+  float s0 = 0.f, s1 = 0.f;
+  if (c < ncols) {
+    const bool two = c + 1 < ncols;
+    for (int r = ty; r < rows; r += 8) {
+      const T* row = dl + (long long)r * ld + c;
+      s0 += to_f32(row[0]);
+      if (two) s1 += to_f32(row[1]);
+    }
+  }
+  part[ty][2 * tx] = s0;
+  part[ty][2 * tx + 1] = s1;
+  __syncthreads();
+  if (ty == 0) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int cc = 2 * tx + k;
+      float t = 0.f;
+#pragma unroll
+      for (int y = 0; y < 8; ++y) t += part[y][cc];
+      if (blockIdx.x * 64 + cc < ncols) db[blockIdx.x * 64 + cc] = t;
+    }
   }
 }
 

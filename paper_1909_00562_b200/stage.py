@@ -24,7 +24,7 @@ class AttnSoftmaxStage:
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.views_meta = binding.attn_softmax_workspace_views(self.shape)
 
-    def alloc_outputs(self, general_score: bool = False):
+    def alloc_outputs(self, general_score: bool = False, bias: bool = False):
         dev, B, N, M, d, V = self.device, self.B, self.N, self.M, self.d, self.V
         out = dict(
             loss=torch.empty(1, dtype=torch.float32, device=dev),
@@ -34,19 +34,32 @@ class AttnSoftmaxStage:
             dW_out=torch.empty(V, d, dtype=torch.float32, device=dev))
         if general_score:
             out["dW_alpha"] = torch.empty(d, d, dtype=torch.float32, device=dev)
+        if bias:
+            out["db_out"] = torch.empty(V, dtype=torch.float32, device=dev)
         return out
 
     def __call__(self, H_dec, H_enc, src_len, tgt_len, tgt_ids, W_c, W_out,
-                 loss_scale: float, out=None, comm=None, stream=None, W_alpha=None):
+                 loss_scale: float, out=None, comm=None, stream=None, W_alpha=None,
+                 b_out=None):
         """W_alpha [d,d] (dtype of the stage) selects the Eq. 2 "general"
-        score; None is the dot score of the hot path."""
+        score; None is the dot score of the hot path.
+        b_out [V] adds the F_c bias of Eq. 5 (NEXT-1); out["db_out"] is its
+        gradient."""
         if out is None:
-            out = self.alloc_outputs(W_alpha is not None)
-        binding.attn_softmax_fwd_bwd(
-            self.shape, H_dec, H_enc, src_len, tgt_len, tgt_ids, W_c, W_out,
-            loss_scale, out["loss"], out["dH_dec"], out["dH_enc"], out["dW_c"],
-            out["dW_out"], self.workspace, comm=comm, stream=stream,
-            W_alpha=W_alpha, dW_alpha=out.get("dW_alpha") if W_alpha is not None else None)
+            out = self.alloc_outputs(W_alpha is not None, b_out is not None)
+        dWa = out.get("dW_alpha") if W_alpha is not None else None
+        if b_out is None:
+            binding.attn_softmax_fwd_bwd(
+                self.shape, H_dec, H_enc, src_len, tgt_len, tgt_ids, W_c, W_out,
+                loss_scale, out["loss"], out["dH_dec"], out["dH_enc"], out["dW_c"],
+                out["dW_out"], self.workspace, comm=comm, stream=stream,
+                W_alpha=W_alpha, dW_alpha=dWa)
+        else:
+            binding.attn_softmax_fwd_bwd_ex(
+                self.shape, H_dec, H_enc, src_len, tgt_len, tgt_ids, W_c, W_out,
+                loss_scale, out["loss"], out["dH_dec"], out["dH_enc"], out["dW_c"],
+                out["dW_out"], self.workspace, comm=comm, stream=stream,
+                W_alpha=W_alpha, dW_alpha=dWa, b_out=b_out, db_out=out["db_out"])
         return out
 
     def views(self):
@@ -71,7 +84,7 @@ def to_device(inp: dict, dtype: str, device="cuda"):
     """numpy inputs from synthetic.make_inputs -> torch device tensors."""
     td = _TORCH_DTYPE[dtype]
     out = {}
-    for k in ("H_dec", "H_enc", "W_c", "W_out", "W_alpha"):
+    for k in ("H_dec", "H_enc", "W_c", "W_out", "W_alpha", "b_out"):
         if k in inp:
             out[k] = torch.from_numpy(inp[k]).to(device=device, dtype=td).contiguous()
     out["tgt_ids"] = torch.from_numpy(inp["tgt_ids"]).to(device=device, dtype=torch.int32).contiguous()

@@ -127,6 +127,15 @@ def test_null_and_workspace_errors(built_lib):
     assert e.value.status == "ATTN_ERR_UNSUPPORTED"
 
 
+def test_bias_args_go_together(built_lib):
+    s = binding.shape(2, 5, 5, 64, 300, "bf16")
+    f = _Fake()
+    with pytest.raises(AttnError) as e:
+        binding.attn_softmax_fwd_bwd_ex(s, f, f, [5, 3], [5, 4], f, f, f, 1.0, f, f, f, f, f,
+                                        f, stream=0, b_out=f)
+    assert e.value.status == "ATTN_ERR_INVALID_ARG" and "db_out" in str(e.value)
+
+
 def test_options_and_comm_args(built_lib):
     with pytest.raises(AttnError):
         binding.attn_softmax_set_option("vocab_chunk", 100)

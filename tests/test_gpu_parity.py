@@ -28,7 +28,8 @@ def run_gpu(cfg, inp, scale, vocab_chunk=0, comm=None):
         st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
         dv = to_device(inp, cfg.dtype)
         out = st(dv["H_dec"], dv["H_enc"], dv["src_len"], dv["tgt_len"], dv["tgt_ids"],
-                 dv["W_c"], dv["W_out"], scale, W_alpha=dv.get("W_alpha"), comm=comm)
+                 dv["W_c"], dv["W_out"], scale, W_alpha=dv.get("W_alpha"), comm=comm,
+                 b_out=dv.get("b_out"))
         torch.cuda.synchronize()
     finally:
         binding.attn_softmax_set_option("vocab_chunk", 0)
@@ -44,7 +45,7 @@ def run_gpu(cfg, inp, scale, vocab_chunk=0, comm=None):
 def oracle(inp, scale):
     return O.fwd_bwd(inp["H_dec"], inp["H_enc"], inp["src_len"], inp["tgt_len"],
                      inp["tgt_ids"], inp["W_c"], inp["W_out"], scale,
-                     W_alpha=inp.get("W_alpha"))
+                     W_alpha=inp.get("W_alpha"), b_out=inp.get("b_out"))
 
 
 # ------------------------------------------------------------ GEMM core ----
@@ -171,6 +172,41 @@ def test_parity_general_score(cuda_lib, name, vc, mode):
         assert np.all(g["dH_dec"][bb, Tb:] == 0.0)
 
 
+@pytest.mark.parametrize("name,vc,mode,alpha", [("tiny_ragged", 0, "p8", False),
+                                                ("small_f32", 256, "p8", True),
+                                                ("odd_f32", 0, "p8", False),
+                                                ("small", 0, "default", False),
+                                                ("small", 1024, "p15", True),
+                                                ("medium", 0, "default", False),
+                                                ("medium", 2048, "w0", True),
+                                                ("odd", 256, "w15", False)])
+def test_parity_output_bias(cuda_lib, name, vc, mode, alpha):
+    """NEXT-1: the F_c bias b_out of Eq. 5 -- added in the
+    forward LSE and the backward dlogits epilogues, db_out = column sums of
+    each dlogits V-chunk -- against the oracle (with and without W_alpha)."""
+    from paper_1909_00562_b200 import binding
+    cfg = CONFIGS[name]
+    inp = make_inputs(cfg, with_alpha=alpha, with_bias=True)
+    scale = 1.0 / global_valid_tokens(cfg, cfg.B)
+    set_modes(binding, mode)
+    try:
+        g = run_gpu(cfg, inp, scale, vocab_chunk=vc)
+    finally:
+        set_modes(binding, "default")
+    f, b = oracle(inp, scale)
+    tol = TOL[cfg.dtype]
+    assert abs(g["loss"] - f["loss"]) <= tol["loss"] * abs(f["loss"]), (g["loss"], f["loss"])
+    keys = ["dH_dec", "dH_enc", "dW_c", "dW_out", "db_out"] + (["dW_alpha"] if alpha else [])
+    for k in keys:
+        e = rel_l2(g[k], b[k])
+        assert e <= tol["grad"], (k, e)
+    lse_tol = 1e-4 if cfg.dtype == "f32" else 2e-2
+    assert np.max(np.abs(g["lse"] - f["lse"])) <= lse_tol
+    for bb in range(cfg.B):
+        Tb = int(inp["tgt_len"][bb])
+        assert np.all(g["dH_dec"][bb, Tb:] == 0.0)
+
+
 @pytest.mark.parametrize("name", ["tiny_ragged", "small"])
 def test_padding_garbage_is_bitwise_inert(cuda_lib, name):
     """I5: finite garbage in padded slots changes no GPU output bit."""
@@ -287,6 +323,13 @@ def test_single_rank_nccl_communicator(cuda_lib):
         torch.cuda.synchronize()
         for k in ("loss", "dH_dec", "dH_enc", "dW_c", "dW_out", "dW_alpha"):
             assert torch.equal(out_a[k], ref_a[k]), k
+        # F_c bias (NEXT-1): db_out joins the allreduce
+        bo = to_device(make_inputs(cfg, with_bias=True), cfg.dtype)["b_out"]
+        ref_b = {k: v.clone() for k, v in st(*args, b_out=bo).items()}
+        out_b = st(*args, b_out=bo, comm=comm)
+        torch.cuda.synchronize()
+        for k in ("loss", "dH_dec", "dH_enc", "dW_c", "dW_out", "db_out"):
+            assert torch.equal(out_b[k], ref_b[k]), k
         buf = torch.arange(1000, dtype=torch.float32, device="cuda")
         binding.attn_grad_allreduce(comm, buf)
         torch.cuda.synchronize()
