@@ -119,6 +119,10 @@ static long long* g_trace = nullptr;   // "gemm_trace": device pointer of a per-
 static long long g_trace_launch = -1;  // "gemm_trace_launch": trace only this launch index of a call (-1 = all)
 static int64_t g_opt_vocab_chunk = 0;
 static int64_t g_opt_gemm_ctas = 0;
+// "pdl": launch the bf16 path's kernels as programmatic dependents of the
+// previous kernel (their prologue overlaps its tail; they griddepcontrol.wait
+// before touching its results)
+static int g_opt_pdl = 1;
 
 extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value) {
   if (!key) return fail(ATTN_ERR_INVALID_ARG, "set_option: key is NULL");
@@ -159,6 +163,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "stage_events")) {
     g_prof.on = value != 0;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "pdl")) {
+    g_opt_pdl = value != 0;
     return ATTN_OK;
   }
   if (!strcmp(key, "gemm_ctas")) {
@@ -402,13 +410,22 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = tc_smem_bytes();
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = csize;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (csize > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = csize;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (g_opt_pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = csize > 1 ? 1 : 0;
+  cfg.numAttrs = na;
   CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<OutT, true, kPair>, P));
   ++g_launches;
   return ATTN_OK;
@@ -428,6 +445,26 @@ static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cu
   if (group_bit && (g_opt_pair & group_bit))
     return launch_tc_group_k<OutT, 2>(gs, n, counter, stream, group_bit);
   return launch_tc_group_k<OutT, 1>(gs, n, counter, stream, group_bit);
+}
+
+// Launch a plain kernel, as a programmatic dependent of the previous kernel
+// when the "pdl" option is on (the kernel must pdl_wait() first).
+template <typename... KArgs, typename... Args>
+static attn_status_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t stream,
+                                Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_opt_pdl ? 1 : 0;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+  ++g_launches;
+  return ATTN_OK;
 }
 
 static attn_status_t launch_simt_group(const GemmDesc* gs, int n, cudaStream_t stream) {
@@ -1022,11 +1059,10 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   // ---- Eq. 6: lse, token NLL, row scale, loss
   {
     const int blocks = (int)((TT + 7) / 8);
-    lse_reduce_kernel<<<blocks, 256, 0, stream>>>(b.part, p.part_ld, b.tgt_logit, b.tgt_len, (int)TT,
-                                                  p.N, loss_scale, b.lse, b.nll, b.rowscale,
-                                                  b.blockpart, b.counters, loss);
-    CUDA_TRY(cudaGetLastError());
-    ++g_launches;
+    st = launch_pdl(lse_reduce_kernel, dim3(blocks), dim3(256), stream, (const float2*)b.part,
+                    p.part_ld, (const float*)b.tgt_logit, (const int*)b.tgt_len, (int)TT, p.N,
+                    loss_scale, b.lse, b.nll, b.rowscale, b.blockpart, b.counters, loss);
+    if (st != ATTN_OK) return st;
   }
   prof_mark("lse_reduce", stream);
   CommRun cr;
@@ -1069,10 +1105,9 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   // tanh backward of Eq. 4: dz = dHc (1 - H_c^2)
   {
     const long long n = TT * d;
-    dz_kernel<T><<<(int)std::min<long long>((n + 255) / 256, 148ll * 16), 256, 0, stream>>>(
-        b.dhc, (const T*)b.hc, (T*)b.dz, n);
-    CUDA_TRY(cudaGetLastError());
-    ++g_launches;
+    st = launch_pdl(dz_kernel<T>, dim3((int)std::min<long long>((n + 255) / 256, 148ll * 16)),
+                    dim3(256), stream, (const float*)b.dhc, (const T*)b.hc, (T*)b.dz, n);
+    if (st != ATTN_OK) return st;
   }
   prof_mark("vocab_bwd", stream);
   // ---- B2: dW_c = dz^T [H | C];  dH_part = dz W_c[:, :d];  dC = dz W_c[:, d:]

@@ -315,6 +315,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // programmatic dependent launch: the prologue above overlapped the previous
+  // kernel's tail; wait for its results, then let the next kernel's CTAs be
+  // scheduled onto SMs as this (persistent, fully resident) grid retires
+  pdl_wait();
+  if (threadIdx.x == 0) pdl_trigger();
 
   // shared::cluster addresses of the leader's barriers (pair mode)
   auto leader_addr = [&](void* p) -> uint32_t { return mapa_shared(smem_u32(p), 0); };

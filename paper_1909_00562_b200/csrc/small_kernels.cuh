@@ -16,6 +16,7 @@
 #include <cstdint>
 
 #include "epilogue.cuh"
+#include "ptx.cuh"
 
 namespace attnsm {
 
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(256) lse_reduce_kernel(
     const int* __restrict__ tgt_len, int T, int N, float loss_scale, float* __restrict__ lse_out,
     float* __restrict__ nll_out, float* __restrict__ rowscale, double* __restrict__ blockpart,
     unsigned int* __restrict__ done_counter, float* __restrict__ loss) {
+  pdl_wait();   // launched as a programmatic dependent of the vocab GEMM
   __shared__ double wsum[8];
   __shared__ bool is_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -136,6 +138,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) dz_kernel(const float* __restrict__ dhc,
                                                  const T* __restrict__ hc, T* __restrict__ dz,
                                                  long long n) {
+  pdl_wait();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long k = i; k < n; k += stride) {
