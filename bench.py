@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-sentences", type=int, default=0)
+    ap.add_argument("--no-next", action="store_true",
+                    help="skip the SURVEY §8(f) NEXT-row measurements (general score, bias, Adam)")
     ap.add_argument("--force-comm", action="store_true",
                     help="use the NCCL communicator even with one rank (exercises the path)")
     return ap.parse_args()
@@ -195,6 +197,66 @@ def run_reference(args, cfg, rank, world):
 
 
 # ------------------------------------------------------------ ours --------
+def measure_next_rows(binding, st, dv, cfg, scale, comm, stream, dev, pk, tok_local, world,
+                      steps=10):
+    """SURVEY §8(f) rows beyond the hot path, each timed with CUDA events on
+    the launching stream (not part of `value`): NEXT-1 the stage with the
+    Eq. 2 general score (W_alpha) and with the F_c bias b_out; NEXT-2 the Adam
+    step over the stage's parameters (sharded reduce-scatter / update /
+    all-gather when a communicator exists), HBM-bound: 30 B per parameter."""
+    import numpy as np
+    import torch
+    from synthetic import make_weights
+
+    def timed(fn, n=steps):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(n):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        return a.elapsed_time(b) / n
+
+    res = {}
+    extra = make_weights(cfg, with_alpha=True, with_bias=True)
+    td = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    Wa = torch.from_numpy(extra["W_alpha"]).to(device=dev, dtype=td)
+    bo = torch.from_numpy(extra["b_out"]).to(device=dev, dtype=td)
+    args = (dv["H_dec"], dv["H_enc"], dv["src_len"], dv["tgt_len"], dv["tgt_ids"],
+            dv["W_c"], dv["W_out"], scale)
+    outs = st.alloc_outputs(True, True)
+    for name, kw in (("general_score", dict(W_alpha=Wa)), ("output_bias", dict(b_out=bo))):
+        ms = timed(lambda: st(*args, out=outs, comm=comm, stream=stream, **kw))
+        res[name] = {"ms_per_step": ms, "target_tokens_per_s": tok_local * world / (ms / 1e3)}
+    # NEXT-2: Adam over W_out, W_c (and W_alpha, b_out would add d^2 + V)
+    n = cfg.V * cfg.d + 2 * cfg.d * cfg.d
+    h = binding.adam_params(1)
+    if comm is None:
+        w = torch.zeros(n, device=dev)
+        m, v, g = torch.zeros_like(w), torch.zeros_like(w), torch.full_like(w, 1e-3)
+        wb = torch.empty(n, dtype=torch.bfloat16, device=dev)
+        ms = timed(lambda: binding.attn_adam_step(h, w, m, v, g, wb, stream=stream))
+        nbytes = 30.0 * n
+        res["adam"] = {"params": n, "ms": ms, "sharded": False,
+                       "roofline": {"bound": "hbm", "achieved": nbytes / (ms / 1e3) / 1e9,
+                                    "peak": pk["hbm"], "unit": "GB/s",
+                                    "frac": nbytes / (ms / 1e3) / 1e9 / pk["hbm"],
+                                    "traffic": None}}
+    else:
+        S = binding.attn_adam_shard_len(comm, n)
+        g = torch.full((S * world,), 1e-3, device=dev)
+        w, m, v = (torch.zeros(S, device=dev) for _ in range(3))
+        wb = torch.empty(S * world, dtype=torch.bfloat16, device=dev)
+        ms = timed(lambda: binding.attn_adam_step_sharded(comm, h, n, g, w, m, v, wb,
+                                                          stream=stream))
+        res["adam"] = {"params": n, "ms": ms, "sharded": True, "shard": S,
+                       "wire_bytes_per_param": 6}
+    return res
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", 0))
@@ -363,6 +425,9 @@ def main():
                               "peak": pk["bf16"], "unit": "TFLOP/s"},
                 "stage_ms": {k: v / args.steps for k, v in stage_ms.items()}}
 
+    next_rows = None if args.no_next else measure_next_rows(
+        binding, st, dv, cfg, scale, comm, stream, dev, pk, tok_local, world)
+
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
@@ -376,6 +441,8 @@ def main():
             "loss": loss,
             "useful_tflops": tok_job * (6 * cfg.d * cfg.V + 12 * cfg.d ** 2 + 12 * cfg.M * cfg.d)
                              * args.steps / (total_ms / 1e3) / 1e12 / world}
+    if next_rows is not None:
+        line["next_rows"] = next_rows
     if world > 1:
         dist.barrier()
     if rank == 0:

@@ -212,6 +212,40 @@ attn_status_t attn_comm_init(const uint8_t id[128], int nranks, int rank,
                              int device, attn_comm_t** out);
 attn_status_t attn_comm_destroy(attn_comm_t* c);
 
+/* ---- NEXT-2: the optimizer step after the gradient exchange --------------
+ * Adam (Kingma & Ba 2015, Algorithm 1), the optimizer of the paper
+ * (PAPER.md:195 Table 2, :207: beta1 0.9, beta2 0.999, eps 1e-8, lr 1e-3):
+ *   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;
+ *   w -= lr (m / (1 - b1^step)) / (sqrt(v / (1 - b2^step)) + eps)
+ * in fp32 on device buffers, asynchronously on `stream`. */
+typedef struct {
+  double lr, beta1, beta2, eps; /* double so 1 - beta2 = 1e-3 is exact enough */
+  int32_t step; /* t >= 1 of Algorithm 1 (bias corrections 1 - beta^t) */
+} attn_adam_t;
+
+/* Replicated update of n parameters: w, m, v [n] fp32 (in/out, 16-byte
+ * aligned), g [n] fp32 (the summed gradient, read-only); w_bf16 [n] bf16 (out,
+ * 8-byte aligned) receives bf16(w) for the next step's GEMMs, or NULL. */
+attn_status_t attn_adam_step(const attn_adam_t* h, size_t n, float* w, float* m,
+                             float* v, const float* g, void* w_bf16, void* stream);
+
+/* Per-rank shard length S of an n-parameter vector on communicator c: the
+ * smallest multiple of 4 with nranks * S >= n (1 rank when c is NULL). */
+size_t attn_adam_shard_len(const attn_comm_t* c, size_t n);
+
+/* Sharded update (data-parallel ZeRO-1 style): g [nranks*S] fp32 holds this
+ * rank's LOCAL gradient of n parameters (the tail [n, nranks*S) is zeroed by
+ * the call); it is reduce-scattered in place (sum over ranks, NCCL), rank r
+ * updates its shard [r S, (r+1) S) with w_shard, m_shard, v_shard [S] fp32
+ * (its fp32 master weights and moments), writes bf16 weights into
+ * w_bf16 + r S, and w_bf16 [nranks*S] bf16 is all-gathered in place, so every
+ * rank ends with the full updated bf16 weights.  Wire bytes per parameter:
+ * 4 (reduce-scatter) + 2 (all-gather) instead of 8 for an fp32 allreduce.
+ * All buffers 16-byte aligned. */
+attn_status_t attn_adam_step_sharded(attn_comm_t* c, const attn_adam_t* h, size_t n,
+                                     float* g, float* w_shard, float* m_shard,
+                                     float* v_shard, void* w_bf16, void* stream);
+
 /* Thread-local message of the last failing call on this thread ("" if none). */
 const char* attn_last_error(void);
 

@@ -32,6 +32,7 @@ EXPORTS = [
     "attn_softmax_workspace_views", "attn_debug_gemm_bf16",
     "attn_softmax_set_option", "attn_softmax_stage_count",
     "attn_softmax_stage_time", "attn_softmax_last_launches",
+    "attn_adam_step", "attn_adam_shard_len", "attn_adam_step_sharded",
 ]
 
 
@@ -46,6 +47,11 @@ class AttnShape(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int32), ("tgt_len", ctypes.c_int32),
                 ("src_len", ctypes.c_int32), ("hidden", ctypes.c_int32),
                 ("vocab", ctypes.c_int32), ("dtype", ctypes.c_int32)]
+
+
+class AdamParams(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
+                ("eps", ctypes.c_double), ("step", ctypes.c_int32)]
 
 
 class AttnWsViews(ctypes.Structure):
@@ -121,6 +127,13 @@ def lib() -> ctypes.CDLL:
     L.attn_softmax_stage_time.restype = ctypes.c_int
     L.attn_softmax_last_launches.argtypes = []
     L.attn_softmax_last_launches.restype = ctypes.c_longlong
+    A = ctypes.POINTER(AdamParams)
+    L.attn_adam_step.argtypes = [A, ctypes.c_size_t, _P, _P, _P, _P, _P, _P]
+    L.attn_adam_step.restype = ctypes.c_int
+    L.attn_adam_shard_len.argtypes = [_P, ctypes.c_size_t]
+    L.attn_adam_shard_len.restype = ctypes.c_size_t
+    L.attn_adam_step_sharded.argtypes = [_P, A, ctypes.c_size_t, _P, _P, _P, _P, _P, _P]
+    L.attn_adam_step_sharded.restype = ctypes.c_int
     _lib = L
     return L
 
@@ -286,3 +299,24 @@ def attn_last_error() -> str:
 
 def attn_version() -> str:
     return lib().attn_version().decode()
+
+
+def adam_params(step, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8) -> AdamParams:
+    """Adam hyper-parameters; the defaults are the paper's."""
+    return AdamParams(lr, beta1, beta2, eps, int(step))
+
+
+def attn_adam_step(h: AdamParams, w, m, v, g, w_bf16=None, stream=None):
+    _check(lib().attn_adam_step(ctypes.byref(h), w.numel(), _ptr(w), _ptr(m), _ptr(v), _ptr(g),
+                                _ptr(w_bf16), _stream(stream)))
+
+
+def attn_adam_shard_len(comm, n: int) -> int:
+    return int(lib().attn_adam_shard_len(comm, n))
+
+
+def attn_adam_step_sharded(comm, h: AdamParams, n: int, g, w_shard, m_shard, v_shard, w_bf16,
+                           stream=None):
+    _check(lib().attn_adam_step_sharded(comm, ctypes.byref(h), n, _ptr(g), _ptr(w_shard),
+                                        _ptr(m_shard), _ptr(v_shard), _ptr(w_bf16),
+                                        _stream(stream)))

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "libattnsm.so")
-SOURCES = ["attn_softmax.cu", "comm.cu"]
+SOURCES = ["attn_softmax.cu", "comm.cu", "adam.cu"]
 HEADERS = ["ptx.cuh", "epilogue.cuh", "gemm_tc.cuh", "gemm_simt.cuh",
            "small_kernels.cuh", "comm.h"]
 

@@ -16,7 +16,7 @@ typedef struct ncclComm* ncclComm_t;
 typedef struct { char internal[128]; } ncclUniqueId;
 typedef int ncclResult_t;
 enum { ncclSuccess_ = 0, ncclInProgress_ = 7 };
-enum { ncclFloat32_ = 7 };
+enum { ncclFloat32_ = 7, ncclBfloat16_ = 9 };
 enum { ncclSum_ = 0 };
 
 struct NcclApi {
@@ -24,6 +24,8 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool ok = false;
   std::string why;
@@ -48,8 +50,11 @@ static NcclApi& nccl() {
     api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
     api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
     api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+    api.ReduceScatter = (decltype(api.ReduceScatter))dlsym(h, "ncclReduceScatter");
+    api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-    api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy;
+    api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy &&
+             api.ReduceScatter && api.AllGather;
     if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
   });
   return api;
@@ -61,6 +66,7 @@ struct attn_comm {
   std::vector<cudaEvent_t> events;  // fork events, reused round-robin
   cudaEvent_t join = nullptr;
   int device = 0;
+  int nranks = 1, rank = 0;
 };
 
 // errors are reported through attn_last_error(); defined in attn_softmax.cu
@@ -108,6 +114,8 @@ extern "C" attn_status_t attn_comm_init(const uint8_t id[128], int nranks, int r
   CUDA_OK(cudaSetDevice(device));
   attn_comm* c = new attn_comm();
   c->device = device;
+  c->nranks = nranks;
+  c->rank = rank;
   ncclUniqueId u;
   memcpy(u.internal, id, 128);
   ncclResult_t r = api.CommInitRank(&c->comm, nranks, u, rank);
@@ -164,5 +172,22 @@ attn_status_t comm_end(attn_comm_t* c, CommRun* run, cudaStream_t compute) {
   (void)run;
   CUDA_OK(cudaEventRecord(c->join, c->stream));
   CUDA_OK(cudaStreamWaitEvent(compute, c->join, 0));
+  return ATTN_OK;
+}
+
+int comm_nranks(const attn_comm_t* c) { return c ? c->nranks : 1; }
+int comm_rank(const attn_comm_t* c) { return c ? c->rank : 0; }
+
+attn_status_t comm_reduce_scatter_f32(attn_comm_t* c, float* buf, size_t shard, cudaStream_t s) {
+  // in place: rank r's summed shard lands at buf + r * shard
+  NCCL_OK(nccl().ReduceScatter(buf, buf + (size_t)c->rank * shard, shard, ncclFloat32_, ncclSum_,
+                               c->comm, s));
+  return ATTN_OK;
+}
+
+attn_status_t comm_all_gather_bf16(attn_comm_t* c, void* buf, size_t shard, cudaStream_t s) {
+  // in place: rank r contributes buf + r * shard
+  char* b = static_cast<char*>(buf);
+  NCCL_OK(nccl().AllGather(b + (size_t)c->rank * shard * 2, b, shard, ncclBfloat16_, c->comm, s));
   return ATTN_OK;
 }

@@ -24,3 +24,11 @@ attn_status_t comm_enqueue_allreduce(attn_comm_t* c, CommRun* run, cudaStream_t 
                                      float* buf, size_t count);
 // Make `compute` wait for every allreduce enqueued in this run.
 attn_status_t comm_end(attn_comm_t* c, CommRun* run, cudaStream_t compute);
+
+// NEXT-2 (sharded optimizer step): communicator size / rank, in-place fp32 sum
+// reduce-scatter (rank r's shard at buf + r * shard) and in-place bf16
+// all-gather, both enqueued on stream s.
+int comm_nranks(const attn_comm_t* c);
+int comm_rank(const attn_comm_t* c);
+attn_status_t comm_reduce_scatter_f32(attn_comm_t* c, float* buf, size_t shard, cudaStream_t s);
+attn_status_t comm_all_gather_bf16(attn_comm_t* c, void* buf, size_t shard, cudaStream_t s);

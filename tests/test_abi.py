@@ -145,3 +145,33 @@ def test_options_and_comm_args(built_lib):
     with pytest.raises(AttnError) as e:
         binding.attn_comm_init(b"\0" * 128, 2, 5, 0)
     assert e.value.status == "ATTN_ERR_INVALID_ARG"
+
+
+def test_adam_args(built_lib):
+    f = _Fake()
+    with pytest.raises(AttnError) as e:
+        binding.attn_adam_step(binding.adam_params(0), _Sized(8), _Sized(8), _Sized(8), _Sized(8),
+                               stream=0)
+    assert e.value.status == "ATTN_ERR_INVALID_ARG" and "step" in str(e.value)
+    with pytest.raises(AttnError) as e:
+        binding.attn_adam_step(binding.adam_params(1, beta1=1.0), _Sized(8), _Sized(8), _Sized(8),
+                               _Sized(8), stream=0)
+    assert e.value.status == "ATTN_ERR_INVALID_ARG"
+    with pytest.raises(AttnError) as e:
+        binding.attn_adam_step(binding.adam_params(1), _Sized(8, 0x10000004), _Sized(8),
+                               _Sized(8), _Sized(8), stream=0)
+    assert e.value.status == "ATTN_ERR_UNSUPPORTED"
+    with pytest.raises(AttnError) as e:
+        binding.attn_adam_step_sharded(None, binding.adam_params(1), 8, f, f, f, f, f, stream=0)
+    assert e.value.status == "ATTN_ERR_INVALID_ARG"
+    assert binding.attn_adam_shard_len(None, 10) == 12
+    assert binding.attn_adam_shard_len(None, 0) == 0
+
+
+class _Sized(_Fake):
+    def __init__(self, n, ptr=0x10000000):
+        super().__init__(n)
+        self._p = ptr
+
+    def data_ptr(self):
+        return self._p
