@@ -534,7 +534,7 @@ struct Plan {
   int nchunks;
   size_t off_lens, off_counters, off_blockpart, off_alpha, off_dalpha, off_ctx, off_hc, off_part,
       off_tgtlogit, off_lse, off_nll, off_rowscale, off_dl, off_dhc, off_dz, off_dhc2, off_abf,
-      off_debf, off_q;
+      off_debf, off_q, off_dbpart;
   int Mp;             // bf16 path: row stride of the bf16 alpha / de operands (64-multiple)
   size_t total;
 };
@@ -593,6 +593,7 @@ static Plan make_plan(const attn_shape_t* s) {
   p.off_abf = take(p.bf16 ? 2 * p.T * p.Mp : 0);
   p.off_debf = take(p.bf16 ? 2 * p.T * p.Mp : 0);
   p.off_q = take(p.elt * p.T * p.d);   // Eq. 2 general score: Q = H W_alpha
+  p.off_dbpart = take(sizeof(float) * 16 * (size_t)p.Vc);   // F_c bias: column-sum partials
   p.total = o;
   return p;
 }
@@ -709,6 +710,7 @@ struct Bufs {
   float* alpha; float* dalpha; void* ctx; void* hc; float2* part; float* tgt_logit;
   float* lse; float* nll; float* rowscale; void* dl[2]; float* dhc; void* dz; float* dhc2;
   void* abf; void* debf; float* dhpart; void* dcbf;   // bf16 path
+  float* dbpart;   // F_c bias: [16, Vc] column-sum partials
   void* q;    // Eq. 2 general score: Q = H W_alpha [T, d] (dtype)
   void* dq;   // its gradient [T, d] (dtype); aliases dz, which is dead by then
 };
@@ -739,6 +741,7 @@ static Bufs carve(const Plan& p, void* ws) {
   b.dhpart = b.dhc2;                          // bf16 path: dH_part fp32 [T, d]
   b.dcbf = (char*)(b.dhc2 + p.T * p.d);       //            dC bf16 [T, d]
   b.q = w + p.off_q;
+  b.dbpart = (float*)(w + p.off_dbpart);
   b.dq = b.dz;
   return b;
 }
@@ -1088,10 +1091,14 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
         // F_c bias: db_out[chunk c] = column sums of dlogits_c (still intact:
         // the next launch is the one that overwrites its buffer)
         const int c0 = c * p.Vc, vcc = std::min(p.Vc, p.V - c0);
-        colsum_kernel<T><<<(vcc + 63) / 64, dim3(32, 8), 0, stream>>>(
-            (const T*)b.dl[c & 1], p.Vc, (int)TT, vcc, db_out + c0);
+        const int splits = (int)std::min<long long>(16, std::max<long long>(1, TT / 256));
+        const int rps = (int)((TT + splits - 1) / splits);
+        float* part = b.dbpart;
+        colsum_part_kernel<T><<<dim3((vcc + 255) / 256, splits), 256, 0, stream>>>(
+            (const T*)b.dl[c & 1], p.Vc, (int)TT, rps, vcc, part);
+        colsum_final_kernel<<<(vcc + 255) / 256, 256, 0, stream>>>(part, splits, vcc, db_out + c0);
         CUDA_TRY(cudaGetLastError());
-        ++g_launches;
+        g_launches += 2;
       }
       if (comm) {
         const int c0 = c * p.Vc;

@@ -10,10 +10,11 @@
 //                        token NLL lse_t - l_{t,y_t} on valid rows, the row
 //                        scale of the backward, and the deterministic loss sum.
 //   check_ids_kernel     target-id range check (ATTN_ERR_TOKEN_RANGE)
-//   colsum_kernel        db_out of the F_c bias (NEXT-1): column sums of one
-//                        dlogits V-chunk, fixed summation order
+//   colsum_*_kernel      db_out of the F_c bias (NEXT-1): column sums of one
+//                        dlogits V-chunk, two passes in a fixed order
 #pragma once
 #include <cstdint>
+#include <cuda_bf16.h>
 
 #include "epilogue.cuh"
 #include "ptx.cuh"
@@ -147,37 +148,64 @@ __global__ void __launch_bounds__(256) dz_kernel(const float* __restrict__ dhc,
   }
 }
 
-// db[c] = sum_t dl[t, c] for c < ncols (dl row stride ld).  Block (32, 8):
-// 64 columns per block, thread (x, y) sums columns 2x, 2x+1 over rows
-// y, y+8, ...; the 8 row partials are then added in a fixed order.
+// db[c] = sum_t dl[t, c] for c < ncols (dl row stride ld, 16-byte aligned
+// rows), in two deterministic passes.  Pass 1: block (x, y) owns columns
+// [256 x, 256 x + 256) and the row split y; thread t of warp w loads 8
+// consecutive columns (16 bytes of bf16 / 2 x 16 of fp32) of rows
+// y*rps + w, +8, ...; the 8 warp partials are added in a fixed order into
+// part[y][c].  Pass 2 adds the splits in order.
 template <typename T>
-__global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ dl, long long ld, int rows,
-                                                     int ncols, float* __restrict__ db) {
-  __shared__ float part[8][64];
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int c = blockIdx.x * 64 + 2 * tx;
-  float s0 = 0.f, s1 = 0.f;
-  if (c < ncols) {
-    const bool two = c + 1 < ncols;
-    for (int r = ty; r < rows; r += 8) {
-      const T* row = dl + (long long)r * ld + c;
-      s0 += to_f32(row[0]);
-      if (two) s1 += to_f32(row[1]);
+__global__ void __launch_bounds__(256) colsum_part_kernel(const T* __restrict__ dl, long long ld,
+                                                          int rows, int rps, int ncols,
+                                                          float* __restrict__ part) {
+  __shared__ float red[8][257];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c0 = blockIdx.x * 256 + lane * 8;
+  const int r0 = blockIdx.y * rps, r1 = min(rows, r0 + rps);
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  if (c0 + 8 <= ncols) {
+    for (int r = r0 + w; r < r1; r += 8) {
+      const T* row = dl + (long long)r * ld + c0;
+      if constexpr (sizeof(T) == 2) {
+        const uint4 u = *reinterpret_cast<const uint4*>(row);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h[e]);
+          acc[2 * e] += f.x;
+          acc[2 * e + 1] += f.y;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += to_f32(row[e]);
+      }
     }
+  } else {
+    for (int r = r0 + w; r < r1; r += 8)
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (c0 + e < ncols) acc[e] += to_f32(dl[(long long)r * ld + c0 + e]);
   }
-  part[ty][2 * tx] = s0;
-  part[ty][2 * tx + 1] = s1;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) red[w][lane * 8 + e] = acc[e];
   __syncthreads();
-  if (ty == 0) {
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c < ncols) {
+    float t = 0.f;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int cc = 2 * tx + k;
-      float t = 0.f;
-#pragma unroll
-      for (int y = 0; y < 8; ++y) t += part[y][cc];
-      if (blockIdx.x * 64 + cc < ncols) db[blockIdx.x * 64 + cc] = t;
-    }
+    for (int k = 0; k < 8; ++k) t += red[k][threadIdx.x];
+    part[(long long)blockIdx.y * ncols + c] = t;
   }
+}
+__global__ void __launch_bounds__(256) colsum_final_kernel(const float* __restrict__ part, int splits,
+                                                           int ncols, float* __restrict__ db) {
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= ncols) return;
+  float t = 0.f;
+  for (int y = 0; y < splits; ++y) t += part[(long long)y * ncols + c];
+  db[c] = t;
 }
 
 __global__ void check_ids_kernel(const int* __restrict__ ids, const int* __restrict__ tgt_len,
