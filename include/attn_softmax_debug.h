@@ -17,7 +17,8 @@ extern "C" {
 
 /* Byte offsets, inside the workspace, of the intermediates that stay valid
  * after attn_softmax_fwd_bwd returns and its stream work completes.  T = B*N.
- *   alpha  fp32 [B,N,M]  attention weights (Eq. 1), exact 0 where masked
+ *   alpha  fp32 [B*N, alpha_ld] (columns < M) attention weights (Eq. 1), exact 0
+ *          where masked; alpha_ld = M (fp32 path) or M rounded up to 64 (bf16)
  *   ctx    dtype [T,d]   context vectors C (Eq. 3)
  *   hc     dtype [T,d]   attentional states H_c (Eq. 4)
  *   lse    fp32 [T]      log-sum-exp of the Eq. 5 logits per row
@@ -26,6 +27,7 @@ extern "C" {
 typedef struct {
   size_t alpha, ctx, hc, lse, nll;
   int64_t vocab_chunk;
+  int64_t alpha_ld;
 } attn_ws_views_t;
 
 attn_status_t attn_softmax_workspace_views(const attn_shape_t* s,

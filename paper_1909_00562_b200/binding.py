@@ -57,7 +57,8 @@ class AdamParams(ctypes.Structure):
 class AttnWsViews(ctypes.Structure):
     _fields_ = [("alpha", ctypes.c_size_t), ("ctx", ctypes.c_size_t),
                 ("hc", ctypes.c_size_t), ("lse", ctypes.c_size_t),
-                ("nll", ctypes.c_size_t), ("vocab_chunk", ctypes.c_int64)]
+                ("nll", ctypes.c_size_t), ("vocab_chunk", ctypes.c_int64),
+                ("alpha_ld", ctypes.c_int64)]
 
 
 _lib = None

@@ -216,13 +216,14 @@ static PFN_encodeTiled get_encode() {
 // rank-r tensor map, 128-byte swizzle, zero fill out of bounds.
 static attn_status_t encode(CUtensorMap* m, const void* ptr, bool f32, int rank,
                             const cuuint64_t* dims, const cuuint64_t* strides_bytes,
-                            const cuuint32_t* box) {
+                            const cuuint32_t* box,
+                            CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
                    const_cast<void*>(ptr), dims, strides_bytes, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(ATTN_ERR_CUDA,
@@ -251,6 +252,7 @@ struct GemmDesc {
   int b_nsplit = 0;  // MN-major B: columns >= b_nsplit come from b1
   int b_koff = 0;
   long long out_bstride = 0;   // batch stride of the epilogue output (elements)
+  int bn = 0;        // tile columns (0 = 256); < 256 only for K-major B on single CTAs
   EpiParams epi{};
 };
 
@@ -286,10 +288,14 @@ static attn_status_t operand_map(CUtensorMap* m, const Operand& o, bool mn, int 
 static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr, int tile_begin,
                              int pair) {
   memset(&pr, 0, sizeof(pr));
-  const int tile_m = pair == 1 ? TC_BM : 2 * TC_BM, b_rows = pair == 2 ? TC_BN / 2 : TC_BN;
+  const int bn = g.bn > 0 ? g.bn : TC_BN;
+  if (bn != TC_BN && (bn % 16 != 0 || bn > TC_BN || g.b_mn || g.b_nsplit || pair == 2 || pair == 3))
+    return fail(ATTN_ERR_UNSUPPORTED, "tile width %d needs a K-major B on single CTAs", bn);
+  const int tile_m = pair == 1 ? TC_BM : 2 * TC_BM, b_rows = pair == 2 ? TC_BN / 2 : bn;
   pr.M = g.M; pr.N = g.N; pr.K = g.K; pr.batch = g.batch;
+  pr.bn = bn;
   pr.tiles_m = (g.M + tile_m - 1) / tile_m;
-  pr.tiles_n = (g.N + TC_BN - 1) / TC_BN;
+  pr.tiles_n = (g.N + bn - 1) / bn;
   pr.kseg = g.kseg;
   pr.kb_total = g.kseg > 0 ? g.kseg + (int)((g.a1.k_ext + TC_BK - 1) / TC_BK)
                            : (g.K + TC_BK - 1) / TC_BK;
@@ -339,7 +345,24 @@ static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr
   pr.b_mode = mode0;
   // epilogue output: TMA store / reduce-add boxes of 32 rows x 128 bytes
   const int k = g.epi.kind;
-  if (k != EPI_LSE && k != EPI_NONE && k != EPI_ATTN_SOFTMAX && k != EPI_ATTN_SOFTMAX_BWD) {
+  if (k == EPI_ATTN_SOFTMAX || k == EPI_ATTN_SOFTMAX_BWD) {
+    // bf16 alpha / de [batch][rows, ldo] (box 32 x 32, 64-byte swizzle) and, for
+    // the forward, the fp32 alpha stash [batch][rows, stash_ld] in maps[3]
+    // (box 32 x 32, 128-byte swizzle; B has one segment, so maps[3] is free)
+    cuuint64_t dims[3] = {(cuuint64_t)g.epi.ncols_store, (cuuint64_t)g.M, (cuuint64_t)g.batch};
+    cuuint64_t strides[2] = {(cuuint64_t)(g.epi.ldo * 2), (cuuint64_t)(g.out_bstride * 2)};
+    cuuint32_t box[3] = {32, 32, 1};
+    if ((st = encode(&maps[4], g.epi.out, false, 3, dims, strides, box,
+                     CU_TENSOR_MAP_SWIZZLE_64B)) != ATTN_OK)
+      return st;
+    if (k == EPI_ATTN_SOFTMAX) {
+      if (g.b_seg || g.b_nsplit) return fail(ATTN_ERR_UNSUPPORTED, "softmax epilogue needs one B map");
+      cuuint64_t d2[3] = {(cuuint64_t)g.epi.ncols_valid, (cuuint64_t)g.M, (cuuint64_t)g.batch};
+      cuuint64_t s2[2] = {(cuuint64_t)(g.epi.stash_ld * 4),
+                          (cuuint64_t)(g.epi.stash_ld * 4 * (long long)g.M)};
+      if ((st = encode(&maps[3], g.epi.stash_f32, true, 3, d2, s2, box)) != ATTN_OK) return st;
+    }
+  } else if (k != EPI_LSE && k != EPI_NONE) {
     const bool f32 = epi_out_is_f32(k);
     const int esz = f32 ? 4 : 2;
     const long long bs = g.batch > 1 ? g.out_bstride : (long long)(g.M + 1) * g.epi.ldo;
@@ -536,6 +559,7 @@ struct Plan {
       off_tgtlogit, off_lse, off_nll, off_rowscale, off_dl, off_dhc, off_dz, off_dhc2, off_abf,
       off_debf, off_q, off_dbpart;
   int Mp;             // bf16 path: row stride of the bf16 alpha / de operands (64-multiple)
+  int ald;            // row stride of the fp32 alpha stash (bf16 path: Mp, for TMA stores)
   size_t total;
 };
 
@@ -576,7 +600,9 @@ static Plan make_plan(const attn_shape_t* s) {
   p.off_lens = take(2 * sizeof(int) * p.B);
   p.off_counters = take(sizeof(int) * kNumCounters);
   p.off_blockpart = take(sizeof(double) * ((p.T + 7) / 8 + 1));
-  p.off_alpha = take(sizeof(float) * p.T * p.M);
+  p.Mp = (p.M + 63) / 64 * 64;
+  p.ald = p.bf16 ? p.Mp : p.M;
+  p.off_alpha = take(sizeof(float) * p.T * p.ald);
   p.off_dalpha = take(sizeof(float) * p.T * p.M);
   p.off_ctx = take(p.elt * p.T * p.d);
   p.off_hc = take(p.elt * p.T * p.d);
@@ -589,7 +615,6 @@ static Plan make_plan(const attn_shape_t* s) {
   p.off_dhc = take(sizeof(float) * p.T * p.d);
   p.off_dz = take(p.elt * p.T * p.d);
   p.off_dhc2 = take(sizeof(float) * p.T * 2 * p.d);
-  p.Mp = (p.M + 63) / 64 * 64;
   p.off_abf = take(p.bf16 ? 2 * p.T * p.Mp : 0);
   p.off_debf = take(p.bf16 ? 2 * p.T * p.Mp : 0);
   p.off_q = take(p.elt * p.T * p.d);   // Eq. 2 general score: Q = H W_alpha
@@ -609,6 +634,7 @@ extern "C" attn_status_t attn_softmax_workspace_views(const attn_shape_t* s, att
   if (!out) return fail(ATTN_ERR_INVALID_ARG, "out is NULL");
   Plan p = make_plan(s);
   out->alpha = p.off_alpha;
+  out->alpha_ld = p.ald;
   out->ctx = p.off_ctx;
   out->hc = p.off_hc;
   out->lse = p.off_lse;
@@ -934,7 +960,9 @@ static attn_status_t attention_forward_tc(const Plan& p, const void* H, const vo
     g.batch = B; g.M = N; g.N = M; g.K = d;
     g.a0 = kmaj(Q, N, d, d, (long long)N * d);
     g.b0 = kmaj(S, M, d, d, (long long)M * d);
-    g.epi.kind = EPI_ATTN_SOFTMAX; g.epi.stash_f32 = b.alpha; g.epi.ncols_valid = M;
+    g.bn = (M + 31) / 32 * 32;   // UMMA N = the source positions, not a 256-wide tile
+    g.epi.kind = EPI_ATTN_SOFTMAX; g.epi.stash_f32 = b.alpha; g.epi.stash_ld = p.ald;
+    g.epi.ncols_valid = M; g.out_bstride = (long long)N * Mp;
     g.epi.out = b.abf; g.epi.ldo = Mp; g.epi.ncols_store = Mp; g.epi.src_len = b.src_len;
     attn_status_t st = launch_tc_group<__nv_bfloat16>(&g, 1, next(ctx_), stream);
     if (st != ATTN_OK) return st;
@@ -962,7 +990,9 @@ static attn_status_t attention_backward_tc(const Plan& p, const void* H, const v
     g.batch = B; g.M = N; g.N = M; g.K = d;
     g.a0 = kmaj(b.dcbf, N, d, d, (long long)N * d);
     g.b0 = kmaj(S, M, d, d, (long long)M * d);
-    g.epi.kind = EPI_ATTN_SOFTMAX_BWD; g.epi.stash_f32 = b.alpha; g.epi.ncols_valid = M;
+    g.bn = (M + 31) / 32 * 32;
+    g.epi.kind = EPI_ATTN_SOFTMAX_BWD; g.epi.stash_f32 = b.alpha; g.epi.stash_ld = p.ald;
+    g.epi.ncols_valid = M; g.out_bstride = (long long)N * Mp;
     g.epi.out = b.debf; g.epi.ldo = Mp; g.epi.ncols_store = Mp;
     attn_status_t st = launch_tc_group<__nv_bfloat16>(&g, 1, next(ctx_), stream);
     if (st != ATTN_OK) return st;

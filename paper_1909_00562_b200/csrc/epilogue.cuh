@@ -50,7 +50,8 @@ struct EpiParams {
   const float* rowscale; // DLOGITS: [rows] loss_scale on valid rows, 0 on padded
                          // (tcgen05 DLOGITS also reads tgt_logit: the forward's
                          // target logit, for the -onehot term)
-  float* stash_f32;      // ATTN_SOFTMAX(_BWD): alpha fp32 [rows, ncols_valid]
+  float* stash_f32;      // ATTN_SOFTMAX(_BWD): alpha fp32 [rows, stash_ld] (cols < ncols_valid)
+  long long stash_ld;
   const int* src_len;    // ATTN_SOFTMAX: [batch]
   const float* addend;   // ADD_BF16: [rows, add_ld] fp32
   long long add_ld;

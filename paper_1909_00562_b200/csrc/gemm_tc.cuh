@@ -88,6 +88,7 @@ struct TcProblem {
   int b_seg;        // B switches to map b1 in segment 1 (else continues in b0)
   int b_nsplit;     // B column split between maps b0 / b1 (MN-major B, 0 = none)
   int b_koff;       // added to B's K coordinate (elements)
+  int bn;           // tile columns (UMMA N): 256, or 16..240 for K-major B on single CTAs
   EpiParams epi;
 };
 
@@ -153,7 +154,7 @@ __device__ __forceinline__ TcTile tc_decode(const TcParams& P, int t) {
   const int tm = local % pr.tiles_m;
   r.tn = local / pr.tiles_m;
   r.m0 = tm * TcCfg<kPair>::TILE_M;
-  r.n0 = r.tn * TC_BN;
+  r.n0 = r.tn * pr.bn;
   return r;
 }
 
@@ -196,12 +197,60 @@ __device__ __forceinline__ void tc_load_operand(uint8_t* dst, const CUtensorMap*
 }
 
 // ---------------------------------------------------------------- attention epilogues
+// Stage one 32-row x 32-column chunk of this warp's rows in its shared-memory
+// staging buffer and TMA-store it (the previous store's smem read is waited
+// for first).  fp32: 128-byte rows, 128-byte swizzle; bf16: 64-byte rows,
+// 64-byte swizzle (the tensor map's box is {32, 32}).
+__device__ __forceinline__ void stage_store_f32(uint8_t* stg, const CUtensorMap* m,
+                                                const float (&v)[32], int col, int row0, int b,
+                                                uint32_t lane) {
+  const uint32_t s = smem_u32(stg);
+  if (lane == 0) bulk_wait_read0();
+  __syncwarp();
+#pragma unroll
+  for (int g = 0; g < 8; ++g)
+    st_shared_v4(s + lane * 128 + ((g ^ (lane & 7)) << 4), __float_as_uint(v[4 * g]),
+                 __float_as_uint(v[4 * g + 1]), __float_as_uint(v[4 * g + 2]),
+                 __float_as_uint(v[4 * g + 3]));
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_3d(m, stg, col, row0, b);
+    bulk_commit();
+  }
+}
+__device__ __forceinline__ void stage_store_bf16(uint8_t* stg, const CUtensorMap* m,
+                                                 const float (&v)[32], int col, int row0, int b,
+                                                 uint32_t lane) {
+  const uint32_t s = smem_u32(stg);
+  if (lane == 0) bulk_wait_read0();
+  __syncwarp();
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * g + 2 * e], v[8 * g + 2 * e + 1]);
+      w[e] = *reinterpret_cast<uint32_t*>(&h2);
+    }
+    st_shared_v4(s + lane * 64 + ((g ^ ((lane >> 1) & 3)) << 4), w[0], w[1], w[2], w[3]);
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_3d(m, stg, col, row0, b);
+    bulk_commit();
+  }
+}
+
 // Masked row softmax of the scores tile (Eq. 1): one thread per decoder row,
-// M_src <= 128 columns (column half 0 only).  Writes alpha (fp32 stash, row
-// stride ncols_valid = M) and its bf16 copy (row stride ldo = Mp, the operand
-// of Eq. 3 and of the backward), both exactly 0 for j >= src_len.
-__device__ __forceinline__ void epi_attn_softmax(const EpiParams& e, uint32_t taddr, int n_act,
-                                                 int rowg, bool row_ok, int L) {
+// M_src <= 128 columns (column half 0 only).  alpha (fp32 stash, row stride
+// stash_ld, tensor map `mstash`) and its bf16 copy (row stride ldo = Mp, map
+// `mbf`, the operand of Eq. 3 and of the backward) leave through TMA stores;
+// both are exactly 0 for j >= src_len.
+__device__ __forceinline__ void epi_attn_softmax(uint32_t taddr, int n_act, int L, uint8_t* stg,
+                                                 const CUtensorMap* mstash, const CUtensorMap* mbf,
+                                                 int row0, int b, uint32_t lane) {
   float v[32];
   float mx = -INFINITY;
   for (int c = 0; c < n_act; ++c) {
@@ -215,50 +264,57 @@ __device__ __forceinline__ void epi_attn_softmax(const EpiParams& e, uint32_t ta
     tmem_ld32(taddr + c * 32, v);
 #pragma unroll
     for (int j = 0; j < 32; ++j)
-      if (c * 32 + j < L) s += expf(v[j] - mx);
+      if (c * 32 + j < L) s += __expf(v[j] - mx);
   }
   const float inv = 1.f / s;
-  float* af = e.stash_f32 + (long long)rowg * e.ncols_valid;
-  __nv_bfloat16* ab = reinterpret_cast<__nv_bfloat16*>(e.out) + (long long)rowg * e.ldo;
   for (int c = 0; c < n_act; ++c) {
     tmem_ld32(taddr + c * 32, v);
-    if (!row_ok) continue;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int col = c * 32 + j;
-      const float a = (col < L) ? expf(v[j] - mx) * inv : 0.f;
-      if (col < e.ncols_valid) af[col] = a;
-      if (col < e.ldo) ab[col] = __float2bfloat16_rn(a);
-    }
+    for (int j = 0; j < 32; ++j) v[j] = (c * 32 + j < L) ? __expf(v[j] - mx) * inv : 0.f;
+    stage_store_f32(stg, mstash, v, c * 32, row0, b, lane);
+    stage_store_bf16(stg, mbf, v, c * 32, row0, b, lane);
   }
 }
 
 // Backward of Eq. 1 on the dalpha tile: de = alpha (dalpha - sum_j alpha dalpha),
-// written as bf16 (row stride ldo = Mp), exactly 0 where alpha is.
+// written as bf16 (row stride ldo = Mp, map `mbf`), exactly 0 where alpha is.
 __device__ __forceinline__ void epi_attn_softmax_bwd(const EpiParams& e, uint32_t taddr, int n_act,
-                                                     int rowg, bool row_ok) {
+                                                     int rowg, bool row_ok, uint8_t* stg,
+                                                     const CUtensorMap* mbf, int row0, int b,
+                                                     uint32_t lane) {
   float v[32];
-  const float* af = e.stash_f32 + (long long)rowg * e.ncols_valid;
+  const float* af = e.stash_f32 + (long long)rowg * e.stash_ld;
+  auto load_alpha = [&](int c, float (&a)[32]) {
+    if (row_ok) {
+      const float4* a4 = reinterpret_cast<const float4*>(af + c * 32);
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const float4 x = a4[g];
+        a[4 * g] = x.x; a[4 * g + 1] = x.y; a[4 * g + 2] = x.z; a[4 * g + 3] = x.w;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (c * 32 + j >= e.ncols_valid) a[j] = 0.f;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) a[j] = 0.f;
+    }
+  };
   float D = 0.f;
   for (int c = 0; c < n_act; ++c) {
+    float a[32];
     tmem_ld32(taddr + c * 32, v);
-    if (!row_ok) continue;
+    load_alpha(c, a);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int col = c * 32 + j;
-      if (col < e.ncols_valid) D += af[col] * v[j];
-    }
+    for (int j = 0; j < 32; ++j) D += a[j] * v[j];
   }
-  __nv_bfloat16* db = reinterpret_cast<__nv_bfloat16*>(e.out) + (long long)rowg * e.ldo;
   for (int c = 0; c < n_act; ++c) {
+    float a[32];
     tmem_ld32(taddr + c * 32, v);
-    if (!row_ok) continue;
+    load_alpha(c, a);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int col = c * 32 + j;
-      const float a = (col < e.ncols_valid) ? af[col] : 0.f;
-      if (col < e.ldo) db[col] = __float2bfloat16_rn(a * (v[j] - D));
-    }
+    for (int j = 0; j < 32; ++j) v[j] = a[j] * (v[j] - D);
+    stage_store_bf16(stg, mbf, v, c * 32, row0, b, lane);
   }
 }
 
@@ -419,7 +475,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
               tc_load_operand_mc(sBh, mb, &full[s], pr.b_mode, Cfg::B_ROWS, bn0, kbk, tl.b);
             }
           } else {
-            if (leader) mbar_arrive_expect_tx(&full[s], Cfg::STAGE * Cfg::CLUSTER);
+            if (leader)
+              mbar_arrive_expect_tx(&full[s], (kPair == 1 || kPair == 4)
+                                                  ? Cfg::A_SMEM + pr.bn * TC_BK * 2
+                                                  : Cfg::STAGE * Cfg::CLUSTER);
             const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
             const int ka = (seg1 ? kb - pr.kseg : kb) * TC_BK;
             tc_load_operand<kPair>(sA, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode, TC_BM, am0,
@@ -495,7 +554,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         TC_TRACE(t, 3);
         const TcProblem& pr = P.prob[tl.p];
         TC_TRACE(t, 8);   // decoded
-        const uint32_t idesc = umma_idesc_bf16(Cfg::MMA_M, TC_BN, pr.a_mn, pr.b_mn);
+        const uint32_t idesc = umma_idesc_bf16(Cfg::MMA_M, pr.bn, pr.a_mn, pr.b_mn);
         const uint32_t a_lbo = pr.a_mn ? 8192u : 16u;
         const uint32_t b_lbo = pr.b_mn ? 8192u : 16u;
         const uint32_t a_kstep = pr.a_mn ? 2048u : 32u;
@@ -597,11 +656,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       const int col_h = tl.n0 + h * 128;
       const int lim = (kind == EPI_LSE || kind == EPI_ATTN_SOFTMAX || kind == EPI_ATTN_SOFTMAX_BWD)
                           ? pr.epi.ncols_valid : pr.epi.ncols_store;
-      const int n_act = max(0, min(4, (lim - col_h + 31) / 32));   // warp-uniform
+      const int n_act =
+          max(0, min(4, (min(lim, tl.n0 + pr.bn) - col_h + 31) / 32));   // warp-uniform
       if (kind == EPI_ATTN_SOFTMAX) {
-        if (n_act > 0) epi_attn_softmax(pr.epi, taddr, n_act, rowg, row_ok, pr.epi.src_len[tl.b]);
+        if (n_act > 0)
+          epi_attn_softmax(taddr, n_act, pr.epi.src_len[tl.b], staging + ew * TC_STG_BYTES,
+                           &P.maps[tl.p][3], omap, row0, tl.b, lane);
       } else if (kind == EPI_ATTN_SOFTMAX_BWD) {
-        if (n_act > 0) epi_attn_softmax_bwd(pr.epi, taddr, n_act, rowg, row_ok);
+        if (n_act > 0)
+          epi_attn_softmax_bwd(pr.epi, taddr, n_act, rowg, row_ok, staging + ew * TC_STG_BYTES,
+                               omap, row0, tl.b, lane);
       } else {
         RowEpilogue<OutT, kFast> epi(pr.epi, rowg, 0);
         const bool f32out = epi_out_is_f32(kind);

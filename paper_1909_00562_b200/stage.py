@@ -72,7 +72,8 @@ class AttnSoftmaxStage:
             return ws[off: off + n * esz].view(dt)
 
         return dict(
-            alpha=view(v.alpha, T * self.M, torch.float32).view(self.B, self.N, self.M),
+            alpha=view(v.alpha, T * v.alpha_ld, torch.float32).view(T, v.alpha_ld)[:, :self.M]
+            .reshape(self.B, self.N, self.M),
             C=view(v.ctx, T * self.d, self.tdtype).view(self.B, self.N, self.d),
             Hc=view(v.hc, T * self.d, self.tdtype).view(self.B, self.N, self.d),
             lse=view(v.lse, T, torch.float32),
