@@ -33,7 +33,8 @@ n = int(np.max(np.nonzero(t[:, 4])[0])) + 1
 t = t[:n]
 kinds = sys.argv[3].split(",") if len(sys.argv) > 3 else None
 span = t[:, 5] - t[:, 4]
-print(f"launch {idx}: {n} tiles; kernel span {(t[:,5].max()-t[:,4].min())} cycles (per-SM clocks, rough)")
+gt0, gt1 = t[:, 14][t[:, 14] > 0], t[:, 15][t[:, 15] > 0]
+print(f"launch {idx}: {n} tiles; first MMA -> last commit {(gt1.max() - gt0.min()) / 1e3:.1f} us (globaltimer)")
 # group by span size (problem types have distinct k-block counts)
 buckets = (((0, 30000, "short"), (30000, 90000, "mid"), (90000, 10**9, "long")) if wide else
            ((0, 13000, "short"), (13000, 40000, "mid"), (40000, 10**9, "long")))
