@@ -45,7 +45,7 @@ import numpy as np
 __all__ = [
     "attention_scores", "attention_weights", "context_vectors",
     "context_decoded", "vocab_logits", "log_sum_exp", "token_nll",
-    "forward", "backward", "fwd_bwd",
+    "forward", "backward", "fwd_bwd", "decode_step",
 ]
 
 F64 = np.float64
@@ -250,3 +250,34 @@ def fwd_bwd(H_dec, H_enc, src_len, tgt_len, tgt_ids, W_c, W_out, loss_scale,
     bwd = backward(H_dec, H_enc, src_len, W_c, W_out, loss_scale, fwd, W_alpha,
                    b_out)
     return fwd, bwd
+
+
+# --------------------------------------------------------------------------
+# NEXT-4: forward-only decoding step
+# --------------------------------------------------------------------------
+
+def decode_step(H_dec, H_enc, src_len, W_c, W_out, k, W_alpha=None, b_out=None):
+    """One step of beam-search decoding on the stage (§4.4; the
+    per-step output distribution of Eqs. 1-5): for each of
+    the N live hypotheses of sentence b (rows H_dec[b, i], all attending over
+    the same encoder states H_enc[b]), log P(v) = l_v - logsumexp(l) and its k
+    best tokens, ordered by log-probability descending, ties by the lower
+    token id (SPEC.md:541 determinism).  Returns (ids [B,N,k] int64,
+    logp [B,N,k] fp64, lse [B,N] fp64)."""
+    H = _f64(H_dec)
+    B, N, d = H.shape
+    e, _ = attention_scores(H, H_enc, W_alpha)                  # Eq. 2
+    alpha = attention_weights(e, src_len)                       # Eq. 1
+    C = context_vectors(alpha, H_enc)                           # Eq. 3
+    _, Hc = context_decoded(H, C, W_c)                          # Eq. 4
+    logits = vocab_logits(Hc.reshape(B * N, d), W_out, b_out)   # Eq. 5
+    lse = log_sum_exp(logits)
+    logp = logits - lse[:, None]
+    V = logp.shape[1]
+    ids = np.empty((B * N, k), np.int64)
+    vals = np.empty((B * N, k))
+    for r in range(B * N):
+        order = np.lexsort((np.arange(V), -logp[r]))[:k]     # value desc, id asc
+        ids[r] = order
+        vals[r] = logp[r, order]
+    return ids.reshape(B, N, k), vals.reshape(B, N, k), lse.reshape(B, N)

@@ -451,3 +451,47 @@ def test_bias_shift_invariance_and_zero_sum():
     # and a nonzero bias really changes the result (the term is not dropped)
     f2, _ = O.fwd_bwd(*args)
     assert abs(f2["loss"] - f0["loss"]) > 1e-3
+
+
+# ------------------------------------------------ decoding step (NEXT-4) --
+def test_decode_step_against_torch_log_softmax_and_topk():
+    """decode_step's log-probabilities equal torch.log_softmax of the logits of
+    an independent torch composition, and its top-k equals torch.topk (no
+    ties in random data); with k = V the probabilities sum to 1."""
+    cfg = CONFIGS["small_f32"]
+    inp = make_inputs(cfg, with_bias=True)
+    k = 5
+    ids, logp, lse = O.decode_step(inp["H_dec"], inp["H_enc"], inp["src_len"], inp["W_c"],
+                                   inp["W_out"], k, b_out=inp["b_out"])
+    t = lambda a: torch.tensor(np.asarray(a, np.float64))
+    Hd, He = t(inp["H_dec"]), t(inp["H_enc"])
+    B, N, d = Hd.shape
+    M = He.shape[1]
+    key_ok = torch.arange(M)[None, None, :] < torch.tensor(inp["src_len"])[:, None, None]
+    e = torch.einsum("bid,bjd->bij", Hd, He).masked_fill(~key_ok, float("-inf"))
+    C = torch.einsum("bij,bjd->bid", torch.softmax(e, -1), He)
+    Hc = torch.tanh(torch.cat([Hd, C], -1) @ t(inp["W_c"]).T)
+    lp = torch.log_softmax(F.linear(Hc.reshape(B * N, d), t(inp["W_out"]), t(inp["b_out"])), -1)
+    tv, ti = torch.topk(lp, k, dim=-1)
+    np.testing.assert_array_equal(ids.reshape(-1, k), ti.numpy())
+    np.testing.assert_allclose(logp.reshape(-1, k), tv.numpy(), rtol=1e-12, atol=1e-12)
+    _, lp_all, _ = O.decode_step(inp["H_dec"][:1], inp["H_enc"][:1], inp["src_len"][:1],
+                                 inp["W_c"], inp["W_out"], cfg.V)
+    np.testing.assert_allclose(np.exp(lp_all).sum(-1), 1.0, rtol=1e-12)
+    assert np.all(np.diff(lp_all, axis=-1) <= 0)
+
+
+def test_decode_step_ties_prefer_lower_ids():
+    """Duplicated W_out rows give exactly equal logits: in the full ranking
+    (k = V) the tied tokens appear consecutively, lower id first."""
+    cfg = CONFIGS["tiny"]
+    inp = make_inputs(cfg)
+    W = inp["W_out"].astype(np.float64).copy()
+    W[7] = W[3]
+    W[40] = W[3]
+    ids, logp, _ = O.decode_step(inp["H_dec"], inp["H_enc"], inp["src_len"], inp["W_c"], W, cfg.V)
+    flat, lp = ids.reshape(-1, cfg.V), logp.reshape(-1, cfg.V)
+    for r in range(flat.shape[0]):
+        pos = [int(np.where(flat[r] == v)[0][0]) for v in (3, 7, 40)]
+        assert pos[1] == pos[0] + 1 and pos[2] == pos[1] + 1, pos
+        assert lp[r, pos[0]] == lp[r, pos[2]]
