@@ -231,6 +231,22 @@ def measure_next_rows(binding, st, dv, cfg, scale, comm, stream, dev, pk, tok_lo
     for name, kw in (("general_score", dict(W_alpha=Wa)), ("output_bias", dict(b_out=bo))):
         ms = timed(lambda: st(*args, out=outs, comm=comm, stream=stream, **kw))
         res[name] = {"ms_per_step": ms, "target_tokens_per_s": tok_local * world / (ms / 1e3)}
+    # NEXT-4: one beam-search decoding step, beam 5 on the config's sentences
+    # (rows = B x 5 hypotheses; fused vocab GEMM + online LSE + top-k epilogue)
+    if cfg.dtype == "bf16":
+        from dataclasses import replace
+        from paper_1909_00562_b200.stage import DecodeStep
+        from synthetic import make_inputs as _mk
+        dcfg = replace(cfg, N=5, lengths="full")
+        dinp = _mk(dcfg, with_weights=False)
+        dH = torch.from_numpy(dinp["H_dec"]).to(device=dev, dtype=td)
+        dS = torch.from_numpy(dinp["H_enc"]).to(device=dev, dtype=td)
+        dstep = DecodeStep(cfg.B, 5, cfg.M, cfg.d, cfg.V, 5, device=dev)
+        ms = timed(lambda: dstep(dH, dS, dinp["src_len"], dv["W_c"], dv["W_out"], stream=stream))
+        rows = cfg.B * 5
+        res["decode_step"] = {"beam": 5, "k": 5, "hypotheses": rows, "us_per_step": ms * 1e3,
+                              "hypothesis_steps_per_s": rows / (ms / 1e3),
+                              "vocab_tflops": 2.0 * rows * cfg.d * cfg.V / (ms / 1e3) / 1e12}
     # NEXT-2: Adam over W_out, W_c (and W_alpha, b_out would add d^2 + V)
     n = cfg.V * cfg.d + 2 * cfg.d * cfg.d
     h = binding.adam_params(1)

@@ -212,6 +212,29 @@ attn_status_t attn_comm_init(const uint8_t id[128], int nranks, int rank,
                              int device, attn_comm_t** out);
 attn_status_t attn_comm_destroy(attn_comm_t* c);
 
+/* ---- NEXT-4: forward-only decoding step -----------------------------------
+ * One step of beam-search decoding (section 4.4) on the stage:
+ * shape s holds B sentences with N = live hypotheses per sentence (tgt_len),
+ * M source positions; H_dec [B,N,d] are the hypotheses' decoder top-layer
+ * states, H_enc [B,M,d] the sentences' encoder states (shared by their
+ * hypotheses); Eqs. 1-5 (W_alpha: general score, b_out: F_c bias, both
+ * nullable) give log P(v) = l_v - logsumexp(l) per row.  Outputs, per row
+ * t = b*N + i: topk_ids [T,k] int32 and topk_logp [T,k] fp32, the k best
+ * tokens by log-probability descending (ties: lower id first),
+ * and lse [T] fp32 (nullable).  1 <= k <= 8.  The logits are never stored:
+ * the vocab GEMM epilogue keeps per-tile (max, sumexp) and top-8 lists.
+ * bf16 only (ATTN_ERR_UNSUPPORTED for fp32).  Workspace from
+ * attn_softmax_decode_workspace_size (0 for an invalid / fp32 shape). */
+size_t attn_softmax_decode_workspace_size(const attn_shape_t* s);
+attn_status_t attn_softmax_decode_step(
+    const attn_shape_t* s,
+    const void* H_dec, const void* H_enc,
+    const int32_t* src_lens_host,
+    const void* W_c, const void* W_out, const void* W_alpha, const void* b_out,
+    int k, int32_t* topk_ids, float* topk_logp, float* lse,
+    void* workspace, size_t workspace_bytes,
+    void* stream);
+
 /* ---- NEXT-2: the optimizer step after the gradient exchange --------------
  * Adam (Kingma & Ba 2015, Algorithm 1), the optimizer of the paper
  * (PAPER.md:195 Table 2, :207: beta1 0.9, beta2 0.999, eps 1e-8, lr 1e-3):

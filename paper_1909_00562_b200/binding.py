@@ -33,6 +33,7 @@ EXPORTS = [
     "attn_softmax_set_option", "attn_softmax_stage_count",
     "attn_softmax_stage_time", "attn_softmax_last_launches",
     "attn_adam_step", "attn_adam_shard_len", "attn_adam_step_sharded",
+    "attn_softmax_decode_workspace_size", "attn_softmax_decode_step",
 ]
 
 
@@ -128,6 +129,11 @@ def lib() -> ctypes.CDLL:
     L.attn_softmax_stage_time.restype = ctypes.c_int
     L.attn_softmax_last_launches.argtypes = []
     L.attn_softmax_last_launches.restype = ctypes.c_longlong
+    L.attn_softmax_decode_workspace_size.argtypes = [S]
+    L.attn_softmax_decode_workspace_size.restype = ctypes.c_size_t
+    L.attn_softmax_decode_step.argtypes = [S, _P, _P, i32p, _P, _P, _P, _P, ctypes.c_int, _P, _P,
+                                           _P, _P, ctypes.c_size_t, _P]
+    L.attn_softmax_decode_step.restype = ctypes.c_int
     A = ctypes.POINTER(AdamParams)
     L.attn_adam_step.argtypes = [A, ctypes.c_size_t, _P, _P, _P, _P, _P, _P]
     L.attn_adam_step.restype = ctypes.c_int
@@ -321,3 +327,19 @@ def attn_adam_step_sharded(comm, h: AdamParams, n: int, g, w_shard, m_shard, v_s
     _check(lib().attn_adam_step_sharded(comm, ctypes.byref(h), n, _ptr(g), _ptr(w_shard),
                                         _ptr(m_shard), _ptr(v_shard), _ptr(w_bf16),
                                         _stream(stream)))
+
+
+def attn_softmax_decode_workspace_size(s: AttnShape) -> int:
+    n = lib().attn_softmax_decode_workspace_size(ctypes.byref(s))
+    if n == 0:
+        raise AttnError(7, "decode step: invalid shape or fp32 (bf16 only)")
+    return n
+
+
+def attn_softmax_decode_step(s, H_dec, H_enc, src_lens, W_c, W_out, k, topk_ids, topk_logp,
+                             workspace, lse=None, W_alpha=None, b_out=None, stream=None):
+    src, src_p = _i32(src_lens)
+    _check(lib().attn_softmax_decode_step(
+        ctypes.byref(s), _ptr(H_dec), _ptr(H_enc), src_p, _ptr(W_c), _ptr(W_out), _ptr(W_alpha),
+        _ptr(b_out), int(k), _ptr(topk_ids), _ptr(topk_logp), _ptr(lse), _ptr(workspace),
+        workspace.numel() * workspace.element_size(), _stream(stream)))

@@ -362,7 +362,7 @@ static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr
                           (cuuint64_t)(g.epi.stash_ld * 4 * (long long)g.M)};
       if ((st = encode(&maps[3], g.epi.stash_f32, true, 3, d2, s2, box)) != ATTN_OK) return st;
     }
-  } else if (k != EPI_LSE && k != EPI_NONE) {
+  } else if (k != EPI_LSE && k != EPI_NONE && k != EPI_TOPK) {
     const bool f32 = epi_out_is_f32(k);
     const int esz = f32 ? 4 : 2;
     const long long bs = g.batch > 1 ? g.out_bstride : (long long)(g.M + 1) * g.epi.ldo;
@@ -401,12 +401,12 @@ static int tc_smem_bytes() { return TC_SMEM_BYTES; }
 
 // g_opt_pair: vocab / projection GEMMs on CTA pairs (cta_group::2)
 
-template <typename OutT, int kPair>
+template <typename OutT, int kPair, bool kDecode = false>
 static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, cudaStream_t stream,
                                        int group_bit) {
   static bool attr_set = false;
   if (!attr_set) {
-    CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<OutT, true, kPair>,
+    CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<OutT, true, kPair, kDecode>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes()));
     attr_set = true;
   }
@@ -449,7 +449,7 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<OutT, true, kPair>, P));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<OutT, true, kPair, kDecode>, P));
   ++g_launches;
   return ATTN_OK;
 }
@@ -1402,6 +1402,85 @@ extern "C" attn_status_t attn_softmax_check_ids(const attn_shape_t* s, const int
   CUDA_TRY(cudaStreamSynchronize(stream));
   if (bad) return fail(ATTN_ERR_TOKEN_RANGE, "a valid target id is outside [0, V = %d)", s->vocab);
   return ATTN_OK;
+}
+
+// ------------------------------------------------------------------ decoding step (NEXT-4)
+// Forward-only Eqs. 1-5 for the N live hypotheses of each of B sentences (the
+// rows of one sentence share its encoder states), and per row the lse and the
+// k best tokens of log P: the vocab GEMM's epilogue keeps per-tile (max,
+// sumexp) and top-8 lists (logits are never stored), decode_final_kernel
+// merges them.
+static size_t decode_topk_bytes(const Plan& p) { return align_up(sizeof(float2) * 8 * p.T * p.part_ld); }
+
+extern "C" size_t attn_softmax_decode_workspace_size(const attn_shape_t* s) {
+  if (check_shape(s) != ATTN_OK || s->dtype != ATTN_BF16) return 0;
+  const Plan p = make_plan(s);
+  return p.total + decode_topk_bytes(p);
+}
+
+extern "C" attn_status_t attn_softmax_decode_step(
+    const attn_shape_t* s, const void* H_dec, const void* H_enc, const int32_t* src_lens_host,
+    const void* W_c, const void* W_out, const void* W_alpha, const void* b_out, int k,
+    int32_t* topk_ids, float* topk_logp, float* lse, void* workspace, size_t workspace_bytes,
+    void* stream_) {
+  attn_status_t st = check_shape(s);
+  if (st != ATTN_OK) return st;
+  if (s->dtype != ATTN_BF16)
+    return fail(ATTN_ERR_UNSUPPORTED, "decode step: bf16 only (tcgen05 top-k epilogue)");
+  if (k < 1 || k > 8 || k > s->vocab)
+    return fail(ATTN_ERR_INVALID_ARG, "decode step: k = %d outside [1, min(8, V = %d)]", k, s->vocab);
+  const void* req[] = {H_dec, H_enc, src_lens_host, W_c, W_out, topk_ids, topk_logp, workspace};
+  const char* nm[] = {"H_dec", "H_enc", "src_lens_host", "W_c", "W_out", "topk_ids", "topk_logp",
+                      "workspace"};
+  for (int i = 0; i < 8; ++i)
+    if (!req[i]) return fail(ATTN_ERR_INVALID_ARG, "decode step: %s is NULL", nm[i]);
+  for (int b = 0; b < s->batch; ++b)
+    if (src_lens_host[b] < 1 || src_lens_host[b] > s->src_len)
+      return fail(src_lens_host[b] < 1 ? ATTN_ERR_EMPTY_SOURCE : ATTN_ERR_SHAPE,
+                  "decode step: src_lens_host[%d] = %d outside [1, M = %d]", b, src_lens_host[b],
+                  s->src_len);
+  const void* al[] = {H_dec, H_enc, W_c, W_out, W_alpha, workspace};
+  for (const void* a : al)
+    if (misaligned(a)) return fail(ATTN_ERR_UNSUPPORTED, "decode step: 16-byte aligned pointers needed");
+  const Plan p = make_plan(s);
+  if (workspace_bytes < p.total + decode_topk_bytes(p))
+    return fail(ATTN_ERR_WORKSPACE, "workspace_bytes = %zu < required %zu", workspace_bytes,
+                p.total + decode_topk_bytes(p));
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const Bufs b = carve(p, workspace);
+  float2* topk = (float2*)((char*)workspace + p.total);
+  std::vector<int32_t> lens(2 * p.B, 0);
+  memcpy(lens.data(), src_lens_host, sizeof(int32_t) * p.B);
+  CUDA_TRY(cudaMemcpyAsync(b.src_len, lens.data(), sizeof(int32_t) * 2 * p.B,
+                           cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemsetAsync(b.counters, 0, sizeof(unsigned int) * kNumCounters, stream));
+  g_launches = 0;
+  CounterCtx cctx{&b, 0};
+  // F1, F2 (and F0 for the general score)
+  if ((st = attention_forward_tc(p, H_dec, H_enc, b, stream, next_counter_fn, &cctx, W_alpha)) !=
+      ATTN_OK)
+    return st;
+  // F3 (Eq. 4)
+  {
+    GemmDesc g = g_proj(p, H_dec, b.ctx, W_c, b.hc);
+    if ((st = launch_tc_group<__nv_bfloat16>(&g, 1, next_counter_fn(&cctx), stream, PAIR_FWD)) !=
+        ATTN_OK)
+      return st;
+  }
+  // F4 (Eq. 5) with the top-k epilogue
+  {
+    GemmDesc g = g_vocab_fwd(p, b, W_out, nullptr, b_out);
+    g.epi.kind = EPI_TOPK;
+    g.epi.topk = topk;
+    g.epi.tgt_logit = nullptr;
+    if ((st = launch_tc_group_k<__nv_bfloat16, 1, true>(&g, 1, next_counter_fn(&cctx), stream, 0)) !=
+        ATTN_OK)
+      return st;
+  }
+  st = launch_pdl(decode_final_kernel, dim3((unsigned)((p.T + 1) / 2)), dim3(64), stream,
+                  (const float2*)b.part, (const float2*)topk, p.part_ld, (int)p.T, k, (int*)topk_ids,
+                  topk_logp, lse);
+  return st;
 }
 
 // ------------------------------------------------------------------ debug GEMM

@@ -26,7 +26,9 @@ enum EpiKind : int {
   EPI_STORE_BF16 = 6,         // out = acc (bf16): C, dC, dH_enc
   EPI_ADD_BF16 = 7,           // out = acc + addend (fp32) -> bf16: dH_dec = dH_part + de S
   EPI_ATTN_SOFTMAX = 8,       // masked row softmax of the scores (Eq. 1), tcgen05 path
-  EPI_ATTN_SOFTMAX_BWD = 9    // its backward, tcgen05 path
+  EPI_ATTN_SOFTMAX_BWD = 9,   // its backward, tcgen05 path
+  EPI_TOPK = 11               // decoding step (NEXT-4): LSE partials as EPI_LSE plus the 8 best
+                              // (logit, token) of the row's columns in the tile (tcgen05 path)
 };
 
 // Output element type of each kind (tcgen05 path: bf16 activations).
@@ -55,7 +57,8 @@ struct EpiParams {
   const int* src_len;    // ATTN_SOFTMAX: [batch]
   const float* addend;   // ADD_BF16: [rows, add_ld] fp32
   long long add_ld;
-  const void* bias;      // LSE / DLOGITS: optional F_c bias b_out [V] (OutT), indexed by
+  float2* topk;          // TOPK: [rows, part_ld, 8] (logit, token id bits) per slot
+  const void* bias;      // LSE / DLOGITS / TOPK: optional F_c bias b_out [V] (OutT), indexed by
                          // col_base + column (NEXT-1); NULL on the hot path
 };
 
@@ -135,6 +138,47 @@ __device__ __forceinline__ void add_bias32(const void* bias, int gcol, int nvali
     for (int j = 0; j < 32; ++j)
       if (j < nvalid_rel) v[j] += to_f32(b[j]);
   }
+}
+
+// ---- top-k keys (decoding step, NEXT-4): a (logit, token) pair as one 64-bit
+// key -- order-preserving float bits, then the complemented token -- so
+// "logit descending, token ascending" is an unsigned compare.
+__device__ __forceinline__ unsigned long long tk_key(float x, int id) {
+  const uint32_t u = __float_as_uint(x);
+  const uint32_t hi = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((unsigned long long)hi << 32) | (uint32_t)(0xFFFFFFFFu - (uint32_t)id);
+}
+__device__ __forceinline__ float tk_val(unsigned long long k) {
+  const uint32_t hi = (uint32_t)(k >> 32);
+  return __uint_as_float((hi & 0x80000000u) ? (hi & 0x7FFFFFFFu) : ~hi);
+}
+__device__ __forceinline__ int tk_id(unsigned long long k) {
+  return (int)(0xFFFFFFFFu - (uint32_t)k);
+}
+// compare-exchange: a keeps the larger key
+__device__ __forceinline__ void tk_ce(unsigned long long& a, unsigned long long& b) {
+  const unsigned long long mx = a > b ? a : b, mn = a > b ? b : a;
+  a = mx;
+  b = mn;
+}
+// sort 8 keys descending (Batcher odd-even merge sort, 19 compare-exchanges)
+__device__ __forceinline__ void tk_sort8(unsigned long long* k) {
+  tk_ce(k[0], k[1]); tk_ce(k[2], k[3]); tk_ce(k[4], k[5]); tk_ce(k[6], k[7]);
+  tk_ce(k[0], k[2]); tk_ce(k[1], k[3]); tk_ce(k[4], k[6]); tk_ce(k[5], k[7]);
+  tk_ce(k[1], k[2]); tk_ce(k[5], k[6]);
+  tk_ce(k[0], k[4]); tk_ce(k[1], k[5]); tk_ce(k[2], k[6]); tk_ce(k[3], k[7]);
+  tk_ce(k[2], k[4]); tk_ce(k[3], k[5]);
+  tk_ce(k[1], k[2]); tk_ce(k[3], k[4]); tk_ce(k[5], k[6]);
+}
+// a, b sorted descending -> a = the best 8 of both, sorted descending
+__device__ __forceinline__ void tk_merge8(unsigned long long* a, const unsigned long long* b) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = a[i] > b[7 - i] ? a[i] : b[7 - i];   // bitonic
+#pragma unroll
+  for (int d = 4; d > 0; d >>= 1)
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if ((i & d) == 0) tk_ce(a[i], a[i + d]);
 }
 
 struct LseState {

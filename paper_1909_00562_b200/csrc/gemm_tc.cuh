@@ -318,7 +318,63 @@ __device__ __forceinline__ void epi_attn_softmax_bwd(const EpiParams& e, uint32_
   }
 }
 
-template <typename OutT, bool kFast, int kPair>
+// Decoding step (NEXT-4): one thread per row, the row's <= 128 columns of this
+// tile: running (max, sumexp) as EPI_LSE and the 8 best (logit, token) pairs
+// under the order "logit descending, token ascending".  A (logit, token) pair
+// is one 64-bit key (order-preserving float bits, then the complemented
+// token), so "better" is an unsigned compare.  Each 32-column chunk's best 8
+// come from sorting networks on registers (no divergence, no memory): four
+// sorted groups of 8, then bitonic top-8 merges, then a merge with the
+// running list.
+template <typename OutT>
+__device__ __forceinline__ void epi_topk(const EpiParams& e, uint32_t taddr, int n_act, int col_h,
+                                         int rowg, bool row_ok, int slot) {
+  float mx = -INFINITY, s = 0.f;
+  unsigned long long best[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) best[i] = 0ull;   // below every real key
+  for (int c = 0; c < n_act; ++c) {
+    float v[32];
+    tmem_ld32(taddr + c * 32, v);
+    const int col0 = col_h + c * 32;
+    const int nv = row_ok ? e.ncols_valid - col0 : 0;
+    if (nv <= 0) continue;
+    if (e.bias) add_bias32<OutT>(e.bias, e.col_base + col0, nv, v);
+    float cm = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nv) cm = fmaxf(cm, v[j]);
+    const float nm = fmaxf(mx, cm);
+    float t = s * __expf(mx - nm);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nv) t += __expf(v[j] - nm);
+    s = t;
+    mx = nm;
+    unsigned long long k[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) k[j] = j < nv ? tk_key(v[j], e.col_base + col0 + j) : 0ull;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) tk_sort8(k + 8 * g);
+    tk_merge8(k, k + 8);
+    tk_merge8(k + 16, k + 24);
+    tk_merge8(k, k + 16);
+    tk_merge8(best, k);
+  }
+  if (row_ok) {
+    const long long o = (long long)rowg * e.part_ld + slot;
+    e.part[o] = make_float2(mx, s);
+    float4* out = reinterpret_cast<float4*>(e.topk + o * 8);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const unsigned long long a = best[2 * i], b = best[2 * i + 1];
+      out[i] = make_float4(a ? tk_val(a) : -INFINITY, __int_as_float(a ? tk_id(a) : 0x7fffffff),
+                           b ? tk_val(b) : -INFINITY, __int_as_float(b ? tk_id(b) : 0x7fffffff));
+    }
+  }
+}
+
+template <typename OutT, bool kFast, int kPair, bool kDecode = false>
 __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_constant__ TcParams P) {
   using Cfg = TcCfg<kPair>;
   extern __shared__ uint8_t smem_raw[];
@@ -654,7 +710,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       const int rowg = tl.b * pr.M + (row_ok ? row : 0);   // row of the flattened [batch*M] arrays
       const uint32_t taddr = tmem_base + ((q * 32u) << 16) + (acc + sub) * TC_BN + h * 128;
       const int col_h = tl.n0 + h * 128;
-      const int lim = (kind == EPI_LSE || kind == EPI_ATTN_SOFTMAX || kind == EPI_ATTN_SOFTMAX_BWD)
+      const int lim = (kind == EPI_LSE || kind == EPI_TOPK || kind == EPI_ATTN_SOFTMAX ||
+                       kind == EPI_ATTN_SOFTMAX_BWD)
                           ? pr.epi.ncols_valid : pr.epi.ncols_store;
       const int n_act =
           max(0, min(4, (min(lim, tl.n0 + pr.bn) - col_h + 31) / 32));   // warp-uniform
@@ -666,6 +723,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         if (n_act > 0)
           epi_attn_softmax_bwd(pr.epi, taddr, n_act, rowg, row_ok, staging + ew * TC_STG_BYTES,
                                omap, row0, tl.b, lane);
+      } else if (kDecode && kind == EPI_TOPK) {
+        if constexpr (kDecode)
+          epi_topk<OutT>(pr.epi, taddr, n_act, col_h, rowg, row_ok, tl.tn * 2 + h);
       } else {
         RowEpilogue<OutT, kFast> epi(pr.epi, rowg, 0);
         const bool f32out = epi_out_is_f32(kind);

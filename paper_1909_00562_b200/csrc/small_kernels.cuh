@@ -10,6 +10,8 @@
 //                        token NLL lse_t - l_{t,y_t} on valid rows, the row
 //                        scale of the backward, and the deterministic loss sum.
 //   check_ids_kernel     target-id range check (ATTN_ERR_TOKEN_RANGE)
+//   decode_final_kernel  decoding step (NEXT-4): lse and the k best tokens of
+//                        each row from the vocab GEMM's per-tile partials
 //   colsum_*_kernel      db_out of the F_c bias (NEXT-1): column sums of one
 //                        dlogits V-chunk, two passes in a fixed order
 #pragma once
@@ -206,6 +208,62 @@ __global__ void __launch_bounds__(256) colsum_final_kernel(const float* __restri
   float t = 0.f;
   for (int y = 0; y < splits; ++y) t += part[(long long)y * ncols + c];
   db[c] = t;
+}
+
+// One warp per row (2 per block): lse from the (max, sumexp) partials (as
+// lse_reduce) and the k <= 8 best (logit, token) pairs merged from the
+// per-slot sorted top-8 lists: each lane merges its slots' lists with
+// branch-free bitonic top-8 merges of 64-bit keys (epilogue.cuh tk_*), then a
+// butterfly across the lanes.  The key order is total, so the result is
+// unique.
+__global__ void __launch_bounds__(64) decode_final_kernel(const float2* __restrict__ part,
+                                                          const float2* __restrict__ topk,
+                                                          int part_ld, int T, int k,
+                                                          int* __restrict__ ids,
+                                                          float* __restrict__ logp,
+                                                          float* __restrict__ lse_out) {
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 2 + warp;
+  if (row >= T) return;
+  const float2* pr = part + (long long)row * part_ld;
+  float mx = -INFINITY;
+  for (int j = lane; j < part_ld; j += 32) mx = fmaxf(mx, pr[j].x);
+  mx = warp_max(mx);
+  float s = 0.f;
+  for (int j = lane; j < part_ld; j += 32) {
+    const float2 q = pr[j];
+    if (q.y > 0.f) s += q.y * __expf(q.x - mx);
+  }
+  s = warp_sum(s);
+  const float lse = mx + logf(s);
+  unsigned long long best[8], b2[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) best[i] = 0ull;
+  const float4* tk = reinterpret_cast<const float4*>(topk + (long long)row * part_ld * 8);
+  for (int j = lane; j < part_ld; j += 32) {
+    const float4* l = tk + (long long)j * 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 c = l[i];
+      b2[2 * i] = c.x == -INFINITY ? 0ull : tk_key(c.x, __float_as_int(c.y));
+      b2[2 * i + 1] = c.z == -INFINITY ? 0ull : tk_key(c.z, __float_as_int(c.w));
+    }
+    tk_merge8(best, b2);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) b2[i] = __shfl_xor_sync(0xffffffffu, best[i], o);
+    tk_merge8(best, b2);
+  }
+  if (lane == 0) {
+    for (int i = 0; i < k; ++i) {
+      ids[(long long)row * k + i] = tk_id(best[i]);
+      logp[(long long)row * k + i] = tk_val(best[i]) - lse;
+    }
+    if (lse_out) lse_out[row] = lse;
+  }
 }
 
 __global__ void check_ids_kernel(const int* __restrict__ ids, const int* __restrict__ tgt_len,

@@ -81,6 +81,31 @@ class AttnSoftmaxStage:
             vocab_chunk=int(v.vocab_chunk))
 
 
+class DecodeStep:
+    """Forward-only decoding step of the stage (NEXT-4): B sentences x N live
+    hypotheses -> per hypothesis the k best next tokens and their
+    log-probabilities (bf16 only)."""
+
+    def __init__(self, B: int, N: int, M: int, d: int, V: int, k: int,
+                 device: Optional[torch.device] = None):
+        self.B, self.N, self.M, self.d, self.V, self.k = B, N, M, d, V, k
+        self.device = torch.device(device or "cuda")
+        self.shape = binding.shape(B, N, M, d, V, "bf16")
+        nbytes = binding.attn_softmax_decode_workspace_size(self.shape)
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+
+    def __call__(self, H_dec, H_enc, src_len, W_c, W_out, W_alpha=None, b_out=None, stream=None):
+        T = self.B * self.N
+        ids = torch.empty(T, self.k, dtype=torch.int32, device=self.device)
+        logp = torch.empty(T, self.k, dtype=torch.float32, device=self.device)
+        lse = torch.empty(T, dtype=torch.float32, device=self.device)
+        binding.attn_softmax_decode_step(self.shape, H_dec, H_enc, src_len, W_c, W_out, self.k,
+                                         ids, logp, self.workspace, lse=lse, W_alpha=W_alpha,
+                                         b_out=b_out, stream=stream)
+        return ids.view(self.B, self.N, self.k), logp.view(self.B, self.N, self.k), \
+            lse.view(self.B, self.N)
+
+
 def to_device(inp: dict, dtype: str, device="cuda"):
     """numpy inputs from synthetic.make_inputs -> torch device tensors."""
     td = _TORCH_DTYPE[dtype]
