@@ -59,7 +59,9 @@ long long attn_softmax_last_launches(void);
  *   "vocab_chunk"   V-chunk width of the vocab backward (multiple of 256,
  *                   0 = automatic from the L2 size)
  *   "gemm_ctas"     persistent GEMM grid size (0 = number of SMs)
- *   "stage_events"  1 = record per-step CUDA events (see above)
+ *   "stage_events"  1 = record per-step CUDA events (see above); 2 = only the
+ *                   marks around the vocab GEMMs (vocab_fwd, lse_reduce,
+ *                   vocab_bwd: fewer events between the step's kernels)
  *   "cta_pair"      bitmask of GEMM groups run on CTA pairs (tcgen05
  *                   cta_group::2, 256 x 256 tiles) instead of single CTAs
  *                   (128 x 256): 1 = forward vocab / projection, 2 = vocab

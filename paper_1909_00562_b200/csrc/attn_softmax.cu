@@ -67,6 +67,7 @@ extern "C" const char* attn_version(void) { return "attnsm 0.1 sm_100a"; }
 // can time every step of the path on the launching stream.
 struct Prof {
   bool on = false;
+  bool vocab_only = false;   // option value 2: only the marks around the vocab GEMMs
   bool created = false;
   int n = 0;
   cudaEvent_t ev[32];
@@ -75,8 +76,8 @@ struct Prof {
 static Prof g_prof;
 static long long g_launches = 0;
 
-static void prof_mark(const char* name, cudaStream_t s) {
-  if (!g_prof.on) return;
+static void prof_mark(const char* name, cudaStream_t s, bool vocab_mark = false) {
+  if (!g_prof.on || (g_prof.vocab_only && !vocab_mark)) return;
   if (!g_prof.created) {
     for (int i = 0; i < 32; ++i) cudaEventCreate(&g_prof.ev[i]);
     g_prof.created = true;
@@ -163,6 +164,7 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "stage_events")) {
     g_prof.on = value != 0;
+    g_prof.vocab_only = value == 2;
     return ATTN_OK;
   }
   if (!strcmp(key, "pdl")) {
@@ -1082,13 +1084,13 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
     GemmDesc g = g_proj(p, H, b.ctx, W_c, b.hc);
     if ((st = gemm(&g, 1, PAIR_FWD)) != ATTN_OK) return st;
   }
-  prof_mark("proj_tanh", stream);
+  prof_mark("proj_tanh", stream, true);
   // ---- F4 (Eq. 5): logits discarded, per-tile (max, sumexp) kept
   {
     GemmDesc g = g_vocab_fwd(p, b, W_out, tgt_ids, b_out);
     if ((st = gemm(&g, 1, PAIR_FWD)) != ATTN_OK) return st;
   }
-  prof_mark("vocab_fwd", stream);
+  prof_mark("vocab_fwd", stream, true);
   // ---- Eq. 6: lse, token NLL, row scale, loss
   {
     const int blocks = (int)((TT + 7) / 8);
@@ -1097,7 +1099,7 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
                     loss_scale, b.lse, b.nll, b.rowscale, b.blockpart, b.counters, loss);
     if (st != ATTN_OK) return st;
   }
-  prof_mark("lse_reduce", stream);
+  prof_mark("lse_reduce", stream, true);
   CommRun cr;
   if (comm) {
     if ((st = comm_begin(comm, stream, &cr)) != ATTN_OK) return st;
@@ -1146,7 +1148,7 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
                     dim3(256), stream, (const float*)b.dhc, (const T*)b.hc, (T*)b.dz, n);
     if (st != ATTN_OK) return st;
   }
-  prof_mark("vocab_bwd", stream);
+  prof_mark("vocab_bwd", stream, true);
   // ---- B2: dW_c = dz^T [H | C];  dH_part = dz W_c[:, :d];  dC = dz W_c[:, d:]
   {
     GemmDesc gs[3];

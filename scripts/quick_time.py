@@ -24,7 +24,7 @@ if os.environ.get("ATTN_PDL"):
     binding.attn_softmax_set_option("pdl", int(os.environ["ATTN_PDL"]))
 if os.environ.get("ATTN_CTAS"):
     binding.attn_softmax_set_option("gemm_ctas", int(os.environ["ATTN_CTAS"]))
-binding.attn_softmax_set_option("stage_events", 1)
+binding.attn_softmax_set_option("stage_events", int(os.environ.get("ATTN_EV", "1")))
 st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
 dv = to_device(inp, cfg.dtype)
 scale = 1.0 / global_valid_tokens(cfg, cfg.B)
@@ -45,5 +45,6 @@ ms = ev[0].elapsed_time(ev[1]) / n
 tok = int(inp["tgt_len"].sum())
 flops = tok * (6 * cfg.d * cfg.V + 12 * cfg.d * cfg.d + 12 * cfg.M * cfg.d)
 st(*args, out=out)
-print({k: round(v, 4) for k, v in binding.attn_softmax_stage_times().items()})
+if os.environ.get("ATTN_EV", "1") != "0":
+    print({k: round(v, 4) for k, v in binding.attn_softmax_stage_times().items()})
 print(f"{name}: {ms:.3f} ms/step, {tok/ms*1e3:.0f} tok/s, useful {flops/ms/1e9:.1f} TFLOP/s")
