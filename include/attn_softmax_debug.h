@@ -59,6 +59,10 @@ long long attn_softmax_last_launches(void);
  *   "vocab_chunk"   V-chunk width of the vocab backward (multiple of 256,
  *                   0 = automatic from the L2 size)
  *   "gemm_ctas"     persistent GEMM grid size (0 = number of SMs)
+ *   "comm_max_ctas" CTA cap given to NCCL by attn_comm_init calls made after
+ *                   it (default 8, 0 = NCCL's default); while gradients are
+ *                   being allreduced the stage's persistent GEMMs leave that
+ *                   many SMs free for NCCL's kernels
  *   "stage_events"  1 = record per-step CUDA events (see above); 2 = only the
  *                   marks around the vocab GEMMs (vocab_fwd, lse_reduce,
  *                   vocab_bwd: fewer events between the step's kernels)

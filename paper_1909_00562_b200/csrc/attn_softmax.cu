@@ -167,6 +167,11 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
     g_prof.vocab_only = value == 2;
     return ATTN_OK;
   }
+  if (!strcmp(key, "comm_max_ctas")) {
+    if (value < 0 || value > 64) return fail(ATTN_ERR_INVALID_ARG, "comm_max_ctas must be in [0, 64]");
+    g_comm_max_ctas = (int)value;
+    return ATTN_OK;
+  }
   if (!strcmp(key, "pdl")) {
     g_opt_pdl = value != 0;
     return ATTN_OK;
@@ -405,7 +410,7 @@ static int tc_smem_bytes() { return TC_SMEM_BYTES; }
 
 template <typename OutT, int kPair, bool kDecode = false>
 static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, cudaStream_t stream,
-                                       int group_bit) {
+                                       int group_bit, int ctas = 0) {
   static bool attr_set = false;
   if (!attr_set) {
     CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<OutT, true, kPair, kDecode>,
@@ -428,7 +433,7 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   if (tiles == 0) return ATTN_OK;
   const DevInfo di = dev_info();
   const int csize = TcCfg<kPair>::CLUSTER;
-  int units = (g_opt_gemm_ctas > 0 ? (int)g_opt_gemm_ctas : di.sms) / csize;
+  int units = (ctas > 0 ? ctas : g_opt_gemm_ctas > 0 ? (int)g_opt_gemm_ctas : di.sms) / csize;
   units = std::max(1, std::min(units, tiles));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * csize);
@@ -462,14 +467,14 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
 // this GEMM group (0 = never paired).
 template <typename OutT>
 static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cudaStream_t stream,
-                                     int group_bit = 0) {
+                                     int group_bit = 0, int ctas = 0) {
   if (group_bit && (g_opt_wide & group_bit))
-    return launch_tc_group_k<OutT, 4>(gs, n, counter, stream, group_bit);
+    return launch_tc_group_k<OutT, 4>(gs, n, counter, stream, group_bit, ctas);
   if (group_bit && (g_opt_mcast & group_bit))
-    return launch_tc_group_k<OutT, 3>(gs, n, counter, stream, group_bit);
+    return launch_tc_group_k<OutT, 3>(gs, n, counter, stream, group_bit, ctas);
   if (group_bit && (g_opt_pair & group_bit))
-    return launch_tc_group_k<OutT, 2>(gs, n, counter, stream, group_bit);
-  return launch_tc_group_k<OutT, 1>(gs, n, counter, stream, group_bit);
+    return launch_tc_group_k<OutT, 2>(gs, n, counter, stream, group_bit, ctas);
+  return launch_tc_group_k<OutT, 1>(gs, n, counter, stream, group_bit, ctas);
 }
 
 // Launch a plain kernel, as a programmatic dependent of the previous kernel
@@ -1055,8 +1060,13 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   attn_status_t st;
   const bool tc = p.bf16;
   CounterCtx cctx{&b, 0};
+  // once gradients are being allreduced (after the first dW_out chunk), the
+  // persistent GEMMs leave the SMs NCCL's kernels are capped to
+  int reserve = 0;
   auto gemm = [&](const GemmDesc* gs, int n, int pair_bit) -> attn_status_t {
-    if (tc) return launch_tc_group<__nv_bfloat16>(gs, n, next_counter_fn(&cctx), stream, pair_bit);
+    if (tc)
+      return launch_tc_group<__nv_bfloat16>(gs, n, next_counter_fn(&cctx), stream, pair_bit,
+                                            reserve > 0 ? dev_info().sms - reserve : 0);
     return launch_simt_group(gs, n, stream);
   };
   const int d = p.d;
@@ -1138,6 +1148,7 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
         if ((st = comm_enqueue_allreduce(comm, &cr, stream, dW_out + (size_t)c0 * d,
                                          (size_t)vcc * d)) != ATTN_OK)
           return st;
+        reserve = comm_max_ctas(comm);
       }
     }
   }

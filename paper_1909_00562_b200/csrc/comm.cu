@@ -19,6 +19,32 @@ enum { ncclSuccess_ = 0, ncclInProgress_ = 7 };
 enum { ncclFloat32_ = 7, ncclBfloat16_ = 9 };
 enum { ncclSum_ = 0 };
 
+// ncclConfig_t of NCCL 2.28 (nccl.h ncclConfig_v22800), so the communicator can
+// cap the CTAs NCCL's kernels use (the stage's persistent GEMMs leave that
+// many SMs free while a gradient allreduce is in flight).
+struct NcclConfigV22800 {
+  size_t size;
+  unsigned int magic;
+  unsigned int version;
+  int blocking, cgaClusterSize, minCTAs, maxCTAs;
+  const char* netName;
+  int splitShare, trafficClass;
+  const char* commName;
+  int collnetEnable, CTAPolicy, shrinkShare, nvlsCTAs, nChannelsPerNetPeer, nvlinkCentricSched;
+};
+static NcclConfigV22800 nccl_config(int max_ctas) {
+  const int U = (int)0x80000000;   // NCCL_CONFIG_UNDEF_INT
+  NcclConfigV22800 c;
+  c.size = sizeof(NcclConfigV22800);
+  c.magic = 0xcafebeef;
+  c.version = 22809;
+  c.blocking = U; c.cgaClusterSize = U; c.minCTAs = U; c.maxCTAs = max_ctas > 0 ? max_ctas : U;
+  c.netName = nullptr; c.splitShare = U; c.trafficClass = U; c.commName = nullptr;
+  c.collnetEnable = U; c.CTAPolicy = U; c.shrinkShare = U; c.nvlsCTAs = U;
+  c.nChannelsPerNetPeer = U; c.nvlinkCentricSched = U;
+  return c;
+}
+
 struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
@@ -26,6 +52,8 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*ReduceScatter)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommInitRankConfig)(ncclComm_t*, int, ncclUniqueId, int, void*) = nullptr;
+  ncclResult_t (*GetVersion)(int*) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool ok = false;
   std::string why;
@@ -52,6 +80,8 @@ static NcclApi& nccl() {
     api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
     api.ReduceScatter = (decltype(api.ReduceScatter))dlsym(h, "ncclReduceScatter");
     api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+    api.CommInitRankConfig = (decltype(api.CommInitRankConfig))dlsym(h, "ncclCommInitRankConfig");
+    api.GetVersion = (decltype(api.GetVersion))dlsym(h, "ncclGetVersion");
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
     api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy &&
              api.ReduceScatter && api.AllGather;
@@ -67,7 +97,12 @@ struct attn_comm {
   cudaEvent_t join = nullptr;
   int device = 0;
   int nranks = 1, rank = 0;
+  int max_ctas = 0;   // the CTA cap given to NCCL (0 = NCCL's default)
 };
+
+// "comm_max_ctas" option (attn_softmax.cu): CTA cap for communicators created
+// afterwards (0 = NCCL default); the stage reserves that many SMs.
+int g_comm_max_ctas = 8;
 
 // errors are reported through attn_last_error(); defined in attn_softmax.cu
 attn_status_t attn_set_error(attn_status_t code, const char* msg);
@@ -118,7 +153,16 @@ extern "C" attn_status_t attn_comm_init(const uint8_t id[128], int nranks, int r
   c->rank = rank;
   ncclUniqueId u;
   memcpy(u.internal, id, 128);
-  ncclResult_t r = api.CommInitRank(&c->comm, nranks, u, rank);
+  ncclResult_t r;
+  int ver = 0;
+  if (api.GetVersion) api.GetVersion(&ver);
+  if (g_comm_max_ctas > 0 && api.CommInitRankConfig && ver >= 22800) {
+    NcclConfigV22800 cfg = nccl_config(g_comm_max_ctas);
+    r = api.CommInitRankConfig(&c->comm, nranks, u, rank, &cfg);
+    if (r == ncclSuccess_) c->max_ctas = g_comm_max_ctas;
+  } else {
+    r = api.CommInitRank(&c->comm, nranks, u, rank);
+  }
   if (r != ncclSuccess_) {
     delete c;
     return err(ATTN_ERR_NCCL, "ncclCommInitRank: %s", api.GetErrorString ? api.GetErrorString(r) : "?");
@@ -191,3 +235,6 @@ attn_status_t comm_all_gather_bf16(attn_comm_t* c, void* buf, size_t shard, cuda
   NCCL_OK(nccl().AllGather(b + (size_t)c->rank * shard * 2, b, shard, ncclBfloat16_, c->comm, s));
   return ATTN_OK;
 }
+
+// one rank: the "allreduce" moves nothing, so no SMs are set aside
+int comm_max_ctas(const attn_comm_t* c) { return c && c->nranks > 1 ? c->max_ctas : 0; }

@@ -32,3 +32,7 @@ int comm_nranks(const attn_comm_t* c);
 int comm_rank(const attn_comm_t* c);
 attn_status_t comm_reduce_scatter_f32(attn_comm_t* c, float* buf, size_t shard, cudaStream_t s);
 attn_status_t comm_all_gather_bf16(attn_comm_t* c, void* buf, size_t shard, cudaStream_t s);
+// CTA cap the communicator gave NCCL (0 = NCCL's default); the stage's
+// persistent GEMMs leave that many SMs free while gradients are in flight.
+int comm_max_ctas(const attn_comm_t* c);
+extern int g_comm_max_ctas;
