@@ -231,11 +231,20 @@ struct RowEpilogue {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
         if (j < nv) cm = fmaxf(cm, v[j]);
-      const float nm = fmaxf(st.m, cm);
-      float s = st.s * exp_f<kFast>(st.m - nm);
+      const float nm = fmaxf(st.m, cm);   // finite: the chunk has a finite logit
+      float s;
+      if constexpr (kFast) {   // exp(v - nm) = 2^(v log2 e - nm log2 e): one FFMA + MUFU
+        const float nml = nm * kLog2e;
+        s = st.s * ex2_mufu(fmaf(st.m, kLog2e, -nml));
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < nv) s += exp_f<kFast>(v[j] - nm);
+        for (int j = 0; j < 32; ++j)
+          if (j < nv) s += ex2_mufu(fmaf(v[j], kLog2e, -nml));
+      } else {
+        s = st.s * exp_f<kFast>(st.m - nm);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nv) s += exp_f<kFast>(v[j] - nm);
+      }
       st.s = s;
       st.m = nm;
       const int yl = y - col0;
