@@ -80,6 +80,11 @@ __device__ __forceinline__ float tanh_f(float x) {
     return tanhf(x);
   }
 }
+__device__ __forceinline__ float fmax3_f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
 __device__ __forceinline__ float ex2_mufu(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -228,9 +233,19 @@ struct RowEpilogue {
       if (nv <= 0) return;
       if (p.bias) add_bias32<OutT>(p.bias, p.col_base + col0, nv, v);
       float cm = -INFINITY;
+      if (kFast && nv >= 32) {   // sm_100 three-input max: 16 FMNMX3 for 32 values
+        float a = fmax3_f(v[0], v[1], v[2]), b = fmax3_f(v[3], v[4], v[5]);
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < nv) cm = fmaxf(cm, v[j]);
+        for (int j = 6; j < 30; j += 4) {
+          a = fmax3_f(a, v[j], v[j + 1]);
+          b = fmax3_f(b, v[j + 2], v[j + 3]);
+        }
+        cm = fmax3_f(a, b, fmaxf(v[30], v[31]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nv) cm = fmaxf(cm, v[j]);
+      }
       const float nm = fmaxf(st.m, cm);   // finite: the chunk has a finite logit
       float s;
       if constexpr (kFast) {   // exp(v - nm) = 2^(v log2 e - nm log2 e): one FFMA + MUFU
