@@ -71,6 +71,11 @@ CONFIGS = {
     # tiles per sentence), M not a multiple of 64, V tiny and odd
     "odd": Config("odd", 3, 130, 100, 320, 777, "bf16", 8, "ragged"),
     "odd_f32": Config("odd_f32", 3, 17, 9, 24, 77, "f32", 9, "ragged"),
+    # boundary shapes of the bf16 path: one token of everything (d = one K
+    # block, V below one 256-wide tile), and the largest source length
+    # (M = 128, one attention tile) with full lengths
+    "edge_min": Config("edge_min", 1, 1, 1, 64, 50, "bf16", 10, "full"),
+    "edge_max_src": Config("edge_max_src", 2, 128, 128, 128, 300, "bf16", 11, "full"),
 }
 
 

@@ -106,7 +106,9 @@ def set_modes(binding, mode):
                                           ("small", 0, "w0"), ("medium", 0, "w0"),
                                           ("medium", 0, "default"), ("small", 0, "default"),
                                           ("odd", 0, "p8"), ("odd", 256, "p15"), ("odd", 256, "w15"),
-                                          ("odd_f32", 0, "p8")])
+                                          ("odd_f32", 0, "p8"), ("edge_min", 0, "default"),
+                                          ("edge_min", 0, "p8"), ("edge_max_src", 0, "default"),
+                                          ("edge_max_src", 256, "w0")])
 def test_parity_vs_oracle(cuda_lib, name, vc, mode):
     """mode = GEMM tile modes per group (see set_modes)."""
     from paper_1909_00562_b200 import binding
