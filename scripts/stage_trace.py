@@ -71,3 +71,16 @@ print("  prev commit->id seen %d | ->decoded %d | ->acc free %d | ->full wait %d
       tuple(np.median(pv[:, i]) for i in range(5)))
 print("  producer: prev last load -> next first load %d | next first load -> its first MMA %d" %
       tuple(np.median(pv[:, i]) for i in (5, 6)))
+# launch-level idle from globaltimer stamps (ns): per SM, start delay after the
+# first SM's first MMA and idle after its own last commit until the last one
+ends, starts = [], []
+for sm in np.unique(t[:, 0]):
+    rows = t[(t[:, 0] == sm) & (t[:, 14] > 0)]
+    if len(rows):
+        starts.append(rows[:, 14].min())
+        ends.append(rows[:, 15].max())
+starts, ends = np.array(starts), np.array(ends)
+span = ends.max() - starts.min()
+print("  span %.1f us; mean start delay %.1f us; mean end idle %.1f us (%.1f%% of span)" % (
+    span / 1e3, (starts - starts.min()).mean() / 1e3, (ends.max() - ends).mean() / 1e3,
+    100 * ((ends.max() - ends).mean() + (starts - starts.min()).mean()) / span))
