@@ -159,7 +159,13 @@ extern "C" attn_status_t attn_comm_init(const uint8_t id[128], int nranks, int r
   if (g_comm_max_ctas > 0 && api.CommInitRankConfig && ver >= 22800) {
     NcclConfigV22800 cfg = nccl_config(g_comm_max_ctas);
     r = api.CommInitRankConfig(&c->comm, nranks, u, rank, &cfg);
-    if (r == ncclSuccess_) c->max_ctas = g_comm_max_ctas;
+    if (r == ncclSuccess_) {
+      c->max_ctas = g_comm_max_ctas;
+    } else {
+      // every rank sees the same library and config, so all fall back together
+      c->comm = nullptr;
+      r = api.CommInitRank(&c->comm, nranks, u, rank);
+    }
   } else {
     r = api.CommInitRank(&c->comm, nranks, u, rank);
   }
