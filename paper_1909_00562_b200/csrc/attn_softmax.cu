@@ -241,6 +241,24 @@ static attn_status_t encode(CUtensorMap* m, const void* ptr, bool f32, int rank,
   return ATTN_OK;
 }
 
+// src_len[0..B) then tgt_len[0..B) (zeros when tgt is NULL) into dst[0..2B),
+// as kernel parameters (capturable, no host staging; see lens_kernel).
+static attn_status_t upload_lens(int* dst, const int32_t* src, const int32_t* tgt, int B,
+                                 cudaStream_t stream) {
+  for (int base = 0; base < 2 * B; base += 512) {
+    LensChunk c;
+    c.dst = dst + base;
+    c.n = std::min(512, 2 * B - base);
+    for (int i = 0; i < c.n; ++i) {
+      const int k = base + i;
+      c.vals[i] = k < B ? src[k] : (tgt ? tgt[k - B] : 0);
+    }
+    lens_kernel<<<1, 512, 0, stream>>>(c);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return ATTN_OK;
+}
+
 // ------------------------------------------------------------------ GEMM descriptions
 // C[M,N] = A[M,K] B[N,K]^T per batch item.  A K-major operand is [rows, K]
 // (row stride ld), an MN-major one [K, cols]; batch items are bstride
@@ -1225,11 +1243,7 @@ extern "C" attn_status_t attn_softmax_fwd_bwd_ex(
   const Plan p = make_plan(s);
   const Bufs b = carve(p, workspace);
   // lengths: host -> workspace (the harness's arrays are small and pageable)
-  std::vector<int32_t> lens(2 * p.B);
-  memcpy(lens.data(), src_lens_host, sizeof(int32_t) * p.B);
-  memcpy(lens.data() + p.B, tgt_lens_host, sizeof(int32_t) * p.B);
-  CUDA_TRY(cudaMemcpyAsync(b.src_len, lens.data(), sizeof(int32_t) * 2 * p.B,
-                           cudaMemcpyHostToDevice, stream));
+  if ((st = upload_lens(b.src_len, src_lens_host, tgt_lens_host, p.B, stream)) != ATTN_OK) return st;
   if (p.bf16)
     return run_stage<__nv_bfloat16>(p, (const __nv_bfloat16*)H_dec, (const __nv_bfloat16*)H_enc,
                                     tgt_ids, (const __nv_bfloat16*)W_c,
@@ -1462,10 +1476,7 @@ extern "C" attn_status_t attn_softmax_decode_step(
   cudaStream_t stream = (cudaStream_t)stream_;
   const Bufs b = carve(p, workspace);
   float2* topk = (float2*)((char*)workspace + p.total);
-  std::vector<int32_t> lens(2 * p.B, 0);
-  memcpy(lens.data(), src_lens_host, sizeof(int32_t) * p.B);
-  CUDA_TRY(cudaMemcpyAsync(b.src_len, lens.data(), sizeof(int32_t) * 2 * p.B,
-                           cudaMemcpyHostToDevice, stream));
+  if ((st = upload_lens(b.src_len, src_lens_host, nullptr, p.B, stream)) != ATTN_OK) return st;
   CUDA_TRY(cudaMemsetAsync(b.counters, 0, sizeof(unsigned int) * kNumCounters, stream));
   g_launches = 0;
   CounterCtx cctx{&b, 0};

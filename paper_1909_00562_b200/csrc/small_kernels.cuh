@@ -291,6 +291,18 @@ __global__ void __launch_bounds__(64) decode_final_kernel(const float2* __restri
   }
 }
 
+// Host length arrays reach the device as kernel parameters (by value): no
+// host staging buffer, so the call is CUDA-graph capturable and a captured
+// graph replays with the lengths it was captured with.
+struct LensChunk {
+  int* dst;
+  int n;
+  int vals[512];
+};
+__global__ void __launch_bounds__(512) lens_kernel(const __grid_constant__ LensChunk c) {
+  if ((int)threadIdx.x < c.n) c.dst[threadIdx.x] = c.vals[threadIdx.x];
+}
+
 __global__ void check_ids_kernel(const int* __restrict__ ids, const int* __restrict__ tgt_len,
                                  int T, int N, int V, int* __restrict__ bad) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
