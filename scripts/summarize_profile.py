@@ -33,9 +33,9 @@ for row in r[1:]:
     launch[key][row[ix["Metric Name"]]] = float(row[ix["Metric Value"]].replace(",", ""))
 n = len(order)
 nchunks = n - 9 - 1   # attn(2) proj vocab_fwd lse dlogits0 | chunks | dz proj_bwd attn_bwd(2)
-names = ["attn scores+masked softmax (batched)", "attn context (batched)", "proj_tanh",
+names = ["lengths upload (kernel parameters)", "attn scores+masked softmax (batched)", "attn context (batched)", "proj_tanh",
          "vocab_fwd (LSE epilogue)", "lse_reduce", "dlogits chunk 0 (128x256 tiles)"]
-names += [f"vocab bwd chunk {c} (dW_out+dHc+dlogits c+1, 256x256 tiles)" for c in range(n - 10)]
+names += [f"vocab bwd chunk {c} (dW_out+dHc+dlogits c+1, 256x256 tiles)" for c in range(n - 11)]
 names += ["dz (tanh bwd)", "proj_bwd (dW_c + dH_part + dC)", "attn bwd dA + softmax bwd",
           "attn bwd dH_dec + dH_enc"]
 tot = sum(launch[k]["gpu__time_duration.sum"] for k in order)
@@ -48,12 +48,12 @@ for i, k in enumerate(order):
     m = launch[k]
     t = m["gpu__time_duration.sum"]
     nm = names[i] if i < len(names) else "?"
-    if 5 <= i <= n - 4:
+    if 6 <= i <= n - 4:
         vb += t
     out.append(f"{i},{nm},{m['kernel'].replace(',', ' ')},{t / 1e3:.1f},{100 * t / tot:.1f},"
                f"{m.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed', 0):.2f},"
                f"{m.get('dram__bytes_read.sum', 0) / 1e6:.1f},{m.get('dram__bytes_write.sum', 0) / 1e6:.1f}")
-out.append(f"# total {tot / 1e3:.1f} us; vocab backward (ids 5-{n - 4}, incl. dz) = {100 * vb / tot:.1f}% of the step")
+out.append(f"# total {tot / 1e3:.1f} us; vocab backward (ids 6-{n - 4}, incl. dz) = {100 * vb / tot:.1f}% of the step")
 open(f"{prefix}_launches_paper.csv", "w").write("\n".join(out) + "\n")
 print("\n".join(out))
 
