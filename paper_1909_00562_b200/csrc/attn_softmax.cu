@@ -1440,7 +1440,7 @@ extern "C" attn_status_t attn_softmax_check_ids(const attn_shape_t* s, const int
 // k best tokens of log P: the vocab GEMM's epilogue keeps per-tile (max,
 // sumexp) and top-8 lists (logits are never stored), decode_final_kernel
 // merges them.
-static size_t decode_topk_bytes(const Plan& p) { return align_up(sizeof(float2) * 8 * p.T * p.part_ld); }
+static size_t decode_topk_bytes(const Plan& p) { return align_up(sizeof(uint32_t) * 8 * p.T * p.part_ld); }
 
 extern "C" size_t attn_softmax_decode_workspace_size(const attn_shape_t* s) {
   if (check_shape(s) != ATTN_OK || s->dtype != ATTN_BF16) return 0;
@@ -1478,7 +1478,7 @@ extern "C" attn_status_t attn_softmax_decode_step(
                 p.total + decode_topk_bytes(p));
   cudaStream_t stream = (cudaStream_t)stream_;
   const Bufs b = carve(p, workspace);
-  float2* topk = (float2*)((char*)workspace + p.total);
+  uint32_t* topk = (uint32_t*)((char*)workspace + p.total);
   if ((st = upload_lens(b.src_len, src_lens_host, nullptr, p.B, stream)) != ATTN_OK) return st;
   CUDA_TRY(cudaMemsetAsync(b.counters, 0, sizeof(unsigned int) * kNumCounters, stream));
   g_launches = 0;
@@ -1505,7 +1505,7 @@ extern "C" attn_status_t attn_softmax_decode_step(
       return st;
   }
   st = launch_pdl(decode_final_kernel, dim3((unsigned)((p.T + 1) / 2)), dim3(64), stream,
-                  (const float2*)b.part, (const float2*)topk, p.part_ld, (int)p.T, k, (int*)topk_ids,
+                  (const float2*)b.part, (const uint32_t*)topk, p.part_ld, (int)p.T, k, (int*)topk_ids,
                   topk_logp, lse);
   return st;
 }

@@ -57,7 +57,7 @@ struct EpiParams {
   const int* src_len;    // ATTN_SOFTMAX: [batch]
   const float* addend;   // ADD_BF16: [rows, add_ld] fp32
   long long add_ld;
-  float2* topk;          // TOPK: [rows, part_ld, 8] (logit, token id bits) per slot
+  uint32_t* topk;        // TOPK: [rows, part_ld, 8] 32-bit keys (tk_key32) per slot, best first
   const void* bias;      // LSE / DLOGITS / TOPK: optional F_c bias b_out [V] (OutT), indexed by
                          // col_base + column (NEXT-1); NULL on the hot path
 };
@@ -160,14 +160,33 @@ __device__ __forceinline__ float tk_val(unsigned long long k) {
 __device__ __forceinline__ int tk_id(unsigned long long k) {
   return (int)(0xFFFFFFFFu - (uint32_t)k);
 }
+// Inside one 128-column tile half the per-tile epilogue uses 32-bit keys: the
+// order-preserving float bits with the low 7 mantissa bits replaced by the
+// complemented local column (0..127).  Candidates whose logits agree to 2^-16
+// relative are ordered by column, and the kept value is truncated by at most
+// that much -- far below the bf16 inputs' resolution -- for a compare-exchange
+// of two integer instructions instead of six.
+__device__ __forceinline__ uint32_t tk_key32(float x, int local) {
+  const uint32_t u = __float_as_uint(x);
+  const uint32_t hi = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return (hi & ~0x7Fu) | (uint32_t)(0x7F - local);
+}
+__device__ __forceinline__ float tk32_val(uint32_t k) {
+  const uint32_t hi = k & ~0x7Fu;
+  return __uint_as_float((hi & 0x80000000u) ? (hi & 0x7FFFFFFFu) : ~hi);
+}
+__device__ __forceinline__ int tk32_local(uint32_t k) { return 0x7F - (int)(k & 0x7Fu); }
+
 // compare-exchange: a keeps the larger key
-__device__ __forceinline__ void tk_ce(unsigned long long& a, unsigned long long& b) {
-  const unsigned long long mx = a > b ? a : b, mn = a > b ? b : a;
+template <typename K>
+__device__ __forceinline__ void tk_ce(K& a, K& b) {
+  const K mx = a > b ? a : b, mn = a > b ? b : a;
   a = mx;
   b = mn;
 }
 // sort 8 keys descending (Batcher odd-even merge sort, 19 compare-exchanges)
-__device__ __forceinline__ void tk_sort8(unsigned long long* k) {
+template <typename K>
+__device__ __forceinline__ void tk_sort8(K* k) {
   tk_ce(k[0], k[1]); tk_ce(k[2], k[3]); tk_ce(k[4], k[5]); tk_ce(k[6], k[7]);
   tk_ce(k[0], k[2]); tk_ce(k[1], k[3]); tk_ce(k[4], k[6]); tk_ce(k[5], k[7]);
   tk_ce(k[1], k[2]); tk_ce(k[5], k[6]);
@@ -176,7 +195,8 @@ __device__ __forceinline__ void tk_sort8(unsigned long long* k) {
   tk_ce(k[1], k[2]); tk_ce(k[3], k[4]); tk_ce(k[5], k[6]);
 }
 // a, b sorted descending -> a = the best 8 of both, sorted descending
-__device__ __forceinline__ void tk_merge8(unsigned long long* a, const unsigned long long* b) {
+template <typename K>
+__device__ __forceinline__ void tk_merge8(K* a, const K* b) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) a[i] = a[i] > b[7 - i] ? a[i] : b[7 - i];   // bitonic
 #pragma unroll

@@ -330,9 +330,9 @@ template <typename OutT>
 __device__ __forceinline__ void epi_topk(const EpiParams& e, uint32_t taddr, int n_act, int col_h,
                                          int rowg, bool row_ok, int slot) {
   float mx = -INFINITY, s = 0.f;
-  unsigned long long best[8];
+  uint32_t best[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) best[i] = 0ull;   // below every real key
+  for (int i = 0; i < 8; ++i) best[i] = 0u;   // below every real key
   for (int c = 0; c < n_act; ++c) {
     float v[32];
     tmem_ld32(taddr + c * 32, v);
@@ -345,15 +345,16 @@ __device__ __forceinline__ void epi_topk(const EpiParams& e, uint32_t taddr, int
     for (int j = 0; j < 32; ++j)
       if (j < nv) cm = fmaxf(cm, v[j]);
     const float nm = fmaxf(mx, cm);
-    float t = s * __expf(mx - nm);
+    const float nml = nm * kLog2e;
+    float t = s * ex2_mufu(fmaf(mx, kLog2e, -nml));
 #pragma unroll
     for (int j = 0; j < 32; ++j)
-      if (j < nv) t += __expf(v[j] - nm);
+      if (j < nv) t += ex2_mufu(fmaf(v[j], kLog2e, -nml));
     s = t;
     mx = nm;
-    unsigned long long k[32];
+    uint32_t k[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) k[j] = j < nv ? tk_key(v[j], e.col_base + col0 + j) : 0ull;
+    for (int j = 0; j < 32; ++j) k[j] = j < nv ? tk_key32(v[j], col0 - col_h + j) : 0u;   // local column
 #pragma unroll
     for (int g = 0; g < 4; ++g) tk_sort8(k + 8 * g);
     tk_merge8(k, k + 8);
@@ -364,13 +365,9 @@ __device__ __forceinline__ void epi_topk(const EpiParams& e, uint32_t taddr, int
   if (row_ok) {
     const long long o = (long long)rowg * e.part_ld + slot;
     e.part[o] = make_float2(mx, s);
-    float4* out = reinterpret_cast<float4*>(e.topk + o * 8);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const unsigned long long a = best[2 * i], b = best[2 * i + 1];
-      out[i] = make_float4(a ? tk_val(a) : -INFINITY, __int_as_float(a ? tk_id(a) : 0x7fffffff),
-                           b ? tk_val(b) : -INFINITY, __int_as_float(b ? tk_id(b) : 0x7fffffff));
-    }
+    uint4* out = reinterpret_cast<uint4*>(e.topk + o * 8);
+    out[0] = make_uint4(best[0], best[1], best[2], best[3]);
+    out[1] = make_uint4(best[4], best[5], best[6], best[7]);
   }
 }
 

@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(256) colsum_final_kernel(const float* __restri
 // butterfly across the lanes.  The key order is total, so the result is
 // unique.
 __global__ void __launch_bounds__(64) decode_final_kernel(const float2* __restrict__ part,
-                                                          const float2* __restrict__ topk,
+                                                          const uint32_t* __restrict__ topk,
                                                           int part_ld, int T, int k,
                                                           int* __restrict__ ids,
                                                           float* __restrict__ logp,
@@ -262,18 +262,18 @@ __global__ void __launch_bounds__(64) decode_final_kernel(const float2* __restri
   }
   s = warp_sum(s);
   const float lse = mx + logf(s);
+  // slot j covers columns [128 j, 128 j + 128): its 32-bit keys become
+  // 64-bit (value, token) keys, merged across slots and lanes
   unsigned long long best[8], b2[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) best[i] = 0ull;
-  const float4* tk = reinterpret_cast<const float4*>(topk + (long long)row * part_ld * 8);
+  const uint4* tk = reinterpret_cast<const uint4*>(topk + (long long)row * part_ld * 8);
   for (int j = lane; j < part_ld; j += 32) {
-    const float4* l = tk + (long long)j * 4;
+    const uint4 a = tk[(long long)j * 2], c = tk[(long long)j * 2 + 1];
+    const uint32_t kk[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float4 c = l[i];
-      b2[2 * i] = c.x == -INFINITY ? 0ull : tk_key(c.x, __float_as_int(c.y));
-      b2[2 * i + 1] = c.z == -INFINITY ? 0ull : tk_key(c.z, __float_as_int(c.w));
-    }
+    for (int i = 0; i < 8; ++i)
+      b2[i] = kk[i] ? tk_key(tk32_val(kk[i]), 128 * j + tk32_local(kk[i])) : 0ull;
     tk_merge8(best, b2);
   }
 #pragma unroll
