@@ -116,6 +116,10 @@ static int g_opt_mcast = 0;   // "b_multicast": bitmask of GEMM groups on 2-CTA 
 // "wide_tiles": bitmask of GEMM groups on 256 x 256 single-CTA tiles; default
 // the vocab backward (same-box A/B at C1 / C3 / C4: -6 to -8% per step)
 static int g_opt_wide = PAIR_VBWD;
+// "mixed_tiles": bitmask of GEMM groups run on the mixed kernel (wide tiles,
+// plus 128 x 256 tiles for problems flagged narrow -- the dlogits -- in a
+// variable-stage ring); takes precedence over wide_tiles
+static int g_opt_mixed = 0;
 static long long* g_trace = nullptr;   // "gemm_trace": device pointer of a per-tile trace buffer
 static long long g_trace_launch = -1;  // "gemm_trace_launch": trace only this launch index of a call (-1 = all)
 static int64_t g_opt_vocab_chunk = 0;
@@ -140,6 +144,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "gemm_trace")) {
     g_trace = reinterpret_cast<long long*>(value);
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "mixed_tiles")) {
+    g_opt_mixed = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "wide_tiles")) {
@@ -278,6 +286,7 @@ struct GemmDesc {
   int b_koff = 0;
   long long out_bstride = 0;   // batch stride of the epilogue output (elements)
   int bn = 0;        // tile columns (0 = 256); < 256 only for K-major B on single CTAs
+  int narrow = 0;    // mixed launches (kPair = 5): 128 x 256 tiles for this problem
   EpiParams epi{};
 };
 
@@ -316,9 +325,11 @@ static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr
   const int bn = g.bn > 0 ? g.bn : TC_BN;
   if (bn != TC_BN && (bn % 16 != 0 || bn > TC_BN || g.b_mn || g.b_nsplit || pair == 2 || pair == 3))
     return fail(ATTN_ERR_UNSUPPORTED, "tile width %d needs a K-major B on single CTAs", bn);
-  const int tile_m = pair == 1 ? TC_BM : 2 * TC_BM, b_rows = pair == 2 ? TC_BN / 2 : bn;
+  const bool narrow = pair == 5 && g.narrow;
+  const int tile_m = (pair == 1 || narrow) ? TC_BM : 2 * TC_BM, b_rows = pair == 2 ? TC_BN / 2 : bn;
   pr.M = g.M; pr.N = g.N; pr.K = g.K; pr.batch = g.batch;
   pr.bn = bn;
+  pr.narrow = narrow ? 1 : 0;
   pr.tiles_m = (g.M + tile_m - 1) / tile_m;
   pr.tiles_n = (g.N + bn - 1) / bn;
   pr.kseg = g.kseg;
@@ -440,7 +451,7 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   int tiles = 0;
   for (int i = 0; i < n; ++i) {
     attn_status_t st = fill_tc(gs[i], P.maps[i], P.prob[i], tiles,
-                               kPair == 4 ? 4 : (kPair >= 2 ? 2 : 1));
+                               kPair >= 4 ? kPair : (kPair >= 2 ? 2 : 1));
     if (st != ATTN_OK) return st;
     tiles += P.prob[i].tiles_m * P.prob[i].tiles_n * P.prob[i].batch;
   }
@@ -486,6 +497,8 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
 template <typename OutT>
 static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cudaStream_t stream,
                                      int group_bit = 0, int ctas = 0) {
+  if (group_bit && (g_opt_mixed & group_bit))
+    return launch_tc_group_k<OutT, 5>(gs, n, counter, stream, group_bit, ctas);
   if (group_bit && (g_opt_wide & group_bit))
     return launch_tc_group_k<OutT, 4>(gs, n, counter, stream, group_bit, ctas);
   if (group_bit && (g_opt_mcast & group_bit))
@@ -878,6 +891,7 @@ static GemmDesc g_dlogits(const Plan& p, const Bufs& b, const void* W_out, const
   g.M = (int)p.T; g.N = vcc; g.K = p.d;
   g.a0 = kmaj(b.hc, p.T, p.d, p.d);
   g.b0 = kmaj((const char*)W_out + (size_t)c0 * p.d * p.elt, vcc, p.d, p.d);
+  g.narrow = 1;   // short K: 128 x 256 tiles in a mixed launch
   g.epi.kind = EPI_DLOGITS; g.epi.out = b.dl[c & 1]; g.epi.ldo = p.Vc;
   g.epi.ncols_valid = vcc; g.epi.ncols_store = p.bf16 ? vcc : p.Vc; g.epi.col_base = c0;
   g.epi.lse = b.lse; g.epi.rowscale = b.rowscale; g.epi.tgt = tgt;

@@ -63,16 +63,23 @@ constexpr int kMaxProblems = 4;
 //            128 x 256 tile, at the price of one tile in TMEM at a time (the
 //            epilogue is not overlapped with the next tile's MMAs).  64 KB
 //            stages, 3 of them.
+// kPair = 5 ("mixed"): wide 256 x 256 tiles and, for problems flagged
+//            `narrow`, 128 x 256 tiles in the same launch.  The operand ring
+//            is a byte ring of variable-size stages (64 KB wide, 48 KB narrow:
+//            3 or 4 in flight) with 8 barrier slots, and the two 256-column
+//            TMEM accumulator slots are handed out per 128-row half, so a
+//            narrow tile's epilogue overlaps the next tile's MMAs.
 template <int kPair>
 struct TcCfg {
-  static constexpr bool WIDE = kPair == 4;
+  static constexpr bool WIDE = kPair == 4 || kPair == 5;
+  static constexpr bool VAR = kPair == 5;
   static constexpr int TILE_M = kPair == 1 ? TC_BM : 2 * TC_BM;   // rows per scheduled tile
   static constexpr int MMA_M = kPair == 2 ? 2 * TC_BM : TC_BM;     // UMMA M
   static constexpr int B_ROWS = (kPair == 2 || kPair == 3) ? TC_BN / 2 : TC_BN;   // B rows loaded per CTA
   static constexpr int A_SMEM = (WIDE ? 2 : 1) * TC_A_BYTES;
   static constexpr int B_SMEM = (kPair == 2 ? TC_BN / 2 : TC_BN) * TC_BK * 2;
   static constexpr int STAGE = A_SMEM + B_SMEM;                    // 48 | 32 | 48 | 64 KB
-  static constexpr int STAGES = TC_RING_BYTES / STAGE;             // 4 | 6 | 4 | 3
+  static constexpr int STAGES = VAR ? 8 : TC_RING_BYTES / STAGE;   // 4 | 6 | 4 | 3 | 8 slots
   static constexpr int CLUSTER = (kPair == 2 || kPair == 3) ? 2 : 1;
   static constexpr int ACCS = WIDE ? 1 : 2;                        // tiles resident in TMEM
 };
@@ -89,6 +96,7 @@ struct TcProblem {
   int b_nsplit;     // B column split between maps b0 / b1 (MN-major B, 0 = none)
   int b_koff;       // added to B's K coordinate (elements)
   int bn;           // tile columns (UMMA N): 256, or 16..240 for K-major B on single CTAs
+  int narrow;       // kPair = 5: this problem uses 128 x 256 tiles
   EpiParams epi;
 };
 
@@ -140,6 +148,7 @@ __device__ __forceinline__ int tc_find_problem(const TcParams& P, int t) {
 
 struct TcTile {
   int p, b, m0, n0, tn;
+  int nsub;   // 128-row accumulator halves: 2 for wide tiles, else 1
 };
 
 template <int kPair>
@@ -153,7 +162,8 @@ __device__ __forceinline__ TcTile tc_decode(const TcParams& P, int t) {
   local -= r.b * per_b;
   const int tm = local % pr.tiles_m;
   r.tn = local / pr.tiles_m;
-  r.m0 = tm * TcCfg<kPair>::TILE_M;
+  r.nsub = (TcCfg<kPair>::WIDE && !(TcCfg<kPair>::VAR && pr.narrow)) ? 2 : 1;
+  r.m0 = tm * (TcCfg<kPair>::VAR ? TC_BM * r.nsub : TcCfg<kPair>::TILE_M);
   r.n0 = r.tn * pr.bn;
   return r;
 }
@@ -387,12 +397,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
   uint64_t* sempty = sfull + TC_SCHED;         // [SCHED]
   int* sched_tile = reinterpret_cast<int*>(sempty + TC_SCHED);   // [SCHED]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_tile + TC_SCHED);
+  uint64_t* rec_vs = reinterpret_cast<uint64_t*>(tmem_slot + 2);   // kVar: [8] stage starts
 
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();
   constexpr bool kClu = kPair == 2 || kPair == 3;   // cluster of 2 CTAs
   constexpr bool kWide = Cfg::WIDE;
   constexpr bool kMc = kPair == 3;      // B multicast, per-CTA MMAs
+  constexpr bool kVar = Cfg::VAR;       // variable-size stages, per-half accumulators
+  constexpr uint64_t kRing = TC_RING_BYTES;
   const uint32_t rank = kClu ? cluster_ctarank() : 0;   // 0 = cluster leader
   const bool leader = rank == 0;
 
@@ -479,6 +492,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       return t;
     };
     if (leader) fetch(-1);
+    uint64_t vs_ = 0;      // kVar: virtual byte offset of the next stage
+    long long vi_ = 0;     // kVar: stage counter
+    long long wfree_ = 0;  // kVar: oldest stage not yet known to be consumed
     int t = next_tile(-1);
     TcTile tl{};
     if (t >= 0) tl = tc_decode<kPair>(P, t);
@@ -495,10 +511,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       int t_nxt = -1;
       TcTile tl_nxt{};
       for (int kb = 0; kb < kb_total; ++kb) {
-        mbar_wait(&empty[s], ph ^ 1);
+        uint32_t poff = 0;
+        uint32_t stage_bytes = Cfg::STAGE;
+        if constexpr (kVar) {
+          // variable-size stages in a byte ring: a stage never wraps; before
+          // writing, every older stage whose bytes (or barrier slot) it reuses
+          // must have been consumed by the MMA warp
+          stage_bytes = tl.nsub == 2 ? Cfg::STAGE : TC_A_BYTES + Cfg::B_SMEM;
+          uint64_t po = vs_ % kRing;
+          if (po + stage_bytes > kRing) { vs_ += kRing - po; po = 0; }
+          const uint64_t ve = vs_ + stage_bytes;
+          while (wfree_ < vi_ && (wfree_ + 8 <= vi_ || rec_vs[wfree_ & 7] + kRing < ve)) {
+            mbar_wait(&empty[wfree_ & 7], (uint32_t)((wfree_ >> 3) & 1));
+            ++wfree_;
+          }
+          if (lane == 0) rec_vs[vi_ & 7] = vs_;
+          __syncwarp();
+          poff = (uint32_t)po;
+          s = (int)(vi_ & 7);
+        } else {
+          mbar_wait(&empty[s], ph ^ 1);
+        }
         if (elect_one()) {
-          uint8_t* sA = smem + s * Cfg::STAGE;
-          uint8_t* sB = sA + Cfg::A_SMEM;
+          uint8_t* sA = smem + (kVar ? poff : s * Cfg::STAGE);
+          uint8_t* sB = sA + (kVar ? (tl.nsub == 2 ? Cfg::A_SMEM : TC_A_BYTES) : Cfg::A_SMEM);
           uint32_t barc = 0;
           if constexpr (kPair == 2) barc = leader_addr(&full[s]);
           if constexpr (kMc) {
@@ -529,14 +565,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
             }
           } else {
             if (leader)
-              mbar_arrive_expect_tx(&full[s], (kPair == 1 || kPair == 4)
+              mbar_arrive_expect_tx(&full[s], kVar ? stage_bytes
+                                              : (kPair == 1 || kPair == 4)
                                                   ? Cfg::A_SMEM + pr.bn * TC_BK * 2
                                                   : Cfg::STAGE * Cfg::CLUSTER);
             const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
             const int ka = (seg1 ? kb - pr.kseg : kb) * TC_BK;
             tc_load_operand<kPair>(sA, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode, TC_BM, am0,
                                    ka, tl.b);
-            if constexpr (kWide)   // the second 128-row half of A
+            if (kWide && tl.nsub == 2)   // the second 128-row half of A
               tc_load_operand<kPair>(sA + TC_A_BYTES, seg1 ? ma1 : ma0, &full[s], barc, pr.a_mode,
                                      TC_BM, am0 + TC_BM, ka, tl.b);
             const bool bseg1 = seg1 && pr.b_seg;
@@ -564,7 +601,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         __syncwarp();
         if (leader && kb == 0) TC_TRACE(t, 11);             // first load issued
         if (leader && kb == kb_total - 1) TC_TRACE(t, 2);   // last load issued
-        if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
+        if constexpr (kVar) {
+          vs_ += stage_bytes;
+          ++vi_;
+        } else {
+          if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
+        }
         if (kb == 0) {
           // the next tile: fetch, publish and decode in the shadow of this one
           t_nxt = next_tile(t);
@@ -587,6 +629,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       uint32_t rph = 0;
       int acc = 0;
       uint32_t aph = 0;
+      uint64_t mvs = 0;     // kVar: the producer's stage sequence, replayed
+      long long mvi = 0;
+      uint32_t sph = 0;     // kVar: phase bit of each TMEM accumulator slot
       auto read_tile = [&]() -> int {
         if (kClu && !leader) mbar_wait_cluster(&sfull[r], rph);
         else mbar_wait(&sfull[r], rph);
@@ -616,26 +661,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         const int kb_read = kb_total > 1 ? 1 : 0;
         int t_nxt = -1;
         TcTile tl_nxt{};
-        mbar_wait(&tempty[acc], aph ^ 1);
+        const int nsub = tl.nsub;
+        const int acc2 = acc ^ 1;
+        if constexpr (kVar) {   // one or two 256-column slots, each with its own phase
+          mbar_wait(&tempty[acc], ((sph >> acc) & 1) ^ 1);
+          if (nsub == 2) mbar_wait(&tempty[acc2], ((sph >> acc2) & 1) ^ 1);
+        } else {
+          mbar_wait(&tempty[acc], aph ^ 1);
+        }
         tc_fence_after();
         TC_TRACE(t, 9);   // accumulator free
         const uint32_t dcol = tmem_base + acc * TC_BN;
+        const uint32_t dcol2 = kVar ? tmem_base + acc2 * TC_BN : dcol + TC_BN;
         for (int kb = 0; kb < kb_total; ++kb) {
           if (kb == 0) TC_TRACE(t, 10);
-          mbar_wait(&full[s], ph);
+          uint32_t poff = 0, stage_bytes = Cfg::STAGE;
+          if constexpr (kVar) {
+            stage_bytes = nsub == 2 ? Cfg::STAGE : TC_A_BYTES + Cfg::B_SMEM;
+            uint64_t po = mvs % kRing;
+            if (po + stage_bytes > kRing) { mvs += kRing - po; po = 0; }
+            poff = (uint32_t)po;
+            s = (int)(mvi & 7);
+            mbar_wait(&full[s], (uint32_t)((mvi >> 3) & 1));
+          } else {
+            mbar_wait(&full[s], ph);
+          }
           tc_fence_after();
           if (elect_one()) {
-            const uint32_t sA = smem_u32(smem + s * Cfg::STAGE);
-            const uint32_t sB = sA + Cfg::A_SMEM;
+            const uint32_t sA = smem_u32(smem + (kVar ? poff : s * Cfg::STAGE));
+            const uint32_t sB = sA + (kVar ? (nsub == 2 ? Cfg::A_SMEM : TC_A_BYTES) : Cfg::A_SMEM);
 #pragma unroll
             for (int k = 0; k < TC_BK / 16; ++k) {
               const uint64_t ad = umma_sdesc(sA + k * a_kstep, a_lbo, 1024);
               const uint64_t bd = umma_sdesc(sB + k * b_kstep, b_lbo, 1024);
               if constexpr (kPair == 2) umma_bf16_pair(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
               else umma_bf16(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
-              if constexpr (kWide) {   // rows 128..255 into TMEM columns 256..511
+              if (kWide && nsub == 2) {   // rows 128..255 into the second accumulator
                 const uint64_t ad2 = umma_sdesc(sA + TC_A_BYTES + k * a_kstep, a_lbo, 1024);
-                umma_bf16(dcol + TC_BN, ad2, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                umma_bf16(dcol2, ad2, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
               }
             }
             if constexpr (kPair == 2) umma_commit_pair(&empty[s]);
@@ -648,7 +711,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
             const long long gt = gtime();
             if (lane == 2) P.trace[(long long)t * 16 + 14] = gt;
           }
-          if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
+          if constexpr (kVar) {
+            mvs += stage_bytes;
+            ++mvi;
+          } else {
+            if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
+          }
           if (kb == kb_read) {
             t_nxt = read_tile();
             if (t_nxt >= 0) tl_nxt = tc_decode<kPair>(P, t_nxt);
@@ -657,6 +725,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         if (elect_one()) {
           if constexpr (kPair == 2) umma_commit_pair(&tfull[acc]);
           else umma_commit(&tfull[acc]);
+          if (kVar && nsub == 2) umma_commit(&tfull[acc2]);
         }
         __syncwarp();
         TC_TRACE(t, 5);   // last commit issued
@@ -664,7 +733,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           const long long gt = gtime();
           if (lane == 2) P.trace[(long long)t * 16 + 15] = gt;
         }
-        if (++acc == Cfg::ACCS) { acc = 0; aph ^= 1; }
+        if constexpr (kVar) {
+          sph ^= 1u << acc;
+          if (nsub == 2) sph ^= 1u << acc2;
+          else acc = acc2;
+        } else {
+          if (++acc == Cfg::ACCS) { acc = 0; aph ^= 1; }
+        }
         t = t_nxt;
         tl = tl_nxt;
       }
@@ -680,6 +755,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     uint32_t rph = 0;
     int acc = 0;
     uint32_t aph = 0;
+    uint32_t esph = 0;   // kVar: phase bit of each TMEM accumulator slot
     for (;;) {
       if (kClu && !leader) mbar_wait_cluster(&sfull[r], rph);
       else mbar_wait(&sfull[r], rph);
@@ -695,17 +771,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       const TcProblem& pr = P.prob[tl.p];
       const int kind = pr.epi.kind;
       const CUtensorMap* omap = &P.maps[tl.p][4];
-      mbar_wait(&tfull[acc], aph);
-      tc_fence_after();
+      if constexpr (!kVar) {
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+      }
       if (warp == 0 && leader) TC_TRACE(t, 6);
       // wide tiles: two 128-row halves, the second in TMEM columns 256..511
+      // (kVar: each half in its own accumulator slot, released when drained)
 #pragma unroll 1
-      for (int sub = 0; sub < (kWide ? 2 : 1); ++sub) {
+      for (int sub = 0; sub < (kVar ? tl.nsub : (kWide ? 2 : 1)); ++sub) {
+      if constexpr (kVar) {
+        mbar_wait(&tfull[acc], (esph >> acc) & 1);
+        tc_fence_after();
+      }
       const int row0 = tl.m0 + TC_BM * rank + sub * TC_BM + q * 32;   // row inside the batch item
       const int row = row0 + lane;
       const bool row_ok = row < pr.M;
       const int rowg = tl.b * pr.M + (row_ok ? row : 0);   // row of the flattened [batch*M] arrays
-      const uint32_t taddr = tmem_base + ((q * 32u) << 16) + (acc + sub) * TC_BN + h * 128;
+      const uint32_t taddr =
+          tmem_base + ((q * 32u) << 16) + (kVar ? acc : acc + sub) * TC_BN + h * 128;
       const int col_h = tl.n0 + h * 128;
       const int lim = (kind == EPI_LSE || kind == EPI_TOPK || kind == EPI_ATTN_SOFTMAX ||
                        kind == EPI_ATTN_SOFTMAX_BWD)
@@ -802,15 +886,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         }
         if (kind == EPI_LSE && row_ok) epi.finish(tl.tn * 2 + h);
       }
+      if constexpr (kVar) {   // this half's slot is free for the next tile's MMAs
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        esph ^= 1u << acc;
+        acc ^= 1;
       }
-      tc_fence_before();
-      __syncwarp();
+      }
+      if constexpr (!kVar) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (kPair == 2 && !leader) mbar_arrive_cluster(leader_addr(&tempty[acc]));
+          else mbar_arrive(&tempty[acc]);
+        }
+        if (++acc == Cfg::ACCS) { acc = 0; aph ^= 1; }
+      }
       if (warp == 0 && leader) TC_TRACE(t, 7);
-      if (lane == 0) {
-        if (kPair == 2 && !leader) mbar_arrive_cluster(leader_addr(&tempty[acc]));
-        else mbar_arrive(&tempty[acc]);
-      }
-      if (++acc == Cfg::ACCS) { acc = 0; aph ^= 1; }
     }
     if (lane == 0) bulk_wait0();
   }

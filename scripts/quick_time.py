@@ -20,6 +20,8 @@ if os.environ.get("ATTN_MCAST"):
     binding.attn_softmax_set_option("b_multicast", int(os.environ["ATTN_MCAST"]))
 if os.environ.get("ATTN_WIDE"):
     binding.attn_softmax_set_option("wide_tiles", int(os.environ["ATTN_WIDE"]))
+if os.environ.get("ATTN_MIXED"):
+    binding.attn_softmax_set_option("mixed_tiles", int(os.environ["ATTN_MIXED"]))
 if os.environ.get("ATTN_PDL"):
     binding.attn_softmax_set_option("pdl", int(os.environ["ATTN_PDL"]))
 if os.environ.get("ATTN_CTAS"):

@@ -13,6 +13,7 @@ if len(sys.argv) > 2:
     binding.attn_softmax_set_option("cta_pair", int(sys.argv[2]))
 wide = int(os.environ.get("ATTN_WIDE", "0"))
 binding.attn_softmax_set_option("wide_tiles", wide)
+binding.attn_softmax_set_option("mixed_tiles", int(os.environ.get("ATTN_MIXED", "0")))
 cfg = CONFIGS["paper"]
 inp = make_inputs(cfg)
 st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)

@@ -85,15 +85,17 @@ def set_modes(binding, mode):
     projection backward, 8 debug entry): "pN" CTA pairs, "mN" B-multicast
     clusters, "wN" wide single-CTA tiles (the other groups on 128x256
     single-CTA tiles), "default" the library default (wide vocab backward)."""
-    pair, mcast, wide = 8, 0, 2
+    pair, mcast, wide, mixed = 8, 0, 2, 0
     if mode != "default":
         mask = int(mode[1:])
         pair = mask if mode[0] == "p" else 0
         mcast = mask if mode[0] == "m" else 0
         wide = mask if mode[0] == "w" else 0
+        mixed = mask if mode[0] == "x" else 0
     binding.attn_softmax_set_option("cta_pair", pair)
     binding.attn_softmax_set_option("b_multicast", mcast)
     binding.attn_softmax_set_option("wide_tiles", wide)
+    binding.attn_softmax_set_option("mixed_tiles", mixed)
 
 
 @pytest.mark.parametrize("name,vc,mode", [("tiny", 0, "p8"), ("tiny_ragged", 0, "p8"),
@@ -108,7 +110,10 @@ def set_modes(binding, mode):
                                           ("odd", 0, "p8"), ("odd", 256, "p15"), ("odd", 256, "w15"),
                                           ("odd_f32", 0, "p8"), ("edge_min", 0, "default"),
                                           ("edge_min", 0, "p8"), ("edge_max_src", 0, "default"),
-                                          ("edge_max_src", 256, "w0")])
+                                          ("edge_max_src", 256, "w0"),
+                                          ("small", 0, "x2"), ("small", 1024, "x2"),
+                                          ("medium", 2048, "x2"), ("medium", 1024, "x15"),
+                                          ("odd", 256, "x2"), ("odd", 0, "x15")])
 def test_parity_vs_oracle(cuda_lib, name, vc, mode):
     """mode = GEMM tile modes per group (see set_modes)."""
     from paper_1909_00562_b200 import binding
