@@ -79,6 +79,14 @@ long long attn_softmax_last_launches(void);
  *   "b_multicast"   bitmask (same bits as cta_pair) of GEMM groups run on
  *                   2-CTA clusters that share the B tile by TMA multicast
  *                   (two 128 x 256 tiles, per-CTA MMAs); wins over cta_pair
+ *   "mixed_tiles"   bitmask (same bits as cta_pair) of GEMM groups run on a
+ *                   kernel mixing wide tiles with 128 x 256 tiles for the
+ *                   short-K dlogits (variable-size operand stages); wins
+ *                   over wide_tiles.  Default 0.
+ *   "wide_multicast" bitmask (same bits as cta_pair) of GEMM groups run on
+ *                   2-CTA clusters of wide 256 x 256 tiles sharing the B tile
+ *                   by TMA multicast (512 rows per cluster); wins over
+ *                   wide_tiles.  Default 0.
  *   "gemm_trace"    device address of an int64 buffer (16 per tile) that the
  *                   next tcgen05 launches fill with per-tile clock64 stamps
  *                   (0 = off; debug only)

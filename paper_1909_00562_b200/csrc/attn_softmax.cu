@@ -120,6 +120,9 @@ static int g_opt_wide = PAIR_VBWD;
 // plus 128 x 256 tiles for problems flagged narrow -- the dlogits -- in a
 // variable-stage ring); takes precedence over wide_tiles
 static int g_opt_mixed = 0;
+// "wide_multicast": bitmask of GEMM groups on 2-CTA clusters of wide tiles
+// sharing B (kPair 6); takes precedence over wide_tiles
+static int g_opt_widemc = 0;
 static long long* g_trace = nullptr;   // "gemm_trace": device pointer of a per-tile trace buffer
 static long long g_trace_launch = -1;  // "gemm_trace_launch": trace only this launch index of a call (-1 = all)
 static int64_t g_opt_vocab_chunk = 0;
@@ -148,6 +151,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "mixed_tiles")) {
     g_opt_mixed = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "wide_multicast")) {
+    g_opt_widemc = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "wide_tiles")) {
@@ -317,16 +324,18 @@ static attn_status_t operand_map(CUtensorMap* m, const Operand& o, bool mn, int 
   return encode(m, o.p, false, 3, dims, st, box);
 }
 
-// pair: 1 = 128 x 256 tiles, 2 = CTA pair (256 rows, B split), 4 = wide
+// pair: 1 = 128 x 256 tiles, 2 = CTA pair (256 rows, B split), 6 = wide
+// multicast (2 CTAs x 256 rows, B split and multicast), 4 = wide
 // single CTA (256 rows, whole B tile)
 static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr, int tile_begin,
                              int pair) {
   memset(&pr, 0, sizeof(pr));
   const int bn = g.bn > 0 ? g.bn : TC_BN;
-  if (bn != TC_BN && (bn % 16 != 0 || bn > TC_BN || g.b_mn || g.b_nsplit || pair == 2 || pair == 3))
+  if (bn != TC_BN && (bn % 16 != 0 || bn > TC_BN || g.b_mn || g.b_nsplit || pair == 2 || pair == 3 || pair == 6))
     return fail(ATTN_ERR_UNSUPPORTED, "tile width %d needs a K-major B on single CTAs", bn);
   const bool narrow = pair == 5 && g.narrow;
-  const int tile_m = (pair == 1 || narrow) ? TC_BM : 2 * TC_BM, b_rows = pair == 2 ? TC_BN / 2 : bn;
+  const int tile_m = (pair == 1 || narrow) ? TC_BM : pair == 6 ? 4 * TC_BM : 2 * TC_BM;
+  const int b_rows = (pair == 2 || pair == 6) ? TC_BN / 2 : bn;
   pr.M = g.M; pr.N = g.N; pr.K = g.K; pr.batch = g.batch;
   pr.bn = bn;
   pr.narrow = narrow ? 1 : 0;
@@ -499,6 +508,8 @@ static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cu
                                      int group_bit = 0, int ctas = 0) {
   if (group_bit && (g_opt_mixed & group_bit))
     return launch_tc_group_k<OutT, 5>(gs, n, counter, stream, group_bit, ctas);
+  if (group_bit && (g_opt_widemc & group_bit))
+    return launch_tc_group_k<OutT, 6>(gs, n, counter, stream, group_bit, ctas);
   if (group_bit && (g_opt_wide & group_bit))
     return launch_tc_group_k<OutT, 4>(gs, n, counter, stream, group_bit, ctas);
   if (group_bit && (g_opt_mcast & group_bit))

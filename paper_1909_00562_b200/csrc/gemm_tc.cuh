@@ -69,18 +69,24 @@ constexpr int kMaxProblems = 4;
 //            3 or 4 in flight) with 8 barrier slots, and the two 256-column
 //            TMEM accumulator slots are handed out per 128-row half, so a
 //            narrow tile's epilogue overlaps the next tile's MMAs.
+// kPair = 6 ("wide multicast"): a cluster of 2 CTAs computes two vertically
+//            adjacent 256 x 256 wide tiles that share the B tile (kPair 3's
+//            multicast on kPair 4's tiles): each CTA loads its 256 A rows and
+//            half of B, multicast into both; L2 -> SM operand bytes per FLOP
+//            drop by a quarter against kPair 4 (48 of 64 KB per stage).
 template <int kPair>
 struct TcCfg {
-  static constexpr bool WIDE = kPair == 4 || kPair == 5;
+  static constexpr bool WIDE = kPair == 4 || kPair == 5 || kPair == 6;
   static constexpr bool VAR = kPair == 5;
-  static constexpr int TILE_M = kPair == 1 ? TC_BM : 2 * TC_BM;   // rows per scheduled tile
+  static constexpr int TILE_M = kPair == 1 ? TC_BM : kPair == 6 ? 4 * TC_BM : 2 * TC_BM;   // rows per scheduled tile
   static constexpr int MMA_M = kPair == 2 ? 2 * TC_BM : TC_BM;     // UMMA M
-  static constexpr int B_ROWS = (kPair == 2 || kPair == 3) ? TC_BN / 2 : TC_BN;   // B rows loaded per CTA
+  static constexpr int B_ROWS = (kPair == 2 || kPair == 3 || kPair == 6) ? TC_BN / 2 : TC_BN;   // B rows loaded per CTA
   static constexpr int A_SMEM = (WIDE ? 2 : 1) * TC_A_BYTES;
   static constexpr int B_SMEM = (kPair == 2 ? TC_BN / 2 : TC_BN) * TC_BK * 2;
-  static constexpr int STAGE = A_SMEM + B_SMEM;                    // 48 | 32 | 48 | 64 KB
+  static constexpr int STAGE = A_SMEM + B_SMEM;                    // 48 | 32 | 48 | 64 | - | 64 KB
+  static constexpr int CTA_ROWS = WIDE ? 2 * TC_BM : TC_BM;        // A rows per CTA of a cluster
   static constexpr int STAGES = VAR ? 8 : TC_RING_BYTES / STAGE;   // 4 | 6 | 4 | 3 | 8 slots
-  static constexpr int CLUSTER = (kPair == 2 || kPair == 3) ? 2 : 1;
+  static constexpr int CLUSTER = (kPair == 2 || kPair == 3 || kPair == 6) ? 2 : 1;
   static constexpr int ACCS = WIDE ? 1 : 2;                        // tiles resident in TMEM
 };
 
@@ -401,9 +407,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
 
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();
-  constexpr bool kClu = kPair == 2 || kPair == 3;   // cluster of 2 CTAs
+  constexpr bool kClu = Cfg::CLUSTER == 2;   // cluster of 2 CTAs
   constexpr bool kWide = Cfg::WIDE;
-  constexpr bool kMc = kPair == 3;      // B multicast, per-CTA MMAs
+  constexpr bool kMc = kPair == 3 || kPair == 6;   // B multicast, per-CTA MMAs
   constexpr bool kVar = Cfg::VAR;       // variable-size stages, per-half accumulators
   constexpr uint64_t kRing = TC_RING_BYTES;
   const uint32_t rank = kClu ? cluster_ctarank() : 0;   // 0 = cluster leader
@@ -505,7 +511,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       const CUtensorMap* ma1 = &P.maps[tl.p][1];
       const CUtensorMap* mb0 = &P.maps[tl.p][2];
       const CUtensorMap* mb1 = &P.maps[tl.p][3];
-      const int am0 = tl.m0 + TC_BM * rank;               // this CTA's A rows
+      const int am0 = tl.m0 + Cfg::CTA_ROWS * rank;       // this CTA's A rows
       const int bn0 = tl.n0 + Cfg::B_ROWS * rank;         // this CTA's B rows
       const int kb_total = pr.kb_total;
       int t_nxt = -1;
@@ -543,6 +549,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
             const bool seg1 = pr.kseg > 0 && kb >= pr.kseg;
             const int ka = (seg1 ? kb - pr.kseg : kb) * TC_BK;
             tc_load_operand<1>(sA, seg1 ? ma1 : ma0, &full[s], 0, pr.a_mode, TC_BM, am0, ka, tl.b);
+            if constexpr (kWide)
+              tc_load_operand<1>(sA + TC_A_BYTES, seg1 ? ma1 : ma0, &full[s], 0, pr.a_mode, TC_BM,
+                                 am0 + TC_BM, ka, tl.b);
             const bool bseg1 = seg1 && pr.b_seg;
             const int kbk = (bseg1 ? kb - pr.kseg : kb) * TC_BK + pr.b_koff;
             const CUtensorMap* mb = bseg1 ? mb1 : mb0;
@@ -784,7 +793,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         mbar_wait(&tfull[acc], (esph >> acc) & 1);
         tc_fence_after();
       }
-      const int row0 = tl.m0 + TC_BM * rank + sub * TC_BM + q * 32;   // row inside the batch item
+      const int row0 = tl.m0 + Cfg::CTA_ROWS * rank + sub * TC_BM + q * 32;   // row inside the batch item
       const int row = row0 + lane;
       const bool row_ok = row < pr.M;
       const int rowg = tl.b * pr.M + (row_ok ? row : 0);   // row of the flattened [batch*M] arrays

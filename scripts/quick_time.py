@@ -22,6 +22,8 @@ if os.environ.get("ATTN_WIDE"):
     binding.attn_softmax_set_option("wide_tiles", int(os.environ["ATTN_WIDE"]))
 if os.environ.get("ATTN_MIXED"):
     binding.attn_softmax_set_option("mixed_tiles", int(os.environ["ATTN_MIXED"]))
+if os.environ.get("ATTN_WIDEMC"):
+    binding.attn_softmax_set_option("wide_multicast", int(os.environ["ATTN_WIDEMC"]))
 if os.environ.get("ATTN_PDL"):
     binding.attn_softmax_set_option("pdl", int(os.environ["ATTN_PDL"]))
 if os.environ.get("ATTN_CTAS"):

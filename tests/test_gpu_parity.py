@@ -49,7 +49,7 @@ def oracle(inp, scale):
 
 
 # ------------------------------------------------------------ GEMM core ----
-@pytest.mark.parametrize("pair", [1, 2, 3, 4])
+@pytest.mark.parametrize("pair", [1, 2, 3, 4, 6])
 @pytest.mark.parametrize("mn3d", [0, 1])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 0), (0, 1), (1, 1)])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (296, 520, 200), (1000, 264, 1536),
@@ -64,6 +64,7 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, pair):
     binding.attn_softmax_set_option("cta_pair", 8 if pair == 2 else 0)
     binding.attn_softmax_set_option("b_multicast", 8 if pair == 3 else 0)
     binding.attn_softmax_set_option("wide_tiles", 8 if pair == 4 else 0)
+    binding.attn_softmax_set_option("wide_multicast", 8 if pair == 6 else 0)
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N + K)
     A = torch.randn(M, K, generator=g).bfloat16()
     B = torch.randn(N, K, generator=g).bfloat16()
@@ -83,19 +84,22 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, pair):
 def set_modes(binding, mode):
     """GEMM tile modes per group (bits: 1 forward, 2 vocab backward, 4
     projection backward, 8 debug entry): "pN" CTA pairs, "mN" B-multicast
-    clusters, "wN" wide single-CTA tiles (the other groups on 128x256
+    clusters, "wN" wide single-CTA tiles, "xN" mixed wide / 128x256 tiles,
+    "cN" B-multicast clusters of wide tiles (the other groups on 128x256
     single-CTA tiles), "default" the library default (wide vocab backward)."""
-    pair, mcast, wide, mixed = 8, 0, 2, 0
+    pair, mcast, wide, mixed, widemc = 8, 0, 2, 0, 0
     if mode != "default":
         mask = int(mode[1:])
         pair = mask if mode[0] == "p" else 0
         mcast = mask if mode[0] == "m" else 0
         wide = mask if mode[0] == "w" else 0
         mixed = mask if mode[0] == "x" else 0
+        widemc = mask if mode[0] == "c" else 0
     binding.attn_softmax_set_option("cta_pair", pair)
     binding.attn_softmax_set_option("b_multicast", mcast)
     binding.attn_softmax_set_option("wide_tiles", wide)
     binding.attn_softmax_set_option("mixed_tiles", mixed)
+    binding.attn_softmax_set_option("wide_multicast", widemc)
 
 
 @pytest.mark.parametrize("name,vc,mode", [("tiny", 0, "p8"), ("tiny_ragged", 0, "p8"),
@@ -113,7 +117,9 @@ def set_modes(binding, mode):
                                           ("edge_max_src", 256, "w0"),
                                           ("small", 0, "x2"), ("small", 1024, "x2"),
                                           ("medium", 2048, "x2"), ("medium", 1024, "x15"),
-                                          ("odd", 256, "x2"), ("odd", 0, "x15")])
+                                          ("odd", 256, "x2"), ("odd", 0, "x15"),
+                                          ("small", 0, "c2"), ("medium", 2048, "c15"),
+                                          ("odd", 256, "c2"), ("odd", 0, "c15")])
 def test_parity_vs_oracle(cuda_lib, name, vc, mode):
     """mode = GEMM tile modes per group (see set_modes)."""
     from paper_1909_00562_b200 import binding
