@@ -83,6 +83,9 @@ long long attn_softmax_last_launches(void);
  *                   kernel mixing wide tiles with 128 x 256 tiles for the
  *                   short-K dlogits (variable-size operand stages); wins
  *                   over wide_tiles.  Default 0.
+ *   "db_gemm"       1 = db_out of the F_c bias as a GEMM against ones inside
+ *                   the vocab-backward launches (single-CTA tiles); 0
+ *                   (default) = column-sum kernels after each launch
  *   "wide_multicast" bitmask (same bits as cta_pair) of GEMM groups run on
  *                   2-CTA clusters of wide 256 x 256 tiles sharing the B tile
  *                   by TMA multicast (512 rows per cluster); wins over

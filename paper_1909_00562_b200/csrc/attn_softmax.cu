@@ -123,6 +123,10 @@ static int g_opt_mixed = 0;
 // "wide_multicast": bitmask of GEMM groups on 2-CTA clusters of wide tiles
 // sharing B (kPair 6); takes precedence over wide_tiles
 static int g_opt_widemc = 0;
+// "db_gemm": db_out as a ones GEMM inside the vocab-backward launches (1) or
+// column-sum kernels after each launch (0, default: same-box A/B at C1 2.34
+// vs 2.37 ms with the bias)
+static int g_opt_db_gemm = 0;
 static long long* g_trace = nullptr;   // "gemm_trace": device pointer of a per-tile trace buffer
 static long long g_trace_launch = -1;  // "gemm_trace_launch": trace only this launch index of a call (-1 = all)
 static int64_t g_opt_vocab_chunk = 0;
@@ -151,6 +155,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "mixed_tiles")) {
     g_opt_mixed = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "db_gemm")) {
+    g_opt_db_gemm = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "wide_multicast")) {
@@ -407,7 +415,7 @@ static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr
                           (cuuint64_t)(g.epi.stash_ld * 4 * (long long)g.M)};
       if ((st = encode(&maps[3], g.epi.stash_f32, true, 3, d2, s2, box)) != ATTN_OK) return st;
     }
-  } else if (k != EPI_LSE && k != EPI_NONE && k != EPI_TOPK) {
+  } else if (k != EPI_LSE && k != EPI_NONE && k != EPI_TOPK && k != EPI_COL0_F32) {
     const bool f32 = epi_out_is_f32(k);
     const int esz = f32 ? 4 : 2;
     const long long bs = g.batch > 1 ? g.out_bstride : (long long)(g.M + 1) * g.epi.ldo;
@@ -519,6 +527,17 @@ static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cu
   return launch_tc_group_k<OutT, 1>(gs, n, counter, stream, group_bit, ctas);
 }
 
+// The engine variant launch_tc_group picks for a group (1 / 2 / 3 / 4 / 5 / 6).
+static int group_kpair(int group_bit) {
+  if (!group_bit) return 1;
+  if (g_opt_mixed & group_bit) return 5;
+  if (g_opt_widemc & group_bit) return 6;
+  if (g_opt_wide & group_bit) return 4;
+  if (g_opt_mcast & group_bit) return 3;
+  if (g_opt_pair & group_bit) return 2;
+  return 1;
+}
+
 // Launch a plain kernel, as a programmatic dependent of the previous kernel
 // when the "pdl" option is on (the kernel must pdl_wait() first).
 template <typename... KArgs, typename... Args>
@@ -606,9 +625,10 @@ struct Plan {
   int nchunks;
   size_t off_lens, off_counters, off_blockpart, off_alpha, off_dalpha, off_ctx, off_hc, off_part,
       off_tgtlogit, off_lse, off_nll, off_rowscale, off_dl, off_dhc, off_dz, off_dhc2, off_abf,
-      off_debf, off_q, off_dbpart;
+      off_debf, off_q, off_dbpart, off_ones;
   int Mp;             // bf16 path: row stride of the bf16 alpha / de operands (64-multiple)
   int ald;            // row stride of the fp32 alpha stash (bf16 path: Mp, for TMA stores)
+  long long Tld;      // row stride of the ones operand of the db_out GEMM (8-multiple >= T)
   size_t total;
 };
 
@@ -668,6 +688,8 @@ static Plan make_plan(const attn_shape_t* s) {
   p.off_debf = take(p.bf16 ? 2 * p.T * p.Mp : 0);
   p.off_q = take(p.elt * p.T * p.d);   // Eq. 2 general score: Q = H W_alpha
   p.off_dbpart = take(sizeof(float) * 16 * (size_t)p.Vc);   // F_c bias: column-sum partials
+  p.Tld = (p.T + 7) / 8 * 8;
+  p.off_ones = take(p.bf16 ? 2 * 16 * (size_t)p.Tld : 0);   // F_c bias, bf16 path: [16, Tld] ones
   p.total = o;
   return p;
 }
@@ -785,7 +807,8 @@ struct Bufs {
   float* alpha; float* dalpha; void* ctx; void* hc; float2* part; float* tgt_logit;
   float* lse; float* nll; float* rowscale; void* dl[2]; float* dhc; void* dz; float* dhc2;
   void* abf; void* debf; float* dhpart; void* dcbf;   // bf16 path
-  float* dbpart;   // F_c bias: [16, Vc] column-sum partials
+  float* dbpart;   // F_c bias: [16, Vc] column-sum partials (when not a GEMM)
+  void* ones;      // F_c bias, bf16 path: [16, Tld] bf16 ones (B operand of the db_out GEMM)
   void* q;    // Eq. 2 general score: Q = H W_alpha [T, d] (dtype)
   void* dq;   // its gradient [T, d] (dtype); aliases dz, which is dead by then
 };
@@ -817,6 +840,7 @@ static Bufs carve(const Plan& p, void* ws) {
   b.dcbf = (char*)(b.dhc2 + p.T * p.d);       //            dC bf16 [T, d]
   b.q = w + p.off_q;
   b.dbpart = (float*)(w + p.off_dbpart);
+  b.ones = w + p.off_ones;
   b.dq = b.dz;
   return b;
 }
@@ -919,6 +943,19 @@ static GemmDesc g_dwout(const Plan& p, const Bufs& b, float* dW_out, int c) {
   g.b_mn = 1; g.b0 = mnmaj(b.hc, p.T, p.d, p.d);
   g.epi.kind = EPI_STORE_F32; g.epi.out = dW_out + (size_t)c0 * p.d; g.epi.ldo = p.d;
   g.epi.ncols_valid = p.d; g.epi.ncols_store = p.d;
+  return g;
+}
+// B1, chunk c, F_c bias: db_out[c0 + v] = sum_t dlogits_c[t, v], as the GEMM
+// dlogits_c^T [vcc, T] x ones [16, T]^T with only column 0 kept: the A operand
+// is dW_out's, read once more by the tensor cores in the same launch
+static GemmDesc g_dbout(const Plan& p, const Bufs& b, float* db_out, int c) {
+  GemmDesc g;
+  const int c0 = c * p.Vc, vcc = std::min(p.Vc, p.V - c0);
+  g.M = vcc; g.N = 16; g.K = (int)p.T; g.bn = 16;
+  g.a_mn = 1; g.a0 = mnmaj(b.dl[c & 1], p.T, vcc, p.Vc);
+  g.b0 = kmaj(b.ones, 16, p.T, p.Tld);
+  g.epi.kind = EPI_COL0_F32; g.epi.out = db_out + c0;
+  g.epi.ncols_valid = 1; g.epi.ncols_store = 1;
   return g;
 }
 // B1, chunk c: dHc (+)= dlogits_c W_out[c]   (B MN-major, K offset c0)
@@ -1163,17 +1200,27 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   {
     // chunk 0's dlogits alone: 128 x 256 tiles (short K; two accumulators in
     // TMEM so each tile's exp epilogue overlaps the next tile's MMAs)
+    // db_out as a GEMM on the tensor cores where the vocab-backward launches
+    // run on single CTAs with uniform stages (narrow B tile); else column sums
+    const bool db_gemm = db_out && tc && g_opt_db_gemm && (group_kpair(PAIR_VBWD) == 1 || group_kpair(PAIR_VBWD) == 4);
+    if (db_gemm) {   // bf16 ones (0x3F80) for the db_out GEMMs
+      const long long words = 16 * p.Tld / 2;
+      st = launch_pdl(fill_u32_kernel, dim3((unsigned)std::min<long long>(148, (words + 255) / 256)),
+                      dim3(256), stream, (uint32_t*)b.ones, words, 0x3F803F80u);
+      if (st != ATTN_OK) return st;
+    }
     GemmDesc g0 = g_dlogits(p, b, W_out, tgt_ids, 0, b_out);
     if ((st = gemm(&g0, 1, 0)) != ATTN_OK) return st;
     for (int c = 0; c < p.nchunks; ++c) {
-      GemmDesc gs[3];
+      GemmDesc gs[4];
       int n = 0;
       gs[n++] = g_dwout(p, b, dW_out, c);   // K = T: the long tiles first
+      if (db_gemm) gs[n++] = g_dbout(p, b, db_out, c);
       gs[n++] = g_dhc(p, b, W_out, c);
       if (c + 1 < p.nchunks) gs[n++] = g_dlogits(p, b, W_out, tgt_ids, c + 1, b_out);
       if ((st = gemm(gs, n, PAIR_VBWD)) != ATTN_OK) return st;
-      if (db_out) {
-        // F_c bias: db_out[chunk c] = column sums of dlogits_c (still intact:
+      if (db_out && !db_gemm) {
+        // F_c bias (fp32 path, paired / mixed tiles): db_out[chunk c] = column sums of dlogits_c (still intact:
         // the next launch is the one that overwrites its buffer)
         const int c0 = c * p.Vc, vcc = std::min(p.Vc, p.V - c0);
         const int splits = (int)std::min<long long>(16, std::max<long long>(1, TT / 256));

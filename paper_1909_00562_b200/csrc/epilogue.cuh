@@ -27,8 +27,10 @@ enum EpiKind : int {
   EPI_ADD_BF16 = 7,           // out = acc + addend (fp32) -> bf16: dH_dec = dH_part + de S
   EPI_ATTN_SOFTMAX = 8,       // masked row softmax of the scores (Eq. 1), tcgen05 path
   EPI_ATTN_SOFTMAX_BWD = 9,   // its backward, tcgen05 path
-  EPI_TOPK = 11               // decoding step (NEXT-4): LSE partials as EPI_LSE plus the 8 best
+  EPI_TOPK = 11,              // decoding step (NEXT-4): LSE partials as EPI_LSE plus the 8 best
                               // (logit, token) of the row's columns in the tile (tcgen05 path)
+  EPI_COL0_F32 = 12           // out[row] = acc[row, 0] (fp32): a matrix-vector product computed
+                              // as a GEMM against a block of ones (db_out, tcgen05 path)
 };
 
 // Output element type of each kind (tcgen05 path: bf16 activations).
@@ -135,7 +137,29 @@ template <typename OutT>
 __device__ __forceinline__ void add_bias32(const void* bias, int gcol, int nvalid_rel,
                                            float (&v)[32]) {
   const OutT* b = reinterpret_cast<const OutT*>(bias) + gcol;
-  if (nvalid_rel >= 32) {
+  if (nvalid_rel >= 32 && (reinterpret_cast<uintptr_t>(b) & 15) == 0) {   // 16-byte vector loads
+    const uint4* b4 = reinterpret_cast<const uint4*>(b);
+#pragma unroll
+    for (int g = 0; g < 32 * (int)sizeof(OutT) / 16; ++g) {
+      const uint4 u = __ldg(b4 + g);
+      const uint32_t w0 = u.x, w1 = u.y, w2 = u.z, w3 = u.w;
+      if constexpr (sizeof(OutT) == 2) {   // bf16 -> fp32: the high half of the word
+        v[8 * g + 0] += __uint_as_float(w0 << 16);
+        v[8 * g + 1] += __uint_as_float(w0 & 0xFFFF0000u);
+        v[8 * g + 2] += __uint_as_float(w1 << 16);
+        v[8 * g + 3] += __uint_as_float(w1 & 0xFFFF0000u);
+        v[8 * g + 4] += __uint_as_float(w2 << 16);
+        v[8 * g + 5] += __uint_as_float(w2 & 0xFFFF0000u);
+        v[8 * g + 6] += __uint_as_float(w3 << 16);
+        v[8 * g + 7] += __uint_as_float(w3 & 0xFFFF0000u);
+      } else {
+        v[4 * g + 0] += __uint_as_float(w0);
+        v[4 * g + 1] += __uint_as_float(w1);
+        v[4 * g + 2] += __uint_as_float(w2);
+        v[4 * g + 3] += __uint_as_float(w3);
+      }
+    }
+  } else if (nvalid_rel >= 32) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] += to_f32(b[j]);
   } else {

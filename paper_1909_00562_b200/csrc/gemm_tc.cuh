@@ -813,6 +813,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         if (n_act > 0)
           epi_attn_softmax_bwd(pr.epi, taddr, n_act, rowg, row_ok, staging + ew * TC_STG_BYTES,
                                omap, row0, tl.b, lane);
+      } else if (kind == EPI_COL0_F32) {
+        if (h == 0 && n_act > 0) {
+          float v[32];
+          tmem_ld32(taddr, v);
+          if (row_ok) static_cast<float*>(pr.epi.out)[rowg] = v[0];
+        }
       } else if (kDecode && kind == EPI_TOPK) {
         if constexpr (kDecode)
           epi_topk<OutT>(pr.epi, taddr, n_act, col_h, rowg, row_ok, tl.tn * 2 + h);

@@ -13,7 +13,8 @@
 //   decode_final_kernel  decoding step (NEXT-4): lse and the k best tokens of
 //                        each row from the vocab GEMM's per-tile partials
 //   colsum_*_kernel      db_out of the F_c bias (NEXT-1): column sums of one
-//                        dlogits V-chunk, two passes in a fixed order
+//                        dlogits V-chunk, two passes in a fixed order (fp32
+//                        path and paired tiles; else a ones GEMM)
 #pragma once
 #include <cstdint>
 #include <cuda_bf16.h>
@@ -301,6 +302,13 @@ struct LensChunk {
 };
 __global__ void __launch_bounds__(512) lens_kernel(const __grid_constant__ LensChunk c) {
   if ((int)threadIdx.x < c.n) c.dst[threadIdx.x] = c.vals[threadIdx.x];
+}
+
+// fill n 32-bit words with v (the ones operand of the db_out GEMM)
+__global__ void __launch_bounds__(256) fill_u32_kernel(uint32_t* __restrict__ p, long long n,
+                                                       uint32_t v) {
+  pdl_wait();
+  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * gridDim.x) p[i] = v;
 }
 
 __global__ void check_ids_kernel(const int* __restrict__ ids, const int* __restrict__ tgt_len,

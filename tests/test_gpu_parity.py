@@ -192,20 +192,30 @@ def test_parity_general_score(cuda_lib, name, vc, mode):
                                                 ("small", 1024, "p15", True),
                                                 ("medium", 0, "default", False),
                                                 ("medium", 2048, "w0", True),
-                                                ("odd", 256, "w15", False)])
+                                                ("odd", 256, "w15", False),
+                                                ("odd", 0, "x2", False),
+                                                ("medium", 1024, "c2", False),
+                                                ("small", 0, "default+db", True),
+                                                ("medium", 2048, "w0+db", False),
+                                                ("odd", 256, "default+db", False)])
 def test_parity_output_bias(cuda_lib, name, vc, mode, alpha):
     """NEXT-1: the F_c bias b_out of Eq. 5 -- added in the
     forward LSE and the backward dlogits epilogues, db_out = column sums of
-    each dlogits V-chunk -- against the oracle (with and without W_alpha)."""
+    each dlogits V-chunk (column-sum kernels, or with "+db" a ones GEMM inside
+    the vocab-backward launches) -- against the oracle (with and without
+    W_alpha)."""
     from paper_1909_00562_b200 import binding
     cfg = CONFIGS[name]
     inp = make_inputs(cfg, with_alpha=alpha, with_bias=True)
     scale = 1.0 / global_valid_tokens(cfg, cfg.B)
+    mode, _, db = mode.partition("+")
     set_modes(binding, mode)
+    binding.attn_softmax_set_option("db_gemm", 1 if db else 0)
     try:
         g = run_gpu(cfg, inp, scale, vocab_chunk=vc)
     finally:
         set_modes(binding, "default")
+        binding.attn_softmax_set_option("db_gemm", 0)
     f, b = oracle(inp, scale)
     tol = TOL[cfg.dtype]
     assert abs(g["loss"] - f["loss"]) <= tol["loss"] * abs(f["loss"]), (g["loss"], f["loss"])
