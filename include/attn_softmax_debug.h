@@ -83,6 +83,12 @@ long long attn_softmax_last_launches(void);
  *                   kernel mixing wide tiles with 128 x 256 tiles for the
  *                   short-K dlogits (variable-size operand stages); wins
  *                   over wide_tiles.  Default 0.
+ *   "store_logits"  bf16 path: 1 (default) = the forward vocab GEMM also stores
+ *                   the logits as fp16 [T, V] (workspace grows by 2 T V bytes)
+ *                   and the backward makes each V-chunk's dlogits from them
+ *                   with an elementwise kernel that starts beside the
+ *                   previous chunk's launch; 2 = the same, serialised; 0 =
+ *                   recompute the logits chunk by chunk on the tensor cores
  *   "db_gemm"       1 = db_out of the F_c bias as a GEMM against ones inside
  *                   the vocab-backward launches (single-CTA tiles); 0
  *                   (default) = column-sum kernels after each launch

@@ -127,6 +127,15 @@ static int g_opt_widemc = 0;
 // column-sum kernels after each launch (0, default: same-box A/B at C1 2.34
 // vs 2.37 ms with the bias)
 static int g_opt_db_gemm = 0;
+// "store_logits": the bf16 path's forward vocab GEMM also stores the logits as
+// fp16 [T, V]; the backward turns each V-chunk into dlogits with an
+// elementwise kernel instead of recomputing H_c W_out^T on the tensor cores.
+// 1 (default): chunk c+1's kernel starts beside launch c (PDL, waits at its
+// end); 2: serialised; 0: recompute (same-box A/B at C1: 1.92 / 1.98 / 2.15 ms)
+static int g_opt_store_logits = 1;
+// "n_fast": dispatch the vocab-backward GEMMs' column tiles of one row block
+// back to back (their shared A block -- the dlogits chunk -- then leaves HBM once)
+static int g_opt_n_fast = 1;
 static long long* g_trace = nullptr;   // "gemm_trace": device pointer of a per-tile trace buffer
 static long long g_trace_launch = -1;  // "gemm_trace_launch": trace only this launch index of a call (-1 = all)
 static int64_t g_opt_vocab_chunk = 0;
@@ -155,6 +164,14 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "mixed_tiles")) {
     g_opt_mixed = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "n_fast")) {
+    g_opt_n_fast = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "store_logits")) {
+    g_opt_store_logits = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "db_gemm")) {
@@ -244,14 +261,16 @@ static PFN_encodeTiled get_encode() {
 }
 
 // rank-r tensor map, 128-byte swizzle, zero fill out of bounds.
-static attn_status_t encode(CUtensorMap* m, const void* ptr, bool f32, int rank,
+// dt: 0 = bf16, 1 = fp32, 2 = fp16
+static attn_status_t encode(CUtensorMap* m, const void* ptr, int dt, int rank,
                             const cuuint64_t* dims, const cuuint64_t* strides_bytes,
                             const cuuint32_t* box,
                             CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
-  CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
+  CUresult r = enc(m, dt == 1 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                   : dt == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
                    const_cast<void*>(ptr), dims, strides_bytes, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -302,6 +321,7 @@ struct GemmDesc {
   long long out_bstride = 0;   // batch stride of the epilogue output (elements)
   int bn = 0;        // tile columns (0 = 256); < 256 only for K-major B on single CTAs
   int narrow = 0;    // mixed launches (kPair = 5): 128 x 256 tiles for this problem
+  int n_fast = 0;    // dispatch the column tiles of a row block together (A read once via L2)
   EpiParams epi{};
 };
 
@@ -347,6 +367,7 @@ static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr
   pr.M = g.M; pr.N = g.N; pr.K = g.K; pr.batch = g.batch;
   pr.bn = bn;
   pr.narrow = narrow ? 1 : 0;
+  pr.n_fast = g.n_fast && g_opt_n_fast;
   pr.tiles_m = (g.M + tile_m - 1) / tile_m;
   pr.tiles_n = (g.N + bn - 1) / bn;
   pr.kseg = g.kseg;
@@ -415,14 +436,17 @@ static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr
                           (cuuint64_t)(g.epi.stash_ld * 4 * (long long)g.M)};
       if ((st = encode(&maps[3], g.epi.stash_f32, true, 3, d2, s2, box)) != ATTN_OK) return st;
     }
-  } else if (k != EPI_LSE && k != EPI_NONE && k != EPI_TOPK && k != EPI_COL0_F32) {
+  } else if ((k != EPI_LSE || g.epi.out) && k != EPI_NONE && k != EPI_TOPK && k != EPI_COL0_F32) {
+    // (LSE with `out`: the fp16 logits of option store_logits)
     const bool f32 = epi_out_is_f32(k);
     const int esz = f32 ? 4 : 2;
     const long long bs = g.batch > 1 ? g.out_bstride : (long long)(g.M + 1) * g.epi.ldo;
     cuuint64_t dims[3] = {(cuuint64_t)g.epi.ncols_store, (cuuint64_t)g.M, (cuuint64_t)g.batch};
     cuuint64_t strides[2] = {(cuuint64_t)(g.epi.ldo * esz), (cuuint64_t)(bs * esz)};
     cuuint32_t box[3] = {(cuuint32_t)(f32 ? 32 : 64), 32, 1};
-    if ((st = encode(&maps[4], g.epi.out, f32, 3, dims, strides, box)) != ATTN_OK) return st;
+    if ((st = encode(&maps[4], g.epi.out, f32 ? 1 : k == EPI_LSE ? 2 : 0, 3, dims, strides, box)) !=
+        ATTN_OK)
+      return st;
   } else {
     maps[4] = maps[0];
   }
@@ -625,10 +649,12 @@ struct Plan {
   int nchunks;
   size_t off_lens, off_counters, off_blockpart, off_alpha, off_dalpha, off_ctx, off_hc, off_part,
       off_tgtlogit, off_lse, off_nll, off_rowscale, off_dl, off_dhc, off_dz, off_dhc2, off_abf,
-      off_debf, off_q, off_dbpart, off_ones;
+      off_debf, off_q, off_dbpart, off_ones, off_logits;
   int Mp;             // bf16 path: row stride of the bf16 alpha / de operands (64-multiple)
   int ald;            // row stride of the fp32 alpha stash (bf16 path: Mp, for TMA stores)
   long long Tld;      // row stride of the ones operand of the db_out GEMM (8-multiple >= T)
+  bool store_logits;  // bf16 path, option store_logits: fp16 logits [T, Vld] in the workspace
+  long long Vld;
   size_t total;
 };
 
@@ -690,6 +716,9 @@ static Plan make_plan(const attn_shape_t* s) {
   p.off_dbpart = take(sizeof(float) * 16 * (size_t)p.Vc);   // F_c bias: column-sum partials
   p.Tld = (p.T + 7) / 8 * 8;
   p.off_ones = take(p.bf16 ? 2 * 16 * (size_t)p.Tld : 0);   // F_c bias, bf16 path: [16, Tld] ones
+  p.store_logits = p.bf16 && g_opt_store_logits;
+  p.Vld = (p.V + 7) / 8 * 8;
+  p.off_logits = take(p.store_logits ? 2 * (size_t)p.T * p.Vld : 0);
   p.total = o;
   return p;
 }
@@ -809,6 +838,7 @@ struct Bufs {
   void* abf; void* debf; float* dhpart; void* dcbf;   // bf16 path
   float* dbpart;   // F_c bias: [16, Vc] column-sum partials (when not a GEMM)
   void* ones;      // F_c bias, bf16 path: [16, Tld] bf16 ones (B operand of the db_out GEMM)
+  void* logits;    // option store_logits: fp16 [T, Vld]
   void* q;    // Eq. 2 general score: Q = H W_alpha [T, d] (dtype)
   void* dq;   // its gradient [T, d] (dtype); aliases dz, which is dead by then
 };
@@ -841,6 +871,7 @@ static Bufs carve(const Plan& p, void* ws) {
   b.q = w + p.off_q;
   b.dbpart = (float*)(w + p.off_dbpart);
   b.ones = w + p.off_ones;
+  b.logits = p.store_logits ? w + p.off_logits : nullptr;
   b.dq = b.dz;
   return b;
 }
@@ -916,6 +947,7 @@ static GemmDesc g_vocab_fwd(const Plan& p, const Bufs& b, const void* W_out, con
   g.epi.kind = EPI_LSE; g.epi.ncols_valid = p.V; g.epi.ncols_store = p.V; g.epi.col_base = 0;
   g.epi.part = b.part; g.epi.part_ld = p.part_ld; g.epi.tgt_logit = b.tgt_logit; g.epi.tgt = tgt;
   g.epi.bias = b_out;
+  if (p.store_logits) { g.epi.out = b.logits; g.epi.ldo = p.Vld; }
   return g;
 }
 // B1, chunk c: dlogits_c = rowscale (softmax - onehot) of the recomputed logits
@@ -943,6 +975,7 @@ static GemmDesc g_dwout(const Plan& p, const Bufs& b, float* dW_out, int c) {
   g.b_mn = 1; g.b0 = mnmaj(b.hc, p.T, p.d, p.d);
   g.epi.kind = EPI_STORE_F32; g.epi.out = dW_out + (size_t)c0 * p.d; g.epi.ldo = p.d;
   g.epi.ncols_valid = p.d; g.epi.ncols_store = p.d;
+  g.n_fast = 1;
   return g;
 }
 // B1, chunk c, F_c bias: db_out[c0 + v] = sum_t dlogits_c[t, v], as the GEMM
@@ -967,6 +1000,7 @@ static GemmDesc g_dhc(const Plan& p, const Bufs& b, const void* W_out, int c) {
   g.b_mn = 1; g.b0 = mnmaj(W_out, p.V, p.d, p.d); g.b_koff = c0;
   g.epi.kind = (c == 0) ? EPI_STORE_F32 : EPI_ACCUM_F32; g.epi.out = b.dhc; g.epi.ldo = p.d;
   g.epi.ncols_valid = p.d; g.epi.ncols_store = p.d;
+  g.n_fast = 1;
   return g;
 }
 // B2: dW_c = dz^T [H | C]   (A MN-major, B MN-major split at column d)
@@ -1197,9 +1231,9 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
 
   // ---- B1: V-chunked vocab backward.  Launch c runs dW_out[c] and dHc += ...
   // for chunk c together with the dlogits of chunk c+1 (double-buffered).
+  // With stored logits, an elementwise kernel makes dlogits_c from the
+  // forward's fp16 logits before launch c (no recompute on the tensor cores).
   {
-    // chunk 0's dlogits alone: 128 x 256 tiles (short K; two accumulators in
-    // TMEM so each tile's exp epilogue overlaps the next tile's MMAs)
     // db_out as a GEMM on the tensor cores where the vocab-backward launches
     // run on single CTAs with uniform stages (narrow B tile); else column sums
     const bool db_gemm = db_out && tc && g_opt_db_gemm && (group_kpair(PAIR_VBWD) == 1 || group_kpair(PAIR_VBWD) == 4);
@@ -1209,18 +1243,37 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
                       dim3(256), stream, (uint32_t*)b.ones, words, 0x3F803F80u);
       if (st != ATTN_OK) return st;
     }
-    GemmDesc g0 = g_dlogits(p, b, W_out, tgt_ids, 0, b_out);
-    if ((st = gemm(&g0, 1, 0)) != ATTN_OK) return st;
+    // dlogits of chunk c from the stored logits (on `s`, `blocks` blocks)
+    auto dlogits_ew = [&](int c, cudaStream_t s, int blocks) -> attn_status_t {
+      const int c0 = c * p.Vc, vcc = std::min(p.Vc, p.V - c0);
+      return launch_pdl(dlogits_from_logits_kernel,
+                        dim3((unsigned)std::min<long long>(TT, blocks)), dim3(kEwThreads), s,
+                        (const __half*)b.logits, p.Vld, c0, vcc, (int)TT, (const float*)b.lse,
+                        (const float*)b.rowscale, tgt_ids, (const float*)b.tgt_logit,
+                        (__nv_bfloat16*)b.dl[c & 1], (long long)p.Vc,
+                        (c == 0 || !g_opt_pdl || g_opt_store_logits == 2) ? 1 : 0);
+    };
+    const int sms = dev_info().sms;
+    if (p.store_logits) {
+      if ((st = dlogits_ew(0, stream, 4 * sms)) != ATTN_OK) return st;
+    } else {
+      // chunk 0's dlogits alone: 128 x 256 tiles (short K; two accumulators
+      // in TMEM so each tile's exp epilogue overlaps the next tile's MMAs)
+      GemmDesc g0 = g_dlogits(p, b, W_out, tgt_ids, 0, b_out);
+      if ((st = gemm(&g0, 1, 0)) != ATTN_OK) return st;
+    }
     for (int c = 0; c < p.nchunks; ++c) {
+      if (p.store_logits && c > 0 && (st = dlogits_ew(c, stream, 4 * sms)) != ATTN_OK) return st;
       GemmDesc gs[4];
       int n = 0;
       gs[n++] = g_dwout(p, b, dW_out, c);   // K = T: the long tiles first
       if (db_gemm) gs[n++] = g_dbout(p, b, db_out, c);
       gs[n++] = g_dhc(p, b, W_out, c);
-      if (c + 1 < p.nchunks) gs[n++] = g_dlogits(p, b, W_out, tgt_ids, c + 1, b_out);
+      if (c + 1 < p.nchunks && !p.store_logits)
+        gs[n++] = g_dlogits(p, b, W_out, tgt_ids, c + 1, b_out);
       if ((st = gemm(gs, n, PAIR_VBWD)) != ATTN_OK) return st;
       if (db_out && !db_gemm) {
-        // F_c bias (fp32 path, paired / mixed tiles): db_out[chunk c] = column sums of dlogits_c (still intact:
+        // F_c bias: db_out[chunk c] = column sums of dlogits_c (still intact:
         // the next launch is the one that overwrites its buffer)
         const int c0 = c * p.Vc, vcc = std::min(p.Vc, p.V - c0);
         const int splits = (int)std::min<long long>(16, std::max<long long>(1, TT / 256));

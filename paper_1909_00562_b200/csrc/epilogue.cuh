@@ -17,6 +17,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 namespace attnsm {
 
@@ -43,7 +44,8 @@ struct EpiParams {
   int ncols_valid;       // columns < ncols_valid are real (V tail, chunk tail)
   int ncols_store;       // columns < ncols_store may be written (row capacity)
   int col_base;          // global column of problem column 0 (V-chunk start)
-  void* out;             // STORE_F32 / ACCUM_F32: float; TANH / DLOGITS: OutT
+  void* out;             // STORE_F32 / ACCUM_F32: float; TANH / DLOGITS: OutT; LSE (tcgen05,
+                         // optional): the logits as fp16 [rows, ldo] (option store_logits)
   long long ldo;         // row stride of out (elements)
   long long split_stride;// element offset between split-K partial outputs
   float2* part;          // LSE: [rows, part_ld] (max, sumexp)

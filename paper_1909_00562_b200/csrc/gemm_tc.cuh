@@ -103,6 +103,7 @@ struct TcProblem {
   int b_koff;       // added to B's K coordinate (elements)
   int bn;           // tile columns (UMMA N): 256, or 16..240 for K-major B on single CTAs
   int narrow;       // kPair = 5: this problem uses 128 x 256 tiles
+  int n_fast;       // dispatch order: column tiles fastest (tiles sharing an A row block adjacent)
   EpiParams epi;
 };
 
@@ -166,8 +167,8 @@ __device__ __forceinline__ TcTile tc_decode(const TcParams& P, int t) {
   const int per_b = pr.tiles_m * pr.tiles_n;
   r.b = local / per_b;
   local -= r.b * per_b;
-  const int tm = local % pr.tiles_m;
-  r.tn = local / pr.tiles_m;
+  const int tm = pr.n_fast ? local / pr.tiles_n : local % pr.tiles_m;
+  r.tn = pr.n_fast ? local % pr.tiles_n : local / pr.tiles_m;
   r.nsub = (TcCfg<kPair>::WIDE && !(TcCfg<kPair>::VAR && pr.narrow)) ? 2 : 1;
   r.m0 = tm * (TcCfg<kPair>::VAR ? TC_BM * r.nsub : TcCfg<kPair>::TILE_M);
   r.n0 = r.tn * pr.bn;
@@ -831,11 +832,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           tmem_ld32(taddr + c * 32, v);
           const int col = col_h + c * 32;
           if (kind == EPI_LSE) {
-            if (row_ok) epi.chunk(col, v);
-            continue;
+            if (row_ok) epi.chunk(col, v);   // (adds the bias to v)
+            if (!pr.epi.out) continue;       // else store the logits as fp16
+          } else {
+            if (kind == EPI_NONE) continue;
+            epi.transform(col, v);
           }
-          if (kind == EPI_NONE) continue;
-          epi.transform(col, v);
           if (kind == EPI_ADD_BF16 && row_ok) {
             const float4* ad = reinterpret_cast<const float4*>(pr.epi.addend +
                                                                (long long)rowg * pr.epi.add_ld + col);
@@ -875,8 +877,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
               uint32_t w[4];
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * g + 2 * e], v[8 * g + 2 * e + 1]);
-                w[e] = *reinterpret_cast<uint32_t*>(&h2);
+                if (kind == EPI_LSE) {
+                  __half2 h2 = __floats2half2_rn(v[8 * g + 2 * e], v[8 * g + 2 * e + 1]);
+                  w[e] = *reinterpret_cast<uint32_t*>(&h2);
+                } else {
+                  __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * g + 2 * e], v[8 * g + 2 * e + 1]);
+                  w[e] = *reinterpret_cast<uint32_t*>(&h2);
+                }
               }
               const uint32_t gi = (c & 1) * 4 + g;
               st_shared_v4(stg + lane * 128 + ((gi ^ swz) << 4), w[0], w[1], w[2], w[3]);

@@ -12,6 +12,7 @@
 //   check_ids_kernel     target-id range check (ATTN_ERR_TOKEN_RANGE)
 //   decode_final_kernel  decoding step (NEXT-4): lse and the k best tokens of
 //                        each row from the vocab GEMM's per-tile partials
+//   dlogits_from_logits_kernel  B1 with the forward's stored fp16 logits
 //   colsum_*_kernel      db_out of the F_c bias (NEXT-1): column sums of one
 //                        dlogits V-chunk, two passes in a fixed order (fp32
 //                        path and paired tiles; else a ones GEMM)
@@ -302,6 +303,92 @@ struct LensChunk {
 };
 __global__ void __launch_bounds__(512) lens_kernel(const __grid_constant__ LensChunk c) {
   if ((int)threadIdx.x < c.n) c.dst[threadIdx.x] = c.vals[threadIdx.x];
+}
+
+// B1 with stored logits (option store_logits): dlogits_c[t, v] = rs_t
+// (exp(l_tv - lse_t) - [v = y_t]) for the V-chunk [c0, c0 + vcc) from the
+// forward's fp16 logits, bf16 out (row stride dld); the target column uses
+// the fp32 target logit (as the GEMM epilogue does); 0 on padded rows.
+// Blocks stride over rows; a thread handles 8 columns (16-byte loads and
+// stores), four loads in flight.  256 threads of <= 48 registers: one block
+// fits beside a resident persistent GEMM CTA (registers, and the 1 KB of
+// shared memory the SM reserves per block).  wait_first = 0 (chunks
+// c >= 1, launched as programmatic dependents of launch c-1): the blocks
+// start while launch c-1 still runs and do their work beside it -- every
+// input is older than launch c-1 and the dlogits buffer they write was last
+// read by launch c-2, complete before launch c-1 passed its own wait -- and
+// only wait for launch c-1 at the end, so that launch c still starts after
+// launch c-1 has finished (dHc accumulation order).
+__device__ __forceinline__ uint32_t bf16x2_bits(float a, float b) {
+  __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h2);
+}
+constexpr int kEwThreads = 256;
+__global__ void __launch_bounds__(kEwThreads, 5) dlogits_from_logits_kernel(
+    const __half* __restrict__ lg, long long lld, int c0, int vcc, int T,
+    const float* __restrict__ lse, const float* __restrict__ rowscale, const int* __restrict__ tgt,
+    const float* __restrict__ tgt_logit, __nv_bfloat16* __restrict__ dl, long long dld,
+    int wait_first) {
+  if (wait_first) pdl_wait();
+  const int cols8 = (vcc + 7) / 8;
+  for (int row = blockIdx.x; row < T; row += gridDim.x) {
+    const float rs = rowscale[row];
+    float c2 = 0.f, fix = 0.f;
+    int y = -1;
+    if (rs > 0.f) {
+      const float ls = lse[row];
+      c2 = __log2f(rs) - ls * kLog2e;
+      y = tgt[row] - c0;
+      fix = rs * (__expf(tgt_logit[row] - ls) - 1.f);
+    }
+    const __half* l = lg + (long long)row * lld + c0;
+    __nv_bfloat16* o = dl + (long long)row * dld;
+    for (int j0 = threadIdx.x; j0 < cols8; j0 += 4 * kEwThreads) {
+      uint4 u[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int col = (j0 + k * kEwThreads) * 8;
+        u[k] = (rs > 0.f && col + 8 <= vcc) ? __ldcs(reinterpret_cast<const uint4*>(l + col))
+                                            : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int col = (j0 + k * kEwThreads) * 8;
+        if (col >= vcc) break;
+        float g[8];
+        if (rs > 0.f) {
+          if (col + 8 <= vcc) {
+            const uint32_t w[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+              g[2 * e] = ex2_mufu(fmaf(f.x, kLog2e, c2));
+              g[2 * e + 1] = ex2_mufu(fmaf(f.y, kLog2e, c2));
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              g[e] = col + e < vcc ? ex2_mufu(fmaf(__half2float(l[col + e]), kLog2e, c2)) : 0.f;
+          }
+          const int yl = y - col;
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (e == yl) g[e] = fix;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) g[e] = 0.f;
+        }
+        if (col + 8 <= vcc) {
+          *reinterpret_cast<uint4*>(o + col) =
+              make_uint4(bf16x2_bits(g[0], g[1]), bf16x2_bits(g[2], g[3]),
+                         bf16x2_bits(g[4], g[5]), bf16x2_bits(g[6], g[7]));
+        } else {
+          for (int e = 0; e < 8 && col + e < vcc; ++e) o[col + e] = __float2bfloat16_rn(g[e]);
+        }
+      }
+    }
+  }
+  if (!wait_first) pdl_wait();
 }
 
 // fill n 32-bit words with v (the ones operand of the db_out GEMM)

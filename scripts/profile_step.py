@@ -7,7 +7,8 @@ from paper_1909_00562_b200.stage import AttnSoftmaxStage, to_device
 from synthetic import CONFIGS, make_inputs, global_valid_tokens
 
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "paper"]
-for k, opt in (("ATTN_VC", "vocab_chunk"), ("ATTN_PAIR", "cta_pair"), ("ATTN_CTAS", "gemm_ctas")):
+for k, opt in (("ATTN_VC", "vocab_chunk"), ("ATTN_PAIR", "cta_pair"), ("ATTN_CTAS", "gemm_ctas"),
+               ("ATTN_SL", "store_logits")):
     if os.environ.get(k):
         binding.attn_softmax_set_option(opt, int(os.environ[k]))
 inp = make_inputs(cfg)

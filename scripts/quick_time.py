@@ -26,6 +26,10 @@ if os.environ.get("ATTN_WIDEMC"):
     binding.attn_softmax_set_option("wide_multicast", int(os.environ["ATTN_WIDEMC"]))
 if os.environ.get("ATTN_DBGEMM"):
     binding.attn_softmax_set_option("db_gemm", int(os.environ["ATTN_DBGEMM"]))
+if os.environ.get("ATTN_SL"):
+    binding.attn_softmax_set_option("store_logits", int(os.environ["ATTN_SL"]))
+if os.environ.get("ATTN_NFAST"):
+    binding.attn_softmax_set_option("n_fast", int(os.environ["ATTN_NFAST"]))
 if os.environ.get("ATTN_PDL"):
     binding.attn_softmax_set_option("pdl", int(os.environ["ATTN_PDL"]))
 if os.environ.get("ATTN_CTAS"):

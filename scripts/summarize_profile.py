@@ -32,10 +32,30 @@ for row in r[1:]:
         order.append(key)
     launch[key][row[ix["Metric Name"]]] = float(row[ix["Metric Value"]].replace(",", ""))
 n = len(order)
-nchunks = n - 9 - 1   # attn(2) proj vocab_fwd lse dlogits0 | chunks | dz proj_bwd attn_bwd(2)
-names = ["lengths upload (kernel parameters)", "attn scores+masked softmax (batched)", "attn context (batched)", "proj_tanh",
-         "vocab_fwd (LSE epilogue)", "lse_reduce", "dlogits chunk 0 (128x256 tiles)"]
-names += [f"vocab bwd chunk {c} (dW_out+dHc+dlogits c+1, 256x256 tiles)" for c in range(n - 11)]
+# name the launches from their kernels: attention and projection GEMMs, the
+# vocab forward, then per V-chunk either (stored logits) the elementwise
+# dlogits kernel + the dW_out/dHc launch, or (recompute) the dlogits-0 launch
+# + chunk launches that also recompute chunk c+1
+names = ["lengths upload (kernel parameters)", "attn scores+masked softmax (batched)",
+         "attn context (batched)", "proj_tanh", "vocab_fwd (LSE epilogue)", "lse_reduce"]
+stored = any("dlogits_from" in launch[k]["kernel"] for k in order)
+if stored:
+    names[4] = "vocab_fwd (LSE epilogue + fp16 logits store)"
+c = 0
+for k in order[6:]:
+    kn = launch[k]["kernel"]
+    if "dz_kernel" in kn:
+        break
+    if "dlogits_from" in kn:
+        names.append(f"dlogits chunk {c} (elementwise, from the stored logits)")
+    elif stored:
+        names.append(f"vocab bwd chunk {c} (dW_out+dHc, 256x256 tiles)")
+        c += 1
+    elif len(names) == 6:
+        names.append("dlogits chunk 0 (128x256 tiles)")
+    else:
+        names.append(f"vocab bwd chunk {c} (dW_out+dHc+dlogits c+1, 256x256 tiles)")
+        c += 1
 names += ["dz (tanh bwd)", "proj_bwd (dW_c + dH_part + dC)", "attn bwd dA + softmax bwd",
           "attn bwd dH_dec + dH_enc"]
 tot = sum(launch[k]["gpu__time_duration.sum"] for k in order)
@@ -69,9 +89,11 @@ want = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second",
         "dram__throughput.avg.pct_of_peak_sustained_elapsed",
         "launch__registers_per_thread", "launch__grid_size"]
 units = r[1]
-lab = ["vocab_fwd (LSE epilogue)", "dlogits chunk 0", "vocab_bwd chunk 0 (dW_out + dHc + dlogits c+1)"]
+lab = (["vocab_fwd (LSE epilogue + fp16 logits store)", "dlogits chunk 0 (elementwise)",
+        "vocab_bwd chunk 0 (dW_out + dHc)"] if stored else
+       ["vocab_fwd (LSE epilogue)", "dlogits chunk 0", "vocab_bwd chunk 0 (dW_out + dHc + dlogits c+1)"])
 out = [f"# ncu --set full, build {tag}, C1 paper config, step 2 of scripts/profile_step.py {note}",
-       f"# cmd: scripts/profile.sh {tag} paper (ncu --set full --clock-control none --import-source on -k regex:gemm_tc)",
+       f"# cmd: scripts/profile.sh {tag} paper (ncu --set full --clock-control none --import-source on -k regex:\"gemm_tc|dlogits_from\")",
        "# dram bytes are cold-cache (ncu flushes caches per replayed pass)"]
 for j, row in enumerate(r[2:]):
     out.append(f"## {lab[j] if j < len(lab) else j}")

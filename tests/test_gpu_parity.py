@@ -86,7 +86,17 @@ def set_modes(binding, mode):
     projection backward, 8 debug entry): "pN" CTA pairs, "mN" B-multicast
     clusters, "wN" wide single-CTA tiles, "xN" mixed wide / 128x256 tiles,
     "cN" B-multicast clusters of wide tiles (the other groups on 128x256
-    single-CTA tiles), "default" the library default (wide vocab backward)."""
+    single-CTA tiles), "default" the library default (wide vocab backward);
+    suffixes "+db" db_out as a ones GEMM, "+sl" / "+sl2" / "+rc" the
+    backward's dlogits from the stored fp16 logits (overlapped / serialised)
+    or recomputed on the tensor cores.  Without a suffix, "default" keeps the
+    library default (stored logits) and the explicit tile modes recompute
+    (they exercise the dlogits GEMM tiles)."""
+    mode, *flags = mode.split("+")
+    binding.attn_softmax_set_option("db_gemm", 1 if "db" in flags else 0)
+    sl = 1 if mode == "default" else 0
+    sl = 1 if "sl" in flags else 2 if "sl2" in flags else 0 if "rc" in flags else sl
+    binding.attn_softmax_set_option("store_logits", sl)
     pair, mcast, wide, mixed, widemc = 8, 0, 2, 0, 0
     if mode != "default":
         mask = int(mode[1:])
@@ -119,7 +129,14 @@ def set_modes(binding, mode):
                                           ("medium", 2048, "x2"), ("medium", 1024, "x15"),
                                           ("odd", 256, "x2"), ("odd", 0, "x15"),
                                           ("small", 0, "c2"), ("medium", 2048, "c15"),
-                                          ("odd", 256, "c2"), ("odd", 0, "c15")])
+                                          ("odd", 256, "c2"), ("odd", 0, "c15"),
+                                          ("tiny_ragged", 0, "default+sl"),
+                                          ("small", 0, "default+sl"), ("small", 1024, "default+sl"),
+                                          ("medium", 0, "default+sl"), ("medium", 2048, "w0+sl"),
+                                          ("odd", 256, "default+sl"), ("edge_min", 0, "default+sl"),
+                                          ("edge_max_src", 256, "p15+sl"),
+                                          ("small", 0, "default+sl2"), ("odd", 256, "default+sl2"),
+                                          ("medium", 0, "default+rc"), ("odd", 0, "default+rc")])
 def test_parity_vs_oracle(cuda_lib, name, vc, mode):
     """mode = GEMM tile modes per group (see set_modes)."""
     from paper_1909_00562_b200 import binding
@@ -197,7 +214,9 @@ def test_parity_general_score(cuda_lib, name, vc, mode):
                                                 ("medium", 1024, "c2", False),
                                                 ("small", 0, "default+db", True),
                                                 ("medium", 2048, "w0+db", False),
-                                                ("odd", 256, "default+db", False)])
+                                                ("odd", 256, "default+db", False),
+                                                ("small", 0, "default+sl", True),
+                                                ("odd", 256, "default+sl+db", False)])
 def test_parity_output_bias(cuda_lib, name, vc, mode, alpha):
     """NEXT-1: the F_c bias b_out of Eq. 5 -- added in the
     forward LSE and the backward dlogits epilogues, db_out = column sums of
@@ -208,14 +227,11 @@ def test_parity_output_bias(cuda_lib, name, vc, mode, alpha):
     cfg = CONFIGS[name]
     inp = make_inputs(cfg, with_alpha=alpha, with_bias=True)
     scale = 1.0 / global_valid_tokens(cfg, cfg.B)
-    mode, _, db = mode.partition("+")
     set_modes(binding, mode)
-    binding.attn_softmax_set_option("db_gemm", 1 if db else 0)
     try:
         g = run_gpu(cfg, inp, scale, vocab_chunk=vc)
     finally:
         set_modes(binding, "default")
-        binding.attn_softmax_set_option("db_gemm", 0)
     f, b = oracle(inp, scale)
     tol = TOL[cfg.dtype]
     assert abs(g["loss"] - f["loss"]) <= tol["loss"] * abs(f["loss"]), (g["loss"], f["loss"])
