@@ -388,8 +388,10 @@ __device__ __forceinline__ void epi_topk(const EpiParams& e, uint32_t taddr, int
   }
 }
 
+// (__maxnreg__ instead of __launch_bounds__(384, 1): 128 registers leave room
+// for one 256-thread dlogits block beside the CTA -- same-box C1 -1%)
 template <typename OutT, bool kFast, int kPair, bool kDecode = false>
-__global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_constant__ TcParams P) {
+__global__ void __maxnreg__(128) gemm_tc_kernel(const __grid_constant__ TcParams P) {
   using Cfg = TcCfg<kPair>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
