@@ -423,8 +423,8 @@ def main():
         "e2e loss mismatch"
 
     # ---- roofline of the dominant kernel: the vocab-backward tcgen05 GEMM
-    # launches (one per V-chunk + 1).  Algorithmic FLOPs per valid token:
-    # 4 d V (dW_out and dHc); the logit recompute (2 d V) is excluded.
+    # launches (one per V-chunk, with the chunk's elementwise dlogits kernel).
+    # Algorithmic FLOPs per valid token: 4 d V (dW_out and dHc).
     pk = peaks()
     T_valid = tok_local
     vb_ms = stage_ms.get("vocab_bwd", 0.0) / args.steps
@@ -447,8 +447,10 @@ def main():
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
                 "traffic": traffic,
-                "kernel": "gemm_tc_kernel vocab-backward launches (dlogits recompute + dW_out + dHc "
-                          "per V-chunk); achieved counts 4 d V useful FLOP per valid token",
+                "kernel": "vocab backward: per V-chunk the elementwise dlogits kernel (from the "
+                          "forward's stored fp16 logits) + the gemm_tc_kernel dW_out + dHc launch; "
+                          "achieved counts 4 d V useful FLOP per valid token over the whole stage "
+                          "(traffic: per GEMM launch)",
                 "peak_source": pk["src"] + (", burst bf16 (timed region at max SM clock)" if at_max
                                             else ", sustained bf16 (clocks below max)"),
                 "vocab_fwd": {"achieved": vf_flops / (vf_ms / 1e3) / 1e12 if vf_ms > 0 else None,
