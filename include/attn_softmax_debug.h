@@ -89,6 +89,9 @@ long long attn_softmax_last_launches(void);
  *                   with an elementwise kernel that starts beside the
  *                   previous chunk's launch; 2 = the same, serialised; 0 =
  *                   recompute the logits chunk by chunk on the tensor cores
+ *   "debug_skip_dlogits" timing only: 1 = skip the elementwise dlogits of
+ *                   chunks >= 1 (gradients WRONG; measures what the overlap
+ *                   could still gain)
  *   "db_gemm"       1 = db_out of the F_c bias as a GEMM against ones inside
  *                   the vocab-backward launches (single-CTA tiles); 0
  *                   (default) = column-sum kernels after each launch

@@ -38,6 +38,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
            "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-o", OUT + ".tmp"]
     cmd += [os.path.join(CSRC, f) for f in SOURCES] + ["-ldl"]
+    cmd += os.environ.get("ATTN_NVCC_EXTRA", "").split()   # development A/B builds only
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -136,6 +136,7 @@ static int g_opt_store_logits = 1;
 // "n_fast": dispatch the vocab-backward GEMMs' column tiles of one row block
 // back to back (their shared A block -- the dlogits chunk -- then leaves HBM once)
 static int g_opt_n_fast = 1;
+static int g_debug_skip_ew = 0;   // "debug_skip_dlogits": timing only -- skip the elementwise dlogits of chunks >= 1 (WRONG gradients)
 static long long* g_trace = nullptr;   // "gemm_trace": device pointer of a per-tile trace buffer
 static long long g_trace_launch = -1;  // "gemm_trace_launch": trace only this launch index of a call (-1 = all)
 static int64_t g_opt_vocab_chunk = 0;
@@ -164,6 +165,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "mixed_tiles")) {
     g_opt_mixed = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "debug_skip_dlogits")) {
+    g_debug_skip_ew = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "n_fast")) {
@@ -1263,7 +1268,13 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
       if ((st = gemm(&g0, 1, 0)) != ATTN_OK) return st;
     }
     for (int c = 0; c < p.nchunks; ++c) {
-      if (p.store_logits && c > 0 && (st = dlogits_ew(c, stream, 4 * sms)) != ATTN_OK) return st;
+      // chunks >= 1 start beside the previous launch: exactly one block per
+      // SM (a finished block waits there for that launch, so a second wave
+      // would only start after it)
+      if (p.store_logits && c > 0 && !g_debug_skip_ew &&
+          (st = dlogits_ew(c, stream, g_opt_store_logits == 1 && g_opt_pdl ? sms : 4 * sms)) !=
+              ATTN_OK)
+        return st;
       GemmDesc gs[4];
       int n = 0;
       gs[n++] = g_dwout(p, b, dW_out, c);   // K = T: the long tiles first

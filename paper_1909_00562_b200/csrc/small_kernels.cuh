@@ -310,9 +310,11 @@ __global__ void __launch_bounds__(512) lens_kernel(const __grid_constant__ LensC
 // forward's fp16 logits, bf16 out (row stride dld); the target column uses
 // the fp32 target logit (as the GEMM epilogue does); 0 on padded rows.
 // Blocks stride over rows; a thread handles 8 columns (16-byte loads and
-// stores), four loads in flight.  256 threads of <= 48 registers: one block
+// stores), four loads in flight.  256 threads of <= 64 registers: one block
 // fits beside a resident persistent GEMM CTA (registers, and the 1 KB of
-// shared memory the SM reserves per block).  wait_first = 0 (chunks
+// shared memory the SM reserves per block); the overlapped chunks launch
+// exactly one block per SM.  (Same-box C1: 6 or 8 loads in flight, or 384
+// threads, were 1-2% slower -- more concurrent traffic slows the GEMM.)  wait_first = 0 (chunks
 // c >= 1, launched as programmatic dependents of launch c-1): the blocks
 // start while launch c-1 still runs and do their work beside it -- every
 // input is older than launch c-1 and the dlogits buffer they write was last
@@ -323,8 +325,16 @@ __device__ __forceinline__ uint32_t bf16x2_bits(float a, float b) {
   __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h2);
 }
-constexpr int kEwThreads = 256;
-__global__ void __launch_bounds__(kEwThreads, 5) dlogits_from_logits_kernel(
+#ifndef ATTN_EW_THREADS
+#define ATTN_EW_THREADS 256
+#endif
+#ifndef ATTN_EW_LOADS
+#define ATTN_EW_LOADS 4
+#endif
+constexpr int kEwThreads = ATTN_EW_THREADS;   // see the block-size note above
+constexpr int kEwLoads = ATTN_EW_LOADS;       // 16-byte loads in flight per thread
+// (min 4 blocks: caps registers at 16384 / threads, what the persistent CTA leaves)
+__global__ void __launch_bounds__(kEwThreads, 4) dlogits_from_logits_kernel(
     const __half* __restrict__ lg, long long lld, int c0, int vcc, int T,
     const float* __restrict__ lse, const float* __restrict__ rowscale, const int* __restrict__ tgt,
     const float* __restrict__ tgt_logit, __nv_bfloat16* __restrict__ dl, long long dld,
@@ -343,16 +353,16 @@ __global__ void __launch_bounds__(kEwThreads, 5) dlogits_from_logits_kernel(
     }
     const __half* l = lg + (long long)row * lld + c0;
     __nv_bfloat16* o = dl + (long long)row * dld;
-    for (int j0 = threadIdx.x; j0 < cols8; j0 += 4 * kEwThreads) {
-      uint4 u[4];
+    for (int j0 = threadIdx.x; j0 < cols8; j0 += kEwLoads * kEwThreads) {
+      uint4 u[kEwLoads];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < kEwLoads; ++k) {
         const int col = (j0 + k * kEwThreads) * 8;
         u[k] = (rs > 0.f && col + 8 <= vcc) ? __ldcs(reinterpret_cast<const uint4*>(l + col))
                                             : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < kEwLoads; ++k) {
         const int col = (j0 + k * kEwThreads) * 8;
         if (col >= vcc) break;
         float g[8];

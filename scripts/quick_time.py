@@ -30,6 +30,8 @@ if os.environ.get("ATTN_SL"):
     binding.attn_softmax_set_option("store_logits", int(os.environ["ATTN_SL"]))
 if os.environ.get("ATTN_NFAST"):
     binding.attn_softmax_set_option("n_fast", int(os.environ["ATTN_NFAST"]))
+if os.environ.get("ATTN_SKIPEW"):
+    binding.attn_softmax_set_option("debug_skip_dlogits", int(os.environ["ATTN_SKIPEW"]))
 if os.environ.get("ATTN_PDL"):
     binding.attn_softmax_set_option("pdl", int(os.environ["ATTN_PDL"]))
 if os.environ.get("ATTN_CTAS"):
