@@ -93,8 +93,10 @@ long long attn_softmax_last_launches(void);
  *                   chunks >= 1 (gradients WRONG; measures what the overlap
  *                   could still gain)
  *   "db_gemm"       1 = db_out of the F_c bias as a GEMM against ones inside
- *                   the vocab-backward launches (single-CTA tiles); 0
- *                   (default) = column-sum kernels after each launch
+ *                   the vocab-backward launches (single-CTA tiles); 0 =
+ *                   column-sum kernels after each launch; -1 (default) = the
+ *                   GEMM when store_logits = 1 (keeps the overlapped chain),
+ *                   else the column sums
  *   "wide_multicast" bitmask (same bits as cta_pair) of GEMM groups run on
  *                   2-CTA clusters of wide 256 x 256 tiles sharing the B tile
  *                   by TMA multicast (512 rows per cluster); wins over

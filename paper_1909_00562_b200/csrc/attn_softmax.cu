@@ -123,10 +123,12 @@ static int g_opt_mixed = 0;
 // "wide_multicast": bitmask of GEMM groups on 2-CTA clusters of wide tiles
 // sharing B (kPair 6); takes precedence over wide_tiles
 static int g_opt_widemc = 0;
-// "db_gemm": db_out as a ones GEMM inside the vocab-backward launches (1) or
-// column-sum kernels after each launch (0, default: same-box A/B at C1 2.34
-// vs 2.37 ms with the bias)
-static int g_opt_db_gemm = 0;
+// "db_gemm": db_out as a ones GEMM inside the vocab-backward launches (1),
+// column-sum kernels after each launch (0), or -1 (default) the GEMM when the
+// dlogits kernels overlap the launches (store_logits = 1: a column-sum launch
+// between them would serialise the chain; C1 2.20 -> see DESIGN), else the
+// column sums (measured faster on the recompute design: 2.34 vs 2.37 ms)
+static int g_opt_db_gemm = -1;
 // "store_logits": the bf16 path's forward vocab GEMM also stores the logits as
 // fp16 [T, V]; the backward turns each V-chunk into dlogits with an
 // elementwise kernel instead of recomputing H_c W_out^T on the tensor cores.
@@ -1241,7 +1243,9 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   {
     // db_out as a GEMM on the tensor cores where the vocab-backward launches
     // run on single CTAs with uniform stages (narrow B tile); else column sums
-    const bool db_gemm = db_out && tc && g_opt_db_gemm && (group_kpair(PAIR_VBWD) == 1 || group_kpair(PAIR_VBWD) == 4);
+    const int db_mode = g_opt_db_gemm >= 0 ? g_opt_db_gemm : (p.store_logits && g_opt_store_logits == 1 ? 1 : 0);
+    const bool db_gemm =
+        db_out && tc && db_mode && (group_kpair(PAIR_VBWD) == 1 || group_kpair(PAIR_VBWD) == 4);
     if (db_gemm) {   // bf16 ones (0x3F80) for the db_out GEMMs
       const long long words = 16 * p.Tld / 2;
       st = launch_pdl(fill_u32_kernel, dim3((unsigned)std::min<long long>(148, (words + 255) / 256)),

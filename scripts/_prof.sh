@@ -1,7 +1,7 @@
-bash scripts/profile.sh r01i paper
-/usr/local/cuda/bin/ncu -i gpurun_out/prof_r01i.ncu-rep --page raw --csv > gpurun_out/prof_r01i_raw.csv 2>/dev/null
-python bench.py > gpurun_out/bench_r01i_paper.json 2> gpurun_out/bench_r01i_paper.err
-python bench.py --config large --no-next --no-cpu-baseline > gpurun_out/bench_r01i_large.json 2> gpurun_out/bench_r01i_large.err
-python bench.py --config long --no-next --no-cpu-baseline > gpurun_out/bench_r01i_long.json 2> gpurun_out/bench_r01i_long.err
-python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_r01i_ref.json 2> gpurun_out/bench_r01i_ref.err
-tail -c 300 gpurun_out/bench_r01i_large.json; tail -c 300 gpurun_out/bench_r01i_long.json
+bash scripts/profile.sh r01j paper
+/usr/local/cuda/bin/ncu -i gpurun_out/prof_r01j.ncu-rep --page raw --csv > gpurun_out/prof_r01j_raw.csv 2>/dev/null
+python bench.py > gpurun_out/bench_r01j_paper.json 2> gpurun_out/bench_r01j_paper.err
+python bench.py --config large --no-next --no-cpu-baseline > gpurun_out/bench_r01j_large.json 2> gpurun_out/bench_r01j_large.err
+python bench.py --config long --no-next --no-cpu-baseline > gpurun_out/bench_r01j_long.json 2> gpurun_out/bench_r01j_long.err
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_r01j_ref.json 2> gpurun_out/bench_r01j_ref.err
+tail -c 300 gpurun_out/bench_r01j_large.json; tail -c 300 gpurun_out/bench_r01j_long.json

@@ -87,13 +87,14 @@ def set_modes(binding, mode):
     clusters, "wN" wide single-CTA tiles, "xN" mixed wide / 128x256 tiles,
     "cN" B-multicast clusters of wide tiles (the other groups on 128x256
     single-CTA tiles), "default" the library default (wide vocab backward);
-    suffixes "+db" db_out as a ones GEMM, "+sl" / "+sl2" / "+rc" the
+    suffixes "+db" / "+cs" db_out as a ones GEMM / column sums (else the
+    library's choice), "+sl" / "+sl2" / "+rc" the
     backward's dlogits from the stored fp16 logits (overlapped / serialised)
     or recomputed on the tensor cores.  Without a suffix, "default" keeps the
     library default (stored logits) and the explicit tile modes recompute
     (they exercise the dlogits GEMM tiles)."""
     mode, *flags = mode.split("+")
-    binding.attn_softmax_set_option("db_gemm", 1 if "db" in flags else 0)
+    binding.attn_softmax_set_option("db_gemm", 1 if "db" in flags else 0 if "cs" in flags else -1)
     sl = 1 if mode == "default" else 0
     sl = 1 if "sl" in flags else 2 if "sl2" in flags else 0 if "rc" in flags else sl
     binding.attn_softmax_set_option("store_logits", sl)
@@ -216,7 +217,9 @@ def test_parity_general_score(cuda_lib, name, vc, mode):
                                                 ("medium", 2048, "w0+db", False),
                                                 ("odd", 256, "default+db", False),
                                                 ("small", 0, "default+sl", True),
-                                                ("odd", 256, "default+sl+db", False)])
+                                                ("odd", 256, "default+sl+db", False),
+                                                ("medium", 0, "default+cs", True),
+                                                ("odd", 0, "default+sl2", False)])
 def test_parity_output_bias(cuda_lib, name, vc, mode, alpha):
     """NEXT-1: the F_c bias b_out of Eq. 5 -- added in the
     forward LSE and the backward dlogits epilogues, db_out = column sums of
