@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -665,6 +666,56 @@ struct Plan {
   size_t total;
 };
 
+// V-chunk width for the stored-logits backward on wide tiles: the balanced
+// width (ceil(V / n) rounded up to 256) for the chunk count n in [2, 24] that
+// minimises a model of the stage -- the persistent scheduler replayed on 148
+// SMs (tiles in dispatch order, each SM takes the next tile when free; a wide
+// tile costs 1024 cycles per 64-deep k-block + 8k epilogue + 1.5k boundary),
+// + 35k cycles per launch (launch, prologue, and the visible share of the
+// overlapped dlogits kernel, fitted), + chunk 0's serialised dlogits kernel
+// (4 B per logit at 6 TB/s).  Its choices match the measured sweeps: C1
+// 12544, C3 20224 (8.54-8.63 ms vs 8.97-9.09 at 10240), C4 10752 (4.78-4.88
+// ms vs 5.10 at the old rule's 5376).  Deterministic in
+// the shape (fixed SM count), so the workspace size does not depend on the
+// device; memoised.
+static long long model_chunk_width(long long T, long long d, long long V) {
+  static std::mutex mu;
+  static long long key[3] = {-1, -1, -1}, memo = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  if (key[0] == T && key[1] == d && key[2] == V) return memo;
+  const long long ntd = (d + 255) / 256, kbT = (T + 63) / 64;
+  const double epi = 8000, bound = 1500, launch = 35000, clk = 1.9e9, bw = 6.0e12;
+  std::vector<double> heap;
+  double best = 1e300;
+  long long best_vc = (V + 255) / 256 * 256;
+  long long prev = -1;
+  for (int n = 2; n <= 24; ++n) {
+    const long long vc = ((V + n - 1) / n + 255) / 256 * 256;
+    if (vc == prev || vc < 256) continue;
+    prev = vc;
+    double total = 0;
+    for (long long c0 = 0; c0 < V; c0 += vc) {
+      const long long vcc = std::min(vc, V - c0);
+      heap.assign(148, 0.0);   // min-heap of SM finish times
+      auto take = [&](double cost) {
+        std::pop_heap(heap.begin(), heap.end(), std::greater<double>());
+        heap.back() += cost;
+        std::push_heap(heap.begin(), heap.end(), std::greater<double>());
+      };
+      const double tw = kbT * 1024.0 + epi + bound;                     // dW_out tile
+      const double th = ((vcc + 63) / 64) * 1024.0 + epi + bound;       // dHc tile
+      for (long long i = 0; i < ((vcc + 255) / 256) * ntd; ++i) take(tw);
+      for (long long i = 0; i < ((T + 255) / 256) * ntd; ++i) take(th);
+      total += *std::max_element(heap.begin(), heap.end()) + launch;
+    }
+    total += (double)std::min(vc, V) * T * 4.0 / bw * clk;
+    if (total < best) { best = total; best_vc = vc; }
+  }
+  key[0] = T; key[1] = d; key[2] = V;
+  memo = best_vc;
+  return best_vc;
+}
+
 static Plan make_plan(const attn_shape_t* s) {
   Plan p;
   p.B = s->batch; p.N = s->tgt_len; p.M = s->src_len; p.d = s->hidden; p.V = s->vocab;
@@ -683,7 +734,9 @@ static Plan make_plan(const attn_shape_t* s) {
     // C1 / C3 / C4)
     vc = ((p.V + 11) / 12 + 255) / 256 * 256;
     vc = std::max(vc, 1024ll);
-    if (p.bf16 && (g_opt_wide & PAIR_VBWD)) {
+    if (p.bf16 && g_opt_store_logits && group_kpair(PAIR_VBWD) == 4) {
+      vc = model_chunk_width(p.T, p.d, p.V);
+    } else if (p.bf16 && (g_opt_wide & PAIR_VBWD)) {
       // wide 256 x 256 tiles: widen the chunk until one launch holds at least
       // two long (dW_out + dHc) tiles per SM of a B200 (148 SMs; a fixed
       // constant so the workspace size does not depend on the device)
