@@ -92,11 +92,11 @@ long long attn_softmax_last_launches(void);
  *   "debug_skip_dlogits" timing only: 1 = skip the elementwise dlogits of
  *                   chunks >= 1 (gradients WRONG; measures what the overlap
  *                   could still gain)
- *   "db_gemm"       1 = db_out of the F_c bias as a GEMM against ones inside
- *                   the vocab-backward launches (single-CTA tiles); 0 =
- *                   column-sum kernels after each launch; -1 (default) = the
- *                   GEMM when store_logits = 1 (keeps the overlapped chain),
- *                   else the column sums
+ *   "db_gemm"       how db_out (F_c bias) is summed: 0 = column-sum kernels
+ *                   after each vocab-backward launch; 1 = a GEMM against ones
+ *                   inside those launches (single-CTA tiles); 2 = by the
+ *                   dlogits kernels (stored logits); -1 (default) = 2 with
+ *                   stored logits, else 0
  *   "wide_multicast" bitmask (same bits as cta_pair) of GEMM groups run on
  *                   2-CTA clusters of wide 256 x 256 tiles sharing the B tile
  *                   by TMA multicast (512 rows per cluster); wins over

@@ -124,12 +124,13 @@ static int g_opt_mixed = 0;
 // "wide_multicast": bitmask of GEMM groups on 2-CTA clusters of wide tiles
 // sharing B (kPair 6); takes precedence over wide_tiles
 static int g_opt_widemc = 0;
-// "db_gemm": db_out as a ones GEMM inside the vocab-backward launches (1),
-// column-sum kernels after each launch (0), or -1 (default) the GEMM when the
-// dlogits kernels overlap the launches (store_logits = 1: a column-sum launch
-// between them would serialise the chain; C1 2.20 -> see DESIGN), else the
-// column sums (measured faster on the recompute design: 2.34 vs 2.37 ms)
+// "db_gemm": how db_out is summed: 0 column-sum kernels after each launch, 1
+// a ones GEMM inside the vocab-backward launches, 2 by the dlogits kernels
+// (stored logits only); -1 (default) = 2 with stored logits, else 0 (a
+// column-sum launch between the overlapped dlogits kernel and the next GEMM
+// launch would serialise the chain; see DESIGN.md for the measurements)
 static int g_opt_db_gemm = -1;
+constexpr int kEwParts = 320;   // row-group partial rows of the dlogits kernels' column sums
 // "store_logits": the bf16 path's forward vocab GEMM also stores the logits as
 // fp16 [T, V]; the backward turns each V-chunk into dlogits with an
 // elementwise kernel instead of recomputing H_c W_out^T on the tensor cores.
@@ -773,7 +774,8 @@ static Plan make_plan(const attn_shape_t* s) {
   p.off_abf = take(p.bf16 ? 2 * p.T * p.Mp : 0);
   p.off_debf = take(p.bf16 ? 2 * p.T * p.Mp : 0);
   p.off_q = take(p.elt * p.T * p.d);   // Eq. 2 general score: Q = H W_alpha
-  p.off_dbpart = take(sizeof(float) * 16 * (size_t)p.Vc);   // F_c bias: column-sum partials
+  p.off_dbpart = take(sizeof(float) * std::max<size_t>(16 * (size_t)p.Vc,   // F_c bias: column-sum partials
+                                                         p.bf16 ? (size_t)kEwParts * p.V : 0));
   p.Tld = (p.T + 7) / 8 * 8;
   p.off_ones = take(p.bf16 ? 2 * 16 * (size_t)p.Tld : 0);   // F_c bias, bf16 path: [16, Tld] ones
   p.store_logits = p.bf16 && g_opt_store_logits;
@@ -1296,9 +1298,11 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   {
     // db_out as a GEMM on the tensor cores where the vocab-backward launches
     // run on single CTAs with uniform stages (narrow B tile); else column sums
-    const int db_mode = g_opt_db_gemm >= 0 ? g_opt_db_gemm : (p.store_logits && g_opt_store_logits == 1 ? 1 : 0);
-    const bool db_gemm =
-        db_out && tc && db_mode && (group_kpair(PAIR_VBWD) == 1 || group_kpair(PAIR_VBWD) == 4);
+    const int db_mode = g_opt_db_gemm >= 0 ? g_opt_db_gemm : (p.store_logits ? 2 : 0);
+    const bool db_gemm = db_out && tc && db_mode == 1 &&
+                         (group_kpair(PAIR_VBWD) == 1 || group_kpair(PAIR_VBWD) == 4);
+    const bool db_ew = db_out && p.store_logits && db_mode == 2;
+    int ew_parts0 = 0, ew_parts = 0;   // db_ew: row groups of chunk 0 / the later chunks
     if (db_gemm) {   // bf16 ones (0x3F80) for the db_out GEMMs
       const long long words = 16 * p.Tld / 2;
       st = launch_pdl(fill_u32_kernel, dim3((unsigned)std::min<long long>(148, (words + 255) / 256)),
@@ -1308,6 +1312,21 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
     // dlogits of chunk c from the stored logits (on `s`, `blocks` blocks)
     auto dlogits_ew = [&](int c, cudaStream_t s, int blocks) -> attn_status_t {
       const int c0 = c * p.Vc, vcc = std::min(p.Vc, p.V - c0);
+      if (db_ew) {   // + column sums: column slabs x row groups, ~`blocks` blocks
+        // (the row-group count depends on the full chunk width only, so every
+        // chunk after the first has the same number of partial rows)
+        const int slabs = (vcc + 8 * kEwThreads - 1) / (8 * kEwThreads);
+        const int full_slabs = (std::min(p.Vc, p.V) + 8 * kEwThreads - 1) / (8 * kEwThreads);
+        const int groups = (int)std::min<long long>(
+            TT, std::max(1, std::min(kEwParts, blocks / full_slabs)));
+        (c == 0 ? ew_parts0 : ew_parts) = groups;
+        return launch_pdl(dlogits_colsum_kernel, dim3((unsigned)groups, (unsigned)slabs),
+                          dim3(kEwThreads), s, (const __half*)b.logits, p.Vld, c0, vcc, (int)TT,
+                          (const float*)b.lse, (const float*)b.rowscale, tgt_ids,
+                          (const float*)b.tgt_logit, (__nv_bfloat16*)b.dl[c & 1], (long long)p.Vc,
+                          b.dbpart, (long long)p.V,
+                          (c == 0 || !g_opt_pdl || g_opt_store_logits == 2) ? 1 : 0);
+      }
       return launch_pdl(dlogits_from_logits_kernel,
                         dim3((unsigned)std::min<long long>(TT, blocks)), dim3(kEwThreads), s,
                         (const __half*)b.logits, p.Vld, c0, vcc, (int)TT, (const float*)b.lse,
@@ -1340,7 +1359,7 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
       if (c + 1 < p.nchunks && !p.store_logits)
         gs[n++] = g_dlogits(p, b, W_out, tgt_ids, c + 1, b_out);
       if ((st = gemm(gs, n, PAIR_VBWD)) != ATTN_OK) return st;
-      if (db_out && !db_gemm) {
+      if (db_out && !db_gemm && !db_ew) {
         // F_c bias: db_out[chunk c] = column sums of dlogits_c (still intact:
         // the next launch is the one that overwrites its buffer)
         const int c0 = c * p.Vc, vcc = std::min(p.Vc, p.V - c0);
@@ -1361,6 +1380,12 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
           return st;
         reserve = comm_max_ctas(comm);
       }
+    }
+    if (db_ew) {   // db_out = the dlogits kernels' row-group partials, added in order
+      st = launch_pdl(ew_colsum_final_kernel, dim3((unsigned)((p.V + 255) / 256)), dim3(256), stream,
+                      (const float*)b.dbpart, ew_parts0, std::min(p.Vc, p.V),
+                      p.nchunks > 1 ? ew_parts : ew_parts0, p.V, db_out);
+      if (st != ATTN_OK) return st;
     }
   }
   // tanh backward of Eq. 4: dz = dHc (1 - H_c^2)

@@ -401,6 +401,103 @@ __global__ void __launch_bounds__(kEwThreads, 4) dlogits_from_logits_kernel(
   if (!wait_first) pdl_wait();
 }
 
+// The same dlogits plus the F_c bias's column sums (db_out): a 2D grid,
+// blockIdx.y = a slab of kEwThreads x 8 columns (one 8-column group per
+// thread), blockIdx.x = a row group (rows blockIdx.x, + gridDim.x, ...,
+// three in flight).  Each thread sums its 8 columns' fp32 dlogits down its
+// rows in a fixed order into dbpart[blockIdx.x][c0 + col] (row stride pld);
+// ew_colsum_final_kernel adds the row groups in order -- deterministic, and
+// no column-sum launch breaks the overlapped chain.
+__global__ void __launch_bounds__(kEwThreads, 4) dlogits_colsum_kernel(
+    const __half* __restrict__ lg, long long lld, int c0, int vcc, int T,
+    const float* __restrict__ lse, const float* __restrict__ rowscale, const int* __restrict__ tgt,
+    const float* __restrict__ tgt_logit, __nv_bfloat16* __restrict__ dl, long long dld,
+    float* __restrict__ dbpart, long long pld, int wait_first) {
+  if (wait_first) pdl_wait();
+  constexpr int kR = 3;
+  const int j = blockIdx.y * kEwThreads + threadIdx.x;
+  const int col = j * 8;
+  if (col < vcc) {
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+    for (int row0 = blockIdx.x; row0 < T; row0 += kR * gridDim.x) {
+      uint4 u[kR];
+      float rs[kR], c2[kR];
+#pragma unroll
+      for (int k = 0; k < kR; ++k) {
+        const int row = row0 + k * (int)gridDim.x;
+        rs[k] = row < T ? rowscale[row] : 0.f;
+        c2[k] = rs[k] > 0.f ? __log2f(rs[k]) - lse[row] * kLog2e : 0.f;
+        u[k] = (rs[k] > 0.f && col + 8 <= vcc)
+                   ? __ldcs(reinterpret_cast<const uint4*>(lg + (long long)row * lld + c0 + col))
+                   : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < kR; ++k) {
+        const int row = row0 + k * (int)gridDim.x;
+        if (row >= T) break;
+        float g[8];
+        if (rs[k] > 0.f) {
+          if (col + 8 <= vcc) {
+            const uint32_t w[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+              g[2 * e] = ex2_mufu(fmaf(f.x, kLog2e, c2[k]));
+              g[2 * e + 1] = ex2_mufu(fmaf(f.y, kLog2e, c2[k]));
+            }
+          } else {
+            const __half* l = lg + (long long)row * lld + c0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              g[e] = col + e < vcc ? ex2_mufu(fmaf(__half2float(l[col + e]), kLog2e, c2[k])) : 0.f;
+          }
+          const int yl = tgt[row] - c0 - col;
+          if ((unsigned)yl < 8u) {
+            const float fix = rs[k] * (__expf(tgt_logit[row] - lse[row]) - 1.f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (e == yl) g[e] = fix;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) g[e] = 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += g[e];
+        __nv_bfloat16* o = dl + (long long)row * dld;
+        if (col + 8 <= vcc) {
+          *reinterpret_cast<uint4*>(o + col) =
+              make_uint4(bf16x2_bits(g[0], g[1]), bf16x2_bits(g[2], g[3]),
+                         bf16x2_bits(g[4], g[5]), bf16x2_bits(g[6], g[7]));
+        } else {
+          for (int e = 0; e < 8 && col + e < vcc; ++e) o[col + e] = __float2bfloat16_rn(g[e]);
+        }
+      }
+    }
+    float* pp = dbpart + (long long)blockIdx.x * pld + c0 + col;
+    for (int e = 0; e < 8 && col + e < vcc; ++e) pp[e] = acc[e];
+  }
+  if (!wait_first) pdl_wait();
+}
+
+// db_out from the dlogits kernels' row-group partials part[y][c] (row stride
+// ncols): columns < first_cols have n_first partial rows, the rest n_rest;
+// added in row order
+__global__ void __launch_bounds__(256) ew_colsum_final_kernel(const float* __restrict__ part,
+                                                              int n_first, int first_cols,
+                                                              int n_rest, int ncols,
+                                                              float* __restrict__ db) {
+  pdl_wait();
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= ncols) return;
+  const int n = c < first_cols ? n_first : n_rest;
+  float t = 0.f;
+  for (int y = 0; y < n; ++y) t += part[(long long)y * ncols + c];
+  db[c] = t;
+}
+
 // fill n 32-bit words with v (the ones operand of the db_out GEMM)
 __global__ void __launch_bounds__(256) fill_u32_kernel(uint32_t* __restrict__ p, long long n,
                                                        uint32_t v) {

@@ -87,14 +87,15 @@ def set_modes(binding, mode):
     clusters, "wN" wide single-CTA tiles, "xN" mixed wide / 128x256 tiles,
     "cN" B-multicast clusters of wide tiles (the other groups on 128x256
     single-CTA tiles), "default" the library default (wide vocab backward);
-    suffixes "+db" / "+cs" db_out as a ones GEMM / column sums (else the
-    library's choice), "+sl" / "+sl2" / "+rc" the
+    suffixes "+db" / "+cs" / "+ew" db_out as a ones GEMM / column-sum
+    kernels / the dlogits kernels' sums (else the library's choice), "+sl" / "+sl2" / "+rc" the
     backward's dlogits from the stored fp16 logits (overlapped / serialised)
     or recomputed on the tensor cores.  Without a suffix, "default" keeps the
     library default (stored logits) and the explicit tile modes recompute
     (they exercise the dlogits GEMM tiles)."""
     mode, *flags = mode.split("+")
-    binding.attn_softmax_set_option("db_gemm", 1 if "db" in flags else 0 if "cs" in flags else -1)
+    binding.attn_softmax_set_option(
+        "db_gemm", 1 if "db" in flags else 0 if "cs" in flags else 2 if "ew" in flags else -1)
     sl = 1 if mode == "default" else 0
     sl = 1 if "sl" in flags else 2 if "sl2" in flags else 0 if "rc" in flags else sl
     binding.attn_softmax_set_option("store_logits", sl)
@@ -219,7 +220,9 @@ def test_parity_general_score(cuda_lib, name, vc, mode):
                                                 ("small", 0, "default+sl", True),
                                                 ("odd", 256, "default+sl+db", False),
                                                 ("medium", 0, "default+cs", True),
-                                                ("odd", 0, "default+sl2", False)])
+                                                ("odd", 0, "default+sl2", False),
+                                                ("tiny_ragged", 0, "default+ew", False),
+                                                ("medium", 2048, "default+ew", True)])
 def test_parity_output_bias(cuda_lib, name, vc, mode, alpha):
     """NEXT-1: the F_c bias b_out of Eq. 5 -- added in the
     forward LSE and the backward dlogits epilogues, db_out = column sums of
