@@ -14,6 +14,7 @@ if len(sys.argv) > 2:
 wide = int(os.environ.get("ATTN_WIDE", "0"))
 binding.attn_softmax_set_option("wide_tiles", wide)
 binding.attn_softmax_set_option("mixed_tiles", int(os.environ.get("ATTN_MIXED", "0")))
+binding.attn_softmax_set_option("store_logits", int(os.environ.get("ATTN_SL", "1")))
 cfg = CONFIGS["paper"]
 inp = make_inputs(cfg)
 st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
@@ -30,7 +31,10 @@ st(*args, out=out)
 torch.cuda.synchronize()
 binding.attn_softmax_set_option("gemm_trace", 0)
 t = tr.view(-1, 16).cpu().numpy()
-n = int(np.max(np.nonzero(t[:, 4])[0])) + 1
+nz = np.nonzero(t[:, 4])[0]
+if len(nz) == 0:
+    sys.exit(f"launch {idx}: no tcgen05 tiles traced")
+n = int(np.max(nz)) + 1
 t = t[:n]
 kinds = sys.argv[3].split(",") if len(sys.argv) > 3 else None
 span = t[:, 5] - t[:, 4]
