@@ -87,10 +87,8 @@ long long attn_softmax_last_launches(void);
  *                   the logits as fp16 [T, V] (workspace grows by 2 T V bytes)
  *                   and the backward makes each V-chunk's dlogits from them
  *                   with an elementwise kernel that starts beside the
- *                   previous chunk's launch; 2 = the same, serialised; 3 =
- *                   done by the previous launch's epilogue warps while they
- *                   wait for accumulators (slower); 0 = recompute the logits
- *                   chunk by chunk on the tensor cores
+ *                   previous chunk's launch; 2 = the same, serialised; 0 =
+ *                   recompute the logits chunk by chunk on the tensor cores
  *   "debug_skip_dlogits" timing only: 1 = skip the elementwise dlogits of
  *                   chunks >= 1 (gradients WRONG; measures what the overlap
  *                   could still gain)

@@ -135,15 +135,12 @@ constexpr int kEwParts = 320;   // row-group partial rows of the dlogits kernels
 // fp16 [T, V]; the backward turns each V-chunk into dlogits with an
 // elementwise kernel instead of recomputing H_c W_out^T on the tensor cores.
 // 1 (default): chunk c+1's kernel starts beside launch c (PDL, waits at its
-// end); 2: serialised; 3: chunk c+1's dlogits done by launch c's epilogue
-// warps between accumulator waits; 0: recompute (same-box A/B at C1: 1.76 /
-// 1.90 / 1.82 / 2.15 ms)
+// end); 2: serialised; 0: recompute (same-box A/B at C1: 1.92 / 1.98 / 2.15 ms)
 static int g_opt_store_logits = 1;
 // "n_fast": dispatch the vocab-backward GEMMs' column tiles of one row block
 // back to back (their shared A block -- the dlogits chunk -- then leaves HBM once)
 static int g_opt_n_fast = 1;
 static int g_debug_skip_ew = 0;   // "debug_skip_dlogits": timing only -- skip the elementwise dlogits of chunks >= 1 (WRONG gradients)
-static TcEw g_next_ew{};   // elementwise work of the next tcgen05 launch (store_logits = 3)
 static long long* g_trace = nullptr;   // "gemm_trace": device pointer of a per-tile trace buffer
 static long long g_trace_launch = -1;  // "gemm_trace_launch": trace only this launch index of a call (-1 = all)
 static int64_t g_opt_vocab_chunk = 0;
@@ -509,7 +506,6 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
     tiles += P.prob[i].tiles_m * P.prob[i].tiles_n * P.prob[i].batch;
   }
   P.nprob = n;
-  P.ew = g_next_ew;
   P.total_tiles = tiles;
   P.tile_counter = counter;
   P.trace = (g_trace_launch < 0 || g_trace_launch == g_launches) ? g_trace : nullptr;
@@ -1351,20 +1347,10 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
       // chunks >= 1 start beside the previous launch: exactly one block per
       // SM (a finished block waits there for that launch, so a second wave
       // would only start after it)
-      // store_logits = 3: chunk c+1's dlogits are done by launch c's
-      // epilogue warps while they wait for accumulators
-      const bool ew_fused = p.store_logits && g_opt_store_logits == 3 && !db_ew;
-      if (p.store_logits && c > 0 && !g_debug_skip_ew && !ew_fused &&
+      if (p.store_logits && c > 0 && !g_debug_skip_ew &&
           (st = dlogits_ew(c, stream, g_opt_store_logits == 1 && g_opt_pdl ? sms : 4 * sms)) !=
               ATTN_OK)
         return st;
-      if (ew_fused && c + 1 < p.nchunks) {
-        const int c1 = (c + 1) * p.Vc;
-        g_next_ew = TcEw{(const __half*)b.logits, p.Vld, c1, std::min(p.Vc, p.V - c1), (int)TT, 1,
-                         (const float*)b.lse, (const float*)b.rowscale, tgt_ids,
-                         (const float*)b.tgt_logit, (__nv_bfloat16*)b.dl[(c + 1) & 1],
-                         (long long)p.Vc};
-      }
       GemmDesc gs[4];
       int n = 0;
       gs[n++] = g_dwout(p, b, dW_out, c);   // K = T: the long tiles first
@@ -1372,9 +1358,7 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
       gs[n++] = g_dhc(p, b, W_out, c);
       if (c + 1 < p.nchunks && !p.store_logits)
         gs[n++] = g_dlogits(p, b, W_out, tgt_ids, c + 1, b_out);
-      st = gemm(gs, n, PAIR_VBWD);
-      g_next_ew.on = 0;
-      if (st != ATTN_OK) return st;
+      if ((st = gemm(gs, n, PAIR_VBWD)) != ATTN_OK) return st;
       if (db_out && !db_gemm && !db_ew) {
         // F_c bias: db_out[chunk c] = column sums of dlogits_c (still intact:
         // the next launch is the one that overwrites its buffer)

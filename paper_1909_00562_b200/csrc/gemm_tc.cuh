@@ -107,25 +107,9 @@ struct TcProblem {
   EpiParams epi;
 };
 
-// Elementwise work the epilogue warps do while they wait for an accumulator
-// (option store_logits = 3): the next V-chunk's dlogits from the stored fp16
-// logits, rows statically interleaved over all epilogue warps of the grid.
-struct TcEw {
-  const __half* lg;
-  long long lld;
-  int c0, vcc, T, on;
-  const float* lse;
-  const float* rowscale;
-  const int* tgt;
-  const float* tgt_logit;
-  __nv_bfloat16* dl;
-  long long dld;
-};
-
 struct alignas(64) TcParams {
   CUtensorMap maps[kMaxProblems][5];  // a0, a1, b0, b1, out
   TcProblem prob[kMaxProblems];
-  TcEw ew;
   int nprob;
   int total_tiles;
   int* tile_counter;
@@ -406,74 +390,6 @@ __device__ __forceinline__ void epi_topk(const EpiParams& e, uint32_t taddr, int
 
 // (__maxnreg__ instead of __launch_bounds__(384, 1): 128 registers leave room
 // for one 256-thread dlogits block beside the CTA -- same-box C1 -1%)
-// One step of the epilogue warps' elementwise work: 1024 columns (four
-// 16-byte fp16 loads per lane in flight) of row `r`; advances (r, j).
-__device__ __noinline__ void tc_ew_step(const TcEw& e, int& r, int& j, int stride, uint32_t lane) {
-  const int row = r;
-  const float rs = e.rowscale[row];
-  __nv_bfloat16* o = e.dl + (long long)row * e.dld;
-  const __half* l = e.lg + (long long)row * e.lld + e.c0;
-  float c2 = 0.f, fix = 0.f;
-  int y = -1;
-  if (rs > 0.f) {
-    const float ls = e.lse[row];
-    c2 = __log2f(rs) - ls * kLog2e;
-    y = e.tgt[row] - e.c0;
-    fix = rs * (__expf(e.tgt_logit[row] - ls) - 1.f);
-  }
-  uint4 u[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int col = (j + (int)lane + 32 * k) * 8;
-    u[k] = (rs > 0.f && col + 8 <= e.vcc) ? __ldcs(reinterpret_cast<const uint4*>(l + col))
-                                          : make_uint4(0, 0, 0, 0);
-  }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int col = (j + (int)lane + 32 * k) * 8;
-    if (col >= e.vcc) break;
-    float g[8];
-    if (rs > 0.f) {
-      if (col + 8 <= e.vcc) {
-        const uint32_t w[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[q]));
-          g[2 * q] = ex2_mufu(fmaf(f.x, kLog2e, c2));
-          g[2 * q + 1] = ex2_mufu(fmaf(f.y, kLog2e, c2));
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          g[q] = col + q < e.vcc ? ex2_mufu(fmaf(__half2float(l[col + q]), kLog2e, c2)) : 0.f;
-      }
-      const int yl = y - col;
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q == yl) g[q] = fix;
-    } else {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) g[q] = 0.f;
-    }
-    if (col + 8 <= e.vcc) {
-      uint32_t w[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(g[2 * q], g[2 * q + 1]);
-        w[q] = *reinterpret_cast<uint32_t*>(&h2);
-      }
-      *reinterpret_cast<uint4*>(o + col) = make_uint4(w[0], w[1], w[2], w[3]);
-    } else {
-      for (int q = 0; q < 8 && col + q < e.vcc; ++q) o[col + q] = __float2bfloat16_rn(g[q]);
-    }
-  }
-  j += 128;
-  if (j * 8 >= e.vcc) {
-    j = 0;
-    r += stride;
-  }
-}
-
 template <typename OutT, bool kFast, int kPair, bool kDecode = false>
 __global__ void __maxnreg__(128) gemm_tc_kernel(const __grid_constant__ TcParams P) {
   using Cfg = TcCfg<kPair>;
@@ -852,9 +768,6 @@ __global__ void __maxnreg__(128) gemm_tc_kernel(const __grid_constant__ TcParams
     int acc = 0;
     uint32_t aph = 0;
     uint32_t esph = 0;   // kVar: phase bit of each TMEM accumulator slot
-    // elementwise work (P.ew): rows blockIdx.x * 8 + ew, + gridDim.x * 8, ...
-    const int ew_stride = (int)gridDim.x * TC_EPI_WARPS;
-    int ew_r = (int)(blockIdx.x * TC_EPI_WARPS + ew), ew_j = 0;
     for (;;) {
       if (kClu && !leader) mbar_wait_cluster(&sfull[r], rph);
       else mbar_wait(&sfull[r], rph);
@@ -871,8 +784,6 @@ __global__ void __maxnreg__(128) gemm_tc_kernel(const __grid_constant__ TcParams
       const int kind = pr.epi.kind;
       const CUtensorMap* omap = &P.maps[tl.p][4];
       if constexpr (!kVar) {
-        if (P.ew.on)   // fill the wait with elementwise steps
-          while (ew_r < P.ew.T && !mbar_test(&tfull[acc], aph)) tc_ew_step(P.ew, ew_r, ew_j, ew_stride, lane);
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
       }
@@ -1018,8 +929,6 @@ __global__ void __maxnreg__(128) gemm_tc_kernel(const __grid_constant__ TcParams
       }
       if (warp == 0 && leader) TC_TRACE(t, 7);
     }
-    if (P.ew.on)   // the rest of this warp's elementwise rows
-      while (ew_r < P.ew.T) tc_ew_step(P.ew, ew_r, ew_j, ew_stride, lane);
     if (lane == 0) bulk_wait0();
   }
   tc_fence_before();

@@ -97,8 +97,7 @@ def set_modes(binding, mode):
     binding.attn_softmax_set_option(
         "db_gemm", 1 if "db" in flags else 0 if "cs" in flags else 2 if "ew" in flags else -1)
     sl = 1 if mode == "default" else 0
-    sl = (1 if "sl" in flags else 2 if "sl2" in flags else 3 if "sl3" in flags
-          else 0 if "rc" in flags else sl)
+    sl = 1 if "sl" in flags else 2 if "sl2" in flags else 0 if "rc" in flags else sl
     binding.attn_softmax_set_option("store_logits", sl)
     pair, mcast, wide, mixed, widemc = 8, 0, 2, 0, 0
     if mode != "default":
@@ -139,9 +138,7 @@ def set_modes(binding, mode):
                                           ("odd", 256, "default+sl"), ("edge_min", 0, "default+sl"),
                                           ("edge_max_src", 256, "p15+sl"),
                                           ("small", 0, "default+sl2"), ("odd", 256, "default+sl2"),
-                                          ("medium", 0, "default+rc"), ("odd", 0, "default+rc"),
-                                          ("small", 0, "default+sl3"), ("medium", 1024, "default+sl3"),
-                                          ("odd", 256, "default+sl3")])
+                                          ("medium", 0, "default+rc"), ("odd", 0, "default+rc")])
 def test_parity_vs_oracle(cuda_lib, name, vc, mode):
     """mode = GEMM tile modes per group (see set_modes)."""
     from paper_1909_00562_b200 import binding
