@@ -31,6 +31,7 @@
 #include "gemm_simt.cuh"
 #include "gemm_tc.cuh"
 #include "small_kernels.cuh"
+#include "vocab_bwd.cuh"
 
 using namespace attnsm;
 
@@ -136,7 +137,27 @@ constexpr int kEwParts = 320;   // row-group partial rows of the dlogits kernels
 // elementwise kernel instead of recomputing H_c W_out^T on the tensor cores.
 // 1 (default): chunk c+1's kernel starts beside launch c (PDL, waits at its
 // end); 2: serialised; 0: recompute (same-box A/B at C1: 1.92 / 1.98 / 2.15 ms)
-static int g_opt_store_logits = 1;
+static int g_opt_store_logits = 0;
+// "vocab_bwd_persistent": 1 (default) = the bf16 vocab backward (recomputed
+// logits) as ONE persistent launch with dependency counters (vocab_bwd.cuh);
+// 0 = one GEMM launch per V-chunk (round-1 design, kept for A/B)
+static int g_opt_vb = 1;
+// "dl_budget_mb": bytes of the dL chunk scratch (all NB buffers) the V-chunk
+// width is sized to, so it stays L2-resident; "dl_buffers": NB
+static int64_t g_opt_dl_budget_mb = 96;
+static int g_opt_dl_nbuf = 3;
+// "vb_last_g2_first": last block of the persistent backward dispatches the
+// long dW_out tiles before the dHc tiles (shorter tail)
+static int g_opt_vb_g2first = 1;
+static long long* g_vb_trace = nullptr;   // "vb_trace": device buffer, 32 int64 per tile
+// "vb_pair": the persistent vocab backward on CTA pairs (cta_group::2, 256 x 256 tiles)
+static int g_opt_vb_pair = 1;
+// "vb_order": dispatch blocks of the persistent vocab backward: 0 = [G3(c),
+// G2(c), G1(c+1)]; 1 = [G1(c+1), G3(c), G2(c)] (chunk c's consumers run a
+// whole G1 set after its producers; needs dl_buffers >= 3)
+static int g_opt_vb_order = 1;
+static int g_vb_debug = 0;
+static int g_opt_vb_l2 = 3;   // "vb_l2hints": VbParams::l2hints   // "vb_debug": timing experiments (vocab_bwd.cuh VbParams::debug)
 // "n_fast": dispatch the vocab-backward GEMMs' column tiles of one row block
 // back to back (their shared A block -- the dlogits chunk -- then leaves HBM once)
 static int g_opt_n_fast = 1;
@@ -177,6 +198,44 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "n_fast")) {
     g_opt_n_fast = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "vocab_bwd_persistent")) {
+    g_opt_vb = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "dl_budget_mb")) {
+    if (value < 1) return fail(ATTN_ERR_INVALID_ARG, "dl_budget_mb must be >= 1");
+    g_opt_dl_budget_mb = value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "dl_buffers")) {
+    if (value < 1 || value > 4) return fail(ATTN_ERR_INVALID_ARG, "dl_buffers must be in [1, 4]");
+    g_opt_dl_nbuf = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "vb_l2hints")) {
+    g_opt_vb_l2 = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "vb_debug")) {
+    g_vb_debug = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "vb_order")) {
+    g_opt_vb_order = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "vb_pair")) {
+    g_opt_vb_pair = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "vb_trace")) {
+    g_vb_trace = reinterpret_cast<long long*>(value);
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "vb_last_g2_first")) {
+    g_opt_vb_g2first = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "store_logits")) {
@@ -663,6 +722,9 @@ struct Plan {
   int ald;            // row stride of the fp32 alpha stash (bf16 path: Mp, for TMA stores)
   long long Tld;      // row stride of the ones operand of the db_out GEMM (8-multiple >= T)
   bool store_logits;  // bf16 path, option store_logits: fp16 logits [T, Vld] in the workspace
+  bool vb;            // bf16 path: persistent vocab backward (vocab_bwd.cuh)
+  int nbuf;           // dL chunk buffers
+  size_t off_vbctr, n_vbctr;   // its dependency counters (unsigned), zeroed per call
   long long Vld;
   size_t total;
 };
@@ -746,9 +808,18 @@ static Plan make_plan(const attn_shape_t* s) {
       if (need > 0) vc = std::max(vc, need * 256);
     }
   }
+  p.store_logits = p.bf16 && g_opt_store_logits;
+  p.vb = p.bf16 && !p.store_logits && g_opt_vb;
+  p.nbuf = p.vb ? g_opt_dl_nbuf : 2;
+  if (p.vb && g_opt_vocab_chunk <= 0) {
+    // the NB dL buffers [T, Vc] bf16 fit the L2 budget
+    vc = (g_opt_dl_budget_mb << 20) / ((long long)p.nbuf * p.T * 2) / 256 * 256;
+    vc = std::max(vc, 256ll);
+  }
   vc = std::min(vc, vpad);
   // one tile counter per tcgen05 launch: keep the chunk count well inside
   while ((p.V + vc - 1) / vc > kNumCounters - 64) vc += 256;
+  while (p.vb && (p.V + vc - 1) / vc > VB_MAX_BLOCKS - 1) vc += 256;
   p.Vc = (int)vc;
   p.nchunks = (int)((p.V + p.Vc - 1) / p.Vc);
   size_t o = 0;
@@ -767,7 +838,7 @@ static Plan make_plan(const attn_shape_t* s) {
   p.off_lse = take(sizeof(float) * p.T);
   p.off_nll = take(sizeof(float) * p.T);
   p.off_rowscale = take(sizeof(float) * p.T);
-  p.off_dl = take(2 * p.elt * p.T * (size_t)p.Vc);
+  p.off_dl = take((size_t)std::max(2, p.nbuf) * p.elt * p.T * (size_t)p.Vc);
   p.off_dhc = take(sizeof(float) * p.T * p.d);
   p.off_dz = take(p.elt * p.T * p.d);
   p.off_dhc2 = take(sizeof(float) * p.T * 2 * p.d);
@@ -778,9 +849,14 @@ static Plan make_plan(const attn_shape_t* s) {
                                                          p.bf16 ? (size_t)kEwParts * p.V : 0));
   p.Tld = (p.T + 7) / 8 * 8;
   p.off_ones = take(p.bf16 ? 2 * 16 * (size_t)p.Tld : 0);   // F_c bias, bf16 path: [16, Tld] ones
-  p.store_logits = p.bf16 && g_opt_store_logits;
   p.Vld = (p.V + 7) / 8 * 8;
   p.off_logits = take(p.store_logits ? 2 * (size_t)p.T * p.Vld : 0);
+  {   // counters of the persistent vocab backward (sized for single-CTA tiles, the larger)
+    const size_t nrb = (p.T + 127) / 128, ndt = (p.d + VB_BN - 1) / VB_BN;
+    const size_t ncolf = p.Vc / VB_BN;
+    p.n_vbctr = p.vb ? 1 + p.nchunks * (nrb + ncolf + 2) + nrb * ndt : 0;
+    p.off_vbctr = take(sizeof(unsigned) * p.n_vbctr);
+  }
   p.total = o;
   return p;
 }
@@ -901,6 +977,7 @@ struct Bufs {
   float* dbpart;   // F_c bias: [16, Vc] column-sum partials (when not a GEMM)
   void* ones;      // F_c bias, bf16 path: [16, Tld] bf16 ones (B operand of the db_out GEMM)
   void* logits;    // option store_logits: fp16 [T, Vld]
+  unsigned* vbctr; // persistent vocab backward: tile counter + dependency counters
   void* q;    // Eq. 2 general score: Q = H W_alpha [T, d] (dtype)
   void* dq;   // its gradient [T, d] (dtype); aliases dz, which is dead by then
 };
@@ -934,6 +1011,7 @@ static Bufs carve(const Plan& p, void* ws) {
   b.dbpart = (float*)(w + p.off_dbpart);
   b.ones = w + p.off_ones;
   b.logits = p.store_logits ? w + p.off_logits : nullptr;
+  b.vbctr = (unsigned*)(w + p.off_vbctr);
   b.dq = b.dz;
   return b;
 }
@@ -1218,6 +1296,184 @@ static attn_status_t attention_backward_tc(const Plan& p, const void* H, const v
   return launch_tc_group<__nv_bfloat16>(ga, 2, next(ctx_), stream, PAIR_PBWD);
 }
 
+// ---------------------------------------------------------------- persistent vocab backward
+// Per-device "max dynamic shared memory" attribute of a kernel (set once per
+// device, under a lock: the attribute belongs to the device's context).
+template <typename K>
+static attn_status_t ensure_smem_attr(K kernel, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;   // (kernel, device)
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  const void* key = reinterpret_cast<const void*>(kernel);
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : done)
+    if (e.first == key && e.second == dev) return ATTN_OK;
+  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.emplace_back(key, dev);
+  return ATTN_OK;
+}
+
+// B1 as one launch (vocab_bwd.cuh): tensor maps, dispatch blocks, counters.
+// Counter layout in `ctr` (zeroed by the caller): [0] tile counter, then
+// rowdone [nchunks][nrb], coldone [nchunks][ncolf], consumed [nchunks],
+// g2done [nchunks], dhcdone [nrb][ndt] (vb_ctr_layout).
+struct VbLayout {
+  int TM, nrb, ndt, ncolf;
+  size_t rowdone, coldone, consumed, g2done, dhcdone, total;
+};
+static VbLayout vb_ctr_layout(const Plan& p, bool pair) {
+  VbLayout L;
+  L.TM = pair ? 256 : 128;
+  L.nrb = (int)((p.T + L.TM - 1) / L.TM);
+  L.ndt = (p.d + VB_BN - 1) / VB_BN;
+  L.ncolf = p.Vc / VB_BN;
+  const size_t nch = p.nchunks;
+  L.rowdone = 1;
+  L.coldone = L.rowdone + nch * L.nrb;
+  L.consumed = L.coldone + nch * L.ncolf;
+  L.g2done = L.consumed + nch;
+  L.dhcdone = L.g2done + nch;
+  L.total = L.dhcdone + (size_t)L.nrb * L.ndt;
+  return L;
+}
+
+template <bool kPair>
+static attn_status_t launch_vocab_bwd_k(const Plan& p, const void* hc, const void* W_out, void* dl,
+                                        float* dhc, float* dW_out, const float* lse,
+                                        const float* rowscale, const int* tgt,
+                                        const float* tgt_logit, const void* bias, unsigned* ctr,
+                                        int ctas, cudaStream_t stream) {
+  using Cfg = VbCfg<kPair>;
+  attn_status_t st;
+  if ((st = ensure_smem_attr(vocab_bwd_kernel<kPair>, VB_SMEM_BYTES)) != ATTN_OK) return st;
+  static VbParams P;   // large (blk_start): filled per call under the lock
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  memset(&P, 0, sizeof(P));
+  const long long T = p.T, d = p.d, V = p.V, Vc = p.Vc, NB = p.nbuf;
+  const cuuint32_t brows = Cfg::B_ROWS;
+  {   // H_c [T, d]: K-major A of G1
+    cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)T, 1};
+    cuuint64_t str[2] = {(cuuint64_t)(d * 2), (cuuint64_t)(T * d * 2)};
+    cuuint32_t box[3] = {64, 128, 1};
+    if ((st = encode(&P.m_hc_k, hc, 0, 3, dims, str, box)) != ATTN_OK) return st;
+  }
+  {   // W_out [V, d]: K-major B of G1
+    cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)V, 1};
+    cuuint64_t str[2] = {(cuuint64_t)(d * 2), (cuuint64_t)(V * d * 2)};
+    cuuint32_t box[3] = {64, brows, 1};
+    if ((st = encode(&P.m_wo_k, W_out, 0, 3, dims, str, box)) != ATTN_OK) return st;
+  }
+  {   // dL [NB][T][Vc]: K-major A of G3
+    cuuint64_t dims[3] = {(cuuint64_t)Vc, (cuuint64_t)T, (cuuint64_t)NB};
+    cuuint64_t str[2] = {(cuuint64_t)(Vc * 2), (cuuint64_t)(T * Vc * 2)};
+    cuuint32_t box[3] = {64, 128, 1};
+    if ((st = encode(&P.m_dl_k, dl, 0, 3, dims, str, box)) != ATTN_OK) return st;
+  }
+  {   // W_out as [K = V][N = d] MN-major: 64-column atoms 128 bytes apart
+    cuuint64_t dims[4] = {64, (cuuint64_t)V, (cuuint64_t)(d / 64), 1};
+    cuuint64_t str[3] = {(cuuint64_t)(d * 2), 128, (cuuint64_t)(V * d * 2)};
+    cuuint32_t box[4] = {64, 64, brows / 64, 1};
+    if ((st = encode(&P.m_wo_mn, W_out, 0, 4, dims, str, box)) != ATTN_OK) return st;
+  }
+  {   // dL as [K = T][M = Vc] MN-major per buffer
+    cuuint64_t dims[4] = {64, (cuuint64_t)T, (cuuint64_t)(Vc / 64), (cuuint64_t)NB};
+    cuuint64_t str[3] = {(cuuint64_t)(Vc * 2), 128, (cuuint64_t)(T * Vc * 2)};
+    cuuint32_t box[4] = {64, 64, 2, 1};
+    if ((st = encode(&P.m_dl_mn, dl, 0, 4, dims, str, box)) != ATTN_OK) return st;
+  }
+  {   // H_c as [K = T][N = d] MN-major
+    cuuint64_t dims[4] = {64, (cuuint64_t)T, (cuuint64_t)(d / 64), 1};
+    cuuint64_t str[3] = {(cuuint64_t)(d * 2), 128, (cuuint64_t)(T * d * 2)};
+    cuuint32_t box[4] = {64, 64, brows / 64, 1};
+    if ((st = encode(&P.m_hc_mn, hc, 0, 4, dims, str, box)) != ATTN_OK) return st;
+  }
+  {   // dL store: bf16 boxes of 32 rows x 64 columns
+    cuuint64_t dims[3] = {(cuuint64_t)Vc, (cuuint64_t)T, (cuuint64_t)NB};
+    cuuint64_t str[2] = {(cuuint64_t)(Vc * 2), (cuuint64_t)(T * Vc * 2)};
+    cuuint32_t box[3] = {64, 32, 1};
+    if ((st = encode(&P.m_dl_st, dl, 0, 3, dims, str, box)) != ATTN_OK) return st;
+  }
+  {   // dW_out fp32 [V, d] and dHc fp32 [T, d]: boxes of 32 x 32
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)V};
+    cuuint64_t str[1] = {(cuuint64_t)(d * 4)};
+    cuuint32_t box[2] = {32, 32};
+    if ((st = encode(&P.m_dw_st, dW_out, 1, 2, dims, str, box)) != ATTN_OK) return st;
+    cuuint64_t dims2[2] = {(cuuint64_t)d, (cuuint64_t)T};
+    if ((st = encode(&P.m_dhc_st, dhc, 1, 2, dims2, str, box)) != ATTN_OK) return st;
+  }
+  const VbLayout L = vb_ctr_layout(p, kPair);
+  P.T = (int)T; P.d = (int)d; P.V = (int)V; P.Vc = (int)Vc; P.nchunks = p.nchunks;
+  P.nbuf = (int)NB;
+  P.nrb = L.nrb;
+  P.ndt = L.ndt;
+  P.nvbf = (int)(Vc / Cfg::TM);
+  P.ncolf = L.ncolf;
+  P.last_g2_first = g_opt_vb_g2first;
+  P.order = NB >= 2 ? g_opt_vb_order : 0;   // order 1 with one buffer would wait on later tiles
+  P.trace = g_vb_trace;
+  P.debug = g_vb_debug;
+  P.l2hints = g_opt_vb_l2;
+  // dispatch blocks: 0 = G1(0); c + 1 = G3(c), G2(c), G1(c + 1)
+  auto vcc = [&](int c) { return (int)std::min(Vc, V - (long long)c * Vc); };
+  int t = 0;
+  P.blk_start[0] = 0;
+  t += P.nrb * ((vcc(0) + VB_BN - 1) / VB_BN);
+  for (int c = 0; c < p.nchunks; ++c) {
+    P.blk_start[c + 1] = t;
+    t += P.nrb * P.ndt + ((vcc(c) + Cfg::TM - 1) / Cfg::TM) * P.ndt;
+    if (c + 1 < p.nchunks) t += P.nrb * ((vcc(c + 1) + VB_BN - 1) / VB_BN);
+  }
+  P.blk_start[p.nchunks + 1] = t;
+  P.total_tiles = t;
+  P.tile_counter = (int*)ctr;
+  P.rowdone = ctr + L.rowdone;
+  P.coldone = ctr + L.coldone;
+  P.consumed = ctr + L.consumed;
+  P.g2done = ctr + L.g2done;
+  P.dhcdone = ctr + L.dhcdone;
+  P.lse = lse; P.rowscale = rowscale; P.tgt = tgt; P.tgt_logit = tgt_logit; P.bias = bias;
+  int units = (ctas > 0 ? ctas : dev_info().sms) / Cfg::CTAS;
+  units = std::max(1, std::min(units, t));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(units * Cfg::CTAS);
+  cfg.blockDim = dim3(VB_THREADS);
+  cfg.dynamicSmemBytes = VB_SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (kPair) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (g_opt_pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, vocab_bwd_kernel<kPair>, P));
+  ++g_launches;
+  return ATTN_OK;
+}
+
+static attn_status_t launch_vocab_bwd(const Plan& p, const void* hc, const void* W_out, void* dl,
+                                      float* dhc, float* dW_out, const float* lse,
+                                      const float* rowscale, const int* tgt, const float* tgt_logit,
+                                      const void* bias, unsigned* ctr, int ctas,
+                                      cudaStream_t stream) {
+  if (g_opt_vb_pair)
+    return launch_vocab_bwd_k<true>(p, hc, W_out, dl, dhc, dW_out, lse, rowscale, tgt, tgt_logit,
+                                    bias, ctr, ctas, stream);
+  return launch_vocab_bwd_k<false>(p, hc, W_out, dl, dhc, dW_out, lse, rowscale, tgt, tgt_logit,
+                                   bias, ctr, ctas, stream);
+}
+
 struct CounterCtx {
   const Bufs* b;
   int idx;
@@ -1291,6 +1547,38 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
     if ((st = comm_begin(comm, stream, &cr)) != ATTN_OK) return st;
   }
 
+  // ---- B1, bf16: the persistent vocab backward (vocab_bwd.cuh): logits
+  // recomputed per V-chunk, dL in the L2-sized chunk scratch, one launch
+  if (p.vb && !db_out) {
+    CUDA_TRY(cudaMemsetAsync(b.vbctr, 0, sizeof(unsigned) * p.n_vbctr, stream));
+    int ctas = 0;
+    if (comm) {
+      // allreduce dW_out in groups of ~32 MB of chunks, each as soon as the
+      // launch has stored those rows (a one-thread wait kernel on the comm
+      // stream watches the counters); the launch leaves NCCL's SMs free
+      if ((st = comm_fork(comm, &cr, stream)) != ATTN_OK) return st;
+      const VbLayout L = vb_ctr_layout(p, g_opt_vb_pair != 0);
+      const unsigned* g2done = b.vbctr + L.g2done;
+      const long long chunk_bytes = 4ll * p.Vc * d;
+      const int per = (int)std::max(1ll, (32ll << 20) / chunk_bytes);
+      for (int c0 = 0; c0 < p.nchunks; c0 += per) {
+        const int c1 = std::min(p.nchunks, c0 + per);
+        vb_wait_g2_kernel<<<1, 32, 0, comm_stream(comm)>>>(
+            g2done, c0, c1, p.Vc, p.V, L.ndt, VB_EPI_WARPS * (g_opt_vb_pair ? 2 : 1), L.TM);
+        CUDA_TRY(cudaGetLastError());
+        ++g_launches;
+        const long long r0 = (long long)c0 * p.Vc, r1 = std::min((long long)p.V, (long long)c1 * p.Vc);
+        if ((st = comm_allreduce_forked(comm, &cr, dW_out + r0 * d, (size_t)((r1 - r0) * d))) !=
+            ATTN_OK)
+          return st;
+      }
+      reserve = comm_max_ctas(comm);
+      if (reserve > 0) ctas = (dev_info().sms - reserve) & ~1;
+    }
+    st = launch_vocab_bwd(p, b.hc, W_out, b.dl[0], b.dhc, dW_out, b.lse, b.rowscale, tgt_ids,
+                          b.tgt_logit, b_out, b.vbctr, ctas, stream);
+    if (st != ATTN_OK) return st;
+  } else
   // ---- B1: V-chunked vocab backward.  Launch c runs dW_out[c] and dHc += ...
   // for chunk c together with the dlogits of chunk c+1 (double-buffered).
   // With stored logits, an elementwise kernel makes dlogits_c from the

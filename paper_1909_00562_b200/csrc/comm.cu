@@ -218,6 +218,22 @@ attn_status_t comm_enqueue_allreduce(attn_comm_t* c, CommRun* run, cudaStream_t 
   return ATTN_OK;
 }
 
+attn_status_t comm_fork(attn_comm_t* c, CommRun* run, cudaStream_t compute) {
+  cudaEvent_t e = c->events[run->n_enqueued % c->events.size()];
+  CUDA_OK(cudaEventRecord(e, compute));
+  CUDA_OK(cudaStreamWaitEvent(c->stream, e, 0));
+  run->n_enqueued++;
+  return ATTN_OK;
+}
+
+cudaStream_t comm_stream(attn_comm_t* c) { return c->stream; }
+
+attn_status_t comm_allreduce_forked(attn_comm_t* c, CommRun* run, float* buf, size_t count) {
+  (void)run;
+  NCCL_OK(nccl().AllReduce(buf, buf, count, ncclFloat32_, ncclSum_, c->comm, c->stream));
+  return ATTN_OK;
+}
+
 attn_status_t comm_end(attn_comm_t* c, CommRun* run, cudaStream_t compute) {
   (void)run;
   CUDA_OK(cudaEventRecord(c->join, c->stream));

@@ -22,6 +22,13 @@ attn_status_t comm_begin(attn_comm_t* c, cudaStream_t compute, CommRun* run);
 // `compute` reaches this point, on the communicator's own stream.
 attn_status_t comm_enqueue_allreduce(attn_comm_t* c, CommRun* run, cudaStream_t compute,
                                      float* buf, size_t count);
+// Fork the comm stream off `compute` at this point (for work enqueued with
+// comm_stream() / comm_allreduce_forked: it starts after everything `compute`
+// has enqueued so far, without waiting for what `compute` enqueues later).
+attn_status_t comm_fork(attn_comm_t* c, CommRun* run, cudaStream_t compute);
+cudaStream_t comm_stream(attn_comm_t* c);
+// In-place fp32 sum allreduce enqueued on the comm stream as it stands.
+attn_status_t comm_allreduce_forked(attn_comm_t* c, CommRun* run, float* buf, size_t count);
 // Make `compute` wait for every allreduce enqueued in this run.
 attn_status_t comm_end(attn_comm_t* c, CommRun* run, cudaStream_t compute);
 

@@ -1,0 +1,681 @@
+// vocab_bwd.cuh -- B1 (backward of Eqs. 5-6) as ONE
+// persistent tcgen05 launch: the logits are never stored; they are recomputed
+// per V-chunk on the tensor cores and turned into dL = rs (softmax - onehot)
+// (bf16) in an L2-sized, double-buffered chunk scratch, which the same launch
+// consumes for dW_out and dHc.
+//
+// Per V-chunk c (width Vc, columns [c0, c0 + vcc) of the vocabulary):
+//   G1(c)  dL_c   = rs (exp(H_c W_out[c]^T - lse) - onehot)    M = T,   N = vcc, K = d
+//   G3(c)  dHc   += dL_c W_out[c]                             M = T,   N = d,   K = vcc
+//   G2(c)  dW_out[c] = dL_c^T H_c                             M = vcc, N = d,   K = T
+// Tiles are TM x 256 with fp32 accumulators in TMEM, two accumulators per
+// CTA so a tile's epilogue overlaps the next tile's MMAs:
+//   kPair = false: TM = 128, one CTA per tile (tcgen05 cta_group::1);
+//   kPair = true:  TM = 256, a CTA pair (cluster of 2) per tile
+//                  (cta_group::2): each CTA stages its 128 rows of A and its
+//                  128 rows (N-columns) of B, both CTAs' TMA loads complete on
+//                  the leader's barrier, the leader issues M = 256 MMAs that
+//                  read the peer's shared memory, and each CTA's epilogue
+//                  drains its own 128 accumulator rows.  L2 -> SM operand
+//                  bytes per FLOP are 2/3 of the single-CTA tile's.
+// The tiles of all chunks form one dispatch list, pulled from a global atomic:
+//   block 0        G1(0)
+//   block c+1      G1(c+1), G3(c), G2(c)       (option order 0: G3(c), G2(c), G1(c+1))
+// (the last block has no G1 and may put G2 first: its long tiles then do not
+// form the tail)
+// and the data dependencies between tiles are tracked with counters in global
+// memory (release / acquire at gpu scope, async-proxy fences around the TMA
+// traffic):
+//   G3(c) tile (row block rb) waits for every G1(c) tile of row block rb
+//        (rowdone[c][rb]) -- and, before its reduce-add into dHc, for the G3
+//        tile of chunk c-1 at the same place (dhcdone[rb][nt]): dHc is summed
+//        in chunk order, so the result is deterministic;
+//   G2(c) tile (vocabulary rows vb) waits for the G1(c) tiles of those columns
+//        over all row blocks (coldone[c][vb]);
+//   G1(c) writes dL buffer c % NB only after every G2 / G3 tile of chunk c-NB
+//        has loaded it (consumed[c - NB]);
+//   G2(c) tiles count their finished dW_out stores (g2done[c]) so an
+//        allreduce of chunk c can start while the launch runs.
+// Every wait targets tiles earlier in the dispatch list and all CTAs are
+// resident (one per SM), so the waits cannot deadlock.  Counters count
+// epilogue-warp portions (8 per CTA and tile), so their targets scale with
+// the CTAs per tile.
+//
+// Roles (384 threads): warps 0-7 epilogue (warp w: TMEM lanes 32 (w % 4).., tile
+// column half w / 4), warp 8 TMEM allocator, warp 10 scheduler + TMA
+// producer, warp 11 MMA issuer (one elected lane; the pair leader's only).
+#pragma once
+#include "epilogue.cuh"
+#include "ptx.cuh"
+
+namespace attnsm {
+
+constexpr int VB_BN = 256;
+constexpr int VB_BK = 64;
+constexpr int VB_EPI_WARPS = 8;
+constexpr int VB_STG_BYTES = 4096;                 // staging per epilogue warp
+constexpr int VB_THREADS = 384;
+constexpr int VB_SCHED = 4;
+constexpr int VB_RING = 192 * 1024;
+constexpr int VB_SMEM_BYTES = VB_RING + VB_EPI_WARPS * VB_STG_BYTES + 1024 + 512;
+constexpr int VB_MAX_BLOCKS = 1024;                // chunks + 1
+constexpr int VB_BM = 128;                         // accumulator rows per CTA
+
+template <bool kPair>
+struct VbCfg {
+  static constexpr int CTAS = kPair ? 2 : 1;
+  static constexpr int TM = 128 * CTAS;            // tile rows (M)
+  static constexpr int B_ROWS = VB_BN / CTAS;      // B rows (N) staged per CTA
+  static constexpr int A_BYTES = 128 * VB_BK * 2;  // 16 KB
+  static constexpr int B_BYTES = B_ROWS * VB_BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;  // 48 KB | 32 KB
+  static constexpr int STAGES = VB_RING / STAGE;   // 4 | 6
+  static constexpr int WARPS_PER_TILE = VB_EPI_WARPS * CTAS;
+};
+
+enum : int { VB_G1 = 0, VB_G3 = 1, VB_G2 = 2 };
+
+struct alignas(64) VbParams {
+  CUtensorMap m_hc_k;    // H_c [T, d] bf16, K-major A of G1: box {64, 128}
+  CUtensorMap m_wo_k;    // W_out [V, d] bf16, K-major B of G1: box {64, B_ROWS}
+  CUtensorMap m_dl_k;    // dL [NB][T][Vc] bf16, K-major A of G3: box {64, 128, 1}
+  CUtensorMap m_wo_mn;   // W_out as [K = V][N = d], MN-major B of G3: box {64, 64, B_ROWS/64, 1}
+  CUtensorMap m_dl_mn;   // dL as [K = T][M = Vc] per buffer, MN-major A of G2: box {64, 64, 2, 1}
+  CUtensorMap m_hc_mn;   // H_c as [K = T][N = d], MN-major B of G2: box {64, 64, B_ROWS/64, 1}
+  CUtensorMap m_dl_st;   // dL store: bf16 [NB][T][Vc], box {64, 32, 1}
+  CUtensorMap m_dw_st;   // dW_out store: fp32 [V, d], box {32, 32}
+  CUtensorMap m_dhc_st;  // dHc store / reduce-add: fp32 [T, d], box {32, 32}
+  int T, d, V, Vc, nchunks, nbuf;
+  int nrb;               // TM-row blocks of T
+  int ndt;               // 256-column tiles of d
+  int nvbf;              // TM-row blocks of a full chunk (Vc / TM)
+  int ncolf;             // 256-column blocks of a full chunk (Vc / 256)
+  int total_tiles;
+  int* tile_counter;
+  unsigned* rowdone;     // [nchunks][nrb]   G1 warp-portions done per row block
+  unsigned* coldone;     // [nchunks][ncolf] G1 warp-portions done per 256-column block
+  unsigned* consumed;    // [nchunks]        G2 + G3 CTA-tiles whose operands are loaded
+  unsigned* g2done;      // [nchunks]        G2 warp-portions whose dW_out stores completed
+  unsigned* dhcdone;     // [nrb][ndt]       G3 warp-portions whose dHc update completed
+  const float* lse;
+  const float* rowscale;
+  const int* tgt;
+  const float* tgt_logit;
+  const void* bias;      // F_c bias b_out [V] bf16 (NEXT-1) or NULL
+  int last_g2_first;     // last block: G2 tiles before G3 tiles
+  int order;             // 0: block c+1 = G3(c), G2(c), G1(c+1); 1: G1(c+1), G3(c), G2(c)
+  long long* trace;      // debug: 16 int64 per tile and CTA rank (see VB_TRACE), NULL = off
+  int l2hints;           // bit 0: H_c loads evict-last; bit 1: dHc updates evict-last
+  int debug;             // timing experiments only (WRONG results): bit 0 skip the G1 stores,
+                         // bit 1 skip the G1 exponentials, bit 2 skip the G2 / G3 stores
+  int blk_start[VB_MAX_BLOCKS + 2];
+};
+
+struct VbTile {
+  int type, c, i, j;     // G1: i = row block, j = 256-col tile; G3: i = row block, j = d tile;
+                         // G2: i = vocabulary row block of the chunk, j = d tile
+  int vcc, kb_total;
+};
+
+__device__ __forceinline__ int vb_vcc(const VbParams& P, int c) {
+  return min(P.Vc, P.V - c * P.Vc);
+}
+
+template <bool kPair>
+__device__ __forceinline__ VbTile vb_decode(const VbParams& P, int t) {
+  constexpr int TM = VbCfg<kPair>::TM;
+  int lo = 0, hi = P.nchunks;   // blocks 0..nchunks
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.blk_start[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  int u = t - P.blk_start[lo];
+  VbTile r;
+  if (lo == 0) {
+    r.type = VB_G1; r.c = 0;
+  } else {
+    const int c = lo - 1;
+    const int n3 = P.nrb * P.ndt;
+    const int n2 = ((vb_vcc(P, c) + TM - 1) / TM) * P.ndt;
+    const bool g2first = P.last_g2_first && c == P.nchunks - 1;
+    const int n1 = (P.order == 1 && c + 1 < P.nchunks)
+                       ? P.nrb * ((vb_vcc(P, c + 1) + VB_BN - 1) / VB_BN) : 0;
+    if (u < n1) {   // order 1: the next chunk's G1 tiles open the block
+      r.type = VB_G1; r.c = c + 1;
+    } else {
+      u -= n1;
+      if (g2first) {
+        if (u < n2) { r.type = VB_G2; r.c = c; }
+        else { u -= n2; r.type = VB_G3; r.c = c; }
+      } else if (u < n3) {
+        r.type = VB_G3; r.c = c;
+      } else if (u < n3 + n2) {
+        u -= n3; r.type = VB_G2; r.c = c;
+      } else {   // order 0: the next chunk's G1 tiles close the block
+        u -= n3 + n2; r.type = VB_G1; r.c = c + 1;
+      }
+    }
+  }
+  r.vcc = vb_vcc(P, r.c);
+  if (r.type == VB_G1) {
+    const int ncol = (r.vcc + VB_BN - 1) / VB_BN;
+    r.i = u / ncol; r.j = u % ncol;
+    r.kb_total = P.d / VB_BK;
+  } else if (r.type == VB_G3) {
+    r.i = u / P.ndt; r.j = u % P.ndt;
+    r.kb_total = (r.vcc + VB_BK - 1) / VB_BK;
+  } else {
+    r.i = u / P.ndt; r.j = u % P.ndt;
+    r.kb_total = (P.T + VB_BK - 1) / VB_BK;
+  }
+  return r;
+}
+
+// trace record of tile t and CTA rank r (option "vb_trace"), at (2 t + r) * 16:
+// [0] smid [1] type << 16 | chunk  [2] / [3] producer globaltimer before / after
+// the dependency wait  [4] / [5] MMA clock64 first MMA issued / last commit
+// [6] / [7] epilogue warp 0 clock64 accumulator ready / tile done  [8] / [9] MMA
+// globaltimer first MMA / last commit  [10] / [11] epilogue globaltimer ready /
+// done  [12] epilogue clock64 after its dependency wait  [13] MMA clock64
+// accumulator free  [14] MMA cycles spent waiting for full stages
+__device__ __forceinline__ long long vb_clk() {
+  long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
+__device__ __forceinline__ long long vb_gt() {
+  long long c;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(c));
+  return c;
+}
+#define VB_TRACE(t, i, val)                                                  \
+  do {                                                                       \
+    if (P.trace) {                                                           \
+      const long long v_ = (val);                                            \
+      if (lane == 2) P.trace[((long long)(t) * 2 + rank) * 16 + (i)] = v_;   \
+    }                                                                        \
+  } while (0)
+
+__device__ __forceinline__ void vb_wait_geq(const unsigned* p, unsigned target) {
+  if (ld_acquire_gpu(p) >= target) return;
+  while (ld_acquire_gpu(p) < target) __nanosleep(64);
+}
+
+template <bool kPair>
+__device__ __forceinline__ void vb_load(void* dst, const CUtensorMap* m, uint64_t* bar,
+                                        uint32_t barc, int c0, int c1, int c2, uint64_t pol) {
+  if constexpr (kPair) tma_load_3d_pair_hint(dst, m, barc, c0, c1, c2, pol);
+  else tma_load_3d_hint(dst, m, bar, c0, c1, c2, pol);
+}
+template <bool kPair>
+__device__ __forceinline__ void vb_load4(void* dst, const CUtensorMap* m, uint64_t* bar,
+                                         uint32_t barc, int c0, int c1, int c2, int c3,
+                                         uint64_t pol) {
+  if constexpr (kPair) tma_load_4d_pair_hint(dst, m, barc, c0, c1, c2, c3, pol);
+  else tma_load_4d_hint(dst, m, bar, c0, c1, c2, c3, pol);
+}
+
+template <bool kPair>
+__global__ void __launch_bounds__(VB_THREADS, 1) vocab_bwd_kernel(const __grid_constant__ VbParams P) {
+  using Cfg = VbCfg<kPair>;
+  constexpr int TM = Cfg::TM;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* staging = smem + VB_RING;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + VB_EPI_WARPS * VB_STG_BYTES);
+  uint64_t* full = bars;                        // [STAGES]
+  uint64_t* empty = full + STAGES;              // [STAGES]
+  uint64_t* tfull = empty + STAGES;             // [2]
+  uint64_t* tempty = tfull + 2;                 // [2]
+  uint64_t* sfull = tempty + 2;                 // [SCHED]
+  uint64_t* sempty = sfull + VB_SCHED;          // [SCHED]
+  int* sched_tile = reinterpret_cast<int*>(sempty + VB_SCHED);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_tile + VB_SCHED);
+
+  const uint32_t warp = warp_id_uniform();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = kPair ? cluster_ctarank() : 0;   // 0 = pair leader
+  const bool leader = rank == 0;
+  constexpr uint32_t kWarpAlloc = 8, kWarpProducer = 10, kWarpMma = 11;
+  // shared::cluster address of a barrier in the leader CTA
+  auto leader_addr = [&](void* p) -> uint32_t { return mapa_shared(smem_u32(p), 0); };
+
+  if (warp == kWarpProducer && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], Cfg::WARPS_PER_TILE);   // every epilogue warp of the tile
+    }
+    for (int i = 0; i < VB_SCHED; ++i) {
+      mbar_init(&sfull[i], 1);
+      // leader: its MMA warp + epilogue warps (+ the peer's producer and epilogue warps)
+      mbar_init(&sempty[i], 1 + VB_EPI_WARPS + (kPair ? 1 + VB_EPI_WARPS : 0));
+    }
+    fence_barrier_init();
+    const CUtensorMap* maps[9] = {&P.m_hc_k, &P.m_wo_k, &P.m_dl_k, &P.m_wo_mn, &P.m_dl_mn,
+                                  &P.m_hc_mn, &P.m_dl_st, &P.m_dw_st, &P.m_dhc_st};
+    for (int i = 0; i < 9; ++i) tma_prefetch_desc(maps[i]);
+  }
+  if (warp == kWarpAlloc) {
+    if constexpr (kPair) tmem_alloc_pair(tmem_slot, 512);
+    else tmem_alloc(tmem_slot, 512);
+  }
+  tc_fence_before();
+  if constexpr (kPair) cluster_sync();
+  else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  if (threadIdx.x == 0) pdl_trigger();
+
+  // the scheduler ring: the leader publishes each tile id into both CTAs' rings
+  auto ring_read = [&](int& r, uint32_t& rph, bool arrive_all_lanes_0) -> int {
+    if (kPair && !leader) mbar_wait_cluster(&sfull[r], rph);
+    else mbar_wait(&sfull[r], rph);
+    const int t = sched_tile[r];
+    __syncwarp();
+    if (arrive_all_lanes_0 ? lane == 0 : elect_one()) {
+      if (kPair && !leader) mbar_arrive_cluster(leader_addr(&sempty[r]));
+      else mbar_arrive(&sempty[r]);
+    }
+    __syncwarp();
+    if (++r == VB_SCHED) { r = 0; rph ^= 1; }
+    return t;
+  };
+
+  if (warp == kWarpProducer) {
+    // ---------------- scheduler (leader) + TMA producer (both CTAs).  The
+    // whole warp runs the loop, one elected lane issues; the next tile is
+    // fetched, published and decoded right after the current tile's first load.
+    int s = 0;
+    uint32_t ph = 0;
+    int r = 0;
+    uint32_t rph = 0;
+    int t_raw = 0;
+    auto fetch = [&]() {
+      if (lane == 1) t_raw = atomicAdd(P.tile_counter, 1);
+    };
+    auto next_tile = [&]() -> int {
+      if (!leader) return ring_read(r, rph, false);
+      int t = __shfl_sync(0xffffffffu, t_raw, 1);
+      if (t >= P.total_tiles) t = -1;
+      mbar_wait(&sempty[r], rph ^ 1);
+      if (elect_one()) {
+        sched_tile[r] = t;
+        if constexpr (kPair) {
+          st_shared_cluster_u32(mapa_shared(smem_u32(&sched_tile[r]), 1), (uint32_t)t);
+          mbar_arrive_cluster(mapa_shared(smem_u32(&sfull[r]), 1));
+        }
+        mbar_arrive(&sfull[r]);
+      }
+      __syncwarp();
+      if (t >= 0) fetch();
+      if (++r == VB_SCHED) { r = 0; rph ^= 1; }
+      return t;
+    };
+    // L2 residency: H_c is re-read by every chunk (evict-last when option
+    // bit 0 of P.l2hints), the streaming operands keep the normal policy
+    const uint64_t pol_keep = (P.l2hints & 1) ? l2_policy_evict_last() : l2_policy_evict_normal();
+    const uint64_t pol_norm = l2_policy_evict_normal();
+    if (leader) fetch();
+    int t = next_tile();
+    VbTile tl{};
+    if (t >= 0) tl = vb_decode<kPair>(P, t);
+    while (t >= 0) {
+      const int buf = tl.c % P.nbuf;
+      const int c0 = tl.c * P.Vc;
+      if (P.trace) {
+        uint32_t sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        VB_TRACE(t, 0, (long long)sm);
+        VB_TRACE(t, 1, ((long long)tl.type << 16) | tl.c);
+        VB_TRACE(t, 2, vb_gt());
+      }
+      // operands of G2 / G3 are the dL chunk: wait for the G1 tiles that write it
+      if (tl.type == VB_G3) {
+        if (lane == 0)
+          vb_wait_geq(P.rowdone + (size_t)tl.c * P.nrb + tl.i,
+                      (unsigned)(Cfg::WARPS_PER_TILE * ((tl.vcc + VB_BN - 1) / VB_BN)));
+        __syncwarp();
+        fence_proxy_async_global();
+      } else if (tl.type == VB_G2) {
+        if (lane == 0) {
+          // this tile's TM vocabulary rows: 256-column blocks of G1
+          const int cb0 = tl.i * TM / VB_BN, cb1 = ((tl.i + 1) * TM - 1) / VB_BN;
+          for (int cb = cb0; cb <= cb1 && cb * VB_BN < tl.vcc; ++cb)
+            vb_wait_geq(P.coldone + (size_t)tl.c * P.ncolf + cb,
+                        (unsigned)(Cfg::WARPS_PER_TILE * P.nrb));
+        }
+        __syncwarp();
+        fence_proxy_async_global();
+      }
+      VB_TRACE(t, 3, vb_gt());
+      const int arow = tl.i * TM + 128 * rank;            // this CTA's A rows (M)
+      const int bcol = tl.j * VB_BN + Cfg::B_ROWS * rank;  // this CTA's B rows (N)
+      int t_nxt = -1;
+      VbTile tl_nxt{};
+      for (int kb = 0; kb < tl.kb_total; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        if (elect_one()) {
+          uint8_t* sA = smem + s * Cfg::STAGE;
+          uint8_t* sB = sA + Cfg::A_BYTES;
+          const uint32_t barc = kPair ? leader_addr(&full[s]) : 0u;
+          if (leader) mbar_arrive_expect_tx(&full[s], Cfg::STAGE * Cfg::CTAS);
+          const int k0 = kb * VB_BK;
+          if (tl.type == VB_G1) {
+            vb_load<kPair>(sA, &P.m_hc_k, &full[s], barc, k0, arow, 0, pol_keep);
+            vb_load<kPair>(sB, &P.m_wo_k, &full[s], barc, k0, c0 + bcol, 0, pol_norm);
+          } else if (tl.type == VB_G3) {
+            vb_load<kPair>(sA, &P.m_dl_k, &full[s], barc, k0, arow, buf, pol_norm);
+            vb_load4<kPair>(sB, &P.m_wo_mn, &full[s], barc, 0, c0 + k0, bcol / 64, 0, pol_norm);
+          } else {
+            vb_load4<kPair>(sA, &P.m_dl_mn, &full[s], barc, 0, k0, arow / 64, buf, pol_norm);
+            vb_load4<kPair>(sB, &P.m_hc_mn, &full[s], barc, 0, k0, bcol / 64, 0, pol_keep);
+          }
+        }
+        __syncwarp();
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+        if (kb == 0) {
+          t_nxt = next_tile();
+          if (t_nxt >= 0) tl_nxt = vb_decode<kPair>(P, t_nxt);
+        }
+      }
+      t = t_nxt;
+      tl = tl_nxt;
+    }
+  } else if (warp == kWarpMma) {
+    if (leader) {
+      // ---------------- MMA issuer (pair: the leader issues for both CTAs)
+      int s = 0;
+      uint32_t ph = 0;
+      int r = 0;
+      uint32_t rph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      int t = ring_read(r, rph, false);
+      VbTile tl{};
+      if (t >= 0) tl = vb_decode<kPair>(P, t);
+      while (t >= 0) {
+        const int a_mn = tl.type == VB_G2 ? 1 : 0;
+        const int b_mn = tl.type == VB_G1 ? 0 : 1;
+        const uint32_t idesc = umma_idesc_bf16(TM, VB_BN, a_mn, b_mn);
+        const uint32_t a_lbo = a_mn ? 8192u : 16u, b_lbo = b_mn ? 8192u : 16u;
+        const uint32_t a_kstep = a_mn ? 2048u : 32u, b_kstep = b_mn ? 2048u : 32u;
+        const int kb_read = tl.kb_total > 1 ? 1 : 0;
+        int t_nxt = -1;
+        VbTile tl_nxt{};
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        VB_TRACE(t, 13, vb_clk());
+        long long wait_cyc = 0;
+        const uint32_t dcol = tmem_base + acc * VB_BN;
+        for (int kb = 0; kb < tl.kb_total; ++kb) {
+          if (P.trace) {
+            const long long w0 = vb_clk();
+            mbar_wait(&full[s], ph);
+            wait_cyc += vb_clk() - w0;
+          } else {
+            mbar_wait(&full[s], ph);
+          }
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sA = smem_u32(smem + s * Cfg::STAGE);
+            const uint32_t sB = sA + Cfg::A_BYTES;
+#pragma unroll
+            for (int k = 0; k < VB_BK / 16; ++k) {
+              const uint64_t ad = umma_sdesc(sA + k * a_kstep, a_lbo, 1024);
+              const uint64_t bd = umma_sdesc(sB + k * b_kstep, b_lbo, 1024);
+              if constexpr (kPair) umma_bf16_pair(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              else umma_bf16(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            }
+            if constexpr (kPair) umma_commit_pair(&empty[s]);
+            else umma_commit(&empty[s]);
+          }
+          __syncwarp();
+          if (kb == 0) {
+            VB_TRACE(t, 4, vb_clk());
+            VB_TRACE(t, 8, vb_gt());
+          }
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+          if (kb == kb_read) {
+            t_nxt = ring_read(r, rph, false);
+            if (t_nxt >= 0) tl_nxt = vb_decode<kPair>(P, t_nxt);
+          }
+        }
+        if (elect_one()) {
+          if constexpr (kPair) umma_commit_pair(&tfull[acc]);
+          else umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        VB_TRACE(t, 5, vb_clk());
+        VB_TRACE(t, 9, vb_gt());
+        VB_TRACE(t, 14, wait_cyc);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+        t = t_nxt;
+        tl = tl_nxt;
+      }
+    }
+  } else if (warp < VB_EPI_WARPS) {
+    // ---------------- epilogue (8 warps per CTA): this CTA's 128 rows of the tile
+    const uint32_t q = warp & 3;        // TMEM lane quarter: rows 32q..32q+31 of this CTA's 128
+    const uint32_t h = warp >> 2;       // column half of the 256-wide tile
+    uint8_t* stg_p = staging + warp * VB_STG_BYTES;
+    const uint32_t stg = smem_u32(stg_p);
+    const uint32_t swz = lane & 7;
+    int r = 0;
+    uint32_t rph = 0;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (;;) {
+      const int t = ring_read(r, rph, true);
+      if (t < 0) break;
+      const VbTile tl = vb_decode<kPair>(P, t);
+      const int buf = tl.c % P.nbuf;
+      const int c0 = tl.c * P.Vc;
+      const int row0 = tl.i * TM + 128 * rank + q * 32;   // problem row of lane 0
+      const int colh = tl.j * VB_BN + h * 128;           // problem column of this warp's first
+      const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * VB_BN + h * 128;
+      if (tl.type == VB_G1) {
+        // ---- dL = rs softmax - rs onehot (bf16) into dL buffer `buf`.  The
+        // row's statistics are read before the accumulator wait (latency hidden
+        // under the tile's MMAs).
+        const int row = row0 + lane;
+        float c2 = -1000.f, fix = 0.f;
+        int yl = -1;   // target column relative to this warp's first column
+        if (row < P.T) {
+          const float rs = P.rowscale[row];
+          if (rs > 0.f) {
+            const float ls = P.lse[row];
+            c2 = __log2f(rs) - ls * kLog2e;
+            fix = rs * (__expf(P.tgt_logit[row] - ls) - 1.f);
+            yl = P.tgt[row] - c0 - colh;
+          }
+        }
+        // the buffer is free once chunk c - NB's G2 / G3 tiles have loaded it
+        if (tl.c >= P.nbuf) {
+          const int cp = tl.c - P.nbuf;
+          const unsigned need = (unsigned)(Cfg::CTAS * P.ndt *
+                                           (P.nrb + (vb_vcc(P, cp) + TM - 1) / TM));
+          if (lane == 0) vb_wait_geq(P.consumed + cp, need);
+          __syncwarp();
+          fence_proxy_async_global();
+        }
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        if (warp == 0) {
+          VB_TRACE(t, 6, vb_clk());
+          VB_TRACE(t, 10, vb_gt());
+          VB_TRACE(t, 12, vb_clk());
+        }
+        const int nvalid = tl.vcc - colh;   // valid columns of this warp's 128 (may be <= 0)
+        uint32_t raw[32];
+        tmem_ld32_issue(taddr, raw);
+        tmem_ld_wait_regs(raw);
+#pragma unroll 1
+        for (int cc = 0; cc < 4; ++cc) {
+          float v[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(raw[e]);
+          if (P.bias && nvalid - cc * 32 > 0)
+            add_bias32<__nv_bfloat16>(P.bias, c0 + colh + cc * 32, nvalid - cc * 32, v);
+          uint32_t w[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            float a, b;
+            if (P.debug & 2) {
+              a = v[2 * e];
+              b = v[2 * e + 1];
+            } else {
+              a = ex2_mufu(fmaf(v[2 * e], kLog2e, c2));
+              b = ex2_mufu(fmaf(v[2 * e + 1], kLog2e, c2));
+            }
+            if (nvalid - cc * 32 < 32) {   // chunk tail: exact zeros past the vocabulary
+              a = cc * 32 + 2 * e < nvalid ? a : 0.f;
+              b = cc * 32 + 2 * e + 1 < nvalid ? b : 0.f;
+            }
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+            w[e] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+          // next chunk's accumulator columns load while this one is staged
+          if (cc < 3) tmem_ld32_issue(taddr + (cc + 1) * 32, raw);
+          if ((cc & 1) == 0) {
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const uint32_t gi = (cc & 1) * 4 + g;
+            st_shared_v4(stg + lane * 128 + ((gi ^ swz) << 4), w[4 * g], w[4 * g + 1],
+                         w[4 * g + 2], w[4 * g + 3]);
+          }
+          const int ycc = yl - cc * 32;
+          if ((unsigned)ycc < 32u) {   // the -onehot term: target column holds rs (p_y - 1)
+            const uint32_t gi = (cc & 1) * 4 + (ycc >> 3);
+            st_shared_u16(stg + lane * 128 + ((gi ^ swz) << 4) + (ycc & 7) * 2,
+                          __bfloat16_as_ushort(__float2bfloat16_rn(fix)));
+          }
+          if (cc & 1) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && !(P.debug & 1)) {
+              tma_store_3d(&P.m_dl_st, stg_p, colh + (cc - 1) * 32, row0, buf);
+              bulk_commit();
+            }
+          }
+          if (cc < 3) tmem_ld_wait_regs(raw);
+        }
+        // accumulator drained: the next tile's MMAs may use it
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (kPair && !leader) mbar_arrive_cluster(leader_addr(&tempty[acc]));
+          else mbar_arrive(&tempty[acc]);
+        }
+        // publish: this warp's 32 x 128 piece of dL_c is in memory
+        if (lane == 0) {
+          bulk_wait0();
+          fence_proxy_async_global();
+          red_release_gpu_add(P.rowdone + (size_t)tl.c * P.nrb + tl.i, 1u);
+          red_release_gpu_add(P.coldone + (size_t)tl.c * P.ncolf + tl.j, 1u);
+        }
+        __syncwarp();
+      } else {
+        // ---- fp32 output: dW_out[c] rows (G2) or dHc (G3; chunk 0 stores, the
+        // later chunks reduce-add in chunk order)
+        const bool g3 = tl.type == VB_G3;
+        const int ncols = min(128, P.d - colh);
+        unsigned* dhc_ctr = P.dhcdone + (size_t)tl.i * P.ndt + tl.j;
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        if (warp == 0) {
+          VB_TRACE(t, 6, vb_clk());
+          VB_TRACE(t, 10, vb_gt());
+        }
+        if (warp == 0 && lane == 0) {
+          // every MMA of the tile has completed, so its dL operand has been read
+          fence_proxy_async_global();
+          red_release_gpu_add(P.consumed + tl.c, 1u);
+        }
+        if (g3 && tl.c > 0) {
+          if (lane == 0) vb_wait_geq(dhc_ctr, (unsigned)(Cfg::WARPS_PER_TILE * tl.c));
+          __syncwarp();
+          fence_proxy_async_global();
+        }
+        if (warp == 0) VB_TRACE(t, 12, vb_clk());
+        const uint64_t pol = l2_policy_evict_first();   // dW_out is not read again here
+        const uint64_t pol_dhc = (P.l2hints & 2) ? l2_policy_evict_last() : l2_policy_evict_normal();
+#pragma unroll 1
+        for (int cc = 0; cc < 4; ++cc) {
+          if (cc * 32 >= ncols) break;
+          float v[32];
+          tmem_ld32(taddr + cc * 32, v);
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            st_shared_v4(stg + lane * 128 + ((g ^ swz) << 4), __float_as_uint(v[4 * g]),
+                         __float_as_uint(v[4 * g + 1]), __float_as_uint(v[4 * g + 2]),
+                         __float_as_uint(v[4 * g + 3]));
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && !(P.debug & 4)) {
+            if (!g3)
+              tma_store_2d_hint(&P.m_dw_st, stg_p, colh + cc * 32, c0 + row0, pol);
+            else if (tl.c == 0)
+              tma_store_2d_hint(&P.m_dhc_st, stg_p, colh + cc * 32, row0, pol_dhc);
+            else
+              tma_reduce_add_2d_hint(&P.m_dhc_st, stg_p, colh + cc * 32, row0, pol_dhc);
+            bulk_commit();
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (kPair && !leader) mbar_arrive_cluster(leader_addr(&tempty[acc]));
+          else mbar_arrive(&tempty[acc]);
+        }
+        if (lane == 0) {
+          bulk_wait0();
+          fence_proxy_async_global();
+          red_release_gpu_add(g3 ? dhc_ctr : P.g2done + tl.c, 1u);
+        }
+        __syncwarp();
+      }
+      if (warp == 0) {
+        VB_TRACE(t, 7, vb_clk());
+        VB_TRACE(t, 11, vb_gt());
+      }
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+    if (lane == 0) bulk_wait0();
+  }
+  tc_fence_before();
+  if constexpr (kPair) cluster_sync();
+  else __syncthreads();
+  tc_fence_after();
+  if (warp == kWarpAlloc) {
+    if constexpr (kPair) tmem_dealloc_pair(tmem_base, 512);
+    else tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// Comm-stream helper: waits until the G2 tiles of chunks [c_lo, c_hi) have
+// stored their dW_out rows (one thread; it runs beside the persistent launch
+// on an SM it leaves free), so the allreduce enqueued after it starts early.
+// `per_tile` = epilogue warps per G2 tile, `tm` = its vocabulary rows.
+__global__ void vb_wait_g2_kernel(const unsigned* __restrict__ g2done, int c_lo, int c_hi, int Vc,
+                                  int V, int ndt, int per_tile, int tm) {
+  if (threadIdx.x != 0) return;
+  for (int c = c_lo; c < c_hi; ++c) {
+    const int vcc = min(Vc, V - c * Vc);
+    vb_wait_geq(g2done + c, (unsigned)(per_tile * ndt * ((vcc + tm - 1) / tm)));
+  }
+  __threadfence();
+}
+
+}  // namespace attnsm
