@@ -212,6 +212,19 @@ attn_status_t attn_comm_init(const uint8_t id[128], int nranks, int rank,
                              int device, attn_comm_t** out);
 attn_status_t attn_comm_destroy(attn_comm_t* c);
 
+/* Failure detection: wait until every collective this
+ * communicator has enqueued (by attn_softmax_fwd_bwd or attn_grad_allreduce)
+ * has completed, polling ncclCommGetAsyncError every millisecond.  Returns
+ * ATTN_OK when the work is done; ATTN_ERR_NCCL (after ncclCommAbort, which
+ * leaves the communicator unusable: destroy it) when NCCL reports an
+ * asynchronous error -- a peer died, a link failed -- or when `timeout_ms`
+ * (> 0) elapses first (a hang: some rank never joined the collective).  The
+ * caller keeps running either way instead of blocking forever in a
+ * synchronize.  Host-blocking; call it from the training loop between steps. */
+attn_status_t attn_comm_poll(attn_comm_t* c, int64_t timeout_ms);
+/* Ranks in the communicator (1 for a NULL communicator). */
+int attn_comm_nranks(const attn_comm_t* c);
+
 /* ---- NEXT-4: forward-only decoding step -----------------------------------
  * One step of beam-search decoding (section 4.4) on the stage:
  * shape s holds B sentences with N = live hypotheses per sentence (tgt_len),

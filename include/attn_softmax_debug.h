@@ -55,9 +55,33 @@ attn_status_t attn_softmax_stage_time(int i, const char** name, float* ms);
 /* Number of kernels the last attn_softmax_fwd_bwd call launched. */
 long long attn_softmax_last_launches(void);
 
-/* Tuning knobs (process-wide).  Keys:
+/* Tuning knobs (process-wide; a call reads them once, at its start, under a
+ * lock, so a concurrent set_option never changes a call in flight.  Options
+ * that change the workspace layout -- vocab_chunk, dl_budget_mb, dl_buffers,
+ * store_logits -- must be set before attn_softmax_workspace_size; a call whose
+ * workspace is too small for the current options fails with
+ * ATTN_ERR_WORKSPACE).  Keys:
  *   "vocab_chunk"   V-chunk width of the vocab backward (multiple of 256,
- *                   0 = automatic from the L2 size)
+ *                   0 = automatic: the dL chunk buffers fit dl_budget_mb)
+ *   "dl_budget_mb"  L2 budget of the bf16 dL chunk scratch, all buffers
+ *                   (default 120)
+ *   "dl_buffers"    dL chunk buffers of the persistent backward (1-4, default 3)
+ *   "vb_pair"       1 (default) = the persistent vocabulary launch on CTA
+ *                   pairs (tcgen05 cta_group::2, 256 x 256 tiles); 0 = single
+ *                   CTAs (128 x 256)
+ *   "vb_fwd_fused"  1 = F4 + F5 (logit tiles, lse, loss) inside the persistent
+ *                   launch; 0 (default) = the single-CTA forward GEMM and the
+ *                   lse_reduce kernel before it
+ *   "vb_order"      dispatch blocks of the persistent backward: 1 (default) =
+ *                   [G1(c+1), G3(c), G2(c)], 0 = [G3(c), G2(c), G1(c+1)]
+ *   "vb_last_g2_first" 1 (default): the last block dispatches dW_out tiles first
+ *   "vb_l2hints"    bit 0: H_c loads evict-last; bit 1: dHc updates evict-last
+ *                   (default 3)
+ *   "vb_trace"      device address of an int64 buffer (32 per tile) that the
+ *                   next persistent launch fills with per-tile stamps (debug)
+ *   "vb_debug"      timing experiments only (WRONG results): bit 0 skip the
+ *                   dL stores, bit 1 skip the exponentials, bit 2 skip the
+ *                   dW_out / dHc stores
  *   "gemm_ctas"     persistent GEMM grid size (0 = number of SMs)
  *   "comm_max_ctas" CTA cap given to NCCL by attn_comm_init calls made after
  *                   it (default 8, 0 = NCCL's default); while gradients are
@@ -66,41 +90,22 @@ long long attn_softmax_last_launches(void);
  *   "stage_events"  1 = record per-step CUDA events (see above); 2 = only the
  *                   marks around the vocab GEMMs (vocab_fwd, lse_reduce,
  *                   vocab_bwd: fewer events between the step's kernels)
- *   "cta_pair"      bitmask of GEMM groups run on CTA pairs (tcgen05
- *                   cta_group::2, 256 x 256 tiles) instead of single CTAs
- *                   (128 x 256): 1 = forward vocab / projection, 2 = vocab
- *                   backward chunks, 4 = projection backward, 8 = the debug
- *                   GEMM entry.  Default 8.
- *   "wide_tiles"    bitmask (same bits as cta_pair) of GEMM groups run on
- *                   wide single-CTA 256 x 256 tiles (two M = 128 MMAs share
- *                   each B tile; one tile in TMEM at a time).  Default 2 (the
- *                   vocab backward; the automatic V-chunk then holds at least
- *                   two long tiles per SM).  Takes precedence over cta_pair.
- *   "b_multicast"   bitmask (same bits as cta_pair) of GEMM groups run on
- *                   2-CTA clusters that share the B tile by TMA multicast
- *                   (two 128 x 256 tiles, per-CTA MMAs); wins over cta_pair
- *   "mixed_tiles"   bitmask (same bits as cta_pair) of GEMM groups run on a
- *                   kernel mixing wide tiles with 128 x 256 tiles for the
- *                   short-K dlogits (variable-size operand stages); wins
- *                   over wide_tiles.  Default 0.
- *   "store_logits"  bf16 path: 1 (default) = the forward vocab GEMM also stores
- *                   the logits as fp16 [T, V] (workspace grows by 2 T V bytes)
- *                   and the backward makes each V-chunk's dlogits from them
- *                   with an elementwise kernel that starts beside the
- *                   previous chunk's launch; 2 = the same, serialised; 0 =
- *                   recompute the logits chunk by chunk on the tensor cores
- *   "debug_skip_dlogits" timing only: 1 = skip the elementwise dlogits of
- *                   chunks >= 1 (gradients WRONG; measures what the overlap
- *                   could still gain)
- *   "db_gemm"       how db_out (F_c bias) is summed: 0 = column-sum kernels
- *                   after each vocab-backward launch; 1 = a GEMM against ones
- *                   inside those launches (single-CTA tiles); 2 = by the
- *                   dlogits kernels (stored logits); -1 (default) = 2 with
- *                   stored logits, else 0
- *   "wide_multicast" bitmask (same bits as cta_pair) of GEMM groups run on
- *                   2-CTA clusters of wide 256 x 256 tiles sharing the B tile
- *                   by TMA multicast (512 rows per cluster); wins over
- *                   wide_tiles.  Default 0.
+ *   "store_logits"  ABLATION (violates "logits never round-tripped through
+ *                   HBM"; kept to quantify the trade): 1 = the forward vocab
+ *                   GEMM also stores the logits as fp16 [T, V] (workspace
+ *                   grows by 2 T V bytes) and the backward makes each
+ *                   V-chunk's dlogits from them with an elementwise kernel
+ *                   beside the previous chunk's launch; 2 = the same,
+ *                   serialised; 0 (default) = the persistent recompute launch
+ *   "wide_tiles"    bitmask of GEMM groups on wide single-CTA 256 x 256 tiles
+ *                   (1 = forward vocab / projection, 2 = stored-logits
+ *                   vocab-backward launches, 4 = projection backward, 8 = the
+ *                   debug GEMM entry).  Default 2.
+ *   "debug_skip_dlogits" stored-logits ablation, timing only: 1 = skip the
+ *                   elementwise dlogits of chunks >= 1 (gradients WRONG)
+ *   "db_gemm"       stored-logits ablation: how db_out (F_c bias) is summed:
+ *                   0 = column-sum kernels after each launch; 2 = by the
+ *                   dlogits kernels; -1 (default) = 2
  *   "gemm_trace"    device address of an int64 buffer (16 per tile) that the
  *                   next tcgen05 launches fill with per-tile clock64 stamps
  *                   (0 = off; debug only)

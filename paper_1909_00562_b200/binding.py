@@ -28,7 +28,8 @@ EXPORTS = [
     "attn_softmax_host_staging_size", "attn_softmax_fwd_bwd_host",
     "attn_softmax_prefetch_host", "attn_softmax_fwd_bwd_staged",
     "attn_softmax_check_ids", "attn_grad_allreduce", "attn_comm_get_unique_id",
-    "attn_comm_init", "attn_comm_destroy", "attn_last_error", "attn_version",
+    "attn_comm_init", "attn_comm_destroy", "attn_comm_poll", "attn_comm_nranks",
+    "attn_last_error", "attn_version",
     "attn_softmax_workspace_views", "attn_debug_gemm_bf16",
     "attn_softmax_set_option", "attn_softmax_stage_count",
     "attn_softmax_stage_time", "attn_softmax_last_launches",
@@ -111,6 +112,10 @@ def lib() -> ctypes.CDLL:
     L.attn_comm_init.restype = ctypes.c_int
     L.attn_comm_destroy.argtypes = [_P]
     L.attn_comm_destroy.restype = ctypes.c_int
+    L.attn_comm_poll.argtypes = [_P, ctypes.c_int64]
+    L.attn_comm_poll.restype = ctypes.c_int
+    L.attn_comm_nranks.argtypes = [_P]
+    L.attn_comm_nranks.restype = ctypes.c_int
     L.attn_last_error.argtypes = []
     L.attn_last_error.restype = ctypes.c_char_p
     L.attn_version.argtypes = []
@@ -274,6 +279,17 @@ def attn_comm_init(uid: bytes, nranks: int, rank: int, device: int):
 
 def attn_comm_destroy(comm):
     _check(lib().attn_comm_destroy(comm))
+
+
+def attn_comm_poll(comm, timeout_ms: int = 0):
+    """Wait for the communicator's enqueued collectives, polling NCCL's
+    asynchronous error state; raises AttnError (ATTN_ERR_NCCL) on an error or
+    after timeout_ms (> 0) -- the communicator is then aborted."""
+    _check(lib().attn_comm_poll(comm, int(timeout_ms)))
+
+
+def attn_comm_nranks(comm) -> int:
+    return int(lib().attn_comm_nranks(comm))
 
 
 def attn_debug_gemm_bf16(M, N, K, A, a_mn, B, b_mn, C, stream=None):

@@ -1,6 +1,7 @@
 """Build libattnsm.so in-tree with nvcc for sm_100a (no JIT cache)."""
 from __future__ import annotations
 
+import glob
 import os
 import shutil
 import subprocess
@@ -10,8 +11,9 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "libattnsm.so")
 SOURCES = ["attn_softmax.cu", "comm.cu", "adam.cu"]
-HEADERS = ["ptx.cuh", "epilogue.cuh", "gemm_tc.cuh", "gemm_simt.cuh",
-           "small_kernels.cuh", "comm.h"]
+# every header of csrc/ (a stale .so after a header edit runs old code)
+HEADERS = sorted(os.path.basename(f) for f in glob.glob(os.path.join(CSRC, "*.cuh")) +
+                 glob.glob(os.path.join(CSRC, "*.h")))
 
 
 def nvcc() -> str:

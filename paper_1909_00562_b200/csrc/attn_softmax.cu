@@ -31,7 +31,7 @@
 #include "gemm_simt.cuh"
 #include "gemm_tc.cuh"
 #include "small_kernels.cuh"
-#include "vocab_bwd.cuh"
+#include "vocab.cuh"
 
 using namespace attnsm;
 
@@ -104,32 +104,18 @@ extern "C" attn_status_t attn_softmax_stage_time(int i, const char** name, float
 extern "C" long long attn_softmax_last_launches(void) { return g_launches; }
 
 // ------------------------------------------------------------------ options
-// GEMM groups, the bits of the cta_pair / b_multicast / wide_tiles
-// options: forward vocab + projection, vocab backward chunks, projection
+// GEMM groups, the bits of the wide_tiles option: forward vocab +
+// projection, vocab backward chunks (stored-logits ablation), projection
 // backward, the debug GEMM entry
 enum : int { PAIR_FWD = 1, PAIR_VBWD = 2, PAIR_PBWD = 4, PAIR_DEBUG = 8 };
-// cta_pair option: bitmask of GEMM groups run on CTA pairs (see PAIR_*)
-#define PAIR_DEFAULT 8   /* stage GEMMs on single CTAs (same-box A/B: fastest); debug entry paired */
 // debug_epilogue option: 0 = fp32 TMA store, 1 = accumulator read only (no store)
 static int g_debug_epi = 0;
 static int g_opt_mn3d = 1;  // MN-major operands via one 3D TMA box
-static int g_opt_pair = PAIR_DEFAULT;
-static int g_opt_mcast = 0;   // "b_multicast": bitmask of GEMM groups on 2-CTA clusters sharing B
 // "wide_tiles": bitmask of GEMM groups on 256 x 256 single-CTA tiles; default
-// the vocab backward (same-box A/B at C1 / C3 / C4: -6 to -8% per step)
+// the stored-logits ablation's vocab-backward launches
 static int g_opt_wide = PAIR_VBWD;
-// "mixed_tiles": bitmask of GEMM groups run on the mixed kernel (wide tiles,
-// plus 128 x 256 tiles for problems flagged narrow -- the dlogits -- in a
-// variable-stage ring); takes precedence over wide_tiles
-static int g_opt_mixed = 0;
-// "wide_multicast": bitmask of GEMM groups on 2-CTA clusters of wide tiles
-// sharing B (kPair 6); takes precedence over wide_tiles
-static int g_opt_widemc = 0;
-// "db_gemm": how db_out is summed: 0 column-sum kernels after each launch, 1
-// a ones GEMM inside the vocab-backward launches, 2 by the dlogits kernels
-// (stored logits only); -1 (default) = 2 with stored logits, else 0 (a
-// column-sum launch between the overlapped dlogits kernel and the next GEMM
-// launch would serialise the chain; see DESIGN.md for the measurements)
+// "db_gemm" (stored-logits ablation only): db_out summed by 0 column-sum
+// kernels after each launch, 2 the dlogits kernels (default -1 = 2)
 static int g_opt_db_gemm = -1;
 constexpr int kEwParts = 320;   // row-group partial rows of the dlogits kernels' column sums
 // "store_logits": the bf16 path's forward vocab GEMM also stores the logits as
@@ -138,13 +124,9 @@ constexpr int kEwParts = 320;   // row-group partial rows of the dlogits kernels
 // 1 (default): chunk c+1's kernel starts beside launch c (PDL, waits at its
 // end); 2: serialised; 0: recompute (same-box A/B at C1: 1.92 / 1.98 / 2.15 ms)
 static int g_opt_store_logits = 0;
-// "vocab_bwd_persistent": 1 (default) = the bf16 vocab backward (recomputed
-// logits) as ONE persistent launch with dependency counters (vocab_bwd.cuh);
-// 0 = one GEMM launch per V-chunk (round-1 design, kept for A/B)
-static int g_opt_vb = 1;
 // "dl_budget_mb": bytes of the dL chunk scratch (all NB buffers) the V-chunk
 // width is sized to, so it stays L2-resident; "dl_buffers": NB
-static int64_t g_opt_dl_budget_mb = 96;
+static int64_t g_opt_dl_budget_mb = 120;
 static int g_opt_dl_nbuf = 3;
 // "vb_last_g2_first": last block of the persistent backward dispatches the
 // long dW_out tiles before the dHc tiles (shorter tail)
@@ -156,8 +138,13 @@ static int g_opt_vb_pair = 1;
 // G2(c), G1(c+1)]; 1 = [G1(c+1), G3(c), G2(c)] (chunk c's consumers run a
 // whole G1 set after its producers; needs dl_buffers >= 3)
 static int g_opt_vb_order = 1;
-static int g_vb_debug = 0;
-static int g_opt_vb_l2 = 3;   // "vb_l2hints": VbParams::l2hints   // "vb_debug": timing experiments (vocab_bwd.cuh VbParams::debug)
+static int g_vb_debug = 0;    // "vb_debug": timing experiments (vocab.cuh VbParams::debug)
+static int g_opt_vb_l2 = 3;   // "vb_l2hints": VbParams::l2hints
+// "vb_fwd_fused": F4 + F5 inside the persistent launch (G0 tiles on CTA pairs,
+// LSE by its warps 8-9) instead of the single-CTA forward GEMM + lse_reduce
+// kernel before it (same-box C1: 2.28 vs 2.17 ms per step -- the power-capped
+// clock runs lower under the pair tiles' forward)
+static int g_opt_vb_fwd = 0;
 // "n_fast": dispatch the vocab-backward GEMMs' column tiles of one row block
 // back to back (their shared A block -- the dlogits chunk -- then leaves HBM once)
 static int g_opt_n_fast = 1;
@@ -171,7 +158,14 @@ static int64_t g_opt_gemm_ctas = 0;
 // before touching its results)
 static int g_opt_pdl = 1;
 
+// Options are read by a call from its start to its last enqueue under this
+// lock (and written under it), so a concurrent set_option never changes a call
+// in flight; recursive because entry points call each other.
+static std::recursive_mutex g_opt_mu;
+#define OPT_LOCK std::lock_guard<std::recursive_mutex> opt_lock_(g_opt_mu)
+
 extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value) {
+  OPT_LOCK;
   if (!key) return fail(ATTN_ERR_INVALID_ARG, "set_option: key is NULL");
   if (!strcmp(key, "vocab_chunk")) {
     if (value < 0 || value % 256 != 0)
@@ -188,20 +182,12 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
     g_trace = reinterpret_cast<long long*>(value);
     return ATTN_OK;
   }
-  if (!strcmp(key, "mixed_tiles")) {
-    g_opt_mixed = (int)value;
-    return ATTN_OK;
-  }
   if (!strcmp(key, "debug_skip_dlogits")) {
     g_debug_skip_ew = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "n_fast")) {
     g_opt_n_fast = (int)value;
-    return ATTN_OK;
-  }
-  if (!strcmp(key, "vocab_bwd_persistent")) {
-    g_opt_vb = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "dl_budget_mb")) {
@@ -212,6 +198,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   if (!strcmp(key, "dl_buffers")) {
     if (value < 1 || value > 4) return fail(ATTN_ERR_INVALID_ARG, "dl_buffers must be in [1, 4]");
     g_opt_dl_nbuf = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "vb_fwd_fused")) {
+    g_opt_vb_fwd = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "vb_l2hints")) {
@@ -246,20 +236,8 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
     g_opt_db_gemm = (int)value;
     return ATTN_OK;
   }
-  if (!strcmp(key, "wide_multicast")) {
-    g_opt_widemc = (int)value;
-    return ATTN_OK;
-  }
   if (!strcmp(key, "wide_tiles")) {
     g_opt_wide = (int)value;
-    return ATTN_OK;
-  }
-  if (!strcmp(key, "b_multicast")) {
-    g_opt_mcast = (int)value;
-    return ATTN_OK;
-  }
-  if (!strcmp(key, "cta_pair")) {
-    g_opt_pair = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "mn_3d_tma")) {
@@ -388,7 +366,6 @@ struct GemmDesc {
   int b_koff = 0;
   long long out_bstride = 0;   // batch stride of the epilogue output (elements)
   int bn = 0;        // tile columns (0 = 256); < 256 only for K-major B on single CTAs
-  int narrow = 0;    // mixed launches (kPair = 5): 128 x 256 tiles for this problem
   int n_fast = 0;    // dispatch the column tiles of a row block together (A read once via L2)
   EpiParams epi{};
 };
@@ -420,21 +397,17 @@ static attn_status_t operand_map(CUtensorMap* m, const Operand& o, bool mn, int 
   return encode(m, o.p, false, 3, dims, st, box);
 }
 
-// pair: 1 = 128 x 256 tiles, 2 = CTA pair (256 rows, B split), 6 = wide
-// multicast (2 CTAs x 256 rows, B split and multicast), 4 = wide
-// single CTA (256 rows, whole B tile)
+// pair: 1 = 128 x 256 tiles, 4 = wide single CTA (256 rows, whole B tile)
 static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr, int tile_begin,
                              int pair) {
   memset(&pr, 0, sizeof(pr));
   const int bn = g.bn > 0 ? g.bn : TC_BN;
-  if (bn != TC_BN && (bn % 16 != 0 || bn > TC_BN || g.b_mn || g.b_nsplit || pair == 2 || pair == 3 || pair == 6))
-    return fail(ATTN_ERR_UNSUPPORTED, "tile width %d needs a K-major B on single CTAs", bn);
-  const bool narrow = pair == 5 && g.narrow;
-  const int tile_m = (pair == 1 || narrow) ? TC_BM : pair == 6 ? 4 * TC_BM : 2 * TC_BM;
-  const int b_rows = (pair == 2 || pair == 6) ? TC_BN / 2 : bn;
+  if (bn != TC_BN && (bn % 16 != 0 || bn > TC_BN || g.b_mn || g.b_nsplit))
+    return fail(ATTN_ERR_UNSUPPORTED, "tile width %d needs a K-major B", bn);
+  const int tile_m = pair == 1 ? TC_BM : 2 * TC_BM;
+  const int b_rows = bn;
   pr.M = g.M; pr.N = g.N; pr.K = g.K; pr.batch = g.batch;
   pr.bn = bn;
-  pr.narrow = narrow ? 1 : 0;
   pr.n_fast = g.n_fast && g_opt_n_fast;
   pr.tiles_m = (g.M + tile_m - 1) / tile_m;
   pr.tiles_n = (g.N + bn - 1) / bn;
@@ -504,7 +477,7 @@ static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr
                           (cuuint64_t)(g.epi.stash_ld * 4 * (long long)g.M)};
       if ((st = encode(&maps[3], g.epi.stash_f32, true, 3, d2, s2, box)) != ATTN_OK) return st;
     }
-  } else if ((k != EPI_LSE || g.epi.out) && k != EPI_NONE && k != EPI_TOPK && k != EPI_COL0_F32) {
+  } else if ((k != EPI_LSE || g.epi.out) && k != EPI_NONE && k != EPI_TOPK) {
     // (LSE with `out`: the fp16 logits of option store_logits)
     const bool f32 = epi_out_is_f32(k);
     const int esz = f32 ? 4 : 2;
@@ -544,23 +517,37 @@ static void fill_simt(const GemmDesc& g, SimtProblem& pr, int tile_begin) {
 
 static int tc_smem_bytes() { return TC_SMEM_BYTES; }
 
-// g_opt_pair: vocab / projection GEMMs on CTA pairs (cta_group::2)
+// Per-device "max dynamic shared memory" attribute of a kernel (set once per
+// device, under a lock: the attribute belongs to the device's context).
+template <typename K>
+static attn_status_t ensure_smem_attr(K kernel, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;   // (kernel, device)
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  const void* key = reinterpret_cast<const void*>(kernel);
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : done)
+    if (e.first == key && e.second == dev) return ATTN_OK;
+  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.emplace_back(key, dev);
+  return ATTN_OK;
+}
+
+
 
 template <typename OutT, int kPair, bool kDecode = false>
 static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, cudaStream_t stream,
-                                       int group_bit, int ctas = 0) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<OutT, true, kPair, kDecode>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes()));
-    attr_set = true;
-  }
+                                       int ctas = 0) {
+  attn_status_t st;
+  if ((st = ensure_smem_attr(gemm_tc_kernel<OutT, true, kPair, kDecode>, tc_smem_bytes())) !=
+      ATTN_OK)
+    return st;
   TcParams P;
   memset(&P, 0, sizeof(P));
   int tiles = 0;
   for (int i = 0; i < n; ++i) {
-    attn_status_t st = fill_tc(gs[i], P.maps[i], P.prob[i], tiles,
-                               kPair >= 4 ? kPair : (kPair >= 2 ? 2 : 1));
+    st = fill_tc(gs[i], P.maps[i], P.prob[i], tiles, kPair);
     if (st != ATTN_OK) return st;
     tiles += P.prob[i].tiles_m * P.prob[i].tiles_n * P.prob[i].batch;
   }
@@ -570,64 +557,32 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   P.trace = (g_trace_launch < 0 || g_trace_launch == g_launches) ? g_trace : nullptr;
   if (tiles == 0) return ATTN_OK;
   const DevInfo di = dev_info();
-  const int csize = TcCfg<kPair>::CLUSTER;
-  int units = (ctas > 0 ? ctas : g_opt_gemm_ctas > 0 ? (int)g_opt_gemm_ctas : di.sms) / csize;
+  int units = ctas > 0 ? ctas : g_opt_gemm_ctas > 0 ? (int)g_opt_gemm_ctas : di.sms;
   units = std::max(1, std::min(units, tiles));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(units * csize);
+  cfg.gridDim = dim3(units);
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = tc_smem_bytes();
   cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
-  int na = 0;
-  if (csize > 1) {
-    attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = csize;
-    attr[na].val.clusterDim.y = 1;
-    attr[na].val.clusterDim.z = 1;
-    ++na;
-  }
-  if (g_opt_pdl) {
-    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[na].val.programmaticStreamSerializationAllowed = 1;
-    ++na;
-  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = na;
+  cfg.numAttrs = g_opt_pdl ? 1 : 0;
   CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<OutT, true, kPair, kDecode>, P));
   ++g_launches;
   return ATTN_OK;
 }
 
-// pair = 2 puts the group on CTA pairs; batched (attention) groups stay on
-// single CTAs (a sentence has <= 128 decoder rows).
-// `group_bit` selects the bit of the "cta_pair" option that enables pairs for
-// this GEMM group (0 = never paired).
+// `group_bit` selects the bit of the "wide_tiles" option that puts this GEMM
+// group on wide 256 x 256 tiles (0 = never); batched (attention) groups stay
+// on 128 x 256 tiles (a sentence has <= 128 decoder rows).
 template <typename OutT>
 static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cudaStream_t stream,
                                      int group_bit = 0, int ctas = 0) {
-  if (group_bit && (g_opt_mixed & group_bit))
-    return launch_tc_group_k<OutT, 5>(gs, n, counter, stream, group_bit, ctas);
-  if (group_bit && (g_opt_widemc & group_bit))
-    return launch_tc_group_k<OutT, 6>(gs, n, counter, stream, group_bit, ctas);
   if (group_bit && (g_opt_wide & group_bit))
-    return launch_tc_group_k<OutT, 4>(gs, n, counter, stream, group_bit, ctas);
-  if (group_bit && (g_opt_mcast & group_bit))
-    return launch_tc_group_k<OutT, 3>(gs, n, counter, stream, group_bit, ctas);
-  if (group_bit && (g_opt_pair & group_bit))
-    return launch_tc_group_k<OutT, 2>(gs, n, counter, stream, group_bit, ctas);
-  return launch_tc_group_k<OutT, 1>(gs, n, counter, stream, group_bit, ctas);
-}
-
-// The engine variant launch_tc_group picks for a group (1 / 2 / 3 / 4 / 5 / 6).
-static int group_kpair(int group_bit) {
-  if (!group_bit) return 1;
-  if (g_opt_mixed & group_bit) return 5;
-  if (g_opt_widemc & group_bit) return 6;
-  if (g_opt_wide & group_bit) return 4;
-  if (g_opt_mcast & group_bit) return 3;
-  if (g_opt_pair & group_bit) return 2;
-  return 1;
+    return launch_tc_group_k<OutT, 4>(gs, n, counter, stream, ctas);
+  return launch_tc_group_k<OutT, 1>(gs, n, counter, stream, ctas);
 }
 
 // Launch a plain kernel, as a programmatic dependent of the previous kernel
@@ -717,12 +672,11 @@ struct Plan {
   int nchunks;
   size_t off_lens, off_counters, off_blockpart, off_alpha, off_dalpha, off_ctx, off_hc, off_part,
       off_tgtlogit, off_lse, off_nll, off_rowscale, off_dl, off_dhc, off_dz, off_dhc2, off_abf,
-      off_debf, off_q, off_dbpart, off_ones, off_logits;
+      off_debf, off_q, off_dbpart, off_logits;
   int Mp;             // bf16 path: row stride of the bf16 alpha / de operands (64-multiple)
   int ald;            // row stride of the fp32 alpha stash (bf16 path: Mp, for TMA stores)
-  long long Tld;      // row stride of the ones operand of the db_out GEMM (8-multiple >= T)
   bool store_logits;  // bf16 path, option store_logits: fp16 logits [T, Vld] in the workspace
-  bool vb;            // bf16 path: persistent vocab backward (vocab_bwd.cuh)
+  bool vb;            // bf16 path: persistent vocabulary launch (vocab.cuh)
   int nbuf;           // dL chunk buffers
   size_t off_vbctr, n_vbctr;   // its dependency counters (unsigned), zeroed per call
   long long Vld;
@@ -779,6 +733,8 @@ static long long model_chunk_width(long long T, long long d, long long V) {
   return best_vc;
 }
 
+static size_t vb_ctr_words(const Plan& p);
+
 static Plan make_plan(const attn_shape_t* s) {
   Plan p;
   p.B = s->batch; p.N = s->tgt_len; p.M = s->src_len; p.d = s->hidden; p.V = s->vocab;
@@ -790,31 +746,22 @@ static Plan make_plan(const attn_shape_t* s) {
   p.part_ld = p.bf16 ? 2 * p.ntn : p.ntn;
   const long long vpad = (p.V + 255) / 256 * 256;
   long long vc = g_opt_vocab_chunk;
-  if (vc <= 0) {
-    // about 12 chunks per step: wide enough that every chunk launch keeps
-    // all SMs busy with long dW_out / dHc tiles, narrow enough that the
-    // double-buffered dlogits chunk mostly stays in L2 (measured sweep at
-    // C1 / C3 / C4)
-    vc = ((p.V + 11) / 12 + 255) / 256 * 256;
-    vc = std::max(vc, 1024ll);
-    if (p.bf16 && g_opt_store_logits && group_kpair(PAIR_VBWD) == 4) {
-      vc = model_chunk_width(p.T, p.d, p.V);
-    } else if (p.bf16 && (g_opt_wide & PAIR_VBWD)) {
-      // wide 256 x 256 tiles: widen the chunk until one launch holds at least
-      // two long (dW_out + dHc) tiles per SM of a B200 (148 SMs; a fixed
-      // constant so the workspace size does not depend on the device)
-      const long long ntd = (p.d + 255) / 256, ntt = (p.T + 255) / 256;
-      const long long need = 2 * 148 / ntd - ntt;   // dW_out row tiles per chunk
-      if (need > 0) vc = std::max(vc, need * 256);
-    }
-  }
   p.store_logits = p.bf16 && g_opt_store_logits;
-  p.vb = p.bf16 && !p.store_logits && g_opt_vb;
+  p.vb = p.bf16 && !p.store_logits;
   p.nbuf = p.vb ? g_opt_dl_nbuf : 2;
-  if (p.vb && g_opt_vocab_chunk <= 0) {
-    // the NB dL buffers [T, Vc] bf16 fit the L2 budget
-    vc = (g_opt_dl_budget_mb << 20) / ((long long)p.nbuf * p.T * 2) / 256 * 256;
-    vc = std::max(vc, 256ll);
+  if (vc <= 0) {
+    if (p.vb) {
+      // the NB dL buffers [T, Vc] bf16 fit the L2 budget
+      vc = (g_opt_dl_budget_mb << 20) / ((long long)p.nbuf * p.T * 2) / 256 * 256;
+      vc = std::max(vc, 256ll);
+    } else if (p.store_logits && (g_opt_wide & PAIR_VBWD)) {
+      vc = model_chunk_width(p.T, p.d, p.V);
+    } else {
+      // fp32 path (and the stored-logits ablation on 128 x 256 tiles): about
+      // 12 chunks per step
+      vc = ((p.V + 11) / 12 + 255) / 256 * 256;
+      vc = std::max(vc, 1024ll);
+    }
   }
   vc = std::min(vc, vpad);
   // one tile counter per tcgen05 launch: keep the chunk count well inside
@@ -845,28 +792,25 @@ static Plan make_plan(const attn_shape_t* s) {
   p.off_abf = take(p.bf16 ? 2 * p.T * p.Mp : 0);
   p.off_debf = take(p.bf16 ? 2 * p.T * p.Mp : 0);
   p.off_q = take(p.elt * p.T * p.d);   // Eq. 2 general score: Q = H W_alpha
-  p.off_dbpart = take(sizeof(float) * std::max<size_t>(16 * (size_t)p.Vc,   // F_c bias: column-sum partials
-                                                         p.bf16 ? (size_t)kEwParts * p.V : 0));
-  p.Tld = (p.T + 7) / 8 * 8;
-  p.off_ones = take(p.bf16 ? 2 * 16 * (size_t)p.Tld : 0);   // F_c bias, bf16 path: [16, Tld] ones
+  // F_c bias: column-sum partials ([T/32][V] for the persistent launch's dL column sums)
+  p.off_dbpart = take(sizeof(float) * std::max<size_t>(
+      16 * (size_t)p.Vc, p.bf16 ? (size_t)std::max<long long>(kEwParts, (p.T + 31) / 32) * p.V : 0));
   p.Vld = (p.V + 7) / 8 * 8;
   p.off_logits = take(p.store_logits ? 2 * (size_t)p.T * p.Vld : 0);
-  {   // counters of the persistent vocab backward (sized for single-CTA tiles, the larger)
-    const size_t nrb = (p.T + 127) / 128, ndt = (p.d + VB_BN - 1) / VB_BN;
-    const size_t ncolf = p.Vc / VB_BN;
-    p.n_vbctr = p.vb ? 1 + p.nchunks * (nrb + ncolf + 2) + nrb * ndt : 0;
-    p.off_vbctr = take(sizeof(unsigned) * p.n_vbctr);
-  }
+  p.n_vbctr = p.vb ? vb_ctr_words(p) : 0;   // counters of the persistent vocabulary launch
+  p.off_vbctr = take(sizeof(unsigned) * p.n_vbctr);
   p.total = o;
   return p;
 }
 
 extern "C" size_t attn_softmax_workspace_size(const attn_shape_t* s) {
+  OPT_LOCK;
   if (check_shape(s) != ATTN_OK) return 0;
   return make_plan(s).total;
 }
 
 extern "C" attn_status_t attn_softmax_workspace_views(const attn_shape_t* s, attn_ws_views_t* out) {
+  OPT_LOCK;
   attn_status_t st = check_shape(s);
   if (st != ATTN_OK) return st;
   if (!out) return fail(ATTN_ERR_INVALID_ARG, "out is NULL");
@@ -975,7 +919,6 @@ struct Bufs {
   float* lse; float* nll; float* rowscale; void* dl[2]; float* dhc; void* dz; float* dhc2;
   void* abf; void* debf; float* dhpart; void* dcbf;   // bf16 path
   float* dbpart;   // F_c bias: [16, Vc] column-sum partials (when not a GEMM)
-  void* ones;      // F_c bias, bf16 path: [16, Tld] bf16 ones (B operand of the db_out GEMM)
   void* logits;    // option store_logits: fp16 [T, Vld]
   unsigned* vbctr; // persistent vocab backward: tile counter + dependency counters
   void* q;    // Eq. 2 general score: Q = H W_alpha [T, d] (dtype)
@@ -1009,7 +952,6 @@ static Bufs carve(const Plan& p, void* ws) {
   b.dcbf = (char*)(b.dhc2 + p.T * p.d);       //            dC bf16 [T, d]
   b.q = w + p.off_q;
   b.dbpart = (float*)(w + p.off_dbpart);
-  b.ones = w + p.off_ones;
   b.logits = p.store_logits ? w + p.off_logits : nullptr;
   b.vbctr = (unsigned*)(w + p.off_vbctr);
   b.dq = b.dz;
@@ -1098,7 +1040,6 @@ static GemmDesc g_dlogits(const Plan& p, const Bufs& b, const void* W_out, const
   g.M = (int)p.T; g.N = vcc; g.K = p.d;
   g.a0 = kmaj(b.hc, p.T, p.d, p.d);
   g.b0 = kmaj((const char*)W_out + (size_t)c0 * p.d * p.elt, vcc, p.d, p.d);
-  g.narrow = 1;   // short K: 128 x 256 tiles in a mixed launch
   g.epi.kind = EPI_DLOGITS; g.epi.out = b.dl[c & 1]; g.epi.ldo = p.Vc;
   g.epi.ncols_valid = vcc; g.epi.ncols_store = p.bf16 ? vcc : p.Vc; g.epi.col_base = c0;
   g.epi.lse = b.lse; g.epi.rowscale = b.rowscale; g.epi.tgt = tgt;
@@ -1116,19 +1057,6 @@ static GemmDesc g_dwout(const Plan& p, const Bufs& b, float* dW_out, int c) {
   g.epi.kind = EPI_STORE_F32; g.epi.out = dW_out + (size_t)c0 * p.d; g.epi.ldo = p.d;
   g.epi.ncols_valid = p.d; g.epi.ncols_store = p.d;
   g.n_fast = 1;
-  return g;
-}
-// B1, chunk c, F_c bias: db_out[c0 + v] = sum_t dlogits_c[t, v], as the GEMM
-// dlogits_c^T [vcc, T] x ones [16, T]^T with only column 0 kept: the A operand
-// is dW_out's, read once more by the tensor cores in the same launch
-static GemmDesc g_dbout(const Plan& p, const Bufs& b, float* db_out, int c) {
-  GemmDesc g;
-  const int c0 = c * p.Vc, vcc = std::min(p.Vc, p.V - c0);
-  g.M = vcc; g.N = 16; g.K = (int)p.T; g.bn = 16;
-  g.a_mn = 1; g.a0 = mnmaj(b.dl[c & 1], p.T, vcc, p.Vc);
-  g.b0 = kmaj(b.ones, 16, p.T, p.Tld);
-  g.epi.kind = EPI_COL0_F32; g.epi.out = db_out + c0;
-  g.epi.ncols_valid = 1; g.epi.ncols_store = 1;
   return g;
 }
 // B1, chunk c: dHc (+)= dlogits_c W_out[c]   (B MN-major, K offset c0)
@@ -1296,31 +1224,15 @@ static attn_status_t attention_backward_tc(const Plan& p, const void* H, const v
   return launch_tc_group<__nv_bfloat16>(ga, 2, next(ctx_), stream, PAIR_PBWD);
 }
 
-// ---------------------------------------------------------------- persistent vocab backward
-// Per-device "max dynamic shared memory" attribute of a kernel (set once per
-// device, under a lock: the attribute belongs to the device's context).
-template <typename K>
-static attn_status_t ensure_smem_attr(K kernel, int bytes) {
-  static std::mutex mu;
-  static std::vector<std::pair<const void*, int>> done;   // (kernel, device)
-  int dev = 0;
-  CUDA_TRY(cudaGetDevice(&dev));
-  const void* key = reinterpret_cast<const void*>(kernel);
-  std::lock_guard<std::mutex> lk(mu);
-  for (auto& e : done)
-    if (e.first == key && e.second == dev) return ATTN_OK;
-  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  done.emplace_back(key, dev);
-  return ATTN_OK;
-}
-
-// B1 as one launch (vocab_bwd.cuh): tensor maps, dispatch blocks, counters.
-// Counter layout in `ctr` (zeroed by the caller): [0] tile counter, then
-// rowdone [nchunks][nrb], coldone [nchunks][ncolf], consumed [nchunks],
-// g2done [nchunks], dhcdone [nrb][ndt] (vb_ctr_layout).
+// F4 + F5 + B1 as one launch (vocab.cuh): tensor maps, dispatch blocks,
+// counters.  Counter layout in `ctr` (zeroed by the caller): [0] tile
+// counter, [1] g5count (LSE CTA-portions), then g0done [nrb], lsedone [nrb], rowdone
+// [nchunks][nrb], coldone [nchunks][ncolf], consumed [nchunks], g2done
+// [nchunks], dhcdone [nrb][ndt], and blockpart (double [nrb * CTAS]) at the
+// end, 8-byte aligned (vb_ctr_layout).
 struct VbLayout {
   int TM, nrb, ndt, ncolf;
-  size_t rowdone, coldone, consumed, g2done, dhcdone, total;
+  size_t g0done, lsedone, rowdone, coldone, consumed, g2done, dhcdone, blockpart, total;
 };
 static VbLayout vb_ctr_layout(const Plan& p, bool pair) {
   VbLayout L;
@@ -1329,93 +1241,104 @@ static VbLayout vb_ctr_layout(const Plan& p, bool pair) {
   L.ndt = (p.d + VB_BN - 1) / VB_BN;
   L.ncolf = p.Vc / VB_BN;
   const size_t nch = p.nchunks;
-  L.rowdone = 1;
+  L.g0done = 2;
+  L.lsedone = L.g0done + L.nrb;
+  L.rowdone = L.lsedone + L.nrb;
   L.coldone = L.rowdone + nch * L.nrb;
   L.consumed = L.coldone + nch * L.ncolf;
   L.g2done = L.consumed + nch;
   L.dhcdone = L.g2done + nch;
-  L.total = L.dhcdone + (size_t)L.nrb * L.ndt;
+  L.blockpart = (L.dhcdone + (size_t)L.nrb * L.ndt + 1) & ~(size_t)1;   // in unsigned units
+  L.total = L.blockpart + 2 * (size_t)L.nrb * (pair ? 2 : 1);
   return L;
 }
+// unsigned words of the counter region, for the larger (single-CTA) layout
+static size_t vb_ctr_words(const Plan& p) { return vb_ctr_layout(p, false).total; }
+
+struct VbArgs {
+  const void* hc; const void* W_out; void* dl; float* dhc; float* dW_out;
+  float2* part; int part_ld; float* tgt_logit; float* lse; float* nll; float* rowscale;
+  float* loss; float loss_scale; const int* tgt; const int* tgt_len; const void* bias;
+  float* db_part; unsigned* ctr;
+  bool fwd;   // F4 + F5 in this launch (else lse / rowscale / tgt_logit are inputs)
+};
 
 template <bool kPair>
-static attn_status_t launch_vocab_bwd_k(const Plan& p, const void* hc, const void* W_out, void* dl,
-                                        float* dhc, float* dW_out, const float* lse,
-                                        const float* rowscale, const int* tgt,
-                                        const float* tgt_logit, const void* bias, unsigned* ctr,
-                                        int ctas, cudaStream_t stream) {
+static attn_status_t launch_vocab_k(const Plan& p, const VbArgs& a, int ctas, cudaStream_t stream) {
   using Cfg = VbCfg<kPair>;
   attn_status_t st;
-  if ((st = ensure_smem_attr(vocab_bwd_kernel<kPair>, VB_SMEM_BYTES)) != ATTN_OK) return st;
+  if ((st = ensure_smem_attr(vocab_kernel<kPair>, VB_SMEM_BYTES)) != ATTN_OK) return st;
   static VbParams P;   // large (blk_start): filled per call under the lock
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
   memset(&P, 0, sizeof(P));
   const long long T = p.T, d = p.d, V = p.V, Vc = p.Vc, NB = p.nbuf;
   const cuuint32_t brows = Cfg::B_ROWS;
-  {   // H_c [T, d]: K-major A of G1
+  {   // H_c [T, d]: K-major A of G0 / G1
     cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)T, 1};
     cuuint64_t str[2] = {(cuuint64_t)(d * 2), (cuuint64_t)(T * d * 2)};
     cuuint32_t box[3] = {64, 128, 1};
-    if ((st = encode(&P.m_hc_k, hc, 0, 3, dims, str, box)) != ATTN_OK) return st;
+    if ((st = encode(&P.m_hc_k, a.hc, 0, 3, dims, str, box)) != ATTN_OK) return st;
   }
-  {   // W_out [V, d]: K-major B of G1
+  {   // W_out [V, d]: K-major B of G0 / G1
     cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)V, 1};
     cuuint64_t str[2] = {(cuuint64_t)(d * 2), (cuuint64_t)(V * d * 2)};
     cuuint32_t box[3] = {64, brows, 1};
-    if ((st = encode(&P.m_wo_k, W_out, 0, 3, dims, str, box)) != ATTN_OK) return st;
+    if ((st = encode(&P.m_wo_k, a.W_out, 0, 3, dims, str, box)) != ATTN_OK) return st;
   }
   {   // dL [NB][T][Vc]: K-major A of G3
     cuuint64_t dims[3] = {(cuuint64_t)Vc, (cuuint64_t)T, (cuuint64_t)NB};
     cuuint64_t str[2] = {(cuuint64_t)(Vc * 2), (cuuint64_t)(T * Vc * 2)};
     cuuint32_t box[3] = {64, 128, 1};
-    if ((st = encode(&P.m_dl_k, dl, 0, 3, dims, str, box)) != ATTN_OK) return st;
+    if ((st = encode(&P.m_dl_k, a.dl, 0, 3, dims, str, box)) != ATTN_OK) return st;
   }
   {   // W_out as [K = V][N = d] MN-major: 64-column atoms 128 bytes apart
     cuuint64_t dims[4] = {64, (cuuint64_t)V, (cuuint64_t)(d / 64), 1};
     cuuint64_t str[3] = {(cuuint64_t)(d * 2), 128, (cuuint64_t)(V * d * 2)};
     cuuint32_t box[4] = {64, 64, brows / 64, 1};
-    if ((st = encode(&P.m_wo_mn, W_out, 0, 4, dims, str, box)) != ATTN_OK) return st;
+    if ((st = encode(&P.m_wo_mn, a.W_out, 0, 4, dims, str, box)) != ATTN_OK) return st;
   }
   {   // dL as [K = T][M = Vc] MN-major per buffer
     cuuint64_t dims[4] = {64, (cuuint64_t)T, (cuuint64_t)(Vc / 64), (cuuint64_t)NB};
     cuuint64_t str[3] = {(cuuint64_t)(Vc * 2), 128, (cuuint64_t)(T * Vc * 2)};
     cuuint32_t box[4] = {64, 64, 2, 1};
-    if ((st = encode(&P.m_dl_mn, dl, 0, 4, dims, str, box)) != ATTN_OK) return st;
+    if ((st = encode(&P.m_dl_mn, a.dl, 0, 4, dims, str, box)) != ATTN_OK) return st;
   }
   {   // H_c as [K = T][N = d] MN-major
     cuuint64_t dims[4] = {64, (cuuint64_t)T, (cuuint64_t)(d / 64), 1};
     cuuint64_t str[3] = {(cuuint64_t)(d * 2), 128, (cuuint64_t)(T * d * 2)};
     cuuint32_t box[4] = {64, 64, brows / 64, 1};
-    if ((st = encode(&P.m_hc_mn, hc, 0, 4, dims, str, box)) != ATTN_OK) return st;
+    if ((st = encode(&P.m_hc_mn, a.hc, 0, 4, dims, str, box)) != ATTN_OK) return st;
   }
   {   // dL store: bf16 boxes of 32 rows x 64 columns
     cuuint64_t dims[3] = {(cuuint64_t)Vc, (cuuint64_t)T, (cuuint64_t)NB};
     cuuint64_t str[2] = {(cuuint64_t)(Vc * 2), (cuuint64_t)(T * Vc * 2)};
     cuuint32_t box[3] = {64, 32, 1};
-    if ((st = encode(&P.m_dl_st, dl, 0, 3, dims, str, box)) != ATTN_OK) return st;
+    if ((st = encode(&P.m_dl_st, a.dl, 0, 3, dims, str, box)) != ATTN_OK) return st;
   }
   {   // dW_out fp32 [V, d] and dHc fp32 [T, d]: boxes of 32 x 32
     cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)V};
     cuuint64_t str[1] = {(cuuint64_t)(d * 4)};
     cuuint32_t box[2] = {32, 32};
-    if ((st = encode(&P.m_dw_st, dW_out, 1, 2, dims, str, box)) != ATTN_OK) return st;
+    if ((st = encode(&P.m_dw_st, a.dW_out, 1, 2, dims, str, box)) != ATTN_OK) return st;
     cuuint64_t dims2[2] = {(cuuint64_t)d, (cuuint64_t)T};
-    if ((st = encode(&P.m_dhc_st, dhc, 1, 2, dims2, str, box)) != ATTN_OK) return st;
+    if ((st = encode(&P.m_dhc_st, a.dhc, 1, 2, dims2, str, box)) != ATTN_OK) return st;
   }
   const VbLayout L = vb_ctr_layout(p, kPair);
   P.T = (int)T; P.d = (int)d; P.V = (int)V; P.Vc = (int)Vc; P.nchunks = p.nchunks;
   P.nbuf = (int)NB;
+  P.N = p.N;
   P.nrb = L.nrb;
   P.ndt = L.ndt;
-  P.nvbf = (int)(Vc / Cfg::TM);
   P.ncolf = L.ncolf;
+  P.ntn = (int)((V + VB_BN - 1) / VB_BN);
+  P.fwd_tiles = a.fwd ? P.nrb * P.ntn : 0;
   P.last_g2_first = g_opt_vb_g2first;
   P.order = NB >= 2 ? g_opt_vb_order : 0;   // order 1 with one buffer would wait on later tiles
   P.trace = g_vb_trace;
   P.debug = g_vb_debug;
   P.l2hints = g_opt_vb_l2;
-  // dispatch blocks: 0 = G1(0); c + 1 = G3(c), G2(c), G1(c + 1)
+  // backward dispatch blocks: 0 = G1(0); c + 1 = G1(c + 1), G3(c), G2(c)
   auto vcc = [&](int c) { return (int)std::min(Vc, V - (long long)c * Vc); };
   int t = 0;
   P.blk_start[0] = 0;
@@ -1426,16 +1349,23 @@ static attn_status_t launch_vocab_bwd_k(const Plan& p, const void* hc, const voi
     if (c + 1 < p.nchunks) t += P.nrb * ((vcc(c + 1) + VB_BN - 1) / VB_BN);
   }
   P.blk_start[p.nchunks + 1] = t;
-  P.total_tiles = t;
+  P.total_tiles = P.fwd_tiles + t;
+  unsigned* ctr = a.ctr;
   P.tile_counter = (int*)ctr;
+  P.g5count = ctr + 1;
+  P.g0done = ctr + L.g0done;
+  P.lsedone = ctr + L.lsedone;
   P.rowdone = ctr + L.rowdone;
   P.coldone = ctr + L.coldone;
   P.consumed = ctr + L.consumed;
   P.g2done = ctr + L.g2done;
   P.dhcdone = ctr + L.dhcdone;
-  P.lse = lse; P.rowscale = rowscale; P.tgt = tgt; P.tgt_logit = tgt_logit; P.bias = bias;
+  P.blockpart = reinterpret_cast<double*>(ctr + L.blockpart);
+  P.part = a.part; P.tgt_logit = a.tgt_logit; P.lse = a.lse; P.nll = a.nll;
+  P.rowscale = a.rowscale; P.loss = a.loss; P.loss_scale = a.loss_scale; P.tgt = a.tgt;
+  P.tgt_len = a.tgt_len; P.bias = a.bias; P.db_part = a.db_part;
   int units = (ctas > 0 ? ctas : dev_info().sms) / Cfg::CTAS;
-  units = std::max(1, std::min(units, t));
+  units = std::max(1, std::min(units, P.total_tiles));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * Cfg::CTAS);
   cfg.blockDim = dim3(VB_THREADS);
@@ -1457,21 +1387,14 @@ static attn_status_t launch_vocab_bwd_k(const Plan& p, const void* hc, const voi
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, vocab_bwd_kernel<kPair>, P));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, vocab_kernel<kPair>, P));
   ++g_launches;
   return ATTN_OK;
 }
 
-static attn_status_t launch_vocab_bwd(const Plan& p, const void* hc, const void* W_out, void* dl,
-                                      float* dhc, float* dW_out, const float* lse,
-                                      const float* rowscale, const int* tgt, const float* tgt_logit,
-                                      const void* bias, unsigned* ctr, int ctas,
-                                      cudaStream_t stream) {
-  if (g_opt_vb_pair)
-    return launch_vocab_bwd_k<true>(p, hc, W_out, dl, dhc, dW_out, lse, rowscale, tgt, tgt_logit,
-                                    bias, ctr, ctas, stream);
-  return launch_vocab_bwd_k<false>(p, hc, W_out, dl, dhc, dW_out, lse, rowscale, tgt, tgt_logit,
-                                   bias, ctr, ctas, stream);
+static attn_status_t launch_vocab(const Plan& p, const VbArgs& a, int ctas, cudaStream_t stream) {
+  return g_opt_vb_pair ? launch_vocab_k<true>(p, a, ctas, stream)
+                       : launch_vocab_k<false>(p, a, ctas, stream);
 }
 
 struct CounterCtx {
@@ -1527,29 +1450,27 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
     if ((st = gemm(&g, 1, PAIR_FWD)) != ATTN_OK) return st;
   }
   prof_mark("proj_tanh", stream, true);
-  // ---- F4 (Eq. 5): logits discarded, per-tile (max, sumexp) kept
-  {
-    GemmDesc g = g_vocab_fwd(p, b, W_out, tgt_ids, b_out);
-    if ((st = gemm(&g, 1, PAIR_FWD)) != ATTN_OK) return st;
-  }
-  prof_mark("vocab_fwd", stream, true);
-  // ---- Eq. 6: lse, token NLL, row scale, loss
-  {
-    const int blocks = (int)((TT + 7) / 8);
-    st = launch_pdl(lse_reduce_kernel, dim3(blocks), dim3(256), stream, (const float2*)b.part,
-                    p.part_ld, (const float*)b.tgt_logit, (const int*)b.tgt_len, (int)TT, p.N,
-                    loss_scale, b.lse, b.nll, b.rowscale, b.blockpart, b.counters, loss);
-    if (st != ATTN_OK) return st;
-  }
-  prof_mark("lse_reduce", stream, true);
   CommRun cr;
   if (comm) {
     if ((st = comm_begin(comm, stream, &cr)) != ATTN_OK) return st;
   }
-
-  // ---- B1, bf16: the persistent vocab backward (vocab_bwd.cuh): logits
-  // recomputed per V-chunk, dL in the L2-sized chunk scratch, one launch
-  if (p.vb && !db_out) {
+  // ---- F4 + F5 + B1, bf16: ONE persistent launch (vocab.cuh): the logits
+  // tiles' (max, sum exp) partials, lse / NLL / loss, and the backward with
+  // the logits recomputed per L2-sized V-chunk -- the logits never reach HBM
+  if (p.vb) {
+    if (!g_opt_vb_fwd) {
+      // F4 on the single-CTA engine (logits discarded, per-tile (max, sum
+      // exp) kept), then Eq. 6
+      GemmDesc g = g_vocab_fwd(p, b, W_out, tgt_ids, b_out);
+      if ((st = gemm(&g, 1, PAIR_FWD)) != ATTN_OK) return st;
+      prof_mark("vocab_fwd", stream, true);
+      const int blocks = (int)((TT + 7) / 8);
+      st = launch_pdl(lse_reduce_kernel, dim3(blocks), dim3(256), stream, (const float2*)b.part,
+                      p.part_ld, (const float*)b.tgt_logit, (const int*)b.tgt_len, (int)TT, p.N,
+                      loss_scale, b.lse, b.nll, b.rowscale, b.blockpart, b.counters, loss);
+      if (st != ATTN_OK) return st;
+      prof_mark("lse_reduce", stream, true);
+    }
     CUDA_TRY(cudaMemsetAsync(b.vbctr, 0, sizeof(unsigned) * p.n_vbctr, stream));
     int ctas = 0;
     if (comm) {
@@ -1575,28 +1496,47 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
       reserve = comm_max_ctas(comm);
       if (reserve > 0) ctas = (dev_info().sms - reserve) & ~1;
     }
-    st = launch_vocab_bwd(p, b.hc, W_out, b.dl[0], b.dhc, dW_out, b.lse, b.rowscale, tgt_ids,
-                          b.tgt_logit, b_out, b.vbctr, ctas, stream);
+    VbArgs va;
+    va.hc = b.hc; va.W_out = W_out; va.dl = b.dl[0]; va.dhc = b.dhc; va.dW_out = dW_out;
+    va.part = b.part; va.part_ld = p.part_ld; va.tgt_logit = b.tgt_logit; va.lse = b.lse;
+    va.nll = b.nll; va.rowscale = b.rowscale; va.loss = loss; va.loss_scale = loss_scale;
+    va.tgt = tgt_ids; va.tgt_len = b.tgt_len; va.bias = b_out; va.db_part = db_out ? b.dbpart : nullptr;
+    va.ctr = b.vbctr;
+    va.fwd = g_opt_vb_fwd != 0;
+    if ((st = launch_vocab(p, va, ctas, stream)) != ATTN_OK) return st;
+    if (db_out) {   // F_c bias: db_out = the launch's per-32-row column sums, added in order
+      st = launch_pdl(db_final_kernel, dim3((unsigned)((p.V + 255) / 256)), dim3(256), stream,
+                      (const float*)b.dbpart, (int)((TT + 31) / 32), p.V, db_out);
+      if (st != ATTN_OK) return st;
+    }
+    prof_mark(g_opt_vb_fwd ? "vocab" : "vocab_bwd", stream, true);
+  } else {
+  // ---- F4 (Eq. 5): logits discarded, per-tile (max, sumexp) kept
+  {
+    GemmDesc g = g_vocab_fwd(p, b, W_out, tgt_ids, b_out);
+    if ((st = gemm(&g, 1, PAIR_FWD)) != ATTN_OK) return st;
+  }
+  prof_mark("vocab_fwd", stream, true);
+  // ---- Eq. 6: lse, token NLL, row scale, loss
+  {
+    const int blocks = (int)((TT + 7) / 8);
+    st = launch_pdl(lse_reduce_kernel, dim3(blocks), dim3(256), stream, (const float2*)b.part,
+                    p.part_ld, (const float*)b.tgt_logit, (const int*)b.tgt_len, (int)TT, p.N,
+                    loss_scale, b.lse, b.nll, b.rowscale, b.blockpart, b.counters, loss);
     if (st != ATTN_OK) return st;
-  } else
+  }
+  prof_mark("lse_reduce", stream, true);
+
   // ---- B1: V-chunked vocab backward.  Launch c runs dW_out[c] and dHc += ...
   // for chunk c together with the dlogits of chunk c+1 (double-buffered).
   // With stored logits, an elementwise kernel makes dlogits_c from the
   // forward's fp16 logits before launch c (no recompute on the tensor cores).
   {
-    // db_out as a GEMM on the tensor cores where the vocab-backward launches
-    // run on single CTAs with uniform stages (narrow B tile); else column sums
+    // db_out: column sums of each dlogits chunk -- by the stored-logits
+    // ablation's dlogits kernels (db_mode 2) or column-sum kernels (0)
     const int db_mode = g_opt_db_gemm >= 0 ? g_opt_db_gemm : (p.store_logits ? 2 : 0);
-    const bool db_gemm = db_out && tc && db_mode == 1 &&
-                         (group_kpair(PAIR_VBWD) == 1 || group_kpair(PAIR_VBWD) == 4);
     const bool db_ew = db_out && p.store_logits && db_mode == 2;
     int ew_parts0 = 0, ew_parts = 0;   // db_ew: row groups of chunk 0 / the later chunks
-    if (db_gemm) {   // bf16 ones (0x3F80) for the db_out GEMMs
-      const long long words = 16 * p.Tld / 2;
-      st = launch_pdl(fill_u32_kernel, dim3((unsigned)std::min<long long>(148, (words + 255) / 256)),
-                      dim3(256), stream, (uint32_t*)b.ones, words, 0x3F803F80u);
-      if (st != ATTN_OK) return st;
-    }
     // dlogits of chunk c from the stored logits (on `s`, `blocks` blocks)
     auto dlogits_ew = [&](int c, cudaStream_t s, int blocks) -> attn_status_t {
       const int c0 = c * p.Vc, vcc = std::min(p.Vc, p.V - c0);
@@ -1625,9 +1565,7 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
     const int sms = dev_info().sms;
     if (p.store_logits) {
       if ((st = dlogits_ew(0, stream, 4 * sms)) != ATTN_OK) return st;
-    } else {
-      // chunk 0's dlogits alone: 128 x 256 tiles (short K; two accumulators
-      // in TMEM so each tile's exp epilogue overlaps the next tile's MMAs)
+    } else {   // fp32 path: chunk 0's dlogits on the CUDA-core engine
       GemmDesc g0 = g_dlogits(p, b, W_out, tgt_ids, 0, b_out);
       if ((st = gemm(&g0, 1, 0)) != ATTN_OK) return st;
     }
@@ -1642,12 +1580,11 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
       GemmDesc gs[4];
       int n = 0;
       gs[n++] = g_dwout(p, b, dW_out, c);   // K = T: the long tiles first
-      if (db_gemm) gs[n++] = g_dbout(p, b, db_out, c);
       gs[n++] = g_dhc(p, b, W_out, c);
       if (c + 1 < p.nchunks && !p.store_logits)
         gs[n++] = g_dlogits(p, b, W_out, tgt_ids, c + 1, b_out);
       if ((st = gemm(gs, n, PAIR_VBWD)) != ATTN_OK) return st;
-      if (db_out && !db_gemm && !db_ew) {
+      if (db_out && !db_ew) {
         // F_c bias: db_out[chunk c] = column sums of dlogits_c (still intact:
         // the next launch is the one that overwrites its buffer)
         const int c0 = c * p.Vc, vcc = std::min(p.Vc, p.V - c0);
@@ -1676,6 +1613,7 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
       if (st != ATTN_OK) return st;
     }
   }
+  }   // fp32 path / stored-logits ablation
   // tanh backward of Eq. 4: dz = dHc (1 - H_c^2)
   {
     const long long n = TT * d;
@@ -1683,7 +1621,7 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
                     dim3(256), stream, (const float*)b.dhc, (const T*)b.hc, (T*)b.dz, n);
     if (st != ATTN_OK) return st;
   }
-  prof_mark("vocab_bwd", stream, true);
+  prof_mark(p.vb ? "dz" : "vocab_bwd", stream, true);
   // ---- B2: dW_c = dz^T [H | C];  dH_part = dz W_c[:, :d];  dC = dz W_c[:, d:]
   {
     GemmDesc gs[3];
@@ -1737,6 +1675,7 @@ extern "C" attn_status_t attn_softmax_fwd_bwd_ex(
     const void* W_alpha, const void* b_out, float loss_scale, float* loss, void* dH_dec,
     void* dH_enc, float* dW_c, float* dW_out, float* dW_alpha, float* db_out, void* workspace,
     size_t workspace_bytes, attn_comm_t* comm, void* stream_) {
+  OPT_LOCK;
   attn_status_t st = validate(s, H_dec, H_enc, src_lens_host, tgt_lens_host, tgt_ids, W_c, W_out,
                               W_alpha, loss, dH_dec, dH_enc, dW_c, dW_out, dW_alpha,
                               workspace_bytes, workspace);
@@ -1949,6 +1888,7 @@ extern "C" attn_status_t attn_softmax_check_ids(const attn_shape_t* s, const int
 static size_t decode_topk_bytes(const Plan& p) { return align_up(sizeof(uint32_t) * 8 * p.T * p.part_ld); }
 
 extern "C" size_t attn_softmax_decode_workspace_size(const attn_shape_t* s) {
+  OPT_LOCK;
   if (check_shape(s) != ATTN_OK || s->dtype != ATTN_BF16) return 0;
   const Plan p = make_plan(s);
   return p.total + decode_topk_bytes(p);
@@ -1959,6 +1899,7 @@ extern "C" attn_status_t attn_softmax_decode_step(
     const void* W_c, const void* W_out, const void* W_alpha, const void* b_out, int k,
     int32_t* topk_ids, float* topk_logp, float* lse, void* workspace, size_t workspace_bytes,
     void* stream_) {
+  OPT_LOCK;
   attn_status_t st = check_shape(s);
   if (st != ATTN_OK) return st;
   if (s->dtype != ATTN_BF16)
@@ -2019,6 +1960,7 @@ extern "C" attn_status_t attn_softmax_decode_step(
 // ------------------------------------------------------------------ debug GEMM
 extern "C" attn_status_t attn_debug_gemm_bf16(int M, int N, int K, const void* A, int a_mn,
                                               const void* B, int b_mn, float* C, void* stream_) {
+  OPT_LOCK;
   if (M <= 0 || N <= 0 || K <= 0 || !A || !B || !C)
     return fail(ATTN_ERR_INVALID_ARG, "debug_gemm: bad arguments");
   GemmDesc g;

@@ -2,7 +2,9 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <chrono>
 #include <cstdarg>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -54,6 +56,8 @@ struct NcclApi {
   ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommInitRankConfig)(ncclComm_t*, int, ncclUniqueId, int, void*) = nullptr;
   ncclResult_t (*GetVersion)(int*) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool ok = false;
   std::string why;
@@ -82,6 +86,8 @@ static NcclApi& nccl() {
     api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
     api.CommInitRankConfig = (decltype(api.CommInitRankConfig))dlsym(h, "ncclCommInitRankConfig");
     api.GetVersion = (decltype(api.GetVersion))dlsym(h, "ncclGetVersion");
+    api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+    api.CommAbort = (decltype(api.CommAbort))dlsym(h, "ncclCommAbort");
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
     api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy &&
              api.ReduceScatter && api.AllGather;
@@ -98,6 +104,8 @@ struct attn_comm {
   int device = 0;
   int nranks = 1, rank = 0;
   int max_ctas = 0;   // the CTA cap given to NCCL (0 = NCCL's default)
+  cudaEvent_t done = nullptr;   // attn_comm_poll: marks the end of the enqueued comm work
+  bool aborted = false;
 };
 
 // "comm_max_ctas" option (attn_softmax.cu): CTA cap for communicators created
@@ -180,19 +188,57 @@ extern "C" attn_status_t attn_comm_init(const uint8_t id[128], int nranks, int r
   c->events.resize(64);
   for (auto& e : c->events) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CUDA_OK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
+  CUDA_OK(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming));
   *out = c;
   return ATTN_OK;
 }
 
 extern "C" attn_status_t attn_comm_destroy(attn_comm_t* c) {
   if (!c) return ATTN_OK;
-  cudaStreamSynchronize(c->stream);
-  if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+  if (!c->aborted) cudaStreamSynchronize(c->stream);
+  if (c->comm && nccl().ok) {
+    if (c->aborted) { /* ncclCommAbort already freed the communicator */ }
+    else nccl().CommDestroy(c->comm);
+  }
+  if (c->done) cudaEventDestroy(c->done);
   for (auto& e : c->events) cudaEventDestroy(e);
   cudaEventDestroy(c->join);
   cudaStreamDestroy(c->stream);
   delete c;
   return ATTN_OK;
+}
+
+extern "C" int attn_comm_nranks(const attn_comm_t* c) { return c ? c->nranks : 1; }
+
+extern "C" attn_status_t attn_comm_poll(attn_comm_t* c, int64_t timeout_ms) {
+  if (!c) return err(ATTN_ERR_INVALID_ARG, "comm is NULL");
+  if (c->aborted) return err(ATTN_ERR_NCCL, "communicator was aborted by an earlier attn_comm_poll");
+  CUDA_OK(cudaSetDevice(c->device));
+  CUDA_OK(cudaEventRecord(c->done, c->stream));
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaEventQuery(c->done);
+    if (q == cudaSuccess) return ATTN_OK;
+    if (q != cudaErrorNotReady) return err(ATTN_ERR_CUDA, "comm stream: %s", cudaGetErrorString(q));
+    ncclResult_t ae = ncclSuccess_;
+    if (nccl().CommGetAsyncError && nccl().CommGetAsyncError(c->comm, &ae) == ncclSuccess_ &&
+        ae != ncclSuccess_ && ae != ncclInProgress_) {
+      if (nccl().CommAbort) nccl().CommAbort(c->comm);
+      c->aborted = true;
+      return err(ATTN_ERR_NCCL, "rank %d of %d: NCCL asynchronous error %d (%s); communicator aborted",
+                 c->rank, c->nranks, (int)ae,
+                 nccl().GetErrorString ? nccl().GetErrorString(ae) : "?");
+    }
+    const long long ms = std::chrono::duration_cast<std::chrono::milliseconds>(
+                             std::chrono::steady_clock::now() - t0).count();
+    if (timeout_ms > 0 && ms >= timeout_ms) {
+      if (nccl().CommAbort) nccl().CommAbort(c->comm);
+      c->aborted = true;
+      return err(ATTN_ERR_NCCL, "rank %d of %d: collectives not complete after %lld ms (a rank hung "
+                 "or left); communicator aborted", c->rank, c->nranks, (long long)timeout_ms);
+    }
+    std::this_thread::sleep_for(std::chrono::milliseconds(1));
+  }
 }
 
 extern "C" attn_status_t attn_grad_allreduce(attn_comm_t* c, float* buf, size_t count, void* stream) {

@@ -11,7 +11,7 @@
 //                  over columns c < ncols_valid, and the target logit when the
 //                  row's target id falls in the tile (Eqs. 5-6 forward)
 //   EPI_DLOGITS    out[r,c] = rowscale[r] * (exp(acc - lse[r]) - [c+col_base == y_r])
-//                  (softmax - onehot; backward of Eqs. 5-6)
+//                  (softmax - onehot; backward of Eqs. 5-6; fp32 engine)
 //   EPI_ACCUM_F32  out[r,c] += acc                   (dHc over V-chunks; the tcgen05
 //                  engine does it with a TMA reduce-add, no loads)
 #pragma once
@@ -28,10 +28,8 @@ enum EpiKind : int {
   EPI_ADD_BF16 = 7,           // out = acc + addend (fp32) -> bf16: dH_dec = dH_part + de S
   EPI_ATTN_SOFTMAX = 8,       // masked row softmax of the scores (Eq. 1), tcgen05 path
   EPI_ATTN_SOFTMAX_BWD = 9,   // its backward, tcgen05 path
-  EPI_TOPK = 11,              // decoding step (NEXT-4): LSE partials as EPI_LSE plus the 8 best
+  EPI_TOPK = 11               // decoding step (NEXT-4): LSE partials as EPI_LSE plus the 8 best
                               // (logit, token) of the row's columns in the tile (tcgen05 path)
-  EPI_COL0_F32 = 12           // out[row] = acc[row, 0] (fp32): a matrix-vector product computed
-                              // as a GEMM against a block of ones (db_out, tcgen05 path)
 };
 
 // Output element type of each kind (tcgen05 path: bf16 activations).
@@ -248,8 +246,6 @@ struct RowEpilogue {
   LseState st;
   int y;
   float lse, rs;
-  float c2;    // tcgen05 DLOGITS: log2(rs) - lse log2(e) (very negative on padded rows)
-  float fix;   // tcgen05 DLOGITS: the target column's value rs (p_y - 1)
   __device__ __forceinline__ RowEpilogue(const EpiParams& p_, int row_, int split_)
       : p(p_), row(row_), split(split_) {
     st.m = -INFINITY;
@@ -260,15 +256,9 @@ struct RowEpilogue {
     lse = 0.f;
     rs = 0.f;
     if (p.kind == EPI_LSE || p.kind == EPI_DLOGITS) y = p.tgt[row] - p.col_base;
-    c2 = 0.f;
-    fix = 0.f;
-    if (p.kind == EPI_DLOGITS) {
+    if (p.kind == EPI_DLOGITS) {   // (fp32 CUDA-core engine)
       lse = p.lse[row];
       rs = p.rowscale[row];
-      if (kFast) {
-        c2 = rs > 0.f ? __log2f(rs) - lse * kLog2e : -1000.f;
-        if (p.tgt_logit) fix = rs * (__expf(p.tgt_logit[row] - lse) - 1.f);
-      }
     }
   }
 
@@ -347,20 +337,13 @@ struct RowEpilogue {
     }
   }
 
-  // tcgen05 path: transform v in place (TANH, DLOGITS) or update the LSE
-  // state; the engine stages and stores the result with TMA.
+  // tcgen05 path: transform v in place (TANH) or update the LSE state; the
+  // engine stages and stores the result with TMA.  (The bf16 dlogits live in
+  // vocab.cuh's G1 epilogue.)
   __device__ __forceinline__ void transform(int col0, float (&v)[32]) {
     const int kind = p.kind;
     if (kind == EPI_LSE) {
       chunk(col0, v);
-    } else if (kind == EPI_DLOGITS) {
-      // rs * softmax = 2^(l log2 e + log2 rs - lse log2 e): one FFMA and one
-      // MUFU ex2 per element; the -rs onehot term is written separately (the
-      // engine overwrites the target column with `fix`).  (Moving part of the
-      // exponentials to an FMA-pipe polynomial measured slower.)
-      if (p.bias) add_bias32<OutT>(p.bias, p.col_base + col0, p.ncols_valid - col0, v);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = ex2_mufu(fmaf(v[j], kLog2e, c2));
     } else if (kind == EPI_TANH) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = tanh_f<kFast>(v[j]);

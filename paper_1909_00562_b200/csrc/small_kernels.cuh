@@ -498,12 +498,6 @@ __global__ void __launch_bounds__(256) ew_colsum_final_kernel(const float* __res
   db[c] = t;
 }
 
-// fill n 32-bit words with v (the ones operand of the db_out GEMM)
-__global__ void __launch_bounds__(256) fill_u32_kernel(uint32_t* __restrict__ p, long long n,
-                                                       uint32_t v) {
-  pdl_wait();
-  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * gridDim.x) p[i] = v;
-}
 
 __global__ void check_ids_kernel(const int* __restrict__ ids, const int* __restrict__ tgt_len,
                                  int T, int N, int V, int* __restrict__ bad) {

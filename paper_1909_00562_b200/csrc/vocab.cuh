@@ -1,15 +1,24 @@
-// vocab_bwd.cuh -- B1 (backward of Eqs. 5-6) as ONE
-// persistent tcgen05 launch: the logits are never stored; they are recomputed
-// per V-chunk on the tensor cores and turned into dL = rs (softmax - onehot)
-// (bf16) in an L2-sized, double-buffered chunk scratch, which the same launch
-// consumes for dW_out and dHc.
+// vocab.cuh -- the vocabulary part of the stage as ONE persistent tcgen05
+// launch: F4 (Eq. 5 logits -> per-tile log-sum-exp partials), F5 (lse, token
+// NLL, loss; Eq. 6) and B1 (their backward).  The logits are never stored:
+// the forward keeps per-tile (max, sum exp) partials only, and the backward
+// recomputes the logits per V-chunk on the tensor cores, turning them into
+// dL = rs (softmax - onehot) (bf16) in an L2-sized chunk scratch that the same
+// launch consumes for dW_out and dHc (north_star "full
+// logits are never round-tripped through HBM").
 //
-// Per V-chunk c (width Vc, columns [c0, c0 + vcc) of the vocabulary):
-//   G1(c)  dL_c   = rs (exp(H_c W_out[c]^T - lse) - onehot)    M = T,   N = vcc, K = d
-//   G3(c)  dHc   += dL_c W_out[c]                             M = T,   N = d,   K = vcc
-//   G2(c)  dW_out[c] = dL_c^T H_c                             M = vcc, N = d,   K = T
-// Tiles are TM x 256 with fp32 accumulators in TMEM, two accumulators per
-// CTA so a tile's epilogue overlaps the next tile's MMAs:
+// Tile types (T = B*N rows, chunk c = vocabulary columns [c0, c0 + vcc)):
+//   G0       logits H_c W_out^T tile -> (max, sum exp) per row of the tile,
+//            and the target logit                           M = T, N = V, K = d
+//   LSE      lse_t, nll_t, rowscale_t of one row block from its G0 partials,
+//            and the loss: not a dispatched tile -- the otherwise idle warps
+//            8-9 of CTA pair p do it for row blocks p, p + pairs, ..., beside
+//            the pair's tiles
+//   G1(c)    dL_c = rs (exp(H_c W_out[c]^T - lse) - onehot)   M = T, N = vcc, K = d
+//   G3(c)    dHc += dL_c W_out[c]                            M = T, N = d, K = vcc
+//   G2(c)    dW_out[c] = dL_c^T H_c                           M = vcc, N = d, K = T
+// MMA tiles are TM x 256 with fp32 accumulators in TMEM, two per CTA so a
+// tile's epilogue overlaps the next tile's MMAs:
 //   kPair = false: TM = 128, one CTA per tile (tcgen05 cta_group::1);
 //   kPair = true:  TM = 256, a CTA pair (cluster of 2) per tile
 //                  (cta_group::2): each CTA stages its 128 rows of A and its
@@ -18,32 +27,34 @@
 //                  read the peer's shared memory, and each CTA's epilogue
 //                  drains its own 128 accumulator rows.  L2 -> SM operand
 //                  bytes per FLOP are 2/3 of the single-CTA tile's.
-// The tiles of all chunks form one dispatch list, pulled from a global atomic:
+// The tiles form one dispatch list, pulled from a global atomic:
+//   forward        G0(rb, all columns) for each row block rb
 //   block 0        G1(0)
 //   block c+1      G1(c+1), G3(c), G2(c)       (option order 0: G3(c), G2(c), G1(c+1))
-// (the last block has no G1 and may put G2 first: its long tiles then do not
-// form the tail)
-// and the data dependencies between tiles are tracked with counters in global
-// memory (release / acquire at gpu scope, async-proxy fences around the TMA
-// traffic):
-//   G3(c) tile (row block rb) waits for every G1(c) tile of row block rb
-//        (rowdone[c][rb]) -- and, before its reduce-add into dHc, for the G3
-//        tile of chunk c-1 at the same place (dhcdone[rb][nt]): dHc is summed
-//        in chunk order, so the result is deterministic;
-//   G2(c) tile (vocabulary rows vb) waits for the G1(c) tiles of those columns
-//        over all row blocks (coldone[c][vb]);
-//   G1(c) writes dL buffer c % NB only after every G2 / G3 tile of chunk c-NB
-//        has loaded it (consumed[c - NB]);
-//   G2(c) tiles count their finished dW_out stores (g2done[c]) so an
-//        allreduce of chunk c can start while the launch runs.
+// (the last block has no G1 and may put G2 first, so its long tiles do not form
+// the tail).  Data dependencies between tiles are tracked with counters in
+// global memory (release / acquire at gpu scope; async-proxy fences around the
+// TMA traffic):
+//   LSE(rb) waits for the G0 tiles of row block rb (g0done[rb]);
+//   G1(c)   reads lse of its row block only after LSE(rb) (lsedone[rb]), and
+//           writes dL buffer c % NB only after every G2 / G3 tile of chunk
+//           c - NB has loaded it (consumed[c - NB]);
+//   G3(c)   tile (row block rb) waits for every G1(c) tile of row block rb
+//           (rowdone[c][rb]) -- and, before its reduce-add into dHc, for the G3
+//           tile of chunk c-1 at the same place (dhcdone[rb][nt]): dHc is summed
+//           in chunk order, so the result is deterministic;
+//   G2(c)   tile waits for the G1(c) tiles of its columns over all row blocks
+//           (coldone[c][cb]), and counts its finished dW_out stores (g2done[c])
+//           so an allreduce of chunk c can start while the launch runs.
 // Every wait targets tiles earlier in the dispatch list and all CTAs are
 // resident (one per SM), so the waits cannot deadlock.  Counters count
-// epilogue-warp portions (8 per CTA and tile), so their targets scale with
-// the CTAs per tile.
+// epilogue-warp portions (8 per CTA and tile), so their targets scale with the
+// CTAs per tile.
 //
 // Roles (384 threads): warps 0-7 epilogue (warp w: TMEM lanes 32 (w % 4).., tile
-// column half w / 4), warp 8 TMEM allocator, warp 10 scheduler + TMA
-// producer, warp 11 MMA issuer (one elected lane; the pair leader's only).
+// column half w / 4), warp 8 TMEM allocator, warps 8-9 the LSE row blocks,
+// warp 10 scheduler + TMA producer, warp 11 MMA issuer (one elected lane; the
+// pair leader's only).
 #pragma once
 #include "epilogue.cuh"
 #include "ptx.cuh"
@@ -59,7 +70,6 @@ constexpr int VB_SCHED = 4;
 constexpr int VB_RING = 192 * 1024;
 constexpr int VB_SMEM_BYTES = VB_RING + VB_EPI_WARPS * VB_STG_BYTES + 1024 + 512;
 constexpr int VB_MAX_BLOCKS = 1024;                // chunks + 1
-constexpr int VB_BM = 128;                         // accumulator rows per CTA
 
 template <bool kPair>
 struct VbCfg {
@@ -73,11 +83,11 @@ struct VbCfg {
   static constexpr int WARPS_PER_TILE = VB_EPI_WARPS * CTAS;
 };
 
-enum : int { VB_G1 = 0, VB_G3 = 1, VB_G2 = 2 };
+enum : int { VB_G1 = 0, VB_G3 = 1, VB_G2 = 2, VB_G0 = 3 };
 
 struct alignas(64) VbParams {
-  CUtensorMap m_hc_k;    // H_c [T, d] bf16, K-major A of G1: box {64, 128}
-  CUtensorMap m_wo_k;    // W_out [V, d] bf16, K-major B of G1: box {64, B_ROWS}
+  CUtensorMap m_hc_k;    // H_c [T, d] bf16, K-major A of G0 / G1: box {64, 128}
+  CUtensorMap m_wo_k;    // W_out [V, d] bf16, K-major B of G0 / G1: box {64, B_ROWS}
   CUtensorMap m_dl_k;    // dL [NB][T][Vc] bf16, K-major A of G3: box {64, 128, 1}
   CUtensorMap m_wo_mn;   // W_out as [K = V][N = d], MN-major B of G3: box {64, 64, B_ROWS/64, 1}
   CUtensorMap m_dl_mn;   // dL as [K = T][M = Vc] per buffer, MN-major A of G2: box {64, 64, 2, 1}
@@ -86,34 +96,49 @@ struct alignas(64) VbParams {
   CUtensorMap m_dw_st;   // dW_out store: fp32 [V, d], box {32, 32}
   CUtensorMap m_dhc_st;  // dHc store / reduce-add: fp32 [T, d], box {32, 32}
   int T, d, V, Vc, nchunks, nbuf;
+  int N;                 // decoder steps per sentence (row t = b N + i)
   int nrb;               // TM-row blocks of T
   int ndt;               // 256-column tiles of d
-  int nvbf;              // TM-row blocks of a full chunk (Vc / TM)
   int ncolf;             // 256-column blocks of a full chunk (Vc / 256)
+  int ntn;               // 256-column tiles of V (forward)
+  int fwd_tiles;         // tiles of the forward section (0: forward not in this launch)
   int total_tiles;
   int* tile_counter;
-  unsigned* rowdone;     // [nchunks][nrb]   G1 warp-portions done per row block
-  unsigned* coldone;     // [nchunks][ncolf] G1 warp-portions done per 256-column block
-  unsigned* consumed;    // [nchunks]        G2 + G3 CTA-tiles whose operands are loaded
-  unsigned* g2done;      // [nchunks]        G2 warp-portions whose dW_out stores completed
-  unsigned* dhcdone;     // [nrb][ndt]       G3 warp-portions whose dHc update completed
-  const float* lse;
-  const float* rowscale;
-  const int* tgt;
-  const float* tgt_logit;
+  unsigned* g0done;      // [nrb]             G0 warp-portions done per row block (4 per CTA-tile)
+  unsigned* lsedone;     // [nrb]             LSE warp-portions done per row block (2 per CTA)
+  unsigned* g5count;     // [1]               LSE CTA-portions done (the last one sums the loss)
+  unsigned* rowdone;     // [nchunks][nrb]    G1 warp-portions done per row block
+  unsigned* coldone;     // [nchunks][ncolf]  G1 warp-portions done per 256-column block
+  unsigned* consumed;    // [nchunks]         G2 + G3 CTA-tiles whose operands are loaded
+  unsigned* g2done;      // [nchunks]         G2 warp-portions whose dW_out stores completed
+  unsigned* dhcdone;     // [nrb][ndt]        G3 warp-portions whose dHc update completed
+  // forward outputs / backward row statistics
+  float2* part;          // [ntn][T] (max, sum exp) per 256-column tile and row
+  float* tgt_logit;      // [T]
+  float* lse;            // [T]
+  float* nll;            // [T] token NLL (0 on padded rows)
+  float* rowscale;       // [T] loss_scale on valid rows, 0 on padded rows
+  double* blockpart;     // [nrb * CTAS] per-CTA NLL sums of a row block
+  float* loss;           // [1] loss_scale * sum of the NLL (fixed summation order)
+  float loss_scale;
+  const int* tgt;        // [T] target ids
+  const int* tgt_len;    // [B]
   const void* bias;      // F_c bias b_out [V] bf16 (NEXT-1) or NULL
+  float* db_part;        // with the bias: [T / 32][V] column sums of dL per 32-row group
   int last_g2_first;     // last block: G2 tiles before G3 tiles
   int order;             // 0: block c+1 = G3(c), G2(c), G1(c+1); 1: G1(c+1), G3(c), G2(c)
-  long long* trace;      // debug: 16 int64 per tile and CTA rank (see VB_TRACE), NULL = off
   int l2hints;           // bit 0: H_c loads evict-last; bit 1: dHc updates evict-last
+  long long* trace;      // debug: 16 int64 per tile and CTA rank (see VB_TRACE), NULL = off
   int debug;             // timing experiments only (WRONG results): bit 0 skip the G1 stores,
                          // bit 1 skip the G1 exponentials, bit 2 skip the G2 / G3 stores
-  int blk_start[VB_MAX_BLOCKS + 2];
+  int blk_start[VB_MAX_BLOCKS + 2];   // backward blocks, relative to fwd_tiles
 };
 
 struct VbTile {
-  int type, c, i, j;     // G1: i = row block, j = 256-col tile; G3: i = row block, j = d tile;
-                         // G2: i = vocabulary row block of the chunk, j = d tile
+  int type, c, i, j;     // G0: i = row block, j = 256-col tile of V;
+                         // G1: i = row block, j = 256-col tile of the chunk;
+                         // G3: i = row block, j = d tile; G2: i = vocabulary row block
+                         // of the chunk, j = d tile
   int vcc, kb_total;
 };
 
@@ -124,13 +149,21 @@ __device__ __forceinline__ int vb_vcc(const VbParams& P, int c) {
 template <bool kPair>
 __device__ __forceinline__ VbTile vb_decode(const VbParams& P, int t) {
   constexpr int TM = VbCfg<kPair>::TM;
+  VbTile r;
+  r.c = 0;
+  if (t < P.fwd_tiles) {
+    r.type = VB_G0; r.i = t / P.ntn; r.j = t % P.ntn;   // row-block major
+    r.vcc = P.V;
+    r.kb_total = P.d / VB_BK;
+    return r;
+  }
+  t -= P.fwd_tiles;
   int lo = 0, hi = P.nchunks;   // blocks 0..nchunks
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (P.blk_start[mid] <= t) lo = mid; else hi = mid - 1;
   }
   int u = t - P.blk_start[lo];
-  VbTile r;
   if (lo == 0) {
     r.type = VB_G1; r.c = 0;
   } else {
@@ -215,8 +248,25 @@ __device__ __forceinline__ void vb_load4(void* dst, const CUtensorMap* m, uint64
   else tma_load_4d_hint(dst, m, bar, c0, c1, c2, c3, pol);
 }
 
+// sum over the 32 lanes of each of 32 values: afterwards lane l holds the
+// total of column l (a butterfly reduce-scatter, 31 shuffles per lane)
+__device__ __forceinline__ float warp_colsum32(float (&v)[32], uint32_t lane) {
+#pragma unroll
+  for (int half = 16; half >= 1; half >>= 1) {
+    const bool upper = (lane & half) != 0;
+#pragma unroll
+    for (int j = 0; j < half; ++j) {
+      // keep the half of the columns this lane will own, send the other half
+      const float send = upper ? v[j] : v[j + half];
+      const float keep = upper ? v[j + half] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+    }
+  }
+  return v[0];
+}
+
 template <bool kPair>
-__global__ void __launch_bounds__(VB_THREADS, 1) vocab_bwd_kernel(const __grid_constant__ VbParams P) {
+__global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_constant__ VbParams P) {
   using Cfg = VbCfg<kPair>;
   constexpr int TM = Cfg::TM;
   constexpr int STAGES = Cfg::STAGES;
@@ -274,12 +324,12 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_bwd_kernel(const __grid_c
   if (threadIdx.x == 0) pdl_trigger();
 
   // the scheduler ring: the leader publishes each tile id into both CTAs' rings
-  auto ring_read = [&](int& r, uint32_t& rph, bool arrive_all_lanes_0) -> int {
+  auto ring_read = [&](int& r, uint32_t& rph, bool lane0) -> int {
     if (kPair && !leader) mbar_wait_cluster(&sfull[r], rph);
     else mbar_wait(&sfull[r], rph);
     const int t = sched_tile[r];
     __syncwarp();
-    if (arrive_all_lanes_0 ? lane == 0 : elect_one()) {
+    if (lane0 ? lane == 0 : elect_one()) {
       if (kPair && !leader) mbar_arrive_cluster(leader_addr(&sempty[r]));
       else mbar_arrive(&sempty[r]);
     }
@@ -357,6 +407,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_bwd_kernel(const __grid_c
       VB_TRACE(t, 3, vb_gt());
       const int arow = tl.i * TM + 128 * rank;            // this CTA's A rows (M)
       const int bcol = tl.j * VB_BN + Cfg::B_ROWS * rank;  // this CTA's B rows (N)
+      const int bcolg = (tl.type == VB_G0 ? 0 : c0) + bcol;
       int t_nxt = -1;
       VbTile tl_nxt{};
       for (int kb = 0; kb < tl.kb_total; ++kb) {
@@ -367,9 +418,9 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_bwd_kernel(const __grid_c
           const uint32_t barc = kPair ? leader_addr(&full[s]) : 0u;
           if (leader) mbar_arrive_expect_tx(&full[s], Cfg::STAGE * Cfg::CTAS);
           const int k0 = kb * VB_BK;
-          if (tl.type == VB_G1) {
+          if (tl.type == VB_G1 || tl.type == VB_G0) {
             vb_load<kPair>(sA, &P.m_hc_k, &full[s], barc, k0, arow, 0, pol_keep);
-            vb_load<kPair>(sB, &P.m_wo_k, &full[s], barc, k0, c0 + bcol, 0, pol_norm);
+            vb_load<kPair>(sB, &P.m_wo_k, &full[s], barc, k0, bcolg, 0, pol_norm);
           } else if (tl.type == VB_G3) {
             vb_load<kPair>(sA, &P.m_dl_k, &full[s], barc, k0, arow, buf, pol_norm);
             vb_load4<kPair>(sB, &P.m_wo_mn, &full[s], barc, 0, c0 + k0, bcol / 64, 0, pol_norm);
@@ -402,7 +453,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_bwd_kernel(const __grid_c
       if (t >= 0) tl = vb_decode<kPair>(P, t);
       while (t >= 0) {
         const int a_mn = tl.type == VB_G2 ? 1 : 0;
-        const int b_mn = tl.type == VB_G1 ? 0 : 1;
+        const int b_mn = (tl.type == VB_G3 || tl.type == VB_G2) ? 1 : 0;
         const uint32_t idesc = umma_idesc_bf16(TM, VB_BN, a_mn, b_mn);
         const uint32_t a_lbo = a_mn ? 8192u : 16u, b_lbo = b_mn ? 8192u : 16u;
         const uint32_t a_kstep = a_mn ? 2048u : 32u, b_kstep = b_mn ? 2048u : 32u;
@@ -460,6 +511,79 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_bwd_kernel(const __grid_c
         tl = tl_nxt;
       }
     }
+  } else if (warp == 8 || warp == 9) {
+    // ---------------- LSE (Eq. 6) of row blocks p, p + pairs, ... (pair p):
+    // this CTA's 128 rows, two per thread, once the row block's G0 tiles have
+    // stored their partials; the partials are slot-major, so a warp's loads
+    // are 256 contiguous bytes
+    const int tid = (warp - 8) * 32 + lane;
+    const int pid = blockIdx.x / Cfg::CTAS, npairs = gridDim.x / Cfg::CTAS;
+    double* red = reinterpret_cast<double*>(bars + 48);   // [2] (spare words of the barrier region)
+    for (int rb = pid; P.fwd_tiles > 0 && rb < P.nrb; rb += npairs) {
+      if (lane == 0) vb_wait_geq(P.g0done + rb, (unsigned)(4 * Cfg::CTAS * P.ntn));
+      __syncwarp();
+      const int rbase = rb * TM + 128 * rank;
+      double wsum = 0.0;
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        const int row = rbase + tid + 64 * half;
+        if (row >= P.T) continue;
+        float mx = -INFINITY, sm = 0.f;
+        int k = 0;
+        for (; k + 16 <= P.ntn; k += 16) {
+          float2 p2[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) p2[u] = __ldcg(P.part + (long long)(k + u) * P.T + row);
+          float bm = p2[0].x;
+#pragma unroll
+          for (int u = 1; u < 16; ++u) bm = fmaxf(bm, p2[u].x);
+          const float nm = fmaxf(mx, bm);
+          if (nm == -INFINITY) continue;
+          float bs = 0.f;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) bs += p2[u].y * ex2_mufu((p2[u].x - nm) * kLog2e);
+          sm = sm * ex2_mufu((mx - nm) * kLog2e) + bs;
+          mx = nm;
+        }
+        for (; k < P.ntn; ++k) {
+          const float2 p2 = __ldcg(P.part + (long long)k * P.T + row);
+          const float nm = fmaxf(mx, p2.x);
+          if (nm == -INFINITY) continue;
+          sm = sm * ex2_mufu((mx - nm) * kLog2e) + p2.y * ex2_mufu((p2.x - nm) * kLog2e);
+          mx = nm;
+        }
+        const float lse = mx + __logf(sm);
+        const bool valid = (row % P.N) < P.tgt_len[row / P.N];
+        const float nll = valid ? lse - __ldcg(P.tgt_logit + row) : 0.f;
+        P.lse[row] = lse;
+        P.nll[row] = nll;
+        P.rowscale[row] = valid ? P.loss_scale : 0.f;
+        wsum += (double)nll;
+      }
+      // this CTA's NLL sum in a fixed order (lane tree, then warp 8 + warp 9)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+      if (lane == 0) red[warp - 8] = wsum;
+      named_bar_sync(6, 64);   // (also: every lse of the CTA's rows is written)
+      if (warp == 8 && lane == 0) {
+        P.blockpart[rb * Cfg::CTAS + rank] = red[0] + red[1];
+        __threadfence();
+        const unsigned prev = atomicAdd(P.g5count, 1u);
+        if (prev == (unsigned)(P.nrb * Cfg::CTAS) - 1) {
+          // the last row block: the loss, summed in block order (deterministic)
+          __threadfence();
+          double tot = 0.0;
+          for (int i = 0; i < P.nrb * Cfg::CTAS; ++i)
+            tot += reinterpret_cast<volatile double*>(P.blockpart)[i];
+          *P.loss = (float)(tot * (double)P.loss_scale);
+        }
+      }
+      if (lane == 0) {
+        __threadfence();
+        red_release_gpu_add(P.lsedone + rb, 1u);
+      }
+      named_bar_sync(6, 64);   // red[] reused by the next row block
+    }
   } else if (warp < VB_EPI_WARPS) {
     // ---------------- epilogue (8 warps per CTA): this CTA's 128 rows of the tile
     const uint32_t q = warp & 3;        // TMEM lane quarter: rows 32q..32q+31 of this CTA's 128
@@ -480,19 +604,105 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_bwd_kernel(const __grid_c
       const int row0 = tl.i * TM + 128 * rank + q * 32;   // problem row of lane 0
       const int colh = tl.j * VB_BN + h * 128;           // problem column of this warp's first
       const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * VB_BN + h * 128;
-      if (tl.type == VB_G1) {
+      if (tl.type == VB_G0) {
+        // ---- Eq. 5 forward: (max, sum exp) of this warp's 128 columns per row,
+        // and the target logit when the row's target falls in them
+        const int row = row0 + lane;
+        const bool row_ok = row < P.T;
+        const int yl = row_ok ? P.tgt[row] - colh : -1;
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        if (warp == 0) {
+          VB_TRACE(t, 6, vb_clk());
+          VB_TRACE(t, 10, vb_gt());
+          VB_TRACE(t, 12, vb_clk());
+        }
+        const int nvalid = P.V - colh;
+        float m = -INFINITY, ssum = 0.f, tval = 0.f;
+        bool has_t = false;
+        uint32_t raw[32];
+        tmem_ld32_issue(taddr, raw);
+        tmem_ld_wait_regs(raw);
+#pragma unroll 1
+        for (int cc = 0; cc < 4; ++cc) {
+          if (cc * 32 >= nvalid) break;
+          float v[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(raw[e]);
+          if (cc < 3 && (cc + 1) * 32 < nvalid) tmem_ld32_issue(taddr + (cc + 1) * 32, raw);
+          const int nv = nvalid - cc * 32;
+          if (P.bias) add_bias32<__nv_bfloat16>(P.bias, colh + cc * 32, nv, v);
+          float cm;
+          if (nv >= 32) {   // sm_100 three-input max: 16 FMNMX3 for 32 values
+            float a = fmax3_f(v[0], v[1], v[2]), b = fmax3_f(v[3], v[4], v[5]);
+#pragma unroll
+            for (int j = 6; j < 30; j += 4) {
+              a = fmax3_f(a, v[j], v[j + 1]);
+              b = fmax3_f(b, v[j + 2], v[j + 3]);
+            }
+            cm = fmax3_f(a, b, fmaxf(v[30], v[31]));
+          } else {
+            cm = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < nv) cm = fmaxf(cm, v[j]);
+          }
+          const float nm = fmaxf(m, cm);
+          const float nml = nm * kLog2e;
+          float sacc = ssum * ex2_mufu(fmaf(m, kLog2e, -nml));
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < nv) sacc += ex2_mufu(fmaf(v[j], kLog2e, -nml));
+          ssum = sacc;
+          m = nm;
+          const int ycc = yl - cc * 32;
+          if ((unsigned)ycc < 32u && ycc < nv) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) tval = (j == ycc) ? v[j] : tval;
+            has_t = true;
+          }
+          if (cc < 3 && (cc + 1) * 32 < nvalid) tmem_ld_wait_regs(raw);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (kPair && !leader) mbar_arrive_cluster(leader_addr(&tempty[acc]));
+          else mbar_arrive(&tempty[acc]);
+        }
+        if (row_ok && has_t) P.tgt_logit[row] = tval;
+        // the two column halves of a row merge through shared memory (warp q
+        // + 4 hands its (max, sum) to warp q; named barrier 2 + q, 64 threads)
+        float2* xchg = reinterpret_cast<float2*>(staging + q * VB_STG_BYTES) + lane;
+        if (h == 1) *xchg = make_float2(m, ssum);
+        named_bar_sync(2 + q, 64);
+        if (h == 0) {
+          const float2 o = *xchg;
+          const float nm = fmaxf(m, o.x);   // (-inf, 0) for a half past the vocabulary
+          if (nm != -INFINITY) ssum = ssum * ex2_mufu((m - nm) * kLog2e) + o.y * ex2_mufu((o.x - nm) * kLog2e);
+          if (row_ok) P.part[(long long)tl.j * P.T + row] = make_float2(nm, ssum);
+          __syncwarp();   // (orders the warp's stores before lane 0's release)
+          if (lane == 0) red_release_gpu_add(P.g0done + tl.i, 1u);
+        }
+        named_bar_sync(2 + q, 64);   // xchg may be overwritten by the next tile
+        __syncwarp();
+      } else if (tl.type == VB_G1) {
         // ---- dL = rs softmax - rs onehot (bf16) into dL buffer `buf`.  The
         // row's statistics are read before the accumulator wait (latency hidden
         // under the tile's MMAs).
         const int row = row0 + lane;
+        if (warp == 0) VB_TRACE(t, 15, vb_gt());
+        if (P.fwd_tiles > 0) {   // lse of this row block comes from this launch's LSE warps
+          if (lane == 0) vb_wait_geq(P.lsedone + tl.i, (unsigned)(2 * Cfg::CTAS));
+          __syncwarp();
+        }
         float c2 = -1000.f, fix = 0.f;
         int yl = -1;   // target column relative to this warp's first column
         if (row < P.T) {
-          const float rs = P.rowscale[row];
+          const float rs = __ldcg(P.rowscale + row);   // written by this launch's LSE warps
           if (rs > 0.f) {
-            const float ls = P.lse[row];
+            const float ls = __ldcg(P.lse + row);
             c2 = __log2f(rs) - ls * kLog2e;
-            fix = rs * (__expf(P.tgt_logit[row] - ls) - 1.f);
+            fix = rs * (__expf(__ldcg(P.tgt_logit + row) - ls) - 1.f);
             yl = P.tgt[row] - c0 - colh;
           }
         }
@@ -505,12 +715,12 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_bwd_kernel(const __grid_c
           __syncwarp();
           fence_proxy_async_global();
         }
+        if (warp == 0) VB_TRACE(t, 12, vb_gt());   // after the lse / buffer waits
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         if (warp == 0) {
           VB_TRACE(t, 6, vb_clk());
           VB_TRACE(t, 10, vb_gt());
-          VB_TRACE(t, 12, vb_clk());
         }
         const int nvalid = tl.vcc - colh;   // valid columns of this warp's 128 (may be <= 0)
         uint32_t raw[32];
@@ -523,22 +733,28 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_bwd_kernel(const __grid_c
           for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(raw[e]);
           if (P.bias && nvalid - cc * 32 > 0)
             add_bias32<__nv_bfloat16>(P.bias, c0 + colh + cc * 32, nvalid - cc * 32, v);
+          const int ycc = yl - cc * 32;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            float x = (P.debug & 2) ? v[e] : ex2_mufu(fmaf(v[e], kLog2e, c2));
+            if (nvalid - cc * 32 < 32 && cc * 32 + e >= nvalid) x = 0.f;   // past the vocabulary
+            v[e] = x;
+          }
+          if (P.db_part) {
+            // F_c bias (NEXT-1): column sums of dL over this warp's 32 rows,
+            // the target column holding rs (p_y - 1)
+            float cs[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) cs[e] = (e == ycc) ? fix : v[e];
+            const float colsum = warp_colsum32(cs, lane);
+            const int gcol = c0 + colh + cc * 32 + (int)lane;
+            if (cc * 32 + (int)lane < nvalid && row0 < P.T)
+              P.db_part[(long long)(row0 >> 5) * P.V + gcol] = colsum;
+          }
           uint32_t w[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            float a, b;
-            if (P.debug & 2) {
-              a = v[2 * e];
-              b = v[2 * e + 1];
-            } else {
-              a = ex2_mufu(fmaf(v[2 * e], kLog2e, c2));
-              b = ex2_mufu(fmaf(v[2 * e + 1], kLog2e, c2));
-            }
-            if (nvalid - cc * 32 < 32) {   // chunk tail: exact zeros past the vocabulary
-              a = cc * 32 + 2 * e < nvalid ? a : 0.f;
-              b = cc * 32 + 2 * e + 1 < nvalid ? b : 0.f;
-            }
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
             w[e] = *reinterpret_cast<uint32_t*>(&h2);
           }
           // next chunk's accumulator columns load while this one is staged
@@ -553,7 +769,6 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_bwd_kernel(const __grid_c
             st_shared_v4(stg + lane * 128 + ((gi ^ swz) << 4), w[4 * g], w[4 * g + 1],
                          w[4 * g + 2], w[4 * g + 3]);
           }
-          const int ycc = yl - cc * 32;
           if ((unsigned)ycc < 32u) {   // the -onehot term: target column holds rs (p_y - 1)
             const uint32_t gi = (cc & 1) * 4 + (ycc >> 3);
             st_shared_u16(stg + lane * 128 + ((gi ^ swz) << 4) + (ycc & 7) * 2,
@@ -676,6 +891,17 @@ __global__ void vb_wait_g2_kernel(const unsigned* __restrict__ g2done, int c_lo,
     vb_wait_geq(g2done + c, (unsigned)(per_tile * ndt * ((vcc + tm - 1) / tm)));
   }
   __threadfence();
+}
+
+// db_out[v] = sum over the 32-row groups g of db_part[g][v] (fixed order)
+__global__ void __launch_bounds__(256) db_final_kernel(const float* __restrict__ db_part, int groups,
+                                                       int V, float* __restrict__ db_out) {
+  pdl_wait();
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  float s = 0.f;
+  for (int g = 0; g < groups; ++g) s += db_part[(long long)g * V + v];
+  db_out[v] = s;
 }
 
 }  // namespace attnsm

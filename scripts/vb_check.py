@@ -27,20 +27,21 @@ def run(cfg, inp, scale, bias=False):
     return {k: (v.float().cpu().numpy() if torch.is_tensor(v) else v) for k, v in out.items()}, st
 
 
-def parity(name, vc=0, budget=None):
+def parity(name, vc=0, budget=None, bias=False):
     cfg = CONFIGS[name]
     if vc:
         binding.attn_softmax_set_option("vocab_chunk", vc)
     if budget:
         binding.attn_softmax_set_option("dl_budget_mb", budget)
-    inp = make_inputs(cfg)
+    inp = make_inputs(cfg, with_bias=bias)
     scale = 1.0 / global_valid_tokens(cfg, cfg.B)
-    g, st = run(cfg, inp, scale)
-    g2, _ = run(cfg, inp, scale)
+    g, st = run(cfg, inp, scale, bias)
+    g2, _ = run(cfg, inp, scale, bias)
     f, b = O.fwd_bwd(inp["H_dec"], inp["H_enc"], inp["src_len"], inp["tgt_len"], inp["tgt_ids"],
-                     inp["W_c"], inp["W_out"], scale)
-    errs = {k: rel(g[k], b[k]) for k in ("dH_dec", "dH_enc", "dW_c", "dW_out")}
-    det = all(np.array_equal(g[k], g2[k]) for k in ("dH_dec", "dH_enc", "dW_c", "dW_out", "loss"))
+                     inp["W_c"], inp["W_out"], scale, b_out=inp.get("b_out"))
+    keys = ("dH_dec", "dH_enc", "dW_c", "dW_out") + (("db_out",) if bias else ())
+    errs = {k: rel(g[k], b[k]) for k in keys}
+    det = all(np.array_equal(g[k], g2[k]) for k in keys + ("loss",))
     print(f"{name} vc={st.views()['vocab_chunk']}: loss {abs(g['loss'][0]-f['loss'])/abs(f['loss']):.2e} "
           + " ".join(f"{k} {v:.2e}" for k, v in errs.items()) + f" deterministic={det}", flush=True)
     binding.attn_softmax_set_option("vocab_chunk", 0)
@@ -85,7 +86,7 @@ def timing(name="paper", n=10, **opts):
         binding.attn_softmax_set_option(k, {"store_logits": 0, "vocab_bwd_persistent": 1,
                                             "dl_budget_mb": 96, "vocab_chunk": 0,
                                             "dl_buffers": 3, "vb_last_g2_first": 1,
-                                            "vb_pair": 1, "vb_order": 1}.get(k, 0))
+                                            "vb_pair": 1, "vb_order": 1, "vb_fwd_fused": 0}.get(k, 0))
 
 
 if __name__ == "__main__":
@@ -96,6 +97,13 @@ if __name__ == "__main__":
         parity("small", vc=256)
         parity("medium", vc=512)
         parity("odd", vc=256)
+        parity("small", bias=True)
+        parity("odd", vc=256, bias=True)
+        binding.attn_softmax_set_option("vb_fwd_fused", 1)
+        parity("small")
+        parity("odd", vc=256, bias=True)
+        parity("edge_min")
+        binding.attn_softmax_set_option("vb_fwd_fused", 0)
     if what in ("pair1",):
         binding.attn_softmax_set_option("vb_pair", 0)
         for nm in ("small", "medium", "odd"):
@@ -103,10 +111,8 @@ if __name__ == "__main__":
         binding.attn_softmax_set_option("vb_pair", 1)
     if what in ("all", "time"):
         timing()
-        timing(vb_pair=0)
-        timing(vb_order=0, dl_buffers=2, dl_budget_mb=64)
-        timing(dl_buffers=2, dl_budget_mb=64)
+        timing(vb_fwd_fused=1)
         for b in (72, 120):
             timing(dl_budget_mb=b)
-        timing(dl_buffers=4, dl_budget_mb=128)
         timing(store_logits=1)
+        timing()

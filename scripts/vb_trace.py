@@ -37,18 +37,30 @@ n = int(np.max(np.nonzero(t[:, 4])[0])) + 1
 t = t[:n]
 typ = t[:, 1] >> 16
 chunk = t[:, 1] & 0xFFFF
-names = {0: "G1 dlogits", 1: "G3 dHc", 2: "G2 dW_out"}
-gt0 = t[:, 8].min()
+names = {0: "G1 dlogits", 1: "G3 dHc", 2: "G2 dW_out", 3: "G0 fwd", 4: "G5 lse"}
+mm = typ != 4
+gt0 = t[mm, 8].min()
 gend = t[:, 11].max()
 print(f"{n} tiles, vc={st.views()['vocab_chunk']}, span first MMA -> last epilogue "
       f"{(gend - gt0) / 1e3:.1f} us")
 T, d = cfg.B * cfg.N, cfg.d
 vc = st.views()["vocab_chunk"]
-for k in (0, 1, 2):
+g5 = typ == 4
+if g5.any():
+    w = (t[g5, 10] - t[g5, 6]) / 1e3
+    wk = (t[g5, 11] - t[g5, 10]) / 1e3
+    st = (t[g5, 6] - t[g5, 2]) / 1e3
+    print(f"  G5 lse      {g5.sum():5d} tiles: dispatch->epilogue {np.median(st):.1f} us, g0 wait median {np.median(w):.1f} max {w.max():.1f} us, "
+          f"work median {np.median(wk):.1f} max {wk.max():.1f} us; ends at {((t[g5, 11] - t[mm, 8].min()) / 1e3).round(0).tolist()}")
+g1 = typ == 0
+if g1.any():
+    lw = (t[g1, 12] - t[g1, 15]) / 1e3
+    print(f"  G1 epilogue lse/buffer wait median {np.median(lw):.2f} us p90 {np.percentile(lw, 90):.2f} max {lw.max():.1f}")
+for k in (3, 0, 1, 2):
     sel = typ == k
     if not sel.any():
         continue
-    kb = {0: d // 64, 1: vc // 64, 2: (T + 63) // 64}[k]
+    kb = {0: d // 64, 1: vc // 64, 2: (T + 63) // 64, 3: d // 64}[k]
     span = (t[sel, 5] - t[sel, 4])
     ghz = np.median(span / np.maximum(t[sel, 9] - t[sel, 8], 1))
     print(f"  {names[k]:11s} {sel.sum():5d} tiles: MMA span/kblock median {np.median(span) / kb:.0f} "
@@ -58,8 +70,9 @@ for k in (0, 1, 2):
           f"epilogue {np.median(t[sel, 7] - t[sel, 6]):.0f} cyc (dep wait {np.median(t[sel, 12] - t[sel, 6]):.0f}, "
           f"p90 {np.percentile(t[sel, 12] - t[sel, 6], 90):.0f}); SM clock {ghz:.2f} GHz")
 busy, gaps, accw = [], [], []
-for sm in np.unique(t[:, 0]):
-    r = t[t[:, 0] == sm]
+tm_ = t[mm]
+for sm in np.unique(tm_[:, 0]):
+    r = tm_[tm_[:, 0] == sm]
     r = r[np.argsort(r[:, 4])]
     busy.append((r[:, 5] - r[:, 4]).sum() / max(1, r[-1, 5] - r[0, 4]))
     for a, b in zip(r[:-1], r[1:]):
@@ -70,20 +83,20 @@ print(f"  per-SM MMA-busy fraction median {np.median(busy):.3f} min {np.min(busy
       f"accumulator-free wait after prev commit median {np.median(accw):.0f}")
 # timeline: fraction of SMs in MMA per type over 20 time bins (globaltimer)
 bins = np.linspace(gt0, t[:, 9].max(), 21)
-print("  timeline (per 5% of the span: SM-equivalents in MMA of G1 / G3 / G2):")
+print("  timeline (per 5% of the span: SM-equivalents in MMA of G0 / G1 / G3 / G2):")
 line = []
 for i in range(20):
     a, b = bins[i], bins[i + 1]
     occ = []
-    for k in (0, 1, 2):
+    for k in (3, 0, 1, 2):
         sel = typ == k
         s0 = np.clip(t[sel, 8], a, b)
         s1 = np.clip(t[sel, 9], a, b)
         occ.append((s1 - s0).sum() / (b - a))
-    line.append("%3.0f/%3.0f/%3.0f" % tuple(occ))
+    line.append("%3.0f/%3.0f/%3.0f/%3.0f" % tuple(occ))
 print("   " + " ".join(line[:10]))
 print("   " + " ".join(line[10:]))
 # last tiles to finish
-end = t[:, 9]
+end = np.where(mm, t[:, 9], 0)
 o = np.argsort(end)[-5:]
 print("  last commits:", [(names[int(typ[i])], int(chunk[i]), round((end[i] - gt0) / 1e3, 1)) for i in o])

@@ -59,24 +59,35 @@ def test_workspace_size(built_lib):
         assert binding.attn_last_error()
 
 
+@pytest.mark.parametrize("B,N,M,d,V,vc", [(128, 50, 50, 1024, 50000, 3072),     # C1
+                                         (256, 64, 64, 1024, 100000, 1280),   # C3
+                                         (64, 120, 120, 2048, 64000, 2560)])  # C4
+def test_vchunk_l2_budget(built_lib, B, N, M, d, V, vc):
+    """The persistent backward's V-chunk: the dl_buffers bf16 dL buffers
+    [T, Vc] fit the dl_budget_mb L2 budget (120 MB, 3 buffers; DESIGN.md
+    "V-chunk schedule"), so the chunk scratch is L2-resident."""
+    s = binding.shape(B, N, M, d, V, "bf16")
+    assert binding.attn_softmax_workspace_views(s).vocab_chunk == vc
+    assert 3 * B * N * vc * 2 <= 120 << 20
+
+
 @pytest.mark.parametrize("B,N,M,d,V,vc", [(128, 50, 50, 1024, 50000, 12544),    # C1
                                          (256, 64, 64, 1024, 100000, 20224),  # C3
                                          (64, 120, 120, 2048, 64000, 10752)]) # C4
-def test_vchunk_model(built_lib, B, N, M, d, V, vc):
-    """The stored-logits backward's V-chunk width comes from the scheduler
-    model (attn_softmax.cu model_chunk_width); these are the widths the
-    measured sweeps favour.  The workspace
-    holds the fp16 logits [T, V8] on top of the recompute layout."""
+def test_vchunk_model_stored_logits(built_lib, B, N, M, d, V, vc):
+    """Ablation store_logits = 1: the V-chunk width comes from the scheduler
+    model (attn_softmax.cu model_chunk_width) -- the widths the round-1
+    sweeps favoured -- and the workspace holds the fp16 logits [T, V8] on top
+    of the recompute layout."""
     s = binding.shape(B, N, M, d, V, "bf16")
-    assert binding.attn_softmax_workspace_views(s).vocab_chunk == vc
-    n_stored = binding.attn_softmax_workspace_size(s)
-    binding.attn_softmax_set_option("store_logits", 0)
+    n_rc = binding.attn_softmax_workspace_size(s)
+    binding.attn_softmax_set_option("store_logits", 1)
     try:
-        n_rc = binding.attn_softmax_workspace_size(s)
-        assert binding.attn_softmax_workspace_views(s).vocab_chunk != 0
+        assert binding.attn_softmax_workspace_views(s).vocab_chunk == vc
+        n_stored = binding.attn_softmax_workspace_size(s)
     finally:
-        binding.attn_softmax_set_option("store_logits", 1)
-    assert n_stored >= n_rc + 2 * B * N * ((V + 7) // 8 * 8) - (64 << 20)
+        binding.attn_softmax_set_option("store_logits", 0)
+    assert n_stored >= n_rc + 2 * B * N * ((V + 7) // 8 * 8) - (256 << 20)
 
 
 class _Fake:

@@ -49,22 +49,18 @@ def oracle(inp, scale):
 
 
 # ------------------------------------------------------------ GEMM core ----
-@pytest.mark.parametrize("pair", [1, 2, 3, 4, 6])
+@pytest.mark.parametrize("wide", [0, 1])
 @pytest.mark.parametrize("mn3d", [0, 1])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 0), (0, 1), (1, 1)])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (296, 520, 200), (1000, 264, 1536),
                                    (320, 640, 192)])
-def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, pair):
-    """The tcgen05 engine alone: single CTA (cta_group::1, 128x256 tiles), CTA
-    pair (cta_group::2, 256x256), B-multicast cluster, and wide single-CTA
-    256x256 tiles; all operand majors (MN-major via per-atom boxes or one box
-    per stage), with M/N/K tails."""
+def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, wide):
+    """The tcgen05 engine alone: 128x256 tiles (two accumulators) and wide
+    256x256 single-CTA tiles; all operand majors (MN-major via per-atom boxes
+    or one box per stage), with M/N/K tails."""
     from paper_1909_00562_b200 import binding
     binding.attn_softmax_set_option("mn_3d_tma", mn3d)
-    binding.attn_softmax_set_option("cta_pair", 8 if pair == 2 else 0)
-    binding.attn_softmax_set_option("b_multicast", 8 if pair == 3 else 0)
-    binding.attn_softmax_set_option("wide_tiles", 8 if pair == 4 else 0)
-    binding.attn_softmax_set_option("wide_multicast", 8 if pair == 6 else 0)
+    binding.attn_softmax_set_option("wide_tiles", 8 if wide else 0)
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N + K)
     A = torch.randn(M, K, generator=g).bfloat16()
     B = torch.randn(N, K, generator=g).bfloat16()
@@ -81,66 +77,62 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, pair):
 
 
 # ------------------------------------------------------ end-to-end parity --
+_DEFAULTS = {"store_logits": 0, "wide_tiles": 2, "db_gemm": -1, "vb_pair": 1, "vb_fwd_fused": 0,
+             "vb_order": 1, "dl_buffers": 3, "dl_budget_mb": 120, "vb_last_g2_first": 1}
+_MODES = {
+    "default": {},                                  # persistent vocab launch on CTA pairs
+    "single": {"vb_pair": 0},                       # ... on single-CTA 128 x 256 tiles
+    "fused": {"vb_fwd_fused": 1},                   # F4 + F5 inside the persistent launch
+    "fused_single": {"vb_fwd_fused": 1, "vb_pair": 0},
+    "order0": {"vb_order": 0, "dl_buffers": 2},     # [G3, G2, G1(next)] dispatch, 2 buffers
+    "nb1": {"dl_buffers": 1},                       # one dL buffer (dispatch order 0 forced)
+    "g3last": {"vb_last_g2_first": 0},
+    "sl": {"store_logits": 1},                      # ablation: stored fp16 logits, wide tiles
+    "sl128": {"store_logits": 1, "wide_tiles": 0},  # ... on 128 x 256 tiles
+    "sl2": {"store_logits": 2},                     # ... serialised dlogits kernels
+}
+
+
 def set_modes(binding, mode):
-    """GEMM tile modes per group (bits: 1 forward, 2 vocab backward, 4
-    projection backward, 8 debug entry): "pN" CTA pairs, "mN" B-multicast
-    clusters, "wN" wide single-CTA tiles, "xN" mixed wide / 128x256 tiles,
-    "cN" B-multicast clusters of wide tiles (the other groups on 128x256
-    single-CTA tiles), "default" the library default (wide vocab backward);
-    suffixes "+db" / "+cs" / "+ew" db_out as a ones GEMM / column-sum
-    kernels / the dlogits kernels' sums (else the library's choice), "+sl" / "+sl2" / "+rc" the
-    backward's dlogits from the stored fp16 logits (overlapped / serialised)
-    or recomputed on the tensor cores.  Without a suffix, "default" keeps the
-    library default (stored logits) and the explicit tile modes recompute
-    (they exercise the dlogits GEMM tiles)."""
+    """Library options of a parity case: a _MODES key, optionally with "+cs" /
+    "+ew" (stored-logits ablation with the F_c bias: db_out by column-sum
+    kernels / by the dlogits kernels' own sums)."""
     mode, *flags = mode.split("+")
-    binding.attn_softmax_set_option(
-        "db_gemm", 1 if "db" in flags else 0 if "cs" in flags else 2 if "ew" in flags else -1)
-    sl = 1 if mode == "default" else 0
-    sl = 1 if "sl" in flags else 2 if "sl2" in flags else 0 if "rc" in flags else sl
-    binding.attn_softmax_set_option("store_logits", sl)
-    pair, mcast, wide, mixed, widemc = 8, 0, 2, 0, 0
-    if mode != "default":
-        mask = int(mode[1:])
-        pair = mask if mode[0] == "p" else 0
-        mcast = mask if mode[0] == "m" else 0
-        wide = mask if mode[0] == "w" else 0
-        mixed = mask if mode[0] == "x" else 0
-        widemc = mask if mode[0] == "c" else 0
-    binding.attn_softmax_set_option("cta_pair", pair)
-    binding.attn_softmax_set_option("b_multicast", mcast)
-    binding.attn_softmax_set_option("wide_tiles", wide)
-    binding.attn_softmax_set_option("mixed_tiles", mixed)
-    binding.attn_softmax_set_option("wide_multicast", widemc)
+    opts = dict(_DEFAULTS, **_MODES[mode])
+    if "cs" in flags:
+        opts["db_gemm"] = 0
+    if "ew" in flags:
+        opts["db_gemm"] = 2
+    for k, v in opts.items():
+        binding.attn_softmax_set_option(k, v)
 
 
-@pytest.mark.parametrize("name,vc,mode", [("tiny", 0, "p8"), ("tiny_ragged", 0, "p8"),
-                                          ("small_f32", 0, "p8"), ("small_f32", 256, "p8"),
-                                          ("small", 0, "p8"), ("small", 1024, "p8"),
-                                          ("small", 0, "p15"), ("medium", 0, "p8"),
-                                          ("medium", 2048, "p8"), ("medium", 2048, "p15"),
-                                          ("small", 0, "m15"), ("medium", 1024, "m15"),
-                                          ("small", 0, "w15"), ("medium", 2048, "w15"),
-                                          ("small", 0, "w0"), ("medium", 0, "w0"),
-                                          ("medium", 0, "default"), ("small", 0, "default"),
-                                          ("odd", 0, "p8"), ("odd", 256, "p15"), ("odd", 256, "w15"),
-                                          ("odd_f32", 0, "p8"), ("edge_min", 0, "default"),
-                                          ("edge_min", 0, "p8"), ("edge_max_src", 0, "default"),
-                                          ("edge_max_src", 256, "w0"),
-                                          ("small", 0, "x2"), ("small", 1024, "x2"),
-                                          ("medium", 2048, "x2"), ("medium", 1024, "x15"),
-                                          ("odd", 256, "x2"), ("odd", 0, "x15"),
-                                          ("small", 0, "c2"), ("medium", 2048, "c15"),
-                                          ("odd", 256, "c2"), ("odd", 0, "c15"),
-                                          ("tiny_ragged", 0, "default+sl"),
-                                          ("small", 0, "default+sl"), ("small", 1024, "default+sl"),
-                                          ("medium", 0, "default+sl"), ("medium", 2048, "w0+sl"),
-                                          ("odd", 256, "default+sl"), ("edge_min", 0, "default+sl"),
-                                          ("edge_max_src", 256, "p15+sl"),
-                                          ("small", 0, "default+sl2"), ("odd", 256, "default+sl2"),
-                                          ("medium", 0, "default+rc"), ("odd", 0, "default+rc")])
+@pytest.mark.parametrize("name,vc,mode", [("tiny", 0, "default"), ("tiny_ragged", 0, "default"),
+                                          ("small_f32", 0, "default"), ("small_f32", 256, "default"),
+                                          ("odd_f32", 0, "default"),
+                                          ("small", 0, "default"), ("small", 256, "default"),
+                                          ("small", 1024, "default"), ("medium", 0, "default"),
+                                          ("medium", 512, "default"), ("medium", 2048, "default"),
+                                          ("odd", 0, "default"), ("odd", 256, "default"),
+                                          ("edge_min", 0, "default"), ("edge_max_src", 0, "default"),
+                                          ("edge_max_src", 256, "default"),
+                                          ("small", 0, "single"), ("small", 256, "single"),
+                                          ("medium", 512, "single"), ("odd", 256, "single"),
+                                          ("edge_min", 0, "single"),
+                                          ("small", 0, "fused"), ("medium", 512, "fused"),
+                                          ("odd", 256, "fused"), ("edge_min", 0, "fused"),
+                                          ("edge_max_src", 256, "fused"),
+                                          ("small", 256, "fused_single"), ("odd", 0, "fused_single"),
+                                          ("small", 256, "order0"), ("medium", 512, "order0"),
+                                          ("small", 256, "nb1"), ("odd", 256, "nb1"),
+                                          ("medium", 512, "g3last"),
+                                          ("tiny_ragged", 0, "sl"), ("small", 0, "sl"),
+                                          ("small", 1024, "sl"), ("medium", 0, "sl"),
+                                          ("medium", 2048, "sl128"), ("odd", 256, "sl"),
+                                          ("edge_min", 0, "sl"), ("edge_max_src", 256, "sl128"),
+                                          ("small", 0, "sl2"), ("odd", 256, "sl2")])
 def test_parity_vs_oracle(cuda_lib, name, vc, mode):
-    """mode = GEMM tile modes per group (see set_modes)."""
+    """mode = library options (see set_modes); vc = V-chunk width (0 = auto)."""
     from paper_1909_00562_b200 import binding
     cfg = CONFIGS[name]
     inp = make_inputs(cfg)
@@ -173,10 +165,11 @@ def test_parity_vs_oracle(cuda_lib, name, vc, mode):
     assert np.abs(g["alpha"].sum(-1) - 1).max() < 1e-5
 
 
-@pytest.mark.parametrize("name,vc,mode", [("tiny_ragged", 0, "p8"), ("small_f32", 0, "p8"),
-                                          ("odd_f32", 0, "p8"), ("small", 0, "default"),
-                                          ("small", 1024, "p15"), ("medium", 0, "default"),
-                                          ("medium", 2048, "w0"), ("odd", 256, "w15")])
+@pytest.mark.parametrize("name,vc,mode", [("tiny_ragged", 0, "default"), ("small_f32", 0, "default"),
+                                          ("odd_f32", 0, "default"), ("small", 0, "default"),
+                                          ("small", 1024, "single"), ("medium", 0, "default"),
+                                          ("medium", 512, "fused"), ("odd", 256, "default"),
+                                          ("odd", 256, "sl")])
 def test_parity_general_score(cuda_lib, name, vc, mode):
     """NEXT-1: the Eq. 2 "general" score alpha_hat = H^T W_alpha S
      -- Q = H W_alpha on the tensor cores, dW_alpha = H^T dQ,
@@ -204,30 +197,27 @@ def test_parity_general_score(cuda_lib, name, vc, mode):
         assert np.all(g["dH_dec"][bb, Tb:] == 0.0)
 
 
-@pytest.mark.parametrize("name,vc,mode,alpha", [("tiny_ragged", 0, "p8", False),
-                                                ("small_f32", 256, "p8", True),
-                                                ("odd_f32", 0, "p8", False),
+@pytest.mark.parametrize("name,vc,mode,alpha", [("tiny_ragged", 0, "default", False),
+                                                ("small_f32", 256, "default", True),
+                                                ("odd_f32", 0, "default", False),
                                                 ("small", 0, "default", False),
-                                                ("small", 1024, "p15", True),
+                                                ("small", 256, "default", True),
                                                 ("medium", 0, "default", False),
-                                                ("medium", 2048, "w0", True),
-                                                ("odd", 256, "w15", False),
-                                                ("odd", 0, "x2", False),
-                                                ("medium", 1024, "c2", False),
-                                                ("small", 0, "default+db", True),
-                                                ("medium", 2048, "w0+db", False),
-                                                ("odd", 256, "default+db", False),
-                                                ("small", 0, "default+sl", True),
-                                                ("odd", 256, "default+sl+db", False),
-                                                ("medium", 0, "default+cs", True),
-                                                ("odd", 0, "default+sl2", False),
-                                                ("tiny_ragged", 0, "default+ew", False),
-                                                ("medium", 2048, "default+ew", True)])
+                                                ("medium", 512, "single", True),
+                                                ("odd", 256, "default", False),
+                                                ("odd", 0, "fused", True),
+                                                ("edge_min", 0, "default", False),
+                                                ("small", 0, "sl", True),
+                                                ("odd", 256, "sl+cs", False),
+                                                ("medium", 0, "sl+cs", True),
+                                                ("odd", 0, "sl2", False),
+                                                ("tiny_ragged", 0, "sl+ew", False),
+                                                ("medium", 2048, "sl+ew", True)])
 def test_parity_output_bias(cuda_lib, name, vc, mode, alpha):
     """NEXT-1: the F_c bias b_out of Eq. 5 -- added in the
     forward LSE and the backward dlogits epilogues, db_out = column sums of
-    each dlogits V-chunk (column-sum kernels, or with "+db" a ones GEMM inside
-    the vocab-backward launches) -- against the oracle (with and without
+    dL (the persistent launch's per-32-row warp sums, added in order; the
+    stored-logits ablation's kernels) -- against the oracle (with and without
     W_alpha)."""
     from paper_1909_00562_b200 import binding
     cfg = CONFIGS[name]
