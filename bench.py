@@ -164,9 +164,32 @@ def cpu_baseline(cfg, target_s=12.0, fixed=0):
         while dt < target_s / 3 and n < cfg.B:
             n = min(cfg.B, max(n + 1, int(n * target_s / max(dt, 1e-3) * 0.6)))
             tok, dt = cpu_oracle_run(cfg, n)
-    return {"value": tok / dt, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
-            "sample": f"{n} of {cfg.B} sentences of {cfg.name} (full d={cfg.d}, V={cfg.V}), "
-                      f"{tok} target tokens, one fwd+bwd in {dt:.2f} s, numpy fp64"}
+    res = {"value": tok / dt, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+           "sample": f"{n} of {cfg.B} sentences of {cfg.name} (full d={cfg.d}, V={cfg.V}), "
+                     f"{tok} target tokens, one fwd+bwd in {dt:.2f} s, numpy fp64",
+           "cpu_model": cpu_model(), "nproc": os.cpu_count()}
+    # the same oracle on one BLAS thread, on a smaller sample
+    try:
+        from threadpoolctl import threadpool_limits
+        n1 = max(1, min(n, 8))
+        with threadpool_limits(limits=1, user_api="blas"):
+            tok1, dt1 = cpu_oracle_run(cfg, n1)
+        res["one_thread"] = {"value": tok1 / dt1, "sample": f"{n1} sentences, {tok1} tokens, "
+                                                            f"{dt1:.2f} s"}
+    except Exception as e:  # noqa: BLE001
+        res["one_thread"] = {"value": None, "error": str(e)[:200]}
+    return res
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def run_reference(args, cfg, rank, world):
@@ -191,12 +214,43 @@ def run_reference(args, cfg, rank, world):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_desc(cfg, world),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
-                             "sample": f"{n} sentences per step of {cfg.name} (full d, V)"},
+                             "sample": f"{n} sentences per step of {cfg.name} (full d, V)",
+                             "cpu_model": cpu_model(), "nproc": os.cpu_count()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------ ours --------
+def verify_exchange(binding, st, call_args, out, comm, stream, barrier):
+    """X step check (N > 1, or --force-comm): the gradients the call
+    allreduces in flight (dW_out per chunk group, dW_c, loss) must equal the
+    local (comm = NULL) call's gradients summed by attn_grad_allreduce, and the
+    local outputs (dH_dec, dH_enc) must be unchanged by the communicator.
+    Bitwise when the two reductions sum in the same order (always at 2 ranks);
+    `max_rel` bounds the reordering otherwise."""
+    import torch
+    loc = st.alloc_outputs()
+    st(*call_args, out=loc, comm=None, stream=stream)
+    for k in ("dW_out", "dW_c", "loss"):
+        binding.attn_grad_allreduce(comm, loc[k], stream=stream)
+    st(*call_args, out=out, comm=comm, stream=stream)
+    binding.attn_comm_poll(comm, 60000)
+    barrier()
+    res = {"bitwise": True, "max_rel": 0.0}
+    for k in ("dW_out", "dW_c", "loss", "dH_dec", "dH_enc"):
+        a, b = out[k].float(), loc[k].float()
+        same = bool(torch.equal(out[k], loc[k]))
+        rel = float((a - b).abs().max() / b.abs().max().clamp_min(1e-30))
+        res["bitwise"] &= same
+        res["max_rel"] = max(res["max_rel"], rel)
+        res[k] = "bitwise" if same else f"max_rel {rel:.2e}"
+    res["verified"] = bool(res["bitwise"] or res["max_rel"] <= 1e-5)
+    if not res["verified"]:
+        raise SystemExit(f"bench.py: allreduced gradients disagree with attn_grad_allreduce: {res}")
+    del loc
+    return res
+
+
 def measure_next_rows(binding, st, dv, cfg, scale, comm, stream, dev, pk, tok_local, world,
                       steps=10):
     """SURVEY §8(f) rows beyond the hot path, each timed with CUDA events on
@@ -231,6 +285,22 @@ def measure_next_rows(binding, st, dv, cfg, scale, comm, stream, dev, pk, tok_lo
     for name, kw in (("general_score", dict(W_alpha=Wa)), ("output_bias", dict(b_out=bo))):
         ms = timed(lambda: st(*args, out=outs, comm=comm, stream=stream, **kw))
         res[name] = {"ms_per_step": ms, "target_tokens_per_s": tok_local * world / (ms / 1e3)}
+    # ablation (NOT the product path: north_star forbids round-tripping the
+    # logits through HBM): the forward stores the logits as fp16 and the
+    # backward reads them instead of recomputing them per V-chunk
+    if cfg.dtype == "bf16" and comm is None:
+        from paper_1909_00562_b200.stage import AttnSoftmaxStage
+        binding.attn_softmax_set_option("store_logits", 1)
+        try:
+            st_sl = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype, device=dev)
+            ms = timed(lambda: st_sl(*args, out=outs, stream=stream))
+            res["ablation_store_logits"] = {
+                "ms_per_step": ms, "target_tokens_per_s": tok_local * world / (ms / 1e3),
+                "note": "ablation only: fp16 logits [T, V] stored by the forward and read by the "
+                        "backward (2 T V x 2 B of HBM per step); not the product path"}
+            del st_sl
+        finally:
+            binding.attn_softmax_set_option("store_logits", 0)
     # NEXT-4: one beam-search decoding step, beam 5 on the config's sentences
     # (rows = B x 5 hypotheses; fused vocab GEMM + online LSE + top-k epilogue)
     if cfg.dtype == "bf16":
@@ -273,11 +343,42 @@ def measure_next_rows(binding, st, dv, cfg, scale, comm, stream, dev, pk, tok_lo
     return res
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(args) -> int:
+    """`bench.py --gpus N` without a torchrun environment: start the N
+    ranks itself (one process per GPU, torchrun on 127.0.0.1) and return
+    their exit code.  A box with fewer than N GPUs is an error, not a
+    smaller run."""
+    if args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this box has {have}",
+                  file=sys.stderr, flush=True)
+            return 3
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    print("bench.py: launching " + " ".join(cmd[1:]), file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(launch_ranks(args))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr, flush=True)
+        sys.exit(2)
     from synthetic import CONFIGS
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -307,6 +408,8 @@ def main():
         if world > 1:
             dist.broadcast_object_list(uid, src=0)
         comm = binding.attn_comm_init(uid[0], world, rank, local)
+        print(f"bench.py: attn_comm_init nranks={binding.attn_comm_nranks(comm)} rank={rank} "
+              f"device={local}", file=sys.stderr, flush=True)
 
     # ---- inputs: this rank's sentences of the global batch (weak scaling)
     B_global = cfg.B * world
@@ -335,6 +438,8 @@ def main():
         step()
     barrier()
     launches_per_step = binding.attn_softmax_last_launches()
+    verify = verify_exchange(binding, st, call_args, out, comm, stream, barrier) \
+        if comm is not None else None
 
     # ---- device-timed region: K steps, L2 flushed between steps
     # only the events around the vocab GEMMs (the roofline's kernels): every
@@ -427,8 +532,15 @@ def main():
     # Algorithmic FLOPs per valid token: 4 d V (dW_out and dHc).
     pk = peaks()
     T_valid = tok_local
-    vb_ms = stage_ms.get("vocab_bwd", 0.0) / args.steps
-    vb_flops = 4.0 * cfg.d * cfg.V * T_valid
+    # the dominant kernel is the persistent vocabulary launch (vocab_kernel):
+    # the backward alone ("vocab_bwd": 4 d V useful FLOP per valid token,
+    # + 2 d V of recomputed logits) or, option vb_fwd_fused, forward and
+    # backward together ("vocab": 6 d V useful, 8 d V executed)
+    fused = "vocab" in stage_ms
+    vb_ms = stage_ms.get("vocab" if fused else "vocab_bwd", 0.0) / args.steps
+    useful_per_tok = (6.0 if fused else 4.0) * cfg.d * cfg.V
+    hw_per_tok = (8.0 if fused else 6.0) * cfg.d * cfg.V
+    vb_flops = useful_per_tok * T_valid
     vf_ms = stage_ms.get("vocab_fwd", 0.0) / args.steps
     vf_flops = 2.0 * cfg.d * cfg.V * T_valid
     achieved = vb_flops / (vb_ms / 1e3) / 1e12 if vb_ms > 0 else None
@@ -436,7 +548,7 @@ def main():
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(cfg.name, {}).get("vocab_bwd_bytes_per_launch")
+            traffic = json.load(open(tp)).get(cfg.name, {}).get("vocab_kernel_bytes_per_launch")
         except Exception:
             traffic = None
     # denominator: the burst peak when the timed region ran at (near) max SM
@@ -447,10 +559,15 @@ def main():
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
                 "traffic": traffic,
-                "kernel": "vocab backward: per V-chunk the elementwise dlogits kernel (from the "
-                          "forward's stored fp16 logits) + the gemm_tc_kernel dW_out + dHc launch; "
-                          "achieved counts 4 d V useful FLOP per valid token over the whole stage "
-                          "(traffic: per GEMM launch)",
+                "kernel": ("vocab_kernel, one persistent tcgen05 launch: " +
+                           ("F4 logits tiles -> online LSE, then " if fused else "") +
+                           "per L2-sized V-chunk the logits recomputed into bf16 dL = "
+                           "rs (softmax - onehot) (never stored in full), dHc += dL W_out, "
+                           "dW_out = dL^T H_c; achieved counts " +
+                           ("6" if fused else "4") + " d V useful FLOP per valid token "
+                           "(the recomputed logits not counted); traffic: DRAM bytes of one "
+                           "launch (ncu full set, profiles/traffic.json)"),
+                "executed_tflops": hw_per_tok * T_valid / (vb_ms / 1e3) / 1e12 if vb_ms > 0 else None,
                 "peak_source": pk["src"] + (", burst bf16 (timed region at max SM clock)" if at_max
                                             else ", sustained bf16 (clocks below max)"),
                 "vocab_fwd": {"achieved": vf_flops / (vf_ms / 1e3) / 1e12 if vf_ms > 0 else None,
@@ -471,6 +588,8 @@ def main():
             "gpu_launches": int(launches_per_step) * args.steps,
             "clocks": clocks,
             "loss": loss,
+            "comm": None if comm is None else {"nranks": binding.attn_comm_nranks(comm),
+                                               "exchange_check": verify},
             "useful_tflops": tok_job * (6 * cfg.d * cfg.V + 12 * cfg.d ** 2 + 12 * cfg.M * cfg.d)
                              * args.steps / (total_ms / 1e3) / 1e12 / world}
     if next_rows is not None:
