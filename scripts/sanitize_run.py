@@ -1,0 +1,48 @@
+"""One fwd+bwd of the stage per case, for compute-sanitizer (memcheck /
+racecheck / synccheck): tiny (fp32 SIMT path), small and odd (bf16 tcgen05
+path: persistent vocab launch on CTA pairs and on single CTAs, and with the
+forward fused), edge_min; then the decoding step and Adam.  Exits non-zero
+on a library error."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_1909_00562_b200 import binding
+from paper_1909_00562_b200.stage import AttnSoftmaxStage, DecodeStep, to_device
+from synthetic import CONFIGS, global_valid_tokens, make_inputs
+
+cases = [("tiny", {}), ("small", {}), ("small", {"vb_pair": 0}), ("odd", {"vb_fwd_fused": 1}),
+         ("edge_min", {}), ("small", {"bias": 1})]
+only = sys.argv[1:] 
+for name, opts in cases:
+    if only and name not in only:
+        continue
+    cfg = CONFIGS[name]
+    bias = bool(opts.pop("bias", 0))
+    for k, v in opts.items():
+        binding.attn_softmax_set_option(k, v)
+    inp = make_inputs(cfg, with_bias=bias)
+    st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
+    dv = to_device(inp, cfg.dtype)
+    out = st(dv["H_dec"], dv["H_enc"], dv["src_len"], dv["tgt_len"], dv["tgt_ids"], dv["W_c"],
+             dv["W_out"], 1.0 / global_valid_tokens(cfg, cfg.B), b_out=dv.get("b_out"))
+    torch.cuda.synchronize()
+    print(f"{name} {opts} bias={bias}: loss {out['loss'].item():.6f}", flush=True)
+    for k in opts:
+        binding.attn_softmax_set_option(k, {"vb_pair": 1, "vb_fwd_fused": 0}[k])
+if not only:
+    cfg = CONFIGS["small"]
+    inp = make_inputs(cfg)
+    dv = to_device(inp, cfg.dtype)
+    ds = DecodeStep(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, 5)
+    ids, logp, lse = ds(dv["H_dec"], dv["H_enc"], inp["src_len"], dv["W_c"], dv["W_out"])
+    torch.cuda.synchronize()
+    print("decode ok", float(lse.float().mean()), flush=True)
+    n = 100003
+    w = torch.zeros(n, device="cuda")
+    m, v, g = torch.zeros_like(w), torch.zeros_like(w), torch.full_like(w, 1e-3)
+    binding.attn_adam_step(binding.adam_params(1), w, m, v, g, torch.empty(n, dtype=torch.bfloat16, device="cuda"))
+    torch.cuda.synchronize()
+    print("adam ok", flush=True)

@@ -1,13 +1,20 @@
 """Full-size parity, in the launch configuration bench.py times.
 
 * C1 (paper-shaped, BASELINE.json configs[1]): the complete fp64 oracle runs
-  on the host in seconds, so every output is compared.
+  on the host in seconds, so every output is compared -- globally, per V-chunk
+  of dW_out (the chunk width the persistent vocab launch uses, tail chunk
+  included) and per sentence of dH_dec / dH_enc, so a bug confined to one
+  chunk or one sentence cannot hide in a global norm.  Also with the logits
+  scaled up (W_out x 8, max |logit| ~ 30-40, the range of a trained model).
 * C3 / C4 (configs[3], configs[4], per-GPU shard): the full oracle is too big
   for the host, so (a) sampled sentences are compared -- alpha, C, H_c, lse,
   token NLL, dH_dec and dH_enc of a sentence depend only on that sentence and
   the weights, so the oracle runs on just those sentences with the global
-  loss scale (invariant I7) -- and (b) whole-matrix properties that hold at
-  any size are checked (I1-I4, I6, loss = sum of token NLL).
+  loss scale (invariant I7); (b) the weight gradients at the same launch
+  configuration: every sentence but the sampled ones gets tgt_len = 0, so
+  dW_out and dW_c are exactly the sampled sentences' and are compared with
+  the oracle element by element (per V-chunk too); (c) whole-matrix
+  properties that hold at any size (I1-I4, I6, loss = sum of token NLL).
 """
 import numpy as np
 import pytest
@@ -18,6 +25,9 @@ from synthetic import CONFIGS, make_inputs, global_valid_tokens
 
 pytestmark = pytest.mark.gpu
 
+GRAD_TOL = 2e-2     # north_star: bf16 paths, every gradient rel-L2
+LOSS_TOL = 2e-3
+
 
 def rel_l2(a, b):
     a = np.asarray(a, np.float64)
@@ -25,34 +35,103 @@ def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-def gpu_run(cfg, inp, scale):
+def gpu_run(cfg, inp, scale, opts=None):
+    from paper_1909_00562_b200 import binding
     from paper_1909_00562_b200.stage import AttnSoftmaxStage, to_device
-    st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
-    dv = to_device(inp, cfg.dtype)
-    out = st(dv["H_dec"], dv["H_enc"], dv["src_len"], dv["tgt_len"], dv["tgt_ids"],
-             dv["W_c"], dv["W_out"], scale)
-    torch.cuda.synchronize()
+    opts = opts or {}
+    saved = {"vb_pair": 1, "vb_fwd_fused": 0}
+    for k, v in opts.items():
+        binding.attn_softmax_set_option(k, v)
+    try:
+        st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
+        dv = to_device(inp, cfg.dtype)
+        out = st(dv["H_dec"], dv["H_enc"], dv["src_len"], dv["tgt_len"], dv["tgt_ids"],
+                 dv["W_c"], dv["W_out"], scale)
+        torch.cuda.synchronize()
+    finally:
+        for k in opts:
+            binding.attn_softmax_set_option(k, saved[k])
     res = {k: v.float().cpu().numpy() for k, v in out.items()}
     res["loss"] = float(res["loss"][0])
     for k, v in st.views().items():
         res[k] = v.float().cpu().numpy() if hasattr(v, "float") else v
+    del st, out
+    torch.cuda.empty_cache()
     return res
 
 
-def test_paper_c1_full_oracle(cuda_lib):
-    cfg = CONFIGS["paper"]
-    inp = make_inputs(cfg)
-    scale = 1.0 / global_valid_tokens(cfg, cfg.B)
-    g = gpu_run(cfg, inp, scale)
-    f, b = O.fwd_bwd(inp["H_dec"], inp["H_enc"], inp["src_len"], inp["tgt_len"],
-                     inp["tgt_ids"], inp["W_c"], inp["W_out"], scale)
-    assert abs(g["loss"] - f["loss"]) <= 2e-3 * abs(f["loss"]), (g["loss"], f["loss"])
+def check_chunks(g_dw, b_dw, vc, what):
+    """rel-L2 of dW_out per V-chunk of width vc (the last one is the tail)."""
+    V = b_dw.shape[0]
+    worst = 0.0
+    for c0 in range(0, V, vc):
+        e = rel_l2(g_dw[c0:c0 + vc], b_dw[c0:c0 + vc])
+        worst = max(worst, e)
+        assert e <= GRAD_TOL, f"{what}: dW_out chunk [{c0}, {min(V, c0 + vc)}) rel-L2 {e:.3e}"
+    return worst
+
+
+def check_sentences(g, b, tgt_len, src_len, what):
+    for s in range(len(tgt_len)):
+        if tgt_len[s] > 0:
+            e = rel_l2(g["dH_dec"][s], b["dH_dec"][s])
+            assert e <= GRAD_TOL, f"{what}: sentence {s} dH_dec rel-L2 {e:.3e}"
+            e = rel_l2(g["dH_enc"][s], b["dH_enc"][s])
+            assert e <= GRAD_TOL, f"{what}: sentence {s} dH_enc rel-L2 {e:.3e}"
+        else:   # no valid target: the sentence's gradients are exactly zero
+            assert np.all(g["dH_dec"][s] == 0.0) and np.all(g["dH_enc"][s] == 0.0), s
+
+
+_C1 = {}
+
+
+def c1_case(w_out_scale):
+    """C1 inputs and the full fp64 oracle (cached per W_out scale)."""
+    if w_out_scale not in _C1:
+        cfg = CONFIGS["paper"]
+        inp = make_inputs(cfg)
+        if w_out_scale != 1:   # a power of two: the bf16 weights stay exact
+            inp = dict(inp, W_out=inp["W_out"] * w_out_scale)
+        scale = 1.0 / global_valid_tokens(cfg, cfg.B)
+        f, b = O.fwd_bwd(inp["H_dec"], inp["H_enc"], inp["src_len"], inp["tgt_len"],
+                         inp["tgt_ids"], inp["W_c"], inp["W_out"], scale)
+        _C1[w_out_scale] = (cfg, inp, scale, f, b)
+    return _C1[w_out_scale]
+
+
+@pytest.mark.parametrize("mode", ["default", "single", "fused"])
+def test_paper_c1_full_oracle(cuda_lib, mode):
+    """C1, the whole oracle, on the bench's path (default: persistent vocab
+    launch on CTA pairs, logits recomputed per L2-sized V-chunk, never
+    stored) and its variants."""
+    opts = {"default": {}, "single": {"vb_pair": 0}, "fused": {"vb_fwd_fused": 1}}[mode]
+    cfg, inp, scale, f, b = c1_case(1)
+    g = gpu_run(cfg, inp, scale, opts)
+    assert abs(g["loss"] - f["loss"]) <= LOSS_TOL * abs(f["loss"]), (g["loss"], f["loss"])
     for k in ("dH_dec", "dH_enc", "dW_c", "dW_out"):
-        assert rel_l2(g[k], b[k]) <= 2e-2, k
+        assert rel_l2(g[k], b[k]) <= GRAD_TOL, k
+    check_chunks(g["dW_out"], b["dW_out"], g["vocab_chunk"], f"C1 {mode}")
+    check_sentences(g, b, inp["tgt_len"], inp["src_len"], f"C1 {mode}")
     assert rel_l2(g["alpha"], f["alpha"]) <= 1e-2
     assert rel_l2(g["Hc"], f["Hc"]) <= 1e-2
     assert np.max(np.abs(g["lse"] - f["lse"])) <= 2e-2
     assert np.abs(g["alpha"].sum(-1) - 1).max() < 1e-5
+
+
+def test_paper_c1_large_logits(cuda_lib):
+    """W_out x 8: max |logit| ~ 30-40 (a trained model's range).  The
+    backward recomputes the logits in fp32 from the same bf16 operands as the
+    forward, so softmax(l) - onehot stays within the bar; a path that kept
+    the logits in a narrow format would lose ~|l| 2^-11 relative here."""
+    cfg, inp, scale, f, b = c1_case(8)
+    g = gpu_run(cfg, inp, scale)
+    assert np.max(np.abs(f["lse"])) > 20   # the case is what it claims to be
+    assert abs(g["loss"] - f["loss"]) <= LOSS_TOL * abs(f["loss"]), (g["loss"], f["loss"])
+    for k in ("dH_dec", "dH_enc", "dW_c", "dW_out"):
+        assert rel_l2(g[k], b[k]) <= GRAD_TOL, k
+    check_chunks(g["dW_out"], b["dW_out"], g["vocab_chunk"], "C1 x8")
+    check_sentences(g, b, inp["tgt_len"], inp["src_len"], "C1 x8")
+    assert np.all(np.isfinite(g["lse"]))
 
 
 @pytest.mark.parametrize("name,sample", [("large", [0, 1, 137, 255]),
@@ -73,9 +152,9 @@ def test_fullsize_sampled(cuda_lib, name, sample):
     assert rel_l2(g["Hc"][sample], f["Hc"]) <= 1e-2
     assert np.max(np.abs(g["lse"][rows] - f["lse"])) <= 2e-2
     assert rel_l2(g["nll"][rows], f["nll"]) <= 2e-3
-    assert rel_l2(g["dH_dec"][sample], b["dH_dec"]) <= 2e-2
-    assert rel_l2(g["dH_enc"][sample], b["dH_enc"]) <= 2e-2
-    # (b) properties at full size
+    gs = {k: g[k][sample] for k in ("dH_dec", "dH_enc")}
+    check_sentences(gs, b, sub["tgt_len"], sub["src_len"], name)
+    # (c) properties at full size
     assert abs(g["loss"] - scale * g["nll"].astype(np.float64).sum()) <= 1e-4 * abs(g["loss"])
     assert 0.9 * np.log(cfg.V) < g["loss"] < 1.1 * np.log(cfg.V) + 1
     assert np.abs(g["alpha"].sum(-1) - 1).max() < 1e-5
@@ -86,4 +165,36 @@ def test_fullsize_sampled(cuda_lib, name, sample):
         assert np.all(g["dH_dec"][bb, Tb:] == 0.0)
     col = g["dW_out"].astype(np.float64).sum(0)
     assert np.abs(col).max() < 2e-2 * np.abs(g["dW_out"]).sum(0).max()
-    assert np.all(np.isfinite(g["dW_c"])) and np.abs(g["dW_c"]).max() > 0
+
+
+@pytest.mark.parametrize("name,sample", [("large", [0, 137, 255]),
+                                         ("long", [0, 1, 33, 63])])
+def test_fullsize_weight_grads(cuda_lib, name, sample):
+    """(b): the full C3 / C4 launch configuration (T, V, d, the V-chunk
+    schedule and tile counts are those of the bench shape), with tgt_len = 0
+    on every sentence but the sampled ones -- the weight gradients then come
+    from the sampled sentences alone and the oracle computes them exactly."""
+    cfg = CONFIGS[name]
+    inp = make_inputs(cfg)
+    keep = np.zeros(cfg.B, bool)
+    keep[sample] = True
+    inp = dict(inp, tgt_len=np.where(keep, inp["tgt_len"], 0).astype(inp["tgt_len"].dtype))
+    scale = 1.0 / max(1, int(inp["tgt_len"].sum()))
+    g = gpu_run(cfg, inp, scale)
+    sub = {k: (v[sample] if k in ("H_dec", "H_enc", "src_len", "tgt_len", "tgt_ids") else v)
+           for k, v in inp.items()}
+    f, b = O.fwd_bwd(sub["H_dec"], sub["H_enc"], sub["src_len"], sub["tgt_len"],
+                     sub["tgt_ids"], sub["W_c"], sub["W_out"], scale)
+    assert abs(g["loss"] - f["loss"]) <= LOSS_TOL * abs(f["loss"]), (g["loss"], f["loss"])
+    assert rel_l2(g["dW_c"], b["dW_c"]) <= GRAD_TOL
+    assert rel_l2(g["dW_out"], b["dW_out"]) <= GRAD_TOL
+    check_chunks(g["dW_out"], b["dW_out"], g["vocab_chunk"], name)
+    # the d = 2048 (C4) dW_c tiles: per 256-column block of both K segments
+    d = cfg.d
+    for j0 in range(0, 2 * d, 256):
+        e = rel_l2(g["dW_c"][:, j0:j0 + 256], b["dW_c"][:, j0:j0 + 256])
+        assert e <= GRAD_TOL, f"{name}: dW_c columns [{j0}, {j0 + 256}) rel-L2 {e:.3e}"
+    gs = {k: g[k][sample] for k in ("dH_dec", "dH_enc")}
+    check_sentences(gs, b, sub["tgt_len"], sub["src_len"], name)
+    others = ~keep
+    assert np.all(g["dH_dec"][others] == 0.0) and np.all(g["dH_enc"][others] == 0.0)
