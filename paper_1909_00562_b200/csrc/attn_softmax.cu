@@ -32,6 +32,7 @@
 #include "gemm_tc.cuh"
 #include "small_kernels.cuh"
 #include "vocab.cuh"
+#include "attn_tc.cuh"
 
 using namespace attnsm;
 
@@ -157,6 +158,10 @@ static int64_t g_opt_gemm_ctas = 0;
 // previous kernel (their prologue overlaps its tail; they griddepcontrol.wait
 // before touching its results)
 static int g_opt_pdl = 1;
+// "attn_fused": the attention steps as one kernel per direction, one CTA per
+// sentence (attn_tc.cuh; N, M <= 128, d % 64 == 0), else the generic engine's
+// batched score / context GEMMs
+static int g_opt_attn_fused = 1;
 
 // Options are read by a call from its start to its last enqueue under this
 // lock (and written under it), so a concurrent set_option never changes a call
@@ -260,6 +265,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "pdl")) {
     g_opt_pdl = value != 0;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "attn_fused")) {
+    g_opt_attn_fused = value != 0;
     return ATTN_OK;
   }
   if (!strcmp(key, "gemm_ctas")) {
@@ -1129,6 +1138,82 @@ static GemmDesc g_query_bwd_dw(const Plan& p, const Bufs& b, const void* H, floa
   return g;
 }
 
+// ---------------------------------------------------------------- fused attention kernels (attn_tc.cuh)
+static bool attn_fused_ok(const Plan& p) {
+  return g_opt_attn_fused && p.bf16 && p.N <= 128 && p.M <= 128 && p.d % 64 == 0;
+}
+// [B][rows][d] bf16 activations as a 3D map, box {64, box_rows, 1}
+static attn_status_t map_rows3(CUtensorMap* m, const void* ptr, int d, int rows, int B, int box_rows) {
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)rows, (cuuint64_t)B};
+  cuuint64_t str[2] = {(cuuint64_t)d * 2, (cuuint64_t)d * 2 * rows};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  return encode(m, ptr, 0, 3, dims, str, box);
+}
+template <typename P>
+static attn_status_t launch_attn_k(void (*kernel)(P), const P& prm, int B, int smem, cudaStream_t stream) {
+  attn_status_t st;
+  if ((st = ensure_smem_attr(kernel, smem)) != ATTN_OK) return st;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(B);
+  cfg.blockDim = dim3(AT_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_opt_pdl ? 1 : 0;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, prm));
+  ++g_launches;
+  return ATTN_OK;
+}
+// F1 + Eq. 1 + F2 (Eqs. 1-3): alpha (fp32 stash + bf16 copy) and C
+static attn_status_t attn_fused_fwd(const Plan& p, const void* Q, const void* S, const Bufs& b,
+                                    cudaStream_t stream) {
+  static AttnFwdParams P;   // large (5 tensor maps): filled under the option lock
+  memset(&P, 0, sizeof(P));
+  const int mbox = (p.M + 63) / 64 * 64;
+  attn_status_t st;
+  if ((st = map_rows3(&P.m_q, Q, p.d, p.N, p.B, 128)) != ATTN_OK) return st;
+  if ((st = map_rows3(&P.m_s, S, p.d, p.M, p.B, mbox)) != ATTN_OK) return st;
+  if ((st = map_rows3(&P.m_c, b.ctx, p.d, p.N, p.B, 32)) != ATTN_OK) return st;
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)p.M, (cuuint64_t)p.N, (cuuint64_t)p.B};
+    cuuint64_t str[2] = {(cuuint64_t)p.ald * 4, (cuuint64_t)p.ald * 4 * p.N};
+    cuuint32_t box[3] = {32, 32, 1};
+    if ((st = encode(&P.m_stash, b.alpha, 1, 3, dims, str, box)) != ATTN_OK) return st;
+  }
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)p.Mp, (cuuint64_t)p.N, (cuuint64_t)p.B};
+    cuuint64_t str[2] = {(cuuint64_t)p.Mp * 2, (cuuint64_t)p.Mp * 2 * p.N};
+    cuuint32_t box[3] = {32, 32, 1};
+    if ((st = encode(&P.m_abf, b.abf, 0, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B)) != ATTN_OK)
+      return st;
+  }
+  P.src_len = b.src_len;
+  P.d = p.d;
+  P.mbox = mbox;
+  return launch_attn_k(attn_fwd_kernel, P, p.B, ATF_SMEM, stream);
+}
+// B3: dH_dec = dH_part + de S (dot score; general score: dQ = de S),
+// dH_enc = alpha^T dC + de^T Q
+static attn_status_t attn_fused_bwd(const Plan& p, const void* Q, const void* S, void* dH, void* dS,
+                                    const Bufs& b, bool general, cudaStream_t stream) {
+  static AttnBwdParams P;
+  memset(&P, 0, sizeof(P));
+  const int mbox = (p.M + 63) / 64 * 64;
+  attn_status_t st;
+  if ((st = map_rows3(&P.m_dc, b.dcbf, p.d, p.N, p.B, 128)) != ATTN_OK) return st;
+  if ((st = map_rows3(&P.m_s, S, p.d, p.M, p.B, mbox)) != ATTN_OK) return st;
+  if ((st = map_rows3(&P.m_q, Q, p.d, p.N, p.B, 128)) != ATTN_OK) return st;
+  if ((st = map_rows3(&P.m_dh, general ? b.dq : dH, p.d, p.N, p.B, 32)) != ATTN_OK) return st;
+  if ((st = map_rows3(&P.m_dhe, dS, p.d, p.M, p.B, 32)) != ATTN_OK) return st;
+  P.alpha = b.alpha;
+  P.dh_part = general ? nullptr : b.dhpart;
+  P.N = p.N; P.M = p.M; P.d = p.d; P.ald = (int)p.ald; P.mbox = mbox;
+  return launch_attn_k(attn_bwd_kernel, P, p.B, ATB_SMEM, stream);
+}
+
 // ---------------------------------------------------------------- attention on tcgen05 (bf16)
 // One small GEMM per sentence (batched problems; M <= 128 source positions).
 static attn_status_t attention_forward_tc(const Plan& p, const void* H, const void* S, const Bufs& b,
@@ -1143,6 +1228,7 @@ static attn_status_t attention_forward_tc(const Plan& p, const void* H, const vo
     if (st != ATTN_OK) return st;
     Q = b.q;
   }
+  if (attn_fused_ok(p)) return attn_fused_fwd(p, Q, S, b, stream);
   // F1 + Eq. 1: scores E_b = H_b S_b^T with the masked row softmax fused
   {
     GemmDesc g;
@@ -1173,6 +1259,12 @@ static attn_status_t attention_backward_tc(const Plan& p, const void* H, const v
                                            float* dWa) {
   const int d = p.d, N = p.N, M = p.M, Mp = p.Mp, B = p.B;
   const void* Q = Wa ? b.q : H;
+  if (attn_fused_ok(p)) {
+    attn_status_t st = attn_fused_bwd(p, Q, S, dH, dS, b, Wa != nullptr, stream);
+    if (st != ATTN_OK || !Wa) return st;
+    GemmDesc ga[2] = {g_query_bwd_dh(p, b, Wa, dH, EPI_ADD_BF16), g_query_bwd_dw(p, b, H, dWa)};
+    return launch_tc_group<__nv_bfloat16>(ga, 2, next(ctx_), stream, PAIR_PBWD);
+  }
   // dalpha_b = dC_b S_b^T with the softmax backward fused: de (bf16)
   {
     GemmDesc g;

@@ -78,7 +78,8 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, wide):
 
 # ------------------------------------------------------ end-to-end parity --
 _DEFAULTS = {"store_logits": 0, "wide_tiles": 2, "db_gemm": -1, "vb_pair": 1, "vb_fwd_fused": 0,
-             "vb_order": 1, "dl_buffers": 3, "dl_budget_mb": 120, "vb_last_g2_first": 1}
+             "vb_order": 1, "dl_buffers": 3, "dl_budget_mb": 120, "vb_last_g2_first": 1,
+             "attn_fused": 1}
 _MODES = {
     "default": {},                                  # persistent vocab launch on CTA pairs
     "single": {"vb_pair": 0},                       # ... on single-CTA 128 x 256 tiles
@@ -90,6 +91,7 @@ _MODES = {
     "sl": {"store_logits": 1},                      # ablation: stored fp16 logits, wide tiles
     "sl128": {"store_logits": 1, "wide_tiles": 0},  # ... on 128 x 256 tiles
     "sl2": {"store_logits": 2},                     # ... serialised dlogits kernels
+    "attn_generic": {"attn_fused": 0},              # attention on the generic engine's batched GEMMs
 }
 
 
@@ -130,7 +132,10 @@ def set_modes(binding, mode):
                                           ("small", 1024, "sl"), ("medium", 0, "sl"),
                                           ("medium", 2048, "sl128"), ("odd", 256, "sl"),
                                           ("edge_min", 0, "sl"), ("edge_max_src", 256, "sl128"),
-                                          ("small", 0, "sl2"), ("odd", 256, "sl2")])
+                                          ("small", 0, "sl2"), ("odd", 256, "sl2"),
+                                          ("small", 0, "attn_generic"), ("medium", 0, "attn_generic"),
+                                          ("edge_max_src", 0, "attn_generic"),
+                                          ("edge_min", 0, "attn_generic")])
 def test_parity_vs_oracle(cuda_lib, name, vc, mode):
     """mode = library options (see set_modes); vc = V-chunk width (0 = auto)."""
     from paper_1909_00562_b200 import binding
@@ -169,7 +174,8 @@ def test_parity_vs_oracle(cuda_lib, name, vc, mode):
                                           ("odd_f32", 0, "default"), ("small", 0, "default"),
                                           ("small", 1024, "single"), ("medium", 0, "default"),
                                           ("medium", 512, "fused"), ("odd", 256, "default"),
-                                          ("odd", 256, "sl")])
+                                          ("odd", 256, "sl"), ("small", 0, "attn_generic"),
+                                          ("medium", 0, "attn_generic")])
 def test_parity_general_score(cuda_lib, name, vc, mode):
     """NEXT-1: the Eq. 2 "general" score alpha_hat = H^T W_alpha S
      -- Q = H W_alpha on the tensor cores, dW_alpha = H^T dQ,
