@@ -162,6 +162,9 @@ static int g_opt_pdl = 1;
 // sentence (attn_tc.cuh; N, M <= 128, d % 64 == 0), else the generic engine's
 // batched score / context GEMMs
 static int g_opt_attn_fused = 1;
+// "attn_trace": device buffer of globaltimer stamps, [2][B][16] int64 (forward,
+// backward) + [B][64][4] backward chunk stamps (scripts/attn_trace.py)
+static long long* g_attn_trace = nullptr;
 
 // Options are read by a call from its start to its last enqueue under this
 // lock (and written under it), so a concurrent set_option never changes a call
@@ -265,6 +268,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "pdl")) {
     g_opt_pdl = value != 0;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "attn_trace")) {
+    g_attn_trace = reinterpret_cast<long long*>(value);
     return ATTN_OK;
   }
   if (!strcmp(key, "attn_fused")) {
@@ -932,6 +939,7 @@ struct Bufs {
   unsigned* vbctr; // persistent vocab backward: tile counter + dependency counters
   void* q;    // Eq. 2 general score: Q = H W_alpha [T, d] (dtype)
   void* dq;   // its gradient [T, d] (dtype); aliases dz, which is dead by then
+  void* dq2;  // fused attention, dot score: dQ = de S bf16 [T, d] (the dH_part slot, unused then)
 };
 
 static Bufs carve(const Plan& p, void* ws) {
@@ -964,6 +972,7 @@ static Bufs carve(const Plan& p, void* ws) {
   b.logits = p.store_logits ? w + p.off_logits : nullptr;
   b.vbctr = (unsigned*)(w + p.off_vbctr);
   b.dq = b.dz;
+  b.dq2 = b.dhc2;
   return b;
 }
 
@@ -1091,6 +1100,24 @@ static GemmDesc g_dwc(const Plan& p, const Bufs& b, const void* H, float* dW_c) 
   g.epi.ncols_valid = 2 * d; g.epi.ncols_store = 2 * d;
   return g;
 }
+// B2, split-K half `h` of dW_c (K = rows [k0, k1) of T): reduce-added into
+// the zeroed dW_c (two addends onto 0: the sum is order-independent, exact
+// IEEE commutativity, so deterministic)
+static GemmDesc g_dwc_half(const Plan& p, const Bufs& b, const void* H, float* dW_c, int h) {
+  GemmDesc g;
+  const int d = p.d;
+  // h = -1: one problem over all of T (small T)
+  const long long mid = ((p.T / 2 + 63) / 64) * 64;
+  const long long k0 = h == 1 ? mid : 0, k1 = h == 0 ? mid : p.T;
+  const size_t off = (size_t)k0 * d * p.elt;
+  g.M = d; g.N = 2 * d; g.K = (int)(k1 - k0);
+  g.a_mn = 1; g.a0 = mnmaj((const char*)b.dz + off, k1 - k0, d, d);
+  g.b_mn = 1; g.b0 = mnmaj((const char*)H + off, k1 - k0, d, d);
+  g.b1 = mnmaj((const char*)b.ctx + off, k1 - k0, d, d); g.b_nsplit = d;
+  g.epi.kind = EPI_ACCUM_F32; g.epi.out = dW_c; g.epi.ldo = 2ll * d;
+  g.epi.ncols_valid = 2 * d; g.epi.ncols_store = 2 * d;
+  return g;
+}
 // B2: dz W_c restricted to output columns [col0, col0 + ncol) (W_c MN-major)
 static GemmDesc g_dzwc(const Plan& p, const Bufs& b, const void* W_c, int col0, int ncol,
                        int kind, void* out, long long ldo) {
@@ -1172,9 +1199,9 @@ static attn_status_t attn_fused_fwd(const Plan& p, const void* Q, const void* S,
                                     cudaStream_t stream) {
   static AttnFwdParams P;   // large (5 tensor maps): filled under the option lock
   memset(&P, 0, sizeof(P));
-  const int mbox = (p.M + 63) / 64 * 64;
+  const int mbox = (p.M + 63) / 64 * 64, qrows = (p.N + 15) / 16 * 16;
   attn_status_t st;
-  if ((st = map_rows3(&P.m_q, Q, p.d, p.N, p.B, 128)) != ATTN_OK) return st;
+  if ((st = map_rows3(&P.m_q, Q, p.d, p.N, p.B, qrows)) != ATTN_OK) return st;
   if ((st = map_rows3(&P.m_s, S, p.d, p.M, p.B, mbox)) != ATTN_OK) return st;
   if ((st = map_rows3(&P.m_c, b.ctx, p.d, p.N, p.B, 32)) != ATTN_OK) return st;
   {
@@ -1193,24 +1220,26 @@ static attn_status_t attn_fused_fwd(const Plan& p, const void* Q, const void* S,
   P.src_len = b.src_len;
   P.d = p.d;
   P.mbox = mbox;
+  P.qrows = qrows;
+  P.store_abf = 0;   // the fused backward builds its bf16 alpha tile from the fp32 stash
+  P.trace = g_attn_trace;
   return launch_attn_k(attn_fwd_kernel, P, p.B, ATF_SMEM, stream);
 }
-// B3: dH_dec = dH_part + de S (dot score; general score: dQ = de S),
-// dH_enc = alpha^T dC + de^T Q
-static attn_status_t attn_fused_bwd(const Plan& p, const void* Q, const void* S, void* dH, void* dS,
-                                    const Bufs& b, bool general, cudaStream_t stream) {
+// B3: dQ = de S (bf16, into `dq`), dH_enc = alpha^T dC + de^T Q
+static attn_status_t attn_fused_bwd(const Plan& p, const void* Q, const void* S, void* dq, void* dS,
+                                    const Bufs& b, cudaStream_t stream) {
   static AttnBwdParams P;
   memset(&P, 0, sizeof(P));
-  const int mbox = (p.M + 63) / 64 * 64;
+  const int mbox = (p.M + 63) / 64 * 64, qrows = (p.N + 15) / 16 * 16;
   attn_status_t st;
-  if ((st = map_rows3(&P.m_dc, b.dcbf, p.d, p.N, p.B, 128)) != ATTN_OK) return st;
+  if ((st = map_rows3(&P.m_dc, b.dcbf, p.d, p.N, p.B, qrows)) != ATTN_OK) return st;
   if ((st = map_rows3(&P.m_s, S, p.d, p.M, p.B, mbox)) != ATTN_OK) return st;
-  if ((st = map_rows3(&P.m_q, Q, p.d, p.N, p.B, 128)) != ATTN_OK) return st;
-  if ((st = map_rows3(&P.m_dh, general ? b.dq : dH, p.d, p.N, p.B, 32)) != ATTN_OK) return st;
+  if ((st = map_rows3(&P.m_q, Q, p.d, p.N, p.B, qrows)) != ATTN_OK) return st;
+  if ((st = map_rows3(&P.m_dq, dq, p.d, p.N, p.B, 32)) != ATTN_OK) return st;
   if ((st = map_rows3(&P.m_dhe, dS, p.d, p.M, p.B, 32)) != ATTN_OK) return st;
   P.alpha = b.alpha;
-  P.dh_part = general ? nullptr : b.dhpart;
-  P.N = p.N; P.M = p.M; P.d = p.d; P.ald = (int)p.ald; P.mbox = mbox;
+  P.N = p.N; P.M = p.M; P.d = p.d; P.ald = (int)p.ald; P.mbox = mbox; P.qrows = qrows;
+  P.trace = g_attn_trace ? g_attn_trace + (long long)p.B * 16 : nullptr;
   return launch_attn_k(attn_bwd_kernel, P, p.B, ATB_SMEM, stream);
 }
 
@@ -1260,7 +1289,10 @@ static attn_status_t attention_backward_tc(const Plan& p, const void* H, const v
   const int d = p.d, N = p.N, M = p.M, Mp = p.Mp, B = p.B;
   const void* Q = Wa ? b.q : H;
   if (attn_fused_ok(p)) {
-    attn_status_t st = attn_fused_bwd(p, Q, S, dH, dS, b, Wa != nullptr, stream);
+    // dot score: dQ into b.dq2, added to dz W_c[:, :d] by the caller's second
+    // projection-backward launch; general score: dQ into b.dq, then
+    // dH_dec = dH_part + dQ W_alpha^T and dW_alpha = H^T dQ
+    attn_status_t st = attn_fused_bwd(p, Q, S, Wa ? b.dq : b.dq2, dS, b, stream);
     if (st != ATTN_OK || !Wa) return st;
     GemmDesc ga[2] = {g_query_bwd_dh(p, b, Wa, dH, EPI_ADD_BF16), g_query_bwd_dw(p, b, H, dWa)};
     return launch_tc_group<__nv_bfloat16>(ga, 2, next(ctx_), stream, PAIR_PBWD);
@@ -1706,11 +1738,17 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
     }
   }
   }   // fp32 path / stored-logits ablation
-  // tanh backward of Eq. 4: dz = dHc (1 - H_c^2)
+  // dot score with the fused attention kernels: B2 as {dC, dW_c split-K in
+  // two halves} before the attention backward and {dH_dec = dz W_c[:, :d] +
+  // dQ} after it (the 64 long dW_c tiles balance against the dC tiles; dQ
+  // travels as bf16 instead of an fp32 dH_part)
+  const bool b2split = tc && !Wa && attn_fused_ok(p);
+  // tanh backward of Eq. 4: dz = dHc (1 - H_c^2)  (and, split B2: dW_c = 0)
   {
     const long long n = TT * d;
     st = launch_pdl(dz_kernel<T>, dim3((int)std::min<long long>((n + 255) / 256, 148ll * 16)),
-                    dim3(256), stream, (const float*)b.dhc, (const T*)b.hc, (T*)b.dz, n);
+                    dim3(256), stream, (const float*)b.dhc, (const T*)b.hc, (T*)b.dz, n,
+                    reinterpret_cast<float4*>(dW_c), b2split ? (long long)d * 2 * d / 4 : 0ll);
     if (st != ATTN_OK) return st;
   }
   prof_mark(p.vb ? "dz" : "vocab_bwd", stream, true);
@@ -1718,8 +1756,18 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   {
     GemmDesc gs[3];
     int n = 0;
-    gs[n++] = g_dwc(p, b, H, dW_c);
-    if (tc) {
+    if (b2split && p.T >= 256) {
+      gs[n++] = g_dwc_half(p, b, H, dW_c, 0);
+      gs[n++] = g_dwc_half(p, b, H, dW_c, 1);
+      gs[n++] = g_dzwc(p, b, W_c, d, d, EPI_STORE_BF16, b.dcbf, d);
+    } else if (b2split) {
+      gs[n++] = g_dwc_half(p, b, H, dW_c, -1);
+      gs[n++] = g_dzwc(p, b, W_c, d, d, EPI_STORE_BF16, b.dcbf, d);
+    } else {
+      gs[n++] = g_dwc(p, b, H, dW_c);
+    }
+    if (b2split) {
+    } else if (tc) {
       gs[n++] = g_dzwc(p, b, W_c, 0, d, EPI_STORE_F32, b.dhpart, d);
       gs[n++] = g_dzwc(p, b, W_c, d, d, EPI_STORE_BF16, b.dcbf, d);
     } else {
@@ -1747,6 +1795,13 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
     }
   }
   if (st != ATTN_OK) return st;
+  if (b2split) {   // dH_dec = dz W_c[:, :d] + dQ (bf16 addend)
+    GemmDesc g = g_dzwc(p, b, W_c, 0, d, EPI_ADD_BF16, dH, d);
+    g.epi.addend = reinterpret_cast<const float*>(b.dq2);
+    g.epi.addend_bf16 = 1;
+    g.epi.add_ld = d;
+    if ((st = gemm(&g, 1, PAIR_PBWD)) != ATTN_OK) return st;
+  }
   prof_mark("attn_bwd", stream);
   if (comm && dWa) {
     if ((st = comm_enqueue_allreduce(comm, &cr, stream, dWa, (size_t)d * d)) != ATTN_OK) return st;

@@ -25,7 +25,8 @@ enum EpiKind : int {
   EPI_STORE_F32 = 0, EPI_TANH = 1, EPI_LSE = 2, EPI_DLOGITS = 3, EPI_ACCUM_F32 = 4,
   EPI_NONE = 5,               // debug: read the accumulator, store nothing
   EPI_STORE_BF16 = 6,         // out = acc (bf16): C, dC, dH_enc
-  EPI_ADD_BF16 = 7,           // out = acc + addend (fp32) -> bf16: dH_dec = dH_part + de S
+  EPI_ADD_BF16 = 7,           // out = acc + addend (fp32, or bf16 with addend_bf16) -> bf16:
+                              // dH_dec = dH_part + de S, or dz W_c[:, :d] + dQ
   EPI_ATTN_SOFTMAX = 8,       // masked row softmax of the scores (Eq. 1), tcgen05 path
   EPI_ATTN_SOFTMAX_BWD = 9,   // its backward, tcgen05 path
   EPI_TOPK = 11               // decoding step (NEXT-4): LSE partials as EPI_LSE plus the 8 best
@@ -57,7 +58,8 @@ struct EpiParams {
   float* stash_f32;      // ATTN_SOFTMAX(_BWD): alpha fp32 [rows, stash_ld] (cols < ncols_valid)
   long long stash_ld;
   const int* src_len;    // ATTN_SOFTMAX: [batch]
-  const float* addend;   // ADD_BF16: [rows, add_ld] fp32
+  const float* addend;   // ADD_BF16: [rows, add_ld] fp32 (bf16 when addend_bf16)
+  int addend_bf16;
   long long add_ld;
   uint32_t* topk;        // TOPK: [rows, part_ld, 8] 32-bit keys (tk_key32) per slot, best first
   const void* bias;      // LSE / DLOGITS / TOPK: optional F_c bias b_out [V] (OutT), indexed by

@@ -624,15 +624,31 @@ __global__ void __maxnreg__(128) gemm_tc_kernel(const __grid_constant__ TcParams
             epi.transform(col, v);
           }
           if (kind == EPI_ADD_BF16 && row_ok) {
-            const float4* ad = reinterpret_cast<const float4*>(pr.epi.addend +
-                                                               (long long)rowg * pr.epi.add_ld + col);
+            if (pr.epi.addend_bf16) {
+              const uint4* ad = reinterpret_cast<const uint4*>(
+                  reinterpret_cast<const __nv_bfloat16*>(pr.epi.addend) + (long long)rowg * pr.epi.add_ld + col);
 #pragma unroll
-            for (int g = 0; g < 8; ++g) {
-              const float4 a4 = ad[g];
-              v[4 * g] += a4.x;
-              v[4 * g + 1] += a4.y;
-              v[4 * g + 2] += a4.z;
-              v[4 * g + 3] += a4.w;
+              for (int g = 0; g < 4; ++g) {
+                const uint4 u = ad[g];
+                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
+                  v[8 * g + 2 * e] += f.x;
+                  v[8 * g + 2 * e + 1] += f.y;
+                }
+              }
+            } else {
+              const float4* ad = reinterpret_cast<const float4*>(pr.epi.addend +
+                                                                 (long long)rowg * pr.epi.add_ld + col);
+#pragma unroll
+              for (int g = 0; g < 8; ++g) {
+                const float4 a4 = ad[g];
+                v[4 * g] += a4.x;
+                v[4 * g + 1] += a4.y;
+                v[4 * g + 2] += a4.z;
+                v[4 * g + 3] += a4.w;
+              }
             }
           }
           if (f32out) {

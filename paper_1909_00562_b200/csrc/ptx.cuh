@@ -107,6 +107,10 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+// at most one committed bulk group may still be reading shared memory
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 // Programmatic dependent launch (the next kernel of the stream may be
 // scheduled before this one finishes; it must pdl_wait() before touching
 // anything this grid writes).
@@ -145,6 +149,13 @@ __device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* m, const vo
           reinterpret_cast<uint64_t>(m)),
       "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
+}
+__device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
 }
 __device__ __forceinline__ void st_shared_u16(uint32_t addr, unsigned short v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v));
@@ -221,6 +232,15 @@ __device__ __forceinline__ void tma_reduce_add_2d_hint(const CUtensorMap* m, con
       : "memory");
 }
 // drop a 128-byte L2 line without writing it back (its contents become undefined)
+// 16-byte asynchronous global -> shared copy (LDGSTS), completed by cp_async_wait_all
+__device__ __forceinline__ void cp_async16(uint32_t smem_dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// bring `bytes` (multiple of 16) of global memory into L2 (no destination)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void discard_l2_line(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }

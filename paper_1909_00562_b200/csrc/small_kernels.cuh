@@ -142,10 +142,12 @@ __global__ void __launch_bounds__(256) lse_reduce_kernel(
 template <typename T>
 __global__ void __launch_bounds__(256) dz_kernel(const float* __restrict__ dhc,
                                                  const T* __restrict__ hc, T* __restrict__ dz,
-                                                 long long n) {
+                                                 long long n, float4* __restrict__ zero, long long nzero4) {
   pdl_wait();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
+  // side job: zero `nzero4` float4 of `zero` (dW_c, summed by split-K reduce-adds)
+  for (long long k = i; k < nzero4; k += stride) zero[k] = make_float4(0.f, 0.f, 0.f, 0.f);
   if constexpr (sizeof(T) == 2) {
     // 8 elements per thread and iteration: 2 x 16 B of dHc, 16 B of H_c, 16 B of dz
     const long long n8 = n / 8;
