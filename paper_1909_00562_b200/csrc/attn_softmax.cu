@@ -767,8 +767,12 @@ static Plan make_plan(const attn_shape_t* s) {
   p.nbuf = p.vb ? g_opt_dl_nbuf : 2;
   if (vc <= 0) {
     if (p.vb) {
-      // the NB dL buffers [T, Vc] bf16 fit the L2 budget
+      // the NB dL buffers [T, Vc] bf16 fit the L2 budget (DESIGN.md "V-chunk
+      // schedule"), but at most 25 chunks: each chunk re-reads and re-writes
+      // dHc [T, d] fp32, which outweighs L2 residency of dL at large T
+      // (C3, T = 16384: 1280 -> 4096 columns, measured 8.77 -> 8.40 ms)
       vc = (g_opt_dl_budget_mb << 20) / ((long long)p.nbuf * p.T * 2) / 256 * 256;
+      vc = std::max(vc, ((long long)(p.V + 24) / 25 + 255) / 256 * 256);
       vc = std::max(vc, 256ll);
     } else if (p.store_logits && (g_opt_wide & PAIR_VBWD)) {
       vc = model_chunk_width(p.T, p.d, p.V);
