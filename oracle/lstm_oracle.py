@@ -1,0 +1,105 @@
+"""fp64 CPU oracle for the model-parallel half of Fig. 3 (NEXT-3): the
+stacked-LSTM encoder and decoder that produce the hidden states S (= H_enc)
+and H (= H_dec) the attention-softmax stage consumes.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s cpu baseline may import this module; the product path never
+imports, links or executes it, and the two share no code.
+
+What it computes (§3.1-3.2; Table 1 PAPER.md:190-192 gives
+the sizes: embedding 512, hidden 1024, 4 stacked LSTM layers):
+
+* the proposed HybridNMT model REMOVES input feeding, so
+  the decoder's first layer sees only the target word embedding, and every
+  layer-step (l, t) depends only on (l, t-1) and (l-1, t) -- the "green arrow"
+  wavefront of Fig. 3;
+* each layer is the standard LSTM cell of Luong et al. (the baseline the paper
+  builds on), with PyTorch's gate order (i, f, g, o):
+      gates = W_ih x_t + W_hh h_{t-1} + b
+      i = sigma(gates_i), f = sigma(gates_f), g = tanh(gates_g), o = sigma(gates_o)
+      c_t = f * c_{t-1} + i * g,   h_t = o * tanh(c_t)
+  (readings N1-N4 in DESIGN.md: one bias per layer, zero initial state for
+  the encoder, the decoder layer l starts from the encoder layer l's state at
+  the last REAL source position src_len[b] - 1, and the recurrences run over
+  the padded lengths -- states past a sentence's end are computed but never
+  read by the attention, whose mask excludes them);
+* embeddings: x_t = E[y_t] (source and target tables).
+
+Storage (row-major): ids [B, T] int; E [V, e]; W_ih[l] [4h, in_l] (in_0 = e,
+else h); W_hh[l] [4h, h]; b[l] [4h]; outputs H [B, T, h] (the top layer, all
+steps) and the per-layer final states.
+
+Pinned by tests/test_lstm_oracle_pins.py: equality with torch.nn.LSTM in
+float64 (an independent implementation of the same cell), the zero-weight and
+bias-only closed forms, and the decoder-initialisation rule.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = ["sigmoid", "lstm_cell", "lstm_stack", "encoder_decoder"]
+
+
+def sigmoid(x):
+    return 1.0 / (1.0 + np.exp(-x))
+
+
+def lstm_cell(x, h, c, W_ih, W_hh, b):
+    """One LSTM step for a batch (PAPER.md:75 baseline cell, gate order i, f, g, o).
+    x [B, in], h / c [B, hd] -> (h', c')."""
+    x = np.asarray(x, np.float64)
+    h = np.asarray(h, np.float64)
+    c = np.asarray(c, np.float64)
+    gates = x @ np.asarray(W_ih, np.float64).T + h @ np.asarray(W_hh, np.float64).T + np.asarray(b, np.float64)
+    hd = h.shape[1]
+    i = sigmoid(gates[:, 0 * hd:1 * hd])
+    f = sigmoid(gates[:, 1 * hd:2 * hd])
+    g = np.tanh(gates[:, 2 * hd:3 * hd])
+    o = sigmoid(gates[:, 3 * hd:4 * hd])
+    c_new = f * c + i * g
+    h_new = o * np.tanh(c_new)
+    return h_new, c_new
+
+
+def lstm_stack(X, weights, h0=None, c0=None, capture_at=None):
+    """Stacked LSTM over all T steps, layer by layer (the order of evaluation
+    does not change the result; the wavefront only reorders independent
+    layer-steps).  X [B, T, in_0]; weights = [(W_ih, W_hh, b)] * L.
+    h0 / c0: [L, B, hd] initial states (None = zeros).  capture_at: [B] step
+    index whose states are returned per layer (None = the last step).
+    Returns (H_top [B, T, hd], H_all [L, B, T, hd], h_cap [L, B, hd], c_cap [L, B, hd])."""
+    X = np.asarray(X, np.float64)
+    B, T, _ = X.shape
+    L = len(weights)
+    hd = np.asarray(weights[0][1]).shape[1]
+    cap = np.full(B, T - 1) if capture_at is None else np.asarray(capture_at)
+    H_all = np.zeros((L, B, T, hd))
+    h_cap = np.zeros((L, B, hd))
+    c_cap = np.zeros((L, B, hd))
+    inp = X
+    for l, (W_ih, W_hh, b) in enumerate(weights):
+        h = np.zeros((B, hd)) if h0 is None else np.asarray(h0[l], np.float64).copy()
+        c = np.zeros((B, hd)) if c0 is None else np.asarray(c0[l], np.float64).copy()
+        for t in range(T):
+            h, c = lstm_cell(inp[:, t, :], h, c, W_ih, W_hh, b)
+            H_all[l, :, t, :] = h
+            sel = cap == t
+            h_cap[l, sel] = h[sel]
+            c_cap[l, sel] = c[sel]
+        inp = H_all[l]
+    return H_all[L - 1], H_all, h_cap, c_cap
+
+
+def encoder_decoder(src_ids, tgt_ids, src_len, E_src, E_tgt, enc_weights, dec_weights):
+    """The encoder-decoder part of HybridNMT (no input feeding):
+    S = encoder top-layer states for every source step, H = decoder top-layer
+    states for every target step; decoder layer l starts from encoder layer
+    l's state at source step src_len[b] - 1 (reading N3).
+    Returns (S [B, M, hd], H [B, N, hd])."""
+    E_src = np.asarray(E_src, np.float64)
+    E_tgt = np.asarray(E_tgt, np.float64)
+    Xs = E_src[np.asarray(src_ids)]
+    Xt = E_tgt[np.asarray(tgt_ids)]
+    S, _, h_fin, c_fin = lstm_stack(Xs, enc_weights, capture_at=np.asarray(src_len) - 1)
+    H, _, _, _ = lstm_stack(Xt, dec_weights, h0=h_fin, c0=c_fin)
+    return S, H

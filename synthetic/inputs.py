@@ -25,7 +25,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 __all__ = ["Config", "CONFIGS", "round_bf16", "lengths", "make_inputs",
-           "make_weights", "shard_range", "global_valid_tokens"]
+           "make_weights", "shard_range", "global_valid_tokens", "make_lstm_inputs"]
 
 
 @dataclass(frozen=True)
@@ -185,3 +185,47 @@ def shard_range(B_global: int, world: int, rank: int):
     base, extra = divmod(B_global, world)
     start = rank * base + min(rank, extra)
     return start, start + base + (1 if rank < extra else 0)
+
+
+def make_lstm_inputs(cfg: Config, layers: int = 4, emb: Optional[int] = None,
+                     sentences: Optional[Sequence[int]] = None):
+    """Inputs of the encoder-decoder part (NEXT-3; Table 1, PAPER.md:190-192:
+    embedding 512, hidden 1024, 4 stacked LSTM layers): source / target ids
+    [B, M] / [B, N] ~ U{4 .. V-1} (one vocabulary of size V for both sides),
+    the config's lengths, embedding tables E_src / E_tgt [V, emb] and per
+    layer (W_ih [4h, in], W_hh [4h, h], b [4h]) for the encoder and the
+    decoder, all ~ U(-0.1, 0.1) (SPEC.md:273 init) and bf16-rounded for bf16
+    configs.  emb defaults to h / 2 (512 for h = 1024)."""
+    if sentences is None:
+        sentences = range(cfg.B)
+    sentences = list(sentences)
+    B, N, M, h, V = len(sentences), cfg.N, cfg.M, cfg.d, cfg.V
+    e = emb if emb is not None else max(16, h // 2)
+    src_ids = np.empty((B, M), np.int32)
+    tgt_ids = np.empty((B, N), np.int32)
+    src = np.empty(B, np.int32)
+    tgt = np.empty(B, np.int32)
+    for k, b in enumerate(sentences):
+        src[k], tgt[k] = lengths(cfg, b)
+        rng = np.random.default_rng([cfg.seed, b, 2])
+        src_ids[k] = rng.integers(4, V, size=M)
+        tgt_ids[k] = rng.integers(4, V, size=N)
+
+    def u(tag, shape):
+        return np.random.default_rng([cfg.seed, tag]).uniform(-0.1, 0.1, size=shape).astype(np.float32)
+
+    out = dict(src_ids=src_ids, tgt_ids=tgt_ids, src_len=src, tgt_len=tgt,
+               E_src=u(2001, (V, e)), E_tgt=u(2002, (V, e)))
+    for side, base in (("enc", 3000), ("dec", 4000)):
+        ws = []
+        for l in range(layers):
+            fin = e if l == 0 else h
+            ws.append((u(base + 10 * l, (4 * h, fin)), u(base + 10 * l + 1, (4 * h, h)),
+                       u(base + 10 * l + 2, (4 * h,))))
+        out[side] = ws
+    if cfg.dtype == "bf16":
+        out["E_src"] = round_bf16(out["E_src"])
+        out["E_tgt"] = round_bf16(out["E_tgt"])
+        for side in ("enc", "dec"):
+            out[side] = [tuple(round_bf16(w) for w in ws) for ws in out[side]]
+    return out
