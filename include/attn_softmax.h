@@ -282,6 +282,62 @@ attn_status_t attn_adam_step_sharded(attn_comm_t* c, const attn_adam_t* h, size_
                                      float* g, float* w_shard, float* m_shard,
                                      float* v_shard, void* w_bf16, void* stream);
 
+/* ---------------------------------------------------------------- NEXT-3
+ * The model-parallel half of Fig. 3: the stacked-LSTM
+ * encoder and decoder WITHOUT input feeding that produce
+ * H_enc (the paper's S) and H_dec (H), the inputs of attn_softmax_fwd_bwd.
+ * Forward only.  Cell (PyTorch gate order i, f, g, o; N1-N4):
+ *   gates = W_ih x_t + W_hh h_{t-1} + b;  c_t = s(f) c_{t-1} + s(i) tanh(g);
+ *   h_t = s(o) tanh(c_t).  Encoder: zero initial state, over all M steps;
+ *   decoder layer l starts from encoder layer l's (h, c) at source step
+ *   src_len[b] - 1, over all N steps.  Layer-step (l, t) depends only on
+ *   (l, t-1) and (l-1, t): the kernels run that wavefront
+ *   with SM groups in the role of the paper's GPUs. */
+typedef struct {
+  int32_t batch;      /* B <= 128 sentences (one 128-row MMA tile per step) */
+  int32_t src_len;    /* M, padded source length */
+  int32_t tgt_len;    /* N, padded target length */
+  int32_t emb;        /* embedding size e (Table 1: 512), multiple of 64 */
+  int32_t hidden;     /* hidden size h (Table 1: 1024), multiple of 64 */
+  int32_t layers;     /* L in [1, 8] (Table 1: 4) */
+  int32_t vocab_src, vocab_tgt;
+} attn_lstm_shape_t;
+
+/* Workspace bytes of attn_encoder_decoder_fwd (0 on an invalid shape). */
+size_t attn_lstm_workspace_size(const attn_lstm_shape_t* s);
+/* Bytes of one packed layer: bf16 [4 hidden][in + hidden]. */
+size_t attn_lstm_packed_bytes(int in, int hidden);
+/* Pack one layer for the kernels: W_ih [4h][in], W_hh [4h][h], b [4h] (bf16,
+ * PyTorch layout: gate blocks i, f, g, o) -> W_packed [4h][in + h] bf16 with
+ * row 4u + q = [W_ih | W_hh] row q h + u (gate-interleaved) and b_packed [4h]
+ * fp32 likewise.  Device buffers, asynchronous on `stream`. */
+attn_status_t attn_lstm_pack_layer(int in, int hidden, const void* W_ih, const void* W_hh,
+                                   const void* b, void* W_packed, float* b_packed, void* stream);
+/* Encoder-decoder forward.  src_ids [B][M], tgt_ids [B][N] int32 (device,
+ * every id in [0, vocab)); src_lens_host [B] HOST (1 <= len <= M); E_src
+ * [vocab_src][e], E_tgt [vocab_tgt][e] bf16; enc_W / dec_W: HOST arrays of
+ * `layers` device pointers to packed layers (attn_lstm_pack_layer; layer 0
+ * has in = e, the others in = h), enc_b / dec_b likewise (packed fp32 biases).
+ * Outputs H_enc [B][M][h], H_dec [B][N][h] bf16 (the top layer's states at
+ * every step).  Errors: ATTN_ERR_UNSUPPORTED for B > 128, sizes not multiples
+ * of 64 or layers x (h / 32) CTAs beyond the SM count; ATTN_ERR_SHAPE for a
+ * source length outside [1, M]. */
+attn_status_t attn_encoder_decoder_fwd(
+    const attn_lstm_shape_t* s, const int32_t* src_ids, const int32_t* tgt_ids,
+    const int32_t* src_lens_host, const void* E_src, const void* E_tgt,
+    const void* const* enc_W, const float* const* enc_b, const void* const* dec_W,
+    const float* const* dec_b, void* H_enc, void* H_dec, void* workspace,
+    size_t workspace_bytes, void* stream);
+
+/* MP -> DP hand-over ("the intermediate results of all hidden
+ * states ... are distributed equally to 4 GPUs"): rank `root` holds `full`
+ * [B_global][rows][hidden] bf16 (H_enc with rows = M, or H_dec with rows =
+ * N); every rank receives its contiguous sentence shard (sizes differing by
+ * at most one, lower ranks first) into `shard` [B_r][rows][hidden], by NCCL
+ * point-to-point on `stream`.  `full` is read on the root only. */
+attn_status_t attn_hidden_scatter(attn_comm_t* c, int root, int B_global, int rows, int hidden,
+                                  const void* full, void* shard, void* stream);
+
 /* Thread-local message of the last failing call on this thread ("" if none). */
 const char* attn_last_error(void);
 

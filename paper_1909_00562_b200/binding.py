@@ -35,6 +35,8 @@ EXPORTS = [
     "attn_softmax_stage_time", "attn_softmax_last_launches",
     "attn_adam_step", "attn_adam_shard_len", "attn_adam_step_sharded",
     "attn_softmax_decode_workspace_size", "attn_softmax_decode_step",
+    "attn_lstm_workspace_size", "attn_lstm_packed_bytes", "attn_lstm_pack_layer",
+    "attn_encoder_decoder_fwd", "attn_hidden_scatter",
 ]
 
 
@@ -54,6 +56,13 @@ class AttnShape(ctypes.Structure):
 class AdamParams(ctypes.Structure):
     _fields_ = [("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
                 ("eps", ctypes.c_double), ("step", ctypes.c_int32)]
+
+
+class LstmShape(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("src_len", ctypes.c_int32),
+                ("tgt_len", ctypes.c_int32), ("emb", ctypes.c_int32),
+                ("hidden", ctypes.c_int32), ("layers", ctypes.c_int32),
+                ("vocab_src", ctypes.c_int32), ("vocab_tgt", ctypes.c_int32)]
 
 
 class AttnWsViews(ctypes.Structure):
@@ -146,6 +155,20 @@ def lib() -> ctypes.CDLL:
     L.attn_adam_shard_len.restype = ctypes.c_size_t
     L.attn_adam_step_sharded.argtypes = [_P, A, ctypes.c_size_t, _P, _P, _P, _P, _P, _P]
     L.attn_adam_step_sharded.restype = ctypes.c_int
+    LS = ctypes.POINTER(LstmShape)
+    L.attn_lstm_workspace_size.argtypes = [LS]
+    L.attn_lstm_workspace_size.restype = ctypes.c_size_t
+    L.attn_lstm_packed_bytes.argtypes = [ctypes.c_int, ctypes.c_int]
+    L.attn_lstm_packed_bytes.restype = ctypes.c_size_t
+    L.attn_lstm_pack_layer.argtypes = [ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _P, _P]
+    L.attn_lstm_pack_layer.restype = ctypes.c_int
+    L.attn_encoder_decoder_fwd.argtypes = [LS, _P, _P, i32p, _P, _P, ctypes.POINTER(_P),
+                                           ctypes.POINTER(_P), ctypes.POINTER(_P),
+                                           ctypes.POINTER(_P), _P, _P, _P, ctypes.c_size_t, _P]
+    L.attn_encoder_decoder_fwd.restype = ctypes.c_int
+    L.attn_hidden_scatter.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      _P, _P, _P]
+    L.attn_hidden_scatter.restype = ctypes.c_int
     _lib = L
     return L
 
@@ -359,3 +382,42 @@ def attn_softmax_decode_step(s, H_dec, H_enc, src_lens, W_c, W_out, k, topk_ids,
         ctypes.byref(s), _ptr(H_dec), _ptr(H_enc), src_p, _ptr(W_c), _ptr(W_out), _ptr(W_alpha),
         _ptr(b_out), int(k), _ptr(topk_ids), _ptr(topk_logp), _ptr(lse), _ptr(workspace),
         workspace.numel() * workspace.element_size(), _stream(stream)))
+
+
+# ---------------------------------------------------------------- NEXT-3
+def lstm_shape(B, M, N, emb, hidden, layers, vocab_src, vocab_tgt) -> LstmShape:
+    return LstmShape(B, M, N, emb, hidden, layers, vocab_src, vocab_tgt)
+
+
+def attn_lstm_workspace_size(s: LstmShape) -> int:
+    n = lib().attn_lstm_workspace_size(ctypes.byref(s))
+    if n == 0:
+        raise AttnError(7, lib().attn_last_error().decode())
+    return n
+
+
+def attn_lstm_packed_bytes(in_dim: int, hidden: int) -> int:
+    return int(lib().attn_lstm_packed_bytes(int(in_dim), int(hidden)))
+
+
+def attn_lstm_pack_layer(in_dim, hidden, W_ih, W_hh, b, W_packed, b_packed, stream=None):
+    _check(lib().attn_lstm_pack_layer(int(in_dim), int(hidden), _ptr(W_ih), _ptr(W_hh), _ptr(b),
+                                      _ptr(W_packed), _ptr(b_packed), _stream(stream)))
+
+
+def attn_encoder_decoder_fwd(s: LstmShape, src_ids, tgt_ids, src_lens, E_src, E_tgt, enc_W, enc_b,
+                             dec_W, dec_b, H_enc, H_dec, workspace, stream=None):
+    src, src_p = _i32(src_lens)
+
+    def arr(ts):
+        return (_P * len(ts))(*[t.data_ptr() for t in ts])
+    eW, eb, dW, db = arr(enc_W), arr(enc_b), arr(dec_W), arr(dec_b)
+    _check(lib().attn_encoder_decoder_fwd(
+        ctypes.byref(s), _ptr(src_ids), _ptr(tgt_ids), src_p, _ptr(E_src), _ptr(E_tgt), eW, eb,
+        dW, db, _ptr(H_enc), _ptr(H_dec), _ptr(workspace),
+        workspace.numel() * workspace.element_size(), _stream(stream)))
+
+
+def attn_hidden_scatter(comm, root, B_global, rows, hidden, full, shard, stream=None):
+    _check(lib().attn_hidden_scatter(comm, int(root), int(B_global), int(rows), int(hidden),
+                                     _ptr(full), _ptr(shard), _stream(stream)))

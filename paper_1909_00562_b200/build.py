@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "libattnsm.so")
-SOURCES = ["attn_softmax.cu", "comm.cu", "adam.cu"]
+SOURCES = ["attn_softmax.cu", "comm.cu", "adam.cu", "lstm.cu"]
 # every header of csrc/ (a stale .so after a header edit runs old code)
 HEADERS = sorted(os.path.basename(f) for f in glob.glob(os.path.join(CSRC, "*.cuh")) +
                  glob.glob(os.path.join(CSRC, "*.h")))

@@ -59,6 +59,10 @@ struct NcclApi {
   ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   bool ok = false;
   std::string why;
 };
@@ -89,6 +93,10 @@ static NcclApi& nccl() {
     api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
     api.CommAbort = (decltype(api.CommAbort))dlsym(h, "ncclCommAbort");
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+    api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
+    api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+    api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
     api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy &&
              api.ReduceScatter && api.AllGather;
     if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
@@ -306,3 +314,46 @@ attn_status_t comm_all_gather_bf16(attn_comm_t* c, void* buf, size_t shard, cuda
 
 // one rank: the "allreduce" moves nothing, so no SMs are set aside
 int comm_max_ctas(const attn_comm_t* c) { return c && c->nranks > 1 ? c->max_ctas : 0; }
+
+// NEXT-3: MP -> DP scatter of the hidden states (attn_softmax.h).  Shards are
+// contiguous sentence ranges, sizes differing by at most one, lower ranks
+// first (the same rule as synthetic.shard_range and the stage's partitioning).
+static void shard_of(int B, int R, int r, int* lo, int* n) {
+  const int base = B / R, extra = B % R;
+  *lo = r * base + (r < extra ? r : extra);
+  *n = base + (r < extra ? 1 : 0);
+}
+
+extern "C" attn_status_t attn_hidden_scatter(attn_comm_t* c, int root, int B_global, int rows,
+                                             int hidden, const void* full, void* shard, void* stream) {
+  if (!c) return err(ATTN_ERR_INVALID_ARG, "hidden_scatter: comm is NULL");
+  if (B_global < 0 || rows < 1 || hidden < 1 || root < 0 || root >= c->nranks)
+    return err(ATTN_ERR_SHAPE, "hidden_scatter: B_global %d, rows %d, hidden %d, root %d of %d ranks",
+               B_global, rows, hidden, root, c->nranks);
+  if (!shard || (c->rank == root && !full)) return err(ATTN_ERR_INVALID_ARG, "hidden_scatter: NULL buffer");
+  if (!nccl().Send || !nccl().Recv || !nccl().GroupStart || !nccl().GroupEnd)
+    return err(ATTN_ERR_NCCL, "hidden_scatter: libnccl lacks ncclSend / ncclRecv / ncclGroup*");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t row_bytes = (size_t)rows * hidden * 2;   // one sentence, bf16
+  int lo = 0, n = 0;
+  if (c->rank == root) {
+    NCCL_OK(nccl().GroupStart());
+    for (int r = 0; r < c->nranks; ++r) {
+      shard_of(B_global, c->nranks, r, &lo, &n);
+      if (r == root || n == 0) continue;
+      NCCL_OK(nccl().Send(static_cast<const char*>(full) + (size_t)lo * row_bytes, (size_t)n * row_bytes,
+                          0 /* ncclInt8: raw bytes */, r, c->comm, s));
+    }
+    NCCL_OK(nccl().GroupEnd());
+    shard_of(B_global, c->nranks, root, &lo, &n);
+    if (n > 0) {
+      cudaError_t e = cudaMemcpyAsync(shard, static_cast<const char*>(full) + (size_t)lo * row_bytes,
+                                      (size_t)n * row_bytes, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return err(ATTN_ERR_CUDA, "hidden_scatter: %s", cudaGetErrorString(e));
+    }
+  } else {
+    shard_of(B_global, c->nranks, c->rank, &lo, &n);
+    if (n > 0) NCCL_OK(nccl().Recv(shard, (size_t)n * row_bytes, 0, root, c->comm, s));
+  }
+  return ATTN_OK;
+}

@@ -117,3 +117,44 @@ def to_device(inp: dict, dtype: str, device="cuda"):
     out["src_len"] = inp["src_len"]
     out["tgt_len"] = inp["tgt_len"]
     return out
+
+
+class EncoderDecoder:
+    """NEXT-3: the stacked-LSTM encoder-decoder (no input feeding) that
+    produces H_enc / H_dec for the stage (attn_encoder_decoder_fwd).  Holds
+    the packed layer weights (attn_lstm_pack_layer) and the workspace."""
+
+    def __init__(self, B: int, M: int, N: int, emb: int, hidden: int, layers: int,
+                 vocab_src: int, vocab_tgt: int, device: Optional[torch.device] = None):
+        self.B, self.M, self.N, self.emb, self.hidden, self.layers = B, M, N, emb, hidden, layers
+        self.device = torch.device(device or "cuda")
+        self.shape = binding.lstm_shape(B, M, N, emb, hidden, layers, vocab_src, vocab_tgt)
+        self.workspace = torch.empty(binding.attn_lstm_workspace_size(self.shape),
+                                     dtype=torch.uint8, device=self.device)
+        self.enc_W = self.enc_b = self.dec_W = self.dec_b = None
+
+    def _pack(self, layers):
+        Ws, bs = [], []
+        for l, (W_ih, W_hh, b) in enumerate(layers):
+            fin = self.emb if l == 0 else self.hidden
+            Wp = torch.empty(4 * self.hidden, fin + self.hidden, dtype=torch.bfloat16, device=self.device)
+            bp = torch.empty(4 * self.hidden, dtype=torch.float32, device=self.device)
+            binding.attn_lstm_pack_layer(fin, self.hidden, W_ih, W_hh, b, Wp, bp)
+            Ws.append(Wp)
+            bs.append(bp)
+        return Ws, bs
+
+    def set_weights(self, enc_layers, dec_layers):
+        """enc_layers / dec_layers: [(W_ih, W_hh, b)] bf16 device tensors (PyTorch layout)."""
+        self.enc_W, self.enc_b = self._pack(enc_layers)
+        self.dec_W, self.dec_b = self._pack(dec_layers)
+
+    def __call__(self, src_ids, tgt_ids, src_len, E_src, E_tgt, H_enc=None, H_dec=None, stream=None):
+        if H_enc is None:
+            H_enc = torch.empty(self.B, self.M, self.hidden, dtype=torch.bfloat16, device=self.device)
+        if H_dec is None:
+            H_dec = torch.empty(self.B, self.N, self.hidden, dtype=torch.bfloat16, device=self.device)
+        binding.attn_encoder_decoder_fwd(self.shape, src_ids, tgt_ids, src_len, E_src, E_tgt,
+                                         self.enc_W, self.enc_b, self.dec_W, self.dec_b,
+                                         H_enc, H_dec, self.workspace, stream=stream)
+        return H_enc, H_dec

@@ -1,0 +1,96 @@
+"""NEXT-3 parity: the wavefront stacked-LSTM encoder-decoder kernels
+(attn_encoder_decoder_fwd, csrc/lstm.cu) against the fp64 oracle
+(oracle/lstm_oracle.py, pinned by tests/test_lstm_oracle_pins.py) on the same
+seeded bf16 inputs, and the MP -> DP hidden-state scatter.
+
+Tolerance: the kernels keep h in bf16 between steps (it is the next step's
+MMA operand) and accumulate in fp32, so the states carry bf16 rounding through
+every recurrence; rel-L2 <= 2e-2 per output (the bf16 gradient bar of
+north_star), also per sentence and per step band so an error confined to one
+layer-step or sentence cannot hide in the global norm."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import lstm_oracle as LO
+from synthetic import CONFIGS, make_lstm_inputs
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+
+
+def _rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _run(cfg, layers, emb):
+    from paper_1909_00562_b200.stage import EncoderDecoder
+    inp = make_lstm_inputs(cfg, layers=layers, emb=emb)
+    dev = torch.device("cuda")
+    bf = lambda a: torch.from_numpy(np.asarray(a, np.float32)).to(dev, torch.bfloat16)
+    ed = EncoderDecoder(cfg.B, cfg.M, cfg.N, emb, cfg.d, layers, cfg.V, cfg.V)
+    ed.set_weights([tuple(bf(w) for w in ws) for ws in inp["enc"]],
+                   [tuple(bf(w) for w in ws) for ws in inp["dec"]])
+    src = torch.from_numpy(inp["src_ids"]).to(dev)
+    tgt = torch.from_numpy(inp["tgt_ids"]).to(dev)
+    H_enc, H_dec = ed(src, tgt, inp["src_len"], bf(inp["E_src"]), bf(inp["E_tgt"]))
+    torch.cuda.synchronize()
+    S, H = LO.encoder_decoder(inp["src_ids"], inp["tgt_ids"], inp["src_len"], inp["E_src"],
+                              inp["E_tgt"], inp["enc"], inp["dec"])
+    return inp, H_enc.double().cpu().numpy(), H_dec.double().cpu().numpy(), S, H
+
+
+@pytest.mark.parametrize("name,layers,emb", [("small", 2, 128), ("medium", 4, 256), ("odd", 3, 64),
+                                             ("edge_min", 1, 64), ("edge_max_src", 2, 64)])
+def test_encoder_decoder_matches_oracle(cuda_lib, name, layers, emb):
+    cfg = CONFIGS[name]
+    if cfg.B > 128:
+        pytest.skip("B > 128")
+    inp, ge, gd, S, H = _run(cfg, layers, emb)
+    assert np.isfinite(ge).all() and np.isfinite(gd).all()
+    assert _rel(ge, S) <= TOL, ("H_enc", _rel(ge, S))
+    assert _rel(gd, H) <= TOL, ("H_dec", _rel(gd, H))
+    for b in range(cfg.B):
+        L = int(inp["src_len"][b])
+        assert _rel(ge[b, :L], S[b, :L]) <= TOL, ("H_enc sentence", b)
+        assert _rel(gd[b], H[b]) <= TOL, ("H_dec sentence", b)
+    for t0 in range(0, cfg.N, 16):   # step bands: the recurrence does not drift
+        assert _rel(gd[:, t0:t0 + 16], H[:, t0:t0 + 16]) <= TOL, ("H_dec steps", t0)
+
+
+def test_encoder_decoder_paper_shape(cuda_lib):
+    """Table 1 sizes (embedding 512, hidden 1024, 4 layers)
+    at the C1 batch (128 sentences, 50 / 50 steps): the launch configuration
+    bench.py times (4 layers x 32 CTAs)."""
+    cfg = CONFIGS["paper"]
+    inp, ge, gd, S, H = _run(cfg, 4, 512)
+    assert _rel(ge, S) <= TOL, _rel(ge, S)
+    assert _rel(gd, H) <= TOL, _rel(gd, H)
+    for b in (0, 63, 127):
+        assert _rel(gd[b], H[b]) <= TOL, b
+
+
+def test_hidden_scatter_single_rank(cuda_lib):
+    """MP -> DP hand-over on a 1-rank communicator: the shard is the whole batch."""
+    from paper_1909_00562_b200 import binding
+    full = torch.randn(5, 7, 64, device="cuda").to(torch.bfloat16)
+    shard = torch.empty_like(full)
+    uid = binding.attn_comm_get_unique_id()
+    comm = binding.attn_comm_init(uid, 1, 0, torch.cuda.current_device())
+    try:
+        binding.attn_hidden_scatter(comm, 0, 5, 7, 64, full, shard)
+        torch.cuda.synchronize()
+        assert torch.equal(shard, full)
+    finally:
+        binding.attn_comm_destroy(comm)
+
+
+def test_lstm_rejects_bad_shapes(cuda_lib):
+    from paper_1909_00562_b200 import binding
+    with pytest.raises(binding.AttnError):
+        binding.attn_lstm_workspace_size(binding.lstm_shape(129, 5, 5, 64, 64, 1, 10, 10))
+    with pytest.raises(binding.AttnError):
+        binding.attn_lstm_workspace_size(binding.lstm_shape(4, 5, 5, 48, 64, 1, 10, 10))
