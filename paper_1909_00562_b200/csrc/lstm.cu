@@ -18,9 +18,9 @@
 //   release / acquire at gpu scope), streams [x_t | h_{t-1}] (128 batch rows,
 //   TMA from the sequences written by the neighbours) and its W rows through
 //   a TMA ring into one 128 x 4U tcgen05 MMA (fp32 in TMEM, two accumulators
-//   so step t+1's input part overlaps step t's cell update), and the 4 epilogue
-//   warps -- one thread per batch row -- apply the LSTM cell to the
-//   accumulator row (c in fp32 global state, h written bf16 into the layer's
+//   so step t+1's input part overlaps step t's cell update), and the 8 epilogue
+//   warps -- one thread per batch row and half of the CTA's units -- apply the
+//   LSTM cell to the accumulator row (c in fp32 global state, h written bf16 into the layer's
 //   [B][T][hd] output, which is the next layer's input and, for the top
 //   layer, H_enc / H_dec itself).
 //
@@ -47,7 +47,7 @@ attn_status_t attn_set_error(attn_status_t code, const char* msg);
 
 namespace attnsm {
 
-constexpr int LS_THREADS = 192;   // warps 0-3 cell epilogue, warp 4 TMA producer + TMEM, warp 5 MMA
+constexpr int LS_THREADS = 320;   // warps 0-7 cell epilogue, warp 8 TMA producer + TMEM, warp 9 MMA
 constexpr int LS_RING = 192 * 1024;
 constexpr int LS_MAXST = 8;
 constexpr int LS_SMEM = LS_RING + 1024 + 512;
@@ -75,7 +75,14 @@ struct alignas(64) LsParams {
   unsigned* done;           // [L][T]: CTAs of (l, t) that published h_t
 };
 
-__device__ __forceinline__ float ls_sigmoid(float x) { return 1.f / (1.f + expf(-x)); }
+// tanh.approx.f32 (one MUFU op, ~2^-11 relative error, below the bf16
+// rounding of h); sigma(x) = (1 + tanh(x / 2)) / 2
+__device__ __forceinline__ float ls_tanh(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ls_sigmoid(float x) { return fmaf(0.5f, ls_tanh(0.5f * x), 0.5f); }
 
 __device__ __forceinline__ void ls_wait_geq(const unsigned* p, unsigned target) {
   if (ld_acquire_gpu(p) >= target) return;
@@ -103,7 +110,7 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_wavefront_kernel(const __g
   const int nst = min(LS_MAXST, (int)(LS_RING / stage));
   const uint32_t tcols = P.ntile <= 16 ? 32 : (P.ntile <= 64 ? 128 : (P.ntile <= 128 ? 256 : 512));
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {
       for (int i = 0; i < LS_MAXST; ++i) {
         mbar_init(&full[i], 1);
@@ -111,7 +118,7 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_wavefront_kernel(const __g
       }
       for (int i = 0; i < 2; ++i) {
         mbar_init(&tfull[i], 1);
-        mbar_init(&tempty[i], 4);
+        mbar_init(&tempty[i], 8);
       }
       fence_barrier_init();
       tma_prefetch_desc(&Ly.m_x);
@@ -126,33 +133,39 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_wavefront_kernel(const __g
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ---------------- TMA producer: the step's [x_t | h_{t-1}] and W k-blocks
     int s = 0;
     uint32_t ph = 0;
+    // Per step the input part (x_t, ready once layer l-1 has published step t,
+    // usually long before) goes first and the recurrent part (h_{t-1}) last,
+    // and each stage's W block is requested before waiting for the flag its A
+    // block needs: only the h_{t-1} loads sit on the recurrence's critical path.
     for (int t = 0; t < P.T; ++t) {
-      if (lane == 0) {
-        if (l > 0) ls_wait_geq(P.done + (size_t)(l - 1) * P.T + t, (unsigned)P.G);
-        if (t > 0) ls_wait_geq(P.done + (size_t)l * P.T + t - 1, (unsigned)P.G);
-      }
-      __syncwarp();
-      fence_proxy_async_global();
       const int nk = kin + ((t > 0 || P.has_init) ? khd : 0);
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&empty[s], ph ^ 1);
-        if (elect_one()) {
+        if (lane == 0) {
           uint8_t* sa = ring + s * stage;
           mbar_arrive_expect_tx(&full[s], stage);
+          tma_load_2d(sa + 16384, &Ly.m_w, &full[s], kb * 64, g * P.ntile);
+          if (kb == 0 && l > 0) {
+            ls_wait_geq(P.done + (size_t)(l - 1) * P.T + t, (unsigned)P.G);
+            fence_proxy_async_global();
+          }
+          if (kb == kin && t > 0) {
+            ls_wait_geq(P.done + (size_t)l * P.T + t - 1, (unsigned)P.G);
+            fence_proxy_async_global();
+          }
           if (kb < kin) tma_load_3d(sa, &Ly.m_x, &full[s], kb * 64, t, 0);
           else if (t > 0) tma_load_3d(sa, &Ly.m_h, &full[s], (kb - kin) * 64, t - 1, 0);
           else tma_load_2d(sa, &Ly.m_h0, &full[s], (kb - kin) * 64, 0);
-          tma_load_2d(sa + 16384, &Ly.m_w, &full[s], kb * 64, g * P.ntile);
         }
         __syncwarp();
         if (++s == nst) { s = 0; ph ^= 1; }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ---------------- MMA issuer: gates[128 rows, 4U] = [x_t | h_{t-1}] W_slice^T
     int s = 0;
     uint32_t ph = 0;
@@ -180,48 +193,57 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_wavefront_kernel(const __g
       __syncwarp();
     }
   } else {
-    // ---------------- LSTM cell (warps 0-3): thread = batch row r
-    const int r = (int)(warp * 32 + lane);
+    // ---------------- LSTM cell (warps 0-7): warp w takes batch rows 32 (w % 4)..
+    // (its TMEM lane quarter) and half w / 4 of the CTA's units; thread = row
+    const uint32_t q = warp & 3, hh = warp >> 2;
+    const int r = (int)(q * 32 + lane);
     const bool row_ok = r < P.B;
     const int U = P.ntile / 4;
-    const int u_base = g * U;
+    const int nc = P.ntile / 64;              // 32-column chunks (8 units) per warp
+    const int u_base = g * U + (int)hh * (U / 2);
     const int cap = (P.cap && row_ok) ? P.cap[r] : -1;
-    const uint32_t tq = tmem_base + ((warp * 32u) << 16);
+    const uint32_t tq = tmem_base + ((q * 32u) << 16) + hh * (P.ntile / 2);
+    const size_t crow = (size_t)(row_ok ? r : 0) * P.hd;
     for (int t = 0; t < P.T; ++t) {
       const int acc = t & 1, use = t >> 1;
+      // c_{t-1} of this row's units, read before the accumulator wait
+      float cp[2][8];
+      for (int cc = 0; cc < nc; ++cc) {
+        const int u0 = u_base + cc * 8;
+        if (t > 0 || Ly.c0) {
+          const float4* src = reinterpret_cast<const float4*>((t > 0 ? Ly.c : Ly.c0) + crow + u0);
+          const float4 a = src[0], b = src[1];
+          cp[cc][0] = a.x; cp[cc][1] = a.y; cp[cc][2] = a.z; cp[cc][3] = a.w;
+          cp[cc][4] = b.x; cp[cc][5] = b.y; cp[cc][6] = b.z; cp[cc][7] = b.w;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) cp[cc][k] = 0.f;
+        }
+      }
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
-      for (int cc = 0; cc < P.ntile / 32; ++cc) {   // 8 units per 32 accumulator columns
+      for (int cc = 0; cc < nc; ++cc) {   // 8 units per 32 accumulator columns
         float v[32];
         tmem_ld32(tq + acc * P.ntile + cc * 32, v);
         const int u0 = u_base + cc * 8;
         const float4* b4 = reinterpret_cast<const float4*>(Ly.bias + 4 * u0);
-        float cp[8];
-        if (t > 0 || Ly.c0) {
-          const float* src = (t > 0 ? Ly.c : Ly.c0) + (size_t)(row_ok ? r : 0) * P.hd + u0;
-          const float4 a = reinterpret_cast<const float4*>(src)[0];
-          const float4 b = reinterpret_cast<const float4*>(src)[1];
-          cp[0] = a.x; cp[1] = a.y; cp[2] = a.z; cp[3] = a.w;
-          cp[4] = b.x; cp[5] = b.y; cp[6] = b.z; cp[7] = b.w;
-        } else {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) cp[k] = 0.f;
-        }
         float hc[8], cn[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const float4 bb = __ldg(b4 + k);
           const float gi = ls_sigmoid(v[4 * k] + bb.x);
           const float gf = ls_sigmoid(v[4 * k + 1] + bb.y);
-          const float gg = tanhf(v[4 * k + 2] + bb.z);
+          const float gg = ls_tanh(v[4 * k + 2] + bb.z);
           const float go = ls_sigmoid(v[4 * k + 3] + bb.w);
-          cn[k] = gf * cp[k] + gi * gg;
-          hc[k] = go * tanhf(cn[k]);
+          cn[k] = fmaf(gf, cp[cc][k], gi * gg);
+          hc[k] = go * ls_tanh(cn[k]);
         }
         if (row_ok) {
           float4* cdst = reinterpret_cast<float4*>(Ly.c + (size_t)r * P.hd + u0);
-          cdst[0] = make_float4(cn[0], cn[1], cn[2], cn[3]);
-          cdst[1] = make_float4(cn[4], cn[5], cn[6], cn[7]);
+          const float4 c_lo = make_float4(cn[0], cn[1], cn[2], cn[3]);
+          const float4 c_hi = make_float4(cn[4], cn[5], cn[6], cn[7]);
+          cdst[0] = c_lo;
+          cdst[1] = c_hi;
           uint32_t w[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -233,8 +255,8 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_wavefront_kernel(const __g
           if (t == cap) {
             *reinterpret_cast<uint4*>(Ly.h_cap + (size_t)r * P.hd + u0) = hv;
             float4* cc4 = reinterpret_cast<float4*>(Ly.c_cap + (size_t)r * P.hd + u0);
-            cc4[0] = cdst[0];
-            cc4[1] = cdst[1];
+            cc4[0] = c_lo;
+            cc4[1] = c_hi;
           }
         }
       }
@@ -242,7 +264,7 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_wavefront_kernel(const __g
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
       // publish (l, t): every epilogue thread's h / c stores, then one release
-      named_bar_sync(1, 128);
+      named_bar_sync(1, 256);
       if (threadIdx.x == 0) {
         __threadfence();
         red_release_gpu_add(P.done + (size_t)l * P.T + t, 1u);
@@ -252,7 +274,7 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_wavefront_kernel(const __g
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 4) tmem_dealloc(tmem_base, tcols);
+  if (warp == 8) tmem_dealloc(tmem_base, tcols);
 }
 
 // layer packing: packed row 4u + q = [W_ih[q hd + u] | W_hh[q hd + u]], b likewise (fp32)

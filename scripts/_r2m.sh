@@ -1,2 +1,3 @@
 python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -3
-timeout 600 python -m pytest tests/test_gpu_lstm.py -x -q 2>&1 | tail -25
+timeout 600 python -m pytest tests/test_gpu_lstm.py -x -q 2>&1 | tail -2
+timeout 300 python scripts/lstm_time.py paper
