@@ -317,6 +317,34 @@ def measure_next_rows(binding, st, dv, cfg, scale, comm, stream, dev, pk, tok_lo
         res["decode_step"] = {"beam": 5, "k": 5, "hypotheses": rows, "us_per_step": ms * 1e3,
                               "hypothesis_steps_per_s": rows / (ms / 1e3),
                               "vocab_tflops": 2.0 * rows * cfg.d * cfg.V / (ms / 1e3) / 1e12}
+    # NEXT-3: the encoder-decoder forward that produces H_enc / H_dec (Table 1
+    # sizes: embedding 512, 4 layers, the config's hidden size and batch;
+    # wavefront kernel, one per side), when the shape fits it (B <= 128)
+    if cfg.dtype == "bf16" and cfg.B <= 128 and cfg.d % 64 == 0:
+        from paper_1909_00562_b200.stage import EncoderDecoder
+        from synthetic import make_lstm_inputs
+        L_, e_ = 4, 512
+        li = make_lstm_inputs(cfg, layers=L_, emb=e_)
+        bfd = lambda a: torch.from_numpy(np.asarray(a, np.float32)).to(device=dev, dtype=torch.bfloat16)
+        ed = EncoderDecoder(cfg.B, cfg.M, cfg.N, e_, cfg.d, L_, cfg.V, cfg.V, device=dev)
+        ed.set_weights([tuple(bfd(w) for w in ws) for ws in li["enc"]],
+                       [tuple(bfd(w) for w in ws) for ws in li["dec"]])
+        s_ids = torch.from_numpy(li["src_ids"]).to(dev)
+        t_ids = torch.from_numpy(li["tgt_ids"]).to(dev)
+        Es, Et = bfd(li["E_src"]), bfd(li["E_tgt"])
+        He = torch.empty(cfg.B, cfg.M, cfg.d, dtype=torch.bfloat16, device=dev)
+        Hd = torch.empty(cfg.B, cfg.N, cfg.d, dtype=torch.bfloat16, device=dev)
+        ms = timed(lambda: ed(s_ids, t_ids, li["src_len"], Es, Et, He, Hd, stream=stream))
+        fl = sum(2.0 * cfg.B * T * 4 * cfg.d * ((e_ if l == 0 else cfg.d) + cfg.d)
+                 for T in (cfg.M, cfg.N) for l in range(L_))
+        res["encoder_decoder"] = {
+            "layers": L_, "emb": e_, "hidden": cfg.d, "ms": ms,
+            "source_plus_target_tokens_per_s": cfg.B * (cfg.M + cfg.N) / (ms / 1e3),
+            "tflops": fl / (ms / 1e3) / 1e12,
+            "us_per_wavefront_step": ms * 1e3 / (cfg.M + cfg.N + 2 * (L_ - 1)),
+            "note": "forward only; one persistent cooperative kernel per side, SM groups in the "
+                    "role of the paper's per-layer GPUs"}
+        del ed
     # NEXT-2: Adam over W_out, W_c (and W_alpha, b_out would add d^2 + V)
     n = cfg.V * cfg.d + 2 * cfg.d * cfg.d
     h = binding.adam_params(1)

@@ -31,28 +31,37 @@ for row in r[1:]:
 starts = [i for i, (k, _) in enumerate(launches) if k.startswith("lens_kernel")]
 a, b = starts[0], (starts[1] if len(starts) > 1 else len(launches))
 step = launches[a:b]
-names = {0: "lengths upload (kernel parameters)", 1: "F1 attn scores + masked softmax",
-         2: "F2 attn context", 3: "F3 proj_tanh (Eq. 4)"}
-tail = ["B2 proj_bwd (dW_c + dH_part + dC)", "B3 attn bwd dA + softmax bwd",
-        "B3 attn bwd dH_dec + dH_enc"]
+tot = sum(t for _, t in step)
 out = [f"# ncu launch list: one C1 step (launches {a}..{b - 1} of the capture) {note}",
        "# ncu --metrics gpu__time_duration.sum --clock-control none; serialised, cold-cache: compare SHARES",
        "id,step,kernel,time_us,share_pct"]
-tot = sum(t for _, t in step)
+
+
+def step_name(i, k, prev):
+    if k.startswith("lens_kernel"):
+        return "lengths upload (kernel parameters)"
+    if k.startswith("attn_fwd_kernel"):
+        return "F1+F2 fused attention fwd (scores, masked softmax, context)"
+    if k.startswith("attn_bwd_kernel"):
+        return "B3 fused attention bwd (dalpha, softmax bwd, dQ, dH_enc)"
+    if k.startswith("lse_reduce"):
+        return "F5 lse_reduce (lse, NLL, loss)"
+    if k.startswith("vocab_kernel"):
+        return "B1 vocab backward, persistent (recompute per V-chunk, dL in L2 scratch, dHc, dW_out)"
+    if k.startswith("dz_kernel"):
+        return "B1' dz = dHc (1 - H_c^2) (+ zero dW_c)"
+    if k.startswith("gemm_tc"):
+        return {"attn_fwd_kernel": "F3 proj_tanh (Eq. 4)",
+                "gemm_tc_kernel": "F4 vocab_fwd (LSE epilogue, no logits stored)",
+                "dz_kernel": "B2a {dC = dz W_c[:, d:], dW_c split-K}",
+                "attn_bwd_kernel": "B2b dH_dec = dz W_c[:, :d] + dQ"}.get(prev, k)
+    return k
+
+
+prev = ""
 for i, (k, t) in enumerate(step):
-    if i in names and not k.startswith("vocab"):
-        nm = names[i]
-    elif k.startswith("gemm_tc") and i == 4:
-        nm = "F4 vocab_fwd (LSE epilogue, no logits stored)"
-    elif k.startswith("lse_reduce"):
-        nm = "F5 lse_reduce (lse, NLL, loss)"
-    elif k.startswith("vocab_kernel"):
-        nm = "B1 vocab backward, persistent (recompute per V-chunk, dL in L2 scratch, dHc, dW_out)"
-    elif k.startswith("dz_kernel"):
-        nm = "B1' dz = dHc (1 - H_c^2)"
-    else:
-        j = i - (len(step) - len(tail))
-        nm = tail[j] if 0 <= j < len(tail) else k
+    nm = step_name(i, k, prev)
+    prev = k.split("<")[0]
     out.append(f"{i},{nm},{k.replace(',', ' ')},{t / 1e3:.1f},{100 * t / tot:.1f}")
 out.append(f"# total {tot / 1e3:.1f} us")
 open(f"{prefix}_launches_paper.csv", "w").write("\n".join(out) + "\n")
