@@ -2,15 +2,17 @@
 // host planner (validation, workspace carving, TMA descriptors, V-chunk
 // schedule, streams / events) and the kernel launches of the stage.
 //
-// Stage order:
-//   F1-F2  attention scores, masked softmax, context       Eqs. 1-3
-//   F3     proj_tanh  H_c = tanh([H|C] W_c^T)              Eq. 4
-//   F4     vocab_fwd  per-tile (max, sumexp) + target logit, then lse_reduce
-//                                                           Eqs. 5-6
-//   B1     for each V-chunk c: dlogits_c (recomputed logits), dW_out[c],
-//          dHc += dL_c W_out[c] (last chunk: dz = dHc (1 - H_c^2))
-//   B2     dW_c = dz^T [H|C];  [dH_part | dC] = dz W_c
-//   B3     attention backward -> dH_dec, dH_enc
+// Stage order (bf16 path, default options):
+//   F1-F2  attention scores, masked softmax, context       Eqs. 1-3   attn_fwd_kernel
+//   F3     proj_tanh  H_c = tanh([H|C] W_c^T)              Eq. 4      gemm_tc
+//   F4     vocab_fwd  per-tile (max, sumexp) + target logit (logits not stored),
+//          then lse_reduce                                 Eqs. 5-6   gemm_tc, lse_reduce_kernel
+//   B1     one persistent launch: per V-chunk c the logits recomputed into
+//          dL_c (L2 scratch), dHc += dL_c W_out[c], dW_out[c] = dL_c^T H_c   vocab_kernel
+//   B1'    dz = dHc (1 - H_c^2)                                          dz_kernel
+//   B2a    dC = dz W_c[:, d:], dW_c = dz^T [H|C] (split-K)               gemm_tc
+//   B3     attention backward -> dQ, dH_enc                              attn_bwd_kernel
+//   B2b    dH_dec = dz W_c[:, :d] + dQ                                   gemm_tc
 //   X      dW_out chunks, dW_c, loss allreduced (comm != NULL)
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -119,11 +121,11 @@ static int g_opt_wide = PAIR_VBWD;
 // kernels after each launch, 2 the dlogits kernels (default -1 = 2)
 static int g_opt_db_gemm = -1;
 constexpr int kEwParts = 320;   // row-group partial rows of the dlogits kernels' column sums
-// "store_logits": the bf16 path's forward vocab GEMM also stores the logits as
-// fp16 [T, V]; the backward turns each V-chunk into dlogits with an
-// elementwise kernel instead of recomputing H_c W_out^T on the tensor cores.
-// 1 (default): chunk c+1's kernel starts beside launch c (PDL, waits at its
-// end); 2: serialised; 0: recompute (same-box A/B at C1: 1.92 / 1.98 / 2.15 ms)
+// "store_logits" (ABLATION, not the product path -- north_star forbids
+// round-tripping the logits through HBM): the forward vocab GEMM also stores
+// the logits as fp16 [T, V] and the backward turns each V-chunk into dL with
+// an elementwise kernel; 1: chunk c+1's kernel beside launch c, 2: serialised.
+// 0 (default): the persistent vocab kernel recomputes the logits per chunk.
 static int g_opt_store_logits = 0;
 // "dl_budget_mb": bytes of the dL chunk scratch (all NB buffers) the V-chunk
 // width is sized to, so it stays L2-resident; "dl_buffers": NB
