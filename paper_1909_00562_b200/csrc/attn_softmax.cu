@@ -164,6 +164,10 @@ static int g_opt_pdl = 1;
 // sentence (attn_tc.cuh; N, M <= 128, d % 64 == 0), else the generic engine's
 // batched score / context GEMMs
 static int g_opt_attn_fused = 1;
+// "proj_bn": tile width of the Eq. 4 projection GEMM (K-major W_c allows
+// 16..256).  128 (400 tiles at C1, 2.7 waves on 148 SMs instead of 1.35) was
+// measured slower: 43.6 vs 36.0 us (same box)
+static int g_opt_proj_bn = 256;
 // "attn_trace": device buffer of globaltimer stamps, [2][B][16] int64 (forward,
 // backward) + [B][64][4] backward chunk stamps (scripts/attn_trace.py)
 static long long* g_attn_trace = nullptr;
@@ -274,6 +278,11 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "attn_trace")) {
     g_attn_trace = reinterpret_cast<long long*>(value);
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "proj_bn")) {
+    if (value < 16 || value > 256 || value % 16) return fail(ATTN_ERR_INVALID_ARG, "proj_bn must be a multiple of 16 in [16, 256]");
+    g_opt_proj_bn = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "attn_fused")) {
@@ -1040,6 +1049,7 @@ static GemmDesc g_proj(const Plan& p, const void* H, const void* ctx, const void
   g.a1 = kmaj(ctx, p.T, d, d);
   g.kseg = (d + TC_BK - 1) / TC_BK;
   g.b0 = kmaj(W_c, d, 2 * d, 2 * d);
+  g.bn = p.bf16 ? g_opt_proj_bn : 0;
   g.epi.kind = EPI_TANH; g.epi.out = hc; g.epi.ldo = d; g.epi.ncols_valid = d; g.epi.ncols_store = d;
   return g;
 }

@@ -597,6 +597,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_bwd_kernel(const __grid_co
       if (lane == 0) mbar_arrive(pfull);
       if (warp == 0) AT_TRACE(4);
     }
+    // the staging area held the alpha rows until here: every epilogue warp
+    // passes this barrier before writing its staging half (the tfull chain
+    // already orders it; the barrier makes the order explicit)
+    named_bar_sync(2, 256);
     int sb = 0;
     for (int j = 0; j < nkb; ++j) {
       const int slot = j % AT_SLOTS, use = j / AT_SLOTS;

@@ -1,8 +1,10 @@
 """One fwd+bwd of the stage per case, for compute-sanitizer (memcheck /
 racecheck / synccheck): tiny (fp32 SIMT path), small and odd (bf16 tcgen05
 path: persistent vocab launch on CTA pairs and on single CTAs, and with the
-forward fused), edge_min; then the decoding step and Adam.  Exits non-zero
-on a library error."""
+forward fused; small / edge_min through the fused attention kernels, odd
+through the generic batched attention), edge_min; then the decoding step,
+Adam and the NEXT-3 encoder-decoder wavefront.  Exits non-zero on a library
+error."""
 import os
 import sys
 
@@ -46,3 +48,17 @@ if not only:
     binding.attn_adam_step(binding.adam_params(1), w, m, v, g, torch.empty(n, dtype=torch.bfloat16, device="cuda"))
     torch.cuda.synchronize()
     print("adam ok", flush=True)
+
+if not only or "lstm" in only:
+    import numpy as np
+    from paper_1909_00562_b200.stage import EncoderDecoder
+    from synthetic import make_lstm_inputs
+    cfg = CONFIGS["small"]
+    li = make_lstm_inputs(cfg, layers=2, emb=128)
+    bf = lambda a: torch.from_numpy(np.asarray(a, np.float32)).cuda().to(torch.bfloat16)
+    ed = EncoderDecoder(cfg.B, cfg.M, cfg.N, 128, cfg.d, 2, cfg.V, cfg.V)
+    ed.set_weights([tuple(bf(w) for w in ws) for ws in li["enc"]], [tuple(bf(w) for w in ws) for ws in li["dec"]])
+    He, Hd = ed(torch.from_numpy(li["src_ids"]).cuda(), torch.from_numpy(li["tgt_ids"]).cuda(), li["src_len"],
+                bf(li["E_src"]), bf(li["E_tgt"]))
+    torch.cuda.synchronize()
+    print("lstm ok", float(Hd.float().abs().mean()), flush=True)
