@@ -345,6 +345,23 @@ def measure_next_rows(binding, st, dv, cfg, scale, comm, stream, dev, pk, tok_lo
             "note": "forward only; one persistent cooperative kernel per side, SM groups in the "
                     "role of the paper's per-layer GPUs"}
         del ed
+        # HybridNMTIF: the same with input feeding -- the decoder
+        # steps run one after another (per step a wavefront over the layers, then
+        # the fused attention step), the paper's reason to remove it
+        li = make_lstm_inputs(cfg, layers=L_, emb=e_, input_feeding=True)
+        ed = EncoderDecoder(cfg.B, cfg.M, cfg.N, e_, cfg.d, L_, cfg.V, cfg.V, device=dev,
+                            input_feeding=True)
+        ed.set_weights([tuple(bfd(w) for w in ws) for ws in li["enc"]],
+                       [tuple(bfd(w) for w in ws) for ws in li["dec"]])
+        Wc_if = bfd(li["W_c"])
+        Ht = torch.empty(cfg.B, cfg.N, cfg.d, dtype=torch.bfloat16, device=dev)
+        ms_if = timed(lambda: ed(s_ids, t_ids, li["src_len"], Es, Et, He, Hd, stream=stream,
+                                 W_c=Wc_if, Htilde=Ht))
+        res["encoder_decoder_input_feeding"] = {
+            "ms": ms_if, "vs_no_input_feeding": ms_if / ms,
+            "source_plus_target_tokens_per_s": cfg.B * (cfg.M + cfg.N) / (ms_if / 1e3),
+            "note": "HybridNMTIF forward: decoder step t waits for Htilde_{t-1} (attention + Eq. 4)"}
+        del ed
     # NEXT-2: Adam over W_out, W_c (and W_alpha, b_out would add d^2 + V)
     n = cfg.V * cfg.d + 2 * cfg.d * cfg.d
     h = binding.adam_params(1)

@@ -329,6 +329,23 @@ attn_status_t attn_encoder_decoder_fwd(
     const float* const* dec_b, void* H_enc, void* H_dec, void* workspace,
     size_t workspace_bytes, void* stream);
 
+/* HybridNMTIF (the baseline model's input feeding, PAPER.md:75,
+ * :99): the same encoder, and a decoder whose layer-0 input at step t is
+ * [E_tgt[y_t] ; Htilde_{t-1}] (Htilde_{-1} = 0), where Htilde_t =
+ * tanh(W_c [h_t ; C_t]) is Eq. 4 of the stage on the top-layer state h_t and
+ * the attention context C_t over H_enc (Eqs. 1-3, dot score, src_len mask).
+ * The steps therefore run one after another (one wavefront launch over the
+ * layers per step, then the fused attention step).  dec_W[0] is packed with
+ * in = emb + hidden.  Outputs H_enc [B][M][h], H_dec [B][N][h] and Htilde
+ * [B][N][h] (bf16).  W_c [h][2h] bf16 as in attn_softmax_fwd_bwd.  M <= 128. */
+size_t attn_lstm_if_workspace_size(const attn_lstm_shape_t* s);
+attn_status_t attn_encoder_decoder_if_fwd(
+    const attn_lstm_shape_t* s, const int32_t* src_ids, const int32_t* tgt_ids,
+    const int32_t* src_lens_host, const void* E_src, const void* E_tgt,
+    const void* const* enc_W, const float* const* enc_b, const void* const* dec_W,
+    const float* const* dec_b, const void* W_c, void* H_enc, void* H_dec, void* Htilde,
+    void* workspace, size_t workspace_bytes, void* stream);
+
 /* MP -> DP hand-over ("the intermediate results of all hidden
  * states ... are distributed equally to 4 GPUs"): rank `root` holds `full`
  * [B_global][rows][hidden] bf16 (H_enc with rows = M, or H_dec with rows =

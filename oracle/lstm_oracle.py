@@ -23,7 +23,11 @@ the sizes: embedding 512, hidden 1024, 4 stacked LSTM layers):
   the last REAL source position src_len[b] - 1, and the recurrences run over
   the padded lengths -- states past a sentence's end are computed but never
   read by the attention, whose mask excludes them);
-* embeddings: x_t = E[y_t] (source and target tables).
+* embeddings: x_t = E[y_t] (source and target tables);
+* HybridNMTIF, encoder_decoder_if: the same model WITH the
+  baseline's input feeding: the decoder's layer-0 input at
+  step t is [E[y_t]; Htilde_{t-1}], Htilde_t = tanh(W_c [h_t; C_t]) from the
+  attention over S at step t (Eqs. 1-4), Htilde_{-1} = 0.
 
 Storage (row-major): ids [B, T] int; E [V, e]; W_ih[l] [4h, in_l] (in_0 = e,
 else h); W_hh[l] [4h, h]; b[l] [4h]; outputs H [B, T, h] (the top layer, all
@@ -31,13 +35,16 @@ steps) and the per-layer final states.
 
 Pinned by tests/test_lstm_oracle_pins.py: equality with torch.nn.LSTM in
 float64 (an independent implementation of the same cell), the zero-weight and
-bias-only closed forms, and the decoder-initialisation rule.
+bias-only closed forms, the decoder-initialisation rule; the input-feeding
+decoder against torch.nn.LSTMCell + scaled_dot_product_attention in float64,
+and reducing to the plain decoder when the feeding columns are zero.
 """
 from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["sigmoid", "lstm_cell", "lstm_stack", "encoder_decoder"]
+__all__ = ["sigmoid", "lstm_cell", "lstm_stack", "encoder_decoder", "attention_step",
+           "encoder_decoder_if"]
 
 
 def sigmoid(x):
@@ -103,3 +110,50 @@ def encoder_decoder(src_ids, tgt_ids, src_len, E_src, E_tgt, enc_weights, dec_we
     S, _, h_fin, c_fin = lstm_stack(Xs, enc_weights, capture_at=np.asarray(src_len) - 1)
     H, _, _, _ = lstm_stack(Xt, dec_weights, h0=h_fin, c0=c_fin)
     return S, H
+
+
+def attention_step(h, S, src_len, W_c):
+    """Eqs. 1-4 for one decoder step of every sentence (dot
+    score): e_j = h . S_j over j < src_len, alpha = softmax, C = sum_j alpha_j S_j,
+    Htilde = tanh(W_c [h; C]) (W_c [d, 2d], columns [0, d) multiply h)."""
+    h = np.asarray(h, np.float64)
+    S = np.asarray(S, np.float64)
+    W_c = np.asarray(W_c, np.float64)
+    B, M, d = S.shape
+    out = np.zeros((B, d))
+    for b in range(B):
+        L = int(src_len[b])
+        e = S[b, :L] @ h[b]
+        a = np.exp(e - e.max())
+        a /= a.sum()
+        C = a @ S[b, :L]
+        out[b] = np.tanh(W_c[:, :d] @ h[b] + W_c[:, d:] @ C)
+    return out
+
+
+def encoder_decoder_if(src_ids, tgt_ids, src_len, E_src, E_tgt, enc_weights, dec_weights, W_c):
+    """HybridNMTIF: the encoder of encoder_decoder, and a decoder
+    with input feeding -- layer 0's input at step t is
+    [E_tgt[y_t]; Htilde_{t-1}] (Htilde_{-1} = 0), Htilde_t = attention_step of
+    the top-layer state.  Returns (S [B, M, hd], H [B, N, hd], Htilde [B, N, hd])."""
+    E_src = np.asarray(E_src, np.float64)
+    E_tgt = np.asarray(E_tgt, np.float64)
+    Xs = E_src[np.asarray(src_ids)]
+    S, _, h_fin, c_fin = lstm_stack(Xs, enc_weights, capture_at=np.asarray(src_len) - 1)
+    B, N = np.asarray(tgt_ids).shape
+    hd = S.shape[2]
+    L = len(dec_weights)
+    h = [h_fin[l].copy() for l in range(L)]
+    c = [c_fin[l].copy() for l in range(L)]
+    H = np.zeros((B, N, hd))
+    Ht = np.zeros((B, N, hd))
+    feed = np.zeros((B, hd))
+    for t in range(N):
+        x = np.concatenate([E_tgt[np.asarray(tgt_ids)[:, t]], feed], axis=1)
+        for l, (W_ih, W_hh, b) in enumerate(dec_weights):
+            h[l], c[l] = lstm_cell(x, h[l], c[l], W_ih, W_hh, b)
+            x = h[l]
+        H[:, t] = h[L - 1]
+        feed = attention_step(h[L - 1], S, src_len, W_c)
+        Ht[:, t] = feed
+    return S, H, Ht

@@ -36,7 +36,8 @@ EXPORTS = [
     "attn_adam_step", "attn_adam_shard_len", "attn_adam_step_sharded",
     "attn_softmax_decode_workspace_size", "attn_softmax_decode_step",
     "attn_lstm_workspace_size", "attn_lstm_packed_bytes", "attn_lstm_pack_layer",
-    "attn_encoder_decoder_fwd", "attn_hidden_scatter",
+    "attn_encoder_decoder_fwd", "attn_hidden_scatter", "attn_lstm_if_workspace_size",
+    "attn_encoder_decoder_if_fwd",
 ]
 
 
@@ -168,6 +169,13 @@ def lib() -> ctypes.CDLL:
     L.attn_encoder_decoder_fwd.restype = ctypes.c_int
     L.attn_hidden_scatter.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                       _P, _P, _P]
+    L.attn_lstm_if_workspace_size.argtypes = [LS]
+    L.attn_lstm_if_workspace_size.restype = ctypes.c_size_t
+    L.attn_encoder_decoder_if_fwd.argtypes = [LS, _P, _P, i32p, _P, _P, ctypes.POINTER(_P),
+                                              ctypes.POINTER(_P), ctypes.POINTER(_P),
+                                              ctypes.POINTER(_P), _P, _P, _P, _P, _P,
+                                              ctypes.c_size_t, _P]
+    L.attn_encoder_decoder_if_fwd.restype = ctypes.c_int
     L.attn_hidden_scatter.restype = ctypes.c_int
     _lib = L
     return L
@@ -421,3 +429,24 @@ def attn_encoder_decoder_fwd(s: LstmShape, src_ids, tgt_ids, src_lens, E_src, E_
 def attn_hidden_scatter(comm, root, B_global, rows, hidden, full, shard, stream=None):
     _check(lib().attn_hidden_scatter(comm, int(root), int(B_global), int(rows), int(hidden),
                                      _ptr(full), _ptr(shard), _stream(stream)))
+
+
+def attn_lstm_if_workspace_size(s: LstmShape) -> int:
+    n = lib().attn_lstm_if_workspace_size(ctypes.byref(s))
+    if n == 0:
+        raise AttnError(7, lib().attn_last_error().decode())
+    return n
+
+
+def attn_encoder_decoder_if_fwd(s: LstmShape, src_ids, tgt_ids, src_lens, E_src, E_tgt, enc_W,
+                                enc_b, dec_W, dec_b, W_c, H_enc, H_dec, Htilde, workspace,
+                                stream=None):
+    src, src_p = _i32(src_lens)
+
+    def arr(ts):
+        return (_P * len(ts))(*[t.data_ptr() for t in ts])
+    eW, eb, dW, db = arr(enc_W), arr(enc_b), arr(dec_W), arr(dec_b)
+    _check(lib().attn_encoder_decoder_if_fwd(
+        ctypes.byref(s), _ptr(src_ids), _ptr(tgt_ids), src_p, _ptr(E_src), _ptr(E_tgt), eW, eb,
+        dW, db, _ptr(W_c), _ptr(H_enc), _ptr(H_dec), _ptr(Htilde), _ptr(workspace),
+        workspace.numel() * workspace.element_size(), _stream(stream)))

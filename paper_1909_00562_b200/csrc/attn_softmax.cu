@@ -2057,6 +2057,32 @@ extern "C" size_t attn_softmax_decode_workspace_size(const attn_shape_t* s) {
   return p.total + decode_topk_bytes(p);
 }
 
+// ---------------------------------------------------------------- input feeding (NEXT-3 IF)
+// Internal entry for lstm.cu's input-feeding decoder (HybridNMTIF, PAPER.md:
+// 157): one decoder step of the attention for B sentences -- alpha and C of
+// q = h (N = 1) over S, then Htilde = tanh(W_c [h; C]) (Eqs. 1-4) written to
+// `out` with row stride ld_out (elements) -- on the same kernels as the stage.
+size_t attn_internal_step_ws(int B, int M, int d) {
+  attn_shape_t s{B, 1, M, d, 64, ATTN_BF16};
+  return make_plan(&s).total;
+}
+attn_status_t attn_internal_step_attention(int B, int M, int d, const void* h, const void* S,
+                                           const int* src_len_dev, const void* W_c, void* out,
+                                           long long ld_out, void* ws, cudaStream_t stream) {
+  OPT_LOCK;
+  attn_shape_t s{B, 1, M, d, 64, ATTN_BF16};
+  const Plan p = make_plan(&s);
+  Bufs b = carve(p, ws);
+  b.src_len = const_cast<int*>(src_len_dev);   // lengths already on the device
+  CUDA_TRY(cudaMemsetAsync(b.counters, 0, sizeof(unsigned int) * kNumCounters, stream));
+  CounterCtx cctx{&b, 0};
+  attn_status_t st = attention_forward_tc(p, h, S, b, stream, next_counter_fn, &cctx, nullptr);
+  if (st != ATTN_OK) return st;
+  GemmDesc g = g_proj(p, h, b.ctx, W_c, out);
+  g.epi.ldo = ld_out;
+  return launch_tc_group<__nv_bfloat16>(&g, 1, next_counter_fn(&cctx), stream, PAIR_FWD);
+}
+
 extern "C" attn_status_t attn_softmax_decode_step(
     const attn_shape_t* s, const void* H_dec, const void* H_enc, const int32_t* src_lens_host,
     const void* W_c, const void* W_out, const void* W_alpha, const void* b_out, int k,

@@ -304,7 +304,35 @@ __global__ void embed_kernel(const int* __restrict__ ids, const __nv_bfloat16* _
   }
 }
 
+// input feeding (HybridNMTIF): X[b][:] = [E[ids[b][t]] | Htilde[b][t-1]] (0 at t = 0)
+__global__ void if_input_kernel(const int* __restrict__ ids, int N, int t,
+                                const __nv_bfloat16* __restrict__ E, int e,
+                                const __nv_bfloat16* __restrict__ Hc, int hd, int B,
+                                __nv_bfloat16* __restrict__ X) {
+  const int w8 = (e + hd) / 8;
+  const long long n = (long long)B * w8;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(i / w8), k = (int)(i % w8);
+    uint4 v;
+    if (k < e / 8) {
+      v = __ldg(reinterpret_cast<const uint4*>(E) + (long long)ids[(long long)b * N + t] * (e / 8) + k);
+    } else if (t > 0) {
+      v = reinterpret_cast<const uint4*>(Hc + ((long long)b * N + t - 1) * hd)[k - e / 8];
+    } else {
+      v = make_uint4(0u, 0u, 0u, 0u);
+    }
+    reinterpret_cast<uint4*>(X)[i] = v;
+  }
+}
+
 }  // namespace attnsm
+
+// internal entry of attn_softmax.cu: one step of Eqs. 1-4 for the IF decoder
+size_t attn_internal_step_ws(int B, int M, int d);
+attn_status_t attn_internal_step_attention(int B, int M, int d, const void* h, const void* S,
+                                           const int* src_len_dev, const void* W_c, void* out,
+                                           long long ld_out, void* ws, cudaStream_t stream);
 
 using namespace attnsm;
 
@@ -434,40 +462,52 @@ extern "C" attn_status_t attn_lstm_pack_layer(int in, int hidden, const void* W_
 
 namespace {
 
-// one side (encoder or decoder): L layers over T steps as one cooperative launch
-attn_status_t run_side(const attn_lstm_shape_t* s, const LsPlan& p, int T, const void* X0,
-                       const void* const* W, const float* const* b, void* H_top, char* ws,
-                       bool decoder, const int* cap_dev, unsigned* done, cudaStream_t st) {
+// One cooperative launch of the wavefront kernel: L layers over T steps.
+// Per layer: its output sequence hout [B][T][hd], running c state, optional
+// initial (h0 bf16 [B][hd], c0 fp32 [B][hd]) and capture buffers.
+struct RunCfg {
+  int B, T, hd, L, G, ntile, in0;
+  const void* X0;                 // layer-0 input [B][T][in0]
+  const void* const* W;           // packed layers
+  const float* const* b;
+  void* hout[LS_MAXL];
+  float* c[LS_MAXL];
+  const void* h0[LS_MAXL];        // NULL: zero initial state (then c0 must be NULL too)
+  const float* c0[LS_MAXL];
+  void* hcap[LS_MAXL];            // capture at cap_dev[b] (or NULL)
+  float* ccap[LS_MAXL];
+  const int* cap_dev;
+  unsigned* done;                 // [L][T], zeroed here
+};
+
+attn_status_t run_layers(const RunCfg& R, cudaStream_t st) {
   static LsParams P;   // large: filled under a lock
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
   memset(&P, 0, sizeof(P));
-  const int B = s->batch, hd = s->hidden, L = s->layers;
+  const int B = R.B, T = R.T, hd = R.hd, L = R.L;
   attn_status_t r;
-  __nv_bfloat16* inter = reinterpret_cast<__nv_bfloat16*>(ws + p.inter);
   for (int l = 0; l < L; ++l) {
     LsLayer& Ly = P.layer[l];
-    Ly.in = l == 0 ? s->emb : hd;
-    const void* xin = l == 0 ? X0 : (const void*)(inter + (size_t)(l - 1) * B * T * hd);
-    __nv_bfloat16* hout = l == L - 1 ? static_cast<__nv_bfloat16*>(H_top) : inter + (size_t)l * B * T * hd;
+    Ly.in = l == 0 ? R.in0 : hd;
+    const void* xin = l == 0 ? R.X0 : R.hout[l - 1];
     if ((r = map_seq(&Ly.m_x, xin, Ly.in, T, B)) != ATTN_OK) return r;
-    if ((r = map_seq(&Ly.m_h, hout, hd, T, B)) != ATTN_OK) return r;
-    __nv_bfloat16* hcap = reinterpret_cast<__nv_bfloat16*>(ws + p.hcap) + (size_t)l * B * hd;
-    float* ccap = reinterpret_cast<float*>(ws + p.ccap) + (size_t)l * B * hd;
-    if ((r = map_mat(&Ly.m_h0, hcap, hd, B, 128)) != ATTN_OK) return r;
-    if ((r = map_mat(&Ly.m_w, W[l], Ly.in + hd, 4 * hd, p.ntile)) != ATTN_OK) return r;
-    Ly.bias = b[l];
-    Ly.h_out = hout;
-    Ly.c = reinterpret_cast<float*>(ws + p.c) + (size_t)l * B * hd;
-    Ly.c0 = decoder ? ccap : nullptr;
-    Ly.h_cap = decoder ? nullptr : hcap;
-    Ly.c_cap = decoder ? nullptr : ccap;
+    if ((r = map_seq(&Ly.m_h, R.hout[l], hd, T, B)) != ATTN_OK) return r;
+    // (a dummy but valid map when there is no initial h: never loaded)
+    if ((r = map_mat(&Ly.m_h0, R.h0[0] ? R.h0[l] : R.hout[l], hd, B, 128)) != ATTN_OK) return r;
+    if ((r = map_mat(&Ly.m_w, R.W[l], Ly.in + hd, 4 * hd, R.ntile)) != ATTN_OK) return r;
+    Ly.bias = R.b[l];
+    Ly.h_out = static_cast<__nv_bfloat16*>(R.hout[l]);
+    Ly.c = R.c[l];
+    Ly.c0 = R.c0[l];
+    Ly.h_cap = static_cast<__nv_bfloat16*>(R.hcap[l]);
+    Ly.c_cap = R.ccap[l];
   }
-  P.L = L; P.B = B; P.T = T; P.hd = hd; P.G = p.G; P.ntile = p.ntile;
-  P.has_init = decoder ? 1 : 0;
-  P.cap = decoder ? nullptr : cap_dev;
-  P.done = done;
-  LS_CUDA(cudaMemsetAsync(done, 0, sizeof(unsigned) * (size_t)L * T, st));
+  P.L = L; P.B = B; P.T = T; P.hd = hd; P.G = R.G; P.ntile = R.ntile;
+  P.has_init = R.h0[0] ? 1 : 0;
+  P.cap = R.cap_dev;
+  P.done = R.done;
+  LS_CUDA(cudaMemsetAsync(R.done, 0, sizeof(unsigned) * (size_t)L * T, st));
   static std::vector<int> attr_set;   // devices with the smem attribute set
   int dev = 0;
   LS_CUDA(cudaGetDevice(&dev));
@@ -476,7 +516,7 @@ attn_status_t run_side(const attn_lstm_shape_t* s, const LsPlan& p, int T, const
     attr_set.push_back(dev);
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(L * p.G);
+  cfg.gridDim = dim3(L * R.G);
   cfg.blockDim = dim3(LS_THREADS);
   cfg.dynamicSmemBytes = LS_SMEM;
   cfg.stream = st;
@@ -487,6 +527,29 @@ attn_status_t run_side(const attn_lstm_shape_t* s, const LsPlan& p, int T, const
   cfg.numAttrs = 1;
   LS_CUDA(cudaLaunchKernelEx(&cfg, lstm_wavefront_kernel, P));
   return ATTN_OK;
+}
+
+// one side (encoder or decoder): L layers over T steps as one cooperative launch
+attn_status_t run_side(const attn_lstm_shape_t* s, const LsPlan& p, int T, const void* X0,
+                       const void* const* W, const float* const* b, void* H_top, char* ws,
+                       bool decoder, const int* cap_dev, unsigned* done, cudaStream_t st) {
+  RunCfg R;
+  memset(&R, 0, sizeof(R));
+  const int B = s->batch, hd = s->hidden, L = s->layers;
+  R.B = B; R.T = T; R.hd = hd; R.L = L; R.G = p.G; R.ntile = p.ntile; R.in0 = s->emb;
+  R.X0 = X0; R.W = W; R.b = b; R.cap_dev = decoder ? nullptr : cap_dev; R.done = done;
+  __nv_bfloat16* inter = reinterpret_cast<__nv_bfloat16*>(ws + p.inter);
+  for (int l = 0; l < L; ++l) {
+    R.hout[l] = l == L - 1 ? H_top : (void*)(inter + (size_t)l * B * T * hd);
+    R.c[l] = reinterpret_cast<float*>(ws + p.c) + (size_t)l * B * hd;
+    __nv_bfloat16* hcap = reinterpret_cast<__nv_bfloat16*>(ws + p.hcap) + (size_t)l * B * hd;
+    float* ccap = reinterpret_cast<float*>(ws + p.ccap) + (size_t)l * B * hd;
+    R.h0[l] = decoder ? hcap : nullptr;
+    R.c0[l] = decoder ? ccap : nullptr;
+    R.hcap[l] = decoder ? nullptr : hcap;
+    R.ccap[l] = decoder ? nullptr : ccap;
+  }
+  return run_layers(R, st);
 }
 
 }  // namespace
@@ -538,4 +601,115 @@ extern "C" attn_status_t attn_encoder_decoder_fwd(
     return r;
   return run_side(s, p, N, Xt, dec_W, dec_b, H_dec, ws, true, nullptr,
                   reinterpret_cast<unsigned*>(ws + p.done_dec), st);
+}
+
+// ---------------------------------------------------------------- input feeding
+namespace {
+struct IfPlan {
+  size_t x, h, c, srclen, done, attn, total;
+};
+IfPlan plan_if(const attn_lstm_shape_t* s, const LsPlan& base) {
+  IfPlan q;
+  const int B = s->batch, hd = s->hidden, L = s->layers;
+  size_t o = base.total;
+  auto take = [&](size_t b) { size_t r = o; o += al(b); return r; };
+  q.x = take((size_t)B * (s->emb + hd) * 2);
+  q.h = take((size_t)2 * L * B * hd * 2);
+  q.c = take((size_t)2 * L * B * hd * 4);
+  q.srclen = take((size_t)B * 4);
+  q.done = take((size_t)L * 4);
+  q.attn = take(attn_internal_step_ws(B, s->src_len, hd));
+  q.total = o;
+  return q;
+}
+}  // namespace
+
+extern "C" size_t attn_lstm_if_workspace_size(const attn_lstm_shape_t* s) {
+  if (check_lstm(s) != ATTN_OK) return 0;
+  const LsPlan p = plan_lstm(s);
+  return plan_if(s, p).total;
+}
+
+extern "C" attn_status_t attn_encoder_decoder_if_fwd(
+    const attn_lstm_shape_t* s, const int32_t* src_ids, const int32_t* tgt_ids,
+    const int32_t* src_lens_host, const void* E_src, const void* E_tgt,
+    const void* const* enc_W, const float* const* enc_b, const void* const* dec_W,
+    const float* const* dec_b, const void* W_c, void* H_enc, void* H_dec, void* Htilde,
+    void* workspace, size_t workspace_bytes, void* stream) {
+  attn_status_t r = check_lstm(s);
+  if (r != ATTN_OK) return r;
+  if (!src_ids || !tgt_ids || !src_lens_host || !E_src || !E_tgt || !enc_W || !enc_b || !dec_W ||
+      !dec_b || !W_c || !H_enc || !H_dec || !Htilde || !workspace)
+    return lfail(ATTN_ERR_INVALID_ARG, "encoder_decoder_if_fwd: NULL argument");
+  for (int l = 0; l < s->layers; ++l)
+    if (!enc_W[l] || !enc_b[l] || !dec_W[l] || !dec_b[l])
+      return lfail(ATTN_ERR_INVALID_ARG, "encoder_decoder_if_fwd: layer %d weights are NULL", l);
+  if (s->src_len > 128)
+    return lfail(ATTN_ERR_UNSUPPORTED, "encoder_decoder_if_fwd: M = %d > 128 (fused attention step)", s->src_len);
+  for (int i = 0; i < s->batch; ++i)
+    if (src_lens_host[i] < 1 || src_lens_host[i] > s->src_len)
+      return lfail(ATTN_ERR_SHAPE, "src_lens_host[%d] = %d outside [1, M = %d]", i, src_lens_host[i], s->src_len);
+  const LsPlan p = plan_lstm(s);
+  const IfPlan q = plan_if(s, p);
+  if (workspace_bytes < q.total)
+    return lfail(ATTN_ERR_WORKSPACE, "workspace_bytes = %zu < required %zu", workspace_bytes, q.total);
+  int dev = 0, sms = 0;
+  LS_CUDA(cudaGetDevice(&dev));
+  LS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (s->layers * p.G > sms)
+    return lfail(ATTN_ERR_UNSUPPORTED, "lstm: %d layers x %d CTAs exceed the %d SMs", s->layers, p.G, sms);
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = static_cast<char*>(workspace);
+  const int B = s->batch, M = s->src_len, N = s->tgt_len, e = s->emb, hd = s->hidden, L = s->layers;
+  // encoder (wavefront over all source steps), capturing the state at src_len - 1
+  std::vector<int> cap(B), sl(B);
+  for (int i = 0; i < B; ++i) {
+    cap[i] = src_lens_host[i] - 1;
+    sl[i] = src_lens_host[i];
+  }
+  int* cap_dev = reinterpret_cast<int*>(ws + p.lens);
+  int* sl_dev = reinterpret_cast<int*>(ws + q.srclen);
+  LS_CUDA(cudaMemcpyAsync(cap_dev, cap.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
+  LS_CUDA(cudaMemcpyAsync(sl_dev, sl.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
+  __nv_bfloat16* Xs = reinterpret_cast<__nv_bfloat16*>(ws + p.xs);
+  embed_kernel<<<sms * 4, 256, 0, st>>>(src_ids, static_cast<const __nv_bfloat16*>(E_src), e,
+                                        (long long)B * M, Xs);
+  LS_CUDA(cudaGetLastError());
+  if ((r = run_side(s, p, M, Xs, enc_W, enc_b, H_enc, ws, false, cap_dev,
+                    reinterpret_cast<unsigned*>(ws + p.done_enc), st)) != ATTN_OK)
+    return r;
+  // decoder with input feeding: step t needs Htilde_{t-1} = tanh(W_c [h_{t-1}; C_{t-1}])
+  // (PAPER.md:75, :99), so the steps run one after another: per step one
+  // wavefront launch over the L layers (T = 1), then Eqs. 1-4 for that step
+  __nv_bfloat16* X = reinterpret_cast<__nv_bfloat16*>(ws + q.x);
+  __nv_bfloat16* hbuf = reinterpret_cast<__nv_bfloat16*>(ws + q.h);
+  float* cbuf = reinterpret_cast<float*>(ws + q.c);
+  __nv_bfloat16* hcap = reinterpret_cast<__nv_bfloat16*>(ws + p.hcap);
+  float* ccap = reinterpret_cast<float*>(ws + p.ccap);
+  const size_t lay = (size_t)B * hd;
+  for (int t = 0; t < N; ++t) {
+    const int cur = t & 1, prv = cur ^ 1;
+    if_input_kernel<<<sms, 256, 0, st>>>(tgt_ids, N, t, static_cast<const __nv_bfloat16*>(E_tgt), e,
+                                         static_cast<const __nv_bfloat16*>(Htilde), hd, B, X);
+    LS_CUDA(cudaGetLastError());
+    RunCfg R;
+    memset(&R, 0, sizeof(R));
+    R.B = B; R.T = 1; R.hd = hd; R.L = L; R.G = p.G; R.ntile = p.ntile; R.in0 = e + hd;
+    R.X0 = X; R.W = dec_W; R.b = dec_b; R.done = reinterpret_cast<unsigned*>(ws + q.done);
+    for (int l = 0; l < L; ++l) {
+      R.hout[l] = hbuf + ((size_t)cur * L + l) * lay;
+      R.c[l] = cbuf + ((size_t)cur * L + l) * lay;
+      R.h0[l] = t == 0 ? (const void*)(hcap + l * lay) : (const void*)(hbuf + ((size_t)prv * L + l) * lay);
+      R.c0[l] = t == 0 ? (const float*)(ccap + l * lay) : (const float*)(cbuf + ((size_t)prv * L + l) * lay);
+    }
+    if ((r = run_layers(R, st)) != ATTN_OK) return r;
+    const void* htop = R.hout[L - 1];
+    LS_CUDA(cudaMemcpy2DAsync(static_cast<char*>(H_dec) + (size_t)t * hd * 2, (size_t)N * hd * 2, htop,
+                              (size_t)hd * 2, (size_t)hd * 2, B, cudaMemcpyDeviceToDevice, st));
+    if ((r = attn_internal_step_attention(B, M, hd, htop, H_enc, sl_dev, W_c,
+                                          static_cast<char*>(Htilde) + (size_t)t * hd * 2,
+                                          (long long)N * hd, ws + q.attn, st)) != ATTN_OK)
+      return r;
+  }
+  return ATTN_OK;
 }

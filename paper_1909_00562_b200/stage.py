@@ -125,18 +125,24 @@ class EncoderDecoder:
     the packed layer weights (attn_lstm_pack_layer) and the workspace."""
 
     def __init__(self, B: int, M: int, N: int, emb: int, hidden: int, layers: int,
-                 vocab_src: int, vocab_tgt: int, device: Optional[torch.device] = None):
+                 vocab_src: int, vocab_tgt: int, device: Optional[torch.device] = None,
+                 input_feeding: bool = False):
+        """input_feeding=True: HybridNMTIF, the decoder's first
+        layer sees [E_tgt[y_t]; Htilde_{t-1}] (its W_ih has emb + hidden columns)
+        and the call also needs W_c and returns Htilde."""
         self.B, self.M, self.N, self.emb, self.hidden, self.layers = B, M, N, emb, hidden, layers
+        self.input_feeding = input_feeding
         self.device = torch.device(device or "cuda")
         self.shape = binding.lstm_shape(B, M, N, emb, hidden, layers, vocab_src, vocab_tgt)
-        self.workspace = torch.empty(binding.attn_lstm_workspace_size(self.shape),
-                                     dtype=torch.uint8, device=self.device)
+        n = (binding.attn_lstm_if_workspace_size if input_feeding else
+             binding.attn_lstm_workspace_size)(self.shape)
+        self.workspace = torch.empty(n, dtype=torch.uint8, device=self.device)
         self.enc_W = self.enc_b = self.dec_W = self.dec_b = None
 
-    def _pack(self, layers):
+    def _pack(self, layers, feed=False):
         Ws, bs = [], []
         for l, (W_ih, W_hh, b) in enumerate(layers):
-            fin = self.emb if l == 0 else self.hidden
+            fin = (self.emb + (self.hidden if feed else 0)) if l == 0 else self.hidden
             Wp = torch.empty(4 * self.hidden, fin + self.hidden, dtype=torch.bfloat16, device=self.device)
             bp = torch.empty(4 * self.hidden, dtype=torch.float32, device=self.device)
             binding.attn_lstm_pack_layer(fin, self.hidden, W_ih, W_hh, b, Wp, bp)
@@ -147,9 +153,19 @@ class EncoderDecoder:
     def set_weights(self, enc_layers, dec_layers):
         """enc_layers / dec_layers: [(W_ih, W_hh, b)] bf16 device tensors (PyTorch layout)."""
         self.enc_W, self.enc_b = self._pack(enc_layers)
-        self.dec_W, self.dec_b = self._pack(dec_layers)
+        self.dec_W, self.dec_b = self._pack(dec_layers, feed=self.input_feeding)
 
-    def __call__(self, src_ids, tgt_ids, src_len, E_src, E_tgt, H_enc=None, H_dec=None, stream=None):
+    def __call__(self, src_ids, tgt_ids, src_len, E_src, E_tgt, H_enc=None, H_dec=None, stream=None,
+                 W_c=None, Htilde=None):
+        if self.input_feeding:
+            mk = lambda T: torch.empty(self.B, T, self.hidden, dtype=torch.bfloat16, device=self.device)
+            H_enc = mk(self.M) if H_enc is None else H_enc
+            H_dec = mk(self.N) if H_dec is None else H_dec
+            Htilde = mk(self.N) if Htilde is None else Htilde
+            binding.attn_encoder_decoder_if_fwd(self.shape, src_ids, tgt_ids, src_len, E_src, E_tgt,
+                                                self.enc_W, self.enc_b, self.dec_W, self.dec_b, W_c,
+                                                H_enc, H_dec, Htilde, self.workspace, stream=stream)
+            return H_enc, H_dec, Htilde
         if H_enc is None:
             H_enc = torch.empty(self.B, self.M, self.hidden, dtype=torch.bfloat16, device=self.device)
         if H_dec is None:

@@ -188,14 +188,16 @@ def shard_range(B_global: int, world: int, rank: int):
 
 
 def make_lstm_inputs(cfg: Config, layers: int = 4, emb: Optional[int] = None,
-                     sentences: Optional[Sequence[int]] = None):
+                     sentences: Optional[Sequence[int]] = None, input_feeding: bool = False):
     """Inputs of the encoder-decoder part (NEXT-3; Table 1, PAPER.md:190-192:
     embedding 512, hidden 1024, 4 stacked LSTM layers): source / target ids
     [B, M] / [B, N] ~ U{4 .. V-1} (one vocabulary of size V for both sides),
     the config's lengths, embedding tables E_src / E_tgt [V, emb] and per
     layer (W_ih [4h, in], W_hh [4h, h], b [4h]) for the encoder and the
     decoder, all ~ U(-0.1, 0.1) (SPEC.md:273 init) and bf16-rounded for bf16
-    configs.  emb defaults to h / 2 (512 for h = 1024)."""
+    configs.  emb defaults to h / 2 (512 for h = 1024).  input_feeding: the
+    decoder's layer-0 W_ih has emb + h columns (HybridNMTIF), and W_c [h, 2h]
+    (as make_weights) is included."""
     if sentences is None:
         sentences = range(cfg.B)
     sentences = list(sentences)
@@ -219,10 +221,12 @@ def make_lstm_inputs(cfg: Config, layers: int = 4, emb: Optional[int] = None,
     for side, base in (("enc", 3000), ("dec", 4000)):
         ws = []
         for l in range(layers):
-            fin = e if l == 0 else h
+            fin = (e + (h if (input_feeding and side == "dec") else 0)) if l == 0 else h
             ws.append((u(base + 10 * l, (4 * h, fin)), u(base + 10 * l + 1, (4 * h, h)),
                        u(base + 10 * l + 2, (4 * h,))))
         out[side] = ws
+    if input_feeding:
+        out["W_c"] = make_weights(cfg)["W_c"]
     if cfg.dtype == "bf16":
         out["E_src"] = round_bf16(out["E_src"])
         out["E_tgt"] = round_bf16(out["E_tgt"])

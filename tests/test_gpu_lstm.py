@@ -94,3 +94,28 @@ def test_lstm_rejects_bad_shapes(cuda_lib):
         binding.attn_lstm_workspace_size(binding.lstm_shape(129, 5, 5, 64, 64, 1, 10, 10))
     with pytest.raises(binding.AttnError):
         binding.attn_lstm_workspace_size(binding.lstm_shape(4, 5, 5, 48, 64, 1, 10, 10))
+
+
+@pytest.mark.parametrize("name,layers,emb", [("small", 2, 128), ("medium", 4, 256), ("edge_min", 1, 64)])
+def test_input_feeding_matches_oracle(cuda_lib, name, layers, emb):
+    """HybridNMTIF: the input-feeding decoder (one wavefront
+    launch per step + the fused attention step) against the fp64 oracle."""
+    from paper_1909_00562_b200.stage import EncoderDecoder
+    cfg = CONFIGS[name]
+    inp = make_lstm_inputs(cfg, layers=layers, emb=emb, input_feeding=True)
+    dev = torch.device("cuda")
+    bf = lambda a: torch.from_numpy(np.asarray(a, np.float32)).to(dev, torch.bfloat16)
+    ed = EncoderDecoder(cfg.B, cfg.M, cfg.N, emb, cfg.d, layers, cfg.V, cfg.V, input_feeding=True)
+    ed.set_weights([tuple(bf(w) for w in ws) for ws in inp["enc"]],
+                   [tuple(bf(w) for w in ws) for ws in inp["dec"]])
+    H_enc, H_dec, Ht = ed(torch.from_numpy(inp["src_ids"]).to(dev), torch.from_numpy(inp["tgt_ids"]).to(dev),
+                          inp["src_len"], bf(inp["E_src"]), bf(inp["E_tgt"]), W_c=bf(inp["W_c"]))
+    torch.cuda.synchronize()
+    S, H, Htl = LO.encoder_decoder_if(inp["src_ids"], inp["tgt_ids"], inp["src_len"], inp["E_src"],
+                                      inp["E_tgt"], inp["enc"], inp["dec"], inp["W_c"])
+    ge, gd, gt = (x.double().cpu().numpy() for x in (H_enc, H_dec, Ht))
+    assert _rel(ge, S) <= TOL, ("H_enc", _rel(ge, S))
+    assert _rel(gd, H) <= TOL, ("H_dec", _rel(gd, H))
+    assert _rel(gt, Htl) <= TOL, ("Htilde", _rel(gt, Htl))
+    for b in range(cfg.B):
+        assert _rel(gt[b], Htl[b]) <= TOL, ("Htilde sentence", b)

@@ -84,3 +84,73 @@ def test_decoder_starts_from_state_at_last_real_source_position():
     assert np.allclose(H, y.numpy(), rtol=1e-11, atol=1e-13)
     # S (all source steps, padded positions included) = the unpacked run
     assert np.allclose(S, s_full.numpy(), rtol=1e-11, atol=1e-13)
+
+
+def _torch_if(inp, cfg):
+    """An independent float64 composition of HybridNMTIF: torch.nn.LSTM for the
+    encoder (packed), torch.nn.LSTMCell per decoder layer, SDPA for Eqs. 1-3."""
+    import torch.nn.functional as F
+    enc = _torch_lstm(inp["enc"], cfg.d)
+    Xs = torch.from_numpy(np.asarray(inp["E_src"], np.float64)[inp["src_ids"]])
+    Et = torch.from_numpy(np.asarray(inp["E_tgt"], np.float64))
+    W_c = torch.from_numpy(np.asarray(inp["W_c"], np.float64))
+    lens = torch.from_numpy(inp["src_len"].astype(np.int64))
+    with torch.no_grad():
+        S, _ = enc(Xs)
+        packed = torch.nn.utils.rnn.pack_padded_sequence(Xs, lens, batch_first=True, enforce_sorted=False)
+        _, (hn, cn) = enc(packed)
+        cells = []
+        for (W_ih, W_hh, b) in inp["dec"]:
+            cell = torch.nn.LSTMCell(W_ih.shape[1], cfg.d).double()
+            cell.weight_ih.copy_(torch.from_numpy(np.asarray(W_ih, np.float64)))
+            cell.weight_hh.copy_(torch.from_numpy(np.asarray(W_hh, np.float64)))
+            cell.bias_ih.copy_(torch.from_numpy(np.asarray(b, np.float64)))
+            cell.bias_hh.zero_()
+            cells.append(cell)
+        h = [hn[l].clone() for l in range(len(cells))]
+        c = [cn[l].clone() for l in range(len(cells))]
+        B, N = inp["tgt_ids"].shape
+        mask = torch.arange(cfg.M)[None, :] < lens[:, None]
+        feed = torch.zeros(B, cfg.d, dtype=torch.float64)
+        Ht = []
+        for t in range(N):
+            x = torch.cat([Et[torch.from_numpy(inp["tgt_ids"][:, t].astype(np.int64))], feed], dim=1)
+            for l, cell in enumerate(cells):
+                h[l], c[l] = cell(x, (h[l], c[l]))
+                x = h[l]
+            C = F.scaled_dot_product_attention(h[-1][:, None, None, :], S[:, None], S[:, None],
+                                               attn_mask=mask[:, None, None, :], scale=1.0)[:, 0, 0]
+            feed = torch.tanh(torch.cat([h[-1], C], dim=1) @ W_c.T)
+            Ht.append(feed)
+    return torch.stack(Ht, 1).numpy()
+
+
+def test_input_feeding_equals_torch_float64():
+    cfg = CONFIGS["small_f32"]
+    inp = make_lstm_inputs(cfg, layers=2, emb=8, input_feeding=True)
+    _, _, Ht = LO.encoder_decoder_if(inp["src_ids"], inp["tgt_ids"], inp["src_len"], inp["E_src"],
+                                     inp["E_tgt"], inp["enc"], inp["dec"], inp["W_c"])
+    assert np.allclose(Ht, _torch_if(inp, cfg), rtol=1e-11, atol=1e-13)
+
+
+def test_input_feeding_with_zero_feed_columns_is_the_plain_decoder():
+    """W_ih[:, e:] = 0 cuts the feedback: H must equal the plain decoder's and
+    Htilde_t the attention step of H_t (Eqs. 1-4 as the stage oracle computes them)."""
+    from oracle import attn_softmax_oracle as AO
+    cfg = CONFIGS["small_f32"]
+    e = 8
+    inp = make_lstm_inputs(cfg, layers=2, emb=e, input_feeding=True)
+    W_ih, W_hh, b = inp["dec"][0]
+    dec_plain = [(W_ih[:, :e], W_hh, b)] + list(inp["dec"][1:])
+    W_ih0 = W_ih.copy()
+    W_ih0[:, e:] = 0.0
+    dec_zero = [(W_ih0, W_hh, b)] + list(inp["dec"][1:])
+    S, H, Ht = LO.encoder_decoder_if(inp["src_ids"], inp["tgt_ids"], inp["src_len"], inp["E_src"],
+                                     inp["E_tgt"], inp["enc"], dec_zero, inp["W_c"])
+    S2, H2 = LO.encoder_decoder(inp["src_ids"], inp["tgt_ids"], inp["src_len"], inp["E_src"],
+                                inp["E_tgt"], inp["enc"], dec_plain)
+    assert np.allclose(H, H2, rtol=1e-12, atol=1e-14)
+    B, N = inp["tgt_ids"].shape
+    f, _ = AO.fwd_bwd(H, S, inp["src_len"], np.full(B, N, np.int32), np.zeros((B, N), np.int32),
+                      inp["W_c"], np.zeros((5, cfg.d)), 1.0)
+    assert np.allclose(Ht, f["Hc"].reshape(B, N, cfg.d), rtol=1e-12, atol=1e-14)
