@@ -127,7 +127,8 @@ struct alignas(64) VbParams {
   float* db_part;        // with the bias: [T / 32][V] column sums of dL per 32-row group
   int last_g2_first;     // last block: G2 tiles before G3 tiles
   int order;             // 0: block c+1 = G3(c), G2(c), G1(c+1); 1: G1(c+1), G3(c), G2(c)
-  int l2hints;           // bit 0: H_c loads evict-last; bit 1: dHc updates evict-last
+  int l2hints;           // bit 0: H_c loads evict-last; bit 1: dHc updates evict-last;
+                         // bit 2: dL stores evict-last
   long long* trace;      // debug: 16 int64 per tile and CTA rank (see VB_TRACE), NULL = off
   int debug;             // timing experiments only (WRONG results): bit 0 skip the G1 stores,
                          // bit 1 skip the G1 exponentials, bit 2 skip the G2 / G3 stores
@@ -591,6 +592,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
     uint8_t* stg_p = staging + warp * VB_STG_BYTES;
     const uint32_t stg = smem_u32(stg_p);
     const uint32_t swz = lane & 7;
+    // l2hints bit 2: the dL chunk stores stay in L2 until its G2 / G3 readers come
+    const uint64_t pol_dl = l2_policy_evict_last();
     int r = 0;
     uint32_t rph = 0;
     int acc = 0;
@@ -778,7 +781,10 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0 && !(P.debug & 1)) {
-              tma_store_3d(&P.m_dl_st, stg_p, colh + (cc - 1) * 32, row0, buf);
+              if (P.l2hints & 4)
+                tma_store_3d_hint(&P.m_dl_st, stg_p, colh + (cc - 1) * 32, row0, buf, pol_dl);
+              else
+                tma_store_3d(&P.m_dl_st, stg_p, colh + (cc - 1) * 32, row0, buf);
               bulk_commit();
             }
           }
