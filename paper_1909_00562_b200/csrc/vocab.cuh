@@ -131,7 +131,8 @@ struct alignas(64) VbParams {
                          // bit 2: dL stores evict-last
   long long* trace;      // debug: 16 int64 per tile and CTA rank (see VB_TRACE), NULL = off
   int debug;             // timing experiments only (WRONG results): bit 0 skip the G1 stores,
-                         // bit 1 skip the G1 exponentials, bit 2 skip the G2 / G3 stores
+                         // bit 1 skip the G1 exponentials, bit 2 skip the G2 / G3 stores,
+                         // bit 3 publish tiles without waiting for their stores to land
   int blk_start[VB_MAX_BLOCKS + 2];   // backward blocks, relative to fwd_tiles
 };
 
@@ -799,7 +800,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
         }
         // publish: this warp's 32 x 128 piece of dL_c is in memory
         if (lane == 0) {
-          bulk_wait0();
+          if (!(P.debug & 8)) bulk_wait0();
           fence_proxy_async_global();
           red_release_gpu_add(P.rowdone + (size_t)tl.c * P.nrb + tl.i, 1u);
           red_release_gpu_add(P.coldone + (size_t)tl.c * P.ncolf + tl.j, 1u);
@@ -861,7 +862,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           else mbar_arrive(&tempty[acc]);
         }
         if (lane == 0) {
-          bulk_wait0();
+          if (!(P.debug & 8)) bulk_wait0();
           fence_proxy_async_global();
           red_release_gpu_add(g3 ? dhc_ctr : P.g2done + tl.c, 1u);
         }

@@ -96,7 +96,8 @@ def test_lstm_rejects_bad_shapes(cuda_lib):
         binding.attn_lstm_workspace_size(binding.lstm_shape(4, 5, 5, 48, 64, 1, 10, 10))
 
 
-@pytest.mark.parametrize("name,layers,emb", [("small", 2, 128), ("medium", 4, 256), ("edge_min", 1, 64)])
+@pytest.mark.parametrize("name,layers,emb", [("small", 2, 128), ("medium", 4, 256), ("edge_min", 1, 64),
+                                             ("paper", 4, 512)])
 def test_input_feeding_matches_oracle(cuda_lib, name, layers, emb):
     """HybridNMTIF: the input-feeding decoder (one wavefront
     launch per step + the fused attention step) against the fp64 oracle."""
@@ -117,5 +118,5 @@ def test_input_feeding_matches_oracle(cuda_lib, name, layers, emb):
     assert _rel(ge, S) <= TOL, ("H_enc", _rel(ge, S))
     assert _rel(gd, H) <= TOL, ("H_dec", _rel(gd, H))
     assert _rel(gt, Htl) <= TOL, ("Htilde", _rel(gt, Htl))
-    for b in range(cfg.B):
+    for b in range(min(cfg.B, 16)):
         assert _rel(gt[b], Htl[b]) <= TOL, ("Htilde sentence", b)
