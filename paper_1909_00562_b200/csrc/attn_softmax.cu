@@ -2123,9 +2123,10 @@ extern "C" attn_status_t attn_softmax_decode_step(
   if ((st = attention_forward_tc(p, H_dec, H_enc, b, stream, next_counter_fn, &cctx, W_alpha)) !=
       ATTN_OK)
     return st;
-  // F3 (Eq. 4)
+  // F3 (Eq. 4): few rows -- narrower tiles so more SMs take part
   {
     GemmDesc g = g_proj(p, H_dec, b.ctx, W_c, b.hc);
+    if ((p.T + 127) / 128 * ((p.d + 255) / 256) < 74) g.bn = 64;
     if ((st = launch_tc_group<__nv_bfloat16>(&g, 1, next_counter_fn(&cctx), stream, PAIR_FWD)) !=
         ATTN_OK)
       return st;
