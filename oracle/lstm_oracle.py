@@ -44,7 +44,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = ["sigmoid", "lstm_cell", "lstm_stack", "encoder_decoder", "attention_step",
-           "encoder_decoder_if"]
+           "encoder_decoder_if", "lstm_stack_backward", "encoder_decoder_backward"]
 
 
 def sigmoid(x):
@@ -157,3 +157,97 @@ def encoder_decoder_if(src_ids, tgt_ids, src_len, E_src, E_tgt, enc_weights, dec
         feed = attention_step(h[L - 1], S, src_len, W_c)
         Ht[:, t] = feed
     return S, H, Ht
+
+
+# ---------------------------------------------------------------- backward
+def lstm_stack_backward(X, weights, dH_top, h0=None, c0=None, inject=None):
+    """Reverse-mode derivative of lstm_stack (backpropagation through time, the
+    plain chain rule of the cell, layer by layer from the top).  dH_top
+    [B, T, hd]: gradient w.r.t. the top layer's states at every step.
+    inject: optional (step [B], dh [L, B, hd], dc [L, B, hd]) added to layer
+    l's (dh_t, dc_t) at t = step[b] (the decoder's initial-state gradients,
+    which reach the encoder at source step src_len - 1).
+    Returns (dX [B, T, in_0], [(dW_ih, dW_hh, db)] * L, dh0 [L, B, hd], dc0 [L, B, hd])."""
+    X = np.asarray(X, np.float64)
+    B, T, _ = X.shape
+    L = len(weights)
+    hd = np.asarray(weights[0][1]).shape[1]
+    # forward again, keeping every activation
+    inp = X
+    acts = []
+    for l, (W_ih, W_hh, b) in enumerate(weights):
+        W_ih = np.asarray(W_ih, np.float64)
+        W_hh = np.asarray(W_hh, np.float64)
+        h = np.zeros((B, hd)) if h0 is None else np.asarray(h0[l], np.float64).copy()
+        c = np.zeros((B, hd)) if c0 is None else np.asarray(c0[l], np.float64).copy()
+        hs, cs, gs = [h], [c], []
+        for t in range(T):
+            z = inp[:, t] @ W_ih.T + h @ W_hh.T + np.asarray(b, np.float64)
+            i, f = sigmoid(z[:, :hd]), sigmoid(z[:, hd:2 * hd])
+            g, o = np.tanh(z[:, 2 * hd:3 * hd]), sigmoid(z[:, 3 * hd:])
+            c = f * c + i * g
+            h = o * np.tanh(c)
+            hs.append(h)
+            cs.append(c)
+            gs.append((i, f, g, o))
+        acts.append((inp, hs, cs, gs))
+        inp = np.stack(hs[1:], axis=1)
+    grads = [None] * L
+    dh0 = np.zeros((L, B, hd))
+    dc0 = np.zeros((L, B, hd))
+    d_above = np.asarray(dH_top, np.float64)
+    for l in range(L - 1, -1, -1):
+        W_ih, W_hh, _ = (np.asarray(w, np.float64) for w in weights[l])
+        xin, hs, cs, gs = acts[l]
+        dW_ih = np.zeros_like(W_ih)
+        dW_hh = np.zeros_like(W_hh)
+        db = np.zeros(4 * hd)
+        dx = np.zeros_like(xin)
+        dh_next = np.zeros((B, hd))
+        dc_next = np.zeros((B, hd))
+        for t in range(T - 1, -1, -1):
+            dh = d_above[:, t] + dh_next
+            dc_in = dc_next.copy()
+            if inject is not None:
+                sel = np.asarray(inject[0]) == t
+                dh[sel] += inject[1][l][sel]
+                dc_in[sel] += inject[2][l][sel]
+            i, f, g, o = gs[t]
+            tc = np.tanh(cs[t + 1])
+            dc = dc_in + dh * o * (1.0 - tc * tc)
+            dz = np.concatenate([dc * g * i * (1 - i), dc * cs[t] * f * (1 - f),
+                                 dc * i * (1 - g * g), dh * tc * o * (1 - o)], axis=1)
+            dW_ih += dz.T @ xin[:, t]
+            dW_hh += dz.T @ hs[t]
+            db += dz.sum(0)
+            dx[:, t] = dz @ W_ih
+            dh_next = dz @ W_hh
+            dc_next = dc * f
+        grads[l] = (dW_ih, dW_hh, db)
+        dh0[l], dc0[l] = dh_next, dc_next
+        d_above = dx
+    return d_above, grads, dh0, dc0
+
+
+def encoder_decoder_backward(src_ids, tgt_ids, src_len, E_src, E_tgt, enc_weights, dec_weights,
+                             dS, dH):
+    """Gradients of encoder_decoder given dS = dL/dH_enc [B, M, hd] and
+    dH = dL/dH_dec [B, N, hd] (what the attention-softmax stage returns):
+    the decoder backward first; its initial-state gradients enter the encoder
+    at source step src_len - 1 (reading N3); the embedding gradients sum the
+    layer-0 input gradients per token id.  Returns dict with "enc" / "dec"
+    [(dW_ih, dW_hh, db)] * L, "dE_src", "dE_tgt"."""
+    E_src = np.asarray(E_src, np.float64)
+    E_tgt = np.asarray(E_tgt, np.float64)
+    src_ids = np.asarray(src_ids)
+    tgt_ids = np.asarray(tgt_ids)
+    Xs, Xt = E_src[src_ids], E_tgt[tgt_ids]
+    cap = np.asarray(src_len) - 1
+    _, _, h_fin, c_fin = lstm_stack(Xs, enc_weights, capture_at=cap)
+    dXt, dec_g, dh0, dc0 = lstm_stack_backward(Xt, dec_weights, dH, h0=h_fin, c0=c_fin)
+    dXs, enc_g, _, _ = lstm_stack_backward(Xs, enc_weights, dS, inject=(cap, dh0, dc0))
+    dE_src = np.zeros_like(E_src)
+    dE_tgt = np.zeros_like(E_tgt)
+    np.add.at(dE_src, src_ids.reshape(-1), dXs.reshape(-1, dXs.shape[-1]))
+    np.add.at(dE_tgt, tgt_ids.reshape(-1), dXt.reshape(-1, dXt.shape[-1]))
+    return {"enc": enc_g, "dec": dec_g, "dE_src": dE_src, "dE_tgt": dE_tgt}

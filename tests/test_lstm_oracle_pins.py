@@ -154,3 +154,36 @@ def test_input_feeding_with_zero_feed_columns_is_the_plain_decoder():
     f, _ = AO.fwd_bwd(H, S, inp["src_len"], np.full(B, N, np.int32), np.zeros((B, N), np.int32),
                       inp["W_c"], np.zeros((5, cfg.d)), 1.0)
     assert np.allclose(Ht, f["Hc"].reshape(B, N, cfg.d), rtol=1e-12, atol=1e-14)
+
+
+def test_encoder_decoder_backward_equals_torch_autograd():
+    """The oracle's BPTT against torch float64 autograd through the same
+    composition (embeddings, packed encoder, decoder started from the packed
+    final states, arbitrary upstream gradients on S and H)."""
+    cfg = CONFIGS["small_f32"]
+    inp = make_lstm_inputs(cfg, layers=2, emb=8)
+    rng = np.random.default_rng(3)
+    dS = rng.normal(size=(cfg.B, cfg.M, cfg.d))
+    dH = rng.normal(size=(cfg.B, cfg.N, cfg.d))
+    got = LO.encoder_decoder_backward(inp["src_ids"], inp["tgt_ids"], inp["src_len"], inp["E_src"],
+                                      inp["E_tgt"], inp["enc"], inp["dec"], dS, dH)
+    enc = _torch_lstm(inp["enc"], cfg.d)
+    dec = _torch_lstm(inp["dec"], cfg.d)
+    Es = torch.tensor(np.asarray(inp["E_src"], np.float64), requires_grad=True)
+    Et = torch.tensor(np.asarray(inp["E_tgt"], np.float64), requires_grad=True)
+    src = torch.from_numpy(inp["src_ids"].astype(np.int64))
+    tgt = torch.from_numpy(inp["tgt_ids"].astype(np.int64))
+    lens = torch.from_numpy(inp["src_len"].astype(np.int64))
+    Xs, Xt = Es[src], Et[tgt]
+    S, _ = enc(Xs)
+    packed = torch.nn.utils.rnn.pack_padded_sequence(Xs, lens, batch_first=True, enforce_sorted=False)
+    _, (hn, cn) = enc(packed)
+    H, _ = dec(Xt, (hn, cn))
+    (S * torch.from_numpy(dS)).sum().add((H * torch.from_numpy(dH)).sum()).backward()
+    for side, m in (("enc", enc), ("dec", dec)):
+        for l, (dWi, dWh, db) in enumerate(got[side]):
+            assert np.allclose(dWi, getattr(m, f"weight_ih_l{l}").grad.numpy(), rtol=1e-9, atol=1e-11), (side, l)
+            assert np.allclose(dWh, getattr(m, f"weight_hh_l{l}").grad.numpy(), rtol=1e-9, atol=1e-11), (side, l)
+            assert np.allclose(db, getattr(m, f"bias_ih_l{l}").grad.numpy(), rtol=1e-9, atol=1e-11), (side, l)
+    assert np.allclose(got["dE_src"], Es.grad.numpy(), rtol=1e-9, atol=1e-11)
+    assert np.allclose(got["dE_tgt"], Et.grad.numpy(), rtol=1e-9, atol=1e-11)
