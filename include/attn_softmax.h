@@ -329,6 +329,35 @@ attn_status_t attn_encoder_decoder_fwd(
     const float* const* dec_b, void* H_enc, void* H_dec, void* workspace,
     size_t workspace_bytes, void* stream);
 
+/* Training (the backward of the encoder-decoder, "the
+ * alternation of data parallelism and model parallelism on the backward
+ * process goes in a similar but opposite direction"):
+ * attn_encoder_decoder_fwd_train is attn_encoder_decoder_fwd that also keeps,
+ * in its (larger) workspace, every layer's states, cell states and gate
+ * activations; attn_encoder_decoder_bwd then takes the stage's dH_enc / dH_dec
+ * (bf16, e.g. the outputs of attn_softmax_fwd_bwd) and the forward's H_enc /
+ * H_dec, runs the reverse wavefront (top layer first, t = T-1 down to 0; the
+ * decoder before the encoder, whose layer-l state at src_len - 1 receives the
+ * decoder's initial-state gradient) and writes per layer dW [4h][in + h] fp32
+ * and db [4h] fp32 in the PACKED (gate-interleaved) order of
+ * attn_lstm_pack_layer (row 4u + q = gate q of unit u; columns [0, in) the
+ * W_ih part), and dE_src [vocab_src][e], dE_tgt [vocab_tgt][e] fp32 (the
+ * embedding rows are summed with atomics: their summation order is not
+ * fixed).  The same workspace must be passed to both calls. */
+size_t attn_lstm_train_workspace_size(const attn_lstm_shape_t* s);
+attn_status_t attn_encoder_decoder_fwd_train(
+    const attn_lstm_shape_t* s, const int32_t* src_ids, const int32_t* tgt_ids,
+    const int32_t* src_lens_host, const void* E_src, const void* E_tgt,
+    const void* const* enc_W, const float* const* enc_b, const void* const* dec_W,
+    const float* const* dec_b, void* H_enc, void* H_dec, void* workspace,
+    size_t workspace_bytes, void* stream);
+attn_status_t attn_encoder_decoder_bwd(
+    const attn_lstm_shape_t* s, const int32_t* src_ids, const int32_t* tgt_ids,
+    const int32_t* src_lens_host, const void* const* enc_W, const void* const* dec_W,
+    const void* H_enc, const void* H_dec, const void* dH_enc, const void* dH_dec,
+    float* const* dW_enc, float* const* db_enc, float* const* dW_dec, float* const* db_dec,
+    float* dE_src, float* dE_tgt, void* workspace, size_t workspace_bytes, void* stream);
+
 /* HybridNMTIF (the baseline model's input feeding, PAPER.md:75,
  * :99): the same encoder, and a decoder whose layer-0 input at step t is
  * [E_tgt[y_t] ; Htilde_{t-1}] (Htilde_{-1} = 0), where Htilde_t =

@@ -37,7 +37,8 @@ EXPORTS = [
     "attn_softmax_decode_workspace_size", "attn_softmax_decode_step",
     "attn_lstm_workspace_size", "attn_lstm_packed_bytes", "attn_lstm_pack_layer",
     "attn_encoder_decoder_fwd", "attn_hidden_scatter", "attn_lstm_if_workspace_size",
-    "attn_encoder_decoder_if_fwd",
+    "attn_encoder_decoder_if_fwd", "attn_lstm_train_workspace_size",
+    "attn_encoder_decoder_fwd_train", "attn_encoder_decoder_bwd",
 ]
 
 
@@ -176,6 +177,14 @@ def lib() -> ctypes.CDLL:
                                               ctypes.POINTER(_P), _P, _P, _P, _P, _P,
                                               ctypes.c_size_t, _P]
     L.attn_encoder_decoder_if_fwd.restype = ctypes.c_int
+    L.attn_lstm_train_workspace_size.argtypes = [LS]
+    L.attn_lstm_train_workspace_size.restype = ctypes.c_size_t
+    L.attn_encoder_decoder_fwd_train.argtypes = L.attn_encoder_decoder_fwd.argtypes
+    L.attn_encoder_decoder_fwd_train.restype = ctypes.c_int
+    PP = ctypes.POINTER(_P)
+    L.attn_encoder_decoder_bwd.argtypes = [LS, _P, _P, i32p, PP, PP, _P, _P, _P, _P, PP, PP, PP, PP,
+                                           _P, _P, _P, ctypes.c_size_t, _P]
+    L.attn_encoder_decoder_bwd.restype = ctypes.c_int
     L.attn_hidden_scatter.restype = ctypes.c_int
     _lib = L
     return L
@@ -449,4 +458,35 @@ def attn_encoder_decoder_if_fwd(s: LstmShape, src_ids, tgt_ids, src_lens, E_src,
     _check(lib().attn_encoder_decoder_if_fwd(
         ctypes.byref(s), _ptr(src_ids), _ptr(tgt_ids), src_p, _ptr(E_src), _ptr(E_tgt), eW, eb,
         dW, db, _ptr(W_c), _ptr(H_enc), _ptr(H_dec), _ptr(Htilde), _ptr(workspace),
+        workspace.numel() * workspace.element_size(), _stream(stream)))
+
+
+def attn_lstm_train_workspace_size(s: LstmShape) -> int:
+    n = lib().attn_lstm_train_workspace_size(ctypes.byref(s))
+    if n == 0:
+        raise AttnError(7, lib().attn_last_error().decode())
+    return n
+
+
+def _ptrs(ts):
+    return (_P * len(ts))(*[t.data_ptr() for t in ts])
+
+
+def attn_encoder_decoder_fwd_train(s: LstmShape, src_ids, tgt_ids, src_lens, E_src, E_tgt, enc_W,
+                                   enc_b, dec_W, dec_b, H_enc, H_dec, workspace, stream=None):
+    src, src_p = _i32(src_lens)
+    _check(lib().attn_encoder_decoder_fwd_train(
+        ctypes.byref(s), _ptr(src_ids), _ptr(tgt_ids), src_p, _ptr(E_src), _ptr(E_tgt),
+        _ptrs(enc_W), _ptrs(enc_b), _ptrs(dec_W), _ptrs(dec_b), _ptr(H_enc), _ptr(H_dec),
+        _ptr(workspace), workspace.numel() * workspace.element_size(), _stream(stream)))
+
+
+def attn_encoder_decoder_bwd(s: LstmShape, src_ids, tgt_ids, src_lens, enc_W, dec_W, H_enc, H_dec,
+                             dH_enc, dH_dec, dW_enc, db_enc, dW_dec, db_dec, dE_src, dE_tgt,
+                             workspace, stream=None):
+    src, src_p = _i32(src_lens)
+    _check(lib().attn_encoder_decoder_bwd(
+        ctypes.byref(s), _ptr(src_ids), _ptr(tgt_ids), src_p, _ptrs(enc_W), _ptrs(dec_W),
+        _ptr(H_enc), _ptr(H_dec), _ptr(dH_enc), _ptr(dH_dec), _ptrs(dW_enc), _ptrs(db_enc),
+        _ptrs(dW_dec), _ptrs(db_dec), _ptr(dE_src), _ptr(dE_tgt), _ptr(workspace),
         workspace.numel() * workspace.element_size(), _stream(stream)))

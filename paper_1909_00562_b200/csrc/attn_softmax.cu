@@ -2083,6 +2083,23 @@ attn_status_t attn_internal_step_attention(int B, int M, int d, const void* h, c
   return launch_tc_group<__nv_bfloat16>(&g, 1, next_counter_fn(&cctx), stream, PAIR_FWD);
 }
 
+// Internal entry for lstm.cu's backward (NEXT-3 training): C[M][N] fp32 =
+// A^T [B0 | B1] with A [K][M], B0 [K][n0], B1 [K][N - n0] row-major bf16 (both
+// operands MN-major): dW_l = dz^T [x | h_prev] over all B T rows.  `counter`
+// is a zeroed int of the caller's workspace.
+attn_status_t attn_internal_gemm_atb(int M, int N, int K, const void* A, const void* B0, int n0,
+                                     const void* B1, float* C, int* counter, cudaStream_t stream) {
+  OPT_LOCK;
+  GemmDesc g;
+  g.M = M; g.N = N; g.K = K;
+  g.a_mn = 1; g.a0 = mnmaj(A, K, M, M);
+  g.b_mn = 1; g.b0 = mnmaj(B0, K, n0, n0);
+  g.b1 = mnmaj(B1, K, N - n0, N - n0); g.b_nsplit = n0;
+  g.epi.kind = EPI_STORE_F32; g.epi.out = C; g.epi.ldo = N;
+  g.epi.ncols_valid = N; g.epi.ncols_store = N;
+  return launch_tc_group<__nv_bfloat16>(&g, 1, counter, stream, 0);
+}
+
 extern "C" attn_status_t attn_softmax_decode_step(
     const attn_shape_t* s, const void* H_dec, const void* H_enc, const int32_t* src_lens_host,
     const void* W_c, const void* W_out, const void* W_alpha, const void* b_out, int k,

@@ -64,6 +64,8 @@ struct LsLayer {
   const float* c0;          // initial c [B][hd] (decoder) or NULL (zero)
   __nv_bfloat16* h_cap;     // [B][hd]: h at step cap[b] (encoder) or NULL
   float* c_cap;             // [B][hd]: c at step cap[b]
+  __nv_bfloat16* gates_seq; // training: [B][T][4hd] post-activation i, f, g, o (packed order) or NULL
+  float* c_seq;             // training: [B][T][hd] c_t
   int in;                   // input width (embedding size for layer 0, else hd)
 };
 
@@ -227,7 +229,7 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_wavefront_kernel(const __g
         tmem_ld32(tq + acc * P.ntile + cc * 32, v);
         const int u0 = u_base + cc * 8;
         const float4* b4 = reinterpret_cast<const float4*>(Ly.bias + 4 * u0);
-        float hc[8], cn[8];
+        float hc[8], cn[8], ga[32];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const float4 bb = __ldg(b4 + k);
@@ -235,8 +237,26 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_wavefront_kernel(const __g
           const float gf = ls_sigmoid(v[4 * k + 1] + bb.y);
           const float gg = ls_tanh(v[4 * k + 2] + bb.z);
           const float go = ls_sigmoid(v[4 * k + 3] + bb.w);
+          ga[4 * k] = gi; ga[4 * k + 1] = gf; ga[4 * k + 2] = gg; ga[4 * k + 3] = go;
           cn[k] = fmaf(gf, cp[cc][k], gi * gg);
           hc[k] = go * ls_tanh(cn[k]);
+        }
+        if (row_ok && Ly.gates_seq) {
+          // training: the cell's activations (packed gate order) and c_t for the backward
+          uint4* gdst = reinterpret_cast<uint4*>(Ly.gates_seq + ((size_t)r * P.T + t) * 4 * P.hd + 4 * u0);
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(ga[8 * q4 + 2 * e], ga[8 * q4 + 2 * e + 1]);
+              w[e] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            gdst[q4] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+          float4* cs = reinterpret_cast<float4*>(Ly.c_seq + ((size_t)r * P.T + t) * P.hd + u0);
+          cs[0] = make_float4(cn[0], cn[1], cn[2], cn[3]);
+          cs[1] = make_float4(cn[4], cn[5], cn[6], cn[7]);
         }
         if (row_ok) {
           float4* cdst = reinterpret_cast<float4*>(Ly.c + (size_t)r * P.hd + u0);
@@ -326,8 +346,347 @@ __global__ void if_input_kernel(const int* __restrict__ ids, int N, int t,
   }
 }
 
+// ============================================================== backward (NEXT-3 training)
+// The reverse wavefront ("the alternation ... on the backward
+// process goes in a similar but opposite direction"): layer-step (l, t)
+// needs (l+1, t) (the gradient w.r.t. its output h_t, from the layer above)
+// and (l, t+1) (W_hh^T dz of the later step and the cell-state carry), so
+// the top layer starts at t = T-1 and the others follow.  One cooperative
+// launch per side, CTA (l, g) again owning units [32 g, 32 g + 32) of layer
+// l.  Per step:
+//   E  (8 epilogue warps, thread = batch row, 16 units each): the cell's
+//      backward from the saved activations (i, f, g, o bf16, c fp32) --
+//      dc = dc_next + dh o (1 - tanh^2 c_t), dz = [dc g i(1-i), dc c_{t-1}
+//      f(1-f), dc i (1-g^2), dh tanh(c_t) o(1-o)], dc_next = dc f -- dz
+//      written bf16 (packed gate order) into dG_l [B][T][4hd]; publish.
+//   G  once every CTA of the layer has published step t: the CTA's 64-column
+//      slices of [dx_t | dh_{t-1}] = dz_t W_l (M = B rows, K = 4hd, N = 64;
+//      dz K-major, W_l as the MN-major B), fp32 into dx_out [B][T][in] (the
+//      layer below's upstream gradient, or the embeddings') and dh_rec
+//      [2][B][hd]; publish.
+// dW_l = sum_t dz_t^T [x_t | h_{t-1}] and db_l are one large GEMM / column
+// sum after the kernel (attn_encoder_decoder_bwd).
+struct LbLayer {
+  CUtensorMap m_dg;            // dG_l [B][T][4hd] bf16, box {64, 1, 128}
+  CUtensorMap m_w;             // W_l packed [4hd][in + hd] bf16, box {64 cols, 64 rows} (MN-major B)
+  __nv_bfloat16* dg;           // dG_l
+  const __nv_bfloat16* gates;  // saved activations [B][T][4hd]
+  const float* c_seq;          // saved c_t [B][T][hd]
+  const float* c0;             // initial c [B][hd] or NULL (zero)
+  const __nv_bfloat16* dh_top; // top layer: dL/dh_t [B][T][hd] bf16 (the stage's dH_enc / dH_dec)
+  const float* dx_above;       // other layers: layer l+1's dx_out [B][T][hd]
+  float* dx_out;               // dL/dx_t of this layer's input [B][T][in] fp32
+  float* dh_rec;               // [2][B][hd] fp32: (W_hh^T dz_{t+1}) for step t
+  float* dh0_out;              // [B][hd] gradient w.r.t. the initial state (decoder) or NULL
+  float* dc0_out;
+  const float* inj_dh;         // encoder: the decoder's initial-state gradient of this layer, added at
+  const float* inj_dc;         //   t = cap[b] (or NULL)
+  int in;
+};
+struct alignas(64) LbParams {
+  LbLayer layer[LS_MAXL];
+  int L, B, T, hd, G;
+  const int* cap;              // [B] (encoder) or NULL
+  unsigned* dgdone;            // [L][T] CTAs that wrote dz of (l, t)
+  unsigned* outdone;           // [L][T] CTAs that stored their [dx | dh] slices of (l, t)
+};
+
+constexpr int LB_STAGE = 24 * 1024;   // dz block 16 KB + W block 8 KB
+constexpr int LB_STAGES = 8;
+constexpr int LB_SMEM = LB_STAGES * LB_STAGE + 1024 + 512;
+
+__global__ void __launch_bounds__(LS_THREADS, 1) lstm_bwd_kernel(const __grid_constant__ LbParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + LB_STAGES * LB_STAGE);
+  uint64_t* full = bars;
+  uint64_t* empty = full + LB_STAGES;
+  uint64_t* tfull = empty + LB_STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const uint32_t warp = warp_id_uniform();
+  const uint32_t lane = lane_id();
+  const int l = blockIdx.x / P.G, g = blockIdx.x % P.G;
+  const LbLayer& Ly = P.layer[l];
+  const int hd = P.hd, T = P.T, U = hd / P.G;
+  const int nsl = (Ly.in + hd) / 64;           // 64-column output slices of the layer
+  const int kb_n = 4 * hd / 64;                // k-blocks (gate columns)
+  if (warp == 8) {
+    if (lane == 0) {
+      for (int i = 0; i < LB_STAGES; ++i) {
+        mbar_init(&full[i], 1);
+        mbar_init(&empty[i], 1);
+      }
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&tfull[i], 1);
+        mbar_init(&tempty[i], 8);
+      }
+      fence_barrier_init();
+      tma_prefetch_desc(&Ly.m_dg);
+      tma_prefetch_desc(&Ly.m_w);
+    }
+    __syncwarp();
+    tmem_alloc(tmem_slot, 128);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 8) {
+    // ---------------- TMA producer: per step, this CTA's slices x 4hd / 64 k-blocks
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = T - 1; t >= 0; --t) {
+      bool first = true;
+      for (int sl = g; sl < nsl; sl += P.G) {
+        for (int kb = 0; kb < kb_n; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (lane == 0) {
+            uint8_t* st = ring + s * LB_STAGE;
+            mbar_arrive_expect_tx(&full[s], LB_STAGE);
+            tma_load_2d(st + 16384, &Ly.m_w, &full[s], sl * 64, kb * 64);
+            if (first) {   // dz of step t: every CTA of the layer has written its units
+              ls_wait_geq(P.dgdone + (size_t)l * T + t, (unsigned)P.G);
+              fence_proxy_async_global();
+              first = false;
+            }
+            tma_load_3d(st, &Ly.m_dg, &full[s], kb * 64, t, 0);
+          }
+          __syncwarp();
+          if (++s == LB_STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ---------------- MMA issuer: out[128, 64] = dz_t (K-major) x W_l[:, slice] (MN-major)
+    int s = 0;
+    uint32_t ph = 0;
+    int n = 0;
+    const uint32_t idesc = umma_idesc_bf16(128, 64, 0, 1);
+    for (int t = T - 1; t >= 0; --t) {
+      for (int sl = g; sl < nsl; sl += P.G, ++n) {
+        const int acc = n & 1, use = n >> 1;
+        if (use > 0) mbar_wait(&tempty[acc], (use - 1) & 1);
+        tc_fence_after();
+        for (int kb = 0; kb < kb_n; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sa = smem_u32(ring + s * LB_STAGE);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              umma_bf16(tmem_base + acc * 64, umma_sdesc(sa + k * 32, 16, 1024),
+                        umma_sdesc(sa + 16384 + k * 2048, 16, 1024), idesc, (kb | k) ? 1u : 0u);
+            umma_commit(&empty[s]);
+          }
+          __syncwarp();
+          if (++s == LB_STAGES) { s = 0; ph ^= 1; }
+        }
+        if (elect_one()) umma_commit(&tfull[acc]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- cell backward (E) and the slices' epilogue (G), warps 0-7
+    const uint32_t q = warp & 3, hh = warp >> 2;
+    const int r = (int)(q * 32 + lane);
+    const bool row_ok = r < P.B;
+    const int rr = row_ok ? r : 0;
+    const int u_base = g * U + (int)hh * (U / 2);   // 16 units per thread (U = 32)
+    const int nu = U / 2;
+    const int cap = (P.cap && row_ok) ? P.cap[r] : -1;
+    float dcc[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) dcc[k] = 0.f;
+    int n = 0;
+    for (int t = T - 1; t >= 0; --t) {
+      // ---- E: wait for the gradient w.r.t. h_t (layer above) and W_hh^T dz_{t+1} (own layer)
+      if (threadIdx.x == 0) {
+        if (l < P.L - 1) ls_wait_geq(P.outdone + (size_t)(l + 1) * T + t, (unsigned)P.G);
+        if (t < T - 1) ls_wait_geq(P.outdone + (size_t)l * T + t + 1, (unsigned)P.G);
+        __threadfence();
+      }
+      named_bar_sync(1, 256);
+      if (row_ok) {
+        for (int k0 = 0; k0 < nu; k0 += 8) {
+          const int u0 = u_base + k0;
+          float dh[8], cp[8], ct[8];
+          if (Ly.dh_top) {
+            const uint4 hv = *reinterpret_cast<const uint4*>(Ly.dh_top + ((size_t)r * T + t) * hd + u0);
+            const uint32_t w4[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
+              dh[2 * e] = f2.x;
+              dh[2 * e + 1] = f2.y;
+            }
+          } else {
+            const float4* a4 = reinterpret_cast<const float4*>(Ly.dx_above + ((size_t)r * T + t) * hd + u0);
+            const float4 a = __ldcg(a4), b = __ldcg(a4 + 1);
+            dh[0] = a.x; dh[1] = a.y; dh[2] = a.z; dh[3] = a.w; dh[4] = b.x; dh[5] = b.y; dh[6] = b.z; dh[7] = b.w;
+          }
+          if (t < T - 1) {
+            const float4* a4 = reinterpret_cast<const float4*>(Ly.dh_rec + ((size_t)((t + 1) & 1) * P.B + r) * hd + u0);
+            const float4 a = __ldcg(a4), b = __ldcg(a4 + 1);
+            dh[0] += a.x; dh[1] += a.y; dh[2] += a.z; dh[3] += a.w; dh[4] += b.x; dh[5] += b.y; dh[6] += b.z; dh[7] += b.w;
+          }
+          if (t == cap && Ly.inj_dh) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              dh[k] += Ly.inj_dh[(size_t)r * hd + u0 + k];
+              dcc[k0 + k] += Ly.inj_dc[(size_t)r * hd + u0 + k];
+            }
+          }
+          const float4* c4 = reinterpret_cast<const float4*>(Ly.c_seq + ((size_t)r * T + t) * hd + u0);
+          {
+            const float4 a = c4[0], b = c4[1];
+            ct[0] = a.x; ct[1] = a.y; ct[2] = a.z; ct[3] = a.w; ct[4] = b.x; ct[5] = b.y; ct[6] = b.z; ct[7] = b.w;
+          }
+          if (t > 0) {
+            const float4* p4 = reinterpret_cast<const float4*>(Ly.c_seq + ((size_t)r * T + t - 1) * hd + u0);
+            const float4 a = p4[0], b = p4[1];
+            cp[0] = a.x; cp[1] = a.y; cp[2] = a.z; cp[3] = a.w; cp[4] = b.x; cp[5] = b.y; cp[6] = b.z; cp[7] = b.w;
+          } else if (Ly.c0) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) cp[k] = Ly.c0[(size_t)r * hd + u0 + k];
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) cp[k] = 0.f;
+          }
+          // saved activations of these 8 units: 32 bf16 in packed order (4u + q)
+          const uint4* g4 = reinterpret_cast<const uint4*>(Ly.gates + ((size_t)r * T + t) * 4 * hd + 4 * u0);
+          float ga[32];
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const uint4 gv = g4[q4];
+            const uint32_t w4[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
+              ga[8 * q4 + 2 * e] = f2.x;
+              ga[8 * q4 + 2 * e + 1] = f2.y;
+            }
+          }
+          float dz[32];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float gi = ga[4 * k], gf = ga[4 * k + 1], gg = ga[4 * k + 2], go = ga[4 * k + 3];
+            const float tc = tanhf(ct[k]);
+            const float dc = dcc[k0 + k] + dh[k] * go * (1.f - tc * tc);
+            dz[4 * k] = dc * gg * gi * (1.f - gi);
+            dz[4 * k + 1] = dc * cp[k] * gf * (1.f - gf);
+            dz[4 * k + 2] = dc * gi * (1.f - gg * gg);
+            dz[4 * k + 3] = dh[k] * tc * go * (1.f - go);
+            dcc[k0 + k] = dc * gf;
+          }
+          uint4* zd = reinterpret_cast<uint4*>(Ly.dg + ((size_t)r * T + t) * 4 * hd + 4 * u0);
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(dz[8 * q4 + 2 * e], dz[8 * q4 + 2 * e + 1]);
+              w[e] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            zd[q4] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+      named_bar_sync(1, 256);
+      if (threadIdx.x == 0) {
+        __threadfence();
+        red_release_gpu_add(P.dgdone + (size_t)l * T + t, 1u);
+      }
+      // ---- G epilogue: this CTA's slices of [dx_t | dh_{t-1}] (fp32)
+      for (int sl = g; sl < nsl; sl += P.G, ++n) {
+        const int acc = n & 1, use = n >> 1;
+        mbar_wait(&tfull[acc], use & 1);
+        tc_fence_after();
+        float v[32];
+        tmem_ld32(tmem_base + ((q * 32u) << 16) + acc * 64 + hh * 32, v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        const int col = sl * 64 + (int)hh * 32;
+        if (row_ok) {
+          float* dst = col < Ly.in ? Ly.dx_out + ((size_t)r * T + t) * Ly.in + col
+                                   : Ly.dh_rec + ((size_t)(t & 1) * P.B + r) * hd + (col - Ly.in);
+          float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) d4[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+        }
+      }
+      named_bar_sync(1, 256);
+      if (threadIdx.x == 0) {
+        __threadfence();
+        red_release_gpu_add(P.outdone + (size_t)l * T + t, 1u);
+      }
+    }
+    // initial-state gradients: dh_{-1} = the h part of step 0's product (all CTAs), dc carry
+    if (Ly.dh0_out) {
+      if (threadIdx.x == 0) {
+        ls_wait_geq(P.outdone + (size_t)l * T, (unsigned)P.G);
+        __threadfence();
+      }
+      named_bar_sync(1, 256);
+      if (row_ok)
+        for (int k = 0; k < nu; ++k) {
+          Ly.dh0_out[(size_t)r * hd + u_base + k] = __ldcg(Ly.dh_rec + (size_t)r * hd + u_base + k);
+          Ly.dc0_out[(size_t)r * hd + u_base + k] = dcc[k];
+        }
+    }
+    (void)rr;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 8) tmem_dealloc(tmem_base, 128);
+}
+
+// dX0 rows scattered into the embedding gradient: dE[ids[b][t]] += dX0[b][t]
+// (fp32 atomics: the summation order over repeated ids is not fixed)
+__global__ void embed_grad_kernel(const int* __restrict__ ids, const float* __restrict__ dX, int e,
+                                  long long rows, float* __restrict__ dE) {
+  const long long n = rows * e;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long row = i / e;
+    atomicAdd(dE + (long long)ids[row] * e + (i % e), dX[i]);
+  }
+}
+// Hprev[b][t] = t > 0 ? H[b][t-1] : h0[b] (zero when h0 is NULL), bf16, 16-byte vectors
+__global__ void shift_h_kernel(const __nv_bfloat16* __restrict__ H, const __nv_bfloat16* __restrict__ h0,
+                               int B, int T, int hd, __nv_bfloat16* __restrict__ Hp) {
+  const int v8 = hd / 8;
+  const long long n = (long long)B * T * v8;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long row = i / v8;
+    const int k = (int)(i % v8);
+    const int b = (int)(row / T), t = (int)(row % T);
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (t > 0) v = reinterpret_cast<const uint4*>(H)[(row - 1) * v8 + k];
+    else if (h0) v = reinterpret_cast<const uint4*>(h0)[(long long)b * v8 + k];
+    reinterpret_cast<uint4*>(Hp)[i] = v;
+  }
+}
+// db[j] = sum over rows of dG[row][j] (fixed order per column)
+__global__ void colsum_bf16_kernel(const __nv_bfloat16* __restrict__ dG, long long rows, int cols,
+                                   float* __restrict__ db) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  float s = 0.f;
+  for (long long r = 0; r < rows; ++r) s += __bfloat162float(dG[r * cols + j]);
+  db[j] = s;
+}
+
 }  // namespace attnsm
 
+// internal entry of attn_softmax.cu: C = A^T [B0 | B1] on the tcgen05 engine (dW of the backward)
+attn_status_t attn_internal_gemm_atb(int M, int N, int K, const void* A, const void* B0, int n0,
+                                     const void* B1, float* C, int* counter, cudaStream_t stream);
 // internal entry of attn_softmax.cu: one step of Eqs. 1-4 for the IF decoder
 size_t attn_internal_step_ws(int B, int M, int d);
 attn_status_t attn_internal_step_attention(int B, int M, int d, const void* h, const void* S,
@@ -476,6 +835,8 @@ struct RunCfg {
   const float* c0[LS_MAXL];
   void* hcap[LS_MAXL];            // capture at cap_dev[b] (or NULL)
   float* ccap[LS_MAXL];
+  void* gates_seq[LS_MAXL];       // training saves (or NULL)
+  float* c_seq[LS_MAXL];
   const int* cap_dev;
   unsigned* done;                 // [L][T], zeroed here
 };
@@ -502,6 +863,8 @@ attn_status_t run_layers(const RunCfg& R, cudaStream_t st) {
     Ly.c0 = R.c0[l];
     Ly.h_cap = static_cast<__nv_bfloat16*>(R.hcap[l]);
     Ly.c_cap = R.ccap[l];
+    Ly.gates_seq = static_cast<__nv_bfloat16*>(R.gates_seq[l]);
+    Ly.c_seq = R.c_seq[l];
   }
   P.L = L; P.B = B; P.T = T; P.hd = hd; P.G = R.G; P.ntile = R.ntile;
   P.has_init = R.h0[0] ? 1 : 0;
@@ -711,5 +1074,259 @@ extern "C" attn_status_t attn_encoder_decoder_if_fwd(
                                           (long long)N * hd, ws + q.attn, st)) != ATTN_OK)
       return r;
   }
+  return ATTN_OK;
+}
+
+// ---------------------------------------------------------------- training (forward saves + backward)
+namespace {
+struct TrPlan {
+  size_t inter_enc, inter_dec, gates_enc, gates_dec, cseq_enc, cseq_dec;   // forward saves
+  size_t dg, dxo, dhrec, dh0, dc0, hprev, flags, counter, total;
+};
+TrPlan plan_train(const attn_lstm_shape_t* s, const LsPlan& base) {
+  TrPlan q;
+  const size_t B = s->batch, M = s->src_len, N = s->tgt_len, hd = s->hidden, L = s->layers;
+  const size_t Tm = std::max(M, N), w0 = std::max<size_t>(s->emb, hd);
+  size_t o = base.total;
+  auto take = [&](size_t b) { size_t r = o; o += al(b); return r; };
+  q.inter_enc = take(std::max<size_t>(L - 1, 1) * B * M * hd * 2);
+  q.inter_dec = take(std::max<size_t>(L - 1, 1) * B * N * hd * 2);
+  q.gates_enc = take(L * B * M * 4 * hd * 2);
+  q.gates_dec = take(L * B * N * 4 * hd * 2);
+  q.cseq_enc = take(L * B * M * hd * 4);
+  q.cseq_dec = take(L * B * N * hd * 4);
+  q.dg = take(L * B * Tm * 4 * hd * 2);
+  q.dxo = take(L * B * Tm * w0 * 4);
+  q.dhrec = take(L * 2 * B * hd * 4);
+  q.dh0 = take(L * B * hd * 4);
+  q.dc0 = take(L * B * hd * 4);
+  q.hprev = take(B * Tm * hd * 2);
+  q.flags = take(2 * L * Tm * 4);
+  q.counter = take(256);
+  q.total = o;
+  return q;
+}
+
+// forward of one side with the training saves (separate intermediates per side)
+attn_status_t run_side_train(const attn_lstm_shape_t* s, const LsPlan& p, const TrPlan& q, bool decoder,
+                             const void* X0, const void* const* W, const float* const* b, void* H_top,
+                             char* ws, const int* cap_dev, cudaStream_t st) {
+  RunCfg R;
+  memset(&R, 0, sizeof(R));
+  const int B = s->batch, hd = s->hidden, L = s->layers, T = decoder ? s->tgt_len : s->src_len;
+  R.B = B; R.T = T; R.hd = hd; R.L = L; R.G = p.G; R.ntile = p.ntile; R.in0 = s->emb;
+  R.X0 = X0; R.W = W; R.b = b; R.cap_dev = decoder ? nullptr : cap_dev;
+  R.done = reinterpret_cast<unsigned*>(ws + (decoder ? p.done_dec : p.done_enc));
+  __nv_bfloat16* inter = reinterpret_cast<__nv_bfloat16*>(ws + (decoder ? q.inter_dec : q.inter_enc));
+  __nv_bfloat16* gates = reinterpret_cast<__nv_bfloat16*>(ws + (decoder ? q.gates_dec : q.gates_enc));
+  float* cseq = reinterpret_cast<float*>(ws + (decoder ? q.cseq_dec : q.cseq_enc));
+  for (int l = 0; l < L; ++l) {
+    R.hout[l] = l == L - 1 ? H_top : (void*)(inter + (size_t)l * B * T * hd);
+    R.c[l] = reinterpret_cast<float*>(ws + p.c) + (size_t)l * B * hd;
+    __nv_bfloat16* hcap = reinterpret_cast<__nv_bfloat16*>(ws + p.hcap) + (size_t)l * B * hd;
+    float* ccap = reinterpret_cast<float*>(ws + p.ccap) + (size_t)l * B * hd;
+    R.h0[l] = decoder ? hcap : nullptr;
+    R.c0[l] = decoder ? ccap : nullptr;
+    R.hcap[l] = decoder ? nullptr : hcap;
+    R.ccap[l] = decoder ? nullptr : ccap;
+    R.gates_seq[l] = gates + (size_t)l * B * T * 4 * hd;
+    R.c_seq[l] = cseq + (size_t)l * B * T * hd;
+  }
+  return run_layers(R, st);
+}
+
+attn_status_t check_common(const attn_lstm_shape_t* s, const int32_t* src_lens_host, size_t need,
+                           size_t have, const LsPlan& p) {
+  for (int i = 0; i < s->batch; ++i)
+    if (src_lens_host[i] < 1 || src_lens_host[i] > s->src_len)
+      return lfail(ATTN_ERR_SHAPE, "src_lens_host[%d] = %d outside [1, M = %d]", i, src_lens_host[i], s->src_len);
+  if (have < need) return lfail(ATTN_ERR_WORKSPACE, "workspace_bytes = %zu < required %zu", have, need);
+  int dev = 0, sms = 0;
+  LS_CUDA(cudaGetDevice(&dev));
+  LS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (s->layers * p.G > sms)
+    return lfail(ATTN_ERR_UNSUPPORTED, "lstm: %d layers x %d CTAs exceed the %d SMs", s->layers, p.G, sms);
+  return ATTN_OK;
+}
+
+// the reverse wavefront of one side
+attn_status_t run_bwd_side(const attn_lstm_shape_t* s, const LsPlan& p, const TrPlan& q, bool decoder,
+                           const void* const* W, const void* dH_top, char* ws, const int* cap_dev,
+                           cudaStream_t st) {
+  static LbParams P;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  memset(&P, 0, sizeof(P));
+  const int B = s->batch, hd = s->hidden, L = s->layers, T = decoder ? s->tgt_len : s->src_len;
+  const size_t w0 = std::max(s->emb, hd);
+  attn_status_t r;
+  __nv_bfloat16* dg = reinterpret_cast<__nv_bfloat16*>(ws + q.dg);
+  float* dxo = reinterpret_cast<float*>(ws + q.dxo);
+  float* dhrec = reinterpret_cast<float*>(ws + q.dhrec);
+  __nv_bfloat16* gates = reinterpret_cast<__nv_bfloat16*>(ws + (decoder ? q.gates_dec : q.gates_enc));
+  float* cseq = reinterpret_cast<float*>(ws + (decoder ? q.cseq_dec : q.cseq_enc));
+  float* ccap = reinterpret_cast<float*>(ws + p.ccap);
+  float* dh0 = reinterpret_cast<float*>(ws + q.dh0);
+  float* dc0 = reinterpret_cast<float*>(ws + q.dc0);
+  for (int l = 0; l < L; ++l) {
+    LbLayer& Ly = P.layer[l];
+    Ly.in = l == 0 ? s->emb : hd;
+    Ly.dg = dg + (size_t)l * B * T * 4 * hd;
+    {
+      cuuint64_t dims[3] = {(cuuint64_t)(4 * hd), (cuuint64_t)T, (cuuint64_t)B};
+      cuuint64_t str[2] = {(cuuint64_t)(4 * hd) * 2, (cuuint64_t)(4 * hd) * 2 * T};
+      cuuint32_t box[3] = {64, 1, 128};
+      if ((r = map_bf16(&Ly.m_dg, Ly.dg, 3, dims, str, box)) != ATTN_OK) return r;
+    }
+    if ((r = map_mat(&Ly.m_w, W[l], Ly.in + hd, 4 * hd, 64)) != ATTN_OK) return r;
+    Ly.gates = gates + (size_t)l * B * T * 4 * hd;
+    Ly.c_seq = cseq + (size_t)l * B * T * hd;
+    Ly.c0 = decoder ? ccap + (size_t)l * B * hd : nullptr;
+    Ly.dh_top = l == L - 1 ? static_cast<const __nv_bfloat16*>(dH_top) : nullptr;
+    Ly.dx_above = l == L - 1 ? nullptr : dxo + (size_t)(l + 1) * B * T * w0;
+    Ly.dx_out = dxo + (size_t)l * B * T * w0;
+    Ly.dh_rec = dhrec + (size_t)l * 2 * B * hd;
+    Ly.dh0_out = decoder ? dh0 + (size_t)l * B * hd : nullptr;
+    Ly.dc0_out = decoder ? dc0 + (size_t)l * B * hd : nullptr;
+    Ly.inj_dh = decoder ? nullptr : dh0 + (size_t)l * B * hd;
+    Ly.inj_dc = decoder ? nullptr : dc0 + (size_t)l * B * hd;
+  }
+  P.L = L; P.B = B; P.T = T; P.hd = hd; P.G = p.G;
+  P.cap = decoder ? nullptr : cap_dev;
+  unsigned* flags = reinterpret_cast<unsigned*>(ws + q.flags);
+  P.dgdone = flags;
+  P.outdone = flags + (size_t)L * T;
+  LS_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned) * 2 * (size_t)L * T, st));
+  static std::vector<int> attr_set;
+  int dev = 0;
+  LS_CUDA(cudaGetDevice(&dev));
+  if (std::find(attr_set.begin(), attr_set.end(), dev) == attr_set.end()) {
+    LS_CUDA(cudaFuncSetAttribute(lstm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LB_SMEM));
+    attr_set.push_back(dev);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(L * p.G);
+  cfg.blockDim = dim3(LS_THREADS);
+  cfg.dynamicSmemBytes = LB_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LS_CUDA(cudaLaunchKernelEx(&cfg, lstm_bwd_kernel, P));
+  return ATTN_OK;
+}
+
+// dW_l = dz^T [x | h_prev], db_l = column sums of dz, for every layer of one side
+attn_status_t side_weight_grads(const attn_lstm_shape_t* s, const LsPlan& p, const TrPlan& q, bool decoder,
+                                const void* X0, const void* H_top, float* const* dW, float* const* db,
+                                char* ws, int sms, cudaStream_t st) {
+  const int B = s->batch, hd = s->hidden, L = s->layers, T = decoder ? s->tgt_len : s->src_len;
+  const long long rows = (long long)B * T;
+  __nv_bfloat16* dg = reinterpret_cast<__nv_bfloat16*>(ws + q.dg);
+  __nv_bfloat16* inter = reinterpret_cast<__nv_bfloat16*>(ws + (decoder ? q.inter_dec : q.inter_enc));
+  __nv_bfloat16* hprev = reinterpret_cast<__nv_bfloat16*>(ws + q.hprev);
+  const __nv_bfloat16* hcap = reinterpret_cast<const __nv_bfloat16*>(ws + p.hcap);
+  int* counter = reinterpret_cast<int*>(ws + q.counter);
+  attn_status_t r;
+  for (int l = 0; l < L; ++l) {
+    const int in = l == 0 ? s->emb : hd;
+    const void* X = l == 0 ? X0 : (const void*)(inter + (size_t)(l - 1) * B * T * hd);
+    const void* Hl = l == L - 1 ? H_top : (const void*)(inter + (size_t)l * B * T * hd);
+    shift_h_kernel<<<sms * 4, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(Hl),
+                                            decoder ? hcap + (size_t)l * B * hd : nullptr, B, T, hd, hprev);
+    LS_CUDA(cudaGetLastError());
+    const __nv_bfloat16* dgl = dg + (size_t)l * B * T * 4 * hd;
+    LS_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
+    if ((r = attn_internal_gemm_atb(4 * hd, in + hd, (int)rows, dgl, X, in, hprev, dW[l], counter, st)) != ATTN_OK)
+      return r;
+    colsum_bf16_kernel<<<(4 * hd + 255) / 256, 256, 0, st>>>(dgl, rows, 4 * hd, db[l]);
+    LS_CUDA(cudaGetLastError());
+  }
+  return ATTN_OK;
+}
+}  // namespace
+
+extern "C" size_t attn_lstm_train_workspace_size(const attn_lstm_shape_t* s) {
+  if (check_lstm(s) != ATTN_OK) return 0;
+  const LsPlan p = plan_lstm(s);
+  return plan_train(s, p).total;
+}
+
+extern "C" attn_status_t attn_encoder_decoder_fwd_train(
+    const attn_lstm_shape_t* s, const int32_t* src_ids, const int32_t* tgt_ids,
+    const int32_t* src_lens_host, const void* E_src, const void* E_tgt,
+    const void* const* enc_W, const float* const* enc_b, const void* const* dec_W,
+    const float* const* dec_b, void* H_enc, void* H_dec, void* workspace, size_t workspace_bytes,
+    void* stream) {
+  attn_status_t r = check_lstm(s);
+  if (r != ATTN_OK) return r;
+  if (!src_ids || !tgt_ids || !src_lens_host || !E_src || !E_tgt || !enc_W || !enc_b || !dec_W ||
+      !dec_b || !H_enc || !H_dec || !workspace)
+    return lfail(ATTN_ERR_INVALID_ARG, "encoder_decoder_fwd_train: NULL argument");
+  const LsPlan p = plan_lstm(s);
+  const TrPlan q = plan_train(s, p);
+  if ((r = check_common(s, src_lens_host, q.total, workspace_bytes, p)) != ATTN_OK) return r;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = static_cast<char*>(workspace);
+  const int B = s->batch, M = s->src_len, N = s->tgt_len, e = s->emb;
+  int sms = 0, dev = 0;
+  LS_CUDA(cudaGetDevice(&dev));
+  LS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  std::vector<int> cap(B);
+  for (int i = 0; i < B; ++i) cap[i] = src_lens_host[i] - 1;
+  int* cap_dev = reinterpret_cast<int*>(ws + p.lens);
+  LS_CUDA(cudaMemcpyAsync(cap_dev, cap.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
+  __nv_bfloat16* Xs = reinterpret_cast<__nv_bfloat16*>(ws + p.xs);
+  __nv_bfloat16* Xt = reinterpret_cast<__nv_bfloat16*>(ws + p.xt);
+  embed_kernel<<<sms * 4, 256, 0, st>>>(src_ids, static_cast<const __nv_bfloat16*>(E_src), e, (long long)B * M, Xs);
+  LS_CUDA(cudaGetLastError());
+  embed_kernel<<<sms * 4, 256, 0, st>>>(tgt_ids, static_cast<const __nv_bfloat16*>(E_tgt), e, (long long)B * N, Xt);
+  LS_CUDA(cudaGetLastError());
+  if ((r = run_side_train(s, p, q, false, Xs, enc_W, enc_b, H_enc, ws, cap_dev, st)) != ATTN_OK) return r;
+  return run_side_train(s, p, q, true, Xt, dec_W, dec_b, H_dec, ws, cap_dev, st);
+}
+
+extern "C" attn_status_t attn_encoder_decoder_bwd(
+    const attn_lstm_shape_t* s, const int32_t* src_ids, const int32_t* tgt_ids,
+    const int32_t* src_lens_host, const void* const* enc_W, const void* const* dec_W,
+    const void* H_enc, const void* H_dec, const void* dH_enc, const void* dH_dec,
+    float* const* dW_enc, float* const* db_enc, float* const* dW_dec, float* const* db_dec,
+    float* dE_src, float* dE_tgt, void* workspace, size_t workspace_bytes, void* stream) {
+  attn_status_t r = check_lstm(s);
+  if (r != ATTN_OK) return r;
+  if (!src_ids || !tgt_ids || !src_lens_host || !enc_W || !dec_W || !H_enc || !H_dec || !dH_enc ||
+      !dH_dec || !dW_enc || !db_enc || !dW_dec || !db_dec || !dE_src || !dE_tgt || !workspace)
+    return lfail(ATTN_ERR_INVALID_ARG, "encoder_decoder_bwd: NULL argument");
+  for (int l = 0; l < s->layers; ++l)
+    if (!enc_W[l] || !dec_W[l] || !dW_enc[l] || !db_enc[l] || !dW_dec[l] || !db_dec[l])
+      return lfail(ATTN_ERR_INVALID_ARG, "encoder_decoder_bwd: layer %d buffer is NULL", l);
+  const LsPlan p = plan_lstm(s);
+  const TrPlan q = plan_train(s, p);
+  if ((r = check_common(s, src_lens_host, q.total, workspace_bytes, p)) != ATTN_OK) return r;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = static_cast<char*>(workspace);
+  const int B = s->batch, M = s->src_len, N = s->tgt_len, e = s->emb;
+  int sms = 0, dev = 0;
+  LS_CUDA(cudaGetDevice(&dev));
+  LS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  std::vector<int> cap(B);
+  for (int i = 0; i < B; ++i) cap[i] = src_lens_host[i] - 1;
+  int* cap_dev = reinterpret_cast<int*>(ws + p.lens);
+  LS_CUDA(cudaMemcpyAsync(cap_dev, cap.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
+  float* dxo = reinterpret_cast<float*>(ws + q.dxo);
+  LS_CUDA(cudaMemsetAsync(dE_src, 0, sizeof(float) * (size_t)s->vocab_src * e, st));
+  LS_CUDA(cudaMemsetAsync(dE_tgt, 0, sizeof(float) * (size_t)s->vocab_tgt * e, st));
+  // decoder first: its initial-state gradients reach the encoder at src_len - 1
+  if ((r = run_bwd_side(s, p, q, true, dec_W, dH_dec, ws, cap_dev, st)) != ATTN_OK) return r;
+  if ((r = side_weight_grads(s, p, q, true, ws + p.xt, H_dec, dW_dec, db_dec, ws, sms, st)) != ATTN_OK) return r;
+  // layer 0's dx_out is dL/dx [B][N][e]: the target embeddings' rows
+  embed_grad_kernel<<<sms * 8, 256, 0, st>>>(tgt_ids, dxo, e, (long long)B * N, dE_tgt);
+  LS_CUDA(cudaGetLastError());
+  if ((r = run_bwd_side(s, p, q, false, enc_W, dH_enc, ws, cap_dev, st)) != ATTN_OK) return r;
+  if ((r = side_weight_grads(s, p, q, false, ws + p.xs, H_enc, dW_enc, db_enc, ws, sms, st)) != ATTN_OK) return r;
+  embed_grad_kernel<<<sms * 8, 256, 0, st>>>(src_ids, dxo, e, (long long)B * M, dE_src);
+  LS_CUDA(cudaGetLastError());
   return ATTN_OK;
 }

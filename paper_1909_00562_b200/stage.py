@@ -174,3 +174,49 @@ class EncoderDecoder:
                                          self.enc_W, self.enc_b, self.dec_W, self.dec_b,
                                          H_enc, H_dec, self.workspace, stream=stream)
         return H_enc, H_dec
+
+
+class EncoderDecoderTrainer(EncoderDecoder):
+    """NEXT-3 training: the encoder-decoder forward that keeps its activations
+    (attn_encoder_decoder_fwd_train) and the reverse-wavefront backward
+    (attn_encoder_decoder_bwd) that turns the stage's dH_enc / dH_dec into the
+    LSTM and embedding gradients.  dW / db come in the packed gate-interleaved
+    order of attn_lstm_pack_layer (unpack_lstm_grad gives PyTorch's layout)."""
+
+    def __init__(self, B, M, N, emb, hidden, layers, vocab_src, vocab_tgt, device=None):
+        super().__init__(B, M, N, emb, hidden, layers, vocab_src, vocab_tgt, device=device)
+        self.vocab_src, self.vocab_tgt = vocab_src, vocab_tgt
+        self.workspace = torch.empty(binding.attn_lstm_train_workspace_size(self.shape),
+                                     dtype=torch.uint8, device=self.device)
+
+    def forward(self, src_ids, tgt_ids, src_len, E_src, E_tgt, stream=None):
+        self.H_enc = torch.empty(self.B, self.M, self.hidden, dtype=torch.bfloat16, device=self.device)
+        self.H_dec = torch.empty(self.B, self.N, self.hidden, dtype=torch.bfloat16, device=self.device)
+        self.saved = (src_ids, tgt_ids, src_len)
+        binding.attn_encoder_decoder_fwd_train(self.shape, src_ids, tgt_ids, src_len, E_src, E_tgt,
+                                               self.enc_W, self.enc_b, self.dec_W, self.dec_b,
+                                               self.H_enc, self.H_dec, self.workspace, stream=stream)
+        return self.H_enc, self.H_dec
+
+    def backward(self, dH_enc, dH_dec, stream=None):
+        dev, L, hd = self.device, self.layers, self.hidden
+        mk = lambda l: torch.empty(4 * hd, (self.emb if l == 0 else hd) + hd, dtype=torch.float32, device=dev)
+        g = {"dW_enc": [mk(l) for l in range(L)], "dW_dec": [mk(l) for l in range(L)],
+             "db_enc": [torch.empty(4 * hd, device=dev) for _ in range(L)],
+             "db_dec": [torch.empty(4 * hd, device=dev) for _ in range(L)],
+             "dE_src": torch.empty(self.vocab_src, self.emb, device=dev),
+             "dE_tgt": torch.empty(self.vocab_tgt, self.emb, device=dev)}
+        src_ids, tgt_ids, src_len = self.saved
+        binding.attn_encoder_decoder_bwd(self.shape, src_ids, tgt_ids, src_len, self.enc_W, self.dec_W,
+                                         self.H_enc, self.H_dec, dH_enc, dH_dec, g["dW_enc"], g["db_enc"],
+                                         g["dW_dec"], g["db_dec"], g["dE_src"], g["dE_tgt"],
+                                         self.workspace, stream=stream)
+        return g
+
+
+def unpack_lstm_grad(dW_packed, db_packed, in_dim: int, hidden: int):
+    """Packed gate-interleaved (row 4u + q) -> PyTorch (W_ih [4h, in], W_hh [4h, h], b [4h])."""
+    K = dW_packed.shape[1]
+    W = dW_packed.reshape(hidden, 4, K).transpose(0, 1).reshape(4 * hidden, K)
+    b = db_packed.reshape(hidden, 4).transpose(0, 1).reshape(4 * hidden)
+    return W[:, :in_dim], W[:, in_dim:], b

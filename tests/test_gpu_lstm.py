@@ -134,3 +134,43 @@ def test_input_feeding_matches_oracle(cuda_lib, name, layers, emb):
         for got, ref, alt, nm in ((gd, H, H2, "H_dec"), (gt, Htl, Ht2, "Htilde")):
             bound = max(TOL, _rel(alt[:, t], ref[:, t]))
             assert _rel(got[:, t], ref[:, t]) <= bound, (nm, t, _rel(got[:, t], ref[:, t]), bound)
+
+
+@pytest.mark.parametrize("name,layers,emb", [("small", 2, 128), ("medium", 4, 256), ("paper", 4, 512)])
+def test_encoder_decoder_backward_matches_oracle(cuda_lib, name, layers, emb):
+    """NEXT-3 training: the reverse wavefront (attn_encoder_decoder_bwd) against
+    the fp64 BPTT oracle (pinned by torch autograd) for upstream gradients of
+    the stage's size on H_enc / H_dec: every layer's dW_ih, dW_hh, db and the
+    embedding gradients, rel-L2 <= 2e-2 each."""
+    from paper_1909_00562_b200.stage import EncoderDecoderTrainer, unpack_lstm_grad
+    cfg = CONFIGS[name]
+    inp = make_lstm_inputs(cfg, layers=layers, emb=emb)
+    dev = torch.device("cuda")
+    bf = lambda a: torch.from_numpy(np.asarray(a, np.float32)).to(dev, torch.bfloat16)
+    tr = EncoderDecoderTrainer(cfg.B, cfg.M, cfg.N, emb, cfg.d, layers, cfg.V, cfg.V)
+    tr.set_weights([tuple(bf(w) for w in ws) for ws in inp["enc"]],
+                   [tuple(bf(w) for w in ws) for ws in inp["dec"]])
+    src = torch.from_numpy(inp["src_ids"]).to(dev)
+    tgt = torch.from_numpy(inp["tgt_ids"]).to(dev)
+    tr.forward(src, tgt, inp["src_len"], bf(inp["E_src"]), bf(inp["E_tgt"]))
+    rng = np.random.default_rng(11)
+    scale = 1.0 / (cfg.B * cfg.N)   # the stage's gradients carry the 1 / tokens loss scale
+    dS = (rng.normal(size=(cfg.B, cfg.M, cfg.d)) * scale).astype(np.float32)
+    dH = (rng.normal(size=(cfg.B, cfg.N, cfg.d)) * scale).astype(np.float32)
+    dS_b, dH_b = bf(dS), bf(dH)
+    g = tr.backward(dS_b, dH_b)
+    torch.cuda.synchronize()
+    ref = LO.encoder_decoder_backward(inp["src_ids"], inp["tgt_ids"], inp["src_len"], inp["E_src"],
+                                      inp["E_tgt"], inp["enc"], inp["dec"],
+                                      dS_b.double().cpu().numpy(), dH_b.double().cpu().numpy())
+    for side in ("enc", "dec"):
+        for l in range(layers):
+            fin = emb if l == 0 else cfg.d
+            dWi, dWh, db = unpack_lstm_grad(g[f"dW_{side}"][l], g[f"db_{side}"][l], fin, cfg.d)
+            rWi, rWh, rb = ref[side][l]
+            for nm, got, want in (("dW_ih", dWi, rWi), ("dW_hh", dWh, rWh), ("db", db, rb)):
+                e = _rel(got.double().cpu().numpy(), want)
+                assert e <= TOL, (side, l, nm, e)
+    for nm in ("dE_src", "dE_tgt"):
+        e = _rel(g[nm].double().cpu().numpy(), ref[nm])
+        assert e <= TOL, (nm, e)
