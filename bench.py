@@ -362,6 +362,28 @@ def measure_next_rows(binding, st, dv, cfg, scale, comm, stream, dev, pk, tok_lo
             "source_plus_target_tokens_per_s": cfg.B * (cfg.M + cfg.N) / (ms_if / 1e3),
             "note": "HybridNMTIF forward: decoder step t waits for Htilde_{t-1} (attention + Eq. 4)"}
         del ed
+        # one whole HybridNMT training step on this GPU (Fig. 3): MP forward
+        # keeping the activations, the DP stage (forward + backward) on its
+        # H_enc / H_dec, then the MP backward (reverse wavefront + dW GEMMs)
+        if comm is None:
+            from paper_1909_00562_b200.stage import EncoderDecoderTrainer
+            li = make_lstm_inputs(cfg, layers=L_, emb=e_)
+            tr = EncoderDecoderTrainer(cfg.B, cfg.M, cfg.N, e_, cfg.d, L_, cfg.V, cfg.V, device=dev)
+            tr.set_weights([tuple(bfd(w) for w in ws) for ws in li["enc"]],
+                           [tuple(bfd(w) for w in ws) for ws in li["dec"]])
+            hout = st.alloc_outputs()
+
+            def hybrid():
+                He_, Hd_ = tr.forward(s_ids, t_ids, li["src_len"], Es, Et, stream=stream)
+                st(Hd_, He_, dv["src_len"], dv["tgt_len"], dv["tgt_ids"], dv["W_c"], dv["W_out"],
+                   scale, out=hout, stream=stream)
+                tr.backward(hout["dH_enc"], hout["dH_dec"], stream=stream)
+            ms_h = timed(hybrid)
+            res["hybrid_training_step"] = {
+                "ms": ms_h, "target_tokens_per_s": tok_local / (ms_h / 1e3),
+                "note": "MP forward (activations kept) + DP stage + MP backward (reverse wavefront, "
+                        "dW GEMMs, embedding gradients) on one GPU; no optimizer step"}
+            del tr
     # NEXT-2: Adam over W_out, W_c (and W_alpha, b_out would add d^2 + V)
     n = cfg.V * cfg.d + 2 * cfg.d * cfg.d
     h = binding.adam_params(1)

@@ -672,13 +672,25 @@ __global__ void shift_h_kernel(const __nv_bfloat16* __restrict__ H, const __nv_b
     reinterpret_cast<uint4*>(Hp)[i] = v;
   }
 }
-// db[j] = sum over rows of dG[row][j] (fixed order per column)
-__global__ void colsum_bf16_kernel(const __nv_bfloat16* __restrict__ dG, long long rows, int cols,
-                                   float* __restrict__ db) {
+// db[j] = sum over rows of dG[row][j], deterministic in two passes: block
+// (x, y) sums rows [128 y, 128 y + 128) of columns [256 x, 256 x + 256) in
+// order into part[y][j]; then part is summed over y in order.
+constexpr int LB_CS_ROWS = 128;
+__global__ void lstm_db_part_kernel(const __nv_bfloat16* __restrict__ dG, long long rows, int cols,
+                                   float* __restrict__ part) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  const long long r0 = (long long)blockIdx.y * LB_CS_ROWS;
+  const long long r1 = r0 + LB_CS_ROWS < rows ? r0 + LB_CS_ROWS : rows;
+  float s = 0.f;
+  for (long long r = r0; r < r1; ++r) s += __bfloat162float(dG[r * cols + j]);
+  part[(long long)blockIdx.y * cols + j] = s;
+}
+__global__ void lstm_db_final_kernel(const float* __restrict__ part, int nparts, int cols, float* __restrict__ db) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= cols) return;
   float s = 0.f;
-  for (long long r = 0; r < rows; ++r) s += __bfloat162float(dG[r * cols + j]);
+  for (int y = 0; y < nparts; ++y) s += part[(long long)y * cols + j];
   db[j] = s;
 }
 
@@ -1081,7 +1093,7 @@ extern "C" attn_status_t attn_encoder_decoder_if_fwd(
 namespace {
 struct TrPlan {
   size_t inter_enc, inter_dec, gates_enc, gates_dec, cseq_enc, cseq_dec;   // forward saves
-  size_t dg, dxo, dhrec, dh0, dc0, hprev, flags, counter, total;
+  size_t dg, dxo, dhrec, dh0, dc0, hprev, flags, counter, dbpart, total;
 };
 TrPlan plan_train(const attn_lstm_shape_t* s, const LsPlan& base) {
   TrPlan q;
@@ -1103,6 +1115,7 @@ TrPlan plan_train(const attn_lstm_shape_t* s, const LsPlan& base) {
   q.hprev = take(B * Tm * hd * 2);
   q.flags = take(2 * L * Tm * 4);
   q.counter = take(256);
+  q.dbpart = take(((B * Tm + 127) / 128) * 4 * hd * 4);
   q.total = o;
   return q;
 }
@@ -1241,7 +1254,11 @@ attn_status_t side_weight_grads(const attn_lstm_shape_t* s, const LsPlan& p, con
     LS_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
     if ((r = attn_internal_gemm_atb(4 * hd, in + hd, (int)rows, dgl, X, in, hprev, dW[l], counter, st)) != ATTN_OK)
       return r;
-    colsum_bf16_kernel<<<(4 * hd + 255) / 256, 256, 0, st>>>(dgl, rows, 4 * hd, db[l]);
+    float* part = reinterpret_cast<float*>(ws + q.dbpart);
+    const int nparts = (int)((rows + LB_CS_ROWS - 1) / LB_CS_ROWS);
+    lstm_db_part_kernel<<<dim3((4 * hd + 255) / 256, nparts), 256, 0, st>>>(dgl, rows, 4 * hd, part);
+    LS_CUDA(cudaGetLastError());
+    lstm_db_final_kernel<<<(4 * hd + 255) / 256, 256, 0, st>>>(part, nparts, 4 * hd, db[l]);
     LS_CUDA(cudaGetLastError());
   }
   return ATTN_OK;
