@@ -171,6 +171,7 @@ static int g_opt_proj_bn = 256;
 // "attn_trace": device buffer of globaltimer stamps, [2][B][16] int64 (forward,
 // backward) + [B][64][4] backward chunk stamps (scripts/attn_trace.py)
 static long long* g_attn_trace = nullptr;
+namespace attnsm { extern long long* g_lstm_trace; }
 
 // Options are read by a call from its start to its last enqueue under this
 // lock (and written under it), so a concurrent set_option never changes a call
@@ -274,6 +275,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "pdl")) {
     g_opt_pdl = value != 0;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "lstm_trace")) {
+    attnsm::g_lstm_trace = reinterpret_cast<long long*>(value);
     return ATTN_OK;
   }
   if (!strcmp(key, "attn_trace")) {

@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -386,10 +387,27 @@ struct LbLayer {
 struct alignas(64) LbParams {
   LbLayer layer[LS_MAXL];
   int L, B, T, hd, G;
+  int C;                       // cluster size (1, 2, 4): the CTAs of a cluster share each dz k-block
+                               // (one of them loads it, TMA multicast to all)
+  int Gk;                      // K split (1, 2, 4): CTA g takes the 4hd / Gk gate columns [kh 4hd / Gk, ..)
+                               // of the product, kh = g / (G / Gk), over 64 Gk-column tiles, and writes
+                               // partial kh of dx / dh_rec; the readers add the Gk partials in order
+  long long dx_kstride;        // floats between the partials of dx_out / dx_above
+  long long rec_kstride;       // floats between the partials of dh_rec
   const int* cap;              // [B] (encoder) or NULL
   unsigned* dgdone;            // [L][T] CTAs that wrote dz of (l, t)
   unsigned* outdone;           // [L][T] CTAs that stored their [dx | dh] slices of (l, t)
+  long long* trace;            // debug (option "lstm_trace"): [L G][T][8] globaltimer stamps, NULL = off
 };
+__device__ __forceinline__ long long lb_gt() {
+  long long c;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(c));
+  return c;
+}
+#define LB_TRACE(t, i)                                                              \
+  do {                                                                              \
+    if (P.trace) P.trace[((long long)blockIdx.x * P.T + (t)) * 8 + (i)] = lb_gt();  \
+  } while (0)
 
 constexpr int LB_STAGE = 24 * 1024;   // dz block 16 KB + W block 8 KB
 constexpr int LB_STAGES = 8;
@@ -410,13 +428,21 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_bwd_kernel(const __grid_co
   const int l = blockIdx.x / P.G, g = blockIdx.x % P.G;
   const LbLayer& Ly = P.layer[l];
   const int hd = P.hd, T = P.T, U = hd / P.G;
-  const int nsl = (Ly.in + hd) / 64;           // 64-column output slices of the layer
-  const int kb_n = 4 * hd / 64;                // k-blocks (gate columns)
+  const int Gk = P.Gk, Gn = P.G / Gk, kh = g / Gn, gn = g % Gn;
+  const int NT = 64 * Gk;                      // output tile width
+  const int ncol = (Ly.in + hd) / NT;          // output tiles of the layer
+  const int kb_n = 4 * hd / 64 / Gk;           // k-blocks (gate columns) of this CTA's K range
+  const int kb0 = kh * kb_n;
+  const uint32_t stage_bytes = 16384u + 8192u * (uint32_t)Gk;
+  const int nst = LB_STAGES * LB_STAGE / (int)stage_bytes;
+  const int C = P.C;
+  const uint32_t crank = C > 1 ? cluster_ctarank() : 0;
+  const uint16_t cmask = (uint16_t)((1u << C) - 1u);
   if (warp == 8) {
     if (lane == 0) {
-      for (int i = 0; i < LB_STAGES; ++i) {
+      for (int i = 0; i < nst; ++i) {
         mbar_init(&full[i], 1);
-        mbar_init(&empty[i], 1);
+        mbar_init(&empty[i], C);   // every CTA of the cluster reads the multicast dz block
       }
       for (int i = 0; i < 2; ++i) {
         mbar_init(&tfull[i], 1);
@@ -427,65 +453,76 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_bwd_kernel(const __grid_co
       tma_prefetch_desc(&Ly.m_w);
     }
     __syncwarp();
-    tmem_alloc(tmem_slot, 128);
+    tmem_alloc(tmem_slot, 2 * NT);
   }
   tc_fence_before();
-  __syncthreads();
+  if (C > 1) cluster_sync();   // the peers' barriers exist before any multicast
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 8) {
-    // ---------------- TMA producer: per step, this CTA's slices x 4hd / 64 k-blocks
+    // ---------------- TMA producer: per step, this CTA's tiles x its k-blocks
     int s = 0;
     uint32_t ph = 0;
     for (int t = T - 1; t >= 0; --t) {
       bool first = true;
-      for (int sl = g; sl < nsl; sl += P.G) {
-        for (int kb = 0; kb < kb_n; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
+      for (int ct = gn; ct < ncol; ct += Gn) {
+        for (int kk = 0; kk < kb_n; ++kk) {
+          const int kb = kb0 + kk;
+          if (C > 1) mbar_wait_cluster(&empty[s], ph ^ 1);
+          else mbar_wait(&empty[s], ph ^ 1);
           if (lane == 0) {
-            uint8_t* st = ring + s * LB_STAGE;
-            mbar_arrive_expect_tx(&full[s], LB_STAGE);
-            tma_load_2d(st + 16384, &Ly.m_w, &full[s], sl * 64, kb * 64);
-            if (first) {   // dz of step t: every CTA of the layer has written its units
-              ls_wait_geq(P.dgdone + (size_t)l * T + t, (unsigned)P.G);
-              fence_proxy_async_global();
-              first = false;
+            uint8_t* st = ring + s * stage_bytes;
+            mbar_arrive_expect_tx(&full[s], stage_bytes);
+            for (int a = 0; a < Gk; ++a)
+              tma_load_2d(st + 16384 + 8192 * a, &Ly.m_w, &full[s], ct * NT + 64 * a, kb * 64);
+            if (kk % C == (int)crank) {   // this CTA's share of the cluster's dz blocks
+              if (first) {   // dz of step t: every CTA of the layer has written its units
+                ls_wait_geq(P.dgdone + (size_t)l * T + t, (unsigned)P.G);
+                fence_proxy_async_global();
+                first = false;
+                LB_TRACE(t, 2);
+              }
+              if (C > 1) tma_load_3d_mc(st, &Ly.m_dg, &full[s], kb * 64, t, 0, cmask);
+              else tma_load_3d(st, &Ly.m_dg, &full[s], kb * 64, t, 0);
             }
-            tma_load_3d(st, &Ly.m_dg, &full[s], kb * 64, t, 0);
           }
           __syncwarp();
-          if (++s == LB_STAGES) { s = 0; ph ^= 1; }
+          if (++s == nst) { s = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 9) {
-    // ---------------- MMA issuer: out[128, 64] = dz_t (K-major) x W_l[:, slice] (MN-major)
+    // ---------------- MMA issuer: out[128, NT] = dz_t[:, K range] (K-major) x W_l[K range, tile] (MN-major)
     int s = 0;
     uint32_t ph = 0;
     int n = 0;
-    const uint32_t idesc = umma_idesc_bf16(128, 64, 0, 1);
+    const uint32_t idesc = umma_idesc_bf16(128, NT, 0, 1);
     for (int t = T - 1; t >= 0; --t) {
-      for (int sl = g; sl < nsl; sl += P.G, ++n) {
+      for (int ct = gn; ct < ncol; ct += Gn, ++n) {
         const int acc = n & 1, use = n >> 1;
         if (use > 0) mbar_wait(&tempty[acc], (use - 1) & 1);
         tc_fence_after();
         for (int kb = 0; kb < kb_n; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
+          if (kb == 0 && lane == 0) LB_TRACE(t, 3);
           if (elect_one()) {
-            const uint32_t sa = smem_u32(ring + s * LB_STAGE);
+            const uint32_t sa = smem_u32(ring + s * stage_bytes);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              umma_bf16(tmem_base + acc * 64, umma_sdesc(sa + k * 32, 16, 1024),
-                        umma_sdesc(sa + 16384 + k * 2048, 16, 1024), idesc, (kb | k) ? 1u : 0u);
-            umma_commit(&empty[s]);
+              umma_bf16(tmem_base + acc * NT, umma_sdesc(sa + k * 32, 16, 1024),
+                        umma_sdesc(sa + 16384 + k * 2048, 8192, 1024), idesc, (kb | k) ? 1u : 0u);
+            if (C > 1) umma_commit_mc(&empty[s], cmask);   // frees the stage in every peer
+            else umma_commit(&empty[s]);
           }
           __syncwarp();
-          if (++s == LB_STAGES) { s = 0; ph ^= 1; }
+          if (++s == nst) { s = 0; ph ^= 1; }
         }
         if (elect_one()) umma_commit(&tfull[acc]);
         __syncwarp();
+        if (lane == 0) LB_TRACE(t, 4);
       }
     }
   } else {
@@ -501,6 +538,36 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_bwd_kernel(const __grid_co
 #pragma unroll
     for (int k = 0; k < 16; ++k) dcc[k] = 0.f;
     int n = 0;
+    // the saved activations of step t (i, f, g, o, c_t, c_{t-1}) do not depend on
+    // the wavefront: they are loaded for step t - 1 while step t's GEMM runs
+    uint4 pg[2][4];
+    float4 pc[2][2], pp[2][2];
+    auto prefetch = [&](int t) {
+      if (!row_ok || t < 0) return;
+#pragma unroll
+      for (int i2 = 0; i2 < 2; ++i2) {
+        if (i2 * 8 >= nu) break;
+        const int u0 = u_base + i2 * 8;
+        const uint4* g4 = reinterpret_cast<const uint4*>(Ly.gates + ((size_t)r * T + t) * 4 * hd + 4 * u0);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) pg[i2][q4] = g4[q4];
+        const float4* c4 = reinterpret_cast<const float4*>(Ly.c_seq + ((size_t)r * T + t) * hd + u0);
+        pc[i2][0] = c4[0];
+        pc[i2][1] = c4[1];
+        if (t > 0) {
+          const float4* p4 = reinterpret_cast<const float4*>(Ly.c_seq + ((size_t)r * T + t - 1) * hd + u0);
+          pp[i2][0] = p4[0];
+          pp[i2][1] = p4[1];
+        } else if (Ly.c0) {
+          const float4* p4 = reinterpret_cast<const float4*>(Ly.c0 + (size_t)r * hd + u0);
+          pp[i2][0] = p4[0];
+          pp[i2][1] = p4[1];
+        } else {
+          pp[i2][0] = pp[i2][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+    };
+    prefetch(T - 1);
     for (int t = T - 1; t >= 0; --t) {
       // ---- E: wait for the gradient w.r.t. h_t (layer above) and W_hh^T dz_{t+1} (own layer)
       if (threadIdx.x == 0) {
@@ -509,8 +576,12 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_bwd_kernel(const __grid_co
         __threadfence();
       }
       named_bar_sync(1, 256);
+      if (threadIdx.x == 0) LB_TRACE(t, 0);
       if (row_ok) {
-        for (int k0 = 0; k0 < nu; k0 += 8) {
+#pragma unroll
+        for (int i2 = 0; i2 < 2; ++i2) {
+          const int k0 = i2 * 8;
+          if (k0 >= nu) break;
           const int u0 = u_base + k0;
           float dh[8], cp[8], ct[8];
           if (Ly.dh_top) {
@@ -523,14 +594,22 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_bwd_kernel(const __grid_co
               dh[2 * e + 1] = f2.y;
             }
           } else {
-            const float4* a4 = reinterpret_cast<const float4*>(Ly.dx_above + ((size_t)r * T + t) * hd + u0);
-            const float4 a = __ldcg(a4), b = __ldcg(a4 + 1);
-            dh[0] = a.x; dh[1] = a.y; dh[2] = a.z; dh[3] = a.w; dh[4] = b.x; dh[5] = b.y; dh[6] = b.z; dh[7] = b.w;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) dh[k] = 0.f;
+            for (int pk = 0; pk < Gk; ++pk) {   // the Gk partials, in order
+              const float4* a4 = reinterpret_cast<const float4*>(Ly.dx_above + pk * P.dx_kstride +
+                                                                 ((size_t)r * T + t) * hd + u0);
+              const float4 a = __ldcg(a4), b = __ldcg(a4 + 1);
+              dh[0] += a.x; dh[1] += a.y; dh[2] += a.z; dh[3] += a.w; dh[4] += b.x; dh[5] += b.y; dh[6] += b.z; dh[7] += b.w;
+            }
           }
           if (t < T - 1) {
-            const float4* a4 = reinterpret_cast<const float4*>(Ly.dh_rec + ((size_t)((t + 1) & 1) * P.B + r) * hd + u0);
-            const float4 a = __ldcg(a4), b = __ldcg(a4 + 1);
-            dh[0] += a.x; dh[1] += a.y; dh[2] += a.z; dh[3] += a.w; dh[4] += b.x; dh[5] += b.y; dh[6] += b.z; dh[7] += b.w;
+            for (int pk = 0; pk < Gk; ++pk) {
+              const float4* a4 = reinterpret_cast<const float4*>(Ly.dh_rec + pk * P.rec_kstride +
+                                                                 ((size_t)((t + 1) & 1) * P.B + r) * hd + u0);
+              const float4 a = __ldcg(a4), b = __ldcg(a4 + 1);
+              dh[0] += a.x; dh[1] += a.y; dh[2] += a.z; dh[3] += a.w; dh[4] += b.x; dh[5] += b.y; dh[6] += b.z; dh[7] += b.w;
+            }
           }
           if (t == cap && Ly.inj_dh) {
 #pragma unroll
@@ -539,28 +618,17 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_bwd_kernel(const __grid_co
               dcc[k0 + k] += Ly.inj_dc[(size_t)r * hd + u0 + k];
             }
           }
-          const float4* c4 = reinterpret_cast<const float4*>(Ly.c_seq + ((size_t)r * T + t) * hd + u0);
           {
-            const float4 a = c4[0], b = c4[1];
+            const float4 a = pc[i2][0], b = pc[i2][1];
             ct[0] = a.x; ct[1] = a.y; ct[2] = a.z; ct[3] = a.w; ct[4] = b.x; ct[5] = b.y; ct[6] = b.z; ct[7] = b.w;
-          }
-          if (t > 0) {
-            const float4* p4 = reinterpret_cast<const float4*>(Ly.c_seq + ((size_t)r * T + t - 1) * hd + u0);
-            const float4 a = p4[0], b = p4[1];
-            cp[0] = a.x; cp[1] = a.y; cp[2] = a.z; cp[3] = a.w; cp[4] = b.x; cp[5] = b.y; cp[6] = b.z; cp[7] = b.w;
-          } else if (Ly.c0) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) cp[k] = Ly.c0[(size_t)r * hd + u0 + k];
-          } else {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) cp[k] = 0.f;
+            const float4 c = pp[i2][0], d = pp[i2][1];
+            cp[0] = c.x; cp[1] = c.y; cp[2] = c.z; cp[3] = c.w; cp[4] = d.x; cp[5] = d.y; cp[6] = d.z; cp[7] = d.w;
           }
           // saved activations of these 8 units: 32 bf16 in packed order (4u + q)
-          const uint4* g4 = reinterpret_cast<const uint4*>(Ly.gates + ((size_t)r * T + t) * 4 * hd + 4 * u0);
           float ga[32];
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
-            const uint4 gv = g4[q4];
+            const uint4 gv = pg[i2][q4];
             const uint32_t w4[4] = {gv.x, gv.y, gv.z, gv.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -596,32 +664,39 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_bwd_kernel(const __grid_co
       }
       named_bar_sync(1, 256);
       if (threadIdx.x == 0) {
+        LB_TRACE(t, 1);
         __threadfence();
         red_release_gpu_add(P.dgdone + (size_t)l * T + t, 1u);
       }
-      // ---- G epilogue: this CTA's slices of [dx_t | dh_{t-1}] (fp32)
-      for (int sl = g; sl < nsl; sl += P.G, ++n) {
+      prefetch(t - 1);
+      // ---- G epilogue: this CTA's tiles of [dx_t | dh_{t-1}] (fp32, partial kh)
+      for (int ct = gn; ct < ncol; ct += Gn, ++n) {
         const int acc = n & 1, use = n >> 1;
         mbar_wait(&tfull[acc], use & 1);
         tc_fence_after();
-        float v[32];
-        tmem_ld32(tmem_base + ((q * 32u) << 16) + acc * 64 + hh * 32, v);
+        if (threadIdx.x == 0) LB_TRACE(t, 5);
+        for (int j = 0; j < Gk; ++j) {   // NT / 2 columns per warp, 32 at a time
+          float v[32];
+          tmem_ld32(tmem_base + ((q * 32u) << 16) + acc * NT + hh * (NT / 2) + 32 * j, v);
+          const int col = ct * NT + (int)hh * (NT / 2) + 32 * j;
+          if (row_ok) {
+            float* dst = col < Ly.in
+                             ? Ly.dx_out + kh * P.dx_kstride + ((size_t)r * T + t) * Ly.in + col
+                             : Ly.dh_rec + kh * P.rec_kstride + ((size_t)(t & 1) * P.B + r) * hd + (col - Ly.in);
+            float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) d4[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+          }
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
-        const int col = sl * 64 + (int)hh * 32;
-        if (row_ok) {
-          float* dst = col < Ly.in ? Ly.dx_out + ((size_t)r * T + t) * Ly.in + col
-                                   : Ly.dh_rec + ((size_t)(t & 1) * P.B + r) * hd + (col - Ly.in);
-          float4* d4 = reinterpret_cast<float4*>(dst);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) d4[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
-        }
       }
       named_bar_sync(1, 256);
       if (threadIdx.x == 0) {
         __threadfence();
         red_release_gpu_add(P.outdone + (size_t)l * T + t, 1u);
+        LB_TRACE(t, 6);
       }
     }
     // initial-state gradients: dh_{-1} = the h part of step 0's product (all CTAs), dc carry
@@ -633,27 +708,33 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_bwd_kernel(const __grid_co
       named_bar_sync(1, 256);
       if (row_ok)
         for (int k = 0; k < nu; ++k) {
-          Ly.dh0_out[(size_t)r * hd + u_base + k] = __ldcg(Ly.dh_rec + (size_t)r * hd + u_base + k);
+          float v = 0.f;
+          for (int pk = 0; pk < Gk; ++pk) v += __ldcg(Ly.dh_rec + pk * P.rec_kstride + (size_t)r * hd + u_base + k);
+          Ly.dh0_out[(size_t)r * hd + u_base + k] = v;
           Ly.dc0_out[(size_t)r * hd + u_base + k] = dcc[k];
         }
     }
     (void)rr;
   }
   tc_fence_before();
-  __syncthreads();
+  if (C > 1) cluster_sync();   // no CTA leaves while a peer may still multicast into it
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 8) tmem_dealloc(tmem_base, 128);
+  if (warp == 8) tmem_dealloc(tmem_base, 2 * NT);
 }
 
 // dX0 rows scattered into the embedding gradient: dE[ids[b][t]] += dX0[b][t]
 // (fp32 atomics: the summation order over repeated ids is not fixed)
-__global__ void embed_grad_kernel(const int* __restrict__ ids, const float* __restrict__ dX, int e,
-                                  long long rows, float* __restrict__ dE) {
+// (dX holds nk K-split partials, kstride floats apart, added in order)
+__global__ void embed_grad_kernel(const int* __restrict__ ids, const float* __restrict__ dX, int nk,
+                                  long long kstride, int e, long long rows, float* __restrict__ dE) {
   const long long n = rows * e;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const long long row = i / e;
-    atomicAdd(dE + (long long)ids[row] * e + (i % e), dX[i]);
+    float v = dX[i];
+    for (int k = 1; k < nk; ++k) v += dX[k * kstride + i];
+    atomicAdd(dE + (long long)ids[row] * e + (i % e), v);
   }
 }
 // Hprev[b][t] = t > 0 ? H[b][t-1] : h0[b] (zero when h0 is NULL), bf16, 16-byte vectors
@@ -693,6 +774,9 @@ __global__ void lstm_db_final_kernel(const float* __restrict__ part, int nparts,
   for (int y = 0; y < nparts; ++y) s += part[(long long)y * cols + j];
   db[j] = s;
 }
+
+// option "lstm_trace" (attn_softmax_set_option): stamps of the last backward launch
+long long* g_lstm_trace = nullptr;
 
 }  // namespace attnsm
 
@@ -1108,8 +1192,8 @@ TrPlan plan_train(const attn_lstm_shape_t* s, const LsPlan& base) {
   q.cseq_enc = take(L * B * M * hd * 4);
   q.cseq_dec = take(L * B * N * hd * 4);
   q.dg = take(L * B * Tm * 4 * hd * 2);
-  q.dxo = take(L * B * Tm * w0 * 4);
-  q.dhrec = take(L * 2 * B * hd * 4);
+  q.dxo = take(4 * L * B * Tm * w0 * 4);     // [Gk <= 4][L][B][Tm][w0]
+  q.dhrec = take(4 * L * 2 * B * hd * 4);    // [Gk <= 4][L][2][B][hd]
   q.dh0 = take(L * B * hd * 4);
   q.dc0 = take(L * B * hd * 4);
   q.hprev = take(B * Tm * hd * 2);
@@ -1162,10 +1246,30 @@ attn_status_t check_common(const attn_lstm_shape_t* s, const int32_t* src_lens_h
   return ATTN_OK;
 }
 
+// K split of the backward wavefront's product: ATTN_LSTM_KSPLIT = 1, 2 or 4 (default 2)
+static int lb_ksplit() {
+  static const int k = [] {
+    const char* e = getenv("ATTN_LSTM_KSPLIT");
+    const int v = e ? atoi(e) : 2;
+    return (v == 1 || v == 2 || v == 4) ? v : 2;
+  }();
+  return k;
+}
+
+// cluster size of the backward wavefront (dz multicast): ATTN_LSTM_CLUSTER = 1, 2 or 4 (default 2)
+static int lb_cluster_size() {
+  static const int c = [] {
+    const char* e = getenv("ATTN_LSTM_CLUSTER");
+    const int v = e ? atoi(e) : 2;
+    return (v == 1 || v == 2 || v == 4) ? v : 2;
+  }();
+  return c;
+}
+
 // the reverse wavefront of one side
 attn_status_t run_bwd_side(const attn_lstm_shape_t* s, const LsPlan& p, const TrPlan& q, bool decoder,
                            const void* const* W, const void* dH_top, char* ws, const int* cap_dev,
-                           cudaStream_t st) {
+                           cudaStream_t st, int* gk_out) {
   static LbParams P;
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
@@ -1205,10 +1309,22 @@ attn_status_t run_bwd_side(const attn_lstm_shape_t* s, const LsPlan& p, const Tr
     Ly.inj_dc = decoder ? nullptr : dc0 + (size_t)l * B * hd;
   }
   P.L = L; P.B = B; P.T = T; P.hd = hd; P.G = p.G;
+  // K split: the largest Gk <= the option with G % Gk == 0 and every layer's output
+  // width a multiple of the 64 Gk-column tile
+  P.Gk = 1;
+  for (int k = lb_ksplit(); k > 1; k /= 2)
+    if (p.G % k == 0 && (s->emb + hd) % (64 * k) == 0 && (2 * hd) % (64 * k) == 0 && (hd / 16) % k == 0) {
+      P.Gk = k;
+      break;
+    }
+  P.dx_kstride = (long long)L * B * std::max(s->src_len, s->tgt_len) * (long long)w0;
+  P.rec_kstride = (long long)L * 2 * B * hd;
+  *gk_out = P.Gk;
   P.cap = decoder ? nullptr : cap_dev;
   unsigned* flags = reinterpret_cast<unsigned*>(ws + q.flags);
   P.dgdone = flags;
   P.outdone = flags + (size_t)L * T;
+  P.trace = g_lstm_trace;
   LS_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned) * 2 * (size_t)L * T, st));
   static std::vector<int> attr_set;
   int dev = 0;
@@ -1222,11 +1338,38 @@ attn_status_t run_bwd_side(const attn_lstm_shape_t* s, const LsPlan& p, const Tr
   cfg.blockDim = dim3(LS_THREADS);
   cfg.dynamicSmemBytes = LB_SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // clusters of C CTAs of one layer share each dz k-block (TMA multicast): C
+  // divides G, every CTA of a cluster owns the same number of 64-column slices,
+  // and all L G / C clusters are co-resident (the flags are spin-waited on)
+  int C = lb_cluster_size();
+  const int Gn = p.G / P.Gk;
+  for (; C > 1; C /= 2) {
+    bool ok = Gn % C == 0;
+    for (int l = 0; ok && l < L; ++l) {
+      const int ncol = ((l == 0 ? s->emb : hd) + hd) / (64 * P.Gk);
+      auto cnt = [&](int gn) { return gn < ncol ? (ncol - 1 - gn) / Gn + 1 : 0; };
+      for (int gn = 0; ok && gn < Gn; ++gn) ok = cnt(gn) == cnt(gn - gn % C);
+    }
+    if (!ok) continue;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = C;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.numAttrs = 2;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, lstm_bwd_kernel, &cfg) == cudaSuccess &&
+        nclusters >= L * p.G / C)
+      break;
+    (void)cudaGetLastError();
+    cfg.numAttrs = 1;
+  }
+  P.C = C > 1 ? C : 1;
+  cfg.numAttrs = P.C > 1 ? 2 : 1;
   LS_CUDA(cudaLaunchKernelEx(&cfg, lstm_bwd_kernel, P));
   return ATTN_OK;
 }
@@ -1336,14 +1479,16 @@ extern "C" attn_status_t attn_encoder_decoder_bwd(
   LS_CUDA(cudaMemsetAsync(dE_src, 0, sizeof(float) * (size_t)s->vocab_src * e, st));
   LS_CUDA(cudaMemsetAsync(dE_tgt, 0, sizeof(float) * (size_t)s->vocab_tgt * e, st));
   // decoder first: its initial-state gradients reach the encoder at src_len - 1
-  if ((r = run_bwd_side(s, p, q, true, dec_W, dH_dec, ws, cap_dev, st)) != ATTN_OK) return r;
+  int gk = 1;
+  if ((r = run_bwd_side(s, p, q, true, dec_W, dH_dec, ws, cap_dev, st, &gk)) != ATTN_OK) return r;
   if ((r = side_weight_grads(s, p, q, true, ws + p.xt, H_dec, dW_dec, db_dec, ws, sms, st)) != ATTN_OK) return r;
   // layer 0's dx_out is dL/dx [B][N][e]: the target embeddings' rows
-  embed_grad_kernel<<<sms * 8, 256, 0, st>>>(tgt_ids, dxo, e, (long long)B * N, dE_tgt);
+  const long long dx_kstride = (long long)s->layers * B * std::max(M, N) * (long long)std::max(e, s->hidden);
+  embed_grad_kernel<<<sms * 8, 256, 0, st>>>(tgt_ids, dxo, gk, dx_kstride, e, (long long)B * N, dE_tgt);
   LS_CUDA(cudaGetLastError());
-  if ((r = run_bwd_side(s, p, q, false, enc_W, dH_enc, ws, cap_dev, st)) != ATTN_OK) return r;
+  if ((r = run_bwd_side(s, p, q, false, enc_W, dH_enc, ws, cap_dev, st, &gk)) != ATTN_OK) return r;
   if ((r = side_weight_grads(s, p, q, false, ws + p.xs, H_enc, dW_enc, db_enc, ws, sms, st)) != ATTN_OK) return r;
-  embed_grad_kernel<<<sms * 8, 256, 0, st>>>(src_ids, dxo, e, (long long)B * M, dE_src);
+  embed_grad_kernel<<<sms * 8, 256, 0, st>>>(src_ids, dxo, gk, dx_kstride, e, (long long)B * M, dE_src);
   LS_CUDA(cudaGetLastError());
   return ATTN_OK;
 }

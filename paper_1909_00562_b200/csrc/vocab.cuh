@@ -132,7 +132,8 @@ struct alignas(64) VbParams {
   long long* trace;      // debug: 16 int64 per tile and CTA rank (see VB_TRACE), NULL = off
   int debug;             // timing experiments only (WRONG results): bit 0 skip the G1 stores,
                          // bit 1 skip the G1 exponentials, bit 2 skip the G2 / G3 stores,
-                         // bit 3 publish tiles without waiting for their stores to land
+                         // bit 3 publish tiles without waiting for their stores to land,
+                         // bit 4 / 5 skip the B / A operand loads
   int blk_start[VB_MAX_BLOCKS + 2];   // backward blocks, relative to fwd_tiles
 };
 
@@ -418,17 +419,20 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           uint8_t* sA = smem + s * Cfg::STAGE;
           uint8_t* sB = sA + Cfg::A_BYTES;
           const uint32_t barc = kPair ? leader_addr(&full[s]) : 0u;
-          if (leader) mbar_arrive_expect_tx(&full[s], Cfg::STAGE * Cfg::CTAS);
+          // debug bits 4 / 5 (timing only): skip the B / A operand loads
+          const bool ldA = !(P.debug & 32), ldB = !(P.debug & 16);
+          if (leader)
+            mbar_arrive_expect_tx(&full[s], ((ldA ? Cfg::A_BYTES : 0) + (ldB ? Cfg::B_BYTES : 0)) * Cfg::CTAS);
           const int k0 = kb * VB_BK;
           if (tl.type == VB_G1 || tl.type == VB_G0) {
-            vb_load<kPair>(sA, &P.m_hc_k, &full[s], barc, k0, arow, 0, pol_keep);
-            vb_load<kPair>(sB, &P.m_wo_k, &full[s], barc, k0, bcolg, 0, pol_norm);
+            if (ldA) vb_load<kPair>(sA, &P.m_hc_k, &full[s], barc, k0, arow, 0, pol_keep);
+            if (ldB) vb_load<kPair>(sB, &P.m_wo_k, &full[s], barc, k0, bcolg, 0, pol_norm);
           } else if (tl.type == VB_G3) {
-            vb_load<kPair>(sA, &P.m_dl_k, &full[s], barc, k0, arow, buf, pol_norm);
-            vb_load4<kPair>(sB, &P.m_wo_mn, &full[s], barc, 0, c0 + k0, bcol / 64, 0, pol_norm);
+            if (ldA) vb_load<kPair>(sA, &P.m_dl_k, &full[s], barc, k0, arow, buf, pol_norm);
+            if (ldB) vb_load4<kPair>(sB, &P.m_wo_mn, &full[s], barc, 0, c0 + k0, bcol / 64, 0, pol_norm);
           } else {
-            vb_load4<kPair>(sA, &P.m_dl_mn, &full[s], barc, 0, k0, arow / 64, buf, pol_norm);
-            vb_load4<kPair>(sB, &P.m_hc_mn, &full[s], barc, 0, k0, bcol / 64, 0, pol_keep);
+            if (ldA) vb_load4<kPair>(sA, &P.m_dl_mn, &full[s], barc, 0, k0, arow / 64, buf, pol_norm);
+            if (ldB) vb_load4<kPair>(sB, &P.m_hc_mn, &full[s], barc, 0, k0, bcol / 64, 0, pol_keep);
           }
         }
         __syncwarp();

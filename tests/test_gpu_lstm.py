@@ -136,12 +136,17 @@ def test_input_feeding_matches_oracle(cuda_lib, name, layers, emb):
             assert _rel(got[:, t], ref[:, t]) <= bound, (nm, t, _rel(got[:, t], ref[:, t]), bound)
 
 
-@pytest.mark.parametrize("name,layers,emb", [("small", 2, 128), ("medium", 4, 256), ("paper", 4, 512)])
+@pytest.mark.parametrize("name,layers,emb", [("small", 2, 128), ("medium", 4, 256), ("paper", 4, 512),
+                                             ("odd", 3, 64), ("edge_min", 1, 64), ("edge_max_src", 2, 64)])
 def test_encoder_decoder_backward_matches_oracle(cuda_lib, name, layers, emb):
     """NEXT-3 training: the reverse wavefront (attn_encoder_decoder_bwd) against
     the fp64 BPTT oracle (pinned by torch autograd) for upstream gradients of
     the stage's size on H_enc / H_dec: every layer's dW_ih, dW_hh, db and the
-    embedding gradients, rel-L2 <= 2e-2 each."""
+    embedding gradients, rel-L2 <= 2e-2 each.  The shapes cover the product's
+    launch variants: K split in two with dz multicast over CTA pairs (small,
+    medium, paper), K split without clusters (odd: G / 2 = 5 column groups;
+    edge_min: one sentence of one step, G = 2), no K split (edge_max_src: 192
+    output columns in layer 0)."""
     from paper_1909_00562_b200.stage import EncoderDecoderTrainer, unpack_lstm_grad
     cfg = CONFIGS[name]
     inp = make_lstm_inputs(cfg, layers=layers, emb=emb)
