@@ -142,6 +142,7 @@ static int g_opt_vb_pair = 1;
 // whole G1 set after its producers; needs dl_buffers >= 3)
 static int g_opt_vb_order = 1;
 static int g_vb_debug = 0;    // "vb_debug": timing experiments (vocab.cuh VbParams::debug)
+static int g_opt_vb_wide = 1; // "vb_wide": 512-column G2 / G3 tiles on CTA pairs (VbParams::wide)
 static int g_opt_vb_l2 = 3;   // "vb_l2hints": VbParams::l2hints
 // "vb_fwd_fused": F4 + F5 inside the persistent launch (G0 tiles on CTA pairs,
 // LSE by its warps 8-9) instead of the single-CTA forward GEMM + lse_reduce
@@ -221,6 +222,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   }
   if (!strcmp(key, "vb_l2hints")) {
     g_opt_vb_l2 = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "vb_wide")) {
+    g_opt_vb_wide = value != 0;
     return ATTN_OK;
   }
   if (!strcmp(key, "vb_debug")) {
@@ -1476,6 +1481,8 @@ static attn_status_t launch_vocab_k(const Plan& p, const VbArgs& a, int ctas, cu
   P.nrb = L.nrb;
   P.ndt = L.ndt;
   P.ncolf = L.ncolf;
+  P.wide = (kPair && g_opt_vb_wide && d % 512 == 0) ? 1 : 0;
+  P.ndw = P.wide ? L.ndt / 2 : L.ndt;
   P.ntn = (int)((V + VB_BN - 1) / VB_BN);
   P.fwd_tiles = a.fwd ? P.nrb * P.ntn : 0;
   P.last_g2_first = g_opt_vb_g2first;
@@ -1490,7 +1497,7 @@ static attn_status_t launch_vocab_k(const Plan& p, const VbArgs& a, int ctas, cu
   t += P.nrb * ((vcc(0) + VB_BN - 1) / VB_BN);
   for (int c = 0; c < p.nchunks; ++c) {
     P.blk_start[c + 1] = t;
-    t += P.nrb * P.ndt + ((vcc(c) + Cfg::TM - 1) / Cfg::TM) * P.ndt;
+    t += P.nrb * P.ndw + ((vcc(c) + Cfg::TM - 1) / Cfg::TM) * P.ndw;
     if (c + 1 < p.nchunks) t += P.nrb * ((vcc(c + 1) + VB_BN - 1) / VB_BN);
   }
   P.blk_start[p.nchunks + 1] = t;

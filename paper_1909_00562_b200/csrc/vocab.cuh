@@ -100,6 +100,11 @@ struct alignas(64) VbParams {
   int nrb;               // TM-row blocks of T
   int ndt;               // 256-column tiles of d
   int ncolf;             // 256-column blocks of a full chunk (Vc / 256)
+  int wide;              // G2 / G3 tiles 512 columns wide (pairs, d % 512 == 0): per k-block two
+                         // ring stages (A + B columns [0, 256), then B columns [256, 512)) and
+                         // two N = 256 MMAs into both TMEM accumulators -- 3/4 of the operand
+                         // bytes per FLOP of the 256-wide tile
+  int ndw;               // G2 / G3 column tiles of d (ndt, or ndt / 2 when wide)
   int ntn;               // 256-column tiles of V (forward)
   int fwd_tiles;         // tiles of the forward section (0: forward not in this launch)
   int total_tiles;
@@ -171,8 +176,8 @@ __device__ __forceinline__ VbTile vb_decode(const VbParams& P, int t) {
     r.type = VB_G1; r.c = 0;
   } else {
     const int c = lo - 1;
-    const int n3 = P.nrb * P.ndt;
-    const int n2 = ((vb_vcc(P, c) + TM - 1) / TM) * P.ndt;
+    const int n3 = P.nrb * P.ndw;
+    const int n2 = ((vb_vcc(P, c) + TM - 1) / TM) * P.ndw;
     const bool g2first = P.last_g2_first && c == P.nchunks - 1;
     const int n1 = (P.order == 1 && c + 1 < P.nchunks)
                        ? P.nrb * ((vb_vcc(P, c + 1) + VB_BN - 1) / VB_BN) : 0;
@@ -198,10 +203,10 @@ __device__ __forceinline__ VbTile vb_decode(const VbParams& P, int t) {
     r.i = u / ncol; r.j = u % ncol;
     r.kb_total = P.d / VB_BK;
   } else if (r.type == VB_G3) {
-    r.i = u / P.ndt; r.j = u % P.ndt;
+    r.i = u / P.ndw; r.j = u % P.ndw;
     r.kb_total = (r.vcc + VB_BK - 1) / VB_BK;
   } else {
-    r.i = u / P.ndt; r.j = u % P.ndt;
+    r.i = u / P.ndw; r.j = u % P.ndw;
     r.kb_total = (P.T + VB_BK - 1) / VB_BK;
   }
   return r;
@@ -408,8 +413,9 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
         fence_proxy_async_global();
       }
       VB_TRACE(t, 3, vb_gt());
+      const bool wide = kPair && P.wide && (tl.type == VB_G2 || tl.type == VB_G3);
       const int arow = tl.i * TM + 128 * rank;            // this CTA's A rows (M)
-      const int bcol = tl.j * VB_BN + Cfg::B_ROWS * rank;  // this CTA's B rows (N)
+      const int bcol = tl.j * (wide ? 2 * VB_BN : VB_BN) + Cfg::B_ROWS * rank;  // this CTA's B rows (N)
       const int bcolg = (tl.type == VB_G0 ? 0 : c0) + bcol;
       int t_nxt = -1;
       VbTile tl_nxt{};
@@ -437,6 +443,22 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
         }
         __syncwarp();
         if (++s == STAGES) { s = 0; ph ^= 1; }
+        if (wide) {
+          // the k-block's second stage: B columns [256, 512) of the tile (its A region unused)
+          mbar_wait(&empty[s], ph ^ 1);
+          if (elect_one()) {
+            uint8_t* sB = smem + s * Cfg::STAGE + Cfg::A_BYTES;
+            const uint32_t barc = kPair ? leader_addr(&full[s]) : 0u;
+            if (leader) mbar_arrive_expect_tx(&full[s], Cfg::B_BYTES * Cfg::CTAS);
+            const int k0 = kb * VB_BK;
+            if (tl.type == VB_G3)
+              vb_load4<kPair>(sB, &P.m_wo_mn, &full[s], barc, 0, c0 + k0, (bcol + VB_BN) / 64, 0, pol_norm);
+            else
+              vb_load4<kPair>(sB, &P.m_hc_mn, &full[s], barc, 0, k0, (bcol + VB_BN) / 64, 0, pol_keep);
+          }
+          __syncwarp();
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
         if (kb == 0) {
           t_nxt = next_tile();
           if (t_nxt >= 0) tl_nxt = vb_decode<kPair>(P, t_nxt);
@@ -464,40 +486,64 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
         const uint32_t a_lbo = a_mn ? 8192u : 16u, b_lbo = b_mn ? 8192u : 16u;
         const uint32_t a_kstep = a_mn ? 2048u : 32u, b_kstep = b_mn ? 2048u : 32u;
         const int kb_read = tl.kb_total > 1 ? 1 : 0;
+        const bool wide = kPair && P.wide && (tl.type == VB_G2 || tl.type == VB_G3);
         int t_nxt = -1;
         VbTile tl_nxt{};
+        // a wide tile takes both accumulators: slot acc, then the next one
+        const int acc2 = acc ^ 1;
+        const uint32_t aph2 = acc2 == 0 ? (aph ^ 1) : aph;
         mbar_wait(&tempty[acc], aph ^ 1);
+        if (wide) mbar_wait(&tempty[acc2], aph2 ^ 1);
         tc_fence_after();
         VB_TRACE(t, 13, vb_clk());
         long long wait_cyc = 0;
         const uint32_t dcol = tmem_base + acc * VB_BN;
+        const uint32_t dcol2 = tmem_base + acc2 * VB_BN;
         for (int kb = 0; kb < tl.kb_total; ++kb) {
+          int s2 = s;
+          uint32_t ph2 = ph;
+          if (wide && ++s2 == STAGES) { s2 = 0; ph2 ^= 1; }
           if (P.trace) {
             const long long w0 = vb_clk();
             mbar_wait(&full[s], ph);
+            if (wide) mbar_wait(&full[s2], ph2);
             wait_cyc += vb_clk() - w0;
           } else {
             mbar_wait(&full[s], ph);
+            if (wide) mbar_wait(&full[s2], ph2);
           }
           tc_fence_after();
           if (elect_one()) {
             const uint32_t sA = smem_u32(smem + s * Cfg::STAGE);
             const uint32_t sB = sA + Cfg::A_BYTES;
+            const uint32_t sB2 = smem_u32(smem + s2 * Cfg::STAGE) + Cfg::A_BYTES;
 #pragma unroll
             for (int k = 0; k < VB_BK / 16; ++k) {
               const uint64_t ad = umma_sdesc(sA + k * a_kstep, a_lbo, 1024);
               const uint64_t bd = umma_sdesc(sB + k * b_kstep, b_lbo, 1024);
               if constexpr (kPair) umma_bf16_pair(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
               else umma_bf16(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              if constexpr (kPair) {
+                if (wide) {
+                  const uint64_t bd2 = umma_sdesc(sB2 + k * b_kstep, b_lbo, 1024);
+                  umma_bf16_pair(dcol2, ad, bd2, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                }
+              }
             }
-            if constexpr (kPair) umma_commit_pair(&empty[s]);
-            else umma_commit(&empty[s]);
+            if constexpr (kPair) {
+              umma_commit_pair(&empty[s]);
+              if (wide) umma_commit_pair(&empty[s2]);
+            } else {
+              umma_commit(&empty[s]);
+            }
           }
           __syncwarp();
           if (kb == 0) {
             VB_TRACE(t, 4, vb_clk());
             VB_TRACE(t, 8, vb_gt());
           }
+          s = s2;
+          ph = ph2;
           if (++s == STAGES) { s = 0; ph ^= 1; }
           if (kb == kb_read) {
             t_nxt = ring_read(r, rph, false);
@@ -505,14 +551,19 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           }
         }
         if (elect_one()) {
-          if constexpr (kPair) umma_commit_pair(&tfull[acc]);
-          else umma_commit(&tfull[acc]);
+          if constexpr (kPair) {
+            umma_commit_pair(&tfull[acc]);
+            if (wide) umma_commit_pair(&tfull[acc2]);
+          } else {
+            umma_commit(&tfull[acc]);
+          }
         }
         __syncwarp();
         VB_TRACE(t, 5, vb_clk());
         VB_TRACE(t, 9, vb_gt());
         VB_TRACE(t, 14, wait_cyc);
         if (++acc == 2) { acc = 0; aph ^= 1; }
+        if (wide && ++acc == 2) { acc = 0; aph ^= 1; }
         t = t_nxt;
         tl = tl_nxt;
       }
@@ -812,65 +863,75 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
         __syncwarp();
       } else {
         // ---- fp32 output: dW_out[c] rows (G2) or dHc (G3; chunk 0 stores, the
-        // later chunks reduce-add in chunk order)
+        // later chunks reduce-add in chunk order); a wide tile is drained as two
+        // 256-column halves, one per accumulator
         const bool g3 = tl.type == VB_G3;
-        const int ncols = min(128, P.d - colh);
-        unsigned* dhc_ctr = P.dhcdone + (size_t)tl.i * P.ndt + tl.j;
-        mbar_wait(&tfull[acc], aph);
-        tc_fence_after();
-        if (warp == 0) {
-          VB_TRACE(t, 6, vb_clk());
-          VB_TRACE(t, 10, vb_gt());
-        }
-        if (warp == 0 && lane == 0) {
-          // every MMA of the tile has completed, so its dL operand has been read
-          fence_proxy_async_global();
-          red_release_gpu_add(P.consumed + tl.c, 1u);
-        }
-        if (g3 && tl.c > 0) {
-          if (lane == 0) vb_wait_geq(dhc_ctr, (unsigned)(Cfg::WARPS_PER_TILE * tl.c));
-          __syncwarp();
-          fence_proxy_async_global();
-        }
-        if (warp == 0) VB_TRACE(t, 12, vb_clk());
-        const uint64_t pol = l2_policy_evict_first();   // dW_out is not read again here
-        const uint64_t pol_dhc = (P.l2hints & 2) ? l2_policy_evict_last() : l2_policy_evict_normal();
+        const bool wide = kPair && P.wide;
+        const int nhalf = wide ? 2 : 1;
 #pragma unroll 1
-        for (int cc = 0; cc < 4; ++cc) {
-          if (cc * 32 >= ncols) break;
-          float v[32];
-          tmem_ld32(taddr + cc * 32, v);
-          if (lane == 0) bulk_wait_read0();
-          __syncwarp();
-#pragma unroll
-          for (int g = 0; g < 8; ++g)
-            st_shared_v4(stg + lane * 128 + ((g ^ swz) << 4), __float_as_uint(v[4 * g]),
-                         __float_as_uint(v[4 * g + 1]), __float_as_uint(v[4 * g + 2]),
-                         __float_as_uint(v[4 * g + 3]));
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0 && !(P.debug & 4)) {
-            if (!g3)
-              tma_store_2d_hint(&P.m_dw_st, stg_p, colh + cc * 32, c0 + row0, pol);
-            else if (tl.c == 0)
-              tma_store_2d_hint(&P.m_dhc_st, stg_p, colh + cc * 32, row0, pol_dhc);
-            else
-              tma_reduce_add_2d_hint(&P.m_dhc_st, stg_p, colh + cc * 32, row0, pol_dhc);
-            bulk_commit();
+        for (int half = 0; half < nhalf; ++half) {
+          if (half > 0 && ++acc == 2) { acc = 0; aph ^= 1; }
+          const int nt = tl.j * nhalf + half;                // 256-column tile of d
+          const int colh = nt * VB_BN + h * 128;
+          const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * VB_BN + h * 128;
+          const int ncols = min(128, P.d - colh);
+          unsigned* dhc_ctr = P.dhcdone + (size_t)tl.i * P.ndt + nt;
+          mbar_wait(&tfull[acc], aph);
+          tc_fence_after();
+          if (warp == 0) {
+            VB_TRACE(t, 6, vb_clk());
+            VB_TRACE(t, 10, vb_gt());
           }
+          if (warp == 0 && lane == 0) {
+            // every MMA of the tile has completed, so its dL operand has been read
+            fence_proxy_async_global();
+            red_release_gpu_add(P.consumed + tl.c, 1u);
+          }
+          if (g3 && tl.c > 0) {
+            if (lane == 0) vb_wait_geq(dhc_ctr, (unsigned)(Cfg::WARPS_PER_TILE * tl.c));
+            __syncwarp();
+            fence_proxy_async_global();
+          }
+          if (warp == 0) VB_TRACE(t, 12, vb_clk());
+          const uint64_t pol = l2_policy_evict_first();   // dW_out is not read again here
+          const uint64_t pol_dhc = (P.l2hints & 2) ? l2_policy_evict_last() : l2_policy_evict_normal();
+#pragma unroll 1
+          for (int cc = 0; cc < 4; ++cc) {
+            if (cc * 32 >= ncols) break;
+            float v[32];
+            tmem_ld32(taddr + cc * 32, v);
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+              st_shared_v4(stg + lane * 128 + ((g ^ swz) << 4), __float_as_uint(v[4 * g]),
+                           __float_as_uint(v[4 * g + 1]), __float_as_uint(v[4 * g + 2]),
+                           __float_as_uint(v[4 * g + 3]));
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && !(P.debug & 4)) {
+              if (!g3)
+                tma_store_2d_hint(&P.m_dw_st, stg_p, colh + cc * 32, c0 + row0, pol);
+              else if (tl.c == 0)
+                tma_store_2d_hint(&P.m_dhc_st, stg_p, colh + cc * 32, row0, pol_dhc);
+              else
+                tma_reduce_add_2d_hint(&P.m_dhc_st, stg_p, colh + cc * 32, row0, pol_dhc);
+              bulk_commit();
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (kPair && !leader) mbar_arrive_cluster(leader_addr(&tempty[acc]));
+            else mbar_arrive(&tempty[acc]);
+          }
+          if (lane == 0) {
+            if (!(P.debug & 8)) bulk_wait0();
+            fence_proxy_async_global();
+            red_release_gpu_add(g3 ? dhc_ctr : P.g2done + tl.c, 1u);
+          }
+          __syncwarp();
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (kPair && !leader) mbar_arrive_cluster(leader_addr(&tempty[acc]));
-          else mbar_arrive(&tempty[acc]);
-        }
-        if (lane == 0) {
-          if (!(P.debug & 8)) bulk_wait0();
-          fence_proxy_async_global();
-          red_release_gpu_add(g3 ? dhc_ctr : P.g2done + tl.c, 1u);
-        }
-        __syncwarp();
       }
       if (warp == 0) {
         VB_TRACE(t, 7, vb_clk());

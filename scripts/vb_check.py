@@ -28,7 +28,8 @@ def run(cfg, inp, scale, bias=False):
 
 
 def parity(name, vc=0, budget=None, bias=False):
-    cfg = CONFIGS[name]
+    cfg = CONFIGS[name] if isinstance(name, str) else name
+    name = cfg.name
     if vc:
         binding.attn_softmax_set_option("vocab_chunk", vc)
     if budget:
@@ -86,7 +87,8 @@ def timing(name="paper", n=10, **opts):
         binding.attn_softmax_set_option(k, {"store_logits": 0, "vocab_bwd_persistent": 1,
                                             "dl_budget_mb": 96, "vocab_chunk": 0,
                                             "dl_buffers": 3, "vb_last_g2_first": 1,
-                                            "vb_pair": 1, "vb_order": 1, "vb_fwd_fused": 0}.get(k, 0))
+                                            "vb_pair": 1, "vb_order": 1, "vb_fwd_fused": 0,
+                                            "vb_wide": 1}.get(k, 0))
 
 
 if __name__ == "__main__":
@@ -104,6 +106,17 @@ if __name__ == "__main__":
         parity("odd", vc=256, bias=True)
         parity("edge_min")
         binding.attn_softmax_set_option("vb_fwd_fused", 0)
+    if what in ("wide",):   # 512-column G2 / G3 tiles (d % 512 == 0)
+        from dataclasses import replace
+        binding.attn_softmax_set_option("vb_wide", 1)
+        parity("medium")
+        parity("medium", vc=512)
+        parity(replace(CONFIGS["small"], name="small_d1024", d=1024, V=3001))
+        parity(replace(CONFIGS["small"], name="small_d1024_bias", d=1024, V=2500), vc=256, bias=True)
+        parity(replace(CONFIGS["odd"], name="odd_d512", d=512, N=100, V=777), vc=256)
+        for _ in range(2):
+            timing()
+            timing(vb_wide=0)
     if what in ("pair1",):
         binding.attn_softmax_set_option("vb_pair", 0)
         for nm in ("small", "medium", "odd"):

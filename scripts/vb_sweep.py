@@ -11,7 +11,7 @@ from paper_1909_00562_b200 import binding, build
 from paper_1909_00562_b200.stage import AttnSoftmaxStage, to_device
 from synthetic import CONFIGS, global_valid_tokens, make_inputs
 
-DEFAULTS = {}
+DEFAULTS = {"vb_wide": 1, "vb_debug": 0}
 build.build()
 name = os.environ.get("CFG", "paper")
 cfg = CONFIGS[name]

@@ -79,7 +79,7 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, wide):
 # ------------------------------------------------------ end-to-end parity --
 _DEFAULTS = {"store_logits": 0, "wide_tiles": 2, "db_gemm": -1, "vb_pair": 1, "vb_fwd_fused": 0,
              "vb_order": 1, "dl_buffers": 3, "dl_budget_mb": 120, "vb_last_g2_first": 1,
-             "attn_fused": 1}
+             "attn_fused": 1, "vb_wide": 1}
 _MODES = {
     "default": {},                                  # persistent vocab launch on CTA pairs
     "single": {"vb_pair": 0},                       # ... on single-CTA 128 x 256 tiles
@@ -92,6 +92,7 @@ _MODES = {
     "sl128": {"store_logits": 1, "wide_tiles": 0},  # ... on 128 x 256 tiles
     "sl2": {"store_logits": 2},                     # ... serialised dlogits kernels
     "attn_generic": {"attn_fused": 0},              # attention on the generic engine's batched GEMMs
+    "narrow": {"vb_wide": 0},                       # G2 / G3 on 256-column tiles (default: 512 when d % 512 == 0)
 }
 
 
@@ -128,6 +129,7 @@ def set_modes(binding, mode):
                                           ("small", 256, "order0"), ("medium", 512, "order0"),
                                           ("small", 256, "nb1"), ("odd", 256, "nb1"),
                                           ("medium", 512, "g3last"),
+                                          ("medium", 0, "narrow"), ("medium", 512, "narrow"),
                                           ("tiny_ragged", 0, "sl"), ("small", 0, "sl"),
                                           ("small", 1024, "sl"), ("medium", 0, "sl"),
                                           ("medium", 2048, "sl128"), ("odd", 256, "sl"),
