@@ -578,39 +578,65 @@ __global__ void __launch_bounds__(LS_THREADS, 1) lstm_bwd_kernel(const __grid_co
       named_bar_sync(1, 256);
       if (threadIdx.x == 0) LB_TRACE(t, 0);
       if (row_ok) {
+        // dL/dh_t of this row's units: every load first (the dz stores below
+        // could alias them for the compiler), added in a fixed order:
+        // (dh_top | 0 + dx_above partials) + dh_rec partials
+        const int ni2 = nu > 8 ? 2 : 1;
+        float dhs[2][8];
+#pragma unroll
+        for (int i2 = 0; i2 < 2; ++i2)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) dhs[i2][k] = 0.f;
+        auto add8 = [](float (&d)[8], const float4& a, const float4& b) {
+          d[0] += a.x; d[1] += a.y; d[2] += a.z; d[3] += a.w; d[4] += b.x; d[5] += b.y; d[6] += b.z; d[7] += b.w;
+        };
+        if (Ly.dh_top) {
+#pragma unroll
+          for (int i2 = 0; i2 < 2; ++i2) {
+            if (i2 >= ni2) break;
+            const uint4 hv = *reinterpret_cast<const uint4*>(Ly.dh_top + ((size_t)r * T + t) * hd + u_base + 8 * i2);
+            const uint32_t w4[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
+              dhs[i2][2 * e] = f2.x;
+              dhs[i2][2 * e + 1] = f2.y;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int pk = 0; pk < 4; ++pk) {   // the Gk partials, in order
+            if (pk >= Gk) break;
+#pragma unroll
+            for (int i2 = 0; i2 < 2; ++i2) {
+              if (i2 >= ni2) break;
+              const float4* a4 = reinterpret_cast<const float4*>(Ly.dx_above + pk * P.dx_kstride +
+                                                                 ((size_t)r * T + t) * hd + u_base + 8 * i2);
+              add8(dhs[i2], __ldcg(a4), __ldcg(a4 + 1));
+            }
+          }
+        }
+        if (t < T - 1) {
+#pragma unroll
+          for (int pk = 0; pk < 4; ++pk) {
+            if (pk >= Gk) break;
+#pragma unroll
+            for (int i2 = 0; i2 < 2; ++i2) {
+              if (i2 >= ni2) break;
+              const float4* a4 = reinterpret_cast<const float4*>(Ly.dh_rec + pk * P.rec_kstride +
+                                                                 ((size_t)((t + 1) & 1) * P.B + r) * hd + u_base + 8 * i2);
+              add8(dhs[i2], __ldcg(a4), __ldcg(a4 + 1));
+            }
+          }
+        }
 #pragma unroll
         for (int i2 = 0; i2 < 2; ++i2) {
           const int k0 = i2 * 8;
           if (k0 >= nu) break;
           const int u0 = u_base + k0;
           float dh[8], cp[8], ct[8];
-          if (Ly.dh_top) {
-            const uint4 hv = *reinterpret_cast<const uint4*>(Ly.dh_top + ((size_t)r * T + t) * hd + u0);
-            const uint32_t w4[4] = {hv.x, hv.y, hv.z, hv.w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
-              dh[2 * e] = f2.x;
-              dh[2 * e + 1] = f2.y;
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) dh[k] = 0.f;
-            for (int pk = 0; pk < Gk; ++pk) {   // the Gk partials, in order
-              const float4* a4 = reinterpret_cast<const float4*>(Ly.dx_above + pk * P.dx_kstride +
-                                                                 ((size_t)r * T + t) * hd + u0);
-              const float4 a = __ldcg(a4), b = __ldcg(a4 + 1);
-              dh[0] += a.x; dh[1] += a.y; dh[2] += a.z; dh[3] += a.w; dh[4] += b.x; dh[5] += b.y; dh[6] += b.z; dh[7] += b.w;
-            }
-          }
-          if (t < T - 1) {
-            for (int pk = 0; pk < Gk; ++pk) {
-              const float4* a4 = reinterpret_cast<const float4*>(Ly.dh_rec + pk * P.rec_kstride +
-                                                                 ((size_t)((t + 1) & 1) * P.B + r) * hd + u0);
-              const float4 a = __ldcg(a4), b = __ldcg(a4 + 1);
-              dh[0] += a.x; dh[1] += a.y; dh[2] += a.z; dh[3] += a.w; dh[4] += b.x; dh[5] += b.y; dh[6] += b.z; dh[7] += b.w;
-            }
-          }
+          for (int k = 0; k < 8; ++k) dh[k] = dhs[i2][k];
           if (t == cap && Ly.inj_dh) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
