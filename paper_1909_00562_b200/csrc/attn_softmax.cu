@@ -166,8 +166,8 @@ static int g_opt_pdl = 1;
 // batched score / context GEMMs
 static int g_opt_attn_fused = 1;
 // "proj_bn": tile width of the Eq. 4 projection GEMM (K-major W_c allows
-// 16..256).  128 (400 tiles at C1, 2.7 waves on 148 SMs instead of 1.35) was
-// measured slower: 43.6 vs 36.0 us (same box)
+// 64, 128, 192, 256).  128 (400 tiles at C1, 2.7 waves on 148 SMs instead of
+// 1.35) was measured slower: 43.6 vs 36.0 us (same box); 192: 43.3 us
 static int g_opt_proj_bn = 256;
 // "attn_trace": device buffer of globaltimer stamps, [2][B][16] int64 (forward,
 // backward) + [B][64][4] backward chunk stamps (scripts/attn_trace.py)
@@ -291,7 +291,7 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
     return ATTN_OK;
   }
   if (!strcmp(key, "proj_bn")) {
-    if (value < 16 || value > 256 || value % 16) return fail(ATTN_ERR_INVALID_ARG, "proj_bn must be a multiple of 16 in [16, 256]");
+    if (value < 64 || value > 256 || value % 64) return fail(ATTN_ERR_INVALID_ARG, "proj_bn must be 64, 128, 192 or 256");
     g_opt_proj_bn = (int)value;
     return ATTN_OK;
   }
@@ -439,8 +439,11 @@ static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr
                              int pair) {
   memset(&pr, 0, sizeof(pr));
   const int bn = g.bn > 0 ? g.bn : TC_BN;
-  if (bn != TC_BN && (bn % 16 != 0 || bn > TC_BN || g.b_mn || g.b_nsplit))
-    return fail(ATTN_ERR_UNSUPPORTED, "tile width %d needs a K-major B", bn);
+  // narrower tiles: K-major B only, and whole 32-column epilogue chunks per
+  // 128-column warp half (widths that are not multiples of 64 gave wrong
+  // results: 160 and 224 were measured broken)
+  if (bn != TC_BN && (bn % 64 != 0 || bn > TC_BN || g.b_mn || g.b_nsplit))
+    return fail(ATTN_ERR_UNSUPPORTED, "tile width %d: needs a multiple of 64 and a K-major B", bn);
   const int tile_m = pair == 1 ? TC_BM : 2 * TC_BM;
   const int b_rows = bn;
   pr.M = g.M; pr.N = g.N; pr.K = g.K; pr.batch = g.batch;
@@ -1939,20 +1942,28 @@ extern "C" attn_status_t attn_softmax_fwd_bwd_host(
 struct StagingSlot {
   const void* ptr = nullptr;
   cudaEvent_t ready = nullptr;
+  int dev = -1;        // the device the event belongs to
 };
 static std::mutex g_stage_mu;
 static StagingSlot g_slots[8];
 static int g_slot_next = 0;
-static cudaStream_t g_copy_stream = nullptr;
-static cudaEvent_t g_free_ev = nullptr;
+// the H2D copy stream and its ordering event, one per device (created on first use)
+constexpr int kMaxDevices = 64;
+static cudaStream_t g_copy_stream[kMaxDevices] = {};
+static cudaEvent_t g_free_ev[kMaxDevices] = {};
 
-static attn_status_t staging_slot(const void* ptr, cudaEvent_t* ev) {
+static attn_status_t staging_slot(const void* ptr, int dev, cudaEvent_t* ev) {
   std::lock_guard<std::mutex> lk(g_stage_mu);
   for (auto& sl : g_slots)
-    if (sl.ptr == ptr) { *ev = sl.ready; return ATTN_OK; }
+    if (sl.ptr == ptr && sl.dev == dev) { *ev = sl.ready; return ATTN_OK; }
   StagingSlot& sl = g_slots[g_slot_next++ % 8];
+  if (sl.ready && sl.dev != dev) {   // an event of another device: replace it
+    CUDA_TRY(cudaEventDestroy(sl.ready));
+    sl.ready = nullptr;
+  }
   if (!sl.ready) CUDA_TRY(cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
   sl.ptr = ptr;
+  sl.dev = dev;
   *ev = sl.ready;
   return ATTN_OK;
 }
@@ -1984,28 +1995,35 @@ extern "C" attn_status_t attn_softmax_prefetch_host(const attn_shape_t* s, const
   if (staging_bytes < attn_softmax_host_staging_size(s))
     return fail(ATTN_ERR_WORKSPACE, "staging_bytes = %zu < required %zu", staging_bytes,
                 attn_softmax_host_staging_size(s));
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev >= kMaxDevices) return fail(ATTN_ERR_UNSUPPORTED, "prefetch: device %d >= %d", dev, kMaxDevices);
+  cudaStream_t copy_stream;
+  cudaEvent_t free_ev;
   {
     std::lock_guard<std::mutex> lk(g_stage_mu);
-    if (!g_copy_stream) {
-      CUDA_TRY(cudaStreamCreateWithFlags(&g_copy_stream, cudaStreamNonBlocking));
-      CUDA_TRY(cudaEventCreateWithFlags(&g_free_ev, cudaEventDisableTiming));
+    if (!g_copy_stream[dev]) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&g_copy_stream[dev], cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&g_free_ev[dev], cudaEventDisableTiming));
     }
+    copy_stream = g_copy_stream[dev];
+    free_ev = g_free_ev[dev];
   }
   cudaEvent_t ready;
-  if ((st = staging_slot(staging, &ready)) != ATTN_OK) return st;
+  if ((st = staging_slot(staging, dev, &ready)) != ATTN_OK) return st;
   // the staging buffer is free once everything enqueued on `stream` so far is done
-  CUDA_TRY(cudaEventRecord(g_free_ev, (cudaStream_t)stream_));
-  CUDA_TRY(cudaStreamWaitEvent(g_copy_stream, g_free_ev, 0));
+  CUDA_TRY(cudaEventRecord(free_ev, (cudaStream_t)stream_));
+  CUDA_TRY(cudaStreamWaitEvent(copy_stream, free_ev, 0));
   const size_t elt = s->dtype == ATTN_BF16 ? 2 : 4;
   const size_t T = (size_t)s->batch * s->tgt_len;
   StagingViews v = staging_views(s, staging);
   CUDA_TRY(cudaMemcpyAsync(v.H_dec, H_dec_host, elt * T * s->hidden, cudaMemcpyHostToDevice,
-                           g_copy_stream));
+                           copy_stream));
   CUDA_TRY(cudaMemcpyAsync(v.H_enc, H_enc_host, elt * (size_t)s->batch * s->src_len * s->hidden,
-                           cudaMemcpyHostToDevice, g_copy_stream));
+                           cudaMemcpyHostToDevice, copy_stream));
   CUDA_TRY(cudaMemcpyAsync(v.ids, tgt_ids_host, sizeof(int32_t) * T, cudaMemcpyHostToDevice,
-                           g_copy_stream));
-  CUDA_TRY(cudaEventRecord(ready, g_copy_stream));
+                           copy_stream));
+  CUDA_TRY(cudaEventRecord(ready, copy_stream));
   return ATTN_OK;
 }
 
@@ -2020,8 +2038,10 @@ extern "C" attn_status_t attn_softmax_fwd_bwd_staged(
   if (staging_bytes < attn_softmax_host_staging_size(s))
     return fail(ATTN_ERR_WORKSPACE, "staging_bytes = %zu < required %zu", staging_bytes,
                 attn_softmax_host_staging_size(s));
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
   cudaEvent_t ready;
-  if ((st = staging_slot(staging, &ready)) != ATTN_OK) return st;
+  if ((st = staging_slot(staging, dev, &ready)) != ATTN_OK) return st;
   cudaStream_t stream = (cudaStream_t)stream_;
   CUDA_TRY(cudaStreamWaitEvent(stream, ready, 0));
   StagingViews v = staging_views(s, staging);
