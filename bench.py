@@ -301,6 +301,42 @@ def measure_next_rows(binding, st, dv, cfg, scale, comm, stream, dev, pk, tok_lo
             del st_sl
         finally:
             binding.attn_softmax_set_option("store_logits", 0)
+    # context rows, NOT the product path: the same stage as a
+    # torch eager bf16 composition with autograd (cuBLAS / cuDNN kernels, the
+    # logits materialised), and one cuBLAS GEMM at the vocabulary shape
+    if cfg.dtype == "bf16" and comm is None:
+        import torch.nn.functional as F
+        B_, N_, M_, d_ = cfg.B, cfg.N, cfg.M, cfg.d
+        srcl = torch.as_tensor(np.asarray(dv["src_len"]), device=dev)
+        tgtl = torch.as_tensor(np.asarray(dv["tgt_len"]), device=dev)
+        kmask = (torch.arange(M_, device=dev)[None, :] < srcl[:, None])[:, None, :]
+        valid = (torch.arange(N_, device=dev)[None, :] < tgtl[:, None]).reshape(-1)
+        y = dv["tgt_ids"].long().reshape(-1)
+
+        def eager():
+            H = dv["H_dec"].detach().requires_grad_()
+            S = dv["H_enc"].detach().requires_grad_()
+            Wc = dv["W_c"].detach().requires_grad_()
+            Wo = dv["W_out"].detach().requires_grad_()
+            e = torch.bmm(H, S.transpose(1, 2)).float().masked_fill(~kmask, float("-inf"))
+            a = torch.softmax(e, -1).to(torch.bfloat16)
+            C = torch.bmm(a, S)
+            Hc = torch.tanh(torch.cat([H, C], -1) @ Wc.T).reshape(-1, d_)
+            logits = Hc @ Wo.T
+            loss = F.cross_entropy(logits[valid].float(), y[valid], reduction="sum") * scale
+            loss.backward()
+            return loss
+
+        ms = timed(eager, n=5)
+        hc = torch.randn(B_ * N_, d_, device=dev).to(torch.bfloat16)
+        ms_mm = timed(lambda: hc @ dv["W_out"].T, n=5)
+        res["context_torch_eager"] = {
+            "ms_per_step": ms, "target_tokens_per_s": tok_local / (ms / 1e3),
+            "vocab_gemm_ms": ms_mm, "vocab_gemm_tflops": 2.0 * B_ * N_ * d_ * cfg.V / (ms_mm / 1e3) / 1e12,
+            "note": "context only (not the product): the stage as torch eager bf16 ops + autograd "
+                    "(logits [T, V] materialised), and one cuBLAS GEMM H_c W_out^T at the vocabulary shape"}
+        del hc
+        torch.cuda.empty_cache()
     # NEXT-4: one beam-search decoding step, beam 5 on the config's sentences
     # (rows = B x 5 hypotheses; fused vocab GEMM + online LSE + top-k epilogue)
     if cfg.dtype == "bf16":
