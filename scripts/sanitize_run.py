@@ -3,8 +3,10 @@ racecheck / synccheck): tiny (fp32 SIMT path), small and odd (bf16 tcgen05
 path: persistent vocab launch on CTA pairs and on single CTAs, and with the
 forward fused; small / edge_min through the fused attention kernels, odd
 through the generic batched attention), edge_min; then the decoding step,
-Adam and the NEXT-3 encoder-decoder wavefront.  Exits non-zero on a library
-error."""
+Adam and the NEXT-3 encoder-decoder wavefront; small512 (the 512-column G2 /
+G3 tiles) and lstm_train (the NEXT-3 training forward and the reverse
+wavefront with its K split and dz multicast) on request or by default.
+Exits non-zero on a library error."""
 import os
 import sys
 
@@ -15,9 +17,12 @@ from paper_1909_00562_b200 import binding
 from paper_1909_00562_b200.stage import AttnSoftmaxStage, DecodeStep, to_device
 from synthetic import CONFIGS, global_valid_tokens, make_inputs
 
+from dataclasses import replace as _replace
+
+CONFIGS = dict(CONFIGS, small512=_replace(CONFIGS["small"], name="small512", d=512, V=3001))
 cases = [("tiny", {}), ("small", {}), ("small", {"vb_pair": 0}), ("odd", {"vb_fwd_fused": 1}),
-         ("edge_min", {}), ("small", {"bias": 1})]
-only = sys.argv[1:] 
+         ("edge_min", {}), ("small", {"bias": 1}), ("small512", {})]   # small512: 512-column G2 / G3 tiles
+only = sys.argv[1:]
 for name, opts in cases:
     if only and name not in only:
         continue
@@ -62,3 +67,20 @@ if not only or "lstm" in only:
                 bf(li["E_src"]), bf(li["E_tgt"]))
     torch.cuda.synchronize()
     print("lstm ok", float(Hd.float().abs().mean()), flush=True)
+
+if not only or "lstm_train" in only:
+    # the reverse wavefront: K split in two with dz multicast over CTA pairs
+    # (hidden 256: G = 8, two column groups of 4 per K half)
+    import numpy as np
+    from paper_1909_00562_b200.stage import EncoderDecoderTrainer
+    from synthetic import make_lstm_inputs
+    cfg = CONFIGS["small"]
+    li = make_lstm_inputs(cfg, layers=2, emb=128)
+    bf = lambda a: torch.from_numpy(np.asarray(a, np.float32)).cuda().to(torch.bfloat16)
+    tr = EncoderDecoderTrainer(cfg.B, cfg.M, cfg.N, 128, cfg.d, 2, cfg.V, cfg.V)
+    tr.set_weights([tuple(bf(w) for w in ws) for ws in li["enc"]], [tuple(bf(w) for w in ws) for ws in li["dec"]])
+    He, Hd = tr.forward(torch.from_numpy(li["src_ids"]).cuda(), torch.from_numpy(li["tgt_ids"]).cuda(),
+                        li["src_len"], bf(li["E_src"]), bf(li["E_tgt"]))
+    g = tr.backward(torch.randn_like(He) * 1e-3, torch.randn_like(Hd) * 1e-3)
+    torch.cuda.synchronize()
+    print("lstm train ok", float(g["dE_src"].abs().sum()), flush=True)
