@@ -2190,7 +2190,7 @@ extern "C" attn_status_t attn_softmax_decode_step(
         ATTN_OK)
       return st;
   }
-  st = launch_pdl(decode_final_kernel, dim3((unsigned)((p.T + 1) / 2)), dim3(64), stream,
+  st = launch_pdl(decode_final_kernel, dim3((unsigned)p.T), dim3(DF_THREADS), stream,
                   (const float2*)b.part, (const uint32_t*)topk, p.part_ld, (int)p.T, k, (int*)topk_ids,
                   topk_logp, lse);
   return st;

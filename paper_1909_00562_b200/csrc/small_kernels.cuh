@@ -239,40 +239,51 @@ __global__ void __launch_bounds__(256) colsum_final_kernel(const float* __restri
   db[c] = t;
 }
 
-// One warp per row (2 per block): lse from the (max, sumexp) partials (as
+// One block of 4 warps per row: lse from the (max, sumexp) partials (as
 // lse_reduce) and the k <= 8 best (logit, token) pairs merged from the
-// per-slot sorted top-8 lists: each lane merges its slots' lists with
-// branch-free bitonic top-8 merges of 64-bit keys (epilogue.cuh tk_*), then a
-// butterfly across the lanes.  The key order is total, so the result is
-// unique.
-__global__ void __launch_bounds__(64) decode_final_kernel(const float2* __restrict__ part,
-                                                          const uint32_t* __restrict__ topk,
-                                                          int part_ld, int T, int k,
-                                                          int* __restrict__ ids,
-                                                          float* __restrict__ logp,
-                                                          float* __restrict__ lse_out) {
+// per-slot sorted top-8 lists: thread i takes slots i, i + 128, ..., merges
+// their lists with branch-free bitonic top-8 merges of 64-bit keys
+// (epilogue.cuh tk_*), then a butterfly across each warp's lanes and warp 0
+// merges the four warps' lists.  The key order is total, so the result is
+// unique; the lse sums run in a fixed order (per thread, then the lanes, then
+// the warps).
+constexpr int DF_THREADS = 128;
+__global__ void __launch_bounds__(DF_THREADS) decode_final_kernel(const float2* __restrict__ part,
+                                                                  const uint32_t* __restrict__ topk,
+                                                                  int part_ld, int T, int k,
+                                                                  int* __restrict__ ids,
+                                                                  float* __restrict__ logp,
+                                                                  float* __restrict__ lse_out) {
   pdl_wait();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row = blockIdx.x * 2 + warp;
+  __shared__ float red[DF_THREADS / 32];
+  __shared__ unsigned long long lists[DF_THREADS / 32][8];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int row = blockIdx.x;
   if (row >= T) return;
   const float2* pr = part + (long long)row * part_ld;
   float mx = -INFINITY;
-  for (int j = lane; j < part_ld; j += 32) mx = fmaxf(mx, pr[j].x);
+  for (int j = tid; j < part_ld; j += DF_THREADS) mx = fmaxf(mx, pr[j].x);
   mx = warp_max(mx);
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  __syncthreads();
   float s = 0.f;
-  for (int j = lane; j < part_ld; j += 32) {
+  for (int j = tid; j < part_ld; j += DF_THREADS) {
     const float2 q = pr[j];
     if (q.y > 0.f) s += q.y * __expf(q.x - mx);
   }
   s = warp_sum(s);
-  const float lse = mx + logf(s);
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  const float lse = mx + logf(((red[0] + red[1]) + red[2]) + red[3]);
   // slot j covers columns [128 j, 128 j + 128): its 32-bit keys become
-  // 64-bit (value, token) keys, merged across slots and lanes
+  // 64-bit (value, token) keys, merged across slots, lanes and warps
   unsigned long long best[8], b2[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) best[i] = 0ull;
   const uint4* tk = reinterpret_cast<const uint4*>(topk + (long long)row * part_ld * 8);
-  for (int j = lane; j < part_ld; j += 32) {
+  for (int j = tid; j < part_ld; j += DF_THREADS) {
     const uint4 a = tk[(long long)j * 2], c = tk[(long long)j * 2 + 1];
     const uint32_t kk[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
 #pragma unroll
@@ -286,7 +297,16 @@ __global__ void __launch_bounds__(64) decode_final_kernel(const float2* __restri
     for (int i = 0; i < 8; ++i) b2[i] = __shfl_xor_sync(0xffffffffu, best[i], o);
     tk_merge8(best, b2);
   }
-  if (lane == 0) {
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) lists[warp][i] = best[i];
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < DF_THREADS / 32; ++w) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) b2[i] = lists[w][i];
+      tk_merge8(best, b2);
+    }
     for (int i = 0; i < k; ++i) {
       ids[(long long)row * k + i] = tk_id(best[i]);
       logp[(long long)row * k + i] = tk_val(best[i]) - lse;
