@@ -439,11 +439,14 @@ static attn_status_t fill_tc(const GemmDesc& g, CUtensorMap* maps, TcProblem& pr
                              int pair) {
   memset(&pr, 0, sizeof(pr));
   const int bn = g.bn > 0 ? g.bn : TC_BN;
-  // narrower tiles: K-major B only, and whole 32-column epilogue chunks per
-  // 128-column warp half (widths that are not multiples of 64 gave wrong
-  // results: 160 and 224 were measured broken)
-  if (bn != TC_BN && (bn % 64 != 0 || bn > TC_BN || g.b_mn || g.b_nsplit))
-    return fail(ATTN_ERR_UNSUPPORTED, "tile width %d: needs a multiple of 64 and a K-major B", bn);
+  // narrower tiles: K-major B only.  The generic epilogues need widths that
+  // are multiples of 64 (160 and 224 were measured broken); the attention
+  // softmax epilogues (tile width = the source positions rounded to 32) handle
+  // any multiple of 32 up to 256
+  const bool attn_epi = g.epi.kind == EPI_ATTN_SOFTMAX || g.epi.kind == EPI_ATTN_SOFTMAX_BWD;
+  if (bn != TC_BN && (bn % (attn_epi ? 32 : 64) != 0 || bn > TC_BN || g.b_mn || g.b_nsplit))
+    return fail(ATTN_ERR_UNSUPPORTED, "tile width %d: needs a multiple of %d and a K-major B", bn,
+                attn_epi ? 32 : 64);
   const int tile_m = pair == 1 ? TC_BM : 2 * TC_BM;
   const int b_rows = bn;
   pr.M = g.M; pr.N = g.N; pr.K = g.K; pr.batch = g.batch;

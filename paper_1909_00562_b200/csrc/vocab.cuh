@@ -61,6 +61,12 @@
 
 namespace attnsm {
 
+// VB_DEBUG_MMA=1 compiles the timing-only MMA-issue variants of VbParams::debug
+// bits 6 and 8-12 (development builds only: they slow the default issue loop)
+#ifndef VB_DEBUG_MMA
+#define VB_DEBUG_MMA 0
+#endif
+
 constexpr int VB_BN = 256;
 constexpr int VB_BK = 64;
 constexpr int VB_EPI_WARPS = 8;
@@ -134,11 +140,14 @@ struct alignas(64) VbParams {
   int order;             // 0: block c+1 = G3(c), G2(c), G1(c+1); 1: G1(c+1), G3(c), G2(c)
   int l2hints;           // bit 0: H_c loads evict-last; bit 1: dHc updates evict-last;
                          // bit 2: dL stores evict-last
-  long long* trace;      // debug: 16 int64 per tile and CTA rank (see VB_TRACE), NULL = off
+  long long* trace;      // debug: 32 int64 per tile and CTA rank (see VB_TRACE), NULL = off
   int debug;             // timing experiments only (WRONG results): bit 0 skip the G1 stores,
                          // bit 1 skip the G1 exponentials, bit 2 skip the G2 / G3 stores,
                          // bit 3 publish tiles without waiting for their stores to land,
-                         // bit 4 / 5 skip the B / A operand loads
+                         // bit 4 / 5 skip the B / A operand loads, bit 6 G1 reads its B
+                         // operand MN-major (garbage values), bit 7 G1 epilogue skips
+                         // its TMEM loads, bits 8 / 9 G1 k-steps as 2 x N = 128 / 4 x N = 64
+                         // MMAs sharing A
   int blk_start[VB_MAX_BLOCKS + 2];   // backward blocks, relative to fwd_tiles
 };
 
@@ -212,13 +221,14 @@ __device__ __forceinline__ VbTile vb_decode(const VbParams& P, int t) {
   return r;
 }
 
-// trace record of tile t and CTA rank r (option "vb_trace"), at (2 t + r) * 16:
+// trace record of tile t and CTA rank r (option "vb_trace"), at (2 t + r) * 32:
 // [0] smid [1] type << 16 | chunk  [2] / [3] producer globaltimer before / after
 // the dependency wait  [4] / [5] MMA clock64 first MMA issued / last commit
 // [6] / [7] epilogue warp 0 clock64 accumulator ready / tile done  [8] / [9] MMA
 // globaltimer first MMA / last commit  [10] / [11] epilogue globaltimer ready /
 // done  [12] epilogue clock64 after its dependency wait  [13] MMA clock64
 // accumulator free  [14] MMA cycles spent waiting for full stages
+// [16] epilogue warp 0 clock64 when it releases the (last) accumulator
 __device__ __forceinline__ long long vb_clk() {
   long long c;
   asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
@@ -233,7 +243,7 @@ __device__ __forceinline__ long long vb_gt() {
   do {                                                                       \
     if (P.trace) {                                                           \
       const long long v_ = (val);                                            \
-      if (lane == 2) P.trace[((long long)(t) * 2 + rank) * 16 + (i)] = v_;   \
+      if (lane == 2) P.trace[((long long)(t) * 2 + rank) * 32 + (i)] = v_;   \
     }                                                                        \
   } while (0)
 
@@ -272,6 +282,49 @@ __device__ __forceinline__ float warp_colsum32(float (&v)[32], uint32_t lane) {
   }
   return v[0];
 }
+
+#if VB_DEBUG_MMA
+// Timing-only MMA-issue variants of G1 k-blocks (VbParams::debug; WRONG
+// results): bits 8 / 9 two N = 128 / four N = 64 MMAs sharing A (bit 12: the
+// two N = 128 chains 256 columns apart), bits 10 / 11 two N = 256 MMAs into both
+// accumulators with the same A and B / the A of another stage.  Returns true if
+// it issued the k-block.
+template <bool kPair>
+__device__ __noinline__ bool vb_debug_mma(const VbParams& P, const VbTile& tl, int kb, int s, int acc,
+                                          uint32_t tmem_base, uint8_t* smem, int a_mn, int b_mn,
+                                          uint64_t ad, uint64_t bd) {
+  using Cfg = VbCfg<kPair>;
+  if (tl.type != VB_G1) return false;
+  const uint32_t a_k16 = a_mn ? 128u : 2u, b_k16 = b_mn ? 128u : 2u;
+  const int nsplit = (P.debug & (256 | 4096)) ? 2 : (P.debug & 512) ? 4 : 1;
+  const int dual = (P.debug & 1024) ? 1 : (P.debug & 2048) ? 2 : 0;
+  if (nsplit == 1 && !dual) return false;
+  const uint32_t dcol = tmem_base + acc * VB_BN;
+  if (nsplit > 1) {
+    const uint32_t qstride = (P.debug & 4096) ? 256u : (uint32_t)(VB_BN / nsplit);
+    const uint32_t idn = umma_idesc_bf16(Cfg::TM, VB_BN / nsplit, a_mn, b_mn);
+    for (int k = 0; k < VB_BK / 16; ++k)
+      for (int q = 0; q < nsplit; ++q) {
+        const uint64_t bq = bd + k * b_k16 + (uint32_t)(q * (Cfg::B_BYTES / nsplit)) / 16;
+        const uint32_t d = tmem_base + ((acc * VB_BN + q * qstride) & 511u);
+        if constexpr (kPair) umma_bf16_pair(d, ad + k * a_k16, bq, idn, (kb > 0 || k > 0) ? 1u : 0u);
+        else umma_bf16(d, ad + k * a_k16, bq, idn, (kb > 0 || k > 0) ? 1u : 0u);
+      }
+    return true;
+  }
+  const uint32_t idesc = umma_idesc_bf16(Cfg::TM, VB_BN, a_mn, b_mn);
+  const uint64_t ado = ad + (uint32_t)(((s + 1) % Cfg::STAGES - s) * Cfg::STAGE) / 16;
+  for (int k = 0; k < VB_BK / 16; ++k) {
+    const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+    if constexpr (kPair) {
+      umma_bf16_pair(dcol, ad + k * a_k16, bd + k * b_k16, idesc, accum);
+      umma_bf16_pair(tmem_base + (acc ^ 1) * VB_BN, (dual == 1 ? ad : ado) + k * a_k16,
+                     bd + k * b_k16, idesc, accum);
+    }
+  }
+  return true;
+}
+#endif
 
 template <bool kPair>
 __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_constant__ VbParams P) {
@@ -430,6 +483,12 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           if (leader)
             mbar_arrive_expect_tx(&full[s], ((ldA ? Cfg::A_BYTES : 0) + (ldB ? Cfg::B_BYTES : 0)) * Cfg::CTAS);
           const int k0 = kb * VB_BK;
+#if VB_DEBUG_MMA
+          if (tl.type == VB_G1 && (P.debug & 64)) {
+            if (ldA) vb_load<kPair>(sA, &P.m_hc_k, &full[s], barc, k0, arow, 0, pol_keep);
+            if (ldB) vb_load4<kPair>(sB, &P.m_wo_mn, &full[s], barc, 0, c0 + k0, (bcol % P.d) / 64, 0, pol_norm);
+          } else
+#endif
           if (tl.type == VB_G1 || tl.type == VB_G0) {
             if (ldA) vb_load<kPair>(sA, &P.m_hc_k, &full[s], barc, k0, arow, 0, pol_keep);
             if (ldB) vb_load<kPair>(sB, &P.m_wo_k, &full[s], barc, k0, bcolg, 0, pol_norm);
@@ -468,27 +527,40 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
       tl = tl_nxt;
     }
   } else if (warp == kWarpMma) {
+    // ---------------- MMA issuer: the pair leader's warp runs the loop, one
+    // elected lane issues for both CTAs (the uniform datapath: a lane-0-only
+    // loop measured 988 instead of 751 cycles per G1 k-block).  The loop is
+    // kept lean -- descriptors are templates plus the stage address -- because
+    // its issue rate is on the critical path (extra code in it measured 1000
+    // cycles per G1 k-block)
     if (leader) {
-      // ---------------- MMA issuer (pair: the leader issues for both CTAs)
       int s = 0;
       uint32_t ph = 0;
       int r = 0;
       uint32_t rph = 0;
       int acc = 0;
       uint32_t aph = 0;
-      int t = ring_read(r, rph, false);
-      VbTile tl{};
-      if (t >= 0) tl = vb_decode<kPair>(P, t);
+      auto ring_read1 = [&]() -> int { return ring_read(r, rph, false); };
+      const uint32_t smem16 = smem_u32(smem) >> 4;   // descriptor start-address units
+      constexpr uint32_t kStage16 = Cfg::STAGE >> 4, kA16 = Cfg::A_BYTES >> 4;
+      int t = ring_read1();
       while (t >= 0) {
+        const VbTile tl = vb_decode<kPair>(P, t);
         const int a_mn = tl.type == VB_G2 ? 1 : 0;
+#if VB_DEBUG_MMA
+        const int b_mn = (tl.type == VB_G3 || tl.type == VB_G2 || (tl.type == VB_G1 && (P.debug & 64))) ? 1 : 0;
+#else
         const int b_mn = (tl.type == VB_G3 || tl.type == VB_G2) ? 1 : 0;
+#endif
         const uint32_t idesc = umma_idesc_bf16(TM, VB_BN, a_mn, b_mn);
-        const uint32_t a_lbo = a_mn ? 8192u : 16u, b_lbo = b_mn ? 8192u : 16u;
-        const uint32_t a_kstep = a_mn ? 2048u : 32u, b_kstep = b_mn ? 2048u : 32u;
+        // descriptor templates (start address 0): + (stage address >> 4) + k-step
+        const uint64_t ad0 = umma_sdesc(0, a_mn ? 8192u : 16u, 1024);
+        const uint64_t bd0 = umma_sdesc(0, b_mn ? 8192u : 16u, 1024);
+        const uint32_t a_k16 = a_mn ? (2048u >> 4) : (32u >> 4);
+        const uint32_t b_k16 = b_mn ? (2048u >> 4) : (32u >> 4);
         const int kb_read = tl.kb_total > 1 ? 1 : 0;
         const bool wide = kPair && P.wide && (tl.type == VB_G2 || tl.type == VB_G3);
         int t_nxt = -1;
-        VbTile tl_nxt{};
         // a wide tile takes both accumulators: slot acc, then the next one
         const int acc2 = acc ^ 1;
         const uint32_t aph2 = acc2 == 0 ? (aph ^ 1) : aph;
@@ -513,20 +585,24 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
             if (wide) mbar_wait(&full[s2], ph2);
           }
           tc_fence_after();
+          const uint32_t sa16 = smem16 + (uint32_t)s * kStage16;
+          const uint64_t ad = ad0 + sa16;
+          const uint64_t bd = bd0 + sa16 + kA16;
+          const uint64_t bd2 = bd0 + smem16 + (uint32_t)s2 * kStage16 + kA16;
           if (elect_one()) {
-            const uint32_t sA = smem_u32(smem + s * Cfg::STAGE);
-            const uint32_t sB = sA + Cfg::A_BYTES;
-            const uint32_t sB2 = smem_u32(smem + s2 * Cfg::STAGE) + Cfg::A_BYTES;
+#if VB_DEBUG_MMA
+            if (vb_debug_mma<kPair>(P, tl, kb, s, acc, tmem_base, smem, a_mn, b_mn, ad, bd)) {
+            } else
+#endif
+            {
 #pragma unroll
-            for (int k = 0; k < VB_BK / 16; ++k) {
-              const uint64_t ad = umma_sdesc(sA + k * a_kstep, a_lbo, 1024);
-              const uint64_t bd = umma_sdesc(sB + k * b_kstep, b_lbo, 1024);
-              if constexpr (kPair) umma_bf16_pair(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
-              else umma_bf16(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
-              if constexpr (kPair) {
-                if (wide) {
-                  const uint64_t bd2 = umma_sdesc(sB2 + k * b_kstep, b_lbo, 1024);
-                  umma_bf16_pair(dcol2, ad, bd2, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              for (int k = 0; k < VB_BK / 16; ++k) {
+                const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+                if constexpr (kPair) {
+                  umma_bf16_pair(dcol, ad + k * a_k16, bd + k * b_k16, idesc, accum);
+                  if (wide) umma_bf16_pair(dcol2, ad + k * a_k16, bd2 + k * b_k16, idesc, accum);
+                } else {
+                  umma_bf16(dcol, ad + k * a_k16, bd + k * b_k16, idesc, accum);
                 }
               }
             }
@@ -545,10 +621,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           s = s2;
           ph = ph2;
           if (++s == STAGES) { s = 0; ph ^= 1; }
-          if (kb == kb_read) {
-            t_nxt = ring_read(r, rph, false);
-            if (t_nxt >= 0) tl_nxt = vb_decode<kPair>(P, t_nxt);
-          }
+          if (kb == kb_read) t_nxt = ring_read1();
         }
         if (elect_one()) {
           if constexpr (kPair) {
@@ -565,9 +638,9 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
         if (++acc == 2) { acc = 0; aph ^= 1; }
         if (wide && ++acc == 2) { acc = 0; aph ^= 1; }
         t = t_nxt;
-        tl = tl_nxt;
       }
     }
+    __syncwarp();
   } else if (warp == 8 || warp == 9) {
     // ---------------- LSE (Eq. 6) of row blocks p, p + pairs, ... (pair p):
     // this CTA's 128 rows, two per thread, once the row block's G0 tiles have
@@ -728,6 +801,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           if (kPair && !leader) mbar_arrive_cluster(leader_addr(&tempty[acc]));
           else mbar_arrive(&tempty[acc]);
         }
+        if (warp == 0) VB_TRACE(t, 16, vb_clk());
         if (row_ok && has_t) P.tgt_logit[row] = tval;
         // the two column halves of a row merge through shared memory (warp q
         // + 4 hands its (max, sum) to warp q; named barrier 2 + q, 64 threads)
@@ -783,10 +857,12 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
         }
         const int nvalid = tl.vcc - colh;   // valid columns of this warp's 128 (may be <= 0)
         uint32_t raw[32];
-        tmem_ld32_issue(taddr, raw);
-        tmem_ld_wait_regs(raw);
+        if (!(P.debug & 128)) {
+          tmem_ld32_issue(taddr, raw);
+          tmem_ld_wait_regs(raw);
+        }
 #pragma unroll 1
-        for (int cc = 0; cc < 4; ++cc) {
+        for (int cc = 0; cc < 4 && !(P.debug & 128); ++cc) {
           float v[32];
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(raw[e]);
@@ -853,6 +929,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           if (kPair && !leader) mbar_arrive_cluster(leader_addr(&tempty[acc]));
           else mbar_arrive(&tempty[acc]);
         }
+        if (warp == 0) VB_TRACE(t, 16, vb_clk());
         // publish: this warp's 32 x 128 piece of dL_c is in memory
         if (lane == 0) {
           if (!(P.debug & 8)) bulk_wait0();
@@ -925,6 +1002,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
             if (kPair && !leader) mbar_arrive_cluster(leader_addr(&tempty[acc]));
             else mbar_arrive(&tempty[acc]);
           }
+          if (warp == 0) VB_TRACE(t, 16, vb_clk());
           if (lane == 0) {
             if (!(P.debug & 8)) bulk_wait0();
             fence_proxy_async_global();

@@ -26,12 +26,12 @@ args = (dv["H_dec"], dv["H_enc"], dv["src_len"], dv["tgt_len"], dv["tgt_ids"], d
         dv["W_out"], scale)
 for _ in range(3):
     st(*args, out=out)
-tr = torch.zeros(400000 * 16, dtype=torch.int64, device="cuda")
+tr = torch.zeros(400000 * 32, dtype=torch.int64, device="cuda")
 binding.attn_softmax_set_option("vb_trace", tr.data_ptr())
 st(*args, out=out)
 torch.cuda.synchronize()
 binding.attn_softmax_set_option("vb_trace", 0)
-t = tr.view(-1, 16).cpu().numpy()
+t = tr.view(-1, 32).cpu().numpy()
 t = t[0::2]   # rank 0 of each tile (the pair leader records the MMA stamps)
 n = int(np.max(np.nonzero(t[:, 4])[0])) + 1
 t = t[:n]
@@ -61,6 +61,8 @@ for k in (3, 0, 1, 2):
     if not sel.any():
         continue
     kb = {0: d // 64, 1: vc // 64, 2: (T + 63) // 64, 3: d // 64}[k]
+    if k in (1, 2) and int(opts.get("vb_wide", 1)) and d % 512 == 0:
+        kb *= 2   # a wide k-block is two N = 256 MMAs: count 512-cycle units
     span = (t[sel, 5] - t[sel, 4])
     ghz = np.median(span / np.maximum(t[sel, 9] - t[sel, 8], 1))
     print(f"  {names[k]:11s} {sel.sum():5d} tiles: MMA span/kblock median {np.median(span) / kb:.0f} "
@@ -68,7 +70,8 @@ for k in (3, 0, 1, 2):
           f"{np.median(t[sel, 14] / np.maximum(span, 1)):.2f}; producer dep wait median "
           f"{np.median(t[sel, 3] - t[sel, 2]) / 1e3:.2f} us p90 {np.percentile(t[sel, 3] - t[sel, 2], 90) / 1e3:.2f}; "
           f"epilogue {np.median(t[sel, 7] - t[sel, 6]):.0f} cyc (dep wait {np.median(t[sel, 12] - t[sel, 6]):.0f}, "
-          f"p90 {np.percentile(t[sel, 12] - t[sel, 6], 90):.0f}); SM clock {ghz:.2f} GHz")
+          f"p90 {np.percentile(t[sel, 12] - t[sel, 6], 90):.0f}); accumulator held {np.median(t[sel, 16] - t[sel, 6]):.0f} cyc "
+          f"after ready, {np.median(t[sel, 16] - t[sel, 5]):.0f} after the last MMA issue; SM clock {ghz:.2f} GHz")
 busy, gaps, accw = [], [], []
 tm_ = t[mm]
 for sm in np.unique(tm_[:, 0]):
