@@ -141,6 +141,15 @@ static int g_opt_vb_pair = 1;
 // G2(c), G1(c+1)]; 1 = [G1(c+1), G3(c), G2(c)] (chunk c's consumers run a
 // whole G1 set after its producers; needs dl_buffers >= 3)
 static int g_opt_vb_order = 1;
+// order 2 (row-interleaved): "vb_lag" = row blocks between G1 and G3 of a row
+// block, "vb_g2split" = G2 split over T in two row halves
+static int g_opt_vb_lag = 2;
+static int g_opt_vb_g2split = 1;
+// "vb_claim": when a pair claims its next tile: 0 = right after the current
+// tile's first load, 1 = two k-blocks before the end of its loads (default: a
+// claimed tile never waits behind a long one; C1 vocab backward 1.57-1.59 ->
+// 1.52 ms, two alternating same-box pairs), -1 = 1 for order 2 only
+static int g_opt_vb_claim = 1;
 static int g_vb_debug = 0;    // "vb_debug": timing experiments (vocab.cuh VbParams::debug)
 static int g_opt_vb_wide = 1; // "vb_wide": 512-column G2 / G3 tiles on CTA pairs (VbParams::wide)
 static int g_opt_vb_l2 = 3;   // "vb_l2hints": VbParams::l2hints
@@ -233,7 +242,21 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
     return ATTN_OK;
   }
   if (!strcmp(key, "vb_order")) {
+    if (value < 0 || value > 2) return fail(ATTN_ERR_INVALID_ARG, "vb_order must be 0, 1 or 2");
     g_opt_vb_order = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "vb_lag")) {
+    if (value < 0 || value > 64) return fail(ATTN_ERR_INVALID_ARG, "vb_lag must be in [0, 64]");
+    g_opt_vb_lag = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "vb_claim")) {
+    g_opt_vb_claim = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "vb_g2split")) {
+    g_opt_vb_g2split = value != 0;
     return ATTN_OK;
   }
   if (!strcmp(key, "vb_pair")) {
@@ -1383,12 +1406,13 @@ static attn_status_t attention_backward_tc(const Plan& p, const void* H, const v
 // F4 + F5 + B1 as one launch (vocab.cuh): tensor maps, dispatch blocks,
 // counters.  Counter layout in `ctr` (zeroed by the caller): [0] tile
 // counter, [1] g5count (LSE CTA-portions), then g0done [nrb], lsedone [nrb], rowdone
-// [nchunks][nrb], coldone [nchunks][ncolf], consumed [nchunks], g2done
-// [nchunks], dhcdone [nrb][ndt], and blockpart (double [nrb * CTAS]) at the
+// [nchunks][nrb], coldone [nchunks][2][ncolf], consumed [nchunks], g2done
+// [nchunks], dhcdone [nrb][ndt], g2part [nchunks][n2max], and blockpart (double [nrb * CTAS]) at the
 // end, 8-byte aligned (vb_ctr_layout).
 struct VbLayout {
   int TM, nrb, ndt, ncolf;
-  size_t g0done, lsedone, rowdone, coldone, consumed, g2done, dhcdone, blockpart, total;
+  size_t g0done, lsedone, rowdone, coldone, consumed, g2done, dhcdone, g2part, blockpart, total;
+  int n2max;
 };
 static VbLayout vb_ctr_layout(const Plan& p, bool pair) {
   VbLayout L;
@@ -1401,10 +1425,12 @@ static VbLayout vb_ctr_layout(const Plan& p, bool pair) {
   L.lsedone = L.g0done + L.nrb;
   L.rowdone = L.lsedone + L.nrb;
   L.coldone = L.rowdone + nch * L.nrb;
-  L.consumed = L.coldone + nch * L.ncolf;
+  L.consumed = L.coldone + 2 * nch * L.ncolf;          // [nchunks][row half][ncolf]
   L.g2done = L.consumed + nch;
   L.dhcdone = L.g2done + nch;
-  L.blockpart = (L.dhcdone + (size_t)L.nrb * L.ndt + 1) & ~(size_t)1;   // in unsigned units
+  L.n2max = (int)((p.Vc + L.TM - 1) / L.TM) * L.ndt;   // G2 tiles of a chunk (narrow: upper bound)
+  L.g2part = L.dhcdone + (size_t)L.nrb * L.ndt;
+  L.blockpart = (L.g2part + nch * L.n2max + 1) & ~(size_t)1;   // in unsigned units
   L.total = L.blockpart + 2 * (size_t)L.nrb * (pair ? 2 : 1);
   return L;
 }
@@ -1492,21 +1518,35 @@ static attn_status_t launch_vocab_k(const Plan& p, const VbArgs& a, int ctas, cu
   P.ntn = (int)((V + VB_BN - 1) / VB_BN);
   P.fwd_tiles = a.fwd ? P.nrb * P.ntn : 0;
   P.last_g2_first = g_opt_vb_g2first;
-  P.order = NB >= 2 ? g_opt_vb_order : 0;   // order 1 with one buffer would wait on later tiles
+  P.order = NB >= 2 ? g_opt_vb_order : 0;   // orders 1 / 2 with one buffer would wait on later tiles
+  P.nh = (P.order == 2 && g_opt_vb_g2split && P.nrb >= 2) ? 2 : 1;
+  P.h0 = P.nh == 2 ? (P.nrb + 1) / 2 : P.nrb;
+  P.lag = g_opt_vb_lag;
+  P.claim_late = g_opt_vb_claim < 0 ? (P.order == 2 ? 1 : 0) : g_opt_vb_claim;
+  P.n2max = L.n2max;
   P.trace = g_vb_trace;
   P.debug = g_vb_debug;
   P.l2hints = g_opt_vb_l2;
   // backward dispatch blocks: 0 = G1(0); c + 1 = G1(c + 1), G3(c), G2(c)
   auto vcc = [&](int c) { return (int)std::min(Vc, V - (long long)c * Vc); };
   int t = 0;
-  P.blk_start[0] = 0;
-  t += P.nrb * ((vcc(0) + VB_BN - 1) / VB_BN);
-  for (int c = 0; c < p.nchunks; ++c) {
-    P.blk_start[c + 1] = t;
-    t += P.nrb * P.ndw + ((vcc(c) + Cfg::TM - 1) / Cfg::TM) * P.ndw;
-    if (c + 1 < p.nchunks) t += P.nrb * ((vcc(c + 1) + VB_BN - 1) / VB_BN);
+  if (P.order == 2) {   // block c = chunk c: G1(c), G3(c), nh x G2(c)
+    for (int c = 0; c < p.nchunks; ++c) {
+      P.blk_start[c] = t;
+      t += P.nrb * ((vcc(c) + VB_BN - 1) / VB_BN) + P.nrb * P.ndw +
+           P.nh * ((vcc(c) + Cfg::TM - 1) / Cfg::TM) * P.ndw;
+    }
+    P.blk_start[p.nchunks] = t;
+  } else {
+    P.blk_start[0] = 0;
+    t += P.nrb * ((vcc(0) + VB_BN - 1) / VB_BN);
+    for (int c = 0; c < p.nchunks; ++c) {
+      P.blk_start[c + 1] = t;
+      t += P.nrb * P.ndw + ((vcc(c) + Cfg::TM - 1) / Cfg::TM) * P.ndw;
+      if (c + 1 < p.nchunks) t += P.nrb * ((vcc(c + 1) + VB_BN - 1) / VB_BN);
+    }
+    P.blk_start[p.nchunks + 1] = t;
   }
-  P.blk_start[p.nchunks + 1] = t;
   P.total_tiles = P.fwd_tiles + t;
   unsigned* ctr = a.ctr;
   P.tile_counter = (int*)ctr;
@@ -1518,6 +1558,7 @@ static attn_status_t launch_vocab_k(const Plan& p, const VbArgs& a, int ctas, cu
   P.consumed = ctr + L.consumed;
   P.g2done = ctr + L.g2done;
   P.dhcdone = ctr + L.dhcdone;
+  P.g2part = ctr + L.g2part;
   P.blockpart = reinterpret_cast<double*>(ctr + L.blockpart);
   P.part = a.part; P.tgt_logit = a.tgt_logit; P.lse = a.lse; P.nll = a.nll;
   P.rowscale = a.rowscale; P.loss = a.loss; P.loss_scale = a.loss_scale; P.tgt = a.tgt;

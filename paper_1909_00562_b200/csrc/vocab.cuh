@@ -119,7 +119,8 @@ struct alignas(64) VbParams {
   unsigned* lsedone;     // [nrb]             LSE warp-portions done per row block (2 per CTA)
   unsigned* g5count;     // [1]               LSE CTA-portions done (the last one sums the loss)
   unsigned* rowdone;     // [nchunks][nrb]    G1 warp-portions done per row block
-  unsigned* coldone;     // [nchunks][ncolf]  G1 warp-portions done per 256-column block
+  unsigned* coldone;     // [nchunks][nh][ncolf] G1 warp-portions done per 256-column block
+                         // (and row half)
   unsigned* consumed;    // [nchunks]         G2 + G3 CTA-tiles whose operands are loaded
   unsigned* g2done;      // [nchunks]         G2 warp-portions whose dW_out stores completed
   unsigned* dhcdone;     // [nrb][ndt]        G3 warp-portions whose dHc update completed
@@ -137,7 +138,15 @@ struct alignas(64) VbParams {
   const void* bias;      // F_c bias b_out [V] bf16 (NEXT-1) or NULL
   float* db_part;        // with the bias: [T / 32][V] column sums of dL per 32-row group
   int last_g2_first;     // last block: G2 tiles before G3 tiles
-  int order;             // 0: block c+1 = G3(c), G2(c), G1(c+1); 1: G1(c+1), G3(c), G2(c)
+  int order;             // 0: block c+1 = G3(c), G2(c), G1(c+1); 1: G1(c+1), G3(c), G2(c);
+                         // 2: row-interleaved (block c = chunk c, see vb_decode_o2)
+  int claim_late;        // claim the next tile near the end of the current one's loads
+                         // (default: right after its first load)
+  int nh;                // order 2: G2 split over T in nh (1 or 2) row halves (else 1)
+  int h0;                // order 2: row blocks of the first half
+  int lag;               // order 2: G3 of row block rb dispatched after G1 of rb + lag
+  int n2max;             // G2 tiles of a full chunk (ceil(Vc / TM) * ndw): g2part stride
+  unsigned* g2part;      // [nchunks][n2max]  order 2: first-half G2 warp-portions done
   int l2hints;           // bit 0: H_c loads evict-last; bit 1: dHc updates evict-last;
                          // bit 2: dL stores evict-last
   long long* trace;      // debug: 32 int64 per tile and CTA rank (see VB_TRACE), NULL = off
@@ -147,7 +156,7 @@ struct alignas(64) VbParams {
                          // bit 4 / 5 skip the B / A operand loads, bit 6 G1 reads its B
                          // operand MN-major (garbage values), bit 7 G1 epilogue skips
                          // its TMEM loads, bits 8 / 9 G1 k-steps as 2 x N = 128 / 4 x N = 64
-                         // MMAs sharing A
+                         // MMAs sharing A, bits 13 / 14 skip the operand loads of G2 / G3
   int blk_start[VB_MAX_BLOCKS + 2];   // backward blocks, relative to fwd_tiles
 };
 
@@ -157,17 +166,87 @@ struct VbTile {
                          // G3: i = row block, j = d tile; G2: i = vocabulary row block
                          // of the chunk, j = d tile
   int vcc, kb_total;
+  int h;                 // G2: row half of the K = T reduction (order 2), else 0
+  int k0;                // G2: first row of its K range
 };
 
 __device__ __forceinline__ int vb_vcc(const VbParams& P, int c) {
   return min(P.Vc, P.V - c * P.Vc);
 }
 
+// G2 tile of row half h: K range [k0, k0 + rows) of the T rows
+template <bool kPair>
+__device__ __forceinline__ void vb_g2_range(const VbParams& P, int h, int& k0, int& kb) {
+  constexpr int TM = VbCfg<kPair>::TM;
+  const int split = P.nh == 2 ? P.h0 * TM : P.T;
+  k0 = h == 0 ? 0 : split;
+  const int k1 = h == 0 ? min(split, P.T) : P.T;
+  kb = (k1 - k0 + VB_BK - 1) / VB_BK;
+}
+
+// order 2 (row-interleaved), block = chunk c, in dispatch order:
+//   for rb = 0 .. nrb-1:  G1(c, rb, all columns),  G3(c, rb - lag, all d tiles) if rb >= lag,
+//                         and after the step rb = h0 - 1 + lag: G2(c, half 0, all tiles)
+//   tail:                 G3(c, the last lag row blocks), [G2(c, half 0) if not yet],
+//                         G2(c, last half)
+// so each dL row block is read by G3 a few tile-steps after it is written and the
+// first half of the chunk by G2 while the second half is produced: the live part
+// of the dL chunk stays a fraction of it (with orders 0 / 1 G3(c) / G2(c) run a
+// block after G1(c) and read most of dL back from DRAM)
+template <bool kPair>
+__device__ __forceinline__ void vb_decode_o2(const VbParams& P, int c, int u, VbTile& r) {
+  constexpr int TM = VbCfg<kPair>::TM;
+  const int vcc = vb_vcc(P, c);
+  const int ncol = (vcc + VB_BN - 1) / VB_BN;
+  const int n2 = ((vcc + TM - 1) / TM) * P.ndw;
+  const int L = P.lag, nrb = P.nrb, ndw = P.ndw;
+  auto prefix = [&](int rb) { return rb * ncol + max(0, rb - L) * ndw; };
+  const int rbg2 = P.h0 - 1 + L;
+  const int pos_g2 = (P.nh == 2 && rbg2 < nrb) ? prefix(rbg2 + 1) : -1;
+  r.c = c;
+  r.h = 0;
+  if (pos_g2 >= 0 && u >= pos_g2) {
+    if (u < pos_g2 + n2) {
+      u -= pos_g2;
+      r.type = VB_G2; r.i = u / ndw; r.j = u % ndw;
+      return;
+    }
+    u -= n2;
+  }
+  const int rows_total = prefix(nrb);
+  if (u < rows_total) {
+    if (u < L * ncol) {
+      r.type = VB_G1; r.i = u / ncol; r.j = u % ncol;
+    } else {
+      const int v = u - L * ncol;
+      const int rb = L + v / (ncol + ndw), w = v % (ncol + ndw);
+      if (w < ncol) { r.type = VB_G1; r.i = rb; r.j = w; }
+      else { r.type = VB_G3; r.i = rb - L; r.j = w - ncol; }
+    }
+    return;
+  }
+  u -= rows_total;
+  const int ntail = min(L, nrb);
+  if (u < ntail * ndw) {
+    r.type = VB_G3; r.i = nrb - ntail + u / ndw; r.j = u % ndw;
+    return;
+  }
+  u -= ntail * ndw;
+  if (P.nh == 2 && pos_g2 < 0) {
+    if (u < n2) { r.type = VB_G2; r.i = u / ndw; r.j = u % ndw; return; }
+    u -= n2;
+  }
+  r.type = VB_G2; r.h = P.nh - 1; r.i = u / ndw; r.j = u % ndw;
+}
+
+
 template <bool kPair>
 __device__ __forceinline__ VbTile vb_decode(const VbParams& P, int t) {
   constexpr int TM = VbCfg<kPair>::TM;
   VbTile r;
   r.c = 0;
+  r.h = 0;
+  r.k0 = 0;
   if (t < P.fwd_tiles) {
     r.type = VB_G0; r.i = t / P.ntn; r.j = t % P.ntn;   // row-block major
     r.vcc = P.V;
@@ -175,12 +254,22 @@ __device__ __forceinline__ VbTile vb_decode(const VbParams& P, int t) {
     return r;
   }
   t -= P.fwd_tiles;
-  int lo = 0, hi = P.nchunks;   // blocks 0..nchunks
+  int lo = 0, hi = P.order == 2 ? P.nchunks - 1 : P.nchunks;   // blocks
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (P.blk_start[mid] <= t) lo = mid; else hi = mid - 1;
   }
   int u = t - P.blk_start[lo];
+  r.h = 0;
+  r.k0 = 0;
+  if (P.order == 2) {
+    vb_decode_o2<kPair>(P, lo, u, r);
+    r.vcc = vb_vcc(P, r.c);
+    if (r.type == VB_G1) r.kb_total = P.d / VB_BK;
+    else if (r.type == VB_G3) r.kb_total = (r.vcc + VB_BK - 1) / VB_BK;
+    else vb_g2_range<kPair>(P, r.h, r.k0, r.kb_total);
+    return r;
+  }
   if (lo == 0) {
     r.type = VB_G1; r.c = 0;
   } else {
@@ -425,7 +514,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
         mbar_arrive(&sfull[r]);
       }
       __syncwarp();
-      if (t >= 0) fetch();
+      if (t >= 0 && !P.claim_late) fetch();
       if (++r == VB_SCHED) { r = 0; rph ^= 1; }
       return t;
     };
@@ -458,9 +547,11 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
         if (lane == 0) {
           // this tile's TM vocabulary rows: 256-column blocks of G1
           const int cb0 = tl.i * TM / VB_BN, cb1 = ((tl.i + 1) * TM - 1) / VB_BN;
+          // ... over the row blocks of its half (order 2 splits the K = T rows)
+          const int nrows = P.nh == 1 ? P.nrb : (tl.h == 0 ? P.h0 : P.nrb - P.h0);
           for (int cb = cb0; cb <= cb1 && cb * VB_BN < tl.vcc; ++cb)
-            vb_wait_geq(P.coldone + (size_t)tl.c * P.ncolf + cb,
-                        (unsigned)(Cfg::WARPS_PER_TILE * P.nrb));
+            vb_wait_geq(P.coldone + ((size_t)tl.c * P.nh + tl.h) * P.ncolf + cb,
+                        (unsigned)(Cfg::WARPS_PER_TILE * nrows));
         }
         __syncwarp();
         fence_proxy_async_global();
@@ -479,7 +570,9 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           uint8_t* sB = sA + Cfg::A_BYTES;
           const uint32_t barc = kPair ? leader_addr(&full[s]) : 0u;
           // debug bits 4 / 5 (timing only): skip the B / A operand loads
-          const bool ldA = !(P.debug & 32), ldB = !(P.debug & 16);
+          // bits 13 / 14: skip the operand loads of G2 / G3 tiles only
+          const bool skip_t = (tl.type == VB_G2 && (P.debug & 8192)) || (tl.type == VB_G3 && (P.debug & 16384));
+          const bool ldA = !(P.debug & 32) && !skip_t, ldB = !(P.debug & 16) && !skip_t;
           if (leader)
             mbar_arrive_expect_tx(&full[s], ((ldA ? Cfg::A_BYTES : 0) + (ldB ? Cfg::B_BYTES : 0)) * Cfg::CTAS);
           const int k0 = kb * VB_BK;
@@ -496,8 +589,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
             if (ldA) vb_load<kPair>(sA, &P.m_dl_k, &full[s], barc, k0, arow, buf, pol_norm);
             if (ldB) vb_load4<kPair>(sB, &P.m_wo_mn, &full[s], barc, 0, c0 + k0, bcol / 64, 0, pol_norm);
           } else {
-            if (ldA) vb_load4<kPair>(sA, &P.m_dl_mn, &full[s], barc, 0, k0, arow / 64, buf, pol_norm);
-            if (ldB) vb_load4<kPair>(sB, &P.m_hc_mn, &full[s], barc, 0, k0, bcol / 64, 0, pol_keep);
+            if (ldA) vb_load4<kPair>(sA, &P.m_dl_mn, &full[s], barc, 0, tl.k0 + k0, arow / 64, buf, pol_norm);
+            if (ldB) vb_load4<kPair>(sB, &P.m_hc_mn, &full[s], barc, 0, tl.k0 + k0, bcol / 64, 0, pol_keep);
           }
         }
         __syncwarp();
@@ -508,20 +601,34 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           if (elect_one()) {
             uint8_t* sB = smem + s * Cfg::STAGE + Cfg::A_BYTES;
             const uint32_t barc = kPair ? leader_addr(&full[s]) : 0u;
-            if (leader) mbar_arrive_expect_tx(&full[s], Cfg::B_BYTES * Cfg::CTAS);
+            const bool skip_t = (tl.type == VB_G2 && (P.debug & 8192)) || (tl.type == VB_G3 && (P.debug & 16384));
+            if (leader) {
+              if (skip_t) mbar_arrive(&full[s]);
+              else mbar_arrive_expect_tx(&full[s], Cfg::B_BYTES * Cfg::CTAS);
+            }
             const int k0 = kb * VB_BK;
-            if (tl.type == VB_G3)
+            if (skip_t) {
+            } else if (tl.type == VB_G3)
               vb_load4<kPair>(sB, &P.m_wo_mn, &full[s], barc, 0, c0 + k0, (bcol + VB_BN) / 64, 0, pol_norm);
             else
-              vb_load4<kPair>(sB, &P.m_hc_mn, &full[s], barc, 0, k0, (bcol + VB_BN) / 64, 0, pol_keep);
+              vb_load4<kPair>(sB, &P.m_hc_mn, &full[s], barc, 0, tl.k0 + k0, (bcol + VB_BN) / 64, 0, pol_keep);
           }
           __syncwarp();
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
-        if (kb == 0) {
+        if (P.claim_late) {
+          // claim the next tile only when this one is nearly issued: a tile is
+          // never queued behind a long one on a busy pair (order 2's short
+          // dependency distances need it)
+          if (leader && kb == max(0, tl.kb_total - 2)) fetch();
+        } else if (kb == 0) {
           t_nxt = next_tile();
           if (t_nxt >= 0) tl_nxt = vb_decode<kPair>(P, t_nxt);
         }
+      }
+      if (P.claim_late) {
+        t_nxt = next_tile();
+        if (t_nxt >= 0) tl_nxt = vb_decode<kPair>(P, t_nxt);
       }
       t = t_nxt;
       tl = tl_nxt;
@@ -621,8 +728,9 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           s = s2;
           ph = ph2;
           if (++s == STAGES) { s = 0; ph ^= 1; }
-          if (kb == kb_read) t_nxt = ring_read1();
+          if (kb == kb_read && !P.claim_late) t_nxt = ring_read1();
         }
+        if (P.claim_late) t_nxt = ring_read1();
         if (elect_one()) {
           if constexpr (kPair) {
             umma_commit_pair(&tfull[acc]);
@@ -843,7 +951,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
         if (tl.c >= P.nbuf) {
           const int cp = tl.c - P.nbuf;
           const unsigned need = (unsigned)(Cfg::CTAS * P.ndt *
-                                           (P.nrb + (vb_vcc(P, cp) + TM - 1) / TM));
+                                           (P.nrb + P.nh * ((vb_vcc(P, cp) + TM - 1) / TM)));
           if (lane == 0) vb_wait_geq(P.consumed + cp, need);
           __syncwarp();
           fence_proxy_async_global();
@@ -935,7 +1043,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           if (!(P.debug & 8)) bulk_wait0();
           fence_proxy_async_global();
           red_release_gpu_add(P.rowdone + (size_t)tl.c * P.nrb + tl.i, 1u);
-          red_release_gpu_add(P.coldone + (size_t)tl.c * P.ncolf + tl.j, 1u);
+          const int hh = (P.nh == 2 && tl.i >= P.h0) ? 1 : 0;
+          red_release_gpu_add(P.coldone + ((size_t)tl.c * P.nh + hh) * P.ncolf + tl.j, 1u);
         }
         __syncwarp();
       } else {
@@ -969,8 +1078,19 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
             __syncwarp();
             fence_proxy_async_global();
           }
+          // order 2, G2 of the second row half: reduce-add onto the first half's
+          // stores of the same tile (fixed order, deterministic)
+          const bool g2_first = !g3 && P.nh == 2 && tl.h == 0;
+          const bool g2_second = !g3 && P.nh == 2 && tl.h == 1;
+          unsigned* g2p_ctr = P.g2part + (size_t)tl.c * P.n2max + tl.i * P.ndw + tl.j;
+          if (g2_second && half == 0) {
+            if (lane == 0) vb_wait_geq(g2p_ctr, (unsigned)(Cfg::WARPS_PER_TILE * nhalf));
+            __syncwarp();
+            fence_proxy_async_global();
+          }
           if (warp == 0) VB_TRACE(t, 12, vb_clk());
-          const uint64_t pol = l2_policy_evict_first();   // dW_out is not read again here
+          // dW_out is not read again here (the first half's partials are, by the second)
+          const uint64_t pol = g2_first ? l2_policy_evict_last() : l2_policy_evict_first();
           const uint64_t pol_dhc = (P.l2hints & 2) ? l2_policy_evict_last() : l2_policy_evict_normal();
 #pragma unroll 1
           for (int cc = 0; cc < 4; ++cc) {
@@ -987,7 +1107,9 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0 && !(P.debug & 4)) {
-              if (!g3)
+              if (g2_second)
+                tma_reduce_add_2d_hint(&P.m_dw_st, stg_p, colh + cc * 32, c0 + row0, pol);
+              else if (!g3)
                 tma_store_2d_hint(&P.m_dw_st, stg_p, colh + cc * 32, c0 + row0, pol);
               else if (tl.c == 0)
                 tma_store_2d_hint(&P.m_dhc_st, stg_p, colh + cc * 32, row0, pol_dhc);
@@ -1006,7 +1128,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           if (lane == 0) {
             if (!(P.debug & 8)) bulk_wait0();
             fence_proxy_async_global();
-            red_release_gpu_add(g3 ? dhc_ctr : P.g2done + tl.c, 1u);
+            red_release_gpu_add(g3 ? dhc_ctr : g2_first ? g2p_ctr : P.g2done + tl.c, 1u);
           }
           __syncwarp();
         }

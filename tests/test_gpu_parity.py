@@ -79,7 +79,7 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, wide):
 # ------------------------------------------------------ end-to-end parity --
 _DEFAULTS = {"store_logits": 0, "wide_tiles": 2, "db_gemm": -1, "vb_pair": 1, "vb_fwd_fused": 0,
              "vb_order": 1, "dl_buffers": 3, "dl_budget_mb": 120, "vb_last_g2_first": 1,
-             "attn_fused": 1, "vb_wide": 1}
+             "attn_fused": 1, "vb_wide": 1, "vb_lag": 2, "vb_g2split": 1, "vb_claim": 1}
 _MODES = {
     "default": {},                                  # persistent vocab launch on CTA pairs
     "single": {"vb_pair": 0},                       # ... on single-CTA 128 x 256 tiles
@@ -93,6 +93,14 @@ _MODES = {
     "sl2": {"store_logits": 2},                     # ... serialised dlogits kernels
     "attn_generic": {"attn_fused": 0},              # attention on the generic engine's batched GEMMs
     "narrow": {"vb_wide": 0},                       # G2 / G3 on 256-column tiles (default: 512 when d % 512 == 0)
+    "order2": {"vb_order": 2},                      # row-interleaved dispatch, G2 split in two row halves
+    "claim0": {"vb_claim": 0},                      # next tile claimed right after the first load
+    "order2_single": {"vb_order": 2, "vb_pair": 0},
+    "order2_nosplit": {"vb_order": 2, "vb_g2split": 0},
+    "order2_lag0": {"vb_order": 2, "vb_lag": 0, "dl_buffers": 2},
+    "order2_lag9": {"vb_order": 2, "vb_lag": 9},
+    "order2_narrow": {"vb_order": 2, "vb_wide": 0},
+    "order2_fused": {"vb_order": 2, "vb_fwd_fused": 1},
 }
 
 
@@ -130,6 +138,15 @@ def set_modes(binding, mode):
                                           ("small", 256, "nb1"), ("odd", 256, "nb1"),
                                           ("medium", 512, "g3last"),
                                           ("medium", 0, "narrow"), ("medium", 512, "narrow"),
+                                          ("small", 256, "claim0"), ("medium", 512, "claim0"),
+                                          ("small", 0, "order2"), ("small", 256, "order2"),
+                                          ("medium", 0, "order2"), ("medium", 512, "order2"),
+                                          ("odd", 256, "order2"), ("edge_min", 0, "order2"),
+                                          ("edge_max_src", 256, "order2"),
+                                          ("small", 256, "order2_single"), ("medium", 512, "order2_single"),
+                                          ("medium", 512, "order2_nosplit"), ("medium", 512, "order2_lag0"),
+                                          ("medium", 512, "order2_lag9"), ("medium", 512, "order2_narrow"),
+                                          ("small", 256, "order2_fused"), ("medium", 0, "order2_fused"),
                                           ("tiny_ragged", 0, "sl"), ("small", 0, "sl"),
                                           ("small", 1024, "sl"), ("medium", 0, "sl"),
                                           ("medium", 2048, "sl128"), ("odd", 256, "sl"),
