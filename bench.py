@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -574,6 +575,9 @@ def main():
     tok_job = float(ntok.item())
     value = tok_job * args.steps / (total_ms / 1e3)
     loss = float(out["loss"].item())
+    if not math.isfinite(loss):   # abort on a non-finite loss
+        print(f"bench.py: non-finite loss {loss} on rank {rank}", file=sys.stderr)
+        sys.exit(1)
 
     # ---- e2e through the C ABI with HOST buffers: every step copies its own
     # activations (H_dec, H_enc, tgt_ids) host->device from pinned memory and

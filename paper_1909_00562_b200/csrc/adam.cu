@@ -20,6 +20,7 @@
 #include <cstdio>
 
 #include "../../include/attn_softmax.h"
+#include "nvtx.cuh"
 #include "comm.h"
 
 attn_status_t attn_set_error(attn_status_t code, const char* msg);
@@ -130,6 +131,7 @@ attn_status_t launch(float* w, float* m, float* v, const float* g, void* wb, siz
 
 extern "C" attn_status_t attn_adam_step(const attn_adam_t* h, size_t n, float* w, float* m,
                                         float* v, const float* g, void* w_bf16, void* stream) {
+  attnsm::NvtxRange nvtx_range_("attn_adam_step");
   attn_status_t st = check(h);
   if (st != ATTN_OK) return st;
   if (n && (!w || !m || !v || !g)) return fail(ATTN_ERR_INVALID_ARG, "adam: w / m / v / g is NULL");
@@ -148,6 +150,7 @@ extern "C" size_t attn_adam_shard_len(const attn_comm_t* c, size_t n) {
 extern "C" attn_status_t attn_adam_step_sharded(attn_comm_t* c, const attn_adam_t* h, size_t n,
                                                 float* g, float* w_shard, float* m_shard,
                                                 float* v_shard, void* w_bf16, void* stream) {
+  attnsm::NvtxRange nvtx_range_("attn_adam_step_sharded");
   attn_status_t st = check(h);
   if (st != ATTN_OK) return st;
   if (!c) return fail(ATTN_ERR_INVALID_ARG, "adam_sharded: comm is NULL (use attn_adam_step)");

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "../../include/attn_softmax.h"
+#include "nvtx.cuh"
 #include "../../include/attn_softmax_debug.h"
 #include "comm.h"
 #include "gemm_simt.cuh"
@@ -82,6 +83,7 @@ static Prof g_prof;
 static long long g_launches = 0;
 
 static void prof_mark(const char* name, cudaStream_t s, bool vocab_mark = false) {
+  nvtxMarkA(name);   // end of stage `name` (host enqueue order)
   if (!g_prof.on || (g_prof.vocab_only && !vocab_mark)) return;
   if (!g_prof.created) {
     for (int i = 0; i < 32; ++i) cudaEventCreate(&g_prof.ev[i]);
@@ -1406,7 +1408,7 @@ static attn_status_t attention_backward_tc(const Plan& p, const void* H, const v
 // F4 + F5 + B1 as one launch (vocab.cuh): tensor maps, dispatch blocks,
 // counters.  Counter layout in `ctr` (zeroed by the caller): [0] tile
 // counter, [1] g5count (LSE CTA-portions), then g0done [nrb], lsedone [nrb], rowdone
-// [nchunks][nrb], coldone [nchunks][2][ncolf], consumed [nchunks], g2done
+// [nchunks][nrb], coldone [nchunks][2][ncolf], consumed [nchunks][2], g2done
 // [nchunks], dhcdone [nrb][ndt], g2part [nchunks][n2max], and blockpart (double [nrb * CTAS]) at the
 // end, 8-byte aligned (vb_ctr_layout).
 struct VbLayout {
@@ -1426,7 +1428,7 @@ static VbLayout vb_ctr_layout(const Plan& p, bool pair) {
   L.rowdone = L.lsedone + L.nrb;
   L.coldone = L.rowdone + nch * L.nrb;
   L.consumed = L.coldone + 2 * nch * L.ncolf;          // [nchunks][row half][ncolf]
-  L.g2done = L.consumed + nch;
+  L.g2done = L.consumed + 2 * nch;                     // consumed: [nchunks][row half]
   L.dhcdone = L.g2done + nch;
   L.n2max = (int)((p.Vc + L.TM - 1) / L.TM) * L.ndt;   // G2 tiles of a chunk (narrow: upper bound)
   L.g2part = L.dhcdone + (size_t)L.nrb * L.ndt;
@@ -1518,7 +1520,9 @@ static attn_status_t launch_vocab_k(const Plan& p, const VbArgs& a, int ctas, cu
   P.ntn = (int)((V + VB_BN - 1) / VB_BN);
   P.fwd_tiles = a.fwd ? P.nrb * P.ntn : 0;
   P.last_g2_first = g_opt_vb_g2first;
-  P.order = NB >= 2 ? g_opt_vb_order : 0;   // orders 1 / 2 with one buffer would wait on later tiles
+  // order 1 with one buffer would wait on later tiles; order 2 reuses the
+  // buffer per row half, whose consumers are dispatched in the previous block
+  P.order = (NB >= 2 || g_opt_vb_order == 2) ? g_opt_vb_order : 0;
   P.nh = (P.order == 2 && g_opt_vb_g2split && P.nrb >= 2) ? 2 : 1;
   P.h0 = P.nh == 2 ? (P.nrb + 1) / 2 : P.nrb;
   P.lag = g_opt_vb_lag;
@@ -1897,6 +1901,7 @@ extern "C" attn_status_t attn_softmax_fwd_bwd_ex(
     const void* W_alpha, const void* b_out, float loss_scale, float* loss, void* dH_dec,
     void* dH_enc, float* dW_c, float* dW_out, float* dW_alpha, float* db_out, void* workspace,
     size_t workspace_bytes, attn_comm_t* comm, void* stream_) {
+  attnsm::NvtxRange nvtx_range_("attn_softmax_fwd_bwd_ex");
   OPT_LOCK;
   attn_status_t st = validate(s, H_dec, H_enc, src_lens_host, tgt_lens_host, tgt_ids, W_c, W_out,
                               W_alpha, loss, dH_dec, dH_enc, dW_c, dW_out, dW_alpha,
@@ -1933,6 +1938,7 @@ extern "C" attn_status_t attn_softmax_fwd_bwd(
     const void* W_alpha, float loss_scale, float* loss, void* dH_dec, void* dH_enc, float* dW_c,
     float* dW_out, float* dW_alpha, void* workspace, size_t workspace_bytes, attn_comm_t* comm,
     void* stream_) {
+  attnsm::NvtxRange nvtx_range_("attn_softmax_fwd_bwd");
   return attn_softmax_fwd_bwd_ex(s, H_dec, H_enc, src_lens_host, tgt_lens_host, tgt_ids, W_c,
                                  W_out, W_alpha, nullptr, loss_scale, loss, dH_dec, dH_enc, dW_c,
                                  dW_out, dW_alpha, nullptr, workspace, workspace_bytes, comm,
@@ -1954,6 +1960,7 @@ extern "C" attn_status_t attn_softmax_fwd_bwd_host(
     const void* W_c, const void* W_out, float loss_scale, float* loss_host, void* dH_dec,
     void* dH_enc, float* dW_c, float* dW_out, void* staging, size_t staging_bytes,
     void* workspace, size_t workspace_bytes, attn_comm_t* comm, void* stream_) {
+  attnsm::NvtxRange nvtx_range_("attn_softmax_fwd_bwd_host");
   attn_status_t st = check_shape(s);
   if (st != ATTN_OK) return st;
   if (!H_dec_host || !H_enc_host || !tgt_ids_host || !loss_host || !staging)
@@ -2076,6 +2083,7 @@ extern "C" attn_status_t attn_softmax_fwd_bwd_staged(
     const int32_t* tgt_lens_host, const void* W_c, const void* W_out, float loss_scale,
     float* loss_host, void* dH_dec, void* dH_enc, float* dW_c, float* dW_out, void* workspace,
     size_t workspace_bytes, attn_comm_t* comm, void* stream_) {
+  attnsm::NvtxRange nvtx_range_("attn_softmax_fwd_bwd_staged");
   attn_status_t st = check_shape(s);
   if (st != ATTN_OK) return st;
   if (!staging || !loss_host) return fail(ATTN_ERR_INVALID_ARG, "staged: NULL argument");
@@ -2181,6 +2189,7 @@ extern "C" attn_status_t attn_softmax_decode_step(
     const void* W_c, const void* W_out, const void* W_alpha, const void* b_out, int k,
     int32_t* topk_ids, float* topk_logp, float* lse, void* workspace, size_t workspace_bytes,
     void* stream_) {
+  attnsm::NvtxRange nvtx_range_("attn_softmax_decode_step");
   OPT_LOCK;
   attn_status_t st = check_shape(s);
   if (st != ATTN_OK) return st;

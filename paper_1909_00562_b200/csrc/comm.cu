@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "comm.h"
+#include "nvtx.cuh"
 
 // Minimal NCCL ABI (nccl.h 2.x): opaque comm, 128-byte unique id, enums.
 typedef struct ncclComm* ncclComm_t;
@@ -250,6 +251,7 @@ extern "C" attn_status_t attn_comm_poll(attn_comm_t* c, int64_t timeout_ms) {
 }
 
 extern "C" attn_status_t attn_grad_allreduce(attn_comm_t* c, float* buf, size_t count, void* stream) {
+  attnsm::NvtxRange nvtx_range_("attn_grad_allreduce");
   if (!c || (!buf && count)) return err(ATTN_ERR_INVALID_ARG, "comm / buf is NULL");
   if (count == 0) return ATTN_OK;
   NCCL_OK(nccl().AllReduce(buf, buf, count, ncclFloat32_, ncclSum_, c->comm, (cudaStream_t)stream));
@@ -326,6 +328,7 @@ static void shard_of(int B, int R, int r, int* lo, int* n) {
 
 extern "C" attn_status_t attn_hidden_scatter(attn_comm_t* c, int root, int B_global, int rows,
                                              int hidden, const void* full, void* shard, void* stream) {
+  attnsm::NvtxRange nvtx_range_("attn_hidden_scatter");
   if (!c) return err(ATTN_ERR_INVALID_ARG, "hidden_scatter: comm is NULL");
   if (B_global < 0 || rows < 1 || hidden < 1 || root < 0 || root >= c->nranks)
     return err(ATTN_ERR_SHAPE, "hidden_scatter: B_global %d, rows %d, hidden %d, root %d of %d ranks",

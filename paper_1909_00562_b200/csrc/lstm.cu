@@ -42,6 +42,7 @@
 #include <vector>
 
 #include "../../include/attn_softmax.h"
+#include "nvtx.cuh"
 #include "ptx.cuh"
 
 attn_status_t attn_set_error(attn_status_t code, const char* msg);
@@ -1045,6 +1046,7 @@ extern "C" attn_status_t attn_encoder_decoder_fwd(
     const void* const* enc_W, const float* const* enc_b, const void* const* dec_W,
     const float* const* dec_b, void* H_enc, void* H_dec, void* workspace, size_t workspace_bytes,
     void* stream) {
+  attnsm::NvtxRange nvtx_range_("attn_encoder_decoder_fwd");
   attn_status_t r = check_lstm(s);
   if (r != ATTN_OK) return r;
   if (!src_ids || !tgt_ids || !src_lens_host || !E_src || !E_tgt || !enc_W || !enc_b || !dec_W ||
@@ -1121,6 +1123,7 @@ extern "C" attn_status_t attn_encoder_decoder_if_fwd(
     const void* const* enc_W, const float* const* enc_b, const void* const* dec_W,
     const float* const* dec_b, const void* W_c, void* H_enc, void* H_dec, void* Htilde,
     void* workspace, size_t workspace_bytes, void* stream) {
+  attnsm::NvtxRange nvtx_range_("attn_encoder_decoder_if_fwd");
   attn_status_t r = check_lstm(s);
   if (r != ATTN_OK) return r;
   if (!src_ids || !tgt_ids || !src_lens_host || !E_src || !E_tgt || !enc_W || !enc_b || !dec_W ||
@@ -1446,6 +1449,7 @@ extern "C" attn_status_t attn_encoder_decoder_fwd_train(
     const void* const* enc_W, const float* const* enc_b, const void* const* dec_W,
     const float* const* dec_b, void* H_enc, void* H_dec, void* workspace, size_t workspace_bytes,
     void* stream) {
+  attnsm::NvtxRange nvtx_range_("attn_encoder_decoder_fwd_train");
   attn_status_t r = check_lstm(s);
   if (r != ATTN_OK) return r;
   if (!src_ids || !tgt_ids || !src_lens_host || !E_src || !E_tgt || !enc_W || !enc_b || !dec_W ||
@@ -1480,6 +1484,7 @@ extern "C" attn_status_t attn_encoder_decoder_bwd(
     const void* H_enc, const void* H_dec, const void* dH_enc, const void* dH_dec,
     float* const* dW_enc, float* const* db_enc, float* const* dW_dec, float* const* db_dec,
     float* dE_src, float* dE_tgt, void* workspace, size_t workspace_bytes, void* stream) {
+  attnsm::NvtxRange nvtx_range_("attn_encoder_decoder_bwd");
   attn_status_t r = check_lstm(s);
   if (r != ATTN_OK) return r;
   if (!src_ids || !tgt_ids || !src_lens_host || !enc_W || !dec_W || !H_enc || !H_dec || !dH_enc ||

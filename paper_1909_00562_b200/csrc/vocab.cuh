@@ -121,7 +121,8 @@ struct alignas(64) VbParams {
   unsigned* rowdone;     // [nchunks][nrb]    G1 warp-portions done per row block
   unsigned* coldone;     // [nchunks][nh][ncolf] G1 warp-portions done per 256-column block
                          // (and row half)
-  unsigned* consumed;    // [nchunks]         G2 + G3 CTA-tiles whose operands are loaded
+  unsigned* consumed;    // [nchunks][2]      G2 + G3 CTA-tiles whose operands are loaded
+                         // (per row half with the order-2 split, else slot 0)
   unsigned* g2done;      // [nchunks]         G2 warp-portions whose dW_out stores completed
   unsigned* dhcdone;     // [nrb][ndt]        G3 warp-portions whose dHc update completed
   // forward outputs / backward row statistics
@@ -947,12 +948,15 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
             yl = P.tgt[row] - c0 - colh;
           }
         }
-        // the buffer is free once chunk c - NB's G2 / G3 tiles have loaded it
+        // the buffer rows are free once chunk c - NB's G2 / G3 tiles have loaded
+        // them (per row half with the order-2 split: its G3 row blocks and G2 tiles)
         if (tl.c >= P.nbuf) {
           const int cp = tl.c - P.nbuf;
+          const int hh = (P.nh == 2 && tl.i >= P.h0) ? 1 : 0;
+          const int rows = P.nh == 1 ? P.nrb : (hh == 0 ? P.h0 : P.nrb - P.h0);
           const unsigned need = (unsigned)(Cfg::CTAS * P.ndt *
-                                           (P.nrb + P.nh * ((vb_vcc(P, cp) + TM - 1) / TM)));
-          if (lane == 0) vb_wait_geq(P.consumed + cp, need);
+                                           (rows + ((vb_vcc(P, cp) + TM - 1) / TM)));
+          if (lane == 0) vb_wait_geq(P.consumed + 2 * cp + hh, need);
           __syncwarp();
           fence_proxy_async_global();
         }
@@ -1071,7 +1075,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           if (warp == 0 && lane == 0) {
             // every MMA of the tile has completed, so its dL operand has been read
             fence_proxy_async_global();
-            red_release_gpu_add(P.consumed + tl.c, 1u);
+            const int hh = P.nh == 1 ? 0 : g3 ? (tl.i >= P.h0 ? 1 : 0) : tl.h;
+            red_release_gpu_add(P.consumed + 2 * tl.c + hh, 1u);
           }
           if (g3 && tl.c > 0) {
             if (lane == 0) vb_wait_geq(dhc_ctr, (unsigned)(Cfg::WARPS_PER_TILE * tl.c));

@@ -2,6 +2,7 @@
 with PyTorch and calls attn_softmax_fwd_bwd.  No arithmetic happens here."""
 from __future__ import annotations
 
+import math
 from typing import Optional
 
 import torch
@@ -9,6 +10,10 @@ import torch
 from . import binding
 
 _TORCH_DTYPE = {"f32": torch.float32, "bf16": torch.bfloat16}
+
+
+class NonFiniteLoss(RuntimeError):
+    """The step's loss is NaN or inf (abort on a non-finite loss)."""
 
 
 class AttnSoftmaxStage:
@@ -40,11 +45,12 @@ class AttnSoftmaxStage:
 
     def __call__(self, H_dec, H_enc, src_len, tgt_len, tgt_ids, W_c, W_out,
                  loss_scale: float, out=None, comm=None, stream=None, W_alpha=None,
-                 b_out=None):
+                 b_out=None, check_finite: bool = False):
         """W_alpha [d,d] (dtype of the stage) selects the Eq. 2 "general"
         score; None is the dot score of the hot path.
         b_out [V] adds the F_c bias of Eq. 5 (NEXT-1); out["db_out"] is its
-        gradient."""
+        gradient.  check_finite reads the loss back (a host synchronisation)
+        and raises NonFiniteLoss when it is NaN or inf."""
         if out is None:
             out = self.alloc_outputs(W_alpha is not None, b_out is not None)
         dWa = out.get("dW_alpha") if W_alpha is not None else None
@@ -60,6 +66,11 @@ class AttnSoftmaxStage:
                 loss_scale, out["loss"], out["dH_dec"], out["dH_enc"], out["dW_c"],
                 out["dW_out"], self.workspace, comm=comm, stream=stream,
                 W_alpha=W_alpha, dW_alpha=dWa, b_out=b_out, db_out=out["db_out"])
+        if check_finite:
+            loss = float(out["loss"].item())
+            if not math.isfinite(loss):
+                raise NonFiniteLoss(f"non-finite loss {loss} (B={self.B}, N={self.N}, M={self.M}, "
+                                    f"d={self.d}, V={self.V}, {self.dtype})")
         return out
 
     def views(self):

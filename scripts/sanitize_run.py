@@ -19,9 +19,13 @@ from synthetic import CONFIGS, global_valid_tokens, make_inputs
 
 from dataclasses import replace as _replace
 
-CONFIGS = dict(CONFIGS, small512=_replace(CONFIGS["small"], name="small512", d=512, V=3001))
+CONFIGS = dict(CONFIGS, small512=_replace(CONFIGS["small"], name="small512", d=512, V=3001),
+               small_o2=_replace(CONFIGS["small"], name="small_o2"))
 cases = [("tiny", {}), ("small", {}), ("small", {"vb_pair": 0}), ("odd", {"vb_fwd_fused": 1}),
-         ("edge_min", {}), ("small", {"bias": 1}), ("small512", {})]   # small512: 512-column G2 / G3 tiles
+         ("edge_min", {}), ("small", {"bias": 1}), ("small512", {}),   # small512: 512-column G2 / G3 tiles
+         # the row-interleaved dispatch with T-split dW_out tiles, 3 and 1 dL buffers
+         ("small_o2", {"vb_order": 2, "vocab_chunk": 512}),
+         ("small_o2", {"vb_order": 2, "dl_buffers": 1, "vocab_chunk": 512})]
 only = sys.argv[1:]
 for name, opts in cases:
     if only and name not in only:
@@ -38,7 +42,8 @@ for name, opts in cases:
     torch.cuda.synchronize()
     print(f"{name} {opts} bias={bias}: loss {out['loss'].item():.6f}", flush=True)
     for k in opts:
-        binding.attn_softmax_set_option(k, {"vb_pair": 1, "vb_fwd_fused": 0}[k])
+        binding.attn_softmax_set_option(k, {"vb_pair": 1, "vb_fwd_fused": 0, "vb_order": 1,
+                                            "dl_buffers": 3, "vocab_chunk": 0}[k])
 if not only:
     cfg = CONFIGS["small"]
     inp = make_inputs(cfg)

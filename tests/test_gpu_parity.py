@@ -101,6 +101,7 @@ _MODES = {
     "order2_lag9": {"vb_order": 2, "vb_lag": 9},
     "order2_narrow": {"vb_order": 2, "vb_wide": 0},
     "order2_fused": {"vb_order": 2, "vb_fwd_fused": 1},
+    "order2_nb1": {"vb_order": 2, "dl_buffers": 1},  # one dL buffer, reused per row half
 }
 
 
@@ -147,6 +148,8 @@ def set_modes(binding, mode):
                                           ("medium", 512, "order2_nosplit"), ("medium", 512, "order2_lag0"),
                                           ("medium", 512, "order2_lag9"), ("medium", 512, "order2_narrow"),
                                           ("small", 256, "order2_fused"), ("medium", 0, "order2_fused"),
+                                          ("small", 256, "order2_nb1"), ("medium", 512, "order2_nb1"),
+                                          ("odd", 256, "order2_nb1"),
                                           ("tiny_ragged", 0, "sl"), ("small", 0, "sl"),
                                           ("small", 1024, "sl"), ("medium", 0, "sl"),
                                           ("medium", 2048, "sl128"), ("odd", 256, "sl"),
@@ -396,3 +399,20 @@ def test_single_rank_nccl_communicator(cuda_lib):
         assert torch.equal(buf, torch.arange(1000, dtype=torch.float32, device="cuda"))
     finally:
         binding.attn_comm_destroy(comm)
+
+
+@pytest.mark.gpu
+def test_nonfinite_loss_aborts(cuda_lib):
+    """a non-finite loss is reported (check_finite), a finite one passes."""
+    from paper_1909_00562_b200.stage import AttnSoftmaxStage, NonFiniteLoss, to_device
+    cfg = CONFIGS["small"]
+    inp = make_inputs(cfg)
+    scale = 1.0 / global_valid_tokens(cfg, cfg.B)
+    st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
+    dv = to_device(inp, cfg.dtype)
+    args = (dv["H_dec"], dv["H_enc"], dv["src_len"], dv["tgt_len"], dv["tgt_ids"], dv["W_c"])
+    st(*args, dv["W_out"], scale, check_finite=True)
+    bad = dv["W_out"].clone()
+    bad[int(inp["tgt_ids"][0, 0])] = float("nan")
+    with pytest.raises(NonFiniteLoss):
+        st(*args, bad, scale, check_finite=True)
