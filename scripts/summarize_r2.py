@@ -47,7 +47,7 @@ def step_name(i, k, prev):
     if k.startswith("lse_reduce"):
         return "F5 lse_reduce (lse, NLL, loss)"
     if k.startswith("vocab_kernel"):
-        return "B1 vocab backward, persistent (recompute per V-chunk, dL in L2 scratch, dHc, dW_out)"
+        return "B1 vocab backward, persistent (recompute per V-chunk, dL chunk scratch, dHc, dW_out)"
     if k.startswith("dz_kernel"):
         return "B1' dz = dHc (1 - H_c^2) (+ zero dW_c)"
     if k.startswith("gemm_tc"):
