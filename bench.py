@@ -634,9 +634,8 @@ def main():
     assert abs(float(loss_pin[(args.steps - 1) % 2].item()) - loss) <= 1e-6 * max(1.0, abs(loss)), \
         "e2e loss mismatch"
 
-    # ---- roofline of the dominant kernel: the vocab-backward tcgen05 GEMM
-    # launches (one per V-chunk, with the chunk's elementwise dlogits kernel).
-    # Algorithmic FLOPs per valid token: 4 d V (dW_out and dHc).
+    # ---- roofline of the dominant kernel: the persistent vocab-backward
+    # launch.  Algorithmic FLOPs per valid token: 4 d V (dW_out and dHc).
     pk = peaks()
     T_valid = tok_local
     # the dominant kernel is the persistent vocabulary launch (vocab_kernel):
@@ -668,8 +667,9 @@ def main():
                 "traffic": traffic,
                 "kernel": ("vocab_kernel, one persistent tcgen05 launch: " +
                            ("F4 logits tiles -> online LSE, then " if fused else "") +
-                           "per L2-sized V-chunk the logits recomputed into bf16 dL = "
-                           "rs (softmax - onehot) (never stored in full), dHc += dL W_out, "
+                           "per V-chunk the logits recomputed into bf16 dL = "
+                           "rs (softmax - onehot) (the logits never stored; the dL chunk "
+                           "scratch is written back to DRAM, DESIGN.md 6.1), dHc += dL W_out, "
                            "dW_out = dL^T H_c; achieved counts " +
                            ("6" if fused else "4") + " d V useful FLOP per valid token "
                            "(the recomputed logits not counted); traffic: DRAM bytes of one "
@@ -677,6 +677,10 @@ def main():
                 "executed_tflops": hw_per_tok * T_valid / (vb_ms / 1e3) / 1e12 if vb_ms > 0 else None,
                 "peak_source": pk["src"] + (", burst bf16 (timed region at max SM clock)" if at_max
                                             else ", sustained bf16 (clocks below max)"),
+                # context: the kernel runs power-capped (clock64 / globaltimer traces
+                # put its SM clock at 1.54-1.65 GHz), i.e. nearer the
+                # sustained figure than the burst one that `frac` divides by
+                "frac_vs_sustained": (achieved / pk["bf16_sus"]) if achieved else None,
                 "vocab_fwd": {"achieved": vf_flops / (vf_ms / 1e3) / 1e12 if vf_ms > 0 else None,
                               "peak": pk["bf16"], "unit": "TFLOP/s"},
                 "stage_ms": {k: v / args.steps for k, v in stage_ms.items()}}
