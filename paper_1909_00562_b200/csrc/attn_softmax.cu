@@ -152,6 +152,8 @@ static int g_opt_vb_g2split = 1;
 // claimed tile never waits behind a long one; C1 vocab backward 1.57-1.59 ->
 // 1.52 ms, two alternating same-box pairs), -1 = 1 for order 2 only
 static int g_opt_vb_claim = 1;
+// "vb_g1wide": G1 (dL) tiles 512 columns wide on CTA pairs (VbParams::g1wide)
+static int g_opt_vb_g1wide = 0;
 static int g_vb_debug = 0;    // "vb_debug": timing experiments (vocab.cuh VbParams::debug)
 static int g_opt_vb_wide = 1; // "vb_wide": 512-column G2 / G3 tiles on CTA pairs (VbParams::wide)
 static int g_opt_vb_l2 = 3;   // "vb_l2hints": VbParams::l2hints
@@ -251,6 +253,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   if (!strcmp(key, "vb_lag")) {
     if (value < 0 || value > 64) return fail(ATTN_ERR_INVALID_ARG, "vb_lag must be in [0, 64]");
     g_opt_vb_lag = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "vb_g1wide")) {
+    g_opt_vb_g1wide = value != 0;
     return ATTN_OK;
   }
   if (!strcmp(key, "vb_claim")) {
@@ -1527,6 +1533,8 @@ static attn_status_t launch_vocab_k(const Plan& p, const VbArgs& a, int ctas, cu
   P.h0 = P.nh == 2 ? (P.nrb + 1) / 2 : P.nrb;
   P.lag = g_opt_vb_lag;
   P.claim_late = g_opt_vb_claim < 0 ? (P.order == 2 ? 1 : 0) : g_opt_vb_claim;
+  P.g1wide = (kPair && g_opt_vb_g1wide) ? 1 : 0;
+  const int g1w = P.g1wide ? 2 * VB_BN : VB_BN;   // G1 tile columns
   P.n2max = L.n2max;
   P.trace = g_vb_trace;
   P.debug = g_vb_debug;
@@ -1537,17 +1545,17 @@ static attn_status_t launch_vocab_k(const Plan& p, const VbArgs& a, int ctas, cu
   if (P.order == 2) {   // block c = chunk c: G1(c), G3(c), nh x G2(c)
     for (int c = 0; c < p.nchunks; ++c) {
       P.blk_start[c] = t;
-      t += P.nrb * ((vcc(c) + VB_BN - 1) / VB_BN) + P.nrb * P.ndw +
+      t += P.nrb * ((vcc(c) + g1w - 1) / g1w) + P.nrb * P.ndw +
            P.nh * ((vcc(c) + Cfg::TM - 1) / Cfg::TM) * P.ndw;
     }
     P.blk_start[p.nchunks] = t;
   } else {
     P.blk_start[0] = 0;
-    t += P.nrb * ((vcc(0) + VB_BN - 1) / VB_BN);
+    t += P.nrb * ((vcc(0) + g1w - 1) / g1w);
     for (int c = 0; c < p.nchunks; ++c) {
       P.blk_start[c + 1] = t;
       t += P.nrb * P.ndw + ((vcc(c) + Cfg::TM - 1) / Cfg::TM) * P.ndw;
-      if (c + 1 < p.nchunks) t += P.nrb * ((vcc(c + 1) + VB_BN - 1) / VB_BN);
+      if (c + 1 < p.nchunks) t += P.nrb * ((vcc(c + 1) + g1w - 1) / g1w);
     }
     P.blk_start[p.nchunks + 1] = t;
   }

@@ -141,6 +141,9 @@ struct alignas(64) VbParams {
   int last_g2_first;     // last block: G2 tiles before G3 tiles
   int order;             // 0: block c+1 = G3(c), G2(c), G1(c+1); 1: G1(c+1), G3(c), G2(c);
                          // 2: row-interleaved (block c = chunk c, see vb_decode_o2)
+  int g1wide;            // G1 tiles 512 columns wide on CTA pairs (both accumulators,
+                         // two chains at the full tensor rate; the epilogue no longer
+                         // overlaps the next tile's MMAs)
   int claim_late;        // claim the next tile near the end of the current one's loads
                          // (default: right after its first load)
   int nh;                // order 2: G2 split over T in nh (1 or 2) row halves (else 1)
@@ -175,6 +178,12 @@ __device__ __forceinline__ int vb_vcc(const VbParams& P, int c) {
   return min(P.Vc, P.V - c * P.Vc);
 }
 
+// G1 tiles per row block of a chunk of vcc columns
+__device__ __forceinline__ int vb_g1cols(const VbParams& P, int vcc) {
+  const int w = P.g1wide ? 2 * VB_BN : VB_BN;
+  return (vcc + w - 1) / w;
+}
+
 // G2 tile of row half h: K range [k0, k0 + rows) of the T rows
 template <bool kPair>
 __device__ __forceinline__ void vb_g2_range(const VbParams& P, int h, int& k0, int& kb) {
@@ -198,7 +207,7 @@ template <bool kPair>
 __device__ __forceinline__ void vb_decode_o2(const VbParams& P, int c, int u, VbTile& r) {
   constexpr int TM = VbCfg<kPair>::TM;
   const int vcc = vb_vcc(P, c);
-  const int ncol = (vcc + VB_BN - 1) / VB_BN;
+  const int ncol = vb_g1cols(P, vcc);
   const int n2 = ((vcc + TM - 1) / TM) * P.ndw;
   const int L = P.lag, nrb = P.nrb, ndw = P.ndw;
   auto prefix = [&](int rb) { return rb * ncol + max(0, rb - L) * ndw; };
@@ -278,8 +287,7 @@ __device__ __forceinline__ VbTile vb_decode(const VbParams& P, int t) {
     const int n3 = P.nrb * P.ndw;
     const int n2 = ((vb_vcc(P, c) + TM - 1) / TM) * P.ndw;
     const bool g2first = P.last_g2_first && c == P.nchunks - 1;
-    const int n1 = (P.order == 1 && c + 1 < P.nchunks)
-                       ? P.nrb * ((vb_vcc(P, c + 1) + VB_BN - 1) / VB_BN) : 0;
+    const int n1 = (P.order == 1 && c + 1 < P.nchunks) ? P.nrb * vb_g1cols(P, vb_vcc(P, c + 1)) : 0;
     if (u < n1) {   // order 1: the next chunk's G1 tiles open the block
       r.type = VB_G1; r.c = c + 1;
     } else {
@@ -298,7 +306,7 @@ __device__ __forceinline__ VbTile vb_decode(const VbParams& P, int t) {
   }
   r.vcc = vb_vcc(P, r.c);
   if (r.type == VB_G1) {
-    const int ncol = (r.vcc + VB_BN - 1) / VB_BN;
+    const int ncol = vb_g1cols(P, r.vcc);
     r.i = u / ncol; r.j = u % ncol;
     r.kb_total = P.d / VB_BK;
   } else if (r.type == VB_G3) {
@@ -558,7 +566,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
         fence_proxy_async_global();
       }
       VB_TRACE(t, 3, vb_gt());
-      const bool wide = kPair && P.wide && (tl.type == VB_G2 || tl.type == VB_G3);
+      const bool wide = kPair && ((P.wide && (tl.type == VB_G2 || tl.type == VB_G3)) ||
+                                  (P.g1wide && tl.type == VB_G1));
       const int arow = tl.i * TM + 128 * rank;            // this CTA's A rows (M)
       const int bcol = tl.j * (wide ? 2 * VB_BN : VB_BN) + Cfg::B_ROWS * rank;  // this CTA's B rows (N)
       const int bcolg = (tl.type == VB_G0 ? 0 : c0) + bcol;
@@ -609,7 +618,9 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
             }
             const int k0 = kb * VB_BK;
             if (skip_t) {
-            } else if (tl.type == VB_G3)
+            } else if (tl.type == VB_G1)
+              vb_load<kPair>(sB, &P.m_wo_k, &full[s], barc, k0, bcolg + VB_BN, 0, pol_norm);
+            else if (tl.type == VB_G3)
               vb_load4<kPair>(sB, &P.m_wo_mn, &full[s], barc, 0, c0 + k0, (bcol + VB_BN) / 64, 0, pol_norm);
             else
               vb_load4<kPair>(sB, &P.m_hc_mn, &full[s], barc, 0, tl.k0 + k0, (bcol + VB_BN) / 64, 0, pol_keep);
@@ -667,7 +678,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
         const uint32_t a_k16 = a_mn ? (2048u >> 4) : (32u >> 4);
         const uint32_t b_k16 = b_mn ? (2048u >> 4) : (32u >> 4);
         const int kb_read = tl.kb_total > 1 ? 1 : 0;
-        const bool wide = kPair && P.wide && (tl.type == VB_G2 || tl.type == VB_G3);
+        const bool wide = kPair && ((P.wide && (tl.type == VB_G2 || tl.type == VB_G3)) ||
+                                    (P.g1wide && tl.type == VB_G1));
         int t_nxt = -1;
         // a wide tile takes both accumulators: slot acc, then the next one
         const int acc2 = acc ^ 1;
@@ -938,14 +950,14 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           __syncwarp();
         }
         float c2 = -1000.f, fix = 0.f;
-        int yl = -1;   // target column relative to this warp's first column
+        int yl0 = -1;   // target column relative to the chunk's first column
         if (row < P.T) {
           const float rs = __ldcg(P.rowscale + row);   // written by this launch's LSE warps
           if (rs > 0.f) {
             const float ls = __ldcg(P.lse + row);
             c2 = __log2f(rs) - ls * kLog2e;
             fix = rs * (__expf(__ldcg(P.tgt_logit + row) - ls) - 1.f);
-            yl = P.tgt[row] - c0 - colh;
+            yl0 = P.tgt[row] - c0;
           }
         }
         // the buffer rows are free once chunk c - NB's G2 / G3 tiles have loaded
@@ -961,6 +973,15 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           fence_proxy_async_global();
         }
         if (warp == 0) VB_TRACE(t, 12, vb_gt());   // after the lse / buffer waits
+        // a wide G1 tile (option vb_g1wide) is 512 columns: two 256-column
+        // halves, one per accumulator, drained in turn
+        const int nhalf1 = (kPair && P.g1wide) ? 2 : 1;
+#pragma unroll 1
+        for (int half = 0; half < nhalf1; ++half) {
+        if (half > 0 && ++acc == 2) { acc = 0; aph ^= 1; }
+        const int colh = (tl.j * nhalf1 + half) * VB_BN + h * 128;
+        const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * VB_BN + h * 128;
+        const int yl = yl0 >= 0 ? yl0 - colh : -1;
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         if (warp == 0) {
@@ -1046,11 +1067,15 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
         if (lane == 0) {
           if (!(P.debug & 8)) bulk_wait0();
           fence_proxy_async_global();
-          red_release_gpu_add(P.rowdone + (size_t)tl.c * P.nrb + tl.i, 1u);
           const int hh = (P.nh == 2 && tl.i >= P.h0) ? 1 : 0;
-          red_release_gpu_add(P.coldone + ((size_t)tl.c * P.nh + hh) * P.ncolf + tl.j, 1u);
+          const int cb = tl.j * nhalf1 + half;   // 256-column block of the chunk
+          if (cb * VB_BN < tl.vcc) {   // (a wide tile's second half may lie past the chunk)
+            red_release_gpu_add(P.rowdone + (size_t)tl.c * P.nrb + tl.i, 1u);
+            red_release_gpu_add(P.coldone + ((size_t)tl.c * P.nh + hh) * P.ncolf + cb, 1u);
+          }
         }
         __syncwarp();
+        }   // half
       } else {
         // ---- fp32 output: dW_out[c] rows (G2) or dHc (G3; chunk 0 stores, the
         // later chunks reduce-add in chunk order); a wide tile is drained as two

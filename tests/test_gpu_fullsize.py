@@ -39,7 +39,7 @@ def gpu_run(cfg, inp, scale, opts=None):
     from paper_1909_00562_b200 import binding
     from paper_1909_00562_b200.stage import AttnSoftmaxStage, to_device
     opts = opts or {}
-    saved = {"vb_pair": 1, "vb_fwd_fused": 0, "vb_order": 1}
+    saved = {"vb_pair": 1, "vb_fwd_fused": 0, "vb_order": 1, "vb_g1wide": 0}
     for k, v in opts.items():
         binding.attn_softmax_set_option(k, v)
     try:
@@ -99,13 +99,13 @@ def c1_case(w_out_scale):
     return _C1[w_out_scale]
 
 
-@pytest.mark.parametrize("mode", ["default", "single", "fused", "order1", "order2"])
+@pytest.mark.parametrize("mode", ["default", "single", "fused", "order1", "order2", "g1wide"])
 def test_paper_c1_full_oracle(cuda_lib, mode):
     """C1, the whole oracle, on the bench's path (default: persistent vocab
     launch on CTA pairs, logits recomputed per L2-sized V-chunk, never
     stored) and its variants."""
     opts = {"default": {}, "single": {"vb_pair": 0}, "fused": {"vb_fwd_fused": 1},
-            "order1": {"vb_order": 1}, "order2": {"vb_order": 2}}[mode]
+            "order1": {"vb_order": 1}, "order2": {"vb_order": 2}, "g1wide": {"vb_g1wide": 1}}[mode]
     cfg, inp, scale, f, b = c1_case(1)
     g = gpu_run(cfg, inp, scale, opts)
     assert abs(g["loss"] - f["loss"]) <= LOSS_TOL * abs(f["loss"]), (g["loss"], f["loss"])

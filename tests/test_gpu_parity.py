@@ -79,7 +79,8 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, wide):
 # ------------------------------------------------------ end-to-end parity --
 _DEFAULTS = {"store_logits": 0, "wide_tiles": 2, "db_gemm": -1, "vb_pair": 1, "vb_fwd_fused": 0,
              "vb_order": 1, "dl_buffers": 3, "dl_budget_mb": 120, "vb_last_g2_first": 1,
-             "attn_fused": 1, "vb_wide": 1, "vb_lag": 2, "vb_g2split": 1, "vb_claim": 1}
+             "attn_fused": 1, "vb_wide": 1, "vb_lag": 2, "vb_g2split": 1, "vb_claim": 1,
+             "vb_g1wide": 0}
 _MODES = {
     "default": {},                                  # persistent vocab launch on CTA pairs
     "single": {"vb_pair": 0},                       # ... on single-CTA 128 x 256 tiles
@@ -95,6 +96,8 @@ _MODES = {
     "narrow": {"vb_wide": 0},                       # G2 / G3 on 256-column tiles (default: 512 when d % 512 == 0)
     "order2": {"vb_order": 2},                      # row-interleaved dispatch, G2 split in two row halves
     "claim0": {"vb_claim": 0},                      # next tile claimed right after the first load
+    "g1wide": {"vb_g1wide": 1},                     # 512-column G1 (dL) tiles, both accumulators
+    "g1wide_o2": {"vb_g1wide": 1, "vb_order": 2},
     "order2_single": {"vb_order": 2, "vb_pair": 0},
     "order2_nosplit": {"vb_order": 2, "vb_g2split": 0},
     "order2_lag0": {"vb_order": 2, "vb_lag": 0, "dl_buffers": 2},
@@ -140,6 +143,10 @@ def set_modes(binding, mode):
                                           ("medium", 512, "g3last"),
                                           ("medium", 0, "narrow"), ("medium", 512, "narrow"),
                                           ("small", 256, "claim0"), ("medium", 512, "claim0"),
+                                          ("small", 0, "g1wide"), ("small", 256, "g1wide"),
+                                          ("medium", 512, "g1wide"), ("medium", 0, "g1wide"),
+                                          ("odd", 256, "g1wide"), ("edge_min", 0, "g1wide"),
+                                          ("edge_max_src", 256, "g1wide"), ("medium", 512, "g1wide_o2"),
                                           ("small", 0, "order2"), ("small", 256, "order2"),
                                           ("medium", 0, "order2"), ("medium", 512, "order2"),
                                           ("odd", 256, "order2"), ("edge_min", 0, "order2"),
