@@ -70,10 +70,19 @@ namespace attnsm {
 constexpr int VB_BN = 256;
 constexpr int VB_BK = 64;
 constexpr int VB_EPI_WARPS = 8;
-constexpr int VB_STG_BYTES = 4096;                 // staging per epilogue warp
+// VB_STG_DB = 1 (experiment): two 4 KB staging buffers per epilogue warp (a
+// store's shared memory is refilled while the previous one is still being
+// read by the TMA unit), paid for with one ring stage (160 instead of 192 KB).
+// Measured 6% slower at C1 (1.645 vs 1.549 ms, three alternating same-box
+// pairs): the wide G2 / G3 tiles need the sixth stage (666-691 instead of
+// ~520 cycles per 512 of work with five)
+#ifndef VB_STG_DB
+#define VB_STG_DB 0
+#endif
+constexpr int VB_STG_BYTES = VB_STG_DB ? 8192 : 4096;   // staging per epilogue warp
 constexpr int VB_THREADS = 384;
 constexpr int VB_SCHED = 4;
-constexpr int VB_RING = 192 * 1024;
+constexpr int VB_RING = (VB_STG_DB ? 160 : 192) * 1024;
 constexpr int VB_SMEM_BYTES = VB_RING + VB_EPI_WARPS * VB_STG_BYTES + 1024 + 512;
 constexpr int VB_MAX_BLOCKS = 1024;                // chunks + 1
 
@@ -839,8 +848,9 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
     // ---------------- epilogue (8 warps per CTA): this CTA's 128 rows of the tile
     const uint32_t q = warp & 3;        // TMEM lane quarter: rows 32q..32q+31 of this CTA's 128
     const uint32_t h = warp >> 2;       // column half of the 256-wide tile
-    uint8_t* stg_p = staging + warp * VB_STG_BYTES;
-    const uint32_t stg = smem_u32(stg_p);
+    uint8_t* stg_base = staging + warp * VB_STG_BYTES;
+    uint32_t stg_seq = 0;   // staged store groups of this warp (buffer = stg_seq & 1)
+    const uint32_t stg_base_u = smem_u32(stg_base);
     const uint32_t swz = lane & 7;
     // l2hints bit 2: the dL chunk stores stay in L2 until its G2 / G3 readers come
     const uint64_t pol_dl = l2_policy_evict_last();
@@ -996,6 +1006,10 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
         }
 #pragma unroll 1
         for (int cc = 0; cc < 4 && !(P.debug & 128); ++cc) {
+          // one store group per two 32-column chunks (32 rows x 64 bf16 = 4 KB)
+          const uint32_t sbuf = VB_STG_DB ? ((stg_seq & 1u) << 12) : 0u;
+          const uint32_t stg = stg_base_u + sbuf;
+          uint8_t* stg_p = stg_base + sbuf;
           float v[32];
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(raw[e]);
@@ -1028,7 +1042,10 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           // next chunk's accumulator columns load while this one is staged
           if (cc < 3) tmem_ld32_issue(taddr + (cc + 1) * 32, raw);
           if ((cc & 1) == 0) {
-            if (lane == 0) bulk_wait_read0();
+            if (lane == 0) {
+              if (VB_STG_DB) bulk_wait_read1();   // the other buffer may still be read
+              else bulk_wait_read0();
+            }
             __syncwarp();
           }
 #pragma unroll
@@ -1052,6 +1069,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
                 tma_store_3d(&P.m_dl_st, stg_p, colh + (cc - 1) * 32, row0, buf);
               bulk_commit();
             }
+            ++stg_seq;
           }
           if (cc < 3) tmem_ld_wait_regs(raw);
         }
@@ -1125,9 +1143,15 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
 #pragma unroll 1
           for (int cc = 0; cc < 4; ++cc) {
             if (cc * 32 >= ncols) break;
+            const uint32_t sbuf = VB_STG_DB ? ((stg_seq & 1u) << 12) : 0u;
+            const uint32_t stg = stg_base_u + sbuf;
+            uint8_t* stg_p = stg_base + sbuf;
             float v[32];
             tmem_ld32(taddr + cc * 32, v);
-            if (lane == 0) bulk_wait_read0();
+            if (lane == 0) {
+              if (VB_STG_DB) bulk_wait_read1();   // the other buffer may still be read
+              else bulk_wait_read0();
+            }
             __syncwarp();
 #pragma unroll
             for (int g = 0; g < 8; ++g)
@@ -1147,6 +1171,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
                 tma_reduce_add_2d_hint(&P.m_dhc_st, stg_p, colh + cc * 32, row0, pol_dhc);
               bulk_commit();
             }
+            ++stg_seq;
           }
           tc_fence_before();
           __syncwarp();
