@@ -59,6 +59,19 @@ def workload_desc(cfg, world):
             "l2": "flushed between timed steps (256 MiB write outside the timed events)"}
 
 
+def build_id(binding):
+    """The library's version string and a hash of the sources it was built
+    from (csrc/ and include/; .git does not travel to the GPU box)."""
+    import hashlib
+    h = hashlib.sha1()
+    for sub in ("paper_1909_00562_b200/csrc", "include"):
+        d = os.path.join(ROOT, sub)
+        for f in sorted(os.listdir(d)):
+            with open(os.path.join(d, f), "rb") as fh:
+                h.update(f.encode() + fh.read())
+    return {"library": binding.lib().attn_version().decode(), "source_sha1": h.hexdigest()[:12]}
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -698,6 +711,7 @@ def main():
             "roofline": roofline,
             "gpu_launches": int(launches_per_step) * args.steps,
             "clocks": clocks,
+            "build": build_id(binding),
             "loss": loss,
             "comm": None if comm is None else {"nranks": binding.attn_comm_nranks(comm),
                                                "exchange_check": verify},
