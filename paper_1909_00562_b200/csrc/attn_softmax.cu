@@ -304,6 +304,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
     g_prof.vocab_only = value == 2;
     return ATTN_OK;
   }
+  if (!strcmp(key, "comm_reserve_1rank")) {
+    g_comm_reserve_1rank = value != 0;
+    return ATTN_OK;
+  }
   if (!strcmp(key, "comm_max_ctas")) {
     if (value < 0 || value > 64) return fail(ATTN_ERR_INVALID_ARG, "comm_max_ctas must be in [0, 64]");
     g_comm_max_ctas = (int)value;

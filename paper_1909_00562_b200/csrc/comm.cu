@@ -315,7 +315,12 @@ attn_status_t comm_all_gather_bf16(attn_comm_t* c, void* buf, size_t shard, cuda
 }
 
 // one rank: the "allreduce" moves nothing, so no SMs are set aside
-int comm_max_ctas(const attn_comm_t* c) { return c && c->nranks > 1 ? c->max_ctas : 0; }
+// "comm_reserve_1rank" option (tests): reserve the communicator's SMs on a
+// 1-rank communicator too, so one GPU exercises the reduced-grid launches
+int g_comm_reserve_1rank = 0;
+int comm_max_ctas(const attn_comm_t* c) {
+  return c && (c->nranks > 1 || g_comm_reserve_1rank) ? c->max_ctas : 0;
+}
 
 // NEXT-3: MP -> DP scatter of the hidden states (attn_softmax.h).  Shards are
 // contiguous sentence ranges, sizes differing by at most one, lower ranks

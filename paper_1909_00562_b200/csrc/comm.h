@@ -43,3 +43,4 @@ attn_status_t comm_all_gather_bf16(attn_comm_t* c, void* buf, size_t shard, cuda
 // persistent GEMMs leave that many SMs free while gradients are in flight.
 int comm_max_ctas(const attn_comm_t* c);
 extern int g_comm_max_ctas;
+extern int g_comm_reserve_1rank;

@@ -363,14 +363,19 @@ def test_host_buffer_paths_match_device_path(cuda_lib):
             assert torch.equal(out[k], ref[k]), k
 
 
-def test_single_rank_nccl_communicator(cuda_lib):
+@pytest.mark.parametrize("name,reserve", [("small", 0), ("small", 1), ("medium", 1)])
+def test_single_rank_nccl_communicator(cuda_lib, name, reserve):
     """The NCCL path of attn_softmax_fwd_bwd (dlopen'ed libnccl, comm stream,
     per-chunk dW_out allreduce, dW_c and loss allreduce, join) on a 1-rank
     communicator: the sum over one rank is the identity, so results must be
-    bitwise equal to the local call.  attn_grad_allreduce is checked too."""
+    bitwise equal to the local call.  attn_grad_allreduce is checked too.
+    reserve = 1 leaves the communicator's SMs free as with several ranks (the
+    persistent launches on a reduced grid: fixed summation orders, so still
+    bitwise)."""
     from paper_1909_00562_b200 import binding
     from paper_1909_00562_b200.stage import AttnSoftmaxStage, to_device
-    cfg = CONFIGS["small"]
+    binding.attn_softmax_set_option("comm_reserve_1rank", reserve)
+    cfg = CONFIGS[name]
     inp = make_inputs(cfg)
     scale = 1.0 / global_valid_tokens(cfg, cfg.B)
     st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
@@ -406,6 +411,7 @@ def test_single_rank_nccl_communicator(cuda_lib):
         assert torch.equal(buf, torch.arange(1000, dtype=torch.float32, device="cuda"))
     finally:
         binding.attn_comm_destroy(comm)
+        binding.attn_softmax_set_option("comm_reserve_1rank", 0)
 
 
 @pytest.mark.gpu
