@@ -130,7 +130,8 @@ constexpr int kEwParts = 320;   // row-group partial rows of the dlogits kernels
 // 0 (default): the persistent vocab kernel recomputes the logits per chunk.
 static int g_opt_store_logits = 0;
 // "dl_budget_mb": bytes of the dL chunk scratch (all NB buffers) the V-chunk
-// width is sized to, so it stays L2-resident; "dl_buffers": NB
+// width is sized to (an L2-sized budget; the dL lines are still written back
+// to DRAM); "dl_buffers": NB
 static int64_t g_opt_dl_budget_mb = 120;
 static int g_opt_dl_nbuf = 3;
 // "vb_last_g2_first": last block of the persistent backward dispatches the
@@ -1671,7 +1672,8 @@ static attn_status_t run_stage(const Plan& p, const T* H, const T* S, const int3
   }
   // ---- F4 + F5 + B1, bf16: ONE persistent launch (vocab.cuh): the logits
   // tiles' (max, sum exp) partials, lse / NLL / loss, and the backward with
-  // the logits recomputed per L2-sized V-chunk -- the logits never reach HBM
+  // the logits recomputed per V-chunk -- the logits never reach HBM (their bf16
+  // gradient dL passes through an L2-sized chunk scratch)
   if (p.vb) {
     if (!g_opt_vb_fwd) {
       // F4 on the single-CTA engine (logits discarded, per-tile (max, sum

@@ -3,9 +3,11 @@
 // NLL, loss; Eq. 6) and B1 (their backward).  The logits are never stored:
 // the forward keeps per-tile (max, sum exp) partials only, and the backward
 // recomputes the logits per V-chunk on the tensor cores, turning them into
-// dL = rs (softmax - onehot) (bf16) in an L2-sized chunk scratch that the same
-// launch consumes for dW_out and dHc (north_star "full
-// logits are never round-tripped through HBM").
+// dL = rs (softmax - onehot) (bf16) in a chunk scratch sized for the L2 that
+// the same launch consumes for dW_out and dHc (north_star
+// "full logits are never round-tripped through HBM").  Measured: the dL lines
+// are written back to DRAM once and, with dispatch orders 0 / 1, read back by
+// their consumers; order 2 keeps the reads in L2.
 //
 // Tile types (T = B*N rows, chunk c = vocabulary columns [c0, c0 + vcc)):
 //   G0       logits H_c W_out^T tile -> (max, sum exp) per row of the tile,
