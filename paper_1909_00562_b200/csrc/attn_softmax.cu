@@ -156,6 +156,12 @@ static int g_opt_vb_g2split = 1;
 static int g_opt_vb_claim = 1;
 // "vb_g1wide": G1 (dL) tiles 512 columns wide on CTA pairs (VbParams::g1wide)
 static int g_opt_vb_g1wide = 0;
+// "gemm_claim": bitmask of GEMM groups (the PAIR_* bits of "wide_tiles") whose
+// tiles are claimed late (TcParams::claim_late).  Default: the projection
+// backward (B2a's mix of 16- and 50-k-block tiles: 46.6 / 49.1 / 54.3 ->
+// 41.0 / 43.9 / 45.5 us, alternating pairs); the uniform forward GEMMs were
+// neutral to slightly slower
+static int g_opt_gemm_claim = PAIR_PBWD;
 static int g_vb_debug = 0;    // "vb_debug": timing experiments (vocab.cuh VbParams::debug)
 static int g_opt_vb_wide = 1; // "vb_wide": 512-column G2 / G3 tiles on CTA pairs (VbParams::wide)
 static int g_opt_vb_l2 = 3;   // "vb_l2hints": VbParams::l2hints
@@ -255,6 +261,10 @@ extern "C" attn_status_t attn_softmax_set_option(const char* key, int64_t value)
   if (!strcmp(key, "vb_lag")) {
     if (value < 0 || value > 64) return fail(ATTN_ERR_INVALID_ARG, "vb_lag must be in [0, 64]");
     g_opt_vb_lag = (int)value;
+    return ATTN_OK;
+  }
+  if (!strcmp(key, "gemm_claim")) {
+    g_opt_gemm_claim = (int)value;
     return ATTN_OK;
   }
   if (!strcmp(key, "vb_g1wide")) {
@@ -618,7 +628,7 @@ static attn_status_t ensure_smem_attr(K kernel, int bytes) {
 
 template <typename OutT, int kPair, bool kDecode = false>
 static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, cudaStream_t stream,
-                                       int ctas = 0) {
+                                       int ctas = 0, int group_bit = 0) {
   attn_status_t st;
   if ((st = ensure_smem_attr(gemm_tc_kernel<OutT, true, kPair, kDecode>, tc_smem_bytes())) !=
       ATTN_OK)
@@ -634,6 +644,7 @@ static attn_status_t launch_tc_group_k(const GemmDesc* gs, int n, int* counter, 
   P.nprob = n;
   P.total_tiles = tiles;
   P.tile_counter = counter;
+  P.claim_late = (g_opt_gemm_claim & group_bit) ? 1 : 0;
   P.trace = (g_trace_launch < 0 || g_trace_launch == g_launches) ? g_trace : nullptr;
   if (tiles == 0) return ATTN_OK;
   const DevInfo di = dev_info();
@@ -661,8 +672,8 @@ template <typename OutT>
 static attn_status_t launch_tc_group(const GemmDesc* gs, int n, int* counter, cudaStream_t stream,
                                      int group_bit = 0, int ctas = 0) {
   if (group_bit && (g_opt_wide & group_bit))
-    return launch_tc_group_k<OutT, 4>(gs, n, counter, stream, ctas);
-  return launch_tc_group_k<OutT, 1>(gs, n, counter, stream, ctas);
+    return launch_tc_group_k<OutT, 4>(gs, n, counter, stream, ctas, group_bit);
+  return launch_tc_group_k<OutT, 1>(gs, n, counter, stream, ctas, group_bit);
 }
 
 // Launch a plain kernel, as a programmatic dependent of the previous kernel

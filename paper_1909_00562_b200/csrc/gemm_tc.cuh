@@ -93,6 +93,8 @@ struct alignas(64) TcParams {
   int total_tiles;
   int* tile_counter;
   long long* trace;   // debug: per-tile timestamps (null = off); 8 x int64 per tile
+  int claim_late;     // claim the next tile two k-blocks before the end of the current
+                      // one's loads (default: right after its first load)
 };
 
 // trace record layout per tile t (clock64 of the SM that ran it):
@@ -428,7 +430,7 @@ __global__ void __maxnreg__(128) gemm_tc_kernel(const __grid_constant__ TcParams
         mbar_arrive(&sfull[r]);
       }
       __syncwarp();
-      if (t >= 0) fetch();
+      if (t >= 0 && !P.claim_late) fetch();
       if (++r == TC_SCHED) { r = 0; rph ^= 1; }
       return t;
     };
@@ -482,12 +484,18 @@ __global__ void __maxnreg__(128) gemm_tc_kernel(const __grid_constant__ TcParams
         if (kb == 0) TC_TRACE(t, 11);             // first load issued
         if (kb == kb_total - 1) TC_TRACE(t, 2);   // last load issued
         if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
-        if (kb == 0) {
+        if (P.claim_late) {
+          if (kb == max(0, kb_total - 2)) fetch();
+        } else if (kb == 0) {
           // the next tile: fetch, publish and decode in the shadow of this one
           t_nxt = next_tile();
           if (t_nxt >= 0) tl_nxt = tc_decode<kPair>(P, t_nxt);
           if (t_nxt >= 0) TC_TRACE(t_nxt, 12);
         }
+      }
+      if (P.claim_late) {
+        t_nxt = next_tile();
+        if (t_nxt >= 0) tl_nxt = tc_decode<kPair>(P, t_nxt);
       }
       t = t_nxt;
       tl = tl_nxt;
@@ -547,13 +555,17 @@ __global__ void __maxnreg__(128) gemm_tc_kernel(const __grid_constant__ TcParams
           if (lane == 2) P.trace[(long long)t * 16 + 14] = gt;
         }
         if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
-        if (kb == kb_read) {
+        if (kb == kb_read && !P.claim_late) {
           t_nxt = ring_read(r, rph, false);
           if (t_nxt >= 0) tl_nxt = tc_decode<kPair>(P, t_nxt);
         }
       }
       if (elect_one()) umma_commit(&tfull[acc]);
       __syncwarp();
+      if (P.claim_late) {   // after the commit: the epilogue starts first
+        t_nxt = ring_read(r, rph, false);
+        if (t_nxt >= 0) tl_nxt = tc_decode<kPair>(P, t_nxt);
+      }
       TC_TRACE(t, 5);   // last commit issued
       if (P.trace) {
         const long long gt = gtime();

@@ -754,7 +754,6 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           if (++s == STAGES) { s = 0; ph ^= 1; }
           if (kb == kb_read && !P.claim_late) t_nxt = ring_read1();
         }
-        if (P.claim_late) t_nxt = ring_read1();
         if (elect_one()) {
           if constexpr (kPair) {
             umma_commit_pair(&tfull[acc]);
@@ -764,6 +763,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           }
         }
         __syncwarp();
+        if (P.claim_late) t_nxt = ring_read1();   // after the commit: the epilogue starts first
         VB_TRACE(t, 5, vb_clk());
         VB_TRACE(t, 9, vb_gt());
         VB_TRACE(t, 14, wait_cyc);

@@ -80,7 +80,7 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, wide):
 _DEFAULTS = {"store_logits": 0, "wide_tiles": 2, "db_gemm": -1, "vb_pair": 1, "vb_fwd_fused": 0,
              "vb_order": 1, "dl_buffers": 3, "dl_budget_mb": 120, "vb_last_g2_first": 1,
              "attn_fused": 1, "vb_wide": 1, "vb_lag": 2, "vb_g2split": 1, "vb_claim": 1,
-             "vb_g1wide": 0}
+             "vb_g1wide": 0, "gemm_claim": 4}
 _MODES = {
     "default": {},                                  # persistent vocab launch on CTA pairs
     "single": {"vb_pair": 0},                       # ... on single-CTA 128 x 256 tiles
@@ -97,6 +97,7 @@ _MODES = {
     "order2": {"vb_order": 2},                      # row-interleaved dispatch, G2 split in two row halves
     "claim0": {"vb_claim": 0},                      # next tile claimed right after the first load
     "g1wide": {"vb_g1wide": 1},                     # 512-column G1 (dL) tiles, both accumulators
+    "gclaim": {"gemm_claim": 15},                   # generic engine: late tile claim in every group
     "g1wide_o2": {"vb_g1wide": 1, "vb_order": 2},
     "order2_single": {"vb_order": 2, "vb_pair": 0},
     "order2_nosplit": {"vb_order": 2, "vb_g2split": 0},
@@ -143,6 +144,9 @@ def set_modes(binding, mode):
                                           ("medium", 512, "g3last"),
                                           ("medium", 0, "narrow"), ("medium", 512, "narrow"),
                                           ("small", 256, "claim0"), ("medium", 512, "claim0"),
+                                          ("small", 0, "gclaim"), ("medium", 512, "gclaim"),
+                                          ("odd", 256, "gclaim"), ("small_f32", 0, "gclaim"),
+                                          ("edge_max_src", 256, "gclaim"), ("edge_min", 0, "gclaim"),
                                           ("small", 0, "g1wide"), ("small", 256, "g1wide"),
                                           ("medium", 512, "g1wide"), ("medium", 0, "g1wide"),
                                           ("odd", 256, "g1wide"), ("edge_min", 0, "g1wide"),
