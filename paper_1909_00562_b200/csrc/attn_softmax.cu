@@ -2240,9 +2240,8 @@ attn_status_t attn_internal_step_attention(int B, int M, int d, const void* h, c
 // A^T [B0 | B1] with A [K][M], B0 [K][n0], B1 [K][N - n0] row-major bf16 (both
 // operands MN-major): dW_l = dz^T [x | h_prev] over all B T rows.  `counter`
 // is a zeroed int of the caller's workspace.
-attn_status_t attn_internal_gemm_atb(int M, int N, int K, const void* A, const void* B0, int n0,
-                                     const void* B1, float* C, int* counter, cudaStream_t stream) {
-  OPT_LOCK;
+static GemmDesc atb_desc(int M, int N, int K, const void* A, const void* B0, int n0, const void* B1,
+                         float* C) {
   GemmDesc g;
   g.M = M; g.N = N; g.K = K;
   g.a_mn = 1; g.a0 = mnmaj(A, K, M, M);
@@ -2250,7 +2249,26 @@ attn_status_t attn_internal_gemm_atb(int M, int N, int K, const void* A, const v
   g.b1 = mnmaj(B1, K, N - n0, N - n0); g.b_nsplit = n0;
   g.epi.kind = EPI_STORE_F32; g.epi.out = C; g.epi.ldo = N;
   g.epi.ncols_valid = N; g.epi.ncols_store = N;
+  return g;
+}
+attn_status_t attn_internal_gemm_atb(int M, int N, int K, const void* A, const void* B0, int n0,
+                                     const void* B1, float* C, int* counter, cudaStream_t stream) {
+  OPT_LOCK;
+  GemmDesc g = atb_desc(M, N, K, A, B0, n0, B1, C);
   return launch_tc_group<__nv_bfloat16>(&g, 1, counter, stream, 0);
+}
+// up to kMaxProblems such products in ONE launch (the layers of an LSTM side:
+// one tile list, so the layers' tiles fill the machine together)
+attn_status_t attn_internal_gemm_atb_group(int n, const int* M, const int* N, const int* K,
+                                           const void* const* A, const void* const* B0,
+                                           const int* n0, const void* const* B1, float* const* C,
+                                           int* counter, cudaStream_t stream) {
+  OPT_LOCK;
+  if (n < 1 || n > kMaxProblems)
+    return fail(ATTN_ERR_INVALID_ARG, "grouped GEMM: %d problems (1..%d)", n, kMaxProblems);
+  GemmDesc g[kMaxProblems];
+  for (int i = 0; i < n; ++i) g[i] = atb_desc(M[i], N[i], K[i], A[i], B0[i], n0[i], B1[i], C[i]);
+  return launch_tc_group<__nv_bfloat16>(g, n, counter, stream, 0);
 }
 
 extern "C" attn_status_t attn_softmax_decode_step(

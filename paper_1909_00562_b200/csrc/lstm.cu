@@ -810,6 +810,10 @@ long long* g_lstm_trace = nullptr;
 // internal entry of attn_softmax.cu: C = A^T [B0 | B1] on the tcgen05 engine (dW of the backward)
 attn_status_t attn_internal_gemm_atb(int M, int N, int K, const void* A, const void* B0, int n0,
                                      const void* B1, float* C, int* counter, cudaStream_t stream);
+attn_status_t attn_internal_gemm_atb_group(int n, const int* M, const int* N, const int* K,
+                                           const void* const* A, const void* const* B0,
+                                           const int* n0, const void* const* B1, float* const* C,
+                                           int* counter, cudaStream_t stream);
 // internal entry of attn_softmax.cu: one step of Eqs. 1-4 for the IF decoder
 size_t attn_internal_step_ws(int B, int M, int d);
 attn_status_t attn_internal_step_attention(int B, int M, int d, const void* h, const void* S,
@@ -1225,7 +1229,7 @@ TrPlan plan_train(const attn_lstm_shape_t* s, const LsPlan& base) {
   q.dhrec = take(4 * L * 2 * B * hd * 4);    // [Gk <= 4][L][2][B][hd]
   q.dh0 = take(L * B * hd * 4);
   q.dc0 = take(L * B * hd * 4);
-  q.hprev = take(B * Tm * hd * 2);
+  q.hprev = take(L * B * Tm * hd * 2);   // one [B][T][hd] h_prev per layer (grouped dW GEMM)
   q.flags = take(2 * L * Tm * 4);
   q.counter = take(256);
   q.dbpart = take(((B * Tm + 127) / 128) * 4 * hd * 4);
@@ -1415,17 +1419,35 @@ attn_status_t side_weight_grads(const attn_lstm_shape_t* s, const LsPlan& p, con
   const __nv_bfloat16* hcap = reinterpret_cast<const __nv_bfloat16*>(ws + p.hcap);
   int* counter = reinterpret_cast<int*>(ws + q.counter);
   attn_status_t r;
+  // h_prev of every layer, then the layers' dW = dz^T [x | h_prev] products in
+  // grouped launches of up to 4 (one tile list: 4 x 256 tiles at Table 1 sizes
+  // instead of 256 per launch, 1.73 waves on 148 SMs)
   for (int l = 0; l < L; ++l) {
-    const int in = l == 0 ? s->emb : hd;
-    const void* X = l == 0 ? X0 : (const void*)(inter + (size_t)(l - 1) * B * T * hd);
     const void* Hl = l == L - 1 ? H_top : (const void*)(inter + (size_t)l * B * T * hd);
     shift_h_kernel<<<sms * 4, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(Hl),
-                                            decoder ? hcap + (size_t)l * B * hd : nullptr, B, T, hd, hprev);
+                                            decoder ? hcap + (size_t)l * B * hd : nullptr, B, T, hd,
+                                            hprev + (size_t)l * B * T * hd);
     LS_CUDA(cudaGetLastError());
-    const __nv_bfloat16* dgl = dg + (size_t)l * B * T * 4 * hd;
+  }
+  for (int l0 = 0; l0 < L; l0 += 4) {
+    const int n = std::min(4, L - l0);
+    int Mv[4], Nv[4], Kv[4], n0v[4];
+    const void* Av[4]; const void* B0v[4]; const void* B1v[4]; float* Cv[4];
+    for (int i = 0; i < n; ++i) {
+      const int l = l0 + i;
+      const int in = l == 0 ? s->emb : hd;
+      Mv[i] = 4 * hd; Nv[i] = in + hd; Kv[i] = (int)rows; n0v[i] = in;
+      Av[i] = dg + (size_t)l * B * T * 4 * hd;
+      B0v[i] = l == 0 ? X0 : (const void*)(inter + (size_t)(l - 1) * B * T * hd);
+      B1v[i] = hprev + (size_t)l * B * T * hd;
+      Cv[i] = dW[l];
+    }
     LS_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
-    if ((r = attn_internal_gemm_atb(4 * hd, in + hd, (int)rows, dgl, X, in, hprev, dW[l], counter, st)) != ATTN_OK)
+    if ((r = attn_internal_gemm_atb_group(n, Mv, Nv, Kv, Av, B0v, n0v, B1v, Cv, counter, st)) != ATTN_OK)
       return r;
+  }
+  for (int l = 0; l < L; ++l) {
+    const __nv_bfloat16* dgl = dg + (size_t)l * B * T * 4 * hd;
     float* part = reinterpret_cast<float*>(ws + q.dbpart);
     const int nparts = (int)((rows + LB_CS_ROWS - 1) / LB_CS_ROWS);
     lstm_db_part_kernel<<<dim3((4 * hd + 255) / 256, nparts), 256, 0, st>>>(dgl, rows, 4 * hd, part);
