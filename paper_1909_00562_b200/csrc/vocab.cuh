@@ -81,6 +81,14 @@ constexpr int VB_EPI_WARPS = 8;
 #ifndef VB_STG_DB
 #define VB_STG_DB 0
 #endif
+// VB_STAGE3 = 1 (default): on CTA pairs a ring stage holds A and two B
+// blocks (48 KB, four stages), so a wide k-block fills ONE stage; with 32 KB
+// stages a wide k-block took two and left the second A region unused.  Wide
+// G2 / G3 tiles: 494-503 instead of 516-552 cycles per 512 of work; vocab
+// backward 1.556-1.559 vs 1.566-1.568 ms (three alternating same-box pairs)
+#ifndef VB_STAGE3
+#define VB_STAGE3 1
+#endif
 constexpr int VB_STG_BYTES = VB_STG_DB ? 8192 : 4096;   // staging per epilogue warp
 constexpr int VB_THREADS = 384;
 constexpr int VB_SCHED = 4;
@@ -95,7 +103,11 @@ struct VbCfg {
   static constexpr int B_ROWS = VB_BN / CTAS;      // B rows (N) staged per CTA
   static constexpr int A_BYTES = 128 * VB_BK * 2;  // 16 KB
   static constexpr int B_BYTES = B_ROWS * VB_BK * 2;
-  static constexpr int STAGE = A_BYTES + B_BYTES;  // 48 KB | 32 KB
+  // VB_STAGE3 (pairs): a stage holds A and TWO B blocks, so a wide k-block
+  // fills one 48 KB stage instead of two 32 KB stages (whose second A region
+  // stays unused); narrow k-blocks leave the second B empty
+  static constexpr bool S3 = kPair && VB_STAGE3;
+  static constexpr int STAGE = A_BYTES + (S3 ? 2 : 1) * B_BYTES;  // 48 KB | 32 KB (48 KB with S3)
   static constexpr int STAGES = VB_RING / STAGE;   // 4 | 6
   static constexpr int WARPS_PER_TILE = VB_EPI_WARPS * CTAS;
 };
@@ -594,8 +606,9 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           // bits 13 / 14: skip the operand loads of G2 / G3 tiles only
           const bool skip_t = (tl.type == VB_G2 && (P.debug & 8192)) || (tl.type == VB_G3 && (P.debug & 16384));
           const bool ldA = !(P.debug & 32) && !skip_t, ldB = !(P.debug & 16) && !skip_t;
+          const int nb = (Cfg::S3 && wide) ? 2 : 1;   // B blocks in this stage
           if (leader)
-            mbar_arrive_expect_tx(&full[s], ((ldA ? Cfg::A_BYTES : 0) + (ldB ? Cfg::B_BYTES : 0)) * Cfg::CTAS);
+            mbar_arrive_expect_tx(&full[s], ((ldA ? Cfg::A_BYTES : 0) + (ldB ? nb * Cfg::B_BYTES : 0)) * Cfg::CTAS);
           const int k0 = kb * VB_BK;
 #if VB_DEBUG_MMA
           if (tl.type == VB_G1 && (P.debug & 64)) {
@@ -613,10 +626,19 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
             if (ldA) vb_load4<kPair>(sA, &P.m_dl_mn, &full[s], barc, 0, tl.k0 + k0, arow / 64, buf, pol_norm);
             if (ldB) vb_load4<kPair>(sB, &P.m_hc_mn, &full[s], barc, 0, tl.k0 + k0, bcol / 64, 0, pol_keep);
           }
+          if (Cfg::S3 && wide && ldB) {   // the tile's B columns [256, 512) in the same stage
+            uint8_t* sB2 = sB + Cfg::B_BYTES;
+            if (tl.type == VB_G1)
+              vb_load<kPair>(sB2, &P.m_wo_k, &full[s], barc, k0, bcolg + VB_BN, 0, pol_norm);
+            else if (tl.type == VB_G3)
+              vb_load4<kPair>(sB2, &P.m_wo_mn, &full[s], barc, 0, c0 + k0, (bcol + VB_BN) / 64, 0, pol_norm);
+            else
+              vb_load4<kPair>(sB2, &P.m_hc_mn, &full[s], barc, 0, tl.k0 + k0, (bcol + VB_BN) / 64, 0, pol_keep);
+          }
         }
         __syncwarp();
         if (++s == STAGES) { s = 0; ph ^= 1; }
-        if (wide) {
+        if (wide && !Cfg::S3) {
           // the k-block's second stage: B columns [256, 512) of the tile (its A region unused)
           mbar_wait(&empty[s], ph ^ 1);
           if (elect_one()) {
@@ -705,21 +727,22 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
         for (int kb = 0; kb < tl.kb_total; ++kb) {
           int s2 = s;
           uint32_t ph2 = ph;
-          if (wide && ++s2 == STAGES) { s2 = 0; ph2 ^= 1; }
+          if (wide && !Cfg::S3 && ++s2 == STAGES) { s2 = 0; ph2 ^= 1; }
           if (P.trace) {
             const long long w0 = vb_clk();
             mbar_wait(&full[s], ph);
-            if (wide) mbar_wait(&full[s2], ph2);
+            if (wide && !Cfg::S3) mbar_wait(&full[s2], ph2);
             wait_cyc += vb_clk() - w0;
           } else {
             mbar_wait(&full[s], ph);
-            if (wide) mbar_wait(&full[s2], ph2);
+            if (wide && !Cfg::S3) mbar_wait(&full[s2], ph2);
           }
           tc_fence_after();
           const uint32_t sa16 = smem16 + (uint32_t)s * kStage16;
           const uint64_t ad = ad0 + sa16;
           const uint64_t bd = bd0 + sa16 + kA16;
-          const uint64_t bd2 = bd0 + smem16 + (uint32_t)s2 * kStage16 + kA16;
+          const uint64_t bd2 = Cfg::S3 ? bd + (uint32_t)(Cfg::B_BYTES >> 4)
+                                       : bd0 + smem16 + (uint32_t)s2 * kStage16 + kA16;
           if (elect_one()) {
 #if VB_DEBUG_MMA
             if (vb_debug_mma<kPair>(P, tl, kb, s, acc, tmem_base, smem, a_mn, b_mn, ad, bd)) {
@@ -739,7 +762,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
             }
             if constexpr (kPair) {
               umma_commit_pair(&empty[s]);
-              if (wide) umma_commit_pair(&empty[s2]);
+              if (wide && !Cfg::S3) umma_commit_pair(&empty[s2]);
             } else {
               umma_commit(&empty[s]);
             }
