@@ -107,7 +107,12 @@ size_t attn_softmax_workspace_size(const attn_shape_t* s);
  *     (summed over ranks when comm != NULL).
  *   dH_dec [B,N,d], dH_enc [B,M,d]: dtype s->dtype, overwritten.
  *   dW_c [d,2d], dW_out [V,d]: fp32, overwritten (allreduced when comm).
- *   comm: NULL for local gradients. */
+ *   comm: NULL for local gradients.  The first call of a path (shape,
+ *     operands, options) with a communicator on a device first runs the stage
+ *     once locally (same outputs, overwritten): it loads every kernel of the
+ *     path before the comm stream's spinning per-chunk wait kernels start
+ *     (under lazy module loading a first launch could otherwise wait for
+ *     them: a deadlock). */
 attn_status_t attn_softmax_fwd_bwd(
     const attn_shape_t* s,
     const void* H_dec, const void* H_enc,
