@@ -133,7 +133,13 @@ static int g_opt_store_logits = 0;
 // "dl_budget_mb": bytes of the dL chunk scratch (all NB buffers) the V-chunk
 // width is sized to (an L2-sized budget; the dL lines are still written back
 // to DRAM); "dl_buffers": NB
-static int64_t g_opt_dl_budget_mb = 120;
+// 200 (C1: Vc = 5376, 10 chunks): re-measured with the final kernel (wide
+// tiles, late claim, 48 KB stages) -- 2.09-2.17 vs 2.15-2.26 ms per step
+// against 120 MB (Vc = 3072), alternating same-box pairs; C4 (Vc 4352 vs
+// 2560) within noise, C3 unchanged (the 25-chunk cap sets Vc = 4096).  The
+// dL lines reach DRAM anyway, so the L2-sized budget no
+// longer decides
+static int64_t g_opt_dl_budget_mb = 200;
 static int g_opt_dl_nbuf = 3;
 // "vb_last_g2_first": last block of the persistent backward dispatches the
 // long dW_out tiles before the dHc tiles (shorter tail)

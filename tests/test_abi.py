@@ -59,18 +59,17 @@ def test_workspace_size(built_lib):
         assert binding.attn_last_error()
 
 
-@pytest.mark.parametrize("B,N,M,d,V,vc,fits", [(128, 50, 50, 1024, 50000, 3072, True),     # C1
+@pytest.mark.parametrize("B,N,M,d,V,vc,fits", [(128, 50, 50, 1024, 50000, 5376, True),     # C1
                                               (256, 64, 64, 1024, 100000, 4096, False),  # C3
-                                              (64, 120, 120, 2048, 64000, 2560, True)])  # C4
-def test_vchunk_l2_budget(built_lib, B, N, M, d, V, vc, fits):
+                                              (64, 120, 120, 2048, 64000, 4352, True)])  # C4
+def test_vchunk_budget(built_lib, B, N, M, d, V, vc, fits):
     """The persistent backward's V-chunk: the dl_buffers bf16 dL buffers
-    [T, Vc] fit the dl_budget_mb L2 budget (120 MB, 3 buffers; DESIGN.md
-    "V-chunk schedule") unless that would take more than 25 chunks (C3: each
-    chunk re-reads and re-writes the fp32 dHc, which costs more than dL's
-    L2 residency at T = 16384)."""
+    [T, Vc] fit the dl_budget_mb budget (200 MB, 3 buffers: measured best
+    with the final kernel) unless that would take more than
+    25 chunks (C3: each chunk re-reads and re-writes the fp32 dHc)."""
     s = binding.shape(B, N, M, d, V, "bf16")
     assert binding.attn_softmax_workspace_views(s).vocab_chunk == vc
-    assert (3 * B * N * vc * 2 <= 120 << 20) == fits
+    assert (3 * B * N * vc * 2 <= 200 << 20) == fits
     assert (V + vc - 1) // vc <= 25
 
 

@@ -78,7 +78,7 @@ def test_tcgen05_gemm_core(cuda_lib, a_mn, b_mn, M, N, K, mn3d, wide):
 
 # ------------------------------------------------------ end-to-end parity --
 _DEFAULTS = {"store_logits": 0, "wide_tiles": 2, "db_gemm": -1, "vb_pair": 1, "vb_fwd_fused": 0,
-             "vb_order": 1, "dl_buffers": 3, "dl_budget_mb": 120, "vb_last_g2_first": 1,
+             "vb_order": 1, "dl_buffers": 3, "dl_budget_mb": 200, "vb_last_g2_first": 1,
              "attn_fused": 1, "vb_wide": 1, "vb_lag": 2, "vb_g2split": 1, "vb_claim": 1,
              "vb_g1wide": 0, "gemm_claim": 4}
 _MODES = {
