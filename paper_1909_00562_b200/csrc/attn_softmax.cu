@@ -1555,7 +1555,10 @@ static attn_status_t launch_vocab_k(const Plan& p, const VbArgs& a, int ctas, cu
   P.nh = (P.order == 2 && g_opt_vb_g2split && P.nrb >= 2) ? 2 : 1;
   P.h0 = P.nh == 2 ? (P.nrb + 1) / 2 : P.nrb;
   P.lag = g_opt_vb_lag;
-  P.claim_late = g_opt_vb_claim < 0 ? (P.order == 2 ? 1 : 0) : g_opt_vb_claim;
+  // vb_claim: -1 = late for order 2 only, 0 = early, 1 = late (two k-blocks
+  // before the end), k >= 2 = k k-blocks before the end
+  P.claim_late = g_opt_vb_claim < 0 ? (P.order == 2 ? 2 : 0)
+                                    : g_opt_vb_claim == 1 ? 2 : g_opt_vb_claim;
   P.g1wide = (kPair && g_opt_vb_g1wide) ? 1 : 0;
   const int g1w = P.g1wide ? 2 * VB_BN : VB_BN;   // G1 tile columns
   P.n2max = L.n2max;

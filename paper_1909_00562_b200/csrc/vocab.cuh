@@ -167,8 +167,8 @@ struct alignas(64) VbParams {
   int g1wide;            // G1 tiles 512 columns wide on CTA pairs (both accumulators,
                          // two chains at the full tensor rate; the epilogue no longer
                          // overlaps the next tile's MMAs)
-  int claim_late;        // claim the next tile near the end of the current one's loads
-                         // (default: right after its first load)
+  int claim_late;        // > 0: claim the next tile claim_late k-blocks before the end of
+                         // the current one's loads; 0: right after its first load
   int nh;                // order 2: G2 split over T in nh (1 or 2) row halves (else 1)
   int h0;                // order 2: row blocks of the first half
   int lag;               // order 2: G3 of row block rb dispatched after G1 of rb + lag
@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) vocab_kernel(const __grid_const
           // claim the next tile only when this one is nearly issued: a tile is
           // never queued behind a long one on a busy pair (order 2's short
           // dependency distances need it)
-          if (leader && kb == max(0, tl.kb_total - 2)) fetch();
+          if (leader && kb == max(0, tl.kb_total - P.claim_late)) fetch();
         } else if (kb == 0) {
           t_nxt = next_tile();
           if (t_nxt >= 0) tl_nxt = vb_decode<kPair>(P, t_nxt);
