@@ -1981,7 +1981,12 @@ extern "C" attn_status_t attn_softmax_fwd_bwd_ex(
   // --force-comm hung when its first call carried the communicator).  So the
   // first call of each path (shape, operands, options) on a device runs once
   // without the communicator, which loads every kernel the path launches.
-  if (comm && !path_warmed(p, W_alpha != nullptr, b_out != nullptr)) {
+  // (not while the stream is being captured into a CUDA graph: nothing runs
+  // during capture, and instantiation loads the graph's kernels)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(stream, &cap));
+  if (comm && cap == cudaStreamCaptureStatusNone &&
+      !path_warmed(p, W_alpha != nullptr, b_out != nullptr)) {
     st = p.bf16 ? run_stage<__nv_bfloat16>(p, (const __nv_bfloat16*)H_dec, (const __nv_bfloat16*)H_enc,
                                            tgt_ids, (const __nv_bfloat16*)W_c,
                                            (const __nv_bfloat16*)W_out, (const __nv_bfloat16*)W_alpha,

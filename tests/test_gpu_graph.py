@@ -71,3 +71,43 @@ def test_decode_graph_replay_matches_eager(cuda_lib):
     run()
     torch.cuda.synchronize()
     assert torch.equal(gi, ids) and torch.equal(gl, logp)
+
+
+def test_stage_graph_with_communicator(cuda_lib):
+    """The communicator path (comm stream fork / join, per-chunk wait kernels,
+    NCCL allreduces) captures into a CUDA graph too; on a 1-rank communicator
+    the replay equals the local eager call bitwise.  The library's first-call
+    warm pass (lazy-loading guard) is skipped while capturing."""
+    from paper_1909_00562_b200 import binding
+    from paper_1909_00562_b200.stage import AttnSoftmaxStage, to_device
+    cfg = CONFIGS["small"]
+    inp = make_inputs(cfg)
+    scale = 1.0 / global_valid_tokens(cfg, cfg.B)
+    st = AttnSoftmaxStage(cfg.B, cfg.N, cfg.M, cfg.d, cfg.V, cfg.dtype)
+    dv = to_device(inp, cfg.dtype)
+    args = (dv["H_dec"], dv["H_enc"], dv["src_len"], dv["tgt_len"], dv["tgt_ids"],
+            dv["W_c"], dv["W_out"], scale)
+    comm = binding.attn_comm_init(binding.attn_comm_get_unique_id(), 1, 0, torch.cuda.current_device())
+    try:
+        out = st.alloc_outputs()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(2):
+                st(*args, out=out, comm=comm)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            st(*args, out=out, comm=comm)
+        g.replay()
+        torch.cuda.synchronize()
+        got = {k: v.clone() for k, v in out.items()}
+        ref = st(*args)
+        torch.cuda.synchronize()
+        for k in ("loss", "dH_dec", "dH_enc", "dW_c", "dW_out"):
+            assert torch.equal(got[k], ref[k]), k
+        del g
+    finally:
+        torch.cuda.synchronize()
+        binding.attn_comm_destroy(comm)
