@@ -89,6 +89,9 @@ __device__ __forceinline__ float ls_tanh(float x) {
 __device__ __forceinline__ float ls_sigmoid(float x) { return fmaf(0.5f, ls_tanh(0.5f * x), 0.5f); }
 
 __device__ __forceinline__ void ls_wait_geq(const unsigned* p, unsigned target) {
+  // (an unbounded spin on purpose: the bounded spin_wait_geq of ptx.cuh made
+  // the wavefront kernels 5-8% slower -- their per-step flag waits are short
+  // and on the recurrence's critical path)
   if (ld_acquire_gpu(p) >= target) return;
   while (ld_acquire_gpu(p) < target) __nanosleep(32);
 }

@@ -133,6 +133,36 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+
+// Bounded spin on a gpu-scope counter (a bounded wait turns
+// a deadlock into an error): waits until *p >= target; after `limit_ns` of
+// waiting (default 20 s -- every legitimate wait here is micro- to
+// milliseconds) it traps, so the launch fails with a CUDA error (sticky:
+// cudaErrorLaunchFailure) instead of hanging the GPU.
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+static __device__ __forceinline__ void spin_timeout_trap(const unsigned* p, unsigned target, unsigned seen) {
+  (void)p; (void)target; (void)seen;
+  __trap();   // no printf: its stack frame slowed the LSTM wavefront kernels by 5-8%
+}
+__device__ __forceinline__ void spin_wait_geq(const unsigned* p, unsigned target, unsigned ns_sleep,
+                                              unsigned long long limit_ns = 20000000000ull) {
+  if (ld_acquire_gpu(p) >= target) return;
+  unsigned long long t0 = 0;   // the clock is read only once a wait is long (1024 polls)
+  unsigned it = 0;
+  unsigned v;
+  while ((v = ld_acquire_gpu(p)) < target) {
+    __nanosleep(ns_sleep);
+    if ((++it & 1023u) == 0) {
+      const unsigned long long t = gtimer_ns();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > limit_ns) spin_timeout_trap(p, target, v);
+    }
+  }
+}
 __device__ __forceinline__ void red_release_gpu_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

@@ -369,8 +369,7 @@ __device__ __forceinline__ long long vb_gt() {
   } while (0)
 
 __device__ __forceinline__ void vb_wait_geq(const unsigned* p, unsigned target) {
-  if (ld_acquire_gpu(p) >= target) return;
-  while (ld_acquire_gpu(p) < target) __nanosleep(64);
+  spin_wait_geq(p, target, 64);
 }
 
 template <bool kPair>
