@@ -61,6 +61,6 @@ def run(spec, n=10):
 
 DEFAULTS.update({"vb_debug": 0, "dl_budget_mb": 200, "dl_buffers": 3, "vb_l2hints": 3,
                  "vb_pair": 1, "vb_order": 1, "vb_fwd_fused": 0, "vocab_chunk": 0,
-                 "store_logits": 0, "vb_last_g2_first": 1, "wide_tiles": 2, "vb_order": 1, "vb_lag": 2, "vb_g2split": 1, "vb_claim": 1, "vb_g1wide": 0, "gemm_claim": 4, "pdl": 1, "attn_fused": 1, "proj_bn": 256})
+                 "store_logits": 0, "vb_last_g2_first": 1, "wide_tiles": 2, "vb_order": 1, "vb_lag": 2, "vb_g2split": 1, "vb_claim": 1, "vb_g1wide": 0, "gemm_claim": 4, "n_fast": 1, "mn_3d_tma": 1, "pdl": 1, "attn_fused": 1, "proj_bn": 256})
 for spec in sys.argv[1:]:
     run("" if spec == "default" else spec)
