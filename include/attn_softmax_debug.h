@@ -63,8 +63,8 @@ long long attn_softmax_last_launches(void);
  * ATTN_ERR_WORKSPACE).  Keys:
  *   "vocab_chunk"   V-chunk width of the vocab backward (multiple of 256,
  *                   0 = automatic: the dL chunk buffers fit dl_budget_mb)
- *   "dl_budget_mb"  L2 budget of the bf16 dL chunk scratch, all buffers
- *                   (default 120)
+ *   "dl_budget_mb"  budget of the bf16 dL chunk scratch, all buffers
+ *                   (default 200; C1: Vc = 5376)
  *   "dl_buffers"    dL chunk buffers of the persistent backward (1-4, default 3)
  *   "vb_pair"       1 (default) = the persistent vocabulary launch on CTA
  *                   pairs (tcgen05 cta_group::2, 256 x 256 tiles); 0 = single
@@ -73,7 +73,23 @@ long long attn_softmax_last_launches(void);
  *                   launch; 0 (default) = the single-CTA forward GEMM and the
  *                   lse_reduce kernel before it
  *   "vb_order"      dispatch blocks of the persistent backward: 1 (default) =
- *                   [G1(c+1), G3(c), G2(c)], 0 = [G3(c), G2(c), G1(c+1)]
+ *                   [G1(c+1), G3(c), G2(c)], 0 = [G3(c), G2(c), G1(c+1)],
+ *                   2 = row-interleaved (G3 of row block rb after G1 of
+ *                   rb + vb_lag, dW_out tiles split over T in two row halves
+ *                   when vb_g2split; works with dl_buffers = 1)
+ *   "vb_lag", "vb_g2split"  order 2 parameters (defaults 2, 1)
+ *   "vb_claim"      when a CTA pair claims its next tile: 0 = right after
+ *                   the current tile's first load, 1 (default) = two
+ *                   k-blocks before the end of its loads, k >= 2 = k
+ *                   k-blocks before the end; -1 = late for order 2 only
+ *   "vb_wide"       1 (default, d % 512 == 0): 512-column dW_out / dHc tiles
+ *                   on both accumulators
+ *   "vb_g1wide"     1 = 512-column dL tiles too (measured slower; default 0)
+ *   "gemm_claim"    bitmask of GEMM groups (the "wide_tiles" bits) of the
+ *                   generic engine whose tiles are claimed late (default 4:
+ *                   the projection backward)
+ *   "comm_reserve_1rank" tests: a 1-rank communicator reserves NCCL's SMs as
+ *                   with several ranks
  *   "vb_last_g2_first" 1 (default): the last block dispatches dW_out tiles first
  *   "vb_l2hints"    bit 0: H_c loads evict-last; bit 1: dHc updates evict-last
  *                   (default 3)
@@ -81,7 +97,11 @@ long long attn_softmax_last_launches(void);
  *                   next persistent launch fills with per-tile stamps (debug)
  *   "vb_debug"      timing experiments only (WRONG results): bit 0 skip the
  *                   dL stores, bit 1 skip the exponentials, bit 2 skip the
- *                   dW_out / dHc stores
+ *                   dW_out / dHc stores, bit 3 publish without waiting for
+ *                   the stores, bits 4 / 5 skip the B / A loads, bit 7 G1
+ *                   epilogue without TMEM loads, bits 13 / 14 skip the G2 /
+ *                   G3 loads (bits 6, 8-12: MMA-issue probes compiled only
+ *                   with -DVB_DEBUG_MMA=1)
  *   "gemm_ctas"     persistent GEMM grid size (0 = number of SMs)
  *   "comm_max_ctas" CTA cap given to NCCL by attn_comm_init calls made after
  *                   it (default 8, 0 = NCCL's default); while gradients are
